@@ -1,0 +1,290 @@
+/*
+ * plora.h — C ABI of the B200-native P-LoRA hot path (libplora.so).
+ *
+ * This is the drop-in boundary.  Plain pointers and sizes only; no torch or
+ * C++ types.  Every entry point names the reference interface it replaces as
+ * file:line under /root/reference/proj (the lorasim C++ library; the paper's
+ * GPU op that the reference only bills as a cost-model constant is cited to
+ * PAPER.md).  INTEGRATION.md shows the ctypes / C++ bindings a maintainer adds.
+ *
+ * Error convention (reference: include/lorasim/errors.hpp:9-24,
+ * src/memory.cpp:19-47): functions return int status codes.
+ *   >= 0  success, or an AllocStatus value for plora_pool_alloc
+ *         (memory.hpp:18-22: 0 ok, 1 out_of_memory, 2 fragmentation_failure)
+ *   <  0  an error; plora_last_error() returns the message of the most recent
+ *         error on the calling thread.  The C++ wrapper (plora.hpp) rethrows
+ *         the same exception types the reference throws.
+ *
+ * Threading: one owner thread per pool/store.  Device work
+ * is stream-ordered on the cudaStream_t the caller passes (NULL = legacy
+ * default stream).
+ */
+#ifndef PLORA_H_
+#define PLORA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+#define PLORA_OK 0
+#define PLORA_OUT_OF_MEMORY 1         /* AllocStatus::out_of_memory (memory.hpp:20) */
+#define PLORA_FRAGMENTATION_FAILURE 2 /* AllocStatus::fragmentation_failure (memory.hpp:21) */
+#define PLORA_E_VALIDATION (-1)       /* lorasim::ValidationError (errors.hpp:9-13)  */
+#define PLORA_E_LOGIC (-2)            /* std::logic_error (memory.cpp:20-21,42-47)   */
+#define PLORA_E_CONFIG (-3)           /* lorasim::ConfigError (errors.hpp:15-19)     */
+#define PLORA_E_PARSE (-4)            /* lorasim::ParseError (errors.hpp:21-25)      */
+#define PLORA_E_CUDA (-5)             /* CUDA runtime failure (new: device path)     */
+#define PLORA_E_NOMEM (-6)            /* host allocation failure                     */
+
+typedef void* plora_stream_t; /* a cudaStream_t, passed through opaquely */
+
+/* Message of the last error raised on this thread ("" if none). */
+const char* plora_last_error(void);
+const char* plora_version(void);
+/* Number of device kernels this process launched through libplora (all
+ * entry points, all threads).  Evidence for bench.py's gpu_launches. */
+uint64_t plora_kernel_launch_count(void);
+
+/* ------------------------------------------------- adapter model (L1) ----
+ * Replaces LoraDims::validate / param_count (include/lorasim/adapter.hpp:15-26,
+ * src/adapter.cpp:12-26) and AdapterSizeTable (adapter.hpp:32-47,
+ * src/adapter.cpp:28-50). */
+int plora_lora_dims_validate(uint32_t d, uint32_t k, uint32_t r, uint32_t adapted_matrices,
+                             uint32_t bytes_per_param);
+int plora_param_count(uint32_t d, uint32_t k, uint32_t r, uint32_t adapted_matrices,
+                      uint32_t bytes_per_param, uint64_t* out);
+
+typedef struct plora_size_table plora_size_table;
+/* AdapterSizeTable(anchor_rank, anchor_bytes, linear_fallback) (adapter.cpp:28-35);
+ * anchor (8, 13 MiB, 1) is the reference default. */
+int plora_size_table_create(uint32_t anchor_rank, uint64_t anchor_bytes, int linear_fallback,
+                            plora_size_table** out);
+void plora_size_table_destroy(plora_size_table* t);
+int plora_size_table_set(plora_size_table* t, uint32_t rank, uint64_t bytes); /* adapter.cpp:37-40 */
+int plora_size_table_bytes_for(const plora_size_table* t, uint32_t rank,
+                               uint64_t* out); /* adapter.cpp:43-50 */
+/* generate_catalog (adapter.cpp:110-144): ranks/bytes of `count` adapters
+ * keyed 0..count-1 (ids "a000".. in catalog order).  sizes NULL = default table. */
+int plora_generate_catalog(uint32_t count, const uint32_t* mix_ranks, const double* mix_weights,
+                           uint64_t n_mix, uint64_t seed, const plora_size_table* sizes,
+                           uint32_t d, uint32_t k, uint32_t adapted_matrices,
+                           uint32_t bytes_per_param, uint32_t* ranks_out, uint64_t* bytes_out);
+
+/* ---------------------------------------------------- page pool (L2) -----
+ * Replaces lorasim::PagePool (include/lorasim/memory.hpp:39-83,
+ * src/memory.cpp:7-146).  Placement is bit-identical to the reference:
+ * alloc takes the lowest free physical indices (memory.cpp:18-38), compact
+ * moves pages >= live into the lowest free slots walking adapter-key then
+ * logical order (memory.cpp:71-89).  Backed by a two-level bitmap instead of
+ * std::set, so alloc/free cost O(pages/64) instead of O(pages·log N). */
+typedef struct plora_pool plora_pool;
+
+typedef struct {
+  double external_frag; /* FragmentationReport (memory.hpp:24-28) */
+  double internal_frag;
+  double utilization;
+} plora_frag_report;
+
+/* A compaction relocation (new: compact() in the reference returns only the
+ * count, memory.cpp:71-89; the device needs the moves). */
+typedef struct {
+  uint32_t adapter;
+  uint32_t logical;
+  uint32_t src; /* physical page before */
+  uint32_t dst; /* physical page after  */
+} plora_reloc;
+
+int plora_pool_create(uint64_t page_bytes, uint32_t total_pages,
+                      plora_pool** out); /* memory.cpp:7-12 */
+void plora_pool_destroy(plora_pool* p);
+uint32_t plora_pool_pages_needed(const plora_pool* p, uint64_t bytes); /* memory.cpp:14-16 */
+/* >= 0: AllocStatus (0 ok / 1 out_of_memory, pool unchanged);
+ * PLORA_E_VALIDATION on 0 bytes; PLORA_E_LOGIC if already allocated.  memory.cpp:18-38 */
+int plora_pool_alloc(plora_pool* p, uint32_t adapter, uint64_t weight_bytes);
+int plora_pool_free(plora_pool* p, uint32_t adapter); /* memory.cpp:40-53; E_LOGIC on double free */
+int plora_pool_translate(const plora_pool* p, uint32_t adapter, uint32_t logical,
+                         uint32_t* phys); /* memory.cpp:55-62 */
+/* PagePool::table (memory.cpp:64-69).  *entries stays valid until the next
+ * mutation of the pool. */
+int plora_pool_table(const plora_pool* p, uint32_t adapter, const uint32_t** entries,
+                     uint32_t* n_entries, uint64_t* weight_bytes);
+int plora_pool_has(const plora_pool* p, uint32_t adapter); /* memory.hpp:60 */
+/* PagePool::compact (memory.cpp:71-89).  *moved = relocation count; the
+ * relocation list stays readable through plora_pool_last_relocations. */
+int plora_pool_compact(plora_pool* p, uint64_t* moved);
+int plora_pool_last_relocations(const plora_pool* p, const plora_reloc** relocs, uint64_t* n);
+void plora_pool_report(const plora_pool* p, plora_frag_report* out); /* memory.cpp:91-100 */
+uint32_t plora_pool_free_pages(const plora_pool* p);                  /* memory.hpp:62 */
+uint32_t plora_pool_total_pages(const plora_pool* p);                 /* memory.hpp:63 */
+uint64_t plora_pool_page_bytes(const plora_pool* p);                  /* memory.hpp:64 */
+uint64_t plora_pool_used_bytes(const plora_pool* p);                  /* memory.hpp:65 */
+uint64_t plora_pool_allocated_bytes(const plora_pool* p);             /* memory.hpp:66-68 */
+uint64_t plora_pool_total_bytes(const plora_pool* p);                 /* memory.hpp:69-71 */
+/* PagePool::resident (memory.cpp:116-121): ascending keys; returns count. */
+uint64_t plora_pool_resident(const plora_pool* p, uint32_t* out, uint64_t cap);
+int plora_pool_check_invariants(const plora_pool* p); /* memory.cpp:123-146 */
+/* PagePool::dump().dump() (memory.cpp:102-114): byte-identical JSON text.
+ * Writes up to cap bytes (NUL-terminated when it fits); *len = full length. */
+int plora_pool_dump(const plora_pool* p, char* buf, uint64_t cap, uint64_t* len);
+
+/* ------------------------------------------- prefetch policy (L2) --------
+ * Replaces include/lorasim/prefetch.hpp:11-72 / src/prefetch.cpp:1-114. */
+typedef struct {
+  double theta, alpha, beta, gamma, tau_ms, freq_half_life_ms, staging_fraction;
+} plora_policy;
+
+#define PLORA_NOT_RESIDENT 0 /* Residency (prefetch.hpp:23) */
+#define PLORA_STAGING 1
+#define PLORA_RESIDENT 2
+
+typedef struct { /* AdapterDynamics (prefetch.hpp:26-37) */
+  int32_t status;
+  uint32_t busy;
+  double last_access_ms;
+  double decayed_count;
+  double decay_stamp_ms;
+  double prediction;
+  int32_t transfer_active;
+  int32_t reserved;
+} plora_dynamics;
+
+void plora_policy_default(plora_policy* p);     /* prefetch.hpp:11-21 defaults */
+int plora_policy_validate(const plora_policy* p); /* prefetch.cpp:8-19 */
+void plora_dynamics_init(plora_dynamics* d);
+void plora_record_access(plora_dynamics* d, double now_ms, double half_life_ms); /* :21-25 */
+double plora_decayed_at(const plora_dynamics* d, double now_ms, double half_life_ms); /* :27-32 */
+double plora_recency_score(double last_access_ms, double now_ms, double tau_ms); /* :34-38 */
+double plora_eviction_score(const plora_dynamics* d, const plora_policy* p, double now_ms,
+                            double max_freq); /* :40-47 */
+/* scored_residents (:49-64): ascending (score, key); returns count. */
+uint64_t plora_scored_residents(const plora_dynamics* dyn, uint64_t n, const plora_policy* p,
+                                double now_ms, double* scores, uint32_t* keys);
+/* select_prefetch (:66-91): returns number of picks written to out. */
+uint64_t plora_select_prefetch(const double* probabilities, uint64_t n_probs,
+                               const plora_dynamics* dyn, uint64_t n, const plora_policy* p,
+                               const uint64_t* units_for, uint64_t n_units,
+                               uint64_t staging_budget_units, uint32_t* out);
+/* plan_evictions (:93-112): returns 1 if satisfied, 0 if not. */
+int plora_plan_evictions(uint64_t bytes_needed, uint64_t free_bytes, const uint32_t* eligible,
+                         uint64_t n_eligible, const uint64_t* bytes_for, uint64_t n_bytes,
+                         uint32_t* victims, uint64_t* n_victims);
+
+/* ----------------------------------- synthetic workload (host input) -----
+ * generate_synthetic (include/lorasim/workload.hpp:36-63, src/workload.cpp:59-144),
+ * restated bit-identically (same libstdc++ engines/distributions).  Adapter
+ * ids "a%0*d" are returned as their integer index. */
+typedef struct {
+  uint32_t num_adapters;
+  double base_rate;
+  double diurnal_amplitude;
+  double period_s;
+  uint32_t hot_set_size;
+  double hot_rotation_s;
+  double hot_share;
+  double rotation_jitter;
+  double burstiness_cv;
+  double input_median, input_sigma, output_median, output_sigma;
+  uint32_t max_tokens;
+} plora_synthetic_profile;
+void plora_synthetic_profile_default(plora_synthetic_profile* p); /* workload.hpp:19-50 */
+/* Returns the number of requests (<0 on error); fills at most cap. */
+int64_t plora_generate_synthetic(const plora_synthetic_profile* p, double duration_s,
+                                 uint64_t seed, double* arrival_ms, uint32_t* adapter,
+                                 uint32_t* input_tokens, uint32_t* output_tokens, uint64_t cap);
+
+/* --------------------------------------- device adapter store (new) -----
+ * The page pool's physical pages backed by ONE HBM arena
+ * (total_pages · page_bytes, one cudaMalloc) plus a device page table and an
+ * adapter directory.  Bookkeeping stays in the host plora_pool.
+ *
+ * Model shape: n_layers × n_proj adapted matrices (Llama-7B q/v: 32 × 2,
+ * adapter.hpp:19 adapted_matrices = 64).  In-adapter layout, for l in
+ * [0,L), p in [0,n_proj): block [A (r × d_in[p]) | Bᵀ (r × d_out[p])],
+ * row-major; so S = r·L·Σ(d_in+d_out)·esize = param_count·bytes_per_param
+ * (adapter.cpp:22-26,52-59). */
+#define PLORA_MAX_PROJ 8
+#define PLORA_BF16 0
+#define PLORA_F32 1
+
+typedef struct {
+  uint32_t n_layers;
+  uint32_t n_proj;
+  uint32_t d_in[PLORA_MAX_PROJ];
+  uint32_t d_out[PLORA_MAX_PROJ];
+  uint32_t dtype; /* PLORA_BF16 or PLORA_F32: weights, x and y */
+} plora_model;
+
+uint64_t plora_model_adapter_bytes(const plora_model* m, uint32_t rank);
+uint64_t plora_model_block_offset(const plora_model* m, uint32_t rank, uint32_t layer,
+                                  uint32_t proj);
+
+typedef struct plora_store plora_store;
+/* pool is borrowed and must outlive the store; page_bytes must be a power of
+ * two >= 16.  max_adapters bounds adapter keys (dense, AdapterKey memory.hpp:16). */
+int plora_store_create(plora_pool* pool, int device, const plora_model* model,
+                       uint32_t max_adapters, plora_store** out);
+void plora_store_destroy(plora_store* s);
+void* plora_store_arena(const plora_store* s); /* device base pointer */
+/* Register adapter key -> rank (the AdapterSpec.dims.r, adapter.hpp:51-61). */
+int plora_store_register(plora_store* s, uint32_t adapter, uint32_t rank);
+int plora_store_rank(const plora_store* s, uint32_t adapter, uint32_t* rank);
+
+#define PLORA_COPY_CE 0 /* copy engines: cudaMemcpyAsync per contiguous physical run;
+                          src may be host (pinned or pageable) or device memory (UVA) */
+#define PLORA_COPY_SM 1 /* SM page-scatter kernel reading mapped pinned host memory */
+/* Page scatter H2D: copy the adapter's logical bytes (host, ideally pinned)
+ * into its physical pages (pool table).  The reference models this transfer
+ * as processor-shared PCIe time (src/engine.cpp:197-288); here it is real. */
+int plora_store_write_pages(plora_store* s, uint32_t adapter, const void* host_src,
+                            uint64_t bytes, int mode, plora_stream_t stream);
+/* Gather the adapter's logical bytes back to host (parity checks). */
+int plora_store_read_pages(plora_store* s, uint32_t adapter, void* host_dst, uint64_t bytes,
+                           plora_stream_t stream);
+/* Publish the adapter's page table to the device and mark it resident: the
+ * promotion point of src/engine.cpp:406-414. */
+int plora_store_publish(plora_store* s, uint32_t adapter, plora_stream_t stream);
+/* Withdraw residency (before PagePool::free / eviction, src/engine.cpp:294-304). */
+int plora_store_retire(plora_store* s, uint32_t adapter, plora_stream_t stream);
+int plora_store_is_published(const plora_store* s, uint32_t adapter);
+/* Apply compaction relocations on device (page_move_d2d) and republish the
+ * affected tables (src/memory.cpp:71-89, idle trigger src/engine.cpp:486-497). */
+int plora_store_apply_relocations(plora_store* s, const plora_reloc* relocs, uint64_t n,
+                                  plora_stream_t stream);
+
+/* --------------------------------------- paged LoRA forward op (new) -----
+ * The op the reference bills as cost_model prefill_ms / step_ms
+ * (include/lorasim/cost_model.hpp:32-40 at src/engine.cpp:355,510);
+ * math PAPER.md:64-69.  A batch plan groups tokens by adapter once per batch
+ * and is reused for every (layer, proj) call of the step. */
+typedef struct plora_plan plora_plan;
+/* token_adapter: HOST array, adapter key per token or -1 (no LoRA).  Every
+ * referenced adapter must be published.  Uploads the plan on `stream`. */
+int plora_plan_create(plora_store* s, const int32_t* token_adapter, uint32_t n_tokens,
+                      plora_stream_t stream, plora_plan** out);
+/* Rebuild an existing plan for a new batch, reusing its buffers. */
+int plora_plan_update(plora_plan* plan, const int32_t* token_adapter, uint32_t n_tokens,
+                      plora_stream_t stream);
+void plora_plan_destroy(plora_plan* plan);
+uint32_t plora_plan_num_segments(const plora_plan* plan);
+
+/* y[t, :] += scale · (x[t, :] · Aᵀ) · Bᵀ for every token, A/B of adapter
+ * a(t) at (layer, proj) read through the device page table.  x: [T, d_in]
+ * with row stride x_stride elements; y: [T, d_out] with row stride y_stride.
+ * The intermediate v = x·Aᵀ is kept in fp32. */
+int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
+               uint64_t x_stride, void* y, uint64_t y_stride, float scale,
+               plora_stream_t stream);
+/* Same contract, prefill path (tcgen05 tensor cores; v rounded to the
+ * storage dtype between shrink and expand). */
+int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
+               uint64_t x_stride, void* y, uint64_t y_stride, float scale,
+               plora_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLORA_H_ */

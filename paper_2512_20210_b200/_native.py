@@ -1,0 +1,217 @@
+"""ctypes binding of libplora.so (C ABI: include/plora.h).
+
+The shared library is built in-tree by ``__graft_entry__.build()`` (or
+``make -C paper_2512_20210_b200/csrc``).  There is no fallback: if the
+library is missing every entry point fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import ConfigError, LogicError, ParseError, ValidationError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libplora.so")
+
+PLORA_OK = 0
+PLORA_E_VALIDATION = -1
+PLORA_E_LOGIC = -2
+PLORA_E_CONFIG = -3
+PLORA_E_PARSE = -4
+PLORA_E_CUDA = -5
+PLORA_E_NOMEM = -6
+
+PLORA_MAX_PROJ = 8
+PLORA_BF16 = 0
+PLORA_F32 = 1
+PLORA_COPY_CE = 0
+PLORA_COPY_SM = 1
+
+
+class CudaError(RuntimeError):
+    """A CUDA runtime failure inside libplora."""
+
+
+class plora_frag_report(C.Structure):
+    _fields_ = [("external_frag", C.c_double), ("internal_frag", C.c_double),
+                ("utilization", C.c_double)]
+
+
+class plora_reloc(C.Structure):
+    _fields_ = [("adapter", C.c_uint32), ("logical", C.c_uint32), ("src", C.c_uint32),
+                ("dst", C.c_uint32)]
+
+
+class plora_policy(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("theta", "alpha", "beta", "gamma", "tau_ms",
+                                          "freq_half_life_ms", "staging_fraction")]
+
+
+class plora_dynamics(C.Structure):
+    _fields_ = [("status", C.c_int32), ("busy", C.c_uint32), ("last_access_ms", C.c_double),
+                ("decayed_count", C.c_double), ("decay_stamp_ms", C.c_double),
+                ("prediction", C.c_double), ("transfer_active", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class plora_synthetic_profile(C.Structure):
+    _fields_ = [("num_adapters", C.c_uint32), ("base_rate", C.c_double),
+                ("diurnal_amplitude", C.c_double), ("period_s", C.c_double),
+                ("hot_set_size", C.c_uint32), ("hot_rotation_s", C.c_double),
+                ("hot_share", C.c_double), ("rotation_jitter", C.c_double),
+                ("burstiness_cv", C.c_double), ("input_median", C.c_double),
+                ("input_sigma", C.c_double), ("output_median", C.c_double),
+                ("output_sigma", C.c_double), ("max_tokens", C.c_uint32)]
+
+
+class plora_model(C.Structure):
+    _fields_ = [("n_layers", C.c_uint32), ("n_proj", C.c_uint32),
+                ("d_in", C.c_uint32 * PLORA_MAX_PROJ), ("d_out", C.c_uint32 * PLORA_MAX_PROJ),
+                ("dtype", C.c_uint32)]
+
+
+_u32, _u64, _i32, _i64, _int, _dbl, _vp = (C.c_uint32, C.c_uint64, C.c_int32, C.c_int64,
+                                           C.c_int, C.c_double, C.c_void_p)
+_P = C.POINTER
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "plora_last_error": (C.c_char_p, []),
+    "plora_version": (C.c_char_p, []),
+    "plora_kernel_launch_count": (_u64, []),
+    "plora_lora_dims_validate": (_int, [_u32, _u32, _u32, _u32, _u32]),
+    "plora_param_count": (_int, [_u32, _u32, _u32, _u32, _u32, _P(_u64)]),
+    "plora_size_table_create": (_int, [_u32, _u64, _int, _P(_vp)]),
+    "plora_size_table_destroy": (None, [_vp]),
+    "plora_size_table_set": (_int, [_vp, _u32, _u64]),
+    "plora_size_table_bytes_for": (_int, [_vp, _u32, _P(_u64)]),
+    "plora_generate_catalog": (_int, [_u32, _P(_u32), _P(_dbl), _u64, _u64, _vp, _u32, _u32,
+                                      _u32, _u32, _P(_u32), _P(_u64)]),
+    "plora_pool_create": (_int, [_u64, _u32, _P(_vp)]),
+    "plora_pool_destroy": (None, [_vp]),
+    "plora_pool_pages_needed": (_u32, [_vp, _u64]),
+    "plora_pool_alloc": (_int, [_vp, _u32, _u64]),
+    "plora_pool_free": (_int, [_vp, _u32]),
+    "plora_pool_translate": (_int, [_vp, _u32, _u32, _P(_u32)]),
+    "plora_pool_table": (_int, [_vp, _u32, _P(_P(_u32)), _P(_u32), _P(_u64)]),
+    "plora_pool_has": (_int, [_vp, _u32]),
+    "plora_pool_compact": (_int, [_vp, _P(_u64)]),
+    "plora_pool_last_relocations": (_int, [_vp, _P(_P(plora_reloc)), _P(_u64)]),
+    "plora_pool_report": (None, [_vp, _P(plora_frag_report)]),
+    "plora_pool_free_pages": (_u32, [_vp]),
+    "plora_pool_total_pages": (_u32, [_vp]),
+    "plora_pool_page_bytes": (_u64, [_vp]),
+    "plora_pool_used_bytes": (_u64, [_vp]),
+    "plora_pool_allocated_bytes": (_u64, [_vp]),
+    "plora_pool_total_bytes": (_u64, [_vp]),
+    "plora_pool_resident": (_u64, [_vp, _P(_u32), _u64]),
+    "plora_pool_check_invariants": (_int, [_vp]),
+    "plora_pool_dump": (_int, [_vp, C.c_char_p, _u64, _P(_u64)]),
+    "plora_policy_default": (None, [_P(plora_policy)]),
+    "plora_policy_validate": (_int, [_P(plora_policy)]),
+    "plora_dynamics_init": (None, [_P(plora_dynamics)]),
+    "plora_record_access": (None, [_P(plora_dynamics), _dbl, _dbl]),
+    "plora_decayed_at": (_dbl, [_P(plora_dynamics), _dbl, _dbl]),
+    "plora_recency_score": (_dbl, [_dbl, _dbl, _dbl]),
+    "plora_eviction_score": (_dbl, [_P(plora_dynamics), _P(plora_policy), _dbl, _dbl]),
+    "plora_scored_residents": (_u64, [_P(plora_dynamics), _u64, _P(plora_policy), _dbl,
+                                      _P(_dbl), _P(_u32)]),
+    "plora_select_prefetch": (_u64, [_P(_dbl), _u64, _P(plora_dynamics), _u64,
+                                     _P(plora_policy), _P(_u64), _u64, _u64, _P(_u32)]),
+    "plora_plan_evictions": (_int, [_u64, _u64, _P(_u32), _u64, _P(_u64), _u64, _P(_u32),
+                                    _P(_u64)]),
+    "plora_synthetic_profile_default": (None, [_P(plora_synthetic_profile)]),
+    "plora_generate_synthetic": (_i64, [_P(plora_synthetic_profile), _dbl, _u64, _P(_dbl),
+                                        _P(_u32), _P(_u32), _P(_u32), _u64]),
+    "plora_model_adapter_bytes": (_u64, [_P(plora_model), _u32]),
+    "plora_model_block_offset": (_u64, [_P(plora_model), _u32, _u32, _u32]),
+    "plora_store_create": (_int, [_vp, _int, _P(plora_model), _u32, _P(_vp)]),
+    "plora_store_destroy": (None, [_vp]),
+    "plora_store_arena": (_vp, [_vp]),
+    "plora_store_register": (_int, [_vp, _u32, _u32]),
+    "plora_store_rank": (_int, [_vp, _u32, _P(_u32)]),
+    "plora_store_write_pages": (_int, [_vp, _u32, _vp, _u64, _int, _vp]),
+    "plora_store_read_pages": (_int, [_vp, _u32, _vp, _u64, _vp]),
+    "plora_store_publish": (_int, [_vp, _u32, _vp]),
+    "plora_store_retire": (_int, [_vp, _u32, _vp]),
+    "plora_store_is_published": (_int, [_vp, _u32]),
+    "plora_store_apply_relocations": (_int, [_vp, _P(plora_reloc), _u64, _vp]),
+    "plora_plan_create": (_int, [_vp, _P(_i32), _u32, _vp, _P(_vp)]),
+    "plora_plan_update": (_int, [_vp, _P(_i32), _u32, _vp]),
+    "plora_plan_destroy": (None, [_vp]),
+    "plora_plan_num_segments": (_u32, [_vp]),
+    "plora_bgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
+    "plora_sgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """The loaded libplora.so (loads on first use; raises if it is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (no CPU fallback exists)")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    return lib().plora_last_error().decode("utf-8", "replace")
+
+
+def check(rc: int) -> int:
+    """Map a plora status code onto the reference's exception types."""
+    if rc >= 0:
+        return rc
+    msg = last_error()
+    if rc == PLORA_E_VALIDATION:
+        raise ValidationError(msg)
+    if rc == PLORA_E_CONFIG:
+        raise ConfigError(msg)
+    if rc == PLORA_E_PARSE:
+        raise ParseError(msg)
+    if rc == PLORA_E_CUDA:
+        raise CudaError(msg)
+    if rc == PLORA_E_NOMEM:
+        raise MemoryError(msg)
+    raise LogicError(msg)
+
+
+def u32_array(values):
+    arr = (C.c_uint32 * max(len(values), 1))()
+    for i, v in enumerate(values):
+        arr[i] = v
+    return arr
+
+
+def u64_array(values):
+    arr = (C.c_uint64 * max(len(values), 1))()
+    for i, v in enumerate(values):
+        arr[i] = v
+    return arr
+
+
+def f64_array(values):
+    arr = (C.c_double * max(len(values), 1))()
+    for i, v in enumerate(values):
+        arr[i] = v
+    return arr
+
+
+def i32_array(values):
+    arr = (C.c_int32 * max(len(values), 1))()
+    for i, v in enumerate(values):
+        arr[i] = v
+    return arr

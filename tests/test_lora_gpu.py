@@ -1,0 +1,260 @@
+"""GPU parity of the paged LoRA forward op (BGMV decode path) against the CPU
+oracle (oracle/lora_oracle.c) on identical inputs, page tables and adapter
+assignment; page tables come from the bit-exact pool (pinned to the reference
+PagePool in test_pagepool.py and here against tests/golden)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from lora_harness import TOL_BF16, TOL_F32, Setup, rel_err, to_np_bits
+from oracle import lora as OL
+from paper_2512_20210_b200 import (AllocStatus, PagePool, ValidationError, synth)
+from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, ModelShape, bgmv,
+                                        kernel_launch_count)
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _run(setup, layer, proj, ta, scale=1.0, salt=0, x_pad=0, y_pad=0):
+    cfg = setup.cfg
+    T = len(ta)
+    din, dout = cfg.shape.d_in[proj], cfg.shape.d_out[proj]
+    x = synth.activations(T, din + x_pad, cfg.shape.dtype, "x", salt=salt)[:, :din]
+    y0 = synth.activations(T, dout + y_pad, cfg.shape.dtype, "y", salt=salt)[:, :dout]
+    xd = torch.empty(T, din + x_pad, dtype=cfg.shape.dtype, device="cuda")[:, :din]
+    yd = torch.empty(T, dout + y_pad, dtype=cfg.shape.dtype, device="cuda")[:, :dout]
+    xd.copy_(x)
+    yd.copy_(y0)
+    plan = BatchPlan(setup.store, ta)
+    bgmv(plan, layer, proj, xd, yd, scale)
+    torch.cuda.synchronize()
+    ref = setup.oracle(layer, proj, x.contiguous(), y0.contiguous(), ta, scale=scale)
+    return yd, ref
+
+
+def test_store_readback_bit_exact(cuda):
+    for mode in (0, 1):  # copy engines, SM page-scatter kernel over mapped pinned memory
+        cfg = synth.cfg1(n_layers=2)
+        s = Setup(cfg, copy_mode=mode)
+        for a in range(cfg.n_adapters):
+            got = s.store.read_pages(a, cfg.shape.adapter_bytes(cfg.ranks[a]))
+            assert torch.equal(got, s.images[a].view(torch.uint8)), (mode, a)
+
+
+def test_small_golden_vectors(cuda):
+    """tests/golden/lora_small.npz: odd ranks, 64-byte pages, -1 tokens."""
+    z = np.load(os.path.join(GOLDEN, "lora_small.npz"))
+    for dt, dtype, tol in (("bf16", torch.bfloat16, TOL_BF16), ("f32", torch.float32, TOL_F32)):
+        ranks = [int(r) for r in z[f"{dt}_ranks"]]
+        page, total = (int(v) for v in z[f"{dt}_page"])
+        shape = ModelShape(2, (64, 128), (64, 32), dtype)
+        pool = PagePool(page, total)
+        sizes = [shape.adapter_bytes(r) for r in ranks]
+        for a, sz in enumerate(sizes):
+            assert pool.alloc(a, sz) == AllocStatus.ok
+        for a in range(0, len(ranks), 2):
+            pool.free(a)
+        for a in range(0, len(ranks), 2):
+            assert pool.alloc(a, sizes[a]) == AllocStatus.ok
+        store = AdapterStore(pool, shape, len(ranks))
+        for a, r in enumerate(ranks):
+            assert pool.table(a) == list(z[f"{dt}_table{a}"])  # reference tables
+            store.register(a, r)
+            img = torch.from_numpy(z[f"{dt}_img{a}"].view(np.uint8).copy())
+            store.write_pages(a, img)
+            store.publish(a)
+        ta = z[f"{dt}_tokens"]
+        plan = BatchPlan(store, ta)
+        for layer in range(2):
+            for proj in range(2):
+                x = z[f"{dt}_x_{layer}_{proj}"]
+                y0 = z[f"{dt}_y0_{layer}_{proj}"]
+                tx = torch.from_numpy(x.view(np.int16) if dt == "bf16" else x)
+                ty = torch.from_numpy(y0.view(np.int16).copy() if dt == "bf16" else y0.copy())
+                if dt == "bf16":
+                    tx, ty = tx.view(torch.bfloat16), ty.view(torch.bfloat16)
+                xd, yd = tx.cuda(), ty.cuda()
+                bgmv(plan, layer, proj, xd, yd, 0.5)
+                torch.cuda.synchronize()
+                err = rel_err(yd, z[f"{dt}_y_{layer}_{proj}_v0"])
+                assert err <= tol, (dt, layer, proj, err)
+                # rows of tokens with no adapter are untouched bit for bit
+                none = ta < 0
+                assert np.array_equal(to_np_bits(yd)[none], y0[none])
+
+
+def test_cfg1_parity_and_checksum(cuda):
+    """BASELINE config 1 at full size (32 layers), four (layer, proj) calls; the
+    oracle itself is pinned by tests/golden/cfg1_checksums.json."""
+    with open(os.path.join(GOLDEN, "cfg1_checksums.json")) as f:
+        g = json.load(f)
+    cfg = synth.cfg1()
+    s = Setup(cfg)
+    tables = np.concatenate([np.asarray(s.pool.table(a), np.uint32) for a in range(16)])
+    assert hashlib.sha256(tables.tobytes()).hexdigest() == g["tables_sha256"]
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    for call in g["calls"]:
+        layer, proj = call["layer"], call["proj"]
+        yd, ref = _run(s, layer, proj, ta, salt=layer * 2 + proj)
+        assert hashlib.sha256(ref.tobytes()).hexdigest() == call["y_sha256"]
+        err = rel_err(yd, ref)
+        assert err <= TOL_BF16, (layer, proj, err)
+
+
+@pytest.mark.parametrize("page_bytes", [2048, 2 << 20])
+def test_cfg2_per_call_parity(cuda, page_bytes):
+    """BASELINE config 2 call shape (256 tokens, 128 adapters, r in {8..64});
+    two layers instead of 32 — the kernel sees identical per-call work."""
+    cfg = synth.cfg2(n_layers=2, page_bytes=page_bytes)
+    s = Setup(cfg)
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    for layer, proj in ((0, 0), (1, 1)):
+        yd, ref = _run(s, layer, proj, ta, salt=7 + layer)
+        err = rel_err(yd, ref)
+        assert err <= TOL_BF16, (page_bytes, layer, proj, err)
+
+
+def test_fp32_accumulate_mode(cuda):
+    cfg = synth.DecodeConfig("f32", ModelShape(2, (512, 256), (256, 1024), torch.float32),
+                             [4, 8, 16, 32, 64, 128, 3, 7], 3, 1024)
+    s = Setup(cfg)
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    for layer, proj in ((0, 0), (1, 1), (1, 0)):
+        yd, ref = _run(s, layer, proj, ta, scale=0.75, salt=layer)
+        err = rel_err(yd, ref)
+        assert err <= TOL_F32, (layer, proj, err)
+
+
+def test_edge_cases(cuda):
+    shape = ModelShape(3, (64, 256), (128, 64), torch.bfloat16)
+    ranks = [1, 5, 12, 33, 100, 128, 200, 2]
+    cfg = synth.DecodeConfig("edge", shape, ranks, 1, 16)  # 16-byte pages
+    s = Setup(cfg)
+    # many tokens for one adapter (> token chunk), unordered, with -1s and repeats
+    rng = np.random.default_rng(3)
+    ta = rng.integers(-1, len(ranks), size=71).astype(np.int32)
+    ta[:20] = 4
+    for layer, proj in ((0, 0), (2, 1), (1, 1)):
+        yd, ref = _run(s, layer, proj, ta, scale=-1.25, salt=layer, x_pad=24, y_pad=8)
+        assert rel_err(yd, ref) <= TOL_BF16
+    # single token
+    yd, ref = _run(s, 1, 0, np.asarray([6], np.int32))
+    assert rel_err(yd, ref) <= TOL_BF16
+    # empty batch and all-(-1) batch leave y untouched
+    for ta in (np.zeros(0, np.int32), np.full(9, -1, np.int32)):
+        plan = BatchPlan(s.store, ta)
+        y = torch.randn(max(len(ta), 1), 128, device="cuda").to(torch.bfloat16)
+        y0 = y.clone()
+        bgmv(plan, 0, 0, torch.randn(max(len(ta), 1), 64, device="cuda").to(torch.bfloat16), y)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0)
+
+
+def test_errors_are_loud(cuda):
+    cfg = synth.cfg1(n_layers=1)
+    s = Setup(cfg)
+    s.store.retire(3)
+    with pytest.raises(ValidationError, match="not resident"):
+        BatchPlan(s.store, [0, 3])
+    plan = BatchPlan(s.store, [0, 1])
+    x = torch.zeros(2, 4096, device="cuda", dtype=torch.bfloat16)
+    y = torch.zeros(2, 4096, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(ValidationError):
+        bgmv(plan, 5, 0, x, y)  # layer out of range
+    with pytest.raises(ValidationError):
+        bgmv(plan, 0, 0, x.float(), y)  # dtype mismatch
+    with pytest.raises(ValidationError):
+        bgmv(plan, 0, 0, x[:, :2048], y)  # width mismatch
+
+
+def test_compaction_relocations_preserve_results(cuda):
+    cfg = synth.cfg1(n_layers=2)
+    s = Setup(cfg)
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    before, _ = _run(s, 1, 1, ta, salt=3)
+    # evict a few adapters, compact, move pages on device, republish
+    for a in (1, 4, 9):
+        s.store.retire(a)
+        s.pool.free(a)
+    moved = s.pool.compact()
+    assert moved > 0
+    relocs = s.pool.last_relocations()
+    s.store.apply_relocations(relocs)
+    s.pool.check_invariants()
+    live = [a for a in range(cfg.n_adapters) if a not in (1, 4, 9)]
+    ta2 = np.asarray([a if a in live else -1 for a in ta], np.int32)
+    x = synth.activations(len(ta), 4096, cfg.shape.dtype, "x", salt=3).cuda()
+    y = synth.activations(len(ta), 4096, cfg.shape.dtype, "y", salt=3).cuda()
+    bgmv(BatchPlan(s.store, ta2), 1, 1, x, y)
+    torch.cuda.synchronize()
+    keep = ta2 >= 0
+    assert torch.equal(y[torch.from_numpy(keep).cuda()], before[torch.from_numpy(keep).cuda()])
+    for a in live:  # device bytes followed their pages
+        got = s.store.read_pages(a, cfg.shape.adapter_bytes(cfg.ranks[a]))
+        assert torch.equal(got, s.images[a].view(torch.uint8))
+
+
+def test_graph_capture_and_determinism(cuda):
+    cfg = synth.cfg2(n_layers=2)
+    s = Setup(cfg)
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    plan = BatchPlan(s.store, ta)
+    x = synth.activations(len(ta), 4096, cfg.shape.dtype, "x").cuda()
+    y0 = synth.activations(len(ta), 4096, cfg.shape.dtype, "y").cuda()
+    y_eager = y0.clone()
+    for layer in range(2):
+        for proj in range(2):
+            bgmv(plan, layer, proj, x, y_eager)
+    torch.cuda.synchronize()
+    y_graph = y0.clone()
+    stream = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            for layer in range(2):
+                for proj in range(2):
+                    bgmv(plan, layer, proj, x, y_graph, stream=stream.cuda_stream)
+    y_graph.copy_(y0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y_graph, y_eager)  # same unit decomposition -> bit-identical
+    y_graph.copy_(y0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y_graph, y_eager)
+
+
+def test_linearity_property_full_cfg2(cuda):
+    """Size-independent property at BASELINE config 2 full size (32 layers):
+    zero x leaves y bit-identical; Δy(scale=2) ≈ 2·Δy(scale=1)."""
+    cfg = synth.cfg2()
+    pool = synth.build_pool(cfg)
+    store = AdapterStore(pool, cfg.shape, cfg.n_adapters)
+    for a, r in enumerate(cfg.ranks):
+        store.register(a, r)
+        img = synth.adapter_image(cfg.shape, r, a, device="cuda")
+        store.write_pages(a, img.view(torch.uint8).cpu())
+        store.publish(a)
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    plan = BatchPlan(store, ta)
+    n0 = kernel_launch_count()
+    x = torch.zeros(256, 4096, device="cuda", dtype=torch.bfloat16)
+    y = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
+    y0 = y.clone()
+    bgmv(plan, 31, 1, x, y)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y0)
+    x = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
+    yz = torch.zeros(256, 4096, device="cuda", dtype=torch.float32).to(torch.bfloat16)
+    y1, y2 = yz.clone(), yz.clone()
+    bgmv(plan, 20, 0, x, y1, 1.0)
+    bgmv(plan, 20, 0, x, y2, 2.0)
+    torch.cuda.synchronize()
+    d = (y2.float() - 2 * y1.float()).abs().max().item()
+    assert d <= 2e-2 * y2.float().abs().max().item()
+    assert kernel_launch_count() - n0 == 3
