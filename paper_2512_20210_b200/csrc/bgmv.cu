@@ -1,92 +1,62 @@
-// Paged multi-LoRA decode op (gathered BGMV) for sm_100a, plus the batch
-// plan it runs from.
+// Paged multi-LoRA decode op (gathered BGMV) for sm_100a.
 //
 // y[t, :] += scale · (x[t, :] · A_{a(t)}ᵀ) · B_{a(t)}ᵀ
 //
 // The reference only bills this op as a cost-model constant
 // (include/lorasim/cost_model.hpp:32-40, billed at src/engine.cpp:355,510);
-// the weights are read straight out of the paged arena through the device
-// page table (PagePool::translate semantics, src/memory.cpp:55-62).
+// weights are read straight out of the paged arena through the device page
+// table (PagePool::translate semantics, src/memory.cpp:55-62).
 //
-// Design (HBM-bound, AI ≈ 1.8 flop/B at Llama-7B decode shapes):
-//  * One persistent kernel per (layer, proj) call, grid = SMs × occupancy,
-//    pulling work units from an atomic ticket.  Units are equal-byte slices:
-//      shrink (segment, 8 rank rows): one warp per row of A streams d_in
-//        elements with 16-byte loads (16 in flight per lane), dots them with
-//        the segment's x rows staged in shared memory, warp-shuffle reduces
-//        and writes v (fp32) to an L2-resident workspace;
-//      expand (segment, column block): each thread holds <= 4 rank rows of
-//        Bᵀ for 8 (bf16) output columns, loaded BEFORE waiting on the
-//        segment's shrink counter, then reduces across row groups in shared
-//        memory and read-modify-writes y once.
-//    All shrink units precede all expand units in ticket order, so an expand
-//    unit only ever waits on units already held by running CTAs — no
-//    deadlock regardless of residency.  The last CTA out resets the ticket
-//    and counters, so the launch is graph-capturable.
-//  * Each adapter's weights are read exactly once per call regardless of how
-//    many of its tokens are in the batch (tokens are grouped by adapter).
-//  * Page lookups: one __ldg of the page table per 16-byte vector (L1-hot;
-//    4 B per page of weights).
+// Design (HBM-bound: AI ≈ 1.8 flop/B at Llama-7B decode shapes).  Two
+// streaming kernels per (layer, proj) call, chained with Programmatic
+// Dependent Launch:
+//
+//  shrink  one CTA per (segment, <= 8 rank rows, <= 2 tokens): warp 0 issues
+//          1-D TMA bulk copies (cp.async.bulk, one per page piece, L2
+//          evict-first) of the rows — one contiguous logical range of the
+//          adapter — and of the tokens' x rows into shared memory, all on one
+//          mbarrier; then warp w dots row w with the x rows and warp-reduces
+//          v = x·Aᵀ (fp32) into an L2-resident workspace.  It triggers the
+//          dependent launch as soon as it starts.
+//  expand  one CTA per (segment, <= 2 tokens, column block CB): it issues the
+//          bulk copies of its Bᵀ tile (r × CB, r row pieces) and the y rows
+//          BEFORE griddepcontrol.wait, so its weight stream overlaps the
+//          shrink grid; after the wait it reads v, splits rows over RG groups
+//          (<= 8 rows per thread), reduces in shared memory and stores y.
+//
+// Units are equal-byte slices built on the host (plan.cu); every adapter's
+// weights are read once per call regardless of its token count.  Several
+// CTAs per SM (48-80 KiB of smem each) keep >= 100 KiB in flight per SM.
 #include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cstring>
-#include <map>
-#include <numeric>
 
 #include "plan.hpp"
+#include "ptx.cuh"
 
 using namespace plora;
 
 namespace {
 
-constexpr uint32_t kTokChunk = 4;   // tokens per shared-memory chunk (shrink)
-constexpr uint32_t kExpTok = 2;     // tokens per accumulation chunk (expand)
-constexpr int kShrinkVecs = 8;      // 16-byte loads in flight per lane (shrink)
-constexpr int kExpandRows = 4;      // Bᵀ rows held per thread (expand)
+constexpr int kThreads = 256;
+constexpr uint32_t kExpandTok = 2;  // tokens per expand pass (reduction buffer)
 
 struct BgmvArgs {
   const char* arena;
   const uint32_t* table;
-  const SegDesc* segs;
-  const uint32_t* toks;
-  const uint2* units;
+  const BgmvUnit* units;
   float* v;
-  uint32_t* sync;  // [0] ticket, [1] exit, [2 + s] shrink-done of segment s
-  const void* x;
-  void* y;
-  uint64_t x_stride;
-  uint64_t y_stride;
+  const char* x;
+  char* y;
+  uint64_t x_stride_b;
+  uint64_t y_stride_b;
   uint64_t blk_mult;  // block (layer, proj) starts at element rank · blk_mult
   uint32_t log2_page;
-  uint32_t n_units;
-  uint32_t n_seg;
   uint32_t d_in;
   uint32_t d_out;
   float scale;
 };
-
-__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
-
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-// Address of logical byte `off` of an adapter through its page table.
-__device__ __forceinline__ const uint4* paged(const BgmvArgs& p, uint32_t table_off,
-                                              uint64_t off) {
-  const uint32_t phys = __ldg(p.table + table_off + static_cast<uint32_t>(off >> p.log2_page));
-  return reinterpret_cast<const uint4*>(p.arena + (static_cast<uint64_t>(phys) << p.log2_page) +
-                                        (off & ((1ull << p.log2_page) - 1)));
-}
 
 template <typename T>
 struct VecOps;
@@ -94,19 +64,6 @@ struct VecOps;
 template <>
 struct VecOps<__nv_bfloat16> {
   static constexpr int N = 8;
-  __device__ static __forceinline__ float dot(const uint4& a, const uint4& b) {
-    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
-    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float2 fa = __bfloat1622float2(pa[i]);
-      float2 fb = __bfloat1622float2(pb[i]);
-      s = fmaf(fa.x, fb.x, s);
-      s = fmaf(fa.y, fb.y, s);
-    }
-    return s;
-  }
   __device__ static __forceinline__ void unpack(const uint4& a, float (&f)[8]) {
     const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
 #pragma unroll
@@ -128,13 +85,6 @@ struct VecOps<__nv_bfloat16> {
 template <>
 struct VecOps<float> {
   static constexpr int N = 4;
-  __device__ static __forceinline__ float dot(const uint4& a, const uint4& b) {
-    float s = __uint_as_float(a.x) * __uint_as_float(b.x);
-    s = fmaf(__uint_as_float(a.y), __uint_as_float(b.y), s);
-    s = fmaf(__uint_as_float(a.z), __uint_as_float(b.z), s);
-    s = fmaf(__uint_as_float(a.w), __uint_as_float(b.w), s);
-    return s;
-  }
   __device__ static __forceinline__ void unpack(const uint4& a, float (&f)[4]) {
     f[0] = __uint_as_float(a.x);
     f[1] = __uint_as_float(a.y);
@@ -147,386 +97,305 @@ struct VecOps<float> {
   }
 };
 
-// ---------------------------------------------------------------- shrink
-template <typename T>
-__device__ void shrink_unit(const BgmvArgs& p, const SegDesc& sd, uint32_t seg, uint32_t j0,
-                            char* smem) {
-  using V = VecOps<T>;
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t j = j0 + warp;
-  const bool active = j < sd.rank;  // warp-uniform
-  const uint32_t nvec = p.d_in / V::N;
-  uint4* xs = reinterpret_cast<uint4*>(smem);
-  const uint64_t row_byte =
-      (static_cast<uint64_t>(sd.rank) * p.blk_mult + static_cast<uint64_t>(j) * p.d_in) * sizeof(T);
+__device__ __forceinline__ float warp_sum(float a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  return a;
+}
 
-  for (uint32_t tc = 0; tc < sd.n_tok; tc += kTokChunk) {
-    const uint32_t nch = min(kTokChunk, sd.n_tok - tc);
-    // the weight loads do not depend on x: issue them first
-    uint4 w[kShrinkVecs];
-    float acc[kTokChunk];
-#pragma unroll
-    for (uint32_t t = 0; t < kTokChunk; ++t) acc[t] = 0.f;
-    uint32_t c0 = lane;
-    if (active) {
-#pragma unroll
-      for (int g = 0; g < kShrinkVecs; ++g) {
-        const uint32_t c = c0 + 32u * g;
-        if (c < nvec) w[g] = ld_stream(paged(p, sd.table_off, row_byte + 16ull * c));
-      }
-    }
-    for (uint32_t i = threadIdx.x; i < nch * nvec; i += blockDim.x) {
-      const uint32_t t = i / nvec, c = i - t * nvec;
-      const uint32_t tok = p.toks[sd.tok_start + tc + t];
-      xs[t * nvec + c] = __ldg(reinterpret_cast<const uint4*>(static_cast<const T*>(p.x) +
-                                                              tok * p.x_stride) + c);
-    }
-    __syncthreads();
-    if (active) {
-      while (true) {
-#pragma unroll
-        for (int g = 0; g < kShrinkVecs; ++g) {
-          const uint32_t c = c0 + 32u * g;
-          if (c < nvec) {
-#pragma unroll
-            for (uint32_t t = 0; t < kTokChunk; ++t)
-              if (t < nch) acc[t] += V::dot(w[g], xs[t * nvec + c]);
-          }
-        }
-        c0 += 32u * kShrinkVecs;
-        if (c0 >= nvec) break;
-#pragma unroll
-        for (int g = 0; g < kShrinkVecs; ++g) {
-          const uint32_t c = c0 + 32u * g;
-          if (c < nvec) w[g] = ld_stream(paged(p, sd.table_off, row_byte + 16ull * c));
-        }
-      }
-#pragma unroll
-      for (uint32_t t = 0; t < kTokChunk; ++t) {
-        float a = acc[t];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        acc[t] = a;
-      }
-      if (lane == 0) {
-        for (uint32_t t = 0; t < nch; ++t)
-          p.v[sd.voff + (tc + t) * sd.rank + j] = acc[t];
-        __threadfence();
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(p.sync + 2 + seg, 1u);
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Bulk-copy the logical byte range [lo, lo + bytes) of an adapter into smem
+// at dst, one cp.async.bulk per page piece, lanes in parallel.
+__device__ __forceinline__ void gather_range(const BgmvArgs& p, uint32_t table_off, uint64_t lo,
+                                             uint32_t bytes, char* dst, uint64_t* bar,
+                                             uint64_t policy, uint32_t lane) {
+  const uint32_t L = p.log2_page;
+  const uint64_t hi = lo + bytes, p0 = lo >> L, p1 = (hi - 1) >> L;
+  for (uint64_t pg = p0 + lane; pg <= p1; pg += 32) {
+    const uint64_t a = max(lo, pg << L), b = min(hi, (pg + 1) << L);
+    const uint32_t phys = __ldg(p.table + table_off + static_cast<uint32_t>(pg));
+    ptx::bulk_g2s_hint(dst + (a - lo),
+                       p.arena + (static_cast<uint64_t>(phys) << L) + (a & ((1ull << L) - 1)),
+                       static_cast<uint32_t>(b - a), bar, policy);
   }
 }
 
-// ---------------------------------------------------------------- expand
-template <typename T, int RG>
-__device__ void expand_unit(const BgmvArgs& p, const SegDesc& sd, uint32_t seg, uint32_t c0,
-                            char* smem) {
+// ------------------------------------------------------------------ shrink
+template <typename T>
+__global__ void __launch_bounds__(kThreads) bgmv_shrink_kernel(const BgmvArgs p) {
   using V = VecOps<T>;
-  constexpr int CT = kThreads / RG;  // column threads
-  constexpr int CB = CT * V::N;      // columns per unit
-  const uint32_t rg = threadIdx.x / CT, ct = threadIdx.x % CT;
-  const uint32_t col = c0 + ct * V::N;
-  const bool col_ok = col < p.d_out;
-  const uint32_t r = sd.rank;
-  const uint64_t bt_byte =
-      (static_cast<uint64_t>(r) * p.blk_mult + static_cast<uint64_t>(r) * p.d_in) * sizeof(T);
-  const uint32_t n_i = rg < r ? (r - rg + RG - 1) / RG : 0;  // rows j = rg + RG·i
-
-  uint4 b[kExpandRows];
-#define PLORA_LOAD_ROWS(i0)                                                                  \
-  _Pragma("unroll") for (int e = 0; e < kExpandRows; ++e) {                                  \
-    const uint32_t i_ = (i0) + e;                                                            \
-    if (col_ok && i_ < n_i) {                                                                \
-      const uint32_t jj = rg + RG * i_;                                                      \
-      b[e] = ld_stream(paged(p, sd.table_off,                                                \
-                             bt_byte + (static_cast<uint64_t>(jj) * p.d_out + col) * sizeof(T))); \
-    }                                                                                        \
-  }
-  PLORA_LOAD_ROWS(0u)  // Bᵀ does not depend on v: prefetch before waiting
-
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  pdl_launch_dependents();  // the expand grid may start streaming Bᵀ now
+  const BgmvUnit u = p.units[blockIdx.x];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rowbytes = p.d_in * sizeof(T);
+  const uint32_t rpu = min(kMaxShrinkRows, kShrinkWeightBytes / rowbytes);
+  char* W = smem;                   // [count <= rpu][d_in]
+  char* X = smem + rpu * rowbytes;  // [ntok][d_in]
   if (threadIdx.x == 0) {
-    const uint32_t* flag = p.sync + 2 + seg;
-    while (ld_acquire(flag) < sd.n_shrink) __nanosleep(32);
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
   }
   __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) ptx::mbar_arrive_expect_tx(&bar, (u.count + u.ntok) * rowbytes);
+    __syncwarp();
+    const uint64_t base =
+        (static_cast<uint64_t>(u.rank) * p.blk_mult + static_cast<uint64_t>(u.off) * p.d_in) *
+        sizeof(T);
+    gather_range(p, u.table_off, base, u.count * rowbytes, W, &bar, ptx::policy_evict_first(),
+                 lane);
+    if (lane < u.ntok)
+      ptx::bulk_g2s(X + lane * rowbytes, p.x + u.tok[lane] * p.x_stride_b, rowbytes, &bar);
+  }
+  ptx::mbar_wait(&bar, 0);
+  if (warp < u.count) {
+    const uint32_t nvec = p.d_in / V::N;
+    const uint4* w = reinterpret_cast<const uint4*>(W + warp * rowbytes);
+    const uint4* xs = reinterpret_cast<const uint4*>(X);
+    float acc[kMaxUnitTok];
+#pragma unroll
+    for (int t = 0; t < kMaxUnitTok; ++t) acc[t] = 0.f;
+#pragma unroll 4
+    for (uint32_t c = lane; c < nvec; c += 32) {
+      float wf[V::N];
+      V::unpack(w[c], wf);
+#pragma unroll
+      for (int t = 0; t < kMaxUnitTok; ++t) {
+        if (t < u.ntok) {
+          float xf[V::N];
+          V::unpack(xs[t * nvec + c], xf);
+          float a = acc[t];
+#pragma unroll
+          for (int e = 0; e < V::N; ++e) a = fmaf(wf[e], xf[e], a);
+          acc[t] = a;
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kMaxUnitTok; ++t) {
+      if (t < u.ntok) {
+        const float s = warp_sum(acc[t]);
+        if (lane == 0) p.v[u.voff + t * rpad4(u.rank) + u.off + warp] = s;
+      }
+    }
+  }
+}
 
-  float* vs = reinterpret_cast<float*>(smem);  // [kExpTok][r]
-  float* red = vs + ((kExpTok * r + 3) & ~3u);  // [RG][kExpTok][CB]
-  bool first = true;
-  for (uint32_t tc = 0; tc < sd.n_tok; tc += kExpTok) {
-    const uint32_t nch = min(kExpTok, sd.n_tok - tc);
-    for (uint32_t i = threadIdx.x; i < nch * r; i += blockDim.x)
-      vs[i] = __ldcg(p.v + sd.voff + tc * r + i);
-    __syncthreads();
-    float acc[kExpTok][V::N];
+// ------------------------------------------------------------------ expand
+struct ExpandSmem {
+  // [0, kSlotWeightBytes)            Bᵀ tile, row j at j · CB · esize
+  // [.., + kSlotAuxBytes)            y rows, token t at t · CB · esize
+  // [.., + kRedBytes)                cross-group partial sums
+  // [.., + kMaxUnitTok·256·4)        v rows of the unit's tokens
+  static constexpr uint32_t y = kSlotWeightBytes;
+  static constexpr uint32_t red = y + kSlotAuxBytes;
+  static constexpr uint32_t v = red + kRedBytes;
+  static constexpr uint32_t total = v + kMaxUnitTok * kMaxBgmvRank * 4;
+};
+
+template <typename T, int RG>
+__device__ __forceinline__ void expand_compute(const BgmvArgs& p, const BgmvUnit& u, char* smem) {
+  using V = VecOps<T>;
+  constexpr int CT = kBgmvConsumers / RG;
+  constexpr int CB = CT * V::N;
+  const uint32_t tid = threadIdx.x, rg = tid / CT, ct = tid % CT;
+  const uint32_t rp = rpad4(u.rank);
+  const uint4* Bs = reinterpret_cast<const uint4*>(smem);
+  const uint4* Ys = reinterpret_cast<const uint4*>(smem + ExpandSmem::y);
+  float* red = reinterpret_cast<float*>(smem + ExpandSmem::red);
+  const float* Vs = reinterpret_cast<const float*>(smem + ExpandSmem::v);
+  // this thread's rows of Bᵀ, converted once and reused by every token pass
+  constexpr int kRows = 8;
+  for (uint32_t t0 = 0; t0 < u.ntok; t0 += kExpandTok) {
+    const uint32_t nt = min(kExpandTok, u.ntok - t0);
+    float acc[kExpandTok][V::N];
 #pragma unroll
-    for (uint32_t t = 0; t < kExpTok; ++t)
+    for (int t = 0; t < kExpandTok; ++t)
 #pragma unroll
-      for (int k = 0; k < V::N; ++k) acc[t][k] = 0.f;
-    for (uint32_t i0 = 0; i0 < n_i; i0 += kExpandRows) {
-      if (!first) { PLORA_LOAD_ROWS(i0) }
-      first = false;
+      for (int e = 0; e < V::N; ++e) acc[t][e] = 0.f;
+    for (uint32_t j0 = rg; j0 < u.rank; j0 += RG * kRows) {
 #pragma unroll
-      for (int e = 0; e < kExpandRows; ++e) {
-        const uint32_t i = i0 + e;
-        if (i < n_i) {
-          const uint32_t jj = rg + RG * i;
+      for (int i = 0; i < kRows; ++i) {
+        const uint32_t j = j0 + i * RG;
+        if (j < u.rank) {
           float bf[V::N];
-          V::unpack(b[e], bf);
+          V::unpack(Bs[j * CT + ct], bf);
 #pragma unroll
-          for (uint32_t t = 0; t < kExpTok; ++t) {
-            if (t < nch) {
-              const float vt = vs[t * r + jj];
+          for (int t = 0; t < kExpandTok; ++t) {
+            if (t < nt) {
+              const float vt = Vs[(t0 + t) * rp + j];
 #pragma unroll
-              for (int k = 0; k < V::N; ++k) acc[t][k] = fmaf(vt, bf[k], acc[t][k]);
+              for (int e = 0; e < V::N; ++e) acc[t][e] = fmaf(vt, bf[e], acc[t][e]);
             }
           }
         }
       }
     }
-    first = false;
-    // partial sums of this row group
+    if constexpr (RG == 1) {
+      if (ct * V::N < u.count) {
 #pragma unroll
-    for (uint32_t t = 0; t < kExpTok; ++t) {
-      float4* dst = reinterpret_cast<float4*>(red + (rg * kExpTok + t) * CB + ct * V::N);
+        for (int t = 0; t < kExpandTok; ++t) {
+          if (t < nt) {
+            float yv[V::N];
+            V::unpack(Ys[(t0 + t) * CT + ct], yv);
 #pragma unroll
-      for (int k = 0; k < V::N; k += 4)
-        dst[k / 4] = make_float4(acc[t][k], acc[t][k + 1], acc[t][k + 2], acc[t][k + 3]);
-    }
-    __syncthreads();
-    for (uint32_t o = threadIdx.x; o < nch * CT; o += blockDim.x) {
-      const uint32_t t = o / CT, cc = o - t * CT;
-      const uint32_t colo = c0 + cc * V::N;
-      if (colo < p.d_out) {
-        float sum[V::N];
-#pragma unroll
-        for (int k = 0; k < V::N; ++k) sum[k] = 0.f;
-#pragma unroll
-        for (int g = 0; g < RG; ++g) {
-          const float4* src =
-              reinterpret_cast<const float4*>(red + (g * kExpTok + t) * CB + cc * V::N);
-#pragma unroll
-          for (int k = 0; k < V::N; k += 4) {
-            float4 q = src[k / 4];
-            sum[k] += q.x;
-            sum[k + 1] += q.y;
-            sum[k + 2] += q.z;
-            sum[k + 3] += q.w;
+            for (int e = 0; e < V::N; ++e) yv[e] = fmaf(p.scale, acc[t][e], yv[e]);
+            *reinterpret_cast<uint4*>(p.y + u.tok[t0 + t] * p.y_stride_b +
+                                      static_cast<uint64_t>(u.off + ct * V::N) * sizeof(T)) =
+                V::pack(yv);
           }
         }
-        const uint32_t tok = p.toks[sd.tok_start + tc + t];
-        uint4* yp = reinterpret_cast<uint4*>(static_cast<T*>(p.y) + tok * p.y_stride + colo);
-        float yv[V::N];
-        V::unpack(*yp, yv);
-#pragma unroll
-        for (int k = 0; k < V::N; ++k) yv[k] = fmaf(p.scale, sum[k], yv[k]);
-        *yp = V::pack(yv);
       }
+    } else {
+#pragma unroll
+      for (int t = 0; t < kExpandTok; ++t) {
+        if (t < nt) {
+          float4* dst = reinterpret_cast<float4*>(red + (t * RG + rg) * CB + ct * V::N);
+#pragma unroll
+          for (int e = 0; e < V::N; e += 4)
+            dst[e / 4] = make_float4(acc[t][e], acc[t][e + 1], acc[t][e + 2], acc[t][e + 3]);
+        }
+      }
+      __syncthreads();
+      for (uint32_t o = tid; o < nt * CT; o += kThreads) {
+        const uint32_t t = o / CT, cc = o - t * CT;
+        if (cc * V::N < u.count) {
+          float s[V::N];
+#pragma unroll
+          for (int e = 0; e < V::N; ++e) s[e] = 0.f;
+#pragma unroll
+          for (int g = 0; g < RG; ++g) {
+            const float4* src = reinterpret_cast<const float4*>(red + (t * RG + g) * CB + cc * V::N);
+#pragma unroll
+            for (int e = 0; e < V::N; e += 4) {
+              const float4 q = src[e / 4];
+              s[e] += q.x;
+              s[e + 1] += q.y;
+              s[e + 2] += q.z;
+              s[e + 3] += q.w;
+            }
+          }
+          float yv[V::N];
+          V::unpack(Ys[(t0 + t) * CT + cc], yv);
+#pragma unroll
+          for (int e = 0; e < V::N; ++e) yv[e] = fmaf(p.scale, s[e], yv[e]);
+          *reinterpret_cast<uint4*>(p.y + u.tok[t0 + t] * p.y_stride_b +
+                                    static_cast<uint64_t>(u.off + cc * V::N) * sizeof(T)) =
+              V::pack(yv);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
-#undef PLORA_LOAD_ROWS
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 2) bgmv_paged_kernel(const BgmvArgs p) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ uint32_t s_unit;
-  __shared__ uint32_t s_last;
-  while (true) {
-    if (threadIdx.x == 0) s_unit = atomicAdd(p.sync, 1u);
-    __syncthreads();
-    const uint32_t u = s_unit;
-    __syncthreads();
-    if (u >= p.n_units) break;
-    const uint2 un = p.units[u];
-    const uint32_t seg = un.x & ~kExpandBit;
-    const SegDesc sd = p.segs[seg];
-    if (!(un.x & kExpandBit)) {
-      shrink_unit<T>(p, sd, seg, un.y, smem);
-    } else {
-      switch (expand_rg(sd.rank)) {
-        case 4: expand_unit<T, 4>(p, sd, seg, un.y, smem); break;
-        case 8: expand_unit<T, 8>(p, sd, seg, un.y, smem); break;
-        case 16: expand_unit<T, 16>(p, sd, seg, un.y, smem); break;
-        default: expand_unit<T, 32>(p, sd, seg, un.y, smem); break;
-      }
-    }
-  }
-  // last CTA out resets the ticket and the per-segment counters
+__global__ void __launch_bounds__(kThreads) bgmv_expand_kernel(const BgmvArgs p) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t bar;
+  const BgmvUnit u = p.units[blockIdx.x];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rg = expand_rg(u.rank);
+  const uint32_t cb = (kBgmvConsumers / rg) * (16 / sizeof(T));
+  const uint32_t segbytes = u.count * sizeof(T);  // one row's column segment
   if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(p.sync + 1, 1u) == gridDim.x - 1;
+    ptx::mbar_init(&bar, 1);
+    ptx::fence_mbar_init();
   }
   __syncthreads();
-  if (s_last) {
-    for (uint32_t i = threadIdx.x; i < p.n_seg; i += blockDim.x) p.sync[2 + i] = 0;
-    if (threadIdx.x == 0) {
-      p.sync[0] = 0;
-      p.sync[1] = 0;
+  // Bᵀ tile + y rows do not depend on the shrink grid: stream them now.
+  if (warp == 0) {
+    if (lane == 0) ptx::mbar_arrive_expect_tx(&bar, (u.rank + u.ntok) * segbytes);
+    __syncwarp();
+    const uint64_t policy = ptx::policy_evict_first();
+    const uint64_t bt = (static_cast<uint64_t>(u.rank) * p.blk_mult +
+                         static_cast<uint64_t>(u.rank) * p.d_in + u.off) * sizeof(T);
+    const uint32_t L = p.log2_page;
+    // rows j: [bt + j·d_out·esize, + segbytes), usually one page piece each
+    for (uint32_t j = lane; j < u.rank; j += 32) {
+      const uint64_t lo = bt + static_cast<uint64_t>(j) * p.d_out * sizeof(T), hi = lo + segbytes;
+      for (uint64_t pg = lo >> L; pg <= ((hi - 1) >> L); ++pg) {
+        const uint64_t a = max(lo, pg << L), b = min(hi, (pg + 1) << L);
+        const uint32_t phys = __ldg(p.table + u.table_off + static_cast<uint32_t>(pg));
+        ptx::bulk_g2s_hint(smem + j * cb * sizeof(T) + (a - lo),
+                           p.arena + (static_cast<uint64_t>(phys) << L) + (a & ((1ull << L) - 1)),
+                           static_cast<uint32_t>(b - a), &bar, policy);
+      }
     }
+    if (lane < u.ntok)
+      ptx::bulk_g2s(smem + ExpandSmem::y + lane * cb * sizeof(T),
+                    p.y + u.tok[lane] * p.y_stride_b + static_cast<uint64_t>(u.off) * sizeof(T),
+                    segbytes, &bar);
+  }
+  // v = x·Aᵀ comes from the shrink grid
+  pdl_wait();
+  {
+    const uint32_t rp = rpad4(u.rank);
+    float* vs = reinterpret_cast<float*>(smem + ExpandSmem::v);
+    for (uint32_t i = threadIdx.x; i < u.ntok * rp; i += kThreads) vs[i] = __ldcg(p.v + u.voff + i);
+  }
+  ptx::mbar_wait(&bar, 0);
+  __syncthreads();
+  switch (rg) {
+    case 1: expand_compute<T, 1>(p, u, smem); break;
+    case 2: expand_compute<T, 2>(p, u, smem); break;
+    case 4: expand_compute<T, 4>(p, u, smem); break;
+    case 8: expand_compute<T, 8>(p, u, smem); break;
+    case 16: expand_compute<T, 16>(p, u, smem); break;
+    default: expand_compute<T, 32>(p, u, smem); break;
   }
 }
 
-// Occupancy cache: (kernel, smem) -> resident CTAs per SM.
-int blocks_per_sm(const void* fn, uint32_t smem) {
-  static std::map<std::pair<const void*, uint32_t>, int> cache;
-  auto key = std::make_pair(fn, smem);
-  auto it = cache.find(key);
-  if (it != cache.end()) return it->second;
-  static std::map<const void*, uint32_t> attr_set;
-  if (smem > 48 * 1024 && attr_set[fn] < smem) {
-    PLORA_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(smem)));
-    attr_set[fn] = smem;
+template <typename T>
+void launch(const BgmvArgs& a, const ProjWork& pw, const BgmvUnit* d_units, uint32_t shrink_smem,
+            cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    PLORA_CUDA(cudaFuncSetAttribute(bgmv_shrink_kernel<T>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    PLORA_CUDA(cudaFuncSetAttribute(bgmv_expand_kernel<T>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(ExpandSmem::total)));
+    attr = true;
   }
-  int n = 0;
-  PLORA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, kThreads, smem));
-  cache[key] = std::max(n, 1);
-  return cache[key];
-}
-
-uint32_t expand_cols(uint32_t rank, uint32_t esize) {
-  return (kThreads / expand_rg(rank)) * (16 / esize);
+  BgmvArgs sa = a;
+  sa.units = d_units;
+  if (pw.n_shrink) {
+    bgmv_shrink_kernel<T><<<pw.n_shrink, kThreads, shrink_smem, s>>>(sa);
+    PLORA_CUDA(cudaGetLastError());
+    count_launch();
+  }
+  const uint32_t n_expand = pw.n_units - pw.n_shrink;
+  if (n_expand) {
+    BgmvArgs ea = a;
+    ea.units = d_units + pw.n_shrink;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_expand);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = ExpandSmem::total;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_expand_kernel<T>, ea));
+    count_launch();
+  }
 }
 
 }  // namespace
 
-// ------------------------------------------------------------------ plan
-void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream) {
-  const plora_store& st = *store;
-  const ModelGeom& g = st.geom;
-  // group tokens by adapter: validate residency first (host shadow)
-  std::vector<uint32_t> count;
-  count.assign(st.max_adapters, 0);
-  for (uint32_t t = 0; t < n; ++t) {
-    const int32_t a = token_adapter[t];
-    if (a < 0) continue;
-    if (static_cast<uint32_t>(a) >= st.max_adapters)
-      throw ValidationError("token " + std::to_string(t) + " names adapter " + std::to_string(a) +
-                            " >= max_adapters");
-    if (!st.slots[a].published)
-      throw ValidationError("token " + std::to_string(t) + " names adapter " + std::to_string(a) +
-                            " which is not resident (publish it first)");
-    ++count[a];
-  }
-  segs.clear();
-  toks.assign(n, 0);
-  std::vector<uint32_t> cursor(st.max_adapters, 0);
-  uint32_t pos = 0;
-  max_rank = 0;
-  v_elems = 0;
-  for (uint32_t a = 0; a < st.max_adapters; ++a) {
-    if (!count[a]) continue;
-    SegDesc sd{};
-    sd.table_off = st.h_dir[a].table_off;
-    sd.rank = st.h_dir[a].rank;
-    sd.tok_start = pos;
-    sd.n_tok = count[a];
-    sd.voff = static_cast<uint32_t>(v_elems);
-    sd.n_shrink = (sd.rank + kShrinkRows - 1) / kShrinkRows;
-    sd.adapter = a;
-    cursor[a] = pos;
-    pos += count[a];
-    v_elems += static_cast<uint64_t>(sd.n_tok) * sd.rank;
-    max_rank = std::max(max_rank, sd.rank);
-    segs.push_back(sd);
-  }
-  if (v_elems > 0xffffffffull) throw ValidationError("batch too large for one plan");
-  for (uint32_t t = 0; t < n; ++t)
-    if (token_adapter[t] >= 0) toks[cursor[token_adapter[t]]++] = t;
-  toks.resize(pos);
-  n_tokens = n;
-  n_seg = static_cast<uint32_t>(segs.size());
-
-  // segment order for scheduling: largest rank first (longest dependency
-  // chains start earliest), ties by adapter key
-  std::vector<uint32_t> order(n_seg);
-  std::iota(order.begin(), order.end(), 0u);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](uint32_t x, uint32_t y) { return segs[x].rank > segs[y].rank; });
-
-  units.clear();
-  for (uint32_t p = 0; p < g.m.n_proj; ++p) {
-    ProjUnits& pu = proj[p];
-    pu.units_off = static_cast<uint32_t>(units.size());
-    for (uint32_t s : order)
-      for (uint32_t j0 = 0; j0 < segs[s].rank; j0 += kShrinkRows) units.push_back(make_uint2(s, j0));
-    for (uint32_t s : order) {
-      const uint32_t cb = expand_cols(segs[s].rank, g.esize);
-      for (uint32_t c0 = 0; c0 < g.m.d_out[p]; c0 += cb) units.push_back(make_uint2(s | kExpandBit, c0));
-    }
-    pu.n_units = static_cast<uint32_t>(units.size()) - pu.units_off;
-    // shared memory: max(shrink x staging, expand v + reduction)
-    const uint32_t shrink_smem = kTokChunk * g.m.d_in[p] * g.esize;
-    // expand: v chunk [kExpTok][max_rank] + partials [RG][kExpTok][CB] floats,
-    // and RG · CB = kThreads · (16 / esize) for every rank
-    const uint32_t expand_smem =
-        (((kExpTok * max_rank + 3) & ~3u) + kExpTok * kThreads * (16 / g.esize)) * 4;
-    pu.smem = std::max(shrink_smem, expand_smem);
-  }
-
-  // pack segs | toks | units into one pinned buffer and upload once
-  auto align = [](uint64_t v) { return (v + 255) & ~255ull; };
-  const uint64_t seg_b = align(segs.size() * sizeof(SegDesc));
-  const uint64_t tok_b = align(toks.size() * sizeof(uint32_t));
-  const uint64_t unit_b = align(units.size() * sizeof(uint2));
-  const uint64_t total = std::max<uint64_t>(seg_b + tok_b + unit_b, 256);
-  DeviceCtx ctx(st.device);
-  if (upload_done) PLORA_CUDA(cudaEventSynchronize(upload_done));  // pinned buffer reuse
-  if (h_cap < total) {
-    if (h_pinned) cudaFreeHost(h_pinned);
-    h_pinned = nullptr;
-    PLORA_CUDA(cudaMallocHost(&h_pinned, total));
-    h_cap = total;
-  }
-  if (d_cap < total) {
-    if (d_buf) {
-      PLORA_CUDA(cudaStreamSynchronize(stream));
-      cudaFree(d_buf);
-    }
-    d_buf = nullptr;
-    PLORA_CUDA(cudaMalloc(&d_buf, total));
-    d_cap = total;
-  }
-  std::memcpy(h_pinned, segs.data(), segs.size() * sizeof(SegDesc));
-  std::memcpy(h_pinned + seg_b, toks.data(), toks.size() * sizeof(uint32_t));
-  std::memcpy(h_pinned + seg_b + tok_b, units.data(), units.size() * sizeof(uint2));
-  d_segs = reinterpret_cast<SegDesc*>(d_buf);
-  d_toks = reinterpret_cast<uint32_t*>(d_buf + seg_b);
-  d_units = reinterpret_cast<uint2*>(d_buf + seg_b + tok_b);
-  PLORA_CUDA(cudaMemcpyAsync(d_buf, h_pinned, seg_b + tok_b + unit_b, cudaMemcpyHostToDevice,
-                             stream));
-  if (!upload_done) PLORA_CUDA(cudaEventCreateWithFlags(&upload_done, cudaEventDisableTiming));
-  PLORA_CUDA(cudaEventRecord(upload_done, stream));
-
-  if (v_cap < std::max<uint64_t>(v_elems, 1)) {
-    if (d_v) {
-      PLORA_CUDA(cudaStreamSynchronize(stream));
-      cudaFree(d_v);
-    }
-    d_v = nullptr;
-    v_cap = std::max<uint64_t>(v_elems, 1024);
-    PLORA_CUDA(cudaMalloc(&d_v, v_cap * sizeof(float)));
-  }
-  if (sync_cap < 2ull + n_seg) {
-    if (d_sync) {
-      PLORA_CUDA(cudaStreamSynchronize(stream));
-      cudaFree(d_sync);
-    }
-    d_sync = nullptr;
-    sync_cap = std::max<uint64_t>(2ull + n_seg, 1024);
-    PLORA_CUDA(cudaMalloc(&d_sync, sync_cap * sizeof(uint32_t)));
-    PLORA_CUDA(cudaMemsetAsync(d_sync, 0, sync_cap * sizeof(uint32_t), stream));
-  }
-}
-
-namespace {
+namespace plora {
 
 void check_io(const plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
               uint64_t x_stride, void* y, uint64_t y_stride) {
@@ -543,94 +412,42 @@ void check_io(const plora_plan* plan, uint32_t layer, uint32_t proj, const void*
     throw ValidationError("x and y must be 16-byte aligned");
 }
 
-}  // namespace
+}  // namespace plora
 
-extern "C" {
-
-int plora_plan_create(plora_store* s, const int32_t* token_adapter, uint32_t n_tokens,
-                      plora_stream_t stream, plora_plan** out) {
-  return guard([&] {
-    if (!s) throw ValidationError("null store");
-    if (n_tokens && !token_adapter) throw ValidationError("null token_adapter");
-    auto plan = std::make_unique<plora_plan>();
-    plan->store = s;
-    plan->build(token_adapter, n_tokens, static_cast<cudaStream_t>(stream));
-    *out = plan.release();
-    return 0;
-  });
-}
-
-int plora_plan_update(plora_plan* plan, const int32_t* token_adapter, uint32_t n_tokens,
-                      plora_stream_t stream) {
-  return guard([&] {
-    if (!plan) throw ValidationError("null plan");
-    if (n_tokens && !token_adapter) throw ValidationError("null token_adapter");
-    plan->build(token_adapter, n_tokens, static_cast<cudaStream_t>(stream));
-    return 0;
-  });
-}
-
-void plora_plan_destroy(plora_plan* plan) {
-  if (!plan) return;
-  DeviceCtx ctx(plan->store->device);
-  if (plan->upload_done) {
-    cudaEventSynchronize(plan->upload_done);
-    cudaEventDestroy(plan->upload_done);
-  }
-  cudaDeviceSynchronize();
-  cudaFreeHost(plan->h_pinned);
-  cudaFree(plan->d_buf);
-  cudaFree(plan->d_v);
-  cudaFree(plan->d_sync);
-  delete plan;
-}
-
-uint32_t plora_plan_num_segments(const plora_plan* plan) { return plan ? plan->n_seg : 0; }
-
-int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
-               uint64_t x_stride, void* y, uint64_t y_stride, float scale,
-               plora_stream_t stream) {
+extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
+                          uint64_t x_stride, void* y, uint64_t y_stride, float scale,
+                          plora_stream_t stream) {
   return guard([&] {
     if (!plan) throw ValidationError("null plan");
     check_io(plan, layer, proj, x, x_stride, y, y_stride);
     const plora_store& st = *plan->store;
     const ModelGeom& g = st.geom;
-    const ProjUnits& pu = plan->proj[proj];
-    if (pu.n_units == 0) return 0;
+    const ProjWork& pw = plan->proj[proj];
+    if (pw.n_units == 0) return 0;
     DeviceCtx ctx(st.device);
     BgmvArgs a{};
     a.arena = st.arena;
     a.table = st.d_table;
-    a.segs = plan->d_segs;
-    a.toks = plan->d_toks;
-    a.units = plan->d_units + pu.units_off;
     a.v = plan->d_v;
-    a.sync = plan->d_sync;
-    a.x = x;
-    a.y = y;
-    a.x_stride = x_stride;
-    a.y_stride = y_stride;
+    a.x = static_cast<const char*>(x);
+    a.y = static_cast<char*>(y);
+    a.x_stride_b = x_stride * g.esize;
+    a.y_stride_b = y_stride * g.esize;
     a.blk_mult = g.blk_mult(layer, proj);
     a.log2_page = st.log2_page;
-    a.n_units = pu.n_units;
-    a.n_seg = plan->n_seg;
     a.d_in = g.m.d_in[proj];
     a.d_out = g.m.d_out[proj];
     a.scale = scale;
+    const uint32_t rowbytes = a.d_in * g.esize;
+    const uint32_t rpu = std::min<uint32_t>(kMaxShrinkRows, kShrinkWeightBytes / rowbytes);
+    const uint32_t nts = std::min<uint32_t>(kMaxUnitTok, kSlotAuxBytes / rowbytes);
+    const uint32_t shrink_smem = (rpu + nts) * rowbytes;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const void* fn = g.esize == 2 ? reinterpret_cast<const void*>(bgmv_paged_kernel<__nv_bfloat16>)
-                                  : reinterpret_cast<const void*>(bgmv_paged_kernel<float>);
-    const int per_sm = blocks_per_sm(fn, pu.smem);
-    const uint32_t grid = std::min<uint32_t>(pu.n_units, static_cast<uint32_t>(per_sm * st.num_sms));
-    if (g.esize == 2) {
-      bgmv_paged_kernel<__nv_bfloat16><<<grid, kThreads, pu.smem, s>>>(a);
-    } else {
-      bgmv_paged_kernel<float><<<grid, kThreads, pu.smem, s>>>(a);
-    }
-    PLORA_CUDA(cudaGetLastError());
-    count_launch();
+    const BgmvUnit* units = plan->d_units + pw.units_off;
+    if (g.esize == 2)
+      launch<__nv_bfloat16>(a, pw, units, shrink_smem, s);
+    else
+      launch<float>(a, pw, units, shrink_smem, s);
     return 0;
   });
 }
-
-}  // extern "C"

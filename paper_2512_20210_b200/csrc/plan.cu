@@ -1,0 +1,238 @@
+// Batch plan construction (host) and its C ABI.  See plan.hpp.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "plan.hpp"
+
+using namespace plora;
+
+namespace {
+
+struct Seg {
+  uint32_t adapter, rank, table_off, voff;
+  std::vector<uint32_t> toks;
+};
+
+}  // namespace
+
+void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream) {
+  const plora_store& st = *store;
+  const ModelGeom& g = st.geom;
+  const uint32_t es = g.esize, vec = 16 / es;
+
+  // ---- group tokens by adapter (validates residency on the host shadow)
+  std::vector<int32_t> seg_of(st.max_adapters, -1);
+  std::vector<Seg> segs;
+  for (uint32_t t = 0; t < n; ++t) {
+    const int32_t a = token_adapter[t];
+    if (a < 0) continue;
+    if (static_cast<uint32_t>(a) >= st.max_adapters)
+      throw ValidationError("token " + std::to_string(t) + " names adapter " + std::to_string(a) +
+                            " >= max_adapters");
+    if (!st.slots[a].published)
+      throw ValidationError("token " + std::to_string(t) + " names adapter " + std::to_string(a) +
+                            " which is not resident (publish it first)");
+    if (seg_of[a] < 0) {
+      seg_of[a] = static_cast<int32_t>(segs.size());
+      segs.push_back(Seg{static_cast<uint32_t>(a), st.h_dir[a].rank, st.h_dir[a].table_off, 0, {}});
+    }
+    segs[seg_of[a]].toks.push_back(t);
+  }
+  // ascending adapter key (deterministic), v offsets 16-byte aligned
+  std::sort(segs.begin(), segs.end(), [](const Seg& x, const Seg& y) { return x.adapter < y.adapter; });
+  v_elems = 0;
+  max_rank = 0;
+  for (Seg& s : segs) {
+    if (s.rank > kMaxBgmvRank)
+      throw ValidationError("adapter " + std::to_string(s.adapter) + " has rank " +
+                            std::to_string(s.rank) + " > " + std::to_string(kMaxBgmvRank));
+    s.voff = static_cast<uint32_t>(v_elems);
+    v_elems += static_cast<uint64_t>(s.toks.size()) * rpad4(s.rank);
+    max_rank = std::max(max_rank, s.rank);
+  }
+  if (v_elems > 0xffffffffull) throw ValidationError("batch too large for one plan");
+  n_tokens = n;
+  n_seg = static_cast<uint32_t>(segs.size());
+
+  // schedule order: largest rank first (LPT), ties by adapter key
+  std::vector<uint32_t> order(n_seg);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](uint32_t x, uint32_t y) { return segs[x].rank > segs[y].rank; });
+
+  // ---- BGMV units per projection
+  units.clear();
+  for (uint32_t p = 0; p < g.m.n_proj; ++p) {
+    const uint32_t din = g.m.d_in[p], dout = g.m.d_out[p];
+    const uint32_t rowbytes = din * es;
+    if (rowbytes > kSlotAuxBytes)
+      throw ValidationError("BGMV needs d_in * esize <= " + std::to_string(kSlotAuxBytes) +
+                            " bytes (d_in=" + std::to_string(din) + ")");
+    const uint32_t rpu = std::min<uint32_t>(kMaxShrinkRows, kShrinkWeightBytes / rowbytes);
+    const uint32_t nts = std::min<uint32_t>(kMaxUnitTok, kSlotAuxBytes / rowbytes);
+    ProjWork& pw = proj[p];
+    pw.units_off = static_cast<uint32_t>(units.size());
+    std::vector<uint32_t> n_shrink(n_seg, 0);
+    for (uint32_t si : order) {
+      const Seg& s = segs[si];
+      const uint32_t rp = rpad4(s.rank), nt_all = static_cast<uint32_t>(s.toks.size());
+      for (uint32_t tc = 0; tc < nt_all; tc += nts) {
+        const uint32_t nt = std::min(nts, nt_all - tc);
+        for (uint32_t j0 = 0; j0 < s.rank; j0 += rpu) {
+          BgmvUnit u{};
+          u.kind_seg = si;
+          u.off = j0;
+          u.count = std::min(rpu, s.rank - j0);
+          u.table_off = s.table_off;
+          u.rank = s.rank;
+          u.voff = s.voff + tc * rp;
+          u.ntok = nt;
+          for (uint32_t t = 0; t < nt; ++t) u.tok[t] = s.toks[tc + t];
+          units.push_back(u);
+          ++n_shrink[si];
+        }
+      }
+    }
+    pw.n_shrink = static_cast<uint32_t>(units.size()) - pw.units_off;
+    for (uint32_t si : order) {
+      const Seg& s = segs[si];
+      const uint32_t rp = rpad4(s.rank), nt_all = static_cast<uint32_t>(s.toks.size());
+      const uint32_t rg = expand_rg(s.rank), cb = (kBgmvConsumers / rg) * vec;
+      const uint32_t per_tok = rp * 4 + cb * es;
+      // tokens per unit: aux area (v + y rows) and, when rows are split over
+      // groups, the reduction buffer (RG · CB fp32 per token)
+      uint32_t nte = std::min<uint32_t>(kMaxUnitTok, kSlotAuxBytes / per_tok);
+      if (rg > 1) nte = std::min<uint32_t>(nte, kRedBytes / (rg * cb * 4));
+      nte = std::max<uint32_t>(nte, 1);
+      for (uint32_t tc = 0; tc < nt_all; tc += nte) {
+        const uint32_t nt = std::min(nte, nt_all - tc);
+        for (uint32_t c0 = 0; c0 < dout; c0 += cb) {
+          BgmvUnit u{};
+          u.kind_seg = si | kExpandBit;
+          u.off = c0;
+          u.count = std::min(cb, dout - c0);
+          u.table_off = s.table_off;
+          u.rank = s.rank;
+          u.voff = s.voff + tc * rp;
+          u.ntok = nt;
+          u.n_shrink = n_shrink[si];
+          for (uint32_t t = 0; t < nt; ++t) u.tok[t] = s.toks[tc + t];
+          units.push_back(u);
+        }
+      }
+    }
+    pw.n_units = static_cast<uint32_t>(units.size()) - pw.units_off;
+  }
+
+  // ---- SGMV tiles: runs of consecutive tokens with the same adapter
+  tiles.clear();
+  uint32_t t = 0;
+  while (t < n) {
+    const int32_t a = token_adapter[t];
+    uint32_t e = t + 1;
+    while (e < n && token_adapter[e] == a) ++e;
+    if (a >= 0) {
+      for (uint32_t r0 = t; r0 < e; r0 += 128)
+        tiles.push_back(SgmvTile{r0, std::min<uint32_t>(128, e - r0), st.h_dir[a].table_off,
+                                 st.h_dir[a].rank});
+    }
+    t = e;
+  }
+  n_tiles = static_cast<uint32_t>(tiles.size());
+
+  // ---- upload units | tiles in one copy from a pinned staging buffer
+  auto align = [](uint64_t v) { return (v + 255) & ~255ull; };
+  const uint64_t unit_b = align(units.size() * sizeof(BgmvUnit));
+  const uint64_t tile_b = align(tiles.size() * sizeof(SgmvTile));
+  const uint64_t total = std::max<uint64_t>(unit_b + tile_b, 256);
+  DeviceCtx ctx(st.device);
+  if (upload_done) PLORA_CUDA(cudaEventSynchronize(upload_done));  // pinned buffer reuse
+  if (h_cap < total) {
+    if (h_pinned) cudaFreeHost(h_pinned);
+    h_pinned = nullptr;
+    PLORA_CUDA(cudaMallocHost(&h_pinned, total));
+    h_cap = total;
+  }
+  if (d_cap < total) {
+    if (d_buf) {
+      PLORA_CUDA(cudaStreamSynchronize(stream));
+      cudaFree(d_buf);
+    }
+    d_buf = nullptr;
+    PLORA_CUDA(cudaMalloc(&d_buf, total));
+    d_cap = total;
+  }
+  std::memcpy(h_pinned, units.data(), units.size() * sizeof(BgmvUnit));
+  std::memcpy(h_pinned + unit_b, tiles.data(), tiles.size() * sizeof(SgmvTile));
+  d_units = reinterpret_cast<BgmvUnit*>(d_buf);
+  d_tiles = reinterpret_cast<SgmvTile*>(d_buf + unit_b);
+  PLORA_CUDA(cudaMemcpyAsync(d_buf, h_pinned, unit_b + tile_b, cudaMemcpyHostToDevice, stream));
+  if (!upload_done) PLORA_CUDA(cudaEventCreateWithFlags(&upload_done, cudaEventDisableTiming));
+  PLORA_CUDA(cudaEventRecord(upload_done, stream));
+
+  if (v_cap < std::max<uint64_t>(v_elems, 1)) {
+    if (d_v) {
+      PLORA_CUDA(cudaStreamSynchronize(stream));
+      cudaFree(d_v);
+    }
+    d_v = nullptr;
+    v_cap = std::max<uint64_t>(v_elems, 4096);
+    PLORA_CUDA(cudaMalloc(&d_v, v_cap * sizeof(float)));
+  }
+  if (sync_cap < 2ull + n_seg) {
+    if (d_sync) {
+      PLORA_CUDA(cudaStreamSynchronize(stream));
+      cudaFree(d_sync);
+    }
+    d_sync = nullptr;
+    sync_cap = std::max<uint64_t>(2ull + n_seg, 1024);
+    PLORA_CUDA(cudaMalloc(&d_sync, sync_cap * sizeof(uint32_t)));
+    PLORA_CUDA(cudaMemsetAsync(d_sync, 0, sync_cap * sizeof(uint32_t), stream));
+  }
+}
+
+extern "C" {
+
+int plora_plan_create(plora_store* s, const int32_t* token_adapter, uint32_t n_tokens,
+                      plora_stream_t stream, plora_plan** out) {
+  return guard([&] {
+    if (!s) throw ValidationError("null store");
+    if (n_tokens && !token_adapter) throw ValidationError("null token_adapter");
+    auto plan = std::make_unique<plora_plan>();
+    plan->store = s;
+    plan->build(token_adapter, n_tokens, static_cast<cudaStream_t>(stream));
+    *out = plan.release();
+    return 0;
+  });
+}
+
+int plora_plan_update(plora_plan* plan, const int32_t* token_adapter, uint32_t n_tokens,
+                      plora_stream_t stream) {
+  return guard([&] {
+    if (!plan) throw ValidationError("null plan");
+    if (n_tokens && !token_adapter) throw ValidationError("null token_adapter");
+    plan->build(token_adapter, n_tokens, static_cast<cudaStream_t>(stream));
+    return 0;
+  });
+}
+
+void plora_plan_destroy(plora_plan* plan) {
+  if (!plan) return;
+  DeviceCtx ctx(plan->store->device);
+  if (plan->upload_done) {
+    cudaEventSynchronize(plan->upload_done);
+    cudaEventDestroy(plan->upload_done);
+  }
+  cudaDeviceSynchronize();
+  cudaFreeHost(plan->h_pinned);
+  cudaFree(plan->d_buf);
+  cudaFree(plan->d_v);
+  cudaFree(plan->d_sync);
+  delete plan;
+}
+
+uint32_t plora_plan_num_segments(const plora_plan* plan) { return plan ? plan->n_seg : 0; }
+
+}  // extern "C"

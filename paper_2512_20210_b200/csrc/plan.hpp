@@ -1,7 +1,7 @@
-// Batch plan: tokens grouped by adapter (segments) and the work-unit lists
-// the persistent kernels consume.  Built on the host once per batch and
-// reused for every (layer, proj) call of the step — the "translation once
-// per batch" of PAPER.md:136.
+// Batch plan: tokens grouped by adapter (segments) and the work lists the
+// persistent kernels consume.  Built on the host once per batch and reused
+// for every (layer, proj) call of the step — the "translation once per
+// batch" of PAPER.md:136.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -13,38 +13,64 @@
 
 namespace plora {
 
-// One segment = the tokens of one adapter in this batch.  32 bytes.
-struct SegDesc {
-  uint32_t table_off;  // adapter's first entry in the device page table
-  uint32_t rank;
-  uint32_t tok_start;  // into the token list
-  uint32_t n_tok;
-  uint32_t voff;       // fp32 offset of this segment's v = x·Aᵀ block
-  uint32_t n_shrink;   // shrink units the expand units of this segment wait for
-  uint32_t adapter;
-  uint32_t pad;
-};
-
-// Work unit: x = segment | kind << 31 (0 shrink, 1 expand); y = first rank
-// row (shrink) or first output column (expand).
+// ---------------------------------------------------------------- BGMV
 constexpr uint32_t kExpandBit = 0x80000000u;
-constexpr uint32_t kShrinkRows = 8;  // one warp per rank row, 8 warps per CTA
-constexpr uint32_t kThreads = 256;
+constexpr uint32_t kStopUnit = 0xffffffffu;
+constexpr uint32_t kMaxUnitTok = 4;           // tokens per work unit
+constexpr uint32_t kShrinkWeightBytes = 65536;  // A rows per shrink CTA
+constexpr uint32_t kSlotWeightBytes = 32768;    // Bᵀ tile per expand CTA
+constexpr uint32_t kSlotAuxBytes = 16384;       // x rows (shrink) / y rows (expand)
+constexpr uint32_t kMaxShrinkRows = 8;          // one warp per rank row
+constexpr uint32_t kMaxBgmvRank = 256;
 
-// Rank rows per thread group in the expand: rows are split over RG groups of
-// CT = 256/RG column-threads so a thread holds <= 4 rows of Bᵀ (ranks up to
-// 128 in one batch of loads; larger ranks loop).
+// A BGMV work unit, fully resolved on the host (48 bytes): the producer warp
+// needs no dependent loads besides the page table.
+struct BgmvUnit {
+  uint32_t kind_seg;  // segment | kExpandBit for expand units
+  uint32_t off;       // first rank row (shrink) or first output column (expand)
+  uint32_t count;     // rows (shrink) or columns (expand)
+  uint32_t table_off; // adapter's first entry in the device page table
+  uint32_t rank;
+  uint32_t voff;      // fp32 index of v for this unit's first token (row stride rpad4)
+  uint32_t ntok;      // tokens (<= kMaxUnitTok)
+  uint32_t n_shrink;  // expand: shrink units of the segment to wait for
+  uint32_t tok[kMaxUnitTok];  // x / y row indices
+};
+static_assert(sizeof(BgmvUnit) == 48, "BgmvUnit layout");
+
+// Expand split: RG row groups × CT column threads (RG·CT = kBgmvConsumers),
+// CB = CT · VEC columns, so the Bᵀ tile r × CB fits one 32 KiB slot and a
+// thread holds <= 8 rank rows.
+constexpr uint32_t kBgmvConsumers = 256;
+constexpr uint32_t kRedBytes = 16384;  // expand cross-group reduction buffer
 #ifdef __CUDACC__
 __host__ __device__
 #endif
 inline uint32_t expand_rg(uint32_t rank) {
-  return rank <= 16 ? 4u : (rank <= 32 ? 8u : (rank <= 64 ? 16u : 32u));
+  uint32_t rg = 1;
+  while (rg * 8 < rank) rg <<= 1;
+  return rg;  // <= 32 for rank <= 256
 }
 
-struct ProjUnits {
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline uint32_t rpad4(uint32_t r) { return (r + 3) & ~3u; }
+
+struct ProjWork {
   uint32_t n_units = 0;
+  uint32_t n_shrink = 0;   // units [0, n_shrink) are shrink, the rest expand
   uint32_t units_off = 0;  // into the unit array
-  uint32_t smem = 0;       // dynamic shared memory for this proj's launch
+};
+
+// ---------------------------------------------------------------- SGMV
+// A run = maximal stretch of consecutive tokens with the same adapter
+// (Punica's seg_indptr formulation); tiles are 128-row slices of runs.
+struct SgmvTile {
+  uint32_t row0;       // first x / y row of the tile
+  uint32_t nrows;      // valid rows (<= 128)
+  uint32_t table_off;
+  uint32_t rank;
 };
 
 }  // namespace plora
@@ -55,22 +81,20 @@ struct plora_plan {
   uint32_t n_seg = 0;
   uint32_t max_rank = 0;
   uint64_t v_elems = 0;
-  plora::ProjUnits proj[PLORA_MAX_PROJ];
+  plora::ProjWork proj[PLORA_MAX_PROJ];
+  uint32_t n_tiles = 0;
 
-  // host staging (pinned) and device mirror of: segs | toks | units
-  std::vector<plora::SegDesc> segs;
-  std::vector<uint32_t> toks;
-  std::vector<uint2> units;
+  std::vector<plora::BgmvUnit> units;
+  std::vector<plora::SgmvTile> tiles;
   char* h_pinned = nullptr;
   uint64_t h_cap = 0;
   char* d_buf = nullptr;
   uint64_t d_cap = 0;
-  plora::SegDesc* d_segs = nullptr;
-  uint32_t* d_toks = nullptr;
-  uint2* d_units = nullptr;
+  plora::BgmvUnit* d_units = nullptr;
+  plora::SgmvTile* d_tiles = nullptr;
   float* d_v = nullptr;
   uint64_t v_cap = 0;
-  uint32_t* d_sync = nullptr;  // [0] ticket, [1] exit count, [2..] per-segment done
+  uint32_t* d_sync = nullptr;  // [0] ticket, [1] exit count, [2..] per-segment shrink done
   uint64_t sync_cap = 0;
   cudaEvent_t upload_done = nullptr;
 

@@ -59,6 +59,20 @@ def cfg2(dtype=torch.bfloat16, n_layers: int = 32, page_bytes: int = 2048) -> De
                         page_bytes)
 
 
+def cfg3(dtype=torch.bfloat16, n_layers: int = 32, page_bytes: int = 2048,
+         n_segments: int = 32, seg_tokens: int = 512) -> DecodeConfig:
+    """Prefill SGMV: 32 segments × 512 tokens, r = [16,64,128][s % 3]
+    (BASELINE.json configs[2]); adapter s serves segment s."""
+    shape = ModelShape(n_layers, (4096, 4096), (4096, 4096), dtype)
+    return DecodeConfig("cfg3", shape, [(16, 64, 128)[s % 3] for s in range(n_segments)],
+                        seg_tokens, page_bytes)
+
+
+def segment_assignment(n_segments: int, seg_tokens: int):
+    """Prefill batch: segment s = tokens [s·L, (s+1)·L) of adapter s (contiguous runs)."""
+    return np.repeat(np.arange(n_segments, dtype=np.int32), seg_tokens)
+
+
 def token_assignment(n_adapters: int, tokens_per_adapter: int, seed: int = SEED_ASSIGN):
     """Each adapter gets tokens_per_adapter tokens, in shuffled order."""
     ta = np.repeat(np.arange(n_adapters, dtype=np.int32), tokens_per_adapter)

@@ -1,0 +1,89 @@
+"""GPU parity of the tcgen05 prefill path (SGMV) against the CPU oracle in its
+SGMV rounding mode (v = x·Aᵀ rounded to bf16 before the expand), plus
+full-size BASELINE config-3 properties."""
+import numpy as np
+import pytest
+import torch
+
+from lora_harness import TOL_BF16, Setup, rel_err, to_np_bits
+from paper_2512_20210_b200 import synth
+from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, ModelShape, bgmv, sgmv,
+                                        kernel_launch_count)
+
+pytestmark = pytest.mark.gpu
+
+
+def _sgmv_vs_oracle(s, ta, layer, proj, scale=1.0, salt=0):
+    shape = s.cfg.shape
+    T = len(ta)
+    x = synth.activations(T, shape.d_in[proj], shape.dtype, "x", salt=salt)
+    y0 = synth.activations(T, shape.d_out[proj], shape.dtype, "y", salt=salt)
+    xd, yd = x.cuda(), y0.cuda()
+    plan = BatchPlan(s.store, ta)
+    n0 = kernel_launch_count()
+    sgmv(plan, layer, proj, xd, yd, scale)
+    torch.cuda.synchronize()
+    assert kernel_launch_count() - n0 == 1
+    ref = s.oracle(layer, proj, x, y0, ta, scale=scale, v_bf16=shape.dtype == torch.bfloat16)
+    return yd, ref, y0
+
+
+def test_sgmv_mixed_ranks_partial_tiles(cuda):
+    """Runs of 1..300 tokens, ranks 3..128 (padded to 16 in smem), -1 gaps."""
+    shape = ModelShape(2, (4096, 1024), (4096, 2048), torch.bfloat16)
+    ranks = [16, 64, 128, 8, 3, 100, 32, 1]
+    cfg = synth.DecodeConfig("sgmv", shape, ranks, 1, 2048)
+    s = Setup(cfg)
+    runs = [(0, 300), (1, 130), (-1, 5), (2, 128), (3, 1), (4, 77), (5, 129), (-1, 2), (6, 64),
+            (7, 9), (2, 40)]
+    ta = np.concatenate([np.full(n, a, np.int32) for a, n in runs])
+    for layer, proj in ((0, 0), (1, 1)):
+        yd, ref, y0 = _sgmv_vs_oracle(s, ta, layer, proj, scale=0.5, salt=layer)
+        assert rel_err(yd, ref) <= TOL_BF16, (layer, proj)
+        none = ta < 0
+        assert np.array_equal(to_np_bits(yd)[none], to_np_bits(y0)[none])
+
+
+def test_sgmv_cfg3_shape_parity(cuda):
+    """BASELINE config 3 call shape at reduced token count (6 segments × 512)."""
+    cfg = synth.cfg3(n_layers=2, n_segments=6)
+    s = Setup(cfg)
+    ta = synth.segment_assignment(6, 512)
+    yd, ref, _ = _sgmv_vs_oracle(s, ta, 1, 0, salt=11)
+    assert rel_err(yd, ref) <= TOL_BF16
+
+
+def test_sgmv_full_cfg3_properties(cuda):
+    """Full BASELINE config 3 (32 × 512 tokens, r in {16,64,128}, 32 layers):
+    SGMV agrees with the BGMV path (independent arithmetic: CUDA cores, fp32
+    intermediate) within the bf16 tolerance; zero x leaves y untouched."""
+    cfg = synth.cfg3()
+    pool = synth.build_pool(cfg)
+    store = AdapterStore(pool, cfg.shape, cfg.n_adapters)
+    for a, r in enumerate(cfg.ranks):
+        store.register(a, r)
+        store.write_pages(a, synth.adapter_image(cfg.shape, r, a, device="cuda").view(torch.uint8))
+        store.publish(a)
+    ta = synth.segment_assignment(32, 512)
+    plan = BatchPlan(store, ta)
+    x = torch.randn(len(ta), 4096, device="cuda").to(torch.bfloat16)
+    y0 = torch.randn(len(ta), 4096, device="cuda").to(torch.bfloat16)
+    ys, yb = y0.clone(), y0.clone()
+    sgmv(plan, 30, 1, x, ys)
+    bgmv(plan, 30, 1, x, yb)
+    torch.cuda.synchronize()
+    err = (ys.float() - yb.float()).abs().max().item() / yb.float().abs().max().item()
+    assert err <= TOL_BF16, err
+    yz = y0.clone()
+    sgmv(plan, 3, 0, torch.zeros_like(x), yz)
+    torch.cuda.synchronize()
+    assert torch.equal(yz, y0)
+
+
+def test_sgmv_fp32_store_routes_to_exact_path(cuda):
+    shape = ModelShape(1, (256,), (512,), torch.float32)
+    cfg = synth.DecodeConfig("f32", shape, [16, 64], 40, 1024)
+    s = Setup(cfg)
+    ta = np.repeat(np.arange(2, dtype=np.int32), 40)
+    yd, ref, _ = _sgmv_vs_oracle(s, ta, 0, 0)
+    assert rel_err(yd, ref) <= 1e-5
