@@ -44,6 +44,14 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
+def load_tensor_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return "measured", json.load(f).get("bf16_tflops", 1590.0)
+    return "fallback", 1590.0
+
+
 def call_bytes(shape, ranks, proj, n_tokens):
     """Algorithmic bytes of one (layer, proj) call: each adapter's A and Bᵀ
     block once + x read + y read-modify-write."""
@@ -187,7 +195,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2512_20210_b200 import synth
-    from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, bgmv, kernel_launch_count)
+    from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, bgmv, kernel_launch_count,
+                                            sgmv)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -196,7 +205,9 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    cfg = synth.cfg2(page_bytes=args.page_bytes)
+    prefill = args.workload == "cfg3"
+    cfg = synth.cfg3(page_bytes=args.page_bytes) if prefill else synth.cfg2(page_bytes=args.page_bytes)
+    op = sgmv if prefill else bgmv
     shape = cfg.shape
     pool = synth.build_pool(cfg)
     store = AdapterStore(pool, shape, cfg.n_adapters, device=local)
@@ -206,7 +217,11 @@ def run_ours(args):
         store.write_pages(a, img.view(torch.uint8))  # D2D page scatter
         store.publish(a)
         del img
-    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter, seed=synth.SEED_ASSIGN + rank)
+    if prefill:
+        ta = synth.segment_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    else:
+        ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter,
+                                    seed=synth.SEED_ASSIGN + rank)
     T = len(ta)
     L, NP = shape.n_layers, shape.n_proj
     plan = BatchPlan(store, ta)
@@ -219,14 +234,27 @@ def run_ours(args):
         for l in range(L):
             for p in range(NP):
                 if ev is not None:
-                    ev[2 * (l * NP + p)].record(stream)
-                bgmv(plan, l, p, x[l], y[l * NP + p])
+                    ev[2 * (l * NP + p)].record()
+                op(plan, l, p, x[l], y[l * NP + p])
                 if ev is not None:
-                    ev[2 * (l * NP + p) + 1].record(stream)
+                    ev[2 * (l * NP + p) + 1].record()
 
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    # The decode step runs as one CUDA graph (as serving engines run decode):
+    # 64 calls, with an event pair around each call captured in the graph.
+    graph = None
+    gevs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(2 * L * NP)]
+    n_graph0 = kernel_launch_count()
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(gevs)
+        per_replay = kernel_launch_count() - n_graph0
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
 
@@ -238,12 +266,20 @@ def run_ours(args):
         torch.cuda.synchronize()
         start.record(stream)
         for k in range(K):
-            step(evs[k])
+            if graph is not None:
+                graph.replay()
+            else:
+                step(evs[k])
         end.record(stream)
         torch.cuda.synchronize()
-    launches = kernel_launch_count() - n0
+    if graph is not None:
+        launches = per_replay * K  # kernels inside each replayed graph
+        kern_ms = [gevs[2 * i].elapsed_time(gevs[2 * i + 1]) for i in range(L * NP)]
+    else:
+        launches = kernel_launch_count() - n0
+        kern_ms = [evs[k][2 * i].elapsed_time(evs[k][2 * i + 1])
+                   for k in range(K) for i in range(L * NP)]
     step_ms = start.elapsed_time(end) / K
-    kern_ms = [evs[k][2 * i].elapsed_time(evs[k][2 * i + 1]) for k in range(K) for i in range(L * NP)]
     mean_kern_ms = statistics.mean(kern_ms)
     if world > 1:
         t = torch.tensor([step_ms], device=dev)
@@ -253,7 +289,7 @@ def run_ours(args):
 
     # ---- e2e through the public API from pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not prefill:
         xh = x.cpu().pin_memory()
         yh = y.cpu().pin_memory()
         yout = torch.empty_like(yh).pin_memory()
@@ -266,8 +302,11 @@ def run_ours(args):
                 e0.record(stream)
             x.copy_(xh, non_blocking=True)
             y.copy_(yh, non_blocking=True)
-            plan.update(ta)
-            step()
+            plan.update(ta)  # same batch shape: the captured graph stays valid
+            if graph is not None:
+                graph.replay()
+            else:
+                step()
             yout.copy_(y, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -281,8 +320,12 @@ def run_ours(args):
                "h2d_bytes_per_step": xh.numel() * 2 + yh.numel() * 2 + plan_bytes,
                "d2h_bytes_per_step": yout.numel() * 2, "ms_per_step": e2e_ms}
 
-    # ---- roofline for the BGMV kernel (per launch, mean over the timed region)
+    # ---- roofline of the op (per (layer, proj) call, mean over the timed region)
     per_call = statistics.mean(call_bytes(shape, cfg.ranks, p, T) for p in range(NP))
+    if prefill:  # every adapter serves one 512-token segment; weights read once per tile
+        toks = cfg.tokens_per_adapter
+        flops = statistics.mean(sum(2 * toks * r * (shape.d_in[p] + shape.d_out[p])
+                                    for r in cfg.ranks) for p in range(NP))
     peak, peak_kind = load_peaks()
     achieved = per_call / (mean_kern_ms / 1e3) / 1e9
     traffic = None
@@ -292,7 +335,7 @@ def run_ours(args):
             traffic = json.load(f).get("dram_bytes_per_launch")
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not prefill:
         nthreads = os.cpu_count() or 1
         per_call_s, n = CpuOracle(nthreads).sample(args.cpu_sample_s)
         cpu = {"value": T / (per_call_s * L * NP), "unit": UNIT, "cores": nthreads, "kind": "port",
@@ -308,11 +351,17 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "cfg2 decode BGMV: 256 tokens / 128 adapters per GPU, "
-                               "r=[8,16,32,64][a%4], Llama-7B q/v (32 layers x 2 = 64 calls/step)",
+        "config": {"workload": ("cfg3 prefill SGMV (tcgen05): 32 segments x 512 tokens per GPU, "
+                                "r=[16,64,128][s%3], Llama-7B q/v (32 layers x 2 = 64 calls/step)")
+                               if prefill else
+                               ("cfg2 decode BGMV: 256 tokens / 128 adapters per GPU, "
+                                "r=[8,16,32,64][a%4], Llama-7B q/v (32 layers x 2 = 64 calls/step)"),
                    "page_bytes": args.page_bytes, "tokens_per_step_per_gpu": T,
                    "parallelism": f"request-sharded x{world} (no collective)",
-                   "l2": "inputs > L2: 3.84 GB of adapter pages + 192 MiB activations per step"},
+                   "cuda_graph": graph is not None,
+                   "l2": ("inputs > L2: 2.1 GiB of adapter pages + 12 GiB activations per step"
+                          if prefill else
+                          "inputs > L2: 3.84 GB of adapter pages + 192 MiB activations per step")},
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -323,6 +372,11 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
+    if prefill:
+        _, tpeak = load_tensor_peak()
+        tach = flops / (mean_kern_ms / 1e3) / 1e12
+        line["roofline"]["tensor"] = {"achieved": tach, "peak": tpeak, "unit": "TFLOP/s",
+                                      "frac": tach / tpeak, "flops_per_launch": flops}
     print(json.dumps(line))
 
 
@@ -336,6 +390,9 @@ def main():
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the 64 calls eagerly")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"],
+                    help="cfg2 = decode BGMV (headline), cfg3 = prefill SGMV")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -284,6 +284,12 @@ int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                plora_stream_t stream);
 
+/* ------------------------------------------------------------ diagnostics
+ * Per-unit device timestamps of the next BGMV launches (globaltimer ns):
+ * trace[(cta * 64 + k) * 4 + {0 issued, 1 data ready, 2 computed, 3 kind}]
+ * for the first 64 units of each CTA.  dev_buf = NULL disables tracing. */
+int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

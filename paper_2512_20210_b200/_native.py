@@ -143,6 +143,7 @@ _SIGS = {
     "plora_plan_num_segments": (_u32, [_vp]),
     "plora_bgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
     "plora_sgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
+    "plora_debug_set_trace": (_int, [_vp, _u64]),
 }
 
 EXPORTED = tuple(_SIGS)

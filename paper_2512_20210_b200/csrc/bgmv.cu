@@ -445,7 +445,7 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const BgmvUnit* units = plan->d_units + pw.units_off;
     if (g.esize == 2)
-      launch<__nv_bfloat16>(a, pw, units, shrink_smem, s);
+      launch_bgmv_ring(*plan, layer, proj, x, x_stride, y, y_stride, scale, s);
     else
       launch<float>(a, pw, units, shrink_smem, s);
     return 0;

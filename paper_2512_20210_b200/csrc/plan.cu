@@ -99,7 +99,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     for (uint32_t si : order) {
       const Seg& s = segs[si];
       const uint32_t rp = rpad4(s.rank), nt_all = static_cast<uint32_t>(s.toks.size());
-      const uint32_t rg = expand_rg(s.rank), cb = (kBgmvConsumers / rg) * vec;
+      const uint32_t rg = es == 2 ? 1 : expand_rg(s.rank), cb = expand_cols(s.rank, es);
       const uint32_t per_tok = rp * 4 + cb * es;
       // tokens per unit: aux area (v + y rows) and, when rows are split over
       // groups, the reduction buffer (RG · CB fp32 per token)

@@ -17,7 +17,7 @@ namespace plora {
 constexpr uint32_t kExpandBit = 0x80000000u;
 constexpr uint32_t kStopUnit = 0xffffffffu;
 constexpr uint32_t kMaxUnitTok = 4;           // tokens per work unit
-constexpr uint32_t kShrinkWeightBytes = 65536;  // A rows per shrink CTA
+constexpr uint32_t kShrinkWeightBytes = 32768;  // A rows per shrink unit
 constexpr uint32_t kSlotWeightBytes = 32768;    // Bᵀ tile per expand CTA
 constexpr uint32_t kSlotAuxBytes = 16384;       // x rows (shrink) / y rows (expand)
 constexpr uint32_t kMaxShrinkRows = 8;          // one warp per rank row
@@ -56,6 +56,22 @@ inline uint32_t expand_rg(uint32_t rank) {
 __host__ __device__
 #endif
 inline uint32_t rpad4(uint32_t r) { return (r + 3) & ~3u; }
+
+// Columns per expand unit.  bf16 (tensor-core path): the Bᵀ tile r16 × CB
+// (rank padded to the MMA K of 16) fits 32 KiB; fp32 (CUDA-core path): RG·CB
+// = 256 threads × 4 columns.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline uint32_t expand_cols(uint32_t rank, uint32_t esize) {
+  if (esize == 2) {
+    const uint32_t r16 = (rank + 15) & ~15u;
+    uint32_t cb = 1024;
+    while (cb * r16 > 16384) cb >>= 1;
+    return cb;  // 1024 (r <= 16) ... 64 (r <= 256)
+  }
+  return (kBgmvConsumers / expand_rg(rank)) * 4;
+}
 
 struct ProjWork {
   uint32_t n_units = 0;
@@ -100,3 +116,10 @@ struct plora_plan {
 
   void build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream);
 };
+
+namespace plora {
+// bf16 decode op (bgmv_ring.cu): persistent TMA ring + warp-level tensor cores.
+void launch_bgmv_ring(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
+                      uint64_t x_stride, void* y, uint64_t y_stride, float scale,
+                      cudaStream_t stream);
+}  // namespace plora

@@ -168,6 +168,8 @@ int plora_store_create(plora_pool* pool, int device, const plora_model* model,
     if (arena_bytes) PLORA_CUDA(cudaMalloc(&s->arena, arena_bytes));
     PLORA_CUDA(cudaMalloc(&s->d_dir, sizeof(DevAdapter) * max_adapters));
     PLORA_CUDA(cudaMemset(s->d_dir, 0, sizeof(DevAdapter) * max_adapters));
+    PLORA_CUDA(cudaMalloc(&s->d_zeros, 4096));
+    PLORA_CUDA(cudaMemset(s->d_zeros, 0, 4096));
     PLORA_CUDA(cudaDeviceSynchronize());
     *out = s.release();
     return 0;
@@ -182,6 +184,7 @@ void plora_store_destroy(plora_store* s) {
   cudaFree(s->d_dir);
   cudaFree(s->d_table);
   cudaFree(s->d_scratch);
+  cudaFree(s->d_zeros);
   delete s;
 }
 

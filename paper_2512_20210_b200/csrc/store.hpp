@@ -90,6 +90,7 @@ struct plora_store {
   std::vector<plora::AdapterSlot> slots;
   std::vector<plora::DevAdapter> h_dir;
   uint32_t* d_scratch = nullptr;  // relocation list staging
+  char* d_zeros = nullptr;        // 4 KiB of zeros (rank-padding rows of MMA tiles)
   uint64_t scratch_cap = 0;
 
   void ensure_table_capacity(uint64_t need, cudaStream_t stream);

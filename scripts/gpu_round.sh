@@ -28,9 +28,19 @@ if has launches; then
   echo "launches rc=$?" >> gpurun_out/launches.log
 fi
 if has full; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:bgmv_paged -s 200 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:bgmv_ -s 400 -c 4 \
     -o gpurun_out/bgmv_full -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/ncu_full.log 2>&1
   echo "full rc=$?" >> gpurun_out/ncu_full.log
+fi
+if has cfg3; then
+  timeout 600 python bench.py --workload cfg3 --steps 5 --warmup 3 > gpurun_out/bench_cfg3.json 2> gpurun_out/bench_cfg3.err
+  echo "cfg3 rc=$?" >> gpurun_out/bench_cfg3.err
+fi
+if has fullsgmv; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgmv_tc -s 70 -c 1 \
+    -o gpurun_out/sgmv_full -f python bench.py --workload cfg3 --steps 1 --warmup 3 --no-e2e --no-cpu \
+    > gpurun_out/ncu_sgmv.log 2>&1
+  echo "fullsgmv rc=$?" >> gpurun_out/ncu_sgmv.log
 fi
 ls -la gpurun_out

@@ -257,4 +257,19 @@ def test_linearity_property_full_cfg2(cuda):
     torch.cuda.synchronize()
     d = (y2.float() - 2 * y1.float()).abs().max().item()
     assert d <= 2e-2 * y2.float().abs().max().item()
-    assert kernel_launch_count() - n0 == 3
+    assert kernel_launch_count() - n0 == 3  # one persistent launch per call
+
+
+def test_ring_stress_random_ranks(cuda):
+    """Many units per CTA (every ring slot, wrap-around phases), ranks 1..256,
+    1..5 tokens per adapter, two projection shapes."""
+    rng = np.random.default_rng(11)
+    shape = ModelShape(1, (4096, 2048), (1024, 4096), torch.bfloat16)
+    ranks = [int(r) for r in rng.integers(1, 257, size=300)]
+    cfg = synth.DecodeConfig("stress", shape, ranks, 1, 2048)
+    s = Setup(cfg)
+    ta = np.concatenate([np.full(int(rng.integers(1, 6)), a, np.int32) for a in range(300)])
+    rng.shuffle(ta)
+    for proj in (0, 1):
+        yd, ref = _run(s, 0, proj, ta, scale=0.5, salt=proj)
+        assert rel_err(yd, ref) <= TOL_BF16, proj
