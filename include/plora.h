@@ -284,9 +284,72 @@ int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                plora_stream_t stream);
 
+/* ----------------------------------------------- demand predictor (host) ---
+ * The LSTM that drives predictor-based prefetch: PredictorModel
+ * (include/lorasim/lstm.hpp:11-85) and OnlinePredictor
+ * (include/lorasim/predictor.hpp:12-111).  Same parameter layout, seeded
+ * initialisation, BPTT, Adam and LSW1 file format; windows are row-major
+ * [n, window] doubles. */
+typedef struct {
+  uint32_t window, hidden, layers, embedding_dim, num_adapters;
+  double learning_rate, adam_beta1, adam_beta2, adam_eps;
+} plora_lstm_config; /* PredictorConfig, lstm.hpp:19-33 */
+typedef struct {
+  plora_lstm_config model;
+  double interval_ms;
+  uint32_t train_every, batch_size, replay_capacity;
+} plora_predictor_config; /* OnlinePredictorConfig, predictor.hpp:45-51 */
+void plora_lstm_config_default(plora_lstm_config* c);
+void plora_predictor_config_default(plora_predictor_config* c);
+/* Summed clamped binary cross-entropy (lstm.hpp:35-37). */
+int plora_cross_entropy(const double* p, const double* y, uint64_t n, double* out);
+
+typedef struct plora_lstm plora_lstm;
+int plora_lstm_create(const plora_lstm_config* cfg, uint64_t seed, plora_lstm** out);
+void plora_lstm_destroy(plora_lstm* m); /* no-op for predictor-owned models */
+uint64_t plora_lstm_param_count(const plora_lstm* m);
+double* plora_lstm_parameters(plora_lstm* m); /* mutable view of θ */
+void plora_lstm_get_config(const plora_lstm* m, plora_lstm_config* out);
+int plora_lstm_forward(const plora_lstm* m, const uint32_t* adapters, const double* windows,
+                       uint64_t n, double* probs);
+int plora_lstm_loss(const plora_lstm* m, const uint32_t* adapters, const double* windows,
+                    const double* labels, uint64_t n, double* out);
+int plora_lstm_gradient(const plora_lstm* m, const uint32_t* adapters, const double* windows,
+                        const double* labels, uint64_t n, double* grad);
+int plora_lstm_train_step(plora_lstm* m, const uint32_t* adapters, const double* windows,
+                          const double* labels, uint64_t n, double* loss);
+int plora_lstm_save(const plora_lstm* m, const char* path);
+int plora_lstm_load(const char* path, plora_lstm** out);
+
+typedef struct plora_predictor plora_predictor;
+int plora_predictor_create(const plora_predictor_config* cfg, uint64_t seed,
+                           plora_predictor** out);
+void plora_predictor_destroy(plora_predictor* p);
+plora_lstm* plora_predictor_model(plora_predictor* p); /* borrowed */
+int plora_predictor_observe(plora_predictor* p, uint32_t adapter, double t_ms);
+int plora_predictor_roll_to(plora_predictor* p, double t_ms);
+/* 1 = trained one batch (loss written), 0 = replay buffer empty. */
+int plora_predictor_train_step(plora_predictor* p, double* loss);
+/* Predictions for every known adapter in key order; returns the count (may
+ * exceed cap; only cap entries written) or a negative status. */
+int64_t plora_predictor_predict_all(plora_predictor* p, double now_ms, uint32_t* adapters,
+                                    double* probs, uint64_t cap);
+int plora_predictor_window(const plora_predictor* p, uint32_t adapter, double* out);
+/* 1 if the adapter has been observed (OnlinePredictor::known, predictor.hpp:77). */
+int plora_predictor_known(const plora_predictor* p, uint32_t adapter);
+typedef struct {
+  uint64_t observed, train_steps, known, buffered;
+  int64_t current_interval;
+  double last_loss;
+} plora_predictor_stats_t;
+void plora_predictor_stats(const plora_predictor* p, plora_predictor_stats_t* out);
+/* Replay buffer entry i (0 = oldest): ReplayBuffer::at (predictor.hpp:31). */
+int plora_predictor_buffer_at(const plora_predictor* p, uint64_t i, uint32_t* adapter,
+                              double* window, double* label);
+
 /* ------------------------------------------------------------ diagnostics
  * Per-unit device timestamps of the next BGMV launches (globaltimer ns):
- * trace[(cta * 64 + k) * 4 + {0 issued, 1 data ready, 2 computed, 3 kind}]
+ * trace[(cta * 64 + k) * 8 + {0 issued, 1 data ready, 2 computed, 3 kind, ...}]
  * for the first 64 units of each CTA.  dev_buf = NULL disables tracing. */
 int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
 

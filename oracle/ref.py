@@ -28,6 +28,8 @@ def lib() -> C.CDLL:
         P = C.POINTER
         sig = {
             "ref_last_error": (C.c_char_p, []),
+            "ref_lstm_forward_probability": (dbl, [u32, u32, u32, u32, u32, P(dbl), u32,
+                                                   P(dbl)]),
             "ref_pool_create": (C.c_int, [u64, u32, P(vp)]),
             "ref_pool_destroy": (None, [vp]),
             "ref_pool_pages_needed": (u32, [vp, u64]),
@@ -276,3 +278,14 @@ def generate_synthetic(profile, duration_s, seed):
     o = (C.c_uint32 * max(n, 1))()
     lib().ref_generate_synthetic(*args, arr, ad, i, o, n)
     return list(arr[:n]), list(ad[:n]), list(i[:n]), list(o[:n])
+
+
+def lstm_forward_probability(cfg, theta, adapter, window) -> float:
+    """tests/support/lstm_reference.hpp forward_probability (the reference's scalar oracle)."""
+    import numpy as np
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    w = np.ascontiguousarray(window, dtype=np.float64)
+    P = C.POINTER(C.c_double)
+    return lib().ref_lstm_forward_probability(cfg.window, cfg.hidden, cfg.layers,
+                                              cfg.embedding_dim, cfg.num_adapters,
+                                              th.ctypes.data_as(P), adapter, w.ctypes.data_as(P))

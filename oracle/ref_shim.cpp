@@ -10,6 +10,8 @@
 //   prefetch policy     include/lorasim/prefetch.hpp:11-72, src/prefetch.cpp:1-114
 //   adapter model       include/lorasim/adapter.hpp:15-76, src/adapter.cpp:12-144
 //   generate_synthetic  include/lorasim/workload.hpp:36-63, src/workload.cpp:59-144
+//   LSTM scalar oracle  tests/support/lstm_reference.hpp (the reference's own
+//                       Eigen-free test oracle for PredictorModel::forward)
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -20,6 +22,7 @@
 #include "lorasim/memory.hpp"
 #include "lorasim/prefetch.hpp"
 #include "lorasim/workload.hpp"
+#include "support/lstm_reference.hpp"
 
 using namespace lorasim;
 
@@ -265,6 +268,15 @@ int64_t ref_generate_synthetic(uint32_t num_adapters, double base_rate, double d
     out_tok[i] = reqs[i].output_tokens;
   }
   return static_cast<int64_t>(reqs.size());
+}
+
+// lstm_reference::forward_probability (tests/support/lstm_reference.hpp)
+double ref_lstm_forward_probability(uint32_t window, uint32_t hidden, uint32_t layers,
+                                    uint32_t embedding_dim, uint32_t num_adapters,
+                                    const double* theta, uint32_t adapter, const double* w) {
+  lstm_reference::Shape s{window, hidden, layers, embedding_dim, num_adapters};
+  return lstm_reference::forward_probability(s, theta, adapter,
+                                             std::vector<double>(w, w + window));
 }
 
 }  // extern "C"

@@ -71,6 +71,25 @@ class plora_model(C.Structure):
                 ("dtype", C.c_uint32)]
 
 
+class plora_lstm_config(C.Structure):
+    _fields_ = [("window", C.c_uint32), ("hidden", C.c_uint32), ("layers", C.c_uint32),
+                ("embedding_dim", C.c_uint32), ("num_adapters", C.c_uint32),
+                ("learning_rate", C.c_double), ("adam_beta1", C.c_double),
+                ("adam_beta2", C.c_double), ("adam_eps", C.c_double)]
+
+
+class plora_predictor_config(C.Structure):
+    _fields_ = [("model", plora_lstm_config), ("interval_ms", C.c_double),
+                ("train_every", C.c_uint32), ("batch_size", C.c_uint32),
+                ("replay_capacity", C.c_uint32)]
+
+
+class plora_predictor_stats_t(C.Structure):
+    _fields_ = [("observed", C.c_uint64), ("train_steps", C.c_uint64), ("known", C.c_uint64),
+                ("buffered", C.c_uint64), ("current_interval", C.c_int64),
+                ("last_loss", C.c_double)]
+
+
 _u32, _u64, _i32, _i64, _int, _dbl, _vp = (C.c_uint32, C.c_uint64, C.c_int32, C.c_int64,
                                            C.c_int, C.c_double, C.c_void_p)
 _P = C.POINTER
@@ -143,6 +162,31 @@ _SIGS = {
     "plora_plan_num_segments": (_u32, [_vp]),
     "plora_bgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
     "plora_sgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
+    "plora_lstm_config_default": (None, [_P(plora_lstm_config)]),
+    "plora_predictor_config_default": (None, [_P(plora_predictor_config)]),
+    "plora_cross_entropy": (_int, [_P(_dbl), _P(_dbl), _u64, _P(_dbl)]),
+    "plora_lstm_create": (_int, [_P(plora_lstm_config), _u64, _P(_vp)]),
+    "plora_lstm_destroy": (None, [_vp]),
+    "plora_lstm_param_count": (_u64, [_vp]),
+    "plora_lstm_parameters": (_P(_dbl), [_vp]),
+    "plora_lstm_get_config": (None, [_vp, _P(plora_lstm_config)]),
+    "plora_lstm_forward": (_int, [_vp, _P(_u32), _P(_dbl), _u64, _P(_dbl)]),
+    "plora_lstm_loss": (_int, [_vp, _P(_u32), _P(_dbl), _P(_dbl), _u64, _P(_dbl)]),
+    "plora_lstm_gradient": (_int, [_vp, _P(_u32), _P(_dbl), _P(_dbl), _u64, _P(_dbl)]),
+    "plora_lstm_train_step": (_int, [_vp, _P(_u32), _P(_dbl), _P(_dbl), _u64, _P(_dbl)]),
+    "plora_lstm_save": (_int, [_vp, C.c_char_p]),
+    "plora_lstm_load": (_int, [C.c_char_p, _P(_vp)]),
+    "plora_predictor_create": (_int, [_P(plora_predictor_config), _u64, _P(_vp)]),
+    "plora_predictor_destroy": (None, [_vp]),
+    "plora_predictor_model": (_vp, [_vp]),
+    "plora_predictor_observe": (_int, [_vp, _u32, _dbl]),
+    "plora_predictor_roll_to": (_int, [_vp, _dbl]),
+    "plora_predictor_train_step": (_int, [_vp, _P(_dbl)]),
+    "plora_predictor_predict_all": (_i64, [_vp, _dbl, _P(_u32), _P(_dbl), _u64]),
+    "plora_predictor_window": (_int, [_vp, _u32, _P(_dbl)]),
+    "plora_predictor_known": (_int, [_vp, _u32]),
+    "plora_predictor_stats": (None, [_vp, _P(plora_predictor_stats_t)]),
+    "plora_predictor_buffer_at": (_int, [_vp, _u64, _P(_u32), _P(_dbl), _P(_dbl)]),
     "plora_debug_set_trace": (_int, [_vp, _u64]),
 }
 
