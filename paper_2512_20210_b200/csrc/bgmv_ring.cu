@@ -4,29 +4,31 @@
 // y[t, :] += scale · (x[t, :] · A_{a(t)}ᵀ) · B_{a(t)}ᵀ,
 // weights read through the device page table (src/memory.cpp:55-62).
 //
-//  * One CTA per SM, 8 consumer warps + 1 producer warp, 4 × 48 KiB slots.
-//    Measured on this B200 (profiles/r01_microbench_loads.txt): 1-D TMA bulk
-//    copies sustain ~7 TB/s once >= ~128 KiB per SM are in flight, while
-//    LDG/LDGSTS streams top out near 2.8 TB/s; the ring keeps three units
-//    (~144 KiB) in flight while the fourth is consumed.
-//  * Static schedule: CTA c owns units c, c + G, c + 2G, ... of the plan's
-//    LPT-ordered list (every shrink unit before every expand unit), so the
-//    producer needs no atomics and prefetches each unit's descriptor one
-//    unit ahead and resolves its page-table entries before waiting for a
-//    free slot.  A CTA only ever waits (on a segment's shrink counter) after
-//    its own shrink units are published, and the grid never exceeds the
-//    co-resident capacity, so the schedule cannot deadlock.
-//  * Producer: per unit, one cp.async.bulk per page piece (weights,
-//    L2 evict-first), one per x / y row, and zero rows for rank padding, all
-//    completing on the slot's mbarrier.
+//  * One CTA per SM: 4 producer warps (one per ring slot) + 2 consumer
+//    groups of 4 warps (even / odd slots), 4 × 48 KiB slots.  Measured on
+//    this B200 (profiles/r01_microbench_loads.txt): 1-D TMA bulk copies
+//    sustain ~7 TB/s once >= ~128 KiB per SM are in flight (LDG/LDGSTS
+//    streams top out near 2.8 TB/s).  A per-unit device trace
+//    (scripts/trace_bgmv.py) showed each unit's issue costs ~2 µs of
+//    dependent latency (descriptor, page-table lookups): four producer warps
+//    run four such chains in parallel and two consumer groups compute two
+//    units at once.
+//  * Static schedule: CTA c owns local units k = 0, 1, ... = global units
+//    c + k·G of the plan's LPT-ordered list (every shrink unit before every
+//    expand unit); unit k goes to slot k % 4 (producer warp k % 4) and to
+//    consumer group k % 2.  No atomics; a blocked expand only ever has
+//    expands behind it, and every shrink counter is published before its
+//    group waits again, so the schedule cannot deadlock.
+//  * Producer: per unit, one cp.async.bulk per page piece (weights, L2
+//    evict-first), one per x / y row, zero rows for rank padding; for an
+//    expand, after those are in flight, it acquires the segment's shrink
+//    counter and copies v through the async proxy.
 //  * Shrink unit (<= 8 rank rows, <= 2 tokens): mma.sync m16n8k16,
-//    D[tok][row] = x · Wᵀ (tokens padded to M = 16), K split over 8 warps,
-//    reduced in smem; v = x·Aᵀ is written in fp32 and the segment's done
-//    counter is bumped one iteration later (fence off the critical path).
-//  * Expand unit (<= 4 tokens, CB columns): thread 0 acquires the segment
-//    counter, v is read from L2, D[tok][col] = v · Bᵀ with v as bf16 hi + lo
-//    (two MMAs, ~16 mantissa bits), y updated in the slot and written back
-//    with one bulk store per token row.
+//    D[tok][row] = x · Wᵀ (tokens padded to M = 16), K split over 4 warps
+//    with 4 independent accumulators each, reduced in smem; v = x·Aᵀ (fp32).
+//  * Expand unit (<= 4 tokens, CB columns): D[tok][col] = v · Bᵀ with v as
+//    bf16 hi + lo (two MMAs, ~16 mantissa bits), A fragments built once per
+//    k-step for 8 column tiles at a time; y += scale·D stored directly.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -38,13 +40,26 @@ namespace plora {
 namespace {
 
 constexpr int kSlots = 4;
-constexpr uint32_t kSlotBytes = 49408;  // shrink 4·(8192+16) + 2·(8192+16); expand <= ~45 KiB
-constexpr int kConsumers = 256;
-constexpr int kThreads = kConsumers + 32;
+constexpr uint32_t kSlotBytes = kRingSlotBytes;  // see plan.hpp
+constexpr int kGroupWarps = 4;          // consumer warps per group
+constexpr int kGroups = 2;
+constexpr int kGroupThreads = kGroupWarps * 32;
+constexpr int kConsumers = kGroups * kGroupThreads;
+constexpr int kProducers = kSlots;      // one producer warp per slot
+constexpr int kThreads = kConsumers + kProducers * 32;
 constexpr uint32_t kRowPad = 16;        // conflict-free ldmatrix rows
 constexpr int kPre = 8;                 // page pieces per producer lane resolved ahead
+constexpr int kTiles = 8;               // expand column tiles per accumulator pass
 constexpr uint32_t kStop = 0xffffffffu;
 constexpr uint32_t kTraceUnits = 64;
+
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ uint64_t now_ns() {
   uint64_t t;
@@ -55,7 +70,7 @@ __device__ __forceinline__ uint64_t now_ns() {
 __device__ __forceinline__ void trace_put(const uint64_t* base, uint32_t k, int field,
                                           uint64_t value) {
   if (base && k < kTraceUnits)
-    const_cast<uint64_t*>(base)[(blockIdx.x * kTraceUnits + k) * 4 + field] = value;
+    const_cast<uint64_t*>(base)[(blockIdx.x * kTraceUnits + k) * 8 + field] = value;
 }
 
 struct RingArgs {
@@ -81,9 +96,9 @@ struct RingArgs {
 
 struct Smem {
   static constexpr uint32_t slots = 0;
-  static constexpr uint32_t vs = kSlots * kSlotBytes;                     // float[4][256]
-  static constexpr uint32_t red = vs + kMaxUnitTok * kMaxBgmvRank * 4;     // float[8][8][8]
-  static constexpr uint32_t hdr = red + 8 * 8 * 8 * 4;
+  static constexpr uint32_t vs = kSlots * kSlotBytes;                            // [2][4][256] f32
+  static constexpr uint32_t red = vs + kGroups * kMaxUnitTok * kMaxBgmvRank * 4; // [2][4][16][8]
+  static constexpr uint32_t hdr = red + kGroups * kGroupWarps * 16 * 8 * 4;
   static constexpr uint32_t bars = hdr + kSlots * sizeof(BgmvUnit);
   static constexpr uint32_t total = bars + 2 * kSlots * 8;
 };
@@ -91,7 +106,7 @@ struct Smem {
 struct Geom {  // per-unit copy geometry (identical in producer and consumers)
   uint32_t stride;    // smem row stride of the weight tile
   uint32_t aux;       // smem offset of x rows (shrink) / y rows (expand)
-  uint32_t segbytes;  // expand: bytes per row segment
+  uint32_t segbytes;  // bytes per copied row segment
   uint32_t r16;       // expand: rank padded to 16
   uint32_t cb;        // expand: columns per unit
 };
@@ -99,10 +114,10 @@ struct Geom {  // per-unit copy geometry (identical in producer and consumers)
 __device__ __forceinline__ Geom geom(const RingArgs& p, const BgmvUnit& u) {
   Geom g;
   if (!(u.kind_seg & kExpandBit)) {
-    const uint32_t rowbytes = p.d_in * 2;
-    g.stride = rowbytes + kRowPad;
-    g.aux = min(kMaxShrinkRows, kShrinkWeightBytes / rowbytes) * g.stride;
-    g.segbytes = rowbytes;
+    // 16 rank rows × one kShrinkK-wide K chunk (the last chunk may be narrower)
+    g.stride = kShrinkK * 2 + kRowPad;
+    g.aux = kShrinkRows16 * g.stride;
+    g.segbytes = min(kShrinkK, p.d_in - u.kc * kShrinkK) * 2;
     g.r16 = 0;
     g.cb = 0;
   } else {
@@ -115,8 +130,7 @@ __device__ __forceinline__ Geom geom(const RingArgs& p, const BgmvUnit& u) {
   return g;
 }
 
-// Piece q of a unit's weight copies: shrink = (row i, page k) of its count
-// rows; expand = (row j, page k) of the rank rows' column segments.
+// Piece q of a unit's weight copies: (row, page k) of the unit's rows.
 __device__ __forceinline__ bool piece(const RingArgs& p, const BgmvUnit& u, const Geom& g,
                                       uint32_t q, uint32_t ppr, uint64_t& src, uint32_t& dst,
                                       uint32_t& len, uint32_t& page) {
@@ -126,7 +140,7 @@ __device__ __forceinline__ bool piece(const RingArgs& p, const BgmvUnit& u, cons
   if (!(u.kind_seg & kExpandBit)) {
     if (row >= u.count) return false;
     lo = (static_cast<uint64_t>(u.rank) * p.blk_mult +
-          static_cast<uint64_t>(u.off + row) * p.d_in) * 2;
+          static_cast<uint64_t>(u.off + row) * p.d_in + u.kc * kShrinkK) * 2;
   } else {
     if (row >= u.rank) return false;
     lo = (static_cast<uint64_t>(u.rank) * p.blk_mult + static_cast<uint64_t>(u.rank) * p.d_in +
@@ -143,21 +157,24 @@ __device__ __forceinline__ bool piece(const RingArgs& p, const BgmvUnit& u, cons
   return true;
 }
 
-__device__ void producer(const RingArgs& p, char* smem) {
+// Producer warp w fills slot w with local units w, w + 4, w + 8, ...
+__device__ void producer(const RingArgs& p, char* smem, uint32_t w) {
   const uint32_t lane = threadIdx.x & 31;
   BgmvUnit* hdr = reinterpret_cast<BgmvUnit*>(smem + Smem::hdr);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Smem::bars);
   uint64_t* empty = full + kSlots;
   const uint64_t evict_first = ptx::policy_evict_first();
-  const uint32_t G = gridDim.x;
-  uint32_t u = blockIdx.x;
+  const uint32_t G = gridDim.x, step = G * kSlots;
+  char* sb = smem + Smem::slots + w * kSlotBytes;
+  uint32_t u = blockIdx.x + w * G;
   BgmvUnit rec{};
   if (u < p.n_units) rec = p.units[u];
-  for (uint32_t k = 0;; ++k, u += G) {
-    const uint32_t slot = k % kSlots, phase = (k / kSlots) & 1u;
+  for (uint32_t k = w, it = 0;; k += kSlots, ++it, u += step) {
+    const uint32_t phase = it & 1u;
     const bool live = u < p.n_units;
+    if (lane == 0) trace_put(p.trace, k, 4, now_ns());
     BgmvUnit next{};
-    if (u + G < p.n_units) next = p.units[u + G];  // descriptor prefetch, used next iteration
+    if (u + step < p.n_units) next = p.units[u + step];  // descriptor prefetch
     Geom g{};
     uint32_t ppr = 0, n = 0;
     uint64_t src[kPre];
@@ -179,27 +196,28 @@ __device__ void producer(const RingArgs& p, char* smem) {
         }
       }
     }
-    ptx::mbar_wait(&empty[slot], phase ^ 1u);
+    if (lane == 0) trace_put(p.trace, k, 5, now_ns());
+    ptx::mbar_wait(&empty[w], phase ^ 1u);
+    if (lane == 0) trace_put(p.trace, k, 6, now_ns());
     if (!live) {
       if (lane == 0) {
-        hdr[slot].kind_seg = kStop;
-        ptx::mbar_arrive(&full[slot]);
+        hdr[w].kind_seg = kStop;
+        ptx::mbar_arrive(&full[w]);
       }
       break;
     }
-    char* sb = smem + Smem::slots + slot * kSlotBytes;
     const bool expand = rec.kind_seg & kExpandBit;
-    const uint32_t vbytes = rec.ntok * rpad4(rec.rank) * 4;
+    const uint32_t vbytes = rec.ntok * rpad4(rec.rank) * 4;  // one K-partial plane
     uint32_t tx = (expand ? rec.rank : rec.count) * g.segbytes + rec.ntok * g.segbytes;
-    if (expand) tx += (g.r16 - rec.rank) * g.segbytes + vbytes;
+    if (expand) tx += (g.r16 - rec.rank) * g.segbytes + rec.nkc * vbytes;
     if (lane == 0) {
-      hdr[slot] = rec;
-      ptx::mbar_arrive_expect_tx(&full[slot], tx);
+      hdr[w] = rec;
+      ptx::mbar_arrive_expect_tx(&full[w], tx);
     }
     __syncwarp();
 #pragma unroll
     for (int m = 0; m < kPre; ++m)
-      if (len[m]) ptx::bulk_g2s_hint(sb + dst[m], p.arena + src[m], len[m], &full[slot], evict_first);
+      if (len[m]) ptx::bulk_g2s_hint(sb + dst[m], p.arena + src[m], len[m], &full[w], evict_first);
     for (uint32_t q = lane + 32u * kPre; q < n; q += 32) {  // very small pages only
       uint64_t s;
       uint32_t d, l, page;
@@ -208,27 +226,35 @@ __device__ void producer(const RingArgs& p, char* smem) {
                            p.arena + s +
                                (static_cast<uint64_t>(__ldg(p.table + rec.table_off + page))
                                 << p.log2_page),
-                           l, &full[slot], evict_first);
+                           l, &full[w], evict_first);
     }
+    // Everything below reads data written by earlier kernels in the stream
+    // (activations, v, counters): with programmatic dependent launch the
+    // weight copies above may run ahead of the previous call's grid.
+    if (it == 0) pdl_wait();
     if (!expand) {
       if (lane < rec.ntok)
-        ptx::bulk_g2s(sb + g.aux + lane * g.stride, p.x + rec.tok[lane] * p.x_stride_b,
-                      g.segbytes, &full[slot]);
+        ptx::bulk_g2s(sb + g.aux + lane * g.stride,
+                      p.x + rec.tok[lane] * p.x_stride_b + rec.kc * kShrinkK * 2, g.segbytes,
+                      &full[w]);
     } else {
       if (lane < rec.ntok)
         ptx::bulk_g2s(sb + g.aux + lane * g.cb * 2,
                       p.y + rec.tok[lane] * p.y_stride_b + static_cast<uint64_t>(rec.off) * 2,
-                      g.segbytes, &full[slot]);
+                      g.segbytes, &full[w]);
       for (uint32_t j = rec.rank + lane; j < g.r16; j += 32)  // zero rank-padding rows
-        ptx::bulk_g2s(sb + j * g.stride, p.zeros, g.segbytes, &full[slot]);
+        ptx::bulk_g2s(sb + j * g.stride, p.zeros, g.segbytes, &full[w]);
       // v = x·Aᵀ of this segment: acquire its shrink counter (the Bᵀ / y copies
       // above are already in flight), then copy v through the async proxy.
       if (lane == 0) {
         const uint32_t* flag = p.sync + 2 + (rec.kind_seg & ~kExpandBit);
         while (ptx::ld_acquire_gpu(flag) < rec.n_shrink) __nanosleep(32);
         ptx::fence_proxy_async_global();
-        ptx::bulk_g2s(sb + g.aux + rec.ntok * g.cb * 2, p.v + rec.voff, vbytes, &full[slot]);
       }
+      __syncwarp();
+      if (lane < rec.nkc)  // one copy per K-partial plane
+        ptx::bulk_g2s(sb + g.aux + rec.ntok * g.cb * 2 + lane * vbytes,
+                      p.v + rec.voff + lane * rec.vstride, vbytes, &full[w]);
     }
     if (lane == 0) {
       trace_put(p.trace, k, 0, now_ns());
@@ -243,55 +269,80 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// gw = warp index within the consumer group, gt = thread index within it.
+// D[row][tok] = W · xᵀ over one K chunk: A = 16 rank rows (ldmatrix), B = the
+// unit's tokens straight from smem into registers (N = 8, lanes of absent
+// tokens hold zeros), K split over the group's 4 warps, 4 accumulators each.
 __device__ __forceinline__ void shrink(const RingArgs& p, const BgmvUnit& u, const Geom& g,
-                                       char* sb, float (*red)[8][8]) {
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t m = lane >> 3, r8 = lane & 7;
-  const uint32_t tok_row = min(r8 + (m & 1) * 8, u.ntok - 1);  // padded tokens repeat the last
-  const uint32_t a_base = ptx::smem_u32(sb + g.aux + tok_row * g.stride + (m >> 1) * 16);
-  // rows >= count repeat row 0 (their D columns are discarded; rows past the
-  // unit would run off the slot)
-  const uint32_t b_base = ptx::smem_u32(sb + (r8 < u.count ? r8 : 0) * g.stride + (m & 1) * 16);
-  float d[4] = {0.f, 0.f, 0.f, 0.f};
-  const uint32_t ksteps = p.d_in / 16;
-  for (uint32_t ks = warp; ks < ksteps; ks += kConsumers / 32) {
+                                       char* sb, float (*red)[16][8], uint32_t gw, uint32_t gt,
+                                       uint32_t bar_id) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t ri = (lane & 7) + ((lane >> 3) & 1) * 8;  // rows >= count: stale, discarded
+  const uint32_t a_base = ptx::smem_u32(sb + ri * g.stride + (lane >> 4) * 16);
+  const uint32_t gq = lane >> 2, c = lane & 3;
+  const bool has_tok = gq < u.ntok;
+  const char* xrow = sb + g.aux + (has_tok ? gq : 0) * g.stride + c * 4;
+  float d[4][4] = {};
+  const uint32_t ksteps = g.segbytes / 32;
+  uint32_t ks = gw;
+  for (; ks + 3 * kGroupWarps < ksteps; ks += 4 * kGroupWarps) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t k = ks + j * kGroupWarps;
+      uint32_t a[4], b[2];
+      ptx::ldsm_x4(a_base + k * 32, a);
+      b[0] = has_tok ? *reinterpret_cast<const uint32_t*>(xrow + k * 32) : 0u;
+      b[1] = has_tok ? *reinterpret_cast<const uint32_t*>(xrow + k * 32 + 16) : 0u;
+      ptx::mma_bf16_16816(d[j], a, b);
+    }
+  }
+  for (; ks < ksteps; ks += kGroupWarps) {
     uint32_t a[4], b[2];
     ptx::ldsm_x4(a_base + ks * 32, a);
-    ptx::ldsm_x2(b_base + ks * 32, b);
-    ptx::mma_bf16_16816(d, a, b);
+    b[0] = has_tok ? *reinterpret_cast<const uint32_t*>(xrow + ks * 32) : 0u;
+    b[1] = has_tok ? *reinterpret_cast<const uint32_t*>(xrow + ks * 32 + 16) : 0u;
+    ptx::mma_bf16_16816(d[0], a, b);
   }
-  const uint32_t gq = lane >> 2, c = lane & 3;  // d0/d1 = (token gq, rows 2c, 2c+1)
-  red[warp][gq][2 * c] = d[0];
-  red[warp][gq][2 * c + 1] = d[1];
-  ptx::named_bar_sync(1, kConsumers);
-  if (threadIdx.x < u.ntok * u.count) {
-    const uint32_t t = threadIdx.x / u.count, i = threadIdx.x - t * u.count;
+  // d0/d1 = (row gq, tokens 2c, 2c+1), d2/d3 = (row gq + 8, tokens 2c, 2c+1)
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    red[gw][gq + (e >> 1) * 8][2 * c + (e & 1)] = d[0][e] + d[1][e] + d[2][e] + d[3][e];
+  ptx::named_bar_sync(bar_id, kGroupThreads);
+  if (gt < u.ntok * u.count) {
+    const uint32_t i = gt / u.ntok, t = gt - i * u.ntok;
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < kConsumers / 32; ++w) s += red[w][t][i];
+    for (int w2 = 0; w2 < kGroupWarps; ++w2) s += red[w2][i][t];
     p.v[u.voff + t * rpad4(u.rank) + u.off + i] = s;
   }
 }
 
 __device__ __forceinline__ void expand(const RingArgs& p, const BgmvUnit& u, const Geom& g,
-                                       char* sb, float (*vs)[kMaxBgmvRank]) {
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                       char* sb, float (*vs)[kMaxBgmvRank], uint32_t gw,
+                                       uint32_t gt, uint32_t bar_id) {
+  const uint32_t lane = threadIdx.x & 31;
   // v rows arrived in the slot (the producer acquired the segment counter)
   const uint32_t rp = rpad4(u.rank);
   const float* vsl = reinterpret_cast<const float*>(sb + g.aux + u.ntok * g.cb * 2);
-  for (uint32_t i = threadIdx.x; i < kMaxUnitTok * g.r16; i += kConsumers) {
+  const uint32_t plane = u.ntok * rp;
+  for (uint32_t i = gt; i < kMaxUnitTok * g.r16; i += kGroupThreads) {
     const uint32_t t = i / g.r16, j = i - t * g.r16;
-    vs[t][j] = (t < u.ntok && j < u.rank) ? vsl[t * rp + j] : 0.f;
+    float s = 0.f;
+    if (t < u.ntok && j < u.rank)
+      for (uint32_t kc = 0; kc < u.nkc; ++kc) s += vsl[kc * plane + t * rp + j];
+    vs[t][j] = s;
   }
-  ptx::named_bar_sync(1, kConsumers);
+  ptx::named_bar_sync(bar_id, kGroupThreads);
   const uint32_t gq = lane >> 2, c = lane & 3;
   const uint32_t tg = min(gq, kMaxUnitTok - 1);
   const float gate = gq < u.ntok ? 1.f : 0.f;
   const uint32_t ksteps = g.r16 / 16;
   const uint32_t b_base = ptx::smem_u32(sb + (lane & 15) * g.stride);
-  char* Y = sb + g.aux;
-  for (uint32_t nt = warp; nt < u.count / 8; nt += kConsumers / 32) {
-    float d[4] = {0.f, 0.f, 0.f, 0.f};
+  const char* Y = sb + g.aux;
+  const uint32_t n_tiles = u.count / 8;
+  // this warp owns column tiles gw, gw + 4, ...; 8 of them per accumulator pass
+  for (uint32_t t0 = gw; t0 < n_tiles; t0 += kTiles * kGroupWarps) {
+    float d[kTiles][4] = {};
     for (uint32_t kk = 0; kk < ksteps; ++kk) {
       const uint32_t j0 = kk * 16 + 2 * c;
       const float v0 = gate * vs[tg][j0], v1 = gate * vs[tg][j0 + 1];
@@ -302,57 +353,75 @@ __device__ __forceinline__ void expand(const RingArgs& p, const BgmvUnit& u, con
       const uint32_t ahi[4] = {h0, 0u, h2, 0u};
       const uint32_t alo[4] = {pack_bf16x2(v0 - f0.x, v1 - f0.y), 0u,
                                pack_bf16x2(v8 - f2.x, v9 - f2.y), 0u};
-      uint32_t b[2];
-      ptx::ldsm_x2_trans(b_base + kk * 16 * g.stride + nt * 16, b);
-      ptx::mma_bf16_16816(d, ahi, b);
-      ptx::mma_bf16_16816(d, alo, b);
+#pragma unroll
+      for (int i = 0; i < kTiles; ++i) {
+        const uint32_t nt = t0 + i * kGroupWarps;
+        if (nt < n_tiles) {
+          uint32_t b[2];
+          ptx::ldsm_x2_trans(b_base + kk * 16 * g.stride + nt * 16, b);
+          ptx::mma_bf16_16816(d[i], ahi, b);
+          ptx::mma_bf16_16816(d[i], alo, b);
+        }
+      }
     }
     if (gq < u.ntok) {  // d0/d1 = (token gq, columns nt·8 + 2c, +1): fire-and-forget store
-      const uint32_t col = nt * 8 + 2 * c;
-      const float2 yo =
-          __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(Y + gq * g.cb * 2 + col * 2));
-      *reinterpret_cast<__nv_bfloat162*>(p.y + u.tok[gq] * p.y_stride_b +
-                                         static_cast<uint64_t>(u.off + col) * 2) =
-          __floats2bfloat162_rn(fmaf(p.scale, d[0], yo.x), fmaf(p.scale, d[1], yo.y));
+      char* yrow = p.y + u.tok[gq] * p.y_stride_b;
+#pragma unroll
+      for (int i = 0; i < kTiles; ++i) {
+        const uint32_t nt = t0 + i * kGroupWarps;
+        if (nt < n_tiles) {
+          const uint32_t col = nt * 8 + 2 * c;
+          const float2 yo = __bfloat1622float2(
+              *reinterpret_cast<const __nv_bfloat162*>(Y + gq * g.cb * 2 + col * 2));
+          *reinterpret_cast<__nv_bfloat162*>(yrow + static_cast<uint64_t>(u.off + col) * 2) =
+              __floats2bfloat162_rn(fmaf(p.scale, d[i][0], yo.x), fmaf(p.scale, d[i][1], yo.y));
+        }
+      }
     }
   }
 }
 
-__device__ void consumer(const RingArgs& p, char* smem) {
+// Consumer group grp processes local units grp, grp + 2, ... (slots k % 4).
+__device__ void consumer(const RingArgs& p, char* smem, uint32_t grp) {
   const BgmvUnit* hdr = reinterpret_cast<const BgmvUnit*>(smem + Smem::hdr);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Smem::bars);
   uint64_t* empty = full + kSlots;
-  float (*red)[8][8] = reinterpret_cast<float (*)[8][8]>(smem + Smem::red);
-  float (*vs)[kMaxBgmvRank] = reinterpret_cast<float (*)[kMaxBgmvRank]>(smem + Smem::vs);
+  float (*red)[16][8] =
+      reinterpret_cast<float (*)[16][8]>(smem + Smem::red) + grp * kGroupWarps;
+  pdl_wait();  // consumers write v / y / counters: the previous call must be done
+  float (*vs)[kMaxBgmvRank] =
+      reinterpret_cast<float (*)[kMaxBgmvRank]>(smem + Smem::vs) + grp * kMaxUnitTok;
+  const uint32_t gt = threadIdx.x - grp * kGroupThreads, gw = gt >> 5;
+  const uint32_t bar_id = 1 + grp;
   uint32_t pending = kStop;  // segment whose shrink unit still has to be published
-  for (uint32_t k = 0;; ++k) {
+  for (uint32_t k = grp;; k += kGroups) {
     const uint32_t slot = k % kSlots, phase = (k / kSlots) & 1u;
     if (pending != kStop) {
-      if (threadIdx.x == kConsumers - 32) {  // warp 7 publishes while the others wait for data
+      if (gt == kGroupThreads - 32) {  // last warp publishes while the others wait for data
         __threadfence();
         atomicAdd(p.sync + 2 + pending, 1u);
       }
       pending = kStop;
     }
     ptx::mbar_wait(&full[slot], phase);
-    if (threadIdx.x == 0) trace_put(p.trace, k, 1, now_ns());
+    if (gt == 0) trace_put(p.trace, k, 1, now_ns());
     const BgmvUnit u = hdr[slot];
     if (u.kind_seg == kStop) break;
     char* sb = smem + Smem::slots + slot * kSlotBytes;
     const Geom g = geom(p, u);
     if (!(u.kind_seg & kExpandBit)) {
-      shrink(p, u, g, sb, red);
+      shrink(p, u, g, sb, red, gw, gt, bar_id);
       pending = u.kind_seg;
     } else {
-      expand(p, u, g, sb, vs);
+      expand(p, u, g, sb, vs, gw, gt, bar_id);
     }
-    ptx::named_bar_sync(1, kConsumers);  // slot + scratch free
-    if (threadIdx.x == 0) {
+    ptx::named_bar_sync(bar_id, kGroupThreads);  // slot + group scratch free
+    if (gt == 0) {
       trace_put(p.trace, k, 2, now_ns());
       ptx::mbar_arrive(&empty[slot]);
     }
   }
-  if (pending != kStop && threadIdx.x == kConsumers - 32) {
+  if (pending != kStop && gt == kGroupThreads - 32) {
     __threadfence();
     atomicAdd(p.sync + 2 + pending, 1u);
   }
@@ -363,6 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) bgmv_ring_kernel(const RingArgs p
   __shared__ uint32_t s_last;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Smem::bars);
   uint64_t* empty = full + kSlots;
+  pdl_launch_dependents();  // the next call may start streaming its weights
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSlots; ++s) {
       ptx::mbar_init(&full[s], 1);
@@ -372,9 +442,9 @@ __global__ void __launch_bounds__(kThreads, 1) bgmv_ring_kernel(const RingArgs p
   }
   __syncthreads();
   if (threadIdx.x >= kConsumers)
-    producer(p, smem);
+    producer(p, smem, (threadIdx.x - kConsumers) >> 5);
   else
-    consumer(p, smem);
+    consumer(p, smem, threadIdx.x / kGroupThreads);
   __syncthreads();
   // the last CTA out resets the per-segment counters (graph-replayable)
   if (threadIdx.x == 0) {
@@ -421,17 +491,27 @@ void launch_bgmv_ring(const plora_plan& plan, uint32_t layer, uint32_t proj, con
   a.d_in = gm.m.d_in[proj];
   a.d_out = gm.m.d_out[proj];
   a.scale = scale;
-  const uint32_t grid0 = std::min<uint32_t>(pw.n_units, static_cast<uint32_t>(st.num_sms));
-  a.trace = g_trace_bytes >= static_cast<uint64_t>(grid0) * kTraceUnits * 32 ? g_trace : nullptr;
+  const uint32_t grid = std::min<uint32_t>(pw.n_units, static_cast<uint32_t>(st.num_sms));
+  a.trace = g_trace_bytes >= static_cast<uint64_t>(grid) * kTraceUnits * 64 ? g_trace : nullptr;
   static bool attr = false;
   if (!attr) {
     PLORA_CUDA(cudaFuncSetAttribute(bgmv_ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(Smem::total)));
     attr = true;
   }
-  const uint32_t grid = std::min<uint32_t>(pw.n_units, static_cast<uint32_t>(st.num_sms));
-  bgmv_ring_kernel<<<grid, kThreads, Smem::total, stream>>>(a);
-  PLORA_CUDA(cudaGetLastError());
+  // programmatic dependent launch: this call's weight streaming may overlap
+  // the previous call's tail (the kernel waits before touching activations)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Smem::total;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_ring_kernel, a));
   count_launch();
 }
 

@@ -44,12 +44,17 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   std::sort(segs.begin(), segs.end(), [](const Seg& x, const Seg& y) { return x.adapter < y.adapter; });
   v_elems = 0;
   max_rank = 0;
+  uint32_t nkc_max = 1;
+  if (es == 2)
+    for (uint32_t p = 0; p < g.m.n_proj; ++p)
+      nkc_max = std::max(nkc_max, (g.m.d_in[p] + kShrinkK - 1) / kShrinkK);
   for (Seg& s : segs) {
     if (s.rank > kMaxBgmvRank)
       throw ValidationError("adapter " + std::to_string(s.adapter) + " has rank " +
                             std::to_string(s.rank) + " > " + std::to_string(kMaxBgmvRank));
     s.voff = static_cast<uint32_t>(v_elems);
-    v_elems += static_cast<uint64_t>(s.toks.size()) * rpad4(s.rank);
+    // bf16: one partial plane of v per kShrinkK-wide K chunk (summed by the expand)
+    v_elems += static_cast<uint64_t>(s.toks.size()) * rpad4(s.rank) * nkc_max;
     max_rank = std::max(max_rank, s.rank);
   }
   if (v_elems > 0xffffffffull) throw ValidationError("batch too large for one plan");
@@ -67,31 +72,41 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   for (uint32_t p = 0; p < g.m.n_proj; ++p) {
     const uint32_t din = g.m.d_in[p], dout = g.m.d_out[p];
     const uint32_t rowbytes = din * es;
-    if (rowbytes > kSlotAuxBytes)
-      throw ValidationError("BGMV needs d_in * esize <= " + std::to_string(kSlotAuxBytes) +
+    if (es == 4 && rowbytes > kSlotAuxBytes)
+      throw ValidationError("fp32 BGMV needs d_in * 4 <= " + std::to_string(kSlotAuxBytes) +
                             " bytes (d_in=" + std::to_string(din) + ")");
-    const uint32_t rpu = std::min<uint32_t>(kMaxShrinkRows, kShrinkWeightBytes / rowbytes);
-    const uint32_t nts = std::min<uint32_t>(kMaxUnitTok, kSlotAuxBytes / rowbytes);
+    // bf16 (tensor-core ring): 16 rank rows × kShrinkK columns per unit, K
+    // partials in separate v planes.  fp32 (CUDA cores): rpu full rows.
+    const bool ksplit = es == 2;
+    const uint32_t nkc = ksplit ? (din + kShrinkK - 1) / kShrinkK : 1;
+    const uint32_t rpu = ksplit ? kShrinkRows16
+                                : std::min<uint32_t>(kMaxShrinkRows, kShrinkWeightBytes / rowbytes);
+    const uint32_t nts = ksplit ? kMaxUnitTok
+                                : std::min<uint32_t>(kMaxUnitTok, kSlotAuxBytes / rowbytes);
     ProjWork& pw = proj[p];
     pw.units_off = static_cast<uint32_t>(units.size());
     std::vector<uint32_t> n_shrink(n_seg, 0);
     for (uint32_t si : order) {
       const Seg& s = segs[si];
       const uint32_t rp = rpad4(s.rank), nt_all = static_cast<uint32_t>(s.toks.size());
+      const uint32_t vstride = nt_all * rp;
       for (uint32_t tc = 0; tc < nt_all; tc += nts) {
         const uint32_t nt = std::min(nts, nt_all - tc);
         for (uint32_t j0 = 0; j0 < s.rank; j0 += rpu) {
-          BgmvUnit u{};
-          u.kind_seg = si;
-          u.off = j0;
-          u.count = std::min(rpu, s.rank - j0);
-          u.table_off = s.table_off;
-          u.rank = s.rank;
-          u.voff = s.voff + tc * rp;
-          u.ntok = nt;
-          for (uint32_t t = 0; t < nt; ++t) u.tok[t] = s.toks[tc + t];
-          units.push_back(u);
-          ++n_shrink[si];
+          for (uint32_t kc = 0; kc < nkc; ++kc) {
+            BgmvUnit u{};
+            u.kind_seg = si;
+            u.off = j0;
+            u.count = std::min(rpu, s.rank - j0);
+            u.table_off = s.table_off;
+            u.rank = s.rank;
+            u.voff = s.voff + kc * vstride + tc * rp;
+            u.ntok = nt;
+            u.kc = kc;
+            for (uint32_t t = 0; t < nt; ++t) u.tok[t] = s.toks[tc + t];
+            units.push_back(u);
+            ++n_shrink[si];
+          }
         }
       }
     }
@@ -100,10 +115,12 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       const Seg& s = segs[si];
       const uint32_t rp = rpad4(s.rank), nt_all = static_cast<uint32_t>(s.toks.size());
       const uint32_t rg = es == 2 ? 1 : expand_rg(s.rank), cb = expand_cols(s.rank, es);
-      const uint32_t per_tok = rp * 4 + cb * es;
-      // tokens per unit: aux area (v + y rows) and, when rows are split over
-      // groups, the reduction buffer (RG · CB fp32 per token)
-      uint32_t nte = std::min<uint32_t>(kMaxUnitTok, kSlotAuxBytes / per_tok);
+      const uint32_t per_tok = nkc * rp * 4 + cb * es;
+      // tokens per unit: aux area (v partial rows + y rows) and, when rows are
+      // split over groups, the reduction buffer (RG · CB fp32 per token)
+      const uint32_t aux_budget =
+          ksplit ? kRingSlotBytes - ((s.rank + 15) & ~15u) * (cb * 2 + kRingRowPad) : kSlotAuxBytes;
+      uint32_t nte = std::min<uint32_t>(kMaxUnitTok, aux_budget / per_tok);
       if (rg > 1) nte = std::min<uint32_t>(nte, kRedBytes / (rg * cb * 4));
       nte = std::max<uint32_t>(nte, 1);
       for (uint32_t tc = 0; tc < nt_all; tc += nte) {
@@ -118,6 +135,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
           u.voff = s.voff + tc * rp;
           u.ntok = nt;
           u.n_shrink = n_shrink[si];
+          u.nkc = nkc;
+          u.vstride = nt_all * rp;
           for (uint32_t t = 0; t < nt; ++t) u.tok[t] = s.toks[tc + t];
           units.push_back(u);
         }

@@ -23,7 +23,7 @@ constexpr uint32_t kSlotAuxBytes = 16384;       // x rows (shrink) / y rows (exp
 constexpr uint32_t kMaxShrinkRows = 8;          // one warp per rank row
 constexpr uint32_t kMaxBgmvRank = 256;
 
-// A BGMV work unit, fully resolved on the host (48 bytes): the producer warp
+// A BGMV work unit, fully resolved on the host (64 bytes): the producer warp
 // needs no dependent loads besides the page table.
 struct BgmvUnit {
   uint32_t kind_seg;  // segment | kExpandBit for expand units
@@ -35,8 +35,20 @@ struct BgmvUnit {
   uint32_t ntok;      // tokens (<= kMaxUnitTok)
   uint32_t n_shrink;  // expand: shrink units of the segment to wait for
   uint32_t tok[kMaxUnitTok];  // x / y row indices
+  uint32_t kc;        // shrink: K chunk (bf16 path: d_in split in kShrinkK slices)
+  uint32_t nkc;       // expand: number of K-chunk partial planes of v to sum
+  uint32_t vstride;   // expand: floats between consecutive partial planes
+  uint32_t pad;
 };
-static_assert(sizeof(BgmvUnit) == 48, "BgmvUnit layout");
+static_assert(sizeof(BgmvUnit) == 64, "BgmvUnit layout");
+
+// bf16 shrink units: 16 rank rows (the MMA M) × kShrinkK input columns.
+constexpr uint32_t kShrinkK = 1024;
+constexpr uint32_t kShrinkRows16 = 16;
+// bf16 ring slot: shrink 16 rows + 4 x rows of (kShrinkK·2 + 16) bytes;
+// expand Bᵀ tile r16 × (CB·2 + 16) + per token: y segment + K-partial v rows.
+constexpr uint32_t kRingSlotBytes = 53248;
+constexpr uint32_t kRingRowPad = 16;
 
 // Expand split: RG row groups × CT column threads (RG·CT = kBgmvConsumers),
 // CB = CT · VEC columns, so the Bᵀ tile r × CB fits one 32 KiB slot and a

@@ -189,15 +189,35 @@ class Lstm {
   }
 
   // d(mean CE)/dθ by backpropagation through time (lstm.cpp:190-281).
+  // d(mean CE)/dθ.  Examples are processed in fixed chunks of kGradChunk
+  // (threads over chunks), partial gradients summed in chunk order, so the
+  // result does not depend on the host's thread count.
+  static constexpr std::size_t kGradChunk = 8;
   std::vector<double> gradient(const std::vector<Example>& batch) const {
     validate_batch(batch);
+    const std::size_t B = batch.size(), P = theta_.size();
+    const std::size_t n_chunks = (B + kGradChunk - 1) / kGradChunk;
+    std::vector<double> part(n_chunks * P, 0.0);
+    parallel_for(n_chunks, 1, [&](std::size_t lo, std::size_t hi) {
+      for (std::size_t c = lo; c < hi; ++c)
+        grad_range(batch, c * kGradChunk, std::min(B, (c + 1) * kGradChunk), part.data() + c * P);
+    });
+    std::vector<double> grad(part.begin(), part.begin() + P);
+    for (std::size_t c = 1; c < n_chunks; ++c) {
+      const double* q = part.data() + c * P;
+      for (std::size_t i = 0; i < P; ++i) grad[i] += q[i];
+    }
+    return grad;
+  }
+
+  void grad_range(const std::vector<Example>& batch, std::size_t b0, std::size_t b1,
+                  double* grad) const {
     const std::size_t B = batch.size(), H = c_.hidden, E = c_.embedding_dim, T = c_.window;
     const std::size_t per_t = 7 * H;
-    std::vector<double> grad(theta_.size(), 0.0);
     std::vector<double> cache(c_.layers * T * per_t);
     std::vector<double> dh_ext(T * H), dx_below(T * std::max<std::size_t>(in0_, H));
     std::vector<double> dz(4 * H), dh(H), dc(H), dc_next(H), dh_carry(H), xs(T * in0_);
-    for (std::size_t b = 0; b < B; ++b) {
+    for (std::size_t b = b0; b < b1; ++b) {
       const Example& ex = batch[b];
       const double z = logit_one(ex, &cache);
       const double dlogit = (sigmoid(z) - ex.label) / static_cast<double>(B);
@@ -215,9 +235,9 @@ class Lstm {
         const std::size_t in = l == 0 ? in0_ : H;
         const double* W = theta_.data() + w_off_[l];
         const double* U = theta_.data() + u_off_[l];
-        double* gW = grad.data() + w_off_[l];
-        double* gU = grad.data() + u_off_[l];
-        double* gb = grad.data() + b_off_[l];
+        double* gW = grad + w_off_[l];
+        double* gU = grad + u_off_[l];
+        double* gb = grad + b_off_[l];
         std::fill(dc_next.begin(), dc_next.end(), 0.0);
         std::fill(dh_carry.begin(), dh_carry.end(), 0.0);
         for (int t = static_cast<int>(T) - 1; t >= 0; --t) {
@@ -268,13 +288,12 @@ class Lstm {
           for (std::size_t t = 0; t < T; ++t)
             for (std::size_t j = 0; j < H; ++j) dh_ext[t * H + j] = dx_below[t * H + j];
         } else {
-          double* g_emb = grad.data() + emb_off_ + ex.adapter * E;
+          double* g_emb = grad + emb_off_ + ex.adapter * E;
           for (std::size_t t = 0; t < T; ++t)
             for (std::size_t e = 0; e < E; ++e) g_emb[e] += dx_below[t * in0_ + 1 + e];
         }
       }
     }
-    return grad;
   }
 
   double train_step(const std::vector<Example>& batch) {  // lstm.cpp:283-296

@@ -10,7 +10,7 @@ has() { [[ ",$STAGES," == *",$1,"* ]]; }
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/nvsmi.txt 2>&1
 nproc > gpurun_out/host_cores.txt; lscpu | grep -i "model name" >> gpurun_out/host_cores.txt
 if has test; then
-  timeout 1200 python -m pytest tests -m gpu -q -rA > gpurun_out/pytest_gpu.log 2>&1
+  timeout 600 python -m pytest tests -m gpu -q -rA > gpurun_out/pytest_gpu.log 2>&1
   echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 fi
 if has smoke; then
@@ -28,7 +28,7 @@ if has launches; then
   echo "launches rc=$?" >> gpurun_out/launches.log
 fi
 if has full; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:bgmv_ -s 400 -c 4 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:bgmv_ -s 200 -c 2 \
     -o gpurun_out/bgmv_full -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/ncu_full.log 2>&1
   echo "full rc=$?" >> gpurun_out/ncu_full.log

@@ -31,7 +31,7 @@ def main():
     for _ in range(3):
         bgmv(plan, 1, 0, x, y)
     ctas, units = 148, 64
-    buf = torch.zeros(ctas * units * 4, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(ctas * units * 8, dtype=torch.int64, device="cuda")
     N.check(N.lib().plora_debug_set_trace(buf.data_ptr(), buf.numel() * 8))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -40,8 +40,9 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     N.check(N.lib().plora_debug_set_trace(None, 0))
-    t = buf.view(ctas, units, 4).cpu().numpy().astype(np.int64)
+    t = buf.view(ctas, units, 8).cpu().numpy().astype(np.int64)
     issued, ready, done, kind = t[..., 0], t[..., 1], t[..., 2], t[..., 3]
+    top, prewait, postwait = t[..., 4], t[..., 5], t[..., 6]
     valid = issued > 0
     t0 = issued[valid].min()
     print(f"call {e0.elapsed_time(e1) * 1e3:.1f} us (event), span {(done[valid].max() - t0) / 1e3:.1f} us")
@@ -68,6 +69,11 @@ def main():
     # issue lead: how far ahead of consumption the producer runs (units)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     np.savez(os.path.join(ROOT, "gpurun_out", "trace_bgmv.npz"), trace=t)
+    for c in (0, 77):
+        v = valid[c]
+        rows = [tuple(int((z - t0) / 100) / 10 for z in (a, b, cc, d))
+                for a, b, cc, d in zip(top[c][v], prewait[c][v], postwait[c][v], issued[c][v])]
+        print(f"CTA {c} producer (loop top, pre-wait, post-wait, issued) us:", rows[:16])
     for c in (0, 1, 77):
         v = valid[c]
         rows = [(int((i - t0) / 1e3 * 10) / 10, int((r - t0) / 1e3 * 10) / 10,
