@@ -284,6 +284,88 @@ int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                plora_stream_t stream);
 
+/* ------------------------------------ loading / prefetch engine (new) -----
+ * The reference simulator's residency control restated on CUDA streams and
+ * events: Simulation::ensure_loading / evict (src/engine.cpp:292-333),
+ * transfers (:197-288), do_boundary / admit_requests / issue_prefetches /
+ * maybe_compact (:406-497), on_arrival / on_round (:515-571).  Transfers
+ * are real page scatters of caller-owned pinned host images; demand loads
+ * run on a high-priority stream and preempt prefetch at chunk granularity;
+ * prefetched adapters are promoted (device table published) at the next
+ * boundary.  One owner thread per engine; the engine's own pump thread
+ * keeps prefetch copies flowing between boundaries. */
+#define PLORA_COPY_AUTO 2 /* CE for pages >= 64 KiB, SM scatter kernel below */
+#define PLORA_ADMIT_LOADING 0 /* weights in flight (demand priority) */
+#define PLORA_ADMIT_READY 1   /* resident and published */
+#define PLORA_ADMIT_FAILED 2  /* could not allocate (engine.cpp:427-431) */
+typedef struct {
+  plora_policy policy;
+  int32_t copy_mode;  /* PLORA_COPY_CE / _SM / _AUTO */
+  int32_t prefetch;   /* issue_prefetches enabled (RunConfig policy.prefetch) */
+  int32_t compaction; /* idle compaction (engine.cpp:486-497) */
+  int32_t reserved;
+  uint64_t chunk_bytes;             /* prefetch issue granularity */
+  uint64_t prefetch_inflight_bytes; /* prefetch bytes in flight at most */
+} plora_engine_config;
+typedef struct { /* MetricsReport counters (include/lorasim/engine.hpp:66-98) */
+  uint64_t arrivals, hits, demand_loads, prefetch_issued, promotions, evictions;
+  uint64_t admission_failures, upgrades, compactions, relocations, prediction_rounds;
+  uint64_t transfers_completed, bytes_h2d;
+  double transfer_ms;        /* Σ per-transfer device time (first chunk -> done) */
+  double demand_transfer_ms; /* the demand share of it */
+  double predictor_ms;       /* async predictor worker busy time */
+  uint64_t in_flight, staged, resident;
+  int32_t copy_mode, reserved;
+} plora_engine_stats;
+typedef struct plora_engine plora_engine;
+typedef struct plora_predictor plora_predictor;
+void plora_engine_config_default(plora_engine_config* c);
+int plora_engine_create(plora_store* s, const plora_engine_config* cfg, plora_engine** out);
+void plora_engine_destroy(plora_engine* e);
+/* Host image of a registered adapter (plora_model_adapter_bytes(rank) bytes,
+ * caller-owned; pinned for PLORA_COPY_SM and for asynchronous CE copies). */
+int plora_engine_set_source(plora_engine* e, uint32_t adapter, const void* host_src,
+                            uint64_t bytes);
+/* NULL detaches.  async = 0: observe/predict_all run inline (the
+ * reference's synchronous semantics).  async = 1: a worker thread owns the
+ * predictor; a round applies the last completed prediction set and requests
+ * the next (one round of lag), keeping the LSTM off the decode loop. */
+int plora_engine_attach_predictor(plora_engine* e, plora_predictor* p, int async);
+/* Wait for the async predictor to drain queued observations and finish the
+ * requested round, then apply its predictions. */
+int plora_engine_flush_predictor(plora_engine* e);
+/* Request arrival (engine.cpp:515-545): access statistics, predictor
+ * observation, reactive demand load.  Returns 1 if resident at arrival. */
+int plora_engine_on_arrival(plora_engine* e, uint32_t adapter, double now_ms,
+                            plora_stream_t compute);
+/* Prediction round (engine.cpp:547-561): predict_all of the attached predictor. */
+int plora_engine_round(plora_engine* e, double now_ms, plora_stream_t compute);
+/* External predictions (oracle mode, engine.cpp:562-571); -1 = no prediction. */
+int plora_engine_set_predictions(plora_engine* e, const double* probs, uint64_t n);
+/* Admission (engine.cpp:416-457): PLORA_ADMIT_READY / _LOADING / _FAILED;
+ * pins the adapter (busy) until plora_engine_release. */
+int plora_engine_acquire(plora_engine* e, uint32_t adapter, double now_ms,
+                         plora_stream_t compute);
+/* Make `compute` wait (device-side) for a loading adapter and publish it. */
+int plora_engine_wait_ready(plora_engine* e, uint32_t adapter, plora_stream_t compute);
+int plora_engine_release(plora_engine* e, uint32_t adapter); /* finish_request :358-372 */
+/* Batch boundary (engine.cpp:406-414): completions, promotions, prefetch
+ * issue, idle compaction.  Table updates are ordered on `compute`.
+ * Returns the number of transfers observed complete. */
+int plora_engine_boundary(plora_engine* e, double now_ms, plora_stream_t compute);
+/* Batched forms for a serving loop: arrivals (returns the hit count),
+ * admission of distinct adapters (status per entry; wait != 0 makes
+ * `compute` wait device-side for loading ones), release. */
+int64_t plora_engine_on_arrivals(plora_engine* e, const uint32_t* adapters, uint64_t n,
+                                 double now_ms, plora_stream_t compute);
+int plora_engine_admit(plora_engine* e, const uint32_t* adapters, uint64_t n, double now_ms,
+                       plora_stream_t compute, int wait, int32_t* status);
+int plora_engine_release_many(plora_engine* e, const uint32_t* adapters, uint64_t n);
+int plora_engine_sync(plora_engine* e); /* wait for every issued copy */
+int plora_engine_status(const plora_engine* e, uint32_t adapter, plora_dynamics* out);
+void plora_engine_get_stats(const plora_engine* e, plora_engine_stats* out);
+int plora_engine_streams(const plora_engine* e, plora_stream_t* demand, plora_stream_t* prefetch);
+
 /* ----------------------------------------------- demand predictor (host) ---
  * The LSTM that drives predictor-based prefetch: PredictorModel
  * (include/lorasim/lstm.hpp:11-85) and OnlinePredictor
@@ -321,7 +403,6 @@ int plora_lstm_train_step(plora_lstm* m, const uint32_t* adapters, const double*
 int plora_lstm_save(const plora_lstm* m, const char* path);
 int plora_lstm_load(const char* path, plora_lstm** out);
 
-typedef struct plora_predictor plora_predictor;
 int plora_predictor_create(const plora_predictor_config* cfg, uint64_t seed,
                            plora_predictor** out);
 void plora_predictor_destroy(plora_predictor* p);

@@ -27,6 +27,13 @@ PLORA_BF16 = 0
 PLORA_F32 = 1
 PLORA_COPY_CE = 0
 PLORA_COPY_SM = 1
+PLORA_COPY_AUTO = 2
+PLORA_ADMIT_LOADING = 0
+PLORA_ADMIT_READY = 1
+PLORA_ADMIT_FAILED = 2
+PLORA_NOT_RESIDENT = 0
+PLORA_STAGING = 1
+PLORA_RESIDENT = 2
 
 
 class CudaError(RuntimeError):
@@ -69,6 +76,23 @@ class plora_model(C.Structure):
     _fields_ = [("n_layers", C.c_uint32), ("n_proj", C.c_uint32),
                 ("d_in", C.c_uint32 * PLORA_MAX_PROJ), ("d_out", C.c_uint32 * PLORA_MAX_PROJ),
                 ("dtype", C.c_uint32)]
+
+
+class plora_engine_config(C.Structure):
+    _fields_ = [("policy", plora_policy), ("copy_mode", C.c_int32), ("prefetch", C.c_int32),
+                ("compaction", C.c_int32), ("reserved", C.c_int32), ("chunk_bytes", C.c_uint64),
+                ("prefetch_inflight_bytes", C.c_uint64)]
+
+
+class plora_engine_stats(C.Structure):
+    _fields_ = ([(n, C.c_uint64) for n in (
+        "arrivals", "hits", "demand_loads", "prefetch_issued", "promotions", "evictions",
+        "admission_failures", "upgrades", "compactions", "relocations", "prediction_rounds",
+        "transfers_completed", "bytes_h2d")]
+        + [("transfer_ms", C.c_double), ("demand_transfer_ms", C.c_double),
+           ("predictor_ms", C.c_double)]
+        + [(n, C.c_uint64) for n in ("in_flight", "staged", "resident")]
+        + [("copy_mode", C.c_int32), ("reserved", C.c_int32)])
 
 
 class plora_lstm_config(C.Structure):
@@ -162,6 +186,26 @@ _SIGS = {
     "plora_plan_num_segments": (_u32, [_vp]),
     "plora_bgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
     "plora_sgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
+    "plora_engine_config_default": (None, [_P(plora_engine_config)]),
+    "plora_engine_create": (_int, [_vp, _P(plora_engine_config), _P(_vp)]),
+    "plora_engine_destroy": (None, [_vp]),
+    "plora_engine_set_source": (_int, [_vp, _u32, _vp, _u64]),
+    "plora_engine_attach_predictor": (_int, [_vp, _vp, _int]),
+    "plora_engine_flush_predictor": (_int, [_vp]),
+    "plora_engine_on_arrival": (_int, [_vp, _u32, _dbl, _vp]),
+    "plora_engine_round": (_int, [_vp, _dbl, _vp]),
+    "plora_engine_set_predictions": (_int, [_vp, _P(_dbl), _u64]),
+    "plora_engine_acquire": (_int, [_vp, _u32, _dbl, _vp]),
+    "plora_engine_wait_ready": (_int, [_vp, _u32, _vp]),
+    "plora_engine_release": (_int, [_vp, _u32]),
+    "plora_engine_boundary": (_int, [_vp, _dbl, _vp]),
+    "plora_engine_sync": (_int, [_vp]),
+    "plora_engine_on_arrivals": (_i64, [_vp, _P(_u32), _u64, _dbl, _vp]),
+    "plora_engine_admit": (_int, [_vp, _P(_u32), _u64, _dbl, _vp, _int, _P(_i32)]),
+    "plora_engine_release_many": (_int, [_vp, _P(_u32), _u64]),
+    "plora_engine_status": (_int, [_vp, _u32, _P(plora_dynamics)]),
+    "plora_engine_get_stats": (None, [_vp, _P(plora_engine_stats)]),
+    "plora_engine_streams": (_int, [_vp, _P(_vp), _P(_vp)]),
     "plora_lstm_config_default": (None, [_P(plora_lstm_config)]),
     "plora_predictor_config_default": (None, [_P(plora_predictor_config)]),
     "plora_cross_entropy": (_int, [_P(_dbl), _P(_dbl), _u64, _P(_dbl)]),

@@ -38,15 +38,16 @@ namespace {
 
 // One page per warp-iteration: 16-byte vectors, src in mapped pinned host
 // memory (PCIe reads), dst in the arena at the physical page.
+// Logical pages [first, first + n_pages); `bytes` is the whole image size.
 __global__ void page_scatter_h2d_kernel(const uint4* __restrict__ src, char* __restrict__ arena,
-                                        const uint32_t* __restrict__ entries, uint32_t n_pages,
-                                        uint32_t log2_page, uint64_t bytes) {
+                                        const uint32_t* __restrict__ entries, uint32_t first,
+                                        uint32_t n_pages, uint32_t log2_page, uint64_t bytes) {
   const uint32_t vec_per_page = (1u << log2_page) / 16;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
   const uint64_t n_vec_total = bytes / 16;
-  for (uint32_t pg = warp; pg < n_pages; pg += n_warps) {
+  for (uint32_t pg = first + warp; pg < first + n_pages; pg += n_warps) {
     const uint64_t base_vec = static_cast<uint64_t>(pg) * vec_per_page;
     uint4* dst = reinterpret_cast<uint4*>(arena + (static_cast<uint64_t>(entries[pg]) << log2_page));
     for (uint32_t i = lane; i < vec_per_page; i += 32 * 4) {
@@ -118,6 +119,44 @@ void plora_store::upload_dir(uint32_t adapter, cudaStream_t stream) {
                              cudaMemcpyHostToDevice, stream));
   // h_dir is pageable: cudaMemcpyAsync stages it before returning, so later
   // host-side edits of the entry cannot race the upload.
+}
+
+const char* plora::mapped_source(const void* host_src, uint64_t bytes) {
+  if (bytes % 16 || reinterpret_cast<uintptr_t>(host_src) % 16)
+    throw ValidationError("SM page scatter needs 16-byte aligned size and source");
+  cudaPointerAttributes attr{};
+  PLORA_CUDA(cudaPointerGetAttributes(&attr, host_src));
+  if (attr.type != cudaMemoryTypeHost)
+    throw ValidationError("SM page scatter needs pinned (cudaHostAlloc/Register) host memory");
+  return static_cast<const char*>(attr.devicePointer ? attr.devicePointer : host_src);
+}
+
+void plora::scatter_pages(plora_store& s, uint32_t adapter, const char* src, const char* src_dev,
+                          uint32_t first, uint32_t n, uint64_t bytes, int mode,
+                          cudaStream_t stream) {
+  if (n == 0) return;
+  const PageTable& t = s.pool->pool.table(adapter);
+  const uint64_t P = s.pool->pool.page_bytes();
+  if (mode == PLORA_COPY_CE) {
+    // coalesce runs of consecutive physical pages into one copy each
+    uint32_t i = first;
+    while (i < first + n) {
+      uint32_t j = i + 1;
+      while (j < first + n && t.entries[j] == t.entries[j - 1] + 1) ++j;
+      const uint64_t off = static_cast<uint64_t>(i) * P;
+      const uint64_t len = std::min<uint64_t>(static_cast<uint64_t>(j - i) * P, bytes - off);
+      PLORA_CUDA(cudaMemcpyAsync(s.arena + static_cast<uint64_t>(t.entries[i]) * P, src + off,
+                                 len, cudaMemcpyDefault, stream));
+      i = j;
+    }
+    return;
+  }
+  const int blocks = std::min<int>(2 * s.num_sms, static_cast<int>((n + 7) / 8));
+  page_scatter_h2d_kernel<<<std::max(blocks, 1), 256, 0, stream>>>(
+      reinterpret_cast<const uint4*>(src_dev), s.arena, s.d_table + s.slots[adapter].table_off,
+      first, n, s.log2_page, bytes);
+  PLORA_CUDA(cudaGetLastError());
+  count_launch();
 }
 
 extern "C" {
@@ -243,36 +282,14 @@ int plora_store_write_pages(plora_store* s, uint32_t adapter, const void* host_s
     const uint64_t P = s->pool->pool.page_bytes();
     const uint32_t n_pages = static_cast<uint32_t>((bytes + P - 1) / P);
     const char* src = static_cast<const char*>(host_src);
-    if (mode == PLORA_COPY_CE) {
-      // coalesce runs of consecutive physical pages into one copy each
-      uint32_t i = 0;
-      while (i < n_pages) {
-        uint32_t j = i + 1;
-        while (j < n_pages && t.entries[j] == t.entries[j - 1] + 1) ++j;
-        const uint64_t off = static_cast<uint64_t>(i) * P;
-        const uint64_t len = std::min<uint64_t>(static_cast<uint64_t>(j - i) * P, bytes - off);
-        PLORA_CUDA(cudaMemcpyAsync(s->arena + static_cast<uint64_t>(t.entries[i]) * P, src + off,
-                                   len, cudaMemcpyDefault, stream));
-        i = j;
-      }
-    } else if (mode == PLORA_COPY_SM) {
-      if (bytes % 16 || reinterpret_cast<uintptr_t>(host_src) % 16)
-        throw ValidationError("SM page scatter needs 16-byte aligned size and source");
-      cudaPointerAttributes attr{};
-      PLORA_CUDA(cudaPointerGetAttributes(&attr, host_src));
-      if (attr.type != cudaMemoryTypeHost)
-        throw ValidationError("SM page scatter needs pinned (cudaHostAlloc/Register) host memory");
-      const void* dev_src = attr.devicePointer ? attr.devicePointer : host_src;
+    const char* src_dev = nullptr;
+    if (mode == PLORA_COPY_SM) {
+      src_dev = plora::mapped_source(host_src, bytes);
       s->upload_table(adapter, stream);  // the kernel reads the entries from the device table
-      const int blocks = std::min<int>(2 * s->num_sms, static_cast<int>((n_pages + 7) / 8));
-      page_scatter_h2d_kernel<<<std::max(blocks, 1), 256, 0, stream>>>(
-          static_cast<const uint4*>(dev_src), s->arena, s->d_table + s->slots[adapter].table_off,
-          n_pages, s->log2_page, bytes);
-      PLORA_CUDA(cudaGetLastError());
-      count_launch();
-    } else {
+    } else if (mode != PLORA_COPY_CE) {
       throw ValidationError("unknown copy mode " + std::to_string(mode));
     }
+    plora::scatter_pages(*s, adapter, src, src_dev, 0, n_pages, bytes, mode, stream);
     return 0;
   });
 }

@@ -97,3 +97,15 @@ struct plora_store {
   void upload_table(uint32_t adapter, cudaStream_t stream);
   void upload_dir(uint32_t adapter, cudaStream_t stream);
 };
+
+namespace plora {
+// Device alias of a pinned host image for the SM copy path (validates
+// alignment and pinning).
+const char* mapped_source(const void* host_src, uint64_t bytes);
+// Copy logical pages [first, first + n) of the adapter image `src` (`bytes`
+// long) into their physical pages.  PLORA_COPY_CE: one cudaMemcpyAsync per
+// physically contiguous run.  PLORA_COPY_SM: one scatter-kernel launch
+// reading src_dev, page entries from the device table (upload_table first).
+void scatter_pages(plora_store& s, uint32_t adapter, const char* src, const char* src_dev,
+                   uint32_t first, uint32_t n, uint64_t bytes, int mode, cudaStream_t stream);
+}  // namespace plora
