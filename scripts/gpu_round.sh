@@ -22,7 +22,7 @@ if has bench; then
   echo "bench rc=$?" >> gpurun_out/bench.err
 fi
 if has launches; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"bgmv|sgmv|page_" -c 2000 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/launches.log 2>&1
   echo "launches rc=$?" >> gpurun_out/launches.log
