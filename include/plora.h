@@ -433,6 +433,10 @@ int plora_predictor_buffer_at(const plora_predictor* p, uint64_t i, uint32_t* ad
  * trace[(cta * 64 + k) * 8 + {0 issued, 1 data ready, 2 computed, 3 kind, ...}]
  * for the first 64 units of each CTA.  dev_buf = NULL disables tracing. */
 int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
+/* Launch geometry the plan chose for the bf16 decode op of projection
+ * `proj`: out[0..7] = {cluster size, input slice, output slice, ring slots,
+ * slot bytes, dynamic smem bytes, clusters, chunks}. */
+int plora_debug_plan_geom(const plora_plan* plan, uint32_t proj, uint32_t out[8]);
 
 #ifdef __cplusplus
 }

@@ -232,6 +232,7 @@ _SIGS = {
     "plora_predictor_stats": (None, [_vp, _P(plora_predictor_stats_t)]),
     "plora_predictor_buffer_at": (_int, [_vp, _u64, _P(_u32), _P(_dbl), _P(_dbl)]),
     "plora_debug_set_trace": (_int, [_vp, _u64]),
+    "plora_debug_plan_geom": (_int, [_vp, _u32, _P(_u32)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,0 +1,736 @@
+// bf16 paged BGMV (decode) on thread-block clusters: the hot path behind
+// plora_bgmv for bf16 stores.
+//
+//   y[t, :] += scale · (x[t, :] · A_{a(t)}ᵀ) · B_{a(t)}ᵀ
+//
+// with A / Bᵀ rows read straight out of the page arena through the device
+// page table (the translation PagePool::translate does on the host,
+// src/memory.cpp:55-62).
+//
+// Decomposition.  A job is one adapter's tokens (<= kJobTok) at one
+// (layer, proj); its rank rows are cut into chunks of kChunkRows.  A cluster
+// of CS CTAs (4 for Llama-7B widths) owns a list of jobs, LPT-balanced on
+// the host by weight bytes.  Every CTA of the cluster walks the same chunk
+// list: CTA c streams the c-th input slice of the chunk's A rows and the
+// c-th output slice of its Bᵀ rows (both independent of the activations, so
+// both are in flight at once), computes the partial v_c = x[:, slice_c] ·
+// A[rows, slice_c]ᵀ and pushes it into every peer's shared memory with
+// st.async (completing bytes on the peer's exchange mbarrier).  After the
+// exchange each CTA holds the full v for the chunk and accumulates
+// v · Bᵀ[rows, slice_c] in registers; y is read once (TMA, prefetched with
+// x at the job's first chunk) and written once at the job's last chunk.  No
+// global-memory flags, no atomics; the only cross-CTA traffic is R·T floats
+// per chunk over DSMEM.
+//
+// Pipelining.  One producer warp per CTA issues 1-D TMA bulk copies (one per
+// page piece, L2 evict-first) into a ring of `slots` chunk slots; weights of
+// the next call are issued before griddepcontrol.wait (PDL), activations
+// after it.  Eight consumer warps: warp w dots rank row w of the chunk
+// (shrink) and all 256 threads share the expand columns.  The expand of
+// chunk i-1 runs after the shrink of chunk i, so the DSMEM round trip is
+// hidden behind a chunk of work.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "plan.hpp"
+#include "ptx.cuh"
+
+namespace plora {
+namespace {
+
+constexpr uint32_t kCWarps = kChunkRows;  // one consumer warp per chunk row
+constexpr uint32_t kCThreads = kCWarps * 32;
+constexpr uint32_t kPWarps = 4;                // producer warps (TMA issue is per-lane serial)
+constexpr uint32_t kThreads = kCThreads + kPWarps * 32;
+constexpr uint32_t kX = 16;                    // exchange slots (>= 2 · kMaxSlots, see shrink_group)
+constexpr uint32_t kMaxCs = 8;
+constexpr uint32_t kMaxSlots = 8;
+constexpr uint32_t kXSlotFloats = kJobTok * kChunkRows * kMaxCs;  // [t][row][src cta]
+constexpr uint32_t kSmemBudget = 200 * 1024;
+constexpr uint32_t kMaxSlice = 1024;  // elements per CTA slice (preferred)
+
+struct CArgs {
+  const char* arena;
+  const uint32_t* table;
+  const ClusterChunk* chunks;
+  const uint32_t* cl_off;
+  const char* x;
+  char* y;
+  uint64_t x_stride_b;
+  uint64_t y_stride_b;
+  uint64_t blk_mult;  // (layer, proj) block of a rank-r adapter starts at element r · blk_mult
+  uint32_t log2_page;
+  uint32_t d_in, d_out;
+  uint32_t cs, ks, ns;  // cluster size, slice widths (elements)
+  uint32_t slots, slot_bytes, jb_bytes;
+  uint32_t off_jb, off_xb, off_bar, off_hdr, off_part, off_ring;
+  uint32_t fast;  // every row slice lies inside one page (see my_piece)
+  float scale;
+  uint64_t* trace;  // diagnostics (plora_debug_set_trace) or nullptr
+};
+
+constexpr uint32_t kTraceChunks = 64;
+__device__ __forceinline__ uint64_t now_ns() {  // SM cycles (cheap; %globaltimer is not)
+  return clock64();
+}
+__device__ __forceinline__ void trace_put(const CArgs& p, uint32_t k, int field) {
+  if (p.trace && k < kTraceChunks) p.trace[(blockIdx.x * kTraceChunks + k) * 8 + field] = now_ns();
+}
+
+struct Bars {
+  uint64_t* full;    // [kMaxSlots] chunk weights landed
+  uint64_t* empty;   // [kMaxSlots] chunk slot free
+  uint64_t* jfull;   // [2] job x / y rows landed
+  uint64_t* jempty;  // [2] job buffer free
+  uint64_t* xfull;   // [kX] all CS partials of a chunk landed
+  __device__ explicit Bars(char* smem, uint32_t off) {
+    full = reinterpret_cast<uint64_t*>(smem + off);
+    empty = full + kMaxSlots;
+    jfull = empty + kMaxSlots;
+    jempty = jfull + 2;
+    xfull = jempty + 2;
+  }
+};
+constexpr uint32_t kBarBytes = (2 * kMaxSlots + 4 + kX) * 8;
+constexpr uint32_t kHdrBytes = kMaxSlots * sizeof(ClusterChunk);
+constexpr uint32_t kPartBytes = 2 * (kCWarps / 2) * kJobTok * kChunkRows * 4;  // shrink partials
+
+struct Slice {  // this CTA's input / output slice
+  uint32_t k0, kb, n0, nb;  // first element, width (elements; may be 0 for tiny widths)
+  __device__ Slice(const CArgs& p, uint32_t crank) {
+    k0 = min(crank * p.ks, p.d_in);
+    kb = min(p.ks, p.d_in - k0);
+    n0 = min(crank * p.ns, p.d_out);
+    nb = min(p.ns, p.d_out - n0);
+  }
+};
+
+// Shared-memory row stride of a slice row: 16 bytes of padding so the eight
+// rows an ldmatrix touches fall in different banks (unpadded 2 KiB rows put
+// all eight in the same bank: an 8-way conflict on every fragment load).
+__host__ __device__ constexpr uint32_t row_stride(uint32_t elems) { return elems * 2 + 16; }
+
+__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+__device__ __forceinline__ float dot8(const uint4 a, const uint4 b, float acc) {
+  acc = fmaf(bf_lo(a.x), bf_lo(b.x), acc);
+  acc = fmaf(bf_hi(a.x), bf_hi(b.x), acc);
+  acc = fmaf(bf_lo(a.y), bf_lo(b.y), acc);
+  acc = fmaf(bf_hi(a.y), bf_hi(b.y), acc);
+  acc = fmaf(bf_lo(a.z), bf_lo(b.z), acc);
+  acc = fmaf(bf_hi(a.z), bf_hi(b.z), acc);
+  acc = fmaf(bf_lo(a.w), bf_lo(b.w), acc);
+  acc = fmaf(bf_hi(a.w), bf_hi(b.w), acc);
+  return acc;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ---------------------------------------------------------------- producer
+// One page piece of a chunk's copies, resolved through the page table.
+struct Piece {
+  uint32_t phys;    // physical page (loaded from the device page table)
+  uint32_t inpage;  // byte offset inside the page
+  uint32_t dst;     // byte offset inside the ring slot
+  uint32_t len;     // bytes (0 = no piece)
+};
+
+struct Rec {  // chunk record fields (ClusterChunk), read from a smem ring
+  uint32_t table_off, rank, ntok, flags, row0, nrows;
+  __device__ explicit Rec(const uint32_t* w) {
+    table_off = w[0];
+    rank = w[1] & 0xffffu;
+    ntok = (w[1] >> 16) & 0xffu;
+    flags = w[1] >> 24;
+    row0 = w[2] & 0xffffu;
+    nrows = (w[2] >> 16) & 0xffu;
+  }
+};
+
+struct PieceGeom {
+  uint32_t KB, NB, KSB, NSB, pprA, pprB;
+};
+
+// Piece q of chunk `c` (A rows first, then Bᵀ rows): logical page, offset in
+// the page, destination in the slot, length (0 = no piece).
+__device__ __forceinline__ uint32_t piece_geom(const CArgs& p, const Slice& sl,
+                                               const PieceGeom& pg, const Rec& c, uint32_t q,
+                                               Piece& out) {
+  out.len = 0;
+  const uint32_t nA = c.nrows * pg.pprA;
+  if (q >= nA + c.nrows * pg.pprB) return 0;
+  const uint32_t L = p.log2_page;
+  const uint64_t a_base = static_cast<uint64_t>(c.rank) * p.blk_mult;  // elements
+  uint64_t lo;
+  uint32_t len, dst, k;
+  if (q < nA) {
+    const uint32_t r = q / pg.pprA;
+    k = q - r * pg.pprA;
+    lo = (a_base + static_cast<uint64_t>(c.row0 + r) * p.d_in + sl.k0) * 2;
+    len = pg.KB;
+    dst = r * pg.KSB;
+  } else {
+    const uint32_t qq = q - nA, r = qq / pg.pprB;
+    k = qq - r * pg.pprB;
+    lo = (a_base + static_cast<uint64_t>(c.rank) * p.d_in +
+          static_cast<uint64_t>(c.row0 + r) * p.d_out + sl.n0) * 2;
+    len = pg.NB;
+    dst = kChunkRows * pg.KSB + r * pg.NSB;
+  }
+  const uint64_t hi = lo + len, page = (lo >> L) + k;
+  const uint64_t a = max(lo, page << L), b = min(hi, (page + 1) << L);
+  if (a >= b) return 0;
+  out.inpage = static_cast<uint32_t>(a & ((1ull << L) - 1));
+  out.dst = dst + static_cast<uint32_t>(a - lo);
+  out.len = static_cast<uint32_t>(b - a);
+  return static_cast<uint32_t>(page);
+}
+
+__device__ __forceinline__ void cp_async_4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Producer lookahead, all through cp.async into two small smem rings so no
+// register ever waits on an in-flight load: at chunk i it fetches the record
+// of chunk i + 2·kAhead and the page-table entries of chunk i + kAhead, and
+// issues chunk i's bulk copies from entries fetched kAhead chunks earlier.
+// (Under a busy HBM a dependent global load takes ~1-1.5 µs.)
+constexpr int kAhead = 4;
+constexpr uint32_t kRecRing = 2 * kAhead;  // records, 32 bytes each
+constexpr uint32_t kRingBytes = kRecRing * 32 + kAhead * 32 * 4;
+
+// This lane's page piece of chunk c.  Aligned fast path (p.fast: every row
+// slice lies inside one page): producer warp pw owns rows 4·(pw&1) .. +3 of
+// the A (pw < 2) or Bᵀ (pw >= 2) block, lanes 0..3 one row each — a shift,
+// no division.  Generic path: pieces [8·pw, 8·pw + 8) of piece_geom's
+// enumeration on lanes 0..7 (the rest go through the small-page loop).
+__device__ __forceinline__ uint32_t my_piece(const CArgs& p, const Slice& sl, const PieceGeom& pg,
+                                             const Rec& c, uint32_t pw, uint32_t lane, Piece& x) {
+  x.len = 0;
+  if (p.fast) {
+    const uint32_t r = (pw & 1u) * 4 + lane;
+    if (lane >= 4 || r >= c.nrows) return 0;
+    const bool isb = pw >= 2;
+    const uint64_t lo =
+        (isb ? static_cast<uint64_t>(c.rank) * (p.blk_mult + p.d_in) +
+                   static_cast<uint64_t>(c.row0 + r) * p.d_out + sl.n0
+             : static_cast<uint64_t>(c.rank) * p.blk_mult +
+                   static_cast<uint64_t>(c.row0 + r) * p.d_in + sl.k0) * 2;
+    x.len = isb ? pg.NB : pg.KB;
+    x.dst = isb ? kChunkRows * pg.KSB + r * pg.NSB : r * pg.KSB;
+    x.inpage = static_cast<uint32_t>(lo & ((1ull << p.log2_page) - 1));
+    return static_cast<uint32_t>(lo >> p.log2_page);
+  }
+  if (lane >= 8) return 0;
+  return piece_geom(p, sl, pg, c, pw * 8 + lane, x);
+}
+
+// Producer warp pw of kPWarps: every warp waits for the slot and issues its
+// share of the chunk's page pieces (my_piece); warp 0 also publishes the
+// record, arms the barrier with the chunk's full byte count (peers' copies
+// may complete first: the phase also needs this arrival) and loads the job's
+// x / y rows.
+__device__ void producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl, uint32_t pw) {
+  const uint32_t lane = threadIdx.x & 31;
+  Bars bar(smem, p.off_bar);
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(smem + p.off_hdr);
+  uint32_t* recring = reinterpret_cast<uint32_t*>(smem + p.off_ring + pw * kRingBytes);  // [kRecRing][8]
+  uint32_t* tblring = recring + kRecRing * 8;                                           // [kAhead][32]
+  const uint32_t* recg = reinterpret_cast<const uint32_t*>(p.chunks);
+  const Slice sl(p, crank);
+  const uint64_t ef = ptx::policy_evict_first();
+  const uint32_t L = p.log2_page;
+  PieceGeom pg;
+  pg.KB = sl.kb * 2;
+  pg.NB = sl.nb * 2;
+  pg.KSB = row_stride(p.ks);
+  pg.NSB = row_stride(p.ns);
+  pg.pprA = pg.KB ? ((pg.KB - 1) >> L) + 2 : 0;  // page pieces per row (upper bound)
+  pg.pprB = pg.NB ? ((pg.NB - 1) >> L) + 2 : 0;
+  const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
+  const uint32_t n = i1 - i0;
+  auto fetch_rec = [&](uint32_t j) {  // 32-byte record of chunk j: lanes 0, 1 copy 16 bytes each
+    if (lane < 2 && j < n)
+      ptx::cp_async_16(recring + (j % kRecRing) * 8 + lane * 4, recg + (i0 + j) * 8 + lane * 4, 16);
+  };
+  auto fetch_tbl = [&](uint32_t j) {  // page-table entry of this lane's piece of chunk j
+    if (j >= n) return;
+    const Rec c(recring + (j % kRecRing) * 8);
+    Piece x;
+    const uint32_t page = my_piece(p, sl, pg, c, pw, lane, x);
+    if (x.len)
+      cp_async_4(ptx::smem_u32(tblring + (j % kAhead) * 32 + lane), p.table + c.table_off + page);
+  };
+  // prologue: records 0 .. 2·kAhead-1 (waited), table entries 0 .. kAhead-1 (one group each)
+  for (uint32_t j = 0; j < kRecRing; ++j) fetch_rec(j);
+  ptx::cp_async_commit();
+  cp_async_wait_group<0>();
+  __syncwarp();
+  for (uint32_t j = 0; j < static_cast<uint32_t>(kAhead); ++j) {
+    fetch_tbl(j);
+    ptx::cp_async_commit();
+  }
+  uint32_t jord = 0;
+  bool waited = false;
+#pragma unroll 1
+  for (uint32_t idx = 0; idx < n; ++idx) {
+    const uint32_t s = idx % p.slots, ph = (idx / p.slots) & 1u;
+    cp_async_wait_group<kAhead - 1>();  // table entries of idx, record of idx + kAhead
+    __syncwarp();
+    if (pw == 0 && lane == 0) trace_put(p, idx, 6);
+    const uint32_t* rw = recring + (idx % kRecRing) * 8;
+    const Rec c(rw);
+    char* sb = smem + s * p.slot_bytes;
+    Piece pc;
+    my_piece(p, sl, pg, c, pw, lane, pc);
+    const uint32_t phys = pc.len ? tblring[(idx % kAhead) * 32 + lane] : 0u;
+    // ---- issue chunk idx
+    if (pw == 0 && lane == 0) trace_put(p, idx, 4);
+    ptx::mbar_wait(&bar.empty[s], ph ^ 1u);
+    if (pw == 0 && lane == 0) trace_put(p, idx, 5);
+    if (pw == 0) {
+      if (lane < 8) hdr[s * 8 + lane] = rw[lane];  // the consumers read the record from here
+      if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.full[s], c.nrows * (pg.KB + pg.NB));
+    }
+    __syncwarp();
+    if (pc.len)
+      ptx::bulk_g2s_hint(sb + pc.dst, p.arena + (static_cast<uint64_t>(phys) << L) + pc.inpage,
+                         pc.len, &bar.full[s], ef);
+    if (!p.fast) {  // small pages: the pieces past the first 32, synchronous lookups
+      for (uint32_t q = 32 + pw * 32 + lane; q < c.nrows * (pg.pprA + pg.pprB); q += 32 * kPWarps) {
+        Piece x;
+        const uint32_t page = piece_geom(p, sl, pg, c, q, x);
+        if (x.len)
+          ptx::bulk_g2s_hint(sb + x.dst,
+                             p.arena + (static_cast<uint64_t>(__ldg(p.table + c.table_off + page)) << L) +
+                                 x.inpage,
+                             x.len, &bar.full[s], ef);
+      }
+    }
+    if (pw == 0 && (c.flags & kChunkFirst)) {  // the job's x / y slices, after the weights
+      const uint32_t jbuf = jord & 1u, jph = (jord >> 1) & 1u;
+      ++jord;
+      char* jb = smem + p.off_jb + jbuf * p.jb_bytes;
+      const uint32_t tokx = rw[4 + (lane & 3)];
+      ptx::mbar_wait(&bar.jempty[jbuf], jph ^ 1u);
+      if (!waited) {  // activations are written by earlier kernels in the stream
+        ptx::pdl_wait();
+        waited = true;
+      }
+      if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.jfull[jbuf], c.ntok * (pg.KB + pg.NB));
+      __syncwarp();
+      if (lane < c.ntok && pg.KB)
+        ptx::bulk_g2s(jb + lane * pg.KSB, p.x + tokx * p.x_stride_b + sl.k0 * 2, pg.KB,
+                      &bar.jfull[jbuf]);
+      else if (lane >= 16 && lane - 16 < c.ntok && pg.NB)
+        ptx::bulk_g2s(jb + kJobTok * pg.KSB + (lane - 16) * pg.NSB,
+                      p.y + tokx * p.y_stride_b + sl.n0 * 2, pg.NB, &bar.jfull[jbuf]);
+    }
+    // ---- lookahead: table entries of idx + kAhead (its record landed), record of
+    // idx + 2·kAhead into the ring slot idx just vacated
+    __syncwarp();
+    fetch_tbl(idx + kAhead);
+    fetch_rec(idx + kRecRing);
+    ptx::cp_async_commit();
+  }
+  cp_async_wait_group<0>();
+  if (pw == 0 && !waited) ptx::pdl_wait();
+}
+
+// ---------------------------------------------------------------- consumers
+// Two warp groups work on consecutive chunks at once (their latency chains
+// overlap instead of adding up); both contractions run on warp-level tensor
+// cores (M = tokens <= 4 is far below a tcgen05 tile and the kernel is
+// HBM-bound — the MMAs keep the instruction count per streamed byte low):
+//  shrink group (warps 0-3)  D[tok][row] = x[tok, slice] · W[row, slice]ᵀ,
+//      m16n8k16, x rows as A and the chunk's 8 A rows as B (ldmatrix), 16
+//      k-steps per warp; the 4 warp partials are summed in a fixed order and
+//      pushed into every cluster peer's exchange slot (st.async).
+//  expand group (warps 4-7)  Dᵀ[col][tok] += Bᵀ[row][col]ᵀ · v[tok][row]ᵀ,
+//      m16n8k8 with 16 output columns per MMA (Bᵀ fragments by
+//      ldmatrix.trans); v is split into bf16 hi + lo (~16 mantissa bits of
+//      the fp32 v) packed side by side in N, so one MMA applies both halves;
+//      accumulators stay in registers across a job.
+constexpr uint32_t kGroupWarps = kCWarps / 2;
+constexpr uint32_t kGroupThreads = kGroupWarps * 32;
+constexpr uint32_t kMaxTiles = 16;  // 16-column expand tiles per warp (ns <= 1024)
+
+__device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_t cl) {
+  const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t gq = lane >> 2, cc = lane & 3;
+  const Bars bar(smem, p.off_bar);
+  const Slice sl(p, crank);
+  const uint32_t KSB = row_stride(p.ks);
+  const uint32_t ksteps = (sl.kb + 15) / 16;  // the last one may be half (kb % 16 == 8)
+  const bool half_tail = (sl.kb & 15u) != 0;
+  const uint32_t xb0 = ptx::smem_u32(smem + p.off_xb);
+  float* part = reinterpret_cast<float*>(smem + p.off_part);  // [2][warp][tok][row]
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(smem + p.off_hdr);
+  const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
+  // ldmatrix lane addressing: A (x rows) = row (lane&7) + 8·((lane>>3)&1), k-half lane>>4
+  // (rows >= kJobTok alias row 0: their D rows are discarded); B (W rows, x4 =
+  // two k-steps) = row lane&7, k-quarter lane>>3
+  const uint32_t xrow = (lane & 7) + ((lane >> 3) & 1) * 8;
+  const uint32_t xoff = (xrow < kJobTok ? xrow : 0) * KSB + (lane >> 4) * 16;
+  const uint32_t woff = (lane & 7) * KSB + (lane >> 3) * 16;
+  uint32_t jord = 0xffffffffu;
+#pragma unroll 1
+  for (uint32_t i = i0; i < i1; ++i) {
+    const uint32_t idx = i - i0, s = idx % p.slots, e = idx % kX;
+    ptx::mbar_wait(&bar.full[s], (idx / p.slots) & 1u);
+    if (tid == 0) trace_put(p, idx, 0);
+    const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
+    const uint32_t ntok = ch->ntok;
+    if (ch->flags & kChunkFirst) {
+      ++jord;
+      ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);
+    }
+    // Arm this chunk's exchange barrier: CS CTAs × kChunkRows rows × ntok
+    // floats.  Peers' st.async may land before this (negative tx count is
+    // fine: the phase also needs this arrival).  Aliasing bound: a peer's
+    // shrink of chunk m needs its slot back, i.e. its expand of m - slots,
+    // i.e. our partial of m - slots, i.e. our slot of that chunk, i.e. our
+    // expand of m - 2·slots: kX >= 2·kMaxSlots keeps every live phase distinct.
+    if (tid == 0) ptx::mbar_arrive_expect_tx(&bar.xfull[e], p.cs * kChunkRows * ntok * 4);
+    const uint32_t xa = ptx::smem_u32(smem + p.off_jb + (jord & 1u) * p.jb_bytes) + xoff;
+    const uint32_t wa = ptx::smem_u32(smem + s * p.slot_bytes) + woff;
+    float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t k = 2 * w;
+#pragma unroll 2
+    for (; k + 1 < ksteps; k += 2 * kGroupWarps) {  // two k-steps per W fragment load
+      uint32_t a0[4], a1[4], b[4];
+      ptx::ldsm_x4(wa + k * 32, b);
+      ptx::ldsm_x4(xa + k * 32, a0);
+      ptx::ldsm_x4(xa + k * 32 + 32, a1);
+      if (half_tail && k + 1 == ksteps - 1) {  // k 8..15 of the last step lie past the slice
+        a1[2] = a1[3] = 0u;
+        b[3] = 0u;
+      }
+      const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
+      ptx::mma_bf16_16816(d0, a0, b0);
+      ptx::mma_bf16_16816(d1, a1, b1);
+    }
+    if (k < ksteps) {  // odd number of k-steps: the last one alone
+      uint32_t a0[4], b[4];
+      ptx::ldsm_x4(wa + k * 32, b);
+      ptx::ldsm_x4(xa + k * 32, a0);
+      if (half_tail) {
+        a0[2] = a0[3] = 0u;
+        b[1] = 0u;
+      }
+      const uint32_t b0[2] = {b[0], b[1]};
+      ptx::mma_bf16_16816(d0, a0, b0);
+    }
+    // d[0]/d[1] = (tok gq, rows 2cc, 2cc+1).  Partial buffers alternate by chunk
+    // parity: warp 0 reads buffer idx&1 before the next chunk's barrier, which
+    // every warp passes before writing that buffer again.
+    float* pb = part + (idx & 1u) * kGroupWarps * kJobTok * kChunkRows;
+    if (gq < kJobTok) {
+      float* pw = pb + (w * kJobTok + gq) * kChunkRows + 2 * cc;
+      pw[0] = d0[0] + d1[0];
+      pw[1] = d0[1] + d1[1];
+    }
+    ptx::named_bar_sync(2, kGroupThreads);  // partials written; slot A rows read
+    if (w == 0) {
+      if (lane < ntok * kChunkRows) {  // lane = tok · 8 + row: sum the warps, push
+        float v = 0.f;
+#pragma unroll
+        for (uint32_t ww = 0; ww < kGroupWarps; ++ww) v += pb[ww * kJobTok * kChunkRows + lane];
+        const uint32_t t = lane / kChunkRows, r = lane % kChunkRows;
+        const uint32_t local = xb0 + (e * kXSlotFloats + (t * kChunkRows + r) * kMaxCs + crank) * 4;
+        const uint32_t lbar = ptx::smem_u32(&bar.xfull[e]);
+        for (uint32_t dst = 0; dst < p.cs; ++dst)
+          ptx::st_async_b32(ptx::mapa(local, dst), __float_as_uint(v), ptx::mapa(lbar, dst));
+      }
+      if (lane == 0) {
+        trace_put(p, idx, 1);
+        ptx::mbar_arrive(&bar.empty[s]);  // shrink side of the slot is free
+      }
+    }
+  }
+}
+
+__device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_t cl) {
+  const uint32_t tid = threadIdx.x - kGroupThreads, w = tid >> 5, lane = tid & 31;
+  const uint32_t gq = lane >> 2, cc = lane & 3;
+  const Bars bar(smem, p.off_bar);
+  const Slice sl(p, crank);
+  const uint32_t NSB = row_stride(p.ns), KSB = row_stride(p.ks);
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(smem + p.off_hdr);
+  const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
+  // this warp's 16-column tiles [t0, t1) of the output slice
+  const uint32_t ntiles = sl.nb / 16, tpw = (ntiles + kGroupWarps - 1) / kGroupWarps;
+  const uint32_t t0 = w * tpw, t1 = min(t0 + tpw, ntiles);
+  const bool tail8 = (sl.nb & 15u) != 0 && w == kGroupWarps - 1;  // a last 8-column tile
+  ptx::pdl_wait();  // y is written below: the previous call must be complete
+  float acc[kMaxTiles + 1][4];
+  uint32_t jord = 0xffffffffu;
+#pragma unroll 1
+  for (uint32_t i = i0; i < i1; ++i) {
+    const uint32_t idx = i - i0, s = idx % p.slots, e = idx % kX;
+    ptx::mbar_wait(&bar.full[s], (idx / p.slots) & 1u);
+    const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
+    const uint32_t ntok = ch->ntok, nrows = ch->nrows, flags = ch->flags;
+    if (flags & kChunkFirst) {
+      ++jord;
+      ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);  // y rows of the job
+#pragma unroll
+      for (uint32_t t = 0; t <= kMaxTiles; ++t)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[t][q] = 0.f;
+    }
+    ptx::mbar_wait(&bar.xfull[e], (idx / kX) & 1u);
+    if (tid == 0) trace_put(p, idx, 2);
+    // B operand: N packs (token, part): column n = 2·tok + part holds the bf16
+    // hi (part 0) or lo (part 1) half of v[tok][row], so one MMA applies both
+    // halves and y[tok] = D[·][2·tok] + D[·][2·tok+1].  This lane supplies
+    // rows 2cc, 2cc+1 of column gq (tokens >= ntok, rows >= nrows are 0).
+    const uint32_t vt = gq >> 1;
+    float v0 = 0.f, v1 = 0.f;
+    if (vt < ntok) {
+      const float* xs = reinterpret_cast<const float*>(smem + p.off_xb) + e * kXSlotFloats;
+      const float4* s0 = reinterpret_cast<const float4*>(xs + (vt * kChunkRows + 2 * cc) * kMaxCs);
+      const float4* s1 = s0 + kMaxCs / 4;
+      float4 q0 = s0[0], q1 = s1[0];
+      v0 = (q0.x + q0.y) + (q0.z + q0.w);  // fixed summation order: deterministic
+      v1 = (q1.x + q1.y) + (q1.z + q1.w);
+      if (p.cs > 4) {
+        q0 = s0[1];
+        q1 = s1[1];
+        v0 += (q0.x + q0.y) + (q0.z + q0.w);
+        v1 += (q1.x + q1.y) + (q1.z + q1.w);
+      }
+      if (2 * cc >= nrows) v0 = 0.f;
+      if (2 * cc + 1 >= nrows) v1 = 0.f;
+    }
+    const uint32_t bhi = pack_bf16x2(v0, v1);
+    const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bhi));
+    const uint32_t bv = (gq & 1u) ? pack_bf16x2(v0 - hf.x, v1 - hf.y) : bhi;
+    // Bᵀ rows >= nrows of the slot are stale: mask their halves of the A fragment
+    const uint32_t amask =
+        (2 * cc < nrows ? 0x0000ffffu : 0u) | (2 * cc + 1 < nrows ? 0xffff0000u : 0u);
+    const char* brow = smem + s * p.slot_bytes + kChunkRows * KSB;
+    // ldmatrix.trans lane addressing: row (lane&7) of matrix lane>>3 = 8 columns
+    const uint32_t brow0 = ptx::smem_u32(brow + (lane & 7) * NSB);
+    const uint32_t baddr = brow0 + (lane >> 3) * 16;
+#pragma unroll
+    for (uint32_t g = 0; g < kMaxTiles; g += 2) {  // two 16-column tiles per ldmatrix.x4
+      if (t0 + g < t1) {
+        uint32_t a[4];  // a lone last tile also reads the next 16 columns: in-bounds, unused
+        ptx::ldsm_x4_trans(baddr + (t0 + g) * 32, a);
+#pragma unroll
+        for (uint32_t m = 0; m < 2; ++m) {
+          if (t0 + g + m < t1) {
+            const uint32_t af[2] = {a[2 * m] & amask, a[2 * m + 1] & amask};
+            ptx::mma_bf16_1688(acc[g + m], af, bv);
+          }
+        }
+      }
+    }
+    if (tail8) {  // a final 8-column tile (nb % 16 == 8): MMA rows 8..15 unused
+      uint32_t a[2];
+      ptx::ldsm_x2_trans(brow0 + ntiles * 32, a);
+      const uint32_t af[2] = {a[0] & amask, 0u};
+      ptx::mma_bf16_1688(acc[kMaxTiles], af, bv);
+    }
+    if ((flags & kChunkLast) && cc < ntok) {  // y[tok cc] += scale · (hi + lo), once per job
+      const char* yrow = smem + p.off_jb + (jord & 1u) * p.jb_bytes + kJobTok * KSB + cc * NSB;
+      char* yg = p.y + ch->tok[cc] * p.y_stride_b + static_cast<uint64_t>(sl.n0) * 2;
+      auto put = [&](uint32_t col, float v) {
+        const float o = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(yrow + col * 2));
+        *reinterpret_cast<__nv_bfloat16*>(yg + col * 2) = __float2bfloat16_rn(fmaf(p.scale, v, o));
+      };
+#pragma unroll
+      for (uint32_t t = 0; t < kMaxTiles; ++t) {
+        if (t0 + t < t1) {  // d0 + d1 = (col gq, tok cc), d2 + d3 = (col gq + 8, tok cc)
+          put((t0 + t) * 16 + gq, acc[t][0] + acc[t][1]);
+          put((t0 + t) * 16 + gq + 8, acc[t][2] + acc[t][3]);
+        }
+      }
+      if (tail8) put(ntiles * 16 + gq, acc[kMaxTiles][0] + acc[kMaxTiles][1]);
+    }
+    ptx::named_bar_sync(1, kGroupThreads);  // slot (and job buffer) reads done
+    if (tid == 0) {
+      trace_put(p, idx, 3);
+      ptx::mbar_arrive(&bar.empty[s]);
+      if (flags & kChunkLast) ptx::mbar_arrive(&bar.jempty[jord & 1u]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) bgmv_cluster_kernel(const CArgs p) {
+  extern __shared__ __align__(128) char smem[];
+  ptx::pdl_launch_dependents();  // the next call may start streaming its weights
+  const uint32_t crank = ptx::cluster_ctarank();
+  const uint32_t cl = blockIdx.x / p.cs;
+  if (threadIdx.x == 0) trace_put(p, kTraceChunks - 1, 6);
+  if (threadIdx.x == 0) {
+    Bars bar(smem, p.off_bar);
+    for (uint32_t s = 0; s < kMaxSlots; ++s) {
+      ptx::mbar_init(&bar.full[s], 1);
+      ptx::mbar_init(&bar.empty[s], 2);  // shrink group + expand group
+    }
+    for (int j = 0; j < 2; ++j) {
+      ptx::mbar_init(&bar.jfull[j], 1);
+      ptx::mbar_init(&bar.jempty[j], 1);
+    }
+    for (uint32_t e = 0; e < kX; ++e) ptx::mbar_init(&bar.xfull[e], 1);
+    ptx::fence_mbar_init();
+  }
+  ptx::cluster_sync();  // peers' exchange barriers are initialised before any st.async
+  if (threadIdx.x >= kCThreads)
+    producer(p, smem, crank, cl, (threadIdx.x - kCThreads) >> 5);
+  else if (threadIdx.x < kGroupThreads)
+    shrink_group(p, smem, crank, cl);
+  else
+    expand_group(p, smem, crank, cl);
+  ptx::cluster_sync();  // no CTA leaves while a peer may still address its smem
+  if (threadIdx.x == 0) trace_put(p, kTraceChunks - 1, 7);
+}
+
+std::mutex g_occ_mu;
+std::map<std::tuple<int, uint32_t, uint32_t>, int> g_occ;  // (device, cs, smem) -> clusters
+
+int max_clusters(int device, uint32_t cs, uint32_t smem) {
+  std::lock_guard<std::mutex> lk(g_occ_mu);
+  auto key = std::make_tuple(device, cs, smem);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) return it->second;
+  PLORA_CUDA(cudaFuncSetAttribute(bgmv_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBudget)));
+  int sms = 0;
+  PLORA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<uint32_t>(sms) / cs * cs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  PLORA_CUDA(cudaOccupancyMaxActiveClusters(&n, bgmv_cluster_kernel, &cfg));
+  if (n <= 0) throw CudaError("bgmv: no cluster of " + std::to_string(cs) + " CTAs fits");
+  g_occ[key] = n;
+  return n;
+}
+
+}  // namespace
+
+ClusterGeom cluster_geom(uint32_t d_in, uint32_t d_out, int device) {
+  ClusterGeom g;
+  auto slice = [](uint32_t d, uint32_t cs) { return ((d + cs - 1) / cs + 7) / 8 * 8; };
+  g.cs = 4;
+  while (std::max(slice(d_in, g.cs), slice(d_out, g.cs)) > kMaxSlice && g.cs < kMaxCs) g.cs *= 2;
+  g.ks = slice(d_in, g.cs);
+  g.ns = slice(d_out, g.cs);
+  if (g.ks > kMaxSlice || g.ns > kMaxSlice)  // expand: 4 columns per consumer thread
+    throw ValidationError("bf16 BGMV: d_in " + std::to_string(d_in) + " / d_out " +
+                          std::to_string(d_out) + " too wide (max " +
+                          std::to_string(kMaxSlice * kMaxCs) + ")");
+  auto up128 = [](uint32_t b) { return (b + 127) / 128 * 128; };
+  g.slot_bytes = up128(kChunkRows * (row_stride(g.ks) + row_stride(g.ns)));
+  g.jb_bytes = up128(kJobTok * (row_stride(g.ks) + row_stride(g.ns)));
+  const uint32_t fixed = 2 * g.jb_bytes + kX * kXSlotFloats * 4 + kBarBytes + kHdrBytes + kPartBytes + kPWarps * kRingBytes;
+  g.slots = fixed < kSmemBudget ? std::min<uint32_t>(kMaxSlots, (kSmemBudget - fixed) / g.slot_bytes) : 0;
+  if (g.slots < 3)
+    throw ValidationError("bf16 BGMV: d_in " + std::to_string(d_in) + " / d_out " +
+                          std::to_string(d_out) + " leave fewer than 3 ring slots");
+  g.smem = g.slots * g.slot_bytes + fixed;
+  g.n_clusters = static_cast<uint32_t>(max_clusters(device, g.cs, g.smem));
+  return g;
+}
+
+void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
+                         uint64_t x_stride, void* y, uint64_t y_stride, float scale,
+                         cudaStream_t stream) {
+  const plora_store& st = *plan.store;
+  const ModelGeom& gm = st.geom;
+  const ClusterWork& cw = plan.cwork[proj];
+  const ClusterGeom& g = cw.geom;
+  if (g.n_clusters == 0) return;  // no LoRA token in the batch
+  if (gm.m.d_in[proj] % 8 || gm.m.d_out[proj] % 8)
+    throw ValidationError("bf16 BGMV needs d_in and d_out multiples of 8");
+  CArgs a{};
+  a.arena = st.arena;
+  a.table = st.d_table;
+  a.chunks = plan.d_cchunks + cw.chunks_off;
+  a.cl_off = plan.d_ccl_off + cw.cl_off;
+  a.x = static_cast<const char*>(x);
+  a.y = static_cast<char*>(y);
+  a.x_stride_b = x_stride * 2;
+  a.y_stride_b = y_stride * 2;
+  a.blk_mult = gm.blk_mult(layer, proj);
+  a.log2_page = st.log2_page;
+  a.d_in = gm.m.d_in[proj];
+  a.d_out = gm.m.d_out[proj];
+  a.cs = g.cs;
+  a.ks = g.ks;
+  a.ns = g.ns;
+  a.slots = g.slots;
+  a.slot_bytes = g.slot_bytes;
+  a.jb_bytes = g.jb_bytes;
+  a.off_jb = g.slots * g.slot_bytes;
+  a.off_xb = a.off_jb + 2 * g.jb_bytes;
+  a.off_bar = a.off_xb + kX * kXSlotFloats * 4;
+  a.off_hdr = a.off_bar + kBarBytes;
+  a.off_part = a.off_hdr + kHdrBytes;
+  a.off_ring = a.off_part + kPartBytes;
+  a.scale = scale;
+  {
+    const uint64_t P = 1ull << st.log2_page;
+    a.fast = a.d_in % a.ks == 0 && a.d_out % a.ns == 0 && P % (2ull * a.ks) == 0 &&
+             P % (2ull * a.ns) == 0 && a.blk_mult % a.ks == 0 && (a.blk_mult + a.d_in) % a.ns == 0;
+  }
+  a.trace = trace_buffer(g.n_clusters * g.cs * kTraceChunks * 64);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.n_clusters * g.cs);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = g.cs;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  // programmatic dependent launch: this call's weight streaming may overlap
+  // the previous call's tail (activations are read after griddepcontrol.wait)
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_cluster_kernel, a));
+  count_launch();
+}
+
+}  // namespace plora
+
+extern "C" int plora_debug_plan_geom(const plora_plan* plan, uint32_t proj, uint32_t out[8]) {
+  using namespace plora;
+  return guard([&] {
+    if (!plan || !out) throw ValidationError("null plan or out");
+    if (proj >= PLORA_MAX_PROJ) throw ValidationError("proj out of range");
+    const ClusterWork& cw = plan->cwork[proj];
+    const ClusterGeom& g = cw.geom;
+    const uint32_t n = g.n_clusters ? plan->ccl_off[cw.cl_off + g.n_clusters] : 0;
+    const uint32_t v[8] = {g.cs, g.ks, g.ns, g.slots, g.slot_bytes, g.smem, g.n_clusters, n};
+    for (int i = 0; i < 8; ++i) out[i] = v[i];
+    return 0;
+  });
+}

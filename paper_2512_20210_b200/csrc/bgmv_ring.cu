@@ -463,6 +463,8 @@ uint64_t g_trace_bytes = 0;
 
 }  // namespace
 
+uint64_t* trace_buffer(uint64_t need_bytes) { return g_trace_bytes >= need_bytes ? g_trace : nullptr; }
+
 // Launch the bf16 decode op for one (layer, proj); see plora_bgmv.
 void launch_bgmv_ring(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
                       uint64_t x_stride, void* y, uint64_t y_stride, float scale,

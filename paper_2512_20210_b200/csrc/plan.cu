@@ -161,11 +161,74 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   }
   n_tiles = static_cast<uint32_t>(tiles.size());
 
-  // ---- upload units | tiles in one copy from a pinned staging buffer
+  // ---- bf16 BGMV on clusters: jobs (<= kJobTok tokens of one adapter),
+  // LPT-assigned to clusters by bytes, cut into kChunkRows-row chunks
+  cjobs.clear();
+  cchunks.clear();
+  ccl_off.clear();
+  if (es == 2) {
+    for (const Seg& s : segs)
+      for (uint32_t tc = 0; tc < s.toks.size(); tc += kJobTok) {
+        ClusterJob j{};
+        j.table_off = s.table_off;
+        j.rank = s.rank;
+        j.ntok = std::min<uint32_t>(kJobTok, static_cast<uint32_t>(s.toks.size()) - tc);
+        for (uint32_t t = 0; t < j.ntok; ++t) j.tok[t] = s.toks[tc + t];
+        cjobs.push_back(j);
+      }
+    const uint32_t nj = static_cast<uint32_t>(cjobs.size());
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) {
+      ClusterWork& cw = cwork[p];
+      cw = ClusterWork{};
+      if (nj == 0) continue;
+      const uint32_t din = g.m.d_in[p], dout = g.m.d_out[p];
+      cw.geom = cluster_geom(din, dout, st.device);
+      const uint32_t nc = std::min(cw.geom.n_clusters, nj);
+      cw.geom.n_clusters = nc;
+      // LPT: heaviest job first onto the least-loaded cluster (ties: lowest index)
+      std::vector<uint32_t> jo(nj);
+      std::iota(jo.begin(), jo.end(), 0u);
+      auto cost = [&](uint32_t j) {
+        return static_cast<uint64_t>(cjobs[j].rank + cjobs[j].ntok) * (din + dout);
+      };
+      std::stable_sort(jo.begin(), jo.end(), [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
+      std::vector<uint64_t> load(nc, 0);
+      std::vector<std::vector<uint32_t>> lists(nc);
+      for (uint32_t j : jo) {
+        const uint32_t c = static_cast<uint32_t>(std::min_element(load.begin(), load.end()) - load.begin());
+        load[c] += cost(j);
+        lists[c].push_back(j);
+      }
+      cw.chunks_off = static_cast<uint32_t>(cchunks.size());
+      cw.cl_off = static_cast<uint32_t>(ccl_off.size());
+      for (uint32_t c = 0; c < nc; ++c) {
+        ccl_off.push_back(static_cast<uint32_t>(cchunks.size()) - cw.chunks_off);
+        for (uint32_t j : lists[c])
+          for (uint32_t r0 = 0; r0 < cjobs[j].rank; r0 += kChunkRows) {
+            ClusterChunk ch{};
+            ch.table_off = cjobs[j].table_off;
+            ch.rank = static_cast<uint16_t>(cjobs[j].rank);
+            ch.ntok = static_cast<uint8_t>(cjobs[j].ntok);
+            for (uint32_t t = 0; t < kJobTok; ++t) ch.tok[t] = cjobs[j].tok[t];
+            ch.row0 = static_cast<uint16_t>(r0);
+            ch.nrows = static_cast<uint8_t>(std::min(kChunkRows, cjobs[j].rank - r0));
+            ch.flags = static_cast<uint8_t>((r0 == 0 ? kChunkFirst : 0) |
+                                            (r0 + kChunkRows >= cjobs[j].rank ? kChunkLast : 0));
+            cchunks.push_back(ch);
+          }
+      }
+      ccl_off.push_back(static_cast<uint32_t>(cchunks.size()) - cw.chunks_off);
+    }
+  }
+
+  // ---- upload units | tiles | cluster chunks | offsets in one copy
+  // from a pinned staging buffer
   auto align = [](uint64_t v) { return (v + 255) & ~255ull; };
   const uint64_t unit_b = align(units.size() * sizeof(BgmvUnit));
   const uint64_t tile_b = align(tiles.size() * sizeof(SgmvTile));
-  const uint64_t total = std::max<uint64_t>(unit_b + tile_b, 256);
+  const uint64_t cch_b = align(cchunks.size() * sizeof(ClusterChunk));
+  const uint64_t ccl_b = align(ccl_off.size() * sizeof(uint32_t));
+  const uint64_t total = std::max<uint64_t>(unit_b + tile_b + cch_b + ccl_b, 256);
   DeviceCtx ctx(st.device);
   if (upload_done) PLORA_CUDA(cudaEventSynchronize(upload_done));  // pinned buffer reuse
   if (h_cap < total) {
@@ -185,9 +248,15 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   }
   std::memcpy(h_pinned, units.data(), units.size() * sizeof(BgmvUnit));
   std::memcpy(h_pinned + unit_b, tiles.data(), tiles.size() * sizeof(SgmvTile));
+  std::memcpy(h_pinned + unit_b + tile_b, cchunks.data(),
+              cchunks.size() * sizeof(ClusterChunk));
+  std::memcpy(h_pinned + unit_b + tile_b + cch_b, ccl_off.data(),
+              ccl_off.size() * sizeof(uint32_t));
   d_units = reinterpret_cast<BgmvUnit*>(d_buf);
   d_tiles = reinterpret_cast<SgmvTile*>(d_buf + unit_b);
-  PLORA_CUDA(cudaMemcpyAsync(d_buf, h_pinned, unit_b + tile_b, cudaMemcpyHostToDevice, stream));
+  d_cchunks = reinterpret_cast<ClusterChunk*>(d_buf + unit_b + tile_b);
+  d_ccl_off = reinterpret_cast<uint32_t*>(d_buf + unit_b + tile_b + cch_b);
+  PLORA_CUDA(cudaMemcpyAsync(d_buf, h_pinned, total, cudaMemcpyHostToDevice, stream));
   if (!upload_done) PLORA_CUDA(cudaEventCreateWithFlags(&upload_done, cudaEventDisableTiming));
   PLORA_CUDA(cudaEventRecord(upload_done, stream));
 

@@ -91,6 +91,55 @@ struct ProjWork {
   uint32_t units_off = 0;  // into the unit array
 };
 
+// ------------------------------------------------ bf16 BGMV (clusters)
+// A job = one adapter's tokens (<= kJobTok of them) at one (layer, proj);
+// it is cut into chunks of <= kChunkRows rank rows.  Every CTA of a cluster
+// of CS CTAs walks the same chunk list, CTA c owning input slice c (shrink,
+// K-split) and output slice c (expand, N-split); partial v rows cross the
+// cluster through distributed shared memory.
+constexpr uint32_t kJobTok = 4;
+constexpr uint32_t kChunkRows = 8;
+constexpr uint32_t kChunkFirst = 1, kChunkLast = 2;
+
+struct ClusterJob {  // host-side only
+  uint32_t table_off;
+  uint32_t rank;
+  uint32_t ntok;
+  uint32_t tok[kJobTok];
+};
+
+// Self-contained chunk record (32 bytes): the kernel's producer loads it
+// ahead of time and forwards it to the consumers through shared memory, so
+// no consumer ever waits on a dependent global load.
+struct ClusterChunk {
+  uint32_t table_off;  // adapter's first entry in the device page table
+  uint16_t rank;
+  uint8_t ntok;
+  uint8_t flags;       // kChunkFirst | kChunkLast of the job
+  uint16_t row0;
+  uint8_t nrows;
+  uint8_t pad0;
+  uint32_t pad1;
+  uint32_t tok[kJobTok];  // x / y row of each job token
+};
+static_assert(sizeof(ClusterChunk) == 32, "ClusterChunk layout");
+
+// Launch geometry of one projection (host-side, decided at plan build).
+struct ClusterGeom {
+  uint32_t cs = 0;          // CTAs per cluster
+  uint32_t ks = 0, ns = 0;  // input / output slice widths (elements)
+  uint32_t slots = 0;       // ring depth
+  uint32_t slot_bytes = 0, jb_bytes = 0, smem = 0;
+  uint32_t n_clusters = 0;  // clusters launched (<= co-resident clusters)
+};
+ClusterGeom cluster_geom(uint32_t d_in, uint32_t d_out, int device);
+
+struct ClusterWork {
+  ClusterGeom geom;
+  uint32_t chunks_off = 0;  // into the chunk array
+  uint32_t cl_off = 0;      // into the cluster offset array (n_clusters + 1 entries)
+};
+
 // ---------------------------------------------------------------- SGMV
 // A run = maximal stretch of consecutive tokens with the same adapter
 // (Punica's seg_indptr formulation); tiles are 128-row slices of runs.
@@ -110,10 +159,16 @@ struct plora_plan {
   uint32_t max_rank = 0;
   uint64_t v_elems = 0;
   plora::ProjWork proj[PLORA_MAX_PROJ];
+  plora::ClusterWork cwork[PLORA_MAX_PROJ];
   uint32_t n_tiles = 0;
 
   std::vector<plora::BgmvUnit> units;
   std::vector<plora::SgmvTile> tiles;
+  std::vector<plora::ClusterJob> cjobs;
+  std::vector<plora::ClusterChunk> cchunks;
+  std::vector<uint32_t> ccl_off;
+  plora::ClusterChunk* d_cchunks = nullptr;
+  uint32_t* d_ccl_off = nullptr;
   char* h_pinned = nullptr;
   uint64_t h_cap = 0;
   char* d_buf = nullptr;
@@ -130,6 +185,12 @@ struct plora_plan {
 };
 
 namespace plora {
+// Diagnostics buffer set by plora_debug_set_trace (nullptr if absent or too small).
+uint64_t* trace_buffer(uint64_t need_bytes);
+// bf16 decode op (bgmv_cluster.cu): 4-CTA clusters, DSMEM exchange of v.
+void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
+                         uint64_t x_stride, void* y, uint64_t y_stride, float scale,
+                         cudaStream_t stream);
 // bf16 decode op (bgmv_ring.cu): persistent TMA ring + warp-level tensor cores.
 void launch_bgmv_ring(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
                       uint64_t x_stride, void* y, uint64_t y_stride, float scale,

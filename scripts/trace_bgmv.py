@@ -1,8 +1,17 @@
-"""Diagnostics: per-unit device timeline of one bf16 BGMV call (cfg2 shape).
+"""Diagnostics: launch geometry and per-chunk device timeline of one bf16
+BGMV call (cfg2 shape) on the cluster kernel.
 
-python scripts/trace_bgmv.py   (on a GPU box) -> prints latency / compute /
-idle statistics per unit kind and writes gpurun_out/trace_bgmv.npz.
+python scripts/trace_bgmv.py   (on a GPU box) -> prints the plan geometry,
+per-CTA chunk timings and writes gpurun_out/trace_bgmv.npz.
+
+Trace fields per (CTA, chunk k), SM clock cycles (shown as us at 1.965 GHz;
+comparable within a CTA only):
+  0 consumer: chunk data landed     1 consumer: partial v sent
+  2 consumer: exchange complete     3 consumer: expand done, slot released
+  4 producer: before slot wait      5 producer: slot free (issuing)
+  6 producer: lookahead landed      (k = 63: 6 CTA start, 7 CTA end)
 """
+import ctypes as C
 import os
 import sys
 
@@ -15,6 +24,8 @@ sys.path.insert(0, ROOT)
 from paper_2512_20210_b200 import _native as N, synth  # noqa: E402
 from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, bgmv  # noqa: E402
 
+K = 64
+
 
 def main():
     cfg = synth.cfg2(n_layers=2)
@@ -26,12 +37,16 @@ def main():
         store.publish(a)
     ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
     plan = BatchPlan(store, ta)
+    geom = (C.c_uint32 * 8)()
+    N.check(N.lib().plora_debug_plan_geom(plan.handle, 0, geom))
+    names = ("cs", "ks", "ns", "slots", "slot_bytes", "smem", "clusters", "chunks")
+    print("geometry:", dict(zip(names, list(geom))))
     x = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
     y = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
     for _ in range(3):
         bgmv(plan, 1, 0, x, y)
-    ctas, units = 148, 64
-    buf = torch.zeros(ctas * units * 8, dtype=torch.int64, device="cuda")
+    ctas = geom[0] * geom[6]
+    buf = torch.zeros(ctas * K * 8, dtype=torch.int64, device="cuda")
     N.check(N.lib().plora_debug_set_trace(buf.data_ptr(), buf.numel() * 8))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -40,46 +55,50 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     N.check(N.lib().plora_debug_set_trace(None, 0))
-    t = buf.view(ctas, units, 8).cpu().numpy().astype(np.int64)
-    issued, ready, done, kind = t[..., 0], t[..., 1], t[..., 2], t[..., 3]
-    top, prewait, postwait = t[..., 4], t[..., 5], t[..., 6]
-    valid = issued > 0
-    t0 = issued[valid].min()
-    print(f"call {e0.elapsed_time(e1) * 1e3:.1f} us (event), span {(done[valid].max() - t0) / 1e3:.1f} us")
-    exp = (kind >> 32) == 1
-    nbytes = kind & 0xffffffff
-    for name, m in (("shrink", valid & ~exp), ("expand", valid & exp)):
-        lat = (ready - issued)[m] / 1e3
-        comp = (done - ready)[m] / 1e3
-        print(f"{name}: n={m.sum()} bytes/unit={nbytes[m].mean():.0f} "
-              f"issue->ready med {np.median(lat):.2f} p90 {np.percentile(lat, 90):.2f} us; "
-              f"ready->done med {np.median(comp):.2f} p90 {np.percentile(comp, 90):.2f} us")
-    # consumer idle: time between done(k-1) and ready(k)
-    gaps = []
-    for c in range(ctas):
+    # untraced timing of the same call
+    for _ in range(3):
+        bgmv(plan, 1, 0, x, y)
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    for _ in range(20):
+        bgmv(plan, 1, 0, x, y)
+    e3.record()
+    torch.cuda.synchronize()
+    t = buf.view(ctas, K, 8).cpu().numpy().astype(np.int64)
+    start = t[:, K - 1, 6]
+    t0 = start.min()
+    t = (t / 1.965).astype(np.int64)  # cycles -> ns
+    start = t[:, K - 1, 6]
+    t0 = start.min()
+    rel = lambda v: (v - t0) / 1e3  # noqa: E731
+    print(f"call {e0.elapsed_time(e1) * 1e3:.1f} us traced; untraced {e2.elapsed_time(e3) * 1e3 / 20:.1f} "
+          f"us/call; CTA duration min/med/max {(t[:, K - 1, 7] - start).min() / 1e3:.1f}/"
+          f"{np.median(t[:, K - 1, 7] - start) / 1e3:.1f}/{(t[:, K - 1, 7] - start).max() / 1e3:.1f} us")
+    valid = t[..., 0] > 0
+    d_ready = np.diff(np.where(valid, t[..., 0], np.nan), axis=1) / 1e3
+    print(f"chunk-to-chunk (data ready) median {np.nanmedian(d_ready):.2f} us, p90 "
+          f"{np.nanpercentile(d_ready, 90):.2f}")
+    xch = (t[..., 2] - t[..., 1])[valid & (t[..., 2] > 0)] / 1e3
+    print(f"exchange wait (sent -> all partials, next iter) median {np.median(xch):.2f} us")
+    tstart = t[:, K - 1, 6].copy()
+    t[:, K - 1, :] = 0
+    wait_slot = (t[..., 5] - t[..., 4])[t[..., 4] > 0] / 1e3
+    m = (t[:, 1:, 6] > 0) & (t[:, :-1, 5] > 0)
+    work = (t[:, 1:, 6] - t[:, :-1, 5])[m] / 1e3
+    pre = (t[..., 4] - t[..., 6])[(t[..., 4] > 0) & (t[..., 6] > 0)] / 1e3
+    print(f"producer: issue work (slot free -> next lookahead landed) median {np.median(work):.2f} us; "
+          f"lookahead-landed -> slot wait start median {np.median(pre):.2f} us")
+    land = (t[..., 0] - t[..., 5])[(t[..., 0] > 0) & (t[..., 5] > 0)] / 1e3
+    print(f"data latency (issued -> consumer saw it) median {np.median(land):.2f} us")
+    print(f"producer slot wait median {np.median(wait_slot):.2f} us, p90 {np.percentile(wait_slot, 90):.2f}")
+    for c in (0, 1, 2, 3, ctas // 2):
         v = valid[c]
-        d, r = done[c][v], ready[c][v]
-        if len(d) > 1:
-            gaps.append(np.clip(r[1:] - d[:-1], 0, None).sum() / max(d[-1] - r[0], 1))
-    print(f"consumer waiting fraction (median over CTAs): {np.median(gaps):.2f}")
-    first_issue = (issued[:, 0] - t0) / 1e3
-    print(f"first issue per CTA: med {np.median(first_issue):.2f} max {first_issue.max():.2f} us")
-    end = np.array([done[c][valid[c]].max() - t0 for c in range(ctas) if valid[c].any()]) / 1e3
-    print(f"CTA end: min {end.min():.1f} med {np.median(end):.1f} max {end.max():.1f} us")
-    # issue lead: how far ahead of consumption the producer runs (units)
+        c0 = tstart[c]
+        rows = [tuple(round((z - c0) / 1e3, 2) for z in (t[c, k, 5], t[c, k, 0], t[c, k, 1], t[c, k, 2], t[c, k, 3]))
+                for k in range(K) if v[k]]
+        print(f"CTA {c} (issue, ready, sent, xchg, done) us:", rows[:20])
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    np.savez(os.path.join(ROOT, "gpurun_out", "trace_bgmv.npz"), trace=t)
-    for c in (0, 77):
-        v = valid[c]
-        rows = [tuple(int((z - t0) / 100) / 10 for z in (a, b, cc, d))
-                for a, b, cc, d in zip(top[c][v], prewait[c][v], postwait[c][v], issued[c][v])]
-        print(f"CTA {c} producer (loop top, pre-wait, post-wait, issued) us:", rows[:16])
-    for c in (0, 1, 77):
-        v = valid[c]
-        rows = [(int((i - t0) / 1e3 * 10) / 10, int((r - t0) / 1e3 * 10) / 10,
-                 int((d - t0) / 1e3 * 10) / 10, int(k >> 32))
-                for i, r, d, k in zip(issued[c][v], ready[c][v], done[c][v], kind[c][v])]
-        print(f"CTA {c}: (issue, ready, done, expand) us:", rows[:24])
+    np.savez(os.path.join(ROOT, "gpurun_out", "trace_bgmv.npz"), trace=t, geom=np.array(list(geom)))
 
 
 if __name__ == "__main__":
