@@ -42,10 +42,12 @@
 namespace plora {
 namespace {
 
-constexpr uint32_t kCWarps = kChunkRows;  // one consumer warp per chunk row
+constexpr uint32_t kSWarps = 4;  // shrink group
+constexpr uint32_t kEWarps = 8;  // expand group
+constexpr uint32_t kCWarps = kSWarps + kEWarps;
 constexpr uint32_t kCThreads = kCWarps * 32;
-constexpr uint32_t kPWarps = 4;                // producer warps (TMA issue is per-lane serial)
-constexpr uint32_t kThreads = kCThreads + kPWarps * 32;
+constexpr uint32_t kPWarps = 4;                // page producer warps (TMA issue is per-lane serial)
+constexpr uint32_t kThreads = kCThreads + (kPWarps + 1) * 32;  // + one control warp
 constexpr uint32_t kX = 16;                    // exchange slots (>= 2 · kMaxSlots, see shrink_group)
 constexpr uint32_t kMaxCs = 8;
 constexpr uint32_t kMaxSlots = 8;
@@ -97,7 +99,7 @@ struct Bars {
 };
 constexpr uint32_t kBarBytes = (2 * kMaxSlots + 4 + kX) * 8;
 constexpr uint32_t kHdrBytes = kMaxSlots * sizeof(ClusterChunk);
-constexpr uint32_t kPartBytes = 2 * (kCWarps / 2) * kJobTok * kChunkRows * 4;  // shrink partials
+constexpr uint32_t kPartBytes = 2 * kSWarps * kJobTok * kChunkRows * 4;  // shrink partials
 
 struct Slice {  // this CTA's input / output slice
   uint32_t k0, kb, n0, nb;  // first element, width (elements; may be 0 for tiny widths)
@@ -238,15 +240,13 @@ __device__ __forceinline__ uint32_t my_piece(const CArgs& p, const Slice& sl, co
   return piece_geom(p, sl, pg, c, pw * 8 + lane, x);
 }
 
-// Producer warp pw of kPWarps: every warp waits for the slot and issues its
-// share of the chunk's page pieces (my_piece); warp 0 also publishes the
-// record, arms the barrier with the chunk's full byte count (peers' copies
-// may complete first: the phase also needs this arrival) and loads the job's
-// x / y rows.
-__device__ void producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl, uint32_t pw) {
+// Page warp pw of kPWarps: waits for the slot, issues its share of the
+// chunk's page pieces (my_piece) and arms the chunk barrier with exactly its
+// own bytes (arrive.expect_tx after the copies: the phase cannot complete
+// before this warp's arrival, so the order is safe).
+__device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl, uint32_t pw) {
   const uint32_t lane = threadIdx.x & 31;
   Bars bar(smem, p.off_bar);
-  uint32_t* hdr = reinterpret_cast<uint32_t*>(smem + p.off_hdr);
   uint32_t* recring = reinterpret_cast<uint32_t*>(smem + p.off_ring + pw * kRingBytes);  // [kRecRing][8]
   uint32_t* tblring = recring + kRecRing * 8;                                           // [kAhead][32]
   const uint32_t* recg = reinterpret_cast<const uint32_t*>(p.chunks);
@@ -283,29 +283,21 @@ __device__ void producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl
     fetch_tbl(j);
     ptx::cp_async_commit();
   }
-  uint32_t jord = 0;
-  bool waited = false;
 #pragma unroll 1
   for (uint32_t idx = 0; idx < n; ++idx) {
     const uint32_t s = idx % p.slots, ph = (idx / p.slots) & 1u;
     cp_async_wait_group<kAhead - 1>();  // table entries of idx, record of idx + kAhead
     __syncwarp();
     if (pw == 0 && lane == 0) trace_put(p, idx, 6);
-    const uint32_t* rw = recring + (idx % kRecRing) * 8;
-    const Rec c(rw);
+    const Rec c(recring + (idx % kRecRing) * 8);
     char* sb = smem + s * p.slot_bytes;
     Piece pc;
     my_piece(p, sl, pg, c, pw, lane, pc);
     const uint32_t phys = pc.len ? tblring[(idx % kAhead) * 32 + lane] : 0u;
-    // ---- issue chunk idx
     if (pw == 0 && lane == 0) trace_put(p, idx, 4);
     ptx::mbar_wait(&bar.empty[s], ph ^ 1u);
     if (pw == 0 && lane == 0) trace_put(p, idx, 5);
-    if (pw == 0) {
-      if (lane < 8) hdr[s * 8 + lane] = rw[lane];  // the consumers read the record from here
-      if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.full[s], c.nrows * (pg.KB + pg.NB));
-    }
-    __syncwarp();
+    uint32_t bytes = pc.len;
     if (pc.len)
       ptx::bulk_g2s_hint(sb + pc.dst, p.arena + (static_cast<uint64_t>(phys) << L) + pc.inpage,
                          pc.len, &bar.full[s], ef);
@@ -313,41 +305,86 @@ __device__ void producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl
       for (uint32_t q = 32 + pw * 32 + lane; q < c.nrows * (pg.pprA + pg.pprB); q += 32 * kPWarps) {
         Piece x;
         const uint32_t page = piece_geom(p, sl, pg, c, q, x);
-        if (x.len)
+        if (x.len) {
           ptx::bulk_g2s_hint(sb + x.dst,
                              p.arena + (static_cast<uint64_t>(__ldg(p.table + c.table_off + page)) << L) +
                                  x.inpage,
                              x.len, &bar.full[s], ef);
+          bytes += x.len;
+        }
       }
     }
-    if (pw == 0 && (c.flags & kChunkFirst)) {  // the job's x / y slices, after the weights
-      const uint32_t jbuf = jord & 1u, jph = (jord >> 1) & 1u;
-      ++jord;
-      char* jb = smem + p.off_jb + jbuf * p.jb_bytes;
-      const uint32_t tokx = rw[4 + (lane & 3)];
-      ptx::mbar_wait(&bar.jempty[jbuf], jph ^ 1u);
-      if (!waited) {  // activations are written by earlier kernels in the stream
-        ptx::pdl_wait();
-        waited = true;
-      }
-      if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.jfull[jbuf], c.ntok * (pg.KB + pg.NB));
-      __syncwarp();
-      if (lane < c.ntok && pg.KB)
-        ptx::bulk_g2s(jb + lane * pg.KSB, p.x + tokx * p.x_stride_b + sl.k0 * 2, pg.KB,
-                      &bar.jfull[jbuf]);
-      else if (lane >= 16 && lane - 16 < c.ntok && pg.NB)
-        ptx::bulk_g2s(jb + kJobTok * pg.KSB + (lane - 16) * pg.NSB,
-                      p.y + tokx * p.y_stride_b + sl.n0 * 2, pg.NB, &bar.jfull[jbuf]);
-    }
+    bytes = __reduce_add_sync(0xffffffffu, bytes);
+    if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.full[s], bytes);
     // ---- lookahead: table entries of idx + kAhead (its record landed), record of
     // idx + 2·kAhead into the ring slot idx just vacated
-    __syncwarp();
     fetch_tbl(idx + kAhead);
     fetch_rec(idx + kRecRing);
     ptx::cp_async_commit();
   }
   cp_async_wait_group<0>();
-  if (pw == 0 && !waited) ptx::pdl_wait();
+}
+
+// Control warp: publishes each chunk's record in the slot header (its arrival
+// on the chunk barrier releases it to the consumers) and, at a job's first
+// chunk, loads the job's x / y slices — after griddepcontrol.wait, since the
+// activations are written by earlier kernels in the stream.
+__device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl) {
+  const uint32_t lane = threadIdx.x & 31;
+  Bars bar(smem, p.off_bar);
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(smem + p.off_hdr);
+  uint32_t* recring = reinterpret_cast<uint32_t*>(smem + p.off_ring + kPWarps * kRingBytes);
+  const uint32_t* recg = reinterpret_cast<const uint32_t*>(p.chunks);
+  const Slice sl(p, crank);
+  const uint32_t KB = sl.kb * 2, NB = sl.nb * 2, KSB = row_stride(p.ks), NSB = row_stride(p.ns);
+  const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
+  const uint32_t n = i1 - i0;
+  auto fetch_rec = [&](uint32_t j) {
+    if (lane < 2 && j < n)
+      ptx::cp_async_16(recring + (j % kRecRing) * 8 + lane * 4, recg + (i0 + j) * 8 + lane * 4, 16);
+  };
+  for (uint32_t j = 0; j < kAhead; ++j) {
+    fetch_rec(j);
+    ptx::cp_async_commit();
+  }
+  uint32_t jord = 0;
+  bool waited = false;
+#pragma unroll 1
+  for (uint32_t idx = 0; idx < n; ++idx) {
+    const uint32_t s = idx % p.slots, ph = (idx / p.slots) & 1u;
+    cp_async_wait_group<kAhead - 1>();
+    __syncwarp();
+    const uint32_t* rw = recring + (idx % kRecRing) * 8;
+    const Rec c(rw);
+    const uint32_t w = lane < 8 ? rw[lane] : 0u;
+    ptx::mbar_wait(&bar.empty[s], ph ^ 1u);
+    if (lane < 8) hdr[s * 8 + lane] = w;  // the consumers read the record from here
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&bar.full[s]);
+    if (c.flags & kChunkFirst) {  // the job's x / y slices
+      const uint32_t jbuf = jord & 1u, jph = (jord >> 1) & 1u;
+      ++jord;
+      char* jb = smem + p.off_jb + jbuf * p.jb_bytes;
+      const uint32_t tokx = rw[4 + (lane & 3)];
+      ptx::mbar_wait(&bar.jempty[jbuf], jph ^ 1u);
+      if (!waited) {
+        ptx::pdl_wait();
+        waited = true;
+      }
+      if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.jfull[jbuf], c.ntok * (KB + NB));
+      __syncwarp();
+      if (lane < c.ntok && KB)
+        ptx::bulk_g2s(jb + lane * KSB, p.x + tokx * p.x_stride_b + sl.k0 * 2, KB, &bar.jfull[jbuf]);
+      else if (lane >= 16 && lane - 16 < c.ntok && NB)
+        ptx::bulk_g2s(jb + kJobTok * KSB + (lane - 16) * NSB, p.y + tokx * p.y_stride_b + sl.n0 * 2,
+                      NB, &bar.jfull[jbuf]);
+    }
+    __syncwarp();
+    fetch_rec(idx + kAhead);
+    ptx::cp_async_commit();
+  }
+  cp_async_wait_group<0>();
+  if (!waited) ptx::pdl_wait();
 }
 
 // ---------------------------------------------------------------- consumers
@@ -359,14 +396,14 @@ __device__ void producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl
 //      m16n8k16, x rows as A and the chunk's 8 A rows as B (ldmatrix), 16
 //      k-steps per warp; the 4 warp partials are summed in a fixed order and
 //      pushed into every cluster peer's exchange slot (st.async).
-//  expand group (warps 4-7)  Dᵀ[col][tok] += Bᵀ[row][col]ᵀ · v[tok][row]ᵀ,
+//  expand group (warps 4-11)  Dᵀ[col][tok] += Bᵀ[row][col]ᵀ · v[tok][row]ᵀ,
 //      m16n8k8 with 16 output columns per MMA (Bᵀ fragments by
 //      ldmatrix.trans); v is split into bf16 hi + lo (~16 mantissa bits of
 //      the fp32 v) packed side by side in N, so one MMA applies both halves;
 //      accumulators stay in registers across a job.
-constexpr uint32_t kGroupWarps = kCWarps / 2;
-constexpr uint32_t kGroupThreads = kGroupWarps * 32;
-constexpr uint32_t kMaxTiles = 16;  // 16-column expand tiles per warp (ns <= 1024)
+constexpr uint32_t kSThreads = kSWarps * 32;
+constexpr uint32_t kEThreads = kEWarps * 32;
+constexpr uint32_t kMaxTiles = 1024 / 16 / kEWarps;  // 16-column expand tiles per warp (ns <= 1024)
 
 __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_t cl) {
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
@@ -410,7 +447,7 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
     uint32_t k = 2 * w;
 #pragma unroll 2
-    for (; k + 1 < ksteps; k += 2 * kGroupWarps) {  // two k-steps per W fragment load
+    for (; k + 1 < ksteps; k += 2 * kSWarps) {  // two k-steps per W fragment load
       uint32_t a0[4], a1[4], b[4];
       ptx::ldsm_x4(wa + k * 32, b);
       ptx::ldsm_x4(xa + k * 32, a0);
@@ -437,18 +474,18 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     // d[0]/d[1] = (tok gq, rows 2cc, 2cc+1).  Partial buffers alternate by chunk
     // parity: warp 0 reads buffer idx&1 before the next chunk's barrier, which
     // every warp passes before writing that buffer again.
-    float* pb = part + (idx & 1u) * kGroupWarps * kJobTok * kChunkRows;
+    float* pb = part + (idx & 1u) * kSWarps * kJobTok * kChunkRows;
     if (gq < kJobTok) {
       float* pw = pb + (w * kJobTok + gq) * kChunkRows + 2 * cc;
       pw[0] = d0[0] + d1[0];
       pw[1] = d0[1] + d1[1];
     }
-    ptx::named_bar_sync(2, kGroupThreads);  // partials written; slot A rows read
+    ptx::named_bar_sync(2, kSThreads);  // partials written; slot A rows read
     if (w == 0) {
       if (lane < ntok * kChunkRows) {  // lane = tok · 8 + row: sum the warps, push
         float v = 0.f;
 #pragma unroll
-        for (uint32_t ww = 0; ww < kGroupWarps; ++ww) v += pb[ww * kJobTok * kChunkRows + lane];
+        for (uint32_t ww = 0; ww < kSWarps; ++ww) v += pb[ww * kJobTok * kChunkRows + lane];
         const uint32_t t = lane / kChunkRows, r = lane % kChunkRows;
         const uint32_t local = xb0 + (e * kXSlotFloats + (t * kChunkRows + r) * kMaxCs + crank) * 4;
         const uint32_t lbar = ptx::smem_u32(&bar.xfull[e]);
@@ -464,7 +501,7 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
 }
 
 __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_t cl) {
-  const uint32_t tid = threadIdx.x - kGroupThreads, w = tid >> 5, lane = tid & 31;
+  const uint32_t tid = threadIdx.x - kSThreads, w = tid >> 5, lane = tid & 31;
   const uint32_t gq = lane >> 2, cc = lane & 3;
   const Bars bar(smem, p.off_bar);
   const Slice sl(p, crank);
@@ -472,9 +509,9 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   const uint32_t* hdr = reinterpret_cast<const uint32_t*>(smem + p.off_hdr);
   const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
   // this warp's 16-column tiles [t0, t1) of the output slice
-  const uint32_t ntiles = sl.nb / 16, tpw = (ntiles + kGroupWarps - 1) / kGroupWarps;
+  const uint32_t ntiles = sl.nb / 16, tpw = (ntiles + kEWarps - 1) / kEWarps;
   const uint32_t t0 = w * tpw, t1 = min(t0 + tpw, ntiles);
-  const bool tail8 = (sl.nb & 15u) != 0 && w == kGroupWarps - 1;  // a last 8-column tile
+  const bool tail8 = (sl.nb & 15u) != 0 && w == kEWarps - 1;  // a last 8-column tile
   ptx::pdl_wait();  // y is written below: the previous call must be complete
   float acc[kMaxTiles + 1][4];
   uint32_t jord = 0xffffffffu;
@@ -562,7 +599,7 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
       }
       if (tail8) put(ntiles * 16 + gq, acc[kMaxTiles][0] + acc[kMaxTiles][1]);
     }
-    ptx::named_bar_sync(1, kGroupThreads);  // slot (and job buffer) reads done
+    ptx::named_bar_sync(1, kEThreads);  // slot (and job buffer) reads done
     if (tid == 0) {
       trace_put(p, idx, 3);
       ptx::mbar_arrive(&bar.empty[s]);
@@ -580,7 +617,7 @@ __global__ void __launch_bounds__(kThreads, 1) bgmv_cluster_kernel(const CArgs p
   if (threadIdx.x == 0) {
     Bars bar(smem, p.off_bar);
     for (uint32_t s = 0; s < kMaxSlots; ++s) {
-      ptx::mbar_init(&bar.full[s], 1);
+      ptx::mbar_init(&bar.full[s], kPWarps + 1);  // page warps + control warp
       ptx::mbar_init(&bar.empty[s], 2);  // shrink group + expand group
     }
     for (int j = 0; j < 2; ++j) {
@@ -591,9 +628,11 @@ __global__ void __launch_bounds__(kThreads, 1) bgmv_cluster_kernel(const CArgs p
     ptx::fence_mbar_init();
   }
   ptx::cluster_sync();  // peers' exchange barriers are initialised before any st.async
-  if (threadIdx.x >= kCThreads)
-    producer(p, smem, crank, cl, (threadIdx.x - kCThreads) >> 5);
-  else if (threadIdx.x < kGroupThreads)
+  if (threadIdx.x >= kCThreads + kPWarps * 32)
+    control_producer(p, smem, crank, cl);
+  else if (threadIdx.x >= kCThreads)
+    page_producer(p, smem, crank, cl, (threadIdx.x - kCThreads) >> 5);
+  else if (threadIdx.x < kSThreads)
     shrink_group(p, smem, crank, cl);
   else
     expand_group(p, smem, crank, cl);
@@ -647,7 +686,7 @@ ClusterGeom cluster_geom(uint32_t d_in, uint32_t d_out, int device) {
   auto up128 = [](uint32_t b) { return (b + 127) / 128 * 128; };
   g.slot_bytes = up128(kChunkRows * (row_stride(g.ks) + row_stride(g.ns)));
   g.jb_bytes = up128(kJobTok * (row_stride(g.ks) + row_stride(g.ns)));
-  const uint32_t fixed = 2 * g.jb_bytes + kX * kXSlotFloats * 4 + kBarBytes + kHdrBytes + kPartBytes + kPWarps * kRingBytes;
+  const uint32_t fixed = 2 * g.jb_bytes + kX * kXSlotFloats * 4 + kBarBytes + kHdrBytes + kPartBytes + (kPWarps + 1) * kRingBytes;
   g.slots = fixed < kSmemBudget ? std::min<uint32_t>(kMaxSlots, (kSmemBudget - fixed) / g.slot_bytes) : 0;
   if (g.slots < 3)
     throw ValidationError("bf16 BGMV: d_in " + std::to_string(d_in) + " / d_out " +
