@@ -80,7 +80,7 @@ __device__ __forceinline__ uint64_t now_ns() {  // SM cycles (cheap; %globaltime
   return clock64();
 }
 __device__ __forceinline__ void trace_put(const CArgs& p, uint32_t k, int field) {
-  if (p.trace && k < kTraceChunks) p.trace[(blockIdx.x * kTraceChunks + k) * 8 + field] = now_ns();
+  if (p.trace && k < kTraceChunks) p.trace[(blockIdx.x * kTraceChunks + k) * 16 + field] = now_ns();
 }
 
 struct Bars {
@@ -314,6 +314,7 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
         }
       }
     }
+    if (pw == 0 && lane == 0) trace_put(p, idx, 12);
     bytes = __reduce_add_sync(0xffffffffu, bytes);
     if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.full[s], bytes);
     // ---- lookahead: table entries of idx + kAhead (its record landed), record of
@@ -360,7 +361,10 @@ __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uin
     ptx::mbar_wait(&bar.empty[s], ph ^ 1u);
     if (lane < 8) hdr[s * 8 + lane] = w;  // the consumers read the record from here
     __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&bar.full[s]);
+    if (lane == 0) {
+      ptx::mbar_arrive(&bar.full[s]);
+      trace_put(p, idx, 13);
+    }
     if (c.flags & kChunkFirst) {  // the job's x / y slices
       const uint32_t jbuf = jord & 1u, jph = (jord >> 1) & 1u;
       ++jord;
@@ -427,6 +431,7 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
 #pragma unroll 1
   for (uint32_t i = i0; i < i1; ++i) {
     const uint32_t idx = i - i0, s = idx % p.slots, e = idx % kX;
+    if (tid == 0) trace_put(p, idx, 14);
     ptx::mbar_wait(&bar.full[s], (idx / p.slots) & 1u);
     if (tid == 0) trace_put(p, idx, 0);
     const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
@@ -442,6 +447,7 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     // i.e. our partial of m - slots, i.e. our slot of that chunk, i.e. our
     // expand of m - 2·slots: kX >= 2·kMaxSlots keeps every live phase distinct.
     if (tid == 0) ptx::mbar_arrive_expect_tx(&bar.xfull[e], p.cs * kChunkRows * ntok * 4);
+    if (tid == 0) trace_put(p, idx, 15);
     const uint32_t xa = ptx::smem_u32(smem + p.off_jb + (jord & 1u) * p.jb_bytes) + xoff;
     const uint32_t wa = ptx::smem_u32(smem + s * p.slot_bytes) + woff;
     float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
@@ -480,7 +486,9 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
       pw[0] = d0[0] + d1[0];
       pw[1] = d0[1] + d1[1];
     }
+    if (tid == 0) trace_put(p, idx, 8);
     ptx::named_bar_sync(2, kSThreads);  // partials written; slot A rows read
+    if (tid == 0) trace_put(p, idx, 9);
     if (w == 0) {
       if (lane < ntok * kChunkRows) {  // lane = tok · 8 + row: sum the warps, push
         float v = 0.f;
@@ -556,6 +564,7 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     const uint32_t bhi = pack_bf16x2(v0, v1);
     const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bhi));
     const uint32_t bv = (gq & 1u) ? pack_bf16x2(v0 - hf.x, v1 - hf.y) : bhi;
+    if (tid == 0) trace_put(p, idx, 10);
     // Bᵀ rows >= nrows of the slot are stale: mask their halves of the A fragment
     const uint32_t amask =
         (2 * cc < nrows ? 0x0000ffffu : 0u) | (2 * cc + 1 < nrows ? 0xffff0000u : 0u);
@@ -583,6 +592,7 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
       const uint32_t af[2] = {a[0] & amask, 0u};
       ptx::mma_bf16_1688(acc[kMaxTiles], af, bv);
     }
+    if (tid == 0) trace_put(p, idx, 11);
     if ((flags & kChunkLast) && cc < ntok) {  // y[tok cc] += scale · (hi + lo), once per job
       const char* yrow = smem + p.off_jb + (jord & 1u) * p.jb_bytes + kJobTok * KSB + cc * NSB;
       char* yg = p.y + ch->tok[cc] * p.y_stride_b + static_cast<uint64_t>(sl.n0) * 2;
@@ -737,7 +747,7 @@ void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, 
     a.fast = a.d_in % a.ks == 0 && a.d_out % a.ns == 0 && P % (2ull * a.ks) == 0 &&
              P % (2ull * a.ns) == 0 && a.blk_mult % a.ks == 0 && (a.blk_mult + a.d_in) % a.ns == 0;
   }
-  a.trace = trace_buffer(g.n_clusters * g.cs * kTraceChunks * 64);
+  a.trace = trace_buffer(g.n_clusters * g.cs * kTraceChunks * 128);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g.n_clusters * g.cs);
   cfg.blockDim = dim3(kThreads);

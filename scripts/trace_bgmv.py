@@ -10,6 +10,9 @@ comparable within a CTA only):
   2 consumer: exchange complete     3 consumer: expand done, slot released
   4 producer: before slot wait      5 producer: slot free (issuing)
   6 producer: lookahead landed      (k = 63: 6 CTA start, 7 CTA end)
+  8 shrink: MMAs done   9 shrink: partial barrier passed   10 expand: v built
+  11 expand: MMAs done  12 page warp 0: copies issued      13 control: header out
+  14 shrink: before the chunk wait  15 shrink: job x landed, barrier armed
 """
 import ctypes as C
 import os
@@ -46,7 +49,7 @@ def main():
     for _ in range(3):
         bgmv(plan, 1, 0, x, y)
     ctas = geom[0] * geom[6]
-    buf = torch.zeros(ctas * K * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(ctas * K * 16, dtype=torch.int64, device="cuda")
     N.check(N.lib().plora_debug_set_trace(buf.data_ptr(), buf.numel() * 8))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -64,7 +67,7 @@ def main():
         bgmv(plan, 1, 0, x, y)
     e3.record()
     torch.cuda.synchronize()
-    t = buf.view(ctas, K, 8).cpu().numpy().astype(np.int64)
+    t = buf.view(ctas, K, 16).cpu().numpy().astype(np.int64)
     start = t[:, K - 1, 6]
     t0 = start.min()
     t = (t / 1.965).astype(np.int64)  # cycles -> ns
@@ -91,6 +94,13 @@ def main():
     land = (t[..., 0] - t[..., 5])[(t[..., 0] > 0) & (t[..., 5] > 0)] / 1e3
     print(f"data latency (issued -> consumer saw it) median {np.median(land):.2f} us")
     print(f"producer slot wait median {np.median(wait_slot):.2f} us, p90 {np.percentile(wait_slot, 90):.2f}")
+    def med(a, b):
+        m = (t[..., a] > 0) & (t[..., b] > 0)
+        return np.median((t[..., b] - t[..., a])[m]) / 1e3
+    print(f"shrink: wait {med(14, 0):.2f} | hdr->x ready {med(0, 15):.2f} | MMAs {med(15, 8):.2f} | barrier {med(8, 9):.2f} | "
+          f"sum+send {med(9, 1):.2f} us")
+    print(f"expand: xchg->v built {med(2, 10):.2f} | MMAs {med(10, 11):.2f} | y+barrier {med(11, 3):.2f} us")
+    print(f"page warp 0: slot free -> issued {med(5, 12):.2f} us; control: header after slot free {med(5, 13):.2f}")
     for c in (0, 1, 2, 3, ctas // 2):
         v = valid[c]
         c0 = tstart[c]
