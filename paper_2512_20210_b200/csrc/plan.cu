@@ -269,6 +269,29 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     v_cap = std::max<uint64_t>(v_elems, 4096);
     PLORA_CUDA(cudaMalloc(&d_v, v_cap * sizeof(float)));
   }
+  if (es == 2 && n_tiles > 0) {  // SGMV workspaces (see sgmv.cu)
+    uint64_t parts = 0;
+    for (uint32_t p = 0; p < g.m.n_proj; ++p)
+      parts = std::max<uint64_t>(parts, sgmv_splits(n_tiles, g.m.d_in[p]));
+    const uint64_t need_part = parts * n_tiles * 128ull * 128ull;
+    const uint64_t need_vbuf = n_tiles * 128ull * 128ull * 2ull;
+    if (vpart_cap < need_part || vbuf_cap < need_vbuf || tcnt_cap < n_tiles) {
+      PLORA_CUDA(cudaStreamSynchronize(stream));
+      cudaFree(d_vpart);
+      cudaFree(d_vbuf);
+      cudaFree(d_tcnt);
+      d_vpart = nullptr;
+      d_vbuf = nullptr;
+      d_tcnt = nullptr;
+      vpart_cap = need_part;
+      vbuf_cap = need_vbuf;
+      tcnt_cap = std::max<uint64_t>(n_tiles, 256);
+      PLORA_CUDA(cudaMalloc(&d_vpart, vpart_cap * sizeof(float)));
+      PLORA_CUDA(cudaMalloc(&d_vbuf, vbuf_cap));
+      PLORA_CUDA(cudaMalloc(&d_tcnt, tcnt_cap * sizeof(uint32_t)));
+      PLORA_CUDA(cudaMemsetAsync(d_tcnt, 0, tcnt_cap * sizeof(uint32_t), stream));
+    }
+  }
   if (sync_cap < 2ull + n_seg) {
     if (d_sync) {
       PLORA_CUDA(cudaStreamSynchronize(stream));
@@ -318,6 +341,9 @@ void plora_plan_destroy(plora_plan* plan) {
   cudaFree(plan->d_buf);
   cudaFree(plan->d_v);
   cudaFree(plan->d_sync);
+  cudaFree(plan->d_vpart);
+  cudaFree(plan->d_vbuf);
+  cudaFree(plan->d_tcnt);
   delete plan;
 }
 

@@ -150,6 +150,14 @@ struct SgmvTile {
   uint32_t rank;
 };
 
+// Split-K factor of the SGMV shrink: enough CTAs to cover the SMs twice,
+// K slices of >= 256 elements that divide d_in into 64-element chunks.
+inline uint32_t sgmv_splits(uint32_t n_tiles, uint32_t d_in) {
+  uint32_t ks = 1;
+  while (n_tiles * ks < 2 * 148 && (d_in / 64) % (ks * 2) == 0 && d_in / (ks * 2) >= 256) ks *= 2;
+  return ks;
+}
+
 }  // namespace plora
 
 struct plora_plan {
@@ -179,6 +187,14 @@ struct plora_plan {
   uint64_t v_cap = 0;
   uint32_t* d_sync = nullptr;  // [0] ticket, [1] exit count, [2..] per-segment shrink done
   uint64_t sync_cap = 0;
+  // SGMV: split-K partials of V (fp32), V tiles (bf16, 128 × 128 per tile),
+  // per-tile arrival counters of the split-K reduction (self-resetting)
+  float* d_vpart = nullptr;
+  uint64_t vpart_cap = 0;  // floats
+  char* d_vbuf = nullptr;
+  uint64_t vbuf_cap = 0;   // bytes
+  uint32_t* d_tcnt = nullptr;
+  uint64_t tcnt_cap = 0;
   cudaEvent_t upload_done = nullptr;
 
   void build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream);

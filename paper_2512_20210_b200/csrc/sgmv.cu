@@ -6,23 +6,28 @@
 // reference bills this as cost_model.prefill_ms (cost_model.hpp:32-34,
 // src/engine.cpp:355).
 //
-// One CTA per 128-token tile of a run, 8 warps:
-//   warp 5      TMA producer: x tile [128 × 64] per K-chunk (2-D tensor map,
-//               128-byte swizzle) into a 4-stage smem ring;
-//   warps 6-7   page-gather producers: cp.async 16-byte pieces of the
-//               adapter's A rows (shrink) / Bᵀ rows (expand), each piece
-//               translated through the device page table, written straight
-//               into the UMMA canonical SW128 layouts (K-major for A,
-//               MN-major for Bᵀ); ranks are zero-padded to a multiple of 16
-//               in shared memory only — no contiguous adapter is built;
-//   warp 4      MMA issuer (one thread): shrink V[128 × r16] += X · Aᵀ over
-//               d_in/64 chunks into TMEM, then expand D[128 × 128] = V · Bᵀ
-//               per 128-column chunk into two TMEM buffers (double-buffered
-//               against the epilogue);
-//   warps 0-3   epilogue: V (TMEM) -> bf16 -> smem (A operand of the
-//               expand); then per chunk D (TMEM) + y -> y, with the y row
-//               prefetched before the accumulator is ready.
-// Rank up to 128 (TMEM columns: V 128 + 2 × 128 accumulators of 512).
+// Two kernels per (layer, proj) call, chained by programmatic dependent
+// launch, each with enough CTAs to keep every SM streaming (a 128-token tile
+// is 1 MiB of x and 2 MiB of y read-modify-write; one CTA per tile would be
+// latency-bound on its own serial stream):
+//
+//  shrink  CTA (tile, k-split): V_part[128 × r16] = X[128, ks] · A[r, ks]ᵀ
+//          over a d_in/KS slice.  Warp 0 TMA-loads x chunks [128 × 64]
+//          (SWIZZLE_128B) into a 4-stage ring; warps 1-3 gather the
+//          adapter's A rows with 16-byte cp.async pieces, each translated
+//          through the device page table, straight into the UMMA K-major
+//          SW128 layout (rank zero-padded to 16 in smem only); warp 4 issues
+//          tcgen05.mma (M = 128, N = r16) into TMEM; warps 4-7 store the fp32
+//          partial.  The last CTA of a tile (arrival counter) sums the KS
+//          partials in split order (deterministic) and writes V in bf16 — the
+//          rounding point between shrink and expand.
+//  expand  CTA (tile, 128-column block): D[128 × 128] = V · Bᵀ[:, block]
+//          (tcgen05, K = r16) with the Bᵀ block gathered from pages
+//          (MN-major SW128) and V / y tiles loaded by TMA; the epilogue adds
+//          D into the y tile in shared memory and TMA-stores it (rows of a
+//          partial tile, which belong to the next run, are stored per row).
+// Rank <= 128; d_in % 64 == 0; d_out % 128 == 0; bf16 stores (otherwise the
+// exact CUDA-core BGMV path runs, see plora_sgmv).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
@@ -48,18 +53,217 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kStages = 4;
 constexpr uint32_t kTileM = 128;
-constexpr uint32_t kChunkK = 64;    // shrink K per stage (one 128-byte swizzle row)
-constexpr uint32_t kChunkN = 128;   // expand N per stage / accumulator
+constexpr uint32_t kChunkK = 64;   // shrink K per stage (one 128-byte swizzle row)
+constexpr uint32_t kBlockN = 128;  // expand output columns per CTA
 constexpr uint32_t kMaxRank = 128;
-constexpr uint32_t kStageBytes = 32768;  // X 16 KiB + A 16 KiB, or Bᵀ r16 × 128 × 2
-constexpr uint32_t kVBytes = kTileM * kMaxRank * 2;
-constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kAccCol0 = 128;  // expand accumulators at columns 128 and 256
-constexpr int kWeightProducers = 64;
+constexpr uint32_t kTmemCols = 128;
+constexpr int kGatherThreads = 96;  // warps 1-3
 
-struct SgmvArgs {
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
+  // 128-byte swizzle inside an 8-row × 128-byte atom
+  return (row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4);
+}
+
+struct PagedSrc {
+  const char* arena;
+  const uint32_t* table;
+  uint32_t table_off;
+  uint32_t log2_page;
+  __device__ const char* at(uint64_t off) const {
+    const uint32_t phys = __ldg(table + table_off + static_cast<uint32_t>(off >> log2_page));
+    return arena + (static_cast<uint64_t>(phys) << log2_page) + (off & ((1ull << log2_page) - 1));
+  }
+};
+
+// ------------------------------------------------------------------ shrink
+constexpr int kSStages = 4;
+constexpr uint32_t kSStageBytes = 32768;  // X [128 × 64] 16 KiB + A [r16 × 64] <= 16 KiB
+
+struct ShrinkArgs {
+  const char* arena;
+  const uint32_t* table;
+  const SgmvTile* tiles;
+  float* vpart;      // [tile][split][128][128] fp32
+  __nv_bfloat16* vbuf;  // [tile][128][128] bf16
+  uint32_t* tcnt;    // [tile] arrivals
+  uint64_t blk_mult;
+  uint32_t log2_page;
+  uint32_t d_in;
+  uint32_t splits;
+};
+
+struct SSmem {
+  static constexpr uint32_t stages = 0;  // 1024-aligned
+  static constexpr uint32_t bars = stages + kSStages * kSStageBytes;
+  static constexpr uint32_t n_bars = 2 * kSStages + 1;  // full[4], empty[4], v_full
+  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
+  static constexpr uint32_t flag = tmem_slot + 8;
+  static constexpr uint32_t total = flag + 8;
+  static constexpr uint32_t alloc = total + 1024;  // alignment slack
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    sgmv_shrink_kernel(const ShrinkArgs p, const __grid_constant__ CUtensorMap tmap_x) {
+  extern __shared__ char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SSmem::bars);
+  uint64_t* empty = full + kSStages;
+  uint64_t* v_full = full + 2 * kSStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SSmem::tmem_slot);
+  volatile uint32_t* last_flag = reinterpret_cast<uint32_t*>(smem + SSmem::flag);
+
+  const uint32_t tile_i = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
+  const SgmvTile tile = p.tiles[tile_i];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t r = tile.rank, r16 = (r + 15) & ~15u;
+  const uint32_t kslice = p.d_in / p.splits, NK = kslice / kChunkK, k0 = split * kslice;
+  const uint64_t blk = static_cast<uint64_t>(r) * p.blk_mult * 2;  // A block, bytes
+  const PagedSrc src{p.arena, p.table, tile.table_off, p.log2_page};
+
+  ptx::pdl_launch_dependents();  // the expand may start gathering its weights
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSStages; ++s) {
+      ptx::mbar_init(&full[s], 1 + kGatherThreads);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(v_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (x chunks)
+    if (lane == 0) {
+      ptx::pdl_wait();  // x is written by earlier kernels in the stream
+      for (uint32_t kc = 0; kc < NK; ++kc) {
+        const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
+        ptx::mbar_wait(&empty[st], ph ^ 1u);
+        ptx::mbar_arrive_expect_tx(&full[st], kTileM * kChunkK * 2);
+        ptx::tma_load_2d(smem + SSmem::stages + st * kSStageBytes, &tmap_x,
+                         static_cast<int32_t>(k0 + kc * kChunkK), static_cast<int32_t>(tile.row0),
+                         &full[st]);
+      }
+    }
+  } else if (warp < 4) {
+    // ----------------------------------------------- A gathers (paged rows)
+    // Thread wt owns rank rows wt and wt + 96.  With pages >= 256 B a row's
+    // 128-byte piece of a chunk lies in one page: one page-table lookup per
+    // row per chunk, issued a chunk ahead (before the slot wait), so the
+    // lookups never serialise the copies.  Smaller pages: per-piece lookups.
+    const uint32_t wt = threadIdx.x - 32;
+    const bool fast = p.log2_page >= 8;
+    const uint32_t n0 = wt, n1 = wt + kGatherThreads;
+    auto row_off = [&](uint32_t n, uint32_t kc) {
+      return blk + (static_cast<uint64_t>(n) * p.d_in + k0 + kc * kChunkK) * 2;
+    };
+    auto lookup = [&](uint32_t n, uint32_t kc) -> uint32_t {
+      return (fast && n < r && kc < NK) ? __ldg(p.table + tile.table_off + static_cast<uint32_t>(row_off(n, kc) >> p.log2_page)) : 0u;
+    };
+    uint32_t ph0 = lookup(n0, 0), ph1 = lookup(n1, 0);
+    const uint64_t pmask = (1ull << p.log2_page) - 1;
+    for (uint32_t kc = 0; kc < NK; ++kc) {
+      const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
+      const uint32_t nx0 = lookup(n0, kc + 1), nx1 = lookup(n1, kc + 1);  // next chunk, in flight
+      ptx::mbar_wait(&empty[st], ph ^ 1u);
+      char* wdst = smem + SSmem::stages + st * kSStageBytes + kTileM * kChunkK * 2;
+#pragma unroll
+      for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t n = h ? n1 : n0;
+        if (n >= r16) continue;
+        if (n >= r) {
+#pragma unroll
+          for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), p.arena, 0);  // zero padding
+        } else if (fast) {
+          const uint64_t off = row_off(n, kc);
+          const char* base = p.arena + (static_cast<uint64_t>(h ? ph1 : ph0) << p.log2_page) + (off & pmask);
+#pragma unroll
+          for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), base + c * 16, 16);
+        } else {
+          for (uint32_t c = 0; c < 8; ++c)
+            ptx::cp_async_16(wdst + swz(n, c), src.at(row_off(n, kc) + c * 16), 16);
+        }
+      }
+      ptx::cp_async_mbar_arrive_noinc(&full[st]);
+      ph0 = nx0;
+      ph1 = nx1;
+    }
+  } else {
+    if (warp == 4 && lane == 0) {
+      // ------------------------------------------------------- MMA issuer
+      const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, r16, false, false);
+      const uint32_t sbase = ptx::smem_u32(smem + SSmem::stages);
+      for (uint32_t kc = 0; kc < NK; ++kc) {
+        const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
+        ptx::mbar_wait(&full[st], ph);
+        ptx::fence_proxy_async_shared();
+        ptx::tc_fence_after();
+        const uint32_t xa = sbase + st * kSStageBytes, wa = xa + kTileM * kChunkK * 2;
+#pragma unroll
+        for (uint32_t k = 0; k < kChunkK / 16; ++k)
+          ptx::umma_f16(tmem, ptx::smem_desc_sw128(xa + k * 32, 16, 1024),
+                        ptx::smem_desc_sw128(wa + k * 32, 16, 1024), idesc, (kc | k) != 0);
+        ptx::umma_commit(&empty[st]);
+      }
+      ptx::umma_commit(v_full);
+    }
+    __syncwarp();
+    // ------------------------------------------- epilogue (warps 4-7): partial
+    const uint32_t m = (warp - 4) * 32 + lane;  // tile row == TMEM lane
+    const uint32_t lane_base = ((warp & 3) * 32) << 16;
+    ptx::mbar_wait(v_full, 0);
+    ptx::tc_fence_after();
+    float* vp = p.vpart + ((static_cast<uint64_t>(tile_i) * p.splits + split) * kTileM + m) * kMaxRank;
+    for (uint32_t cc = 0; cc < r16 / 16; ++cc) {
+      uint32_t rv[16];
+      ptx::tmem_ld_32x32b_x16(tmem + lane_base + cc * 16, rv);
+      ptx::tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<uint4*>(vp + cc * 16)[i] = make_uint4(rv[4 * i], rv[4 * i + 1], rv[4 * i + 2], rv[4 * i + 3]);
+    }
+    // split-K reduction: the last CTA of the tile sums the partials in split order
+    __threadfence();
+    ptx::named_bar_sync(1, 128);
+    if (warp == 4 && lane == 0)
+      *last_flag = atomicAdd(p.tcnt + tile_i, 1u) == p.splits - 1;
+    ptx::named_bar_sync(1, 128);
+    if (*last_flag) {
+      __threadfence();
+      const float* v0 = p.vpart + (static_cast<uint64_t>(tile_i) * p.splits * kTileM + m) * kMaxRank;
+      __nv_bfloat16* vb = p.vbuf + (static_cast<uint64_t>(tile_i) * kTileM + m) * kMaxRank;
+      for (uint32_t c = 0; c < r16; c += 8) {
+        float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (uint32_t sp = 0; sp < p.splits; ++sp) {
+          const float4* q = reinterpret_cast<const float4*>(v0 + static_cast<uint64_t>(sp) * kTileM * kMaxRank + c);
+          const float4 lo = __ldcg(q), hi = __ldcg(q + 1);
+          a[0] += lo.x; a[1] += lo.y; a[2] += lo.z; a[3] += lo.w;
+          a[4] += hi.x; a[5] += hi.y; a[6] += hi.z; a[7] += hi.w;
+        }
+        uint4 o;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
+        *reinterpret_cast<uint4*>(vb + c) = o;
+      }
+      if (warp == 4 && lane == 0) p.tcnt[tile_i] = 0;  // graph-replayable
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+// ------------------------------------------------------------------ expand
+struct ExpandArgs {
   const char* arena;
   const uint32_t* table;
   const SgmvTile* tiles;
@@ -69,227 +273,160 @@ struct SgmvArgs {
   uint32_t log2_page;
   uint32_t d_in;
   uint32_t d_out;
+  uint32_t nblk;  // d_out / kBlockN
   float scale;
 };
 
-struct Smem {
-  static constexpr uint32_t stages = 0;  // 1024-aligned
-  static constexpr uint32_t v = stages + kStages * kStageBytes;
-  static constexpr uint32_t bars = v + kVBytes;
-  // full[4], empty[4], v_full, v_ready, acc_full[2], acc_empty[2]
-  static constexpr uint32_t n_bars = 2 * kStages + 6;
-  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
-  static constexpr uint32_t total = tmem_slot + 16;
-  static constexpr uint32_t alloc = total + 1024;  // alignment slack
+struct ESmem {
+  static constexpr uint32_t y = 0;                 // [2 boxes][128 rows × 128 B] SW128
+  static constexpr uint32_t v = y + 32768;         // [2 atoms][128 rows × 128 B] SW128 (K-major)
+  static constexpr uint32_t b = v + 32768;         // [2 col groups][r16 rows × 128 B] SW128 (MN-major)
+  static constexpr uint32_t bars = b + 32768;      // in_full, b_full, acc_full
+  static constexpr uint32_t tmem_slot = bars + 3 * 8;
+  static constexpr uint32_t total = tmem_slot + 8;
+  static constexpr uint32_t alloc = total + 1024;
 };
 
-__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
-  // 128-byte swizzle inside an 8-row × 128-byte atom
-  return (row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4);
-}
-
-__device__ __forceinline__ const char* paged_src(const SgmvArgs& p, uint32_t table_off,
-                                                 uint64_t off) {
-  const uint32_t phys = __ldg(p.table + table_off + static_cast<uint32_t>(off >> p.log2_page));
-  return p.arena + (static_cast<uint64_t>(phys) << p.log2_page) +
-         (off & ((1ull << p.log2_page) - 1));
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
-    sgmv_tc_kernel(const SgmvArgs p, const __grid_constant__ CUtensorMap tmap_x) {
+    sgmv_expand_kernel(const ExpandArgs p, const __grid_constant__ CUtensorMap tmap_y,
+                       const __grid_constant__ CUtensorMap tmap_v) {
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::bars);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + kStages;
-  uint64_t* v_full = bars + 2 * kStages;
-  uint64_t* v_ready = v_full + 1;
-  uint64_t* acc_full = v_full + 2;
-  uint64_t* acc_empty = v_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + Smem::tmem_slot);
+  uint64_t* in_full = reinterpret_cast<uint64_t*>(smem + ESmem::bars);
+  uint64_t* b_full = in_full + 1;
+  uint64_t* acc_full = in_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ESmem::tmem_slot);
 
-  const SgmvTile tile = p.tiles[blockIdx.x];
+  const uint32_t tile_i = blockIdx.x / p.nblk, nb = blockIdx.x % p.nblk;
+  const SgmvTile tile = p.tiles[tile_i];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r = tile.rank, r16 = (r + 15) & ~15u;
-  const uint32_t NK = p.d_in / kChunkK, NC = p.d_out / kChunkN;
-  const uint64_t blk = static_cast<uint64_t>(r) * p.blk_mult * 2;       // A block, bytes
-  const uint64_t bt = blk + static_cast<uint64_t>(r) * p.d_in * 2;       // Bᵀ block, bytes
+  const uint64_t bt = (static_cast<uint64_t>(r) * p.blk_mult + static_cast<uint64_t>(r) * p.d_in) * 2;
+  const PagedSrc src{p.arena, p.table, tile.table_off, p.log2_page};
+  const uint32_t col0 = nb * kBlockN;
+  const uint32_t vboxes = r16 > 64 ? 2 : 1;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], 1 + kWeightProducers);
-      ptx::mbar_init(&empty[s], 1);
-    }
-    ptx::mbar_init(v_full, 1);
-    ptx::mbar_init(v_ready, kTileM);
-    for (int b = 0; b < 2; ++b) {
-      ptx::mbar_init(&acc_full[b], 1);
-      ptx::mbar_init(&acc_empty[b], kTileM);
-    }
+    ptx::mbar_init(in_full, 1);
+    ptx::mbar_init(b_full, kGatherThreads);
+    ptx::mbar_init(acc_full, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 4) ptx::tmem_alloc(tmem_slot, kTmemCols);
-  if (warp == 5 && lane == 0) ptx::prefetch_tmap(&tmap_x);
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_y);
+    ptx::prefetch_tmap(&tmap_v);
+  }
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 5) {
-    // ------------------------------------------------ TMA producer (x tiles)
+  if (warp == 0) {
+    // ------------------------------- TMA: y tile (2 boxes) and V tile (1-2 boxes)
     if (lane == 0) {
-      uint32_t it = 0;
-      for (uint32_t kc = 0; kc < NK; ++kc, ++it) {
-        const uint32_t st = it % kStages, ph = (it / kStages) & 1u;
-        ptx::mbar_wait(&empty[st], ph ^ 1u);
-        ptx::mbar_arrive_expect_tx(&full[st], kTileM * kChunkK * 2);
-        ptx::tma_load_2d(smem + Smem::stages + st * kStageBytes, &tmap_x,
-                         static_cast<int32_t>(kc * kChunkK), static_cast<int32_t>(tile.row0),
-                         &full[st]);
-      }
-      for (uint32_t nc = 0; nc < NC; ++nc, ++it) {
-        const uint32_t st = it % kStages, ph = (it / kStages) & 1u;
-        ptx::mbar_wait(&empty[st], ph ^ 1u);
-        ptx::mbar_arrive(&full[st]);
-      }
+      ptx::pdl_wait();  // V comes from the shrink; y from earlier kernels
+      ptx::mbar_arrive_expect_tx(in_full, 2 * 16384 + vboxes * 16384);
+      for (uint32_t bx = 0; bx < 2; ++bx)
+        ptx::tma_load_2d(smem + ESmem::y + bx * 16384, &tmap_y, static_cast<int32_t>(col0 + bx * 64),
+                         static_cast<int32_t>(tile.row0), in_full);
+      for (uint32_t bx = 0; bx < vboxes; ++bx)
+        ptx::tma_load_2d(smem + ESmem::v + bx * 16384, &tmap_v, static_cast<int32_t>(bx * 64),
+                         static_cast<int32_t>(tile_i * kTileM), in_full);
     }
-  } else if (warp >= 6) {
-    // ------------------------------------------- page-gather producers (A, Bᵀ)
-    const uint32_t wt = threadIdx.x - 6 * 32;
-    uint32_t it = 0;
-    for (uint32_t kc = 0; kc < NK; ++kc, ++it) {
-      const uint32_t st = it % kStages, ph = (it / kStages) & 1u;
-      ptx::mbar_wait(&empty[st], ph ^ 1u);
-      char* wdst = smem + Smem::stages + st * kStageBytes + kTileM * kChunkK * 2;
-      for (uint32_t q = wt; q < r16 * 8; q += kWeightProducers) {
-        const uint32_t n = q >> 3, c = q & 7;
-        if (n < r) {
-          const uint64_t off = blk + (static_cast<uint64_t>(n) * p.d_in + kc * kChunkK + c * 8) * 2;
-          ptx::cp_async_16(wdst + swz(n, c), paged_src(p, tile.table_off, off), 16);
-        } else {
-          ptx::cp_async_16(wdst + swz(n, c), p.arena, 0);  // zero rank padding
-        }
-      }
-      ptx::cp_async_mbar_arrive_noinc(&full[st]);
+  } else if (warp < 4) {
+    // ----------------------------------------- Bᵀ block gather (paged rows)
+    // Thread wt owns rank rows wt and wt + 96; with pages >= 256 B a row's
+    // 256-byte block slice lies in one page (one lookup, both issued first).
+    const uint32_t wt = threadIdx.x - 32;
+    const uint32_t lbo = r16 * 128;  // stride between the two 64-column groups
+    const bool fast = p.log2_page >= 8;
+    const uint64_t pmask = (1ull << p.log2_page) - 1;
+    auto row_off = [&](uint32_t j) {
+      return bt + (static_cast<uint64_t>(j) * p.d_out + col0) * 2;
+    };
+    uint32_t phys[2];
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+      const uint32_t j = wt + h * kGatherThreads;
+      phys[h] = (fast && j < r) ? __ldg(p.table + tile.table_off + static_cast<uint32_t>(row_off(j) >> p.log2_page)) : 0u;
     }
-    const uint32_t lbo = (r16 / 8) * 1024;  // N-group stride of the MN-major Bᵀ tile
-    for (uint32_t nc = 0; nc < NC; ++nc, ++it) {
-      const uint32_t st = it % kStages, ph = (it / kStages) & 1u;
-      ptx::mbar_wait(&empty[st], ph ^ 1u);
-      char* bdst = smem + Smem::stages + st * kStageBytes;
-      for (uint32_t q = wt; q < r16 * 16; q += kWeightProducers) {
-        const uint32_t j = q >> 4, g = (q >> 3) & 1, c = q & 7;
-        char* dst = bdst + g * lbo + swz(j, c);
-        if (j < r) {
-          const uint64_t off =
-              bt + (static_cast<uint64_t>(j) * p.d_out + nc * kChunkN + g * 64 + c * 8) * 2;
-          ptx::cp_async_16(dst, paged_src(p, tile.table_off, off), 16);
-        } else {
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+      const uint32_t j = wt + h * kGatherThreads;
+      if (j >= r16) continue;
+      const uint64_t off = row_off(j);
+      const char* base = p.arena + (static_cast<uint64_t>(phys[h]) << p.log2_page) + (off & pmask);
+#pragma unroll
+      for (uint32_t q = 0; q < 16; ++q) {
+        const uint32_t g = q >> 3, c = q & 7;
+        char* dst = smem + ESmem::b + g * lbo + swz(j, c);
+        if (j >= r)
           ptx::cp_async_16(dst, p.arena, 0);
-        }
-      }
-      ptx::cp_async_mbar_arrive_noinc(&full[st]);
-    }
-  } else if (warp == 4) {
-    // --------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc_s = ptx::idesc_bf16_f32(kTileM, r16, false, false);
-      const uint32_t idesc_e = ptx::idesc_bf16_f32(kTileM, kChunkN, false, true);
-      const uint32_t sbase = ptx::smem_u32(smem + Smem::stages);
-      const uint32_t vbase = ptx::smem_u32(smem + Smem::v);
-      uint32_t it = 0;
-      for (uint32_t kc = 0; kc < NK; ++kc, ++it) {
-        const uint32_t st = it % kStages, ph = (it / kStages) & 1u;
-        ptx::mbar_wait(&full[st], ph);
-        ptx::fence_proxy_async_shared();
-        ptx::tc_fence_after();
-        const uint32_t xa = sbase + st * kStageBytes, wa = xa + kTileM * kChunkK * 2;
-#pragma unroll
-        for (uint32_t k = 0; k < kChunkK / 16; ++k)
-          ptx::umma_f16(tmem, ptx::smem_desc_sw128(xa + k * 32, 16, 1024),
-                        ptx::smem_desc_sw128(wa + k * 32, 16, 1024), idesc_s, (kc | k) != 0);
-        ptx::umma_commit(&empty[st]);
-      }
-      ptx::umma_commit(v_full);
-      ptx::mbar_wait(v_ready, 0);
-      ptx::tc_fence_after();
-      const uint32_t lbo = (r16 / 8) * 1024;
-      for (uint32_t nc = 0; nc < NC; ++nc, ++it) {
-        const uint32_t buf = nc & 1u;
-        ptx::mbar_wait(&acc_empty[buf], ((nc >> 1) & 1u) ^ 1u);
-        const uint32_t st = it % kStages, ph = (it / kStages) & 1u;
-        ptx::mbar_wait(&full[st], ph);
-        ptx::fence_proxy_async_shared();
-        ptx::tc_fence_after();
-        const uint32_t ba = sbase + st * kStageBytes;
-        for (uint32_t kk = 0; kk < r16 / 16; ++kk)
-          ptx::umma_f16(tmem + kAccCol0 + buf * kChunkN,
-                        ptx::smem_desc_sw128(vbase + (kk >> 2) * (kTileM * 128) + (kk & 3) * 32,
-                                             16, 1024),
-                        ptx::smem_desc_sw128(ba + kk * 2048, lbo, 1024), idesc_e, kk != 0);
-        ptx::umma_commit(&empty[st]);
-        ptx::umma_commit(&acc_full[buf]);
+        else if (fast)
+          ptx::cp_async_16(dst, base + q * 16, 16);
+        else
+          ptx::cp_async_16(dst, src.at(off + q * 16), 16);
       }
     }
+    ptx::cp_async_mbar_arrive_noinc(b_full);
   } else {
-    // ------------------------------------------------- epilogue (warps 0-3)
-    const uint32_t m = warp * 32 + lane;  // tile row == TMEM lane
-    const uint32_t lane_base = (warp * 32) << 16;
-    ptx::mbar_wait(v_full, 0);
+    if (warp == 4 && lane == 0) {
+      // ------------------------------------------------------- MMA issuer
+      ptx::mbar_wait(in_full, 0);
+      ptx::mbar_wait(b_full, 0);
+      ptx::fence_proxy_async_shared();
+      ptx::tc_fence_after();
+      const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, kBlockN, false, true);
+      const uint32_t vbase = ptx::smem_u32(smem + ESmem::v), bbase = ptx::smem_u32(smem + ESmem::b);
+      const uint32_t lbo = r16 * 128;
+      for (uint32_t kk = 0; kk < r16 / 16; ++kk)
+        ptx::umma_f16(tmem, ptx::smem_desc_sw128(vbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                      ptx::smem_desc_sw128(bbase + kk * 2048, lbo, 1024), idesc, kk != 0);
+      ptx::umma_commit(acc_full);
+    }
+    __syncwarp();
+    // ------------------------------------------------- epilogue (warps 4-7)
+    const uint32_t m = (warp - 4) * 32 + lane;  // tile row == TMEM lane
+    const uint32_t lane_base = ((warp & 3) * 32) << 16;
+    ptx::mbar_wait(acc_full, 0);  // also implies in_full (the MMA waited on it)
     ptx::tc_fence_after();
-    char* vs = smem + Smem::v;
-    for (uint32_t cc = 0; cc < r16 / 16; ++cc) {
+    char* ys = smem + ESmem::y;
+    const bool full_tile = tile.nrows == kTileM;
+    char* yrow = p.y + static_cast<uint64_t>(tile.row0 + m) * p.y_stride_b + static_cast<uint64_t>(col0) * 2;
+#pragma unroll 1
+    for (uint32_t q = 0; q < kBlockN / 16; ++q) {  // 16 columns = two 16-byte chunks
       uint32_t rv[16];
-      ptx::tmem_ld_32x32b_x16(tmem + lane_base + cc * 16, rv);
+      ptx::tmem_ld_32x32b_x16(tmem + lane_base + q * 16, rv);
       ptx::tmem_ld_wait();
-      uint4 pk[2];
-      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(pk);
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        h[i] = __floats2bfloat162_rn(__uint_as_float(rv[2 * i]), __uint_as_float(rv[2 * i + 1]));
+      for (uint32_t hh = 0; hh < 2; ++hh) {
+        const uint32_t chunk = (q * 2 + hh) & 7, box = (q * 2 + hh) >> 3;
+        uint4* yp = reinterpret_cast<uint4*>(ys + box * 16384 + swz(m, chunk));
+        uint4 yv = *yp;
+        __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&yv);
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t chunk = cc * 2 + hh;  // 16-byte chunk along K
-        *reinterpret_cast<uint4*>(vs + (chunk >> 3) * (kTileM * 128) + swz(m, chunk & 7)) = pk[hh];
+        for (int i = 0; i < 4; ++i) {
+          float2 f = __bfloat1622float2(hy[i]);
+          f.x = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i]), f.x);
+          f.y = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i + 1]), f.y);
+          hy[i] = __floats2bfloat162_rn(f.x, f.y);
+        }
+        if (full_tile)
+          *yp = yv;
+        else if (m < tile.nrows)  // rows past the run belong to the next one
+          reinterpret_cast<uint4*>(yrow)[q * 2 + hh] = yv;
       }
     }
-    ptx::fence_proxy_async_shared();
-    ptx::mbar_arrive(v_ready);
-
-    const bool valid = m < tile.nrows;
-    char* yrow = p.y + static_cast<uint64_t>(tile.row0 + m) * p.y_stride_b;
-    for (uint32_t nc = 0; nc < NC; ++nc) {
-      const uint32_t buf = nc & 1u;
-      uint4 yv[16];
-      uint4* yp = reinterpret_cast<uint4*>(yrow + static_cast<uint64_t>(nc) * kChunkN * 2);
-      if (valid) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) yv[i] = yp[i];
-      }
-      ptx::mbar_wait(&acc_full[buf], (nc >> 1) & 1u);
-      ptx::tc_fence_after();
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        uint32_t rv[16];
-        ptx::tmem_ld_32x32b_x16(tmem + lane_base + kAccCol0 + buf * kChunkN + q * 16, rv);
-        ptx::tmem_ld_wait();
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&yv[q * 2 + hh]);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float2 f = __bfloat1622float2(hy[i]);
-            f.x = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i]), f.x);
-            f.y = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i + 1]), f.y);
-            hy[i] = __floats2bfloat162_rn(f.x, f.y);
-          }
-        }
-      }
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(&acc_empty[buf]);
-      if (valid) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) yp[i] = yv[i];
+    if (full_tile) {
+      ptx::fence_proxy_async_shared();  // generic-proxy smem writes -> TMA store
+      ptx::named_bar_sync(1, 128);
+      if (warp == 4 && lane == 0) {
+        for (uint32_t bx = 0; bx < 2; ++bx)
+          ptx::tma_store_2d(&tmap_y, static_cast<int32_t>(col0 + bx * 64),
+                            static_cast<int32_t>(tile.row0), ys + bx * 16384);
+        ptx::bulk_commit();
+        ptx::bulk_wait_all();
       }
     }
   }
@@ -316,6 +453,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+
+void make_tmap_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
+                  uint64_t row_stride_b, uint32_t box_cols, uint32_t box_rows) {
+  const cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
+  const cuuint64_t strides[1] = {row_stride_b};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(cr));
+}
+
 }  // namespace
 
 extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
@@ -330,40 +481,65 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     // The tensor-core path: bf16, rank <= 128, d_in % 64 == 0, d_out % 128 == 0.
     // Anything else (fp32 storage, wider ranks, odd widths) runs the exact
     // CUDA-core BGMV path, which handles every segment length.
-    if (g.esize != 2 || plan->max_rank > kMaxRank || din % kChunkK || dout % kChunkN)
+    if (g.esize != 2 || plan->max_rank > kMaxRank || din % kChunkK || dout % kBlockN)
       return plora_bgmv(plan, layer, proj, x, x_stride, y, y_stride, scale, stream);
     if (plan->n_tiles == 0) return 0;
     DeviceCtx ctx(st.device);
-    CUtensorMap tmap;
-    const cuuint64_t dims[2] = {din, std::max<uint64_t>(plan->n_tokens, 1)};
-    const cuuint64_t strides[1] = {x_stride * 2};
-    const cuuint32_t box[2] = {kChunkK, kTileM};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult cr = encode_fn()(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x),
-                              dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(cr));
-    SgmvArgs a{};
-    a.arena = st.arena;
-    a.table = st.d_table;
-    a.tiles = plan->d_tiles;
-    a.y = static_cast<char*>(y);
-    a.y_stride_b = y_stride * 2;
-    a.blk_mult = g.blk_mult(layer, proj);
-    a.log2_page = st.log2_page;
-    a.d_in = din;
-    a.d_out = dout;
-    a.scale = scale;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t splits = sgmv_splits(plan->n_tiles, din);
+    CUtensorMap tmap_x, tmap_y, tmap_v;
+    make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kChunkK, kTileM);
+    make_tmap_2d(&tmap_y, y, dout, plan->n_tokens, y_stride * 2, 64, kTileM);
+    make_tmap_2d(&tmap_v, plan->d_vbuf, kMaxRank, static_cast<uint64_t>(plan->n_tiles) * kTileM,
+                 kMaxRank * 2, 64, kTileM);
     static bool attr = false;
     if (!attr) {
-      PLORA_CUDA(cudaFuncSetAttribute(sgmv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(Smem::alloc)));
+      PLORA_CUDA(cudaFuncSetAttribute(sgmv_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(SSmem::alloc)));
+      PLORA_CUDA(cudaFuncSetAttribute(sgmv_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(ESmem::alloc)));
       attr = true;
     }
-    sgmv_tc_kernel<<<plan->n_tiles, kThreads, Smem::alloc, static_cast<cudaStream_t>(stream)>>>(
-        a, tmap);
-    PLORA_CUDA(cudaGetLastError());
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+
+    ShrinkArgs sa{};
+    sa.arena = st.arena;
+    sa.table = st.d_table;
+    sa.tiles = plan->d_tiles;
+    sa.vpart = plan->d_vpart;
+    sa.vbuf = reinterpret_cast<__nv_bfloat16*>(plan->d_vbuf);
+    sa.tcnt = plan->d_tcnt;
+    sa.blk_mult = g.blk_mult(layer, proj);
+    sa.log2_page = st.log2_page;
+    sa.d_in = din;
+    sa.splits = splits;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(plan->n_tiles * splits);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = SSmem::alloc;
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_shrink_kernel, sa, tmap_x));
+    count_launch();
+
+    ExpandArgs ea{};
+    ea.arena = st.arena;
+    ea.table = st.d_table;
+    ea.tiles = plan->d_tiles;
+    ea.y = static_cast<char*>(y);
+    ea.y_stride_b = y_stride * 2;
+    ea.blk_mult = g.blk_mult(layer, proj);
+    ea.log2_page = st.log2_page;
+    ea.d_in = din;
+    ea.d_out = dout;
+    ea.nblk = dout / kBlockN;
+    ea.scale = scale;
+    cfg.gridDim = dim3(plan->n_tiles * ea.nblk);
+    cfg.dynamicSmemBytes = ESmem::alloc;
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y, tmap_v));
     count_launch();
     return 0;
   });
