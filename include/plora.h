@@ -284,6 +284,24 @@ int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                plora_stream_t stream);
 
+/* ------------------- tensor-parallel decode (new; BASELINE cfg5) -----
+ * The S-LoRA scheme for a column-parallel base projection (hidden-dim
+ * sharded 70B config; the reference has no multi-GPU path).
+ * TP rank i of N shrinks rows [i·r/N, (i+1)·r/N) of every adapter into
+ * v_part [n_tokens × rs] fp32 (rs = plora_tp_shard_rows), the caller
+ * all-gathers v_part over the TP group into v_gathered [N][n_tokens][rs]
+ * (rank-major, e.g. ncclAllGather), and the expand adds
+ * scale · v · Bᵀ[:, i·d_out/N : (i+1)·d_out/N] into the rank's output shard
+ * y_shard [n_tokens × d_out/N].  Every adapter rank must be divisible by N;
+ * bf16 stores only. */
+uint32_t plora_tp_shard_rows(const plora_plan* plan, uint32_t tp_size);
+int plora_bgmv_tp_shrink(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
+                         uint32_t tp_size, const void* x, uint64_t x_stride, float* v_part,
+                         plora_stream_t stream);
+int plora_bgmv_tp_expand(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
+                         uint32_t tp_size, const float* v_gathered, void* y_shard,
+                         uint64_t y_stride, float scale, plora_stream_t stream);
+
 /* ------------------------------------ loading / prefetch engine (new) -----
  * The reference simulator's residency control restated on CUDA streams and
  * events: Simulation::ensure_loading / evict (src/engine.cpp:292-333),

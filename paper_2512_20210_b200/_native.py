@@ -231,6 +231,9 @@ _SIGS = {
     "plora_predictor_known": (_int, [_vp, _u32]),
     "plora_predictor_stats": (None, [_vp, _P(plora_predictor_stats_t)]),
     "plora_predictor_buffer_at": (_int, [_vp, _u64, _P(_u32), _P(_dbl), _P(_dbl)]),
+    "plora_tp_shard_rows": (_u32, [_vp, _u32]),
+    "plora_bgmv_tp_shrink": (_int, [_vp, _u32, _u32, _u32, _u32, _vp, _u64, _vp, _vp]),
+    "plora_bgmv_tp_expand": (_int, [_vp, _u32, _u32, _u32, _u32, _vp, _vp, _u64, C.c_float, _vp]),
     "plora_debug_set_trace": (_int, [_vp, _u64]),
     "plora_debug_plan_geom": (_int, [_vp, _u32, _P(_u32)]),
 }

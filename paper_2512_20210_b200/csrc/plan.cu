@@ -228,7 +228,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   const uint64_t tile_b = align(tiles.size() * sizeof(SgmvTile));
   const uint64_t cch_b = align(cchunks.size() * sizeof(ClusterChunk));
   const uint64_t ccl_b = align(ccl_off.size() * sizeof(uint32_t));
-  const uint64_t total = std::max<uint64_t>(unit_b + tile_b + cch_b + ccl_b, 256);
+  const uint64_t cjob_b = align(cjobs.size() * sizeof(ClusterJob));
+  const uint64_t total = std::max<uint64_t>(unit_b + tile_b + cch_b + ccl_b + cjob_b, 256);
   DeviceCtx ctx(st.device);
   if (upload_done) PLORA_CUDA(cudaEventSynchronize(upload_done));  // pinned buffer reuse
   if (h_cap < total) {
@@ -256,6 +257,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   d_tiles = reinterpret_cast<SgmvTile*>(d_buf + unit_b);
   d_cchunks = reinterpret_cast<ClusterChunk*>(d_buf + unit_b + tile_b);
   d_ccl_off = reinterpret_cast<uint32_t*>(d_buf + unit_b + tile_b + cch_b);
+  std::memcpy(h_pinned + unit_b + tile_b + cch_b + ccl_b, cjobs.data(), cjobs.size() * sizeof(ClusterJob));
+  d_cjobs = reinterpret_cast<ClusterJob*>(d_buf + unit_b + tile_b + cch_b + ccl_b);
   PLORA_CUDA(cudaMemcpyAsync(d_buf, h_pinned, total, cudaMemcpyHostToDevice, stream));
   if (!upload_done) PLORA_CUDA(cudaEventCreateWithFlags(&upload_done, cudaEventDisableTiming));
   PLORA_CUDA(cudaEventRecord(upload_done, stream));

@@ -101,12 +101,14 @@ constexpr uint32_t kJobTok = 4;
 constexpr uint32_t kChunkRows = 8;
 constexpr uint32_t kChunkFirst = 1, kChunkLast = 2;
 
-struct ClusterJob {  // host-side only
+struct ClusterJob {  // 32 bytes; uploaded for the tensor-parallel path (tp.cu)
   uint32_t table_off;
   uint32_t rank;
   uint32_t ntok;
+  uint32_t pad;
   uint32_t tok[kJobTok];
 };
+static_assert(sizeof(ClusterJob) == 32, "ClusterJob layout");
 
 // Self-contained chunk record (32 bytes): the kernel's producer loads it
 // ahead of time and forwards it to the consumers through shared memory, so
@@ -176,6 +178,7 @@ struct plora_plan {
   std::vector<plora::ClusterChunk> cchunks;
   std::vector<uint32_t> ccl_off;
   plora::ClusterChunk* d_cchunks = nullptr;
+  plora::ClusterJob* d_cjobs = nullptr;
   uint32_t* d_ccl_off = nullptr;
   char* h_pinned = nullptr;
   uint64_t h_cap = 0;
@@ -203,6 +206,7 @@ struct plora_plan {
 namespace plora {
 // Diagnostics buffer set by plora_debug_set_trace (nullptr if absent or too small).
 uint64_t* trace_buffer(uint64_t need_bytes);
+// Tensor-parallel decode halves (tp.cu).
 // bf16 decode op (bgmv_cluster.cu): 4-CTA clusters, DSMEM exchange of v.
 void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
                          uint64_t x_stride, void* y, uint64_t y_stride, float scale,

@@ -68,6 +68,15 @@ def cfg3(dtype=torch.bfloat16, n_layers: int = 32, page_bytes: int = 2048,
                         seg_tokens, page_bytes)
 
 
+def cfg5(dtype=torch.bfloat16, n_layers: int = 80, page_bytes: int = 2048,
+         n_adapters: int = 128) -> DecodeConfig:
+    """Tensor-parallel decode at Llama-2-70B q/v shapes (q 8192 -> 8192, v
+    8192 -> 1024 GQA): 256 tokens over 128 adapters, r = [8,16,64][a % 3]
+    (BASELINE.json configs[4])."""
+    return DecodeConfig("cfg5", ModelShape.llama70b_qv(dtype),
+                        [(8, 16, 64)[a % 3] for a in range(n_adapters)], 2, page_bytes)
+
+
 def segment_assignment(n_segments: int, seg_tokens: int):
     """Prefill batch: segment s = tokens [s·L, (s+1)·L) of adapter s (contiguous runs)."""
     return np.repeat(np.arange(n_segments, dtype=np.int32), seg_tokens)

@@ -1,0 +1,112 @@
+"""Tensor-parallel paged LoRA for the hidden-dim-sharded configuration
+(BASELINE configs[4]: Llama-2-70B q/v at 2/4/8 GPUs).
+
+The S-LoRA scheme for a column-parallel base projection: TP rank i of N
+
+  1. shrinks its rows [i·r/N, (i+1)·r/N) of every adapter:
+     v_part = x · A[rows_i]ᵀ                         (plora_bgmv_tp_shrink)
+  2. all-gathers v_part over the TP group (NCCL over NVLink; a T·r/N fp32
+     message per rank, 4-32 KiB in total at cfg5)
+  3. expands into its output-column shard:
+     y[:, cols_i] += scale · v · Bᵀ[:, cols_i]       (plora_bgmv_tp_expand)
+
+x is replicated across the group (the input of a column-parallel layer) and
+y is the rank's output shard.  The reference has no multi-GPU path
+(SPEC.md:8); the math is PAPER.md:64-69.  Every rank's pool holds the full
+adapter pages; each rank reads only its shard (1/N of the adapter bytes).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional
+
+import torch
+
+from . import _native as N
+from .lora import BatchPlan, current_stream_handle
+
+
+def tp_shard_rows(plan: BatchPlan, tp_size: int) -> int:
+    """Row stride (floats) of a v_part buffer: ceil(max rank / tp_size)."""
+    return int(N.lib().plora_tp_shard_rows(plan.handle, tp_size))
+
+
+def bgmv_tp_shrink(plan: BatchPlan, layer: int, proj: int, tp_rank: int, tp_size: int,
+                   x: torch.Tensor, v_part: torch.Tensor, stream: int | None = None) -> torch.Tensor:
+    """v_part[t, j] = x[t] · A_{a(t)}[tp_rank·r/N + j]ᵀ (fp32, [T, rs])."""
+    if not (x.is_cuda and v_part.is_cuda) or v_part.dtype != torch.float32:
+        raise N.ValidationError("x and v_part must be CUDA tensors, v_part float32")
+    if x.dim() != 2 or x.stride(1) != 1 or not v_part.is_contiguous():
+        raise N.ValidationError("x must be 2-D with unit column stride; v_part contiguous")
+    rs = tp_shard_rows(plan, tp_size)
+    if v_part.numel() < plan.n_tokens * rs:
+        raise N.ValidationError("v_part smaller than n_tokens x shard rows")
+    s = current_stream_handle(x.device) if stream is None else stream
+    N.check(N.lib().plora_bgmv_tp_shrink(plan.handle, layer, proj, tp_rank, tp_size, x.data_ptr(),
+                                         x.stride(0), v_part.data_ptr(), s))
+    return v_part
+
+
+def bgmv_tp_expand(plan: BatchPlan, layer: int, proj: int, tp_rank: int, tp_size: int,
+                   v_gathered: torch.Tensor, y_shard: torch.Tensor, scale: float = 1.0,
+                   stream: int | None = None) -> torch.Tensor:
+    """y_shard += scale · v · Bᵀ[:, cols of tp_rank]; v_gathered is [N, T, rs]."""
+    if not (v_gathered.is_cuda and y_shard.is_cuda) or v_gathered.dtype != torch.float32:
+        raise N.ValidationError("v_gathered and y_shard must be CUDA tensors, v float32")
+    if not v_gathered.is_contiguous() or y_shard.dim() != 2 or y_shard.stride(1) != 1:
+        raise N.ValidationError("v_gathered contiguous; y_shard 2-D with unit column stride")
+    rs = tp_shard_rows(plan, tp_size)
+    if v_gathered.numel() < tp_size * plan.n_tokens * rs:
+        raise N.ValidationError("v_gathered smaller than tp_size x n_tokens x shard rows")
+    s = current_stream_handle(y_shard.device) if stream is None else stream
+    N.check(N.lib().plora_bgmv_tp_expand(plan.handle, layer, proj, tp_rank, tp_size,
+                                         v_gathered.data_ptr(), y_shard.data_ptr(),
+                                         y_shard.stride(0), C.c_float(scale), s))
+    return y_shard
+
+
+def _all_gather(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    import torch.distributed as dist
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+    else:  # gloo: list form (same rank-major result)
+        dist.all_gather(list(out.unbind(0)), inp, group=group)
+
+
+class TensorParallelLoRA:
+    """One TP rank's paged LoRA for a column-parallel projection.
+
+    ``forward(layer, proj, x, y_shard)`` runs shrink -> all-gather -> expand
+    on the current stream.  ``shrink`` / ``expand`` / ``all_gather`` default
+    to the sm_100a kernels and torch.distributed; they are injectable so the
+    orchestration (buffer shapes, gathered layout, rank bookkeeping) can be
+    exercised on CPU ranks with gloo in tests.
+    """
+
+    def __init__(self, plan, tp_rank: int, tp_size: int, group=None,
+                 shrink: Optional[Callable] = None, expand: Optional[Callable] = None,
+                 all_gather: Optional[Callable] = None, shard_rows: Optional[int] = None,
+                 n_tokens: Optional[int] = None, device=None):
+        if tp_size < 1 or not 0 <= tp_rank < tp_size:
+            raise N.ValidationError("tp_rank must be in [0, tp_size)")
+        self.plan, self.tp_rank, self.tp_size, self.group = plan, tp_rank, tp_size, group
+        self._shrink = shrink or bgmv_tp_shrink
+        self._expand = expand or bgmv_tp_expand
+        self._gather = all_gather or (lambda out, inp: _all_gather(out, inp, group))
+        self.rs = shard_rows if shard_rows is not None else tp_shard_rows(plan, tp_size)
+        self.n_tokens = n_tokens if n_tokens is not None else plan.n_tokens
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.v_part = torch.empty(self.n_tokens, self.rs, dtype=torch.float32, device=dev)
+        self.v_gathered = torch.empty(tp_size, self.n_tokens, self.rs, dtype=torch.float32, device=dev)
+
+    def forward(self, layer: int, proj: int, x: torch.Tensor, y_shard: torch.Tensor,
+                scale: float = 1.0) -> torch.Tensor:
+        self._shrink(self.plan, layer, proj, self.tp_rank, self.tp_size, x, self.v_part)
+        if self.tp_size > 1:
+            self._gather(self.v_gathered, self.v_part)
+        else:
+            self.v_gathered[0].copy_(self.v_part)
+        return self._expand(self.plan, layer, proj, self.tp_rank, self.tp_size, self.v_gathered,
+                            y_shard, scale)
+
+    __call__ = forward
