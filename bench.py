@@ -560,6 +560,113 @@ def run_cfg4(args):
     print(json.dumps(line))
 
 
+# --------------------------------------------------------------------- cfg5
+def run_cfg5(args):
+    """BASELINE configs[4]: Llama-2-70B q/v (q 8192 -> 8192, v 8192 -> 1024)
+    tensor-parallel LoRA: every rank serves the same 256 decode tokens; rank i
+    shrinks its r/N rows, the shard outputs are all-gathered (NCCL over
+    NVLink) and rank i expands into its d_out/N output columns.  80 layers x
+    2 projections per step, captured in one CUDA graph (collectives included).
+    Strong scaling: the total work is fixed as N grows."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_20210_b200 import synth
+    from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, kernel_launch_count
+    from paper_2512_20210_b200.tp import TensorParallelLoRA
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.cfg5(n_layers=args.cfg5_layers, page_bytes=args.page_bytes)
+    shape = cfg.shape
+    pool = synth.build_pool(cfg)
+    store = AdapterStore(pool, shape, cfg.n_adapters, device=local)
+    for a, r in enumerate(cfg.ranks):
+        store.register(a, r)
+        img = synth.adapter_image(shape, r, a, device=dev)  # identical on every rank
+        store.write_pages(a, img.view(torch.uint8))
+        store.publish(a)
+        del img
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    T = len(ta)
+    L, NP = shape.n_layers, shape.n_proj
+    plan = BatchPlan(store, ta)
+    tp = TensorParallelLoRA(plan, rank, world)
+    x = torch.randn(L, T, shape.d_in[0], device=dev).to(torch.bfloat16)
+    ys = [torch.randn(L, T, shape.d_out[p] // world, device=dev).to(torch.bfloat16)
+          for p in range(NP)]
+
+    def step():
+        for l in range(L):
+            for p in range(NP):
+                tp(l, p, x[l], ys[p][l])
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    n_g0 = kernel_launch_count()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    per_replay = kernel_launch_count() - n_g0
+    graph.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    K = args.steps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(K):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    # per-rank algorithmic bytes of one (layer, proj) call: its A rows, its Bᵀ
+    # columns, x, its y shard RMW
+    per_call = statistics.mean(
+        sum((r // world) * shape.d_in[p] + r * (shape.d_out[p] // world) for r in cfg.ranks) * 2
+        + T * shape.d_in[p] * 2 + 2 * T * (shape.d_out[p] // world) * 2 for p in range(NP))
+    peak, peak_kind = load_peaks()
+    avg_call_ms = ms / (L * NP)
+    gather_bytes = world * T * (max(cfg.ranks) // world) * 4
+    line = {
+        "metric": METRIC, "value": T / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": (f"cfg5 tensor-parallel LoRA, Llama-2-70B q/v (q 8192->8192, "
+                                f"v 8192->1024), {L} layers x 2 per step, 256 tokens / "
+                                f"{cfg.n_adapters} adapters, r=[8,16,64][a%3], TP={world}"),
+                   "page_bytes": args.page_bytes, "parallelism": f"tp{world} (S-LoRA all-gather)",
+                   "cuda_graph": True, "all_gather_bytes_per_call": gather_bytes,
+                   "l2": "inputs > L2: adapter pages of 160 (layer, proj) blocks per step"},
+        "gpu_launches": per_replay * K,
+        "roofline": {"bound": "hbm", "achieved": per_call / (avg_call_ms / 1e3) / 1e9,
+                     "peak": peak, "unit": "GB/s",
+                     "frac": per_call / (avg_call_ms / 1e3) / 1e9 / peak, "traffic": None,
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": per_call,
+                     "avg_launch_us": avg_call_ms * 1e3,
+                     "note": "per (layer, proj) call = shrink + all-gather + expand on one rank"},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -571,9 +678,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the 64 calls eagerly")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4"],
+    ap.add_argument("--cfg5-layers", type=int, default=80)
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg2 = decode BGMV (headline), cfg3 = prefill SGMV, "
-                         "cfg4 = trace-driven decode with LSTM prefetch")
+                         "cfg4 = trace-driven decode with LSTM prefetch, "
+                         "cfg5 = tensor-parallel 70B (run under torchrun for N > 1)")
     ap.add_argument("--cfg4-adapters", type=int, default=1000)
     ap.add_argument("--cfg4-images", type=int, default=4)
     ap.add_argument("--cfg4-pool-gib", type=float, default=16.0)
@@ -587,6 +696,8 @@ def main():
         run_reference(args)
     elif args.workload == "cfg4":
         run_cfg4(args)
+    elif args.workload == "cfg5":
+        run_cfg5(args)
     else:
         run_ours(args)
 
