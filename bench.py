@@ -195,8 +195,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2512_20210_b200 import synth
-    from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, bgmv, kernel_launch_count,
-                                            sgmv)
+    from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, bgmv, bgmv_layer,
+                                            kernel_launch_count, sgmv)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -230,8 +230,20 @@ def run_ours(args):
     y = torch.randn(L * NP, T, 4096, device=dev).to(torch.bfloat16)
     stream = torch.cuda.current_stream()
 
+    # decode: both projections of a layer (they read the same x) in one
+    # launch unless --per-proj; prefill: one launch pair per (layer, proj)
+    fused = not prefill and not args.per_proj
+    LPS = NP if not fused else 1  # launches per layer
+
     def step(ev=None):
         for l in range(L):
+            if fused:
+                if ev is not None:
+                    ev[2 * l].record()
+                bgmv_layer(plan, l, x[l], [y[l * NP + p] for p in range(NP)])
+                if ev is not None:
+                    ev[2 * l + 1].record()
+                continue
             for p in range(NP):
                 if ev is not None:
                     ev[2 * (l * NP + p)].record()
@@ -286,11 +298,11 @@ def run_ours(args):
         for _ in range(3):  # per-launch durations (separate, serialised replays)
             tgraph.replay()
             torch.cuda.synchronize()
-            kern_ms += [gevs[2 * i].elapsed_time(gevs[2 * i + 1]) for i in range(L * NP)]
+            kern_ms += [gevs[2 * i].elapsed_time(gevs[2 * i + 1]) for i in range(L * LPS)]
     else:
         launches = kernel_launch_count() - n0
         kern_ms = [evs[k][2 * i].elapsed_time(evs[k][2 * i + 1])
-                   for k in range(K) for i in range(L * NP)]
+                   for k in range(K) for i in range(L * LPS)]
     step_ms = start.elapsed_time(end) / K
     mean_kern_ms = statistics.mean(kern_ms)
     if world > 1:
@@ -334,6 +346,9 @@ def run_ours(args):
 
     # ---- roofline of the op (per (layer, proj) call, mean over the timed region)
     per_call = statistics.mean(call_bytes(shape, cfg.ranks, p, T) for p in range(NP))
+    if fused:  # one launch applies every projection of the layer (x read once)
+        per_call = sum(call_bytes(shape, cfg.ranks, p, T) for p in range(NP)) - \
+            (NP - 1) * T * shape.d_in[0] * shape.esize
     if prefill:  # every adapter serves one 512-token segment; weights read once per tile
         toks = cfg.tokens_per_adapter
         flops = statistics.mean(sum(2 * toks * r * (shape.d_in[p] + shape.d_out[p])
@@ -341,7 +356,7 @@ def run_ours(args):
     peak, peak_kind = load_peaks()
     # average launch duration over the timed region: the step is the L·NP
     # launches back to back (overlapping through PDL), nothing else
-    avg_launch_ms = step_ms / (L * NP)
+    avg_launch_ms = step_ms / (L * LPS)
     achieved = per_call / (avg_launch_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "bgmv_traffic.json")
@@ -374,6 +389,7 @@ def run_ours(args):
                    "page_bytes": args.page_bytes, "tokens_per_step_per_gpu": T,
                    "parallelism": f"request-sharded x{world} (no collective)",
                    "cuda_graph": graph is not None,
+                   "launches_per_layer": LPS,
                    "l2": ("inputs > L2: 2.1 GiB of adapter pages + 12 GiB activations per step"
                           if prefill else
                           "inputs > L2: 3.84 GB of adapter pages + 192 MiB activations per step")},
@@ -678,6 +694,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the 64 calls eagerly")
+    ap.add_argument("--per-proj", action="store_true",
+                    help="decode: one launch per (layer, proj) instead of one per layer")
     ap.add_argument("--cfg5-layers", type=int, default=80)
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg2 = decode BGMV (headline), cfg3 = prefill SGMV, "

@@ -278,6 +278,13 @@ uint32_t plora_plan_num_segments(const plora_plan* plan);
 int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                plora_stream_t stream);
+/* Every projection p of `layer` at once (they read the same x, as q/k/v of
+ * an attention block do): ys[p] += scale · (x · A_pᵀ) · B_pᵀ with row stride
+ * y_strides[p].  One launch when the projections have equal shapes (the
+ * per-call fixed cost is paid once per layer), else one per projection. */
+int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x_stride,
+                     void* const* ys, const uint64_t* y_strides, float scale,
+                     plora_stream_t stream);
 /* Same contract, prefill path (tcgen05 tensor cores; v rounded to the
  * storage dtype between shrink and expand). */
 int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,

@@ -451,3 +451,30 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     return 0;
   });
 }
+
+extern "C" int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x,
+                                uint64_t x_stride, void* const* ys, const uint64_t* y_strides,
+                                float scale, plora_stream_t stream) {
+  return guard([&] {
+    if (!plan) throw ValidationError("null plan");
+    if (!ys || !y_strides) throw ValidationError("null ys or y_strides");
+    const plora_store& st = *plan->store;
+    const ModelGeom& g = st.geom;
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) {
+      if (g.m.d_in[p] != g.m.d_in[0])
+        throw ValidationError("plora_bgmv_layer: projections read different input widths");
+      check_io(plan, layer, p, x, x_stride, ys[p], y_strides[p]);
+    }
+    if (g.esize == 2 && plan->n_layer_proj == g.m.n_proj) {
+      DeviceCtx ctx(st.device);
+      launch_bgmv_cluster_layer(*plan, layer, x, x_stride, ys, y_strides, scale,
+                                static_cast<cudaStream_t>(stream));
+      return 0;
+    }
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) {  // shapes differ: one launch per projection
+      const int rc = plora_bgmv(plan, layer, p, x, x_stride, ys[p], y_strides[p], scale, stream);
+      if (rc < 0) return rc;
+    }
+    return 0;
+  });
+}

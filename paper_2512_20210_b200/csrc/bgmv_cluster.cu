@@ -61,10 +61,13 @@ struct CArgs {
   const ClusterChunk* chunks;
   const uint32_t* cl_off;
   const char* x;
-  char* y;
   uint64_t x_stride_b;
-  uint64_t y_stride_b;
-  uint64_t blk_mult;  // (layer, proj) block of a rank-r adapter starts at element r · blk_mult
+  // per projection of the launch (chunk record field `proj`): output, its row
+  // stride, and where the (layer, proj) block of a rank-r adapter starts
+  // (element r · blk_mult)
+  char* y[PLORA_MAX_PROJ];
+  uint64_t y_stride_b[PLORA_MAX_PROJ];
+  uint64_t blk_mult[PLORA_MAX_PROJ];
   uint32_t log2_page;
   uint32_t d_in, d_out;
   uint32_t cs, ks, ns;  // cluster size, slice widths (elements)
@@ -146,7 +149,7 @@ struct Piece {
 };
 
 struct Rec {  // chunk record fields (ClusterChunk), read from a smem ring
-  uint32_t table_off, rank, ntok, flags, row0, nrows;
+  uint32_t table_off, rank, ntok, flags, row0, nrows, proj;
   __device__ explicit Rec(const uint32_t* w) {
     table_off = w[0];
     rank = w[1] & 0xffffu;
@@ -154,6 +157,7 @@ struct Rec {  // chunk record fields (ClusterChunk), read from a smem ring
     flags = w[1] >> 24;
     row0 = w[2] & 0xffffu;
     nrows = (w[2] >> 16) & 0xffu;
+    proj = w[2] >> 24;
   }
 };
 
@@ -170,7 +174,7 @@ __device__ __forceinline__ uint32_t piece_geom(const CArgs& p, const Slice& sl,
   const uint32_t nA = c.nrows * pg.pprA;
   if (q >= nA + c.nrows * pg.pprB) return 0;
   const uint32_t L = p.log2_page;
-  const uint64_t a_base = static_cast<uint64_t>(c.rank) * p.blk_mult;  // elements
+  const uint64_t a_base = static_cast<uint64_t>(c.rank) * p.blk_mult[c.proj];  // elements
   uint64_t lo;
   uint32_t len, dst, k;
   if (q < nA) {
@@ -227,9 +231,9 @@ __device__ __forceinline__ uint32_t my_piece(const CArgs& p, const Slice& sl, co
     if (lane >= 4 || r >= c.nrows) return 0;
     const bool isb = pw >= 2;
     const uint64_t lo =
-        (isb ? static_cast<uint64_t>(c.rank) * (p.blk_mult + p.d_in) +
+        (isb ? static_cast<uint64_t>(c.rank) * (p.blk_mult[c.proj] + p.d_in) +
                    static_cast<uint64_t>(c.row0 + r) * p.d_out + sl.n0
-             : static_cast<uint64_t>(c.rank) * p.blk_mult +
+             : static_cast<uint64_t>(c.rank) * p.blk_mult[c.proj] +
                    static_cast<uint64_t>(c.row0 + r) * p.d_in + sl.k0) * 2;
     x.len = isb ? pg.NB : pg.KB;
     x.dst = isb ? kChunkRows * pg.KSB + r * pg.NSB : r * pg.KSB;
@@ -380,7 +384,8 @@ __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uin
       if (lane < c.ntok && KB)
         ptx::bulk_g2s(jb + lane * KSB, p.x + tokx * p.x_stride_b + sl.k0 * 2, KB, &bar.jfull[jbuf]);
       else if (lane >= 16 && lane - 16 < c.ntok && NB)
-        ptx::bulk_g2s(jb + kJobTok * KSB + (lane - 16) * NSB, p.y + tokx * p.y_stride_b + sl.n0 * 2,
+        ptx::bulk_g2s(jb + kJobTok * KSB + (lane - 16) * NSB,
+                      p.y[c.proj] + tokx * p.y_stride_b[c.proj] + sl.n0 * 2,
                       NB, &bar.jfull[jbuf]);
     }
     __syncwarp();
@@ -595,7 +600,7 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     if (tid == 0) trace_put(p, idx, 11);
     if ((flags & kChunkLast) && cc < ntok) {  // y[tok cc] += scale · (hi + lo), once per job
       const char* yrow = smem + p.off_jb + (jord & 1u) * p.jb_bytes + kJobTok * KSB + cc * NSB;
-      char* yg = p.y + ch->tok[cc] * p.y_stride_b + static_cast<uint64_t>(sl.n0) * 2;
+      char* yg = p.y[ch->proj] + ch->tok[cc] * p.y_stride_b[ch->proj] + static_cast<uint64_t>(sl.n0) * 2;
       auto put = [&](uint32_t col, float v) {
         const float o = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(yrow + col * 2));
         *reinterpret_cast<__nv_bfloat16*>(yg + col * 2) = __float2bfloat16_rn(fmaf(p.scale, v, o));
@@ -706,29 +711,26 @@ ClusterGeom cluster_geom(uint32_t d_in, uint32_t d_out, int device) {
   return g;
 }
 
-void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
-                         uint64_t x_stride, void* y, uint64_t y_stride, float scale,
-                         cudaStream_t stream) {
+namespace {
+
+void launch(const plora_plan& plan, const ClusterWork& cw, uint32_t layer, const uint32_t* projs,
+            uint32_t np, const void* x, uint64_t x_stride, void* const* ys,
+            const uint64_t* y_strides, float scale, cudaStream_t stream) {
   const plora_store& st = *plan.store;
   const ModelGeom& gm = st.geom;
-  const ClusterWork& cw = plan.cwork[proj];
   const ClusterGeom& g = cw.geom;
   if (g.n_clusters == 0) return;  // no LoRA token in the batch
-  if (gm.m.d_in[proj] % 8 || gm.m.d_out[proj] % 8)
-    throw ValidationError("bf16 BGMV needs d_in and d_out multiples of 8");
   CArgs a{};
   a.arena = st.arena;
   a.table = st.d_table;
   a.chunks = plan.d_cchunks + cw.chunks_off;
   a.cl_off = plan.d_ccl_off + cw.cl_off;
   a.x = static_cast<const char*>(x);
-  a.y = static_cast<char*>(y);
   a.x_stride_b = x_stride * 2;
-  a.y_stride_b = y_stride * 2;
-  a.blk_mult = gm.blk_mult(layer, proj);
   a.log2_page = st.log2_page;
-  a.d_in = gm.m.d_in[proj];
-  a.d_out = gm.m.d_out[proj];
+  a.d_in = gm.m.d_in[projs[0]];
+  a.d_out = gm.m.d_out[projs[0]];
+  if (a.d_in % 8 || a.d_out % 8) throw ValidationError("bf16 BGMV needs d_in and d_out multiples of 8");
   a.cs = g.cs;
   a.ks = g.ks;
   a.ns = g.ns;
@@ -742,10 +744,14 @@ void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, 
   a.off_part = a.off_hdr + kHdrBytes;
   a.off_ring = a.off_part + kPartBytes;
   a.scale = scale;
-  {
-    const uint64_t P = 1ull << st.log2_page;
-    a.fast = a.d_in % a.ks == 0 && a.d_out % a.ns == 0 && P % (2ull * a.ks) == 0 &&
-             P % (2ull * a.ns) == 0 && a.blk_mult % a.ks == 0 && (a.blk_mult + a.d_in) % a.ns == 0;
+  const uint64_t P = 1ull << st.log2_page;
+  a.fast = a.d_in % a.ks == 0 && a.d_out % a.ns == 0 && P % (2ull * a.ks) == 0 &&
+           P % (2ull * a.ns) == 0;
+  for (uint32_t i = 0; i < np; ++i) {
+    a.y[i] = static_cast<char*>(ys[i]);
+    a.y_stride_b[i] = y_strides[i] * 2;
+    a.blk_mult[i] = gm.blk_mult(layer, projs[i]);
+    a.fast = a.fast && a.blk_mult[i] % a.ks == 0 && (a.blk_mult[i] + a.d_in) % a.ns == 0;
   }
   a.trace = trace_buffer(g.n_clusters * g.cs * kTraceChunks * 128);
   cudaLaunchConfig_t cfg{};
@@ -766,6 +772,25 @@ void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, 
   cfg.numAttrs = 2;
   PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_cluster_kernel, a));
   count_launch();
+}
+
+}  // namespace
+
+void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
+                         uint64_t x_stride, void* y, uint64_t y_stride, float scale,
+                         cudaStream_t stream) {
+  void* ys[1] = {y};
+  const uint64_t strides[1] = {y_stride};
+  launch(plan, plan.cwork[proj], layer, &proj, 1, x, x_stride, ys, strides, scale, stream);
+}
+
+void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const void* x,
+                               uint64_t x_stride, void* const* ys, const uint64_t* y_strides,
+                               float scale, cudaStream_t stream) {
+  uint32_t projs[PLORA_MAX_PROJ];
+  for (uint32_t i = 0; i < plan.n_layer_proj; ++i) projs[i] = i;
+  launch(plan, plan.cwork_layer, layer, projs, plan.n_layer_proj, x, x_stride, ys, y_strides,
+         scale, stream);
 }
 
 }  // namespace plora

@@ -177,47 +177,65 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
         cjobs.push_back(j);
       }
     const uint32_t nj = static_cast<uint32_t>(cjobs.size());
-    for (uint32_t p = 0; p < g.m.n_proj; ++p) {
-      ClusterWork& cw = cwork[p];
+    // One chunk list per launch: the jobs of the given projections (tagged
+    // with their index in the launch) LPT-assigned to clusters by bytes
+    // (heaviest first onto the least-loaded cluster, ties: lowest index).
+    auto build = [&](ClusterWork& cw, const uint32_t* projs, uint32_t np) {
       cw = ClusterWork{};
-      if (nj == 0) continue;
-      const uint32_t din = g.m.d_in[p], dout = g.m.d_out[p];
+      if (nj == 0) return;
+      const uint32_t din = g.m.d_in[projs[0]], dout = g.m.d_out[projs[0]];
       cw.geom = cluster_geom(din, dout, st.device);
-      const uint32_t nc = std::min(cw.geom.n_clusters, nj);
+      const uint32_t nw = nj * np;
+      const uint32_t nc = std::min(cw.geom.n_clusters, nw);
       cw.geom.n_clusters = nc;
-      // LPT: heaviest job first onto the least-loaded cluster (ties: lowest index)
-      std::vector<uint32_t> jo(nj);
+      std::vector<uint32_t> jo(nw);  // work item w = job w % nj of projection w / nj
       std::iota(jo.begin(), jo.end(), 0u);
-      auto cost = [&](uint32_t j) {
-        return static_cast<uint64_t>(cjobs[j].rank + cjobs[j].ntok) * (din + dout);
+      auto cost = [&](uint32_t w) {
+        const ClusterJob& j = cjobs[w % nj];
+        return static_cast<uint64_t>(j.rank + j.ntok) * (din + dout);
       };
       std::stable_sort(jo.begin(), jo.end(), [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
       std::vector<uint64_t> load(nc, 0);
       std::vector<std::vector<uint32_t>> lists(nc);
-      for (uint32_t j : jo) {
+      for (uint32_t w : jo) {
         const uint32_t c = static_cast<uint32_t>(std::min_element(load.begin(), load.end()) - load.begin());
-        load[c] += cost(j);
-        lists[c].push_back(j);
+        load[c] += cost(w);
+        lists[c].push_back(w);
       }
       cw.chunks_off = static_cast<uint32_t>(cchunks.size());
       cw.cl_off = static_cast<uint32_t>(ccl_off.size());
       for (uint32_t c = 0; c < nc; ++c) {
         ccl_off.push_back(static_cast<uint32_t>(cchunks.size()) - cw.chunks_off);
-        for (uint32_t j : lists[c])
-          for (uint32_t r0 = 0; r0 < cjobs[j].rank; r0 += kChunkRows) {
+        for (uint32_t w : lists[c]) {
+          const ClusterJob& j = cjobs[w % nj];
+          for (uint32_t r0 = 0; r0 < j.rank; r0 += kChunkRows) {
             ClusterChunk ch{};
-            ch.table_off = cjobs[j].table_off;
-            ch.rank = static_cast<uint16_t>(cjobs[j].rank);
-            ch.ntok = static_cast<uint8_t>(cjobs[j].ntok);
-            for (uint32_t t = 0; t < kJobTok; ++t) ch.tok[t] = cjobs[j].tok[t];
+            ch.table_off = j.table_off;
+            ch.rank = static_cast<uint16_t>(j.rank);
+            ch.ntok = static_cast<uint8_t>(j.ntok);
+            ch.proj = static_cast<uint8_t>(w / nj);
+            for (uint32_t t = 0; t < kJobTok; ++t) ch.tok[t] = j.tok[t];
             ch.row0 = static_cast<uint16_t>(r0);
-            ch.nrows = static_cast<uint8_t>(std::min(kChunkRows, cjobs[j].rank - r0));
+            ch.nrows = static_cast<uint8_t>(std::min(kChunkRows, j.rank - r0));
             ch.flags = static_cast<uint8_t>((r0 == 0 ? kChunkFirst : 0) |
-                                            (r0 + kChunkRows >= cjobs[j].rank ? kChunkLast : 0));
+                                            (r0 + kChunkRows >= j.rank ? kChunkLast : 0));
             cchunks.push_back(ch);
           }
+        }
       }
       ccl_off.push_back(static_cast<uint32_t>(cchunks.size()) - cw.chunks_off);
+    };
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) build(cwork[p], &p, 1);
+    n_layer_proj = 0;
+    cwork_layer = ClusterWork{};
+    bool same = g.m.n_proj > 1;
+    for (uint32_t p = 1; p < g.m.n_proj; ++p)
+      same = same && g.m.d_in[p] == g.m.d_in[0] && g.m.d_out[p] == g.m.d_out[0];
+    if (same) {
+      uint32_t all[PLORA_MAX_PROJ];
+      for (uint32_t p = 0; p < g.m.n_proj; ++p) all[p] = p;
+      build(cwork_layer, all, g.m.n_proj);
+      n_layer_proj = g.m.n_proj;
     }
   }
 

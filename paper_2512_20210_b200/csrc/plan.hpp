@@ -120,7 +120,7 @@ struct ClusterChunk {
   uint8_t flags;       // kChunkFirst | kChunkLast of the job
   uint16_t row0;
   uint8_t nrows;
-  uint8_t pad0;
+  uint8_t proj;        // index into the launch's projection list (plora_bgmv_layer)
   uint32_t pad1;
   uint32_t tok[kJobTok];  // x / y row of each job token
 };
@@ -170,6 +170,8 @@ struct plora_plan {
   uint64_t v_elems = 0;
   plora::ProjWork proj[PLORA_MAX_PROJ];
   plora::ClusterWork cwork[PLORA_MAX_PROJ];
+  plora::ClusterWork cwork_layer;  // every projection of a layer in one launch (same d_in, d_out)
+  uint32_t n_layer_proj = 0;       // 0: the projections' shapes differ, no fused launch
   uint32_t n_tiles = 0;
 
   std::vector<plora::BgmvUnit> units;
@@ -211,6 +213,10 @@ uint64_t* trace_buffer(uint64_t need_bytes);
 void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
                          uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                          cudaStream_t stream);
+// Every projection of `layer` (they read the same x) in one launch.
+void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const void* x,
+                               uint64_t x_stride, void* const* ys, const uint64_t* y_strides,
+                               float scale, cudaStream_t stream);
 // bf16 decode op (bgmv_ring.cu): persistent TMA ring + warp-level tensor cores.
 void launch_bgmv_ring(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
                       uint64_t x_stride, void* y, uint64_t y_stride, float scale,

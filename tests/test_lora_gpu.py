@@ -273,3 +273,29 @@ def test_ring_stress_random_ranks(cuda):
     for proj in (0, 1):
         yd, ref = _run(s, 0, proj, ta, scale=0.5, salt=proj)
         assert rel_err(yd, ref) <= TOL_BF16, proj
+
+
+@pytest.mark.parametrize("page_bytes", [2048, 2097152])
+def test_bgmv_layer_fused_equals_per_projection(cuda, page_bytes):
+    """plora_bgmv_layer (q and v of a layer in one launch) computes exactly
+    what two plora_bgmv calls do: same chunks, same partial sums, same order."""
+    from paper_2512_20210_b200.lora import bgmv_layer
+    cfg = synth.cfg2(n_layers=2, page_bytes=page_bytes)
+    s = Setup(cfg)
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    T = len(ta)
+    x = synth.activations(T, 4096, torch.bfloat16, "x").cuda()
+    y0 = [synth.activations(T, 4096, torch.bfloat16, "y", salt=p).cuda() for p in range(2)]
+    plan = BatchPlan(s.store, ta)
+    sep = [y.clone() for y in y0]
+    for p in range(2):
+        bgmv(plan, 1, p, x, sep[p], 0.75)
+    fused = [y.clone() for y in y0]
+    n0 = kernel_launch_count()
+    bgmv_layer(plan, 1, x, fused, 0.75)
+    torch.cuda.synchronize()
+    assert kernel_launch_count() - n0 == 1
+    for p in range(2):
+        assert torch.equal(fused[p], sep[p])
+    ref = s.oracle(1, 1, x.cpu(), y0[1].cpu(), ta, scale=0.75)
+    assert rel_err(fused[1], ref) <= TOL_BF16
