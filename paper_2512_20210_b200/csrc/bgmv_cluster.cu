@@ -412,7 +412,7 @@ __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uin
 //      accumulators stay in registers across a job.
 constexpr uint32_t kSThreads = kSWarps * 32;
 constexpr uint32_t kEThreads = kEWarps * 32;
-constexpr uint32_t kMaxTiles = 1024 / 16 / kEWarps;  // 16-column expand tiles per warp (ns <= 1024)
+constexpr uint32_t kMaxTiles = (1024 / 16 + kEWarps - 1) / kEWarps;  // 16-column expand tiles per warp (ns <= 1024)
 
 __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_t cl) {
   const uint32_t tid = threadIdx.x, w = tid >> 5, lane = tid & 31;

@@ -25,7 +25,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2512_20210_b200 import _native as N, synth  # noqa: E402
-from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, bgmv  # noqa: E402
+from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, bgmv, bgmv_layer  # noqa: E402
 
 K = 64
 
@@ -40,31 +40,34 @@ def main():
         store.publish(a)
     ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
     plan = BatchPlan(store, ta)
+    fused = "--layer" in sys.argv  # q and v in one launch (plora_bgmv_layer)
     geom = (C.c_uint32 * 8)()
     N.check(N.lib().plora_debug_plan_geom(plan.handle, 0, geom))
     names = ("cs", "ks", "ns", "slots", "slot_bytes", "smem", "clusters", "chunks")
     print("geometry:", dict(zip(names, list(geom))))
     x = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
     y = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
+    y2 = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
+    call = (lambda: bgmv_layer(plan, 1, x, [y, y2])) if fused else (lambda: bgmv(plan, 1, 0, x, y))
     for _ in range(3):
-        bgmv(plan, 1, 0, x, y)
+        call()
     ctas = geom[0] * geom[6]
     buf = torch.zeros(ctas * K * 16, dtype=torch.int64, device="cuda")
     N.check(N.lib().plora_debug_set_trace(buf.data_ptr(), buf.numel() * 8))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    bgmv(plan, 1, 0, x, y)
+    call()
     e1.record()
     torch.cuda.synchronize()
     N.check(N.lib().plora_debug_set_trace(None, 0))
     # untraced timing of the same call
     for _ in range(3):
-        bgmv(plan, 1, 0, x, y)
+        call()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record()
     for _ in range(20):
-        bgmv(plan, 1, 0, x, y)
+        call()
     e3.record()
     torch.cuda.synchronize()
     t = buf.view(ctas, K, 16).cpu().numpy().astype(np.int64)
@@ -93,6 +96,10 @@ def main():
           f"lookahead-landed -> slot wait start median {np.median(pre):.2f} us")
     land = (t[..., 0] - t[..., 5])[(t[..., 0] > 0) & (t[..., 5] > 0)] / 1e3
     print(f"data latency (issued -> consumer saw it) median {np.median(land):.2f} us")
+    first_ready = np.array([(t[c, 0, 0] - tstart[c]) for c in range(ctas) if t[c, 0, 0] > 0]) / 1e3
+    print(f"first chunk ready after CTA start: median {np.median(first_ready):.2f} max {first_ready.max():.2f} us")
+    nchunks = (t[..., 0] > 0).sum(axis=1)
+    print(f"chunks per CTA min/med/max {nchunks.min()}/{int(np.median(nchunks))}/{nchunks.max()}")
     print(f"producer slot wait median {np.median(wait_slot):.2f} us, p90 {np.percentile(wait_slot, 90):.2f}")
     def med(a, b):
         m = (t[..., a] > 0) & (t[..., b] > 0)
