@@ -21,11 +21,13 @@
 //          partial.  The last CTA of a tile (arrival counter) sums the KS
 //          partials in split order (deterministic) and writes V in bf16 — the
 //          rounding point between shrink and expand.
-//  expand  CTA (tile, 128-column block): D[128 × 128] = V · Bᵀ[:, block]
-//          (tcgen05, K = r16) with the Bᵀ block gathered from pages
-//          (MN-major SW128) and V / y tiles loaded by TMA; the epilogue adds
-//          D into the y tile in shared memory and TMA-stores it (rows of a
-//          partial tile, which belong to the next run, are stored per row).
+//  expand  CTA (tile, 4 column blocks of 128): D[128 × 128] = V · Bᵀ[:, block]
+//          (tcgen05, K = r16) per block, with the V tile loaded once by TMA,
+//          the Bᵀ blocks gathered from pages (MN-major SW128) and the y tiles
+//          TMA-loaded into a 2-stage ring, two TMEM accumulators; the
+//          epilogue adds D into the y tile in shared memory and TMA-stores
+//          it (rows of a partial tile, which belong to the next run, are
+//          stored per row).
 // Rank <= 128; d_in % 64 == 0; d_out % 128 == 0; bf16 stores (otherwise the
 // exact CUDA-core BGMV path runs, see plora_sgmv).
 #include <cuda.h>
@@ -263,6 +265,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------ expand
+// CTA (tile, group of kGroupBlocks 128-column blocks): the V tile is loaded
+// once; the Bᵀ block and y tile of block b go to stage b % 2 and the MMA to
+// TMEM accumulator b % 2, so the epilogue of block b overlaps the loads and
+// MMA of block b + 1.
+constexpr uint32_t kGroupBlocks = 4;
+constexpr uint32_t kETmemCols = 2 * kBlockN;
+// warps 0 TMA, 1-3 Bᵀ gathers, 4-7 epilogue, 8 MMA issuer (its own warp: the
+// epilogue releases the accumulators the MMA loop waits for)
+constexpr int kEThreads = 288;
+
 struct ExpandArgs {
   const char* arena;
   const uint32_t* table;
@@ -273,46 +285,59 @@ struct ExpandArgs {
   uint32_t log2_page;
   uint32_t d_in;
   uint32_t d_out;
-  uint32_t nblk;  // d_out / kBlockN
+  uint32_t ngroups;  // column groups per tile
   float scale;
 };
 
 struct ESmem {
-  static constexpr uint32_t y = 0;                 // [2 boxes][128 rows × 128 B] SW128
-  static constexpr uint32_t v = y + 32768;         // [2 atoms][128 rows × 128 B] SW128 (K-major)
-  static constexpr uint32_t b = v + 32768;         // [2 col groups][r16 rows × 128 B] SW128 (MN-major)
-  static constexpr uint32_t bars = b + 32768;      // in_full, b_full, acc_full
-  static constexpr uint32_t tmem_slot = bars + 3 * 8;
+  static constexpr uint32_t v = 0;                  // [2 atoms][128 rows × 128 B] SW128 (K-major)
+  static constexpr uint32_t y = v + 32768;          // [2 stages][2 boxes][128 rows × 128 B] SW128
+  static constexpr uint32_t b = y + 2 * 32768;      // [2 stages][2 col groups][r16 × 128 B] MN-major
+  static constexpr uint32_t bars = b + 2 * 32768;
+  // v_full, y_full[2], y_empty[2], b_full[2], b_empty[2], acc_full[2], acc_empty[2]
+  static constexpr uint32_t n_bars = 13;
+  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
   static constexpr uint32_t total = tmem_slot + 8;
   static constexpr uint32_t alloc = total + 1024;
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kEThreads, 1)
     sgmv_expand_kernel(const ExpandArgs p, const __grid_constant__ CUtensorMap tmap_y,
                        const __grid_constant__ CUtensorMap tmap_v) {
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* in_full = reinterpret_cast<uint64_t*>(smem + ESmem::bars);
-  uint64_t* b_full = in_full + 1;
-  uint64_t* acc_full = in_full + 2;
+  uint64_t* v_full = reinterpret_cast<uint64_t*>(smem + ESmem::bars);
+  uint64_t* y_full = v_full + 1;
+  uint64_t* y_empty = v_full + 3;
+  uint64_t* b_full = v_full + 5;
+  uint64_t* b_empty = v_full + 7;
+  uint64_t* acc_full = v_full + 9;
+  uint64_t* acc_empty = v_full + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ESmem::tmem_slot);
 
-  const uint32_t tile_i = blockIdx.x / p.nblk, nb = blockIdx.x % p.nblk;
+  const uint32_t tile_i = blockIdx.x / p.ngroups, grp = blockIdx.x % p.ngroups;
   const SgmvTile tile = p.tiles[tile_i];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r = tile.rank, r16 = (r + 15) & ~15u;
   const uint64_t bt = (static_cast<uint64_t>(r) * p.blk_mult + static_cast<uint64_t>(r) * p.d_in) * 2;
   const PagedSrc src{p.arena, p.table, tile.table_off, p.log2_page};
-  const uint32_t col0 = nb * kBlockN;
+  const uint32_t nblk = min(kGroupBlocks, p.d_out / kBlockN - grp * kGroupBlocks);
+  const uint32_t col_base = grp * kGroupBlocks * kBlockN;
   const uint32_t vboxes = r16 > 64 ? 2 : 1;
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(in_full, 1);
-    ptx::mbar_init(b_full, kGatherThreads);
-    ptx::mbar_init(acc_full, 1);
+    ptx::mbar_init(v_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&y_full[i], 1);
+      ptx::mbar_init(&y_empty[i], 1);
+      ptx::mbar_init(&b_full[i], kGatherThreads);
+      ptx::mbar_init(&b_empty[i], 1);
+      ptx::mbar_init(&acc_full[i], 1);
+      ptx::mbar_init(&acc_empty[i], 1);
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 4) ptx::tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, kETmemCols);
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmap_y);
     ptx::prefetch_tmap(&tmap_v);
@@ -323,118 +348,145 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ------------------------------- TMA: y tile (2 boxes) and V tile (1-2 boxes)
+    // ----------------------- TMA: V tile once, then the y tile of each block
     if (lane == 0) {
       ptx::pdl_wait();  // V comes from the shrink; y from earlier kernels
-      ptx::mbar_arrive_expect_tx(in_full, 2 * 16384 + vboxes * 16384);
-      for (uint32_t bx = 0; bx < 2; ++bx)
-        ptx::tma_load_2d(smem + ESmem::y + bx * 16384, &tmap_y, static_cast<int32_t>(col0 + bx * 64),
-                         static_cast<int32_t>(tile.row0), in_full);
+      ptx::mbar_arrive_expect_tx(v_full, vboxes * 16384);
       for (uint32_t bx = 0; bx < vboxes; ++bx)
         ptx::tma_load_2d(smem + ESmem::v + bx * 16384, &tmap_v, static_cast<int32_t>(bx * 64),
-                         static_cast<int32_t>(tile_i * kTileM), in_full);
+                         static_cast<int32_t>(tile_i * kTileM), v_full);
+      for (uint32_t b = 0; b < nblk; ++b) {
+        const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
+        ptx::mbar_wait(&y_empty[st], ph ^ 1u);
+        ptx::mbar_arrive_expect_tx(&y_full[st], 2 * 16384);
+        for (uint32_t bx = 0; bx < 2; ++bx)
+          ptx::tma_load_2d(smem + ESmem::y + st * 32768 + bx * 16384, &tmap_y,
+                           static_cast<int32_t>(col_base + b * kBlockN + bx * 64),
+                           static_cast<int32_t>(tile.row0), &y_full[st]);
+      }
     }
   } else if (warp < 4) {
-    // ----------------------------------------- Bᵀ block gather (paged rows)
+    // ----------------------------------- Bᵀ block gathers (paged rows)
     // Thread wt owns rank rows wt and wt + 96; with pages >= 256 B a row's
-    // 256-byte block slice lies in one page (one lookup, both issued first).
+    // 256-byte block slice lies in one page (one lookup, issued a block ahead).
     const uint32_t wt = threadIdx.x - 32;
     const uint32_t lbo = r16 * 128;  // stride between the two 64-column groups
     const bool fast = p.log2_page >= 8;
     const uint64_t pmask = (1ull << p.log2_page) - 1;
-    auto row_off = [&](uint32_t j) {
-      return bt + (static_cast<uint64_t>(j) * p.d_out + col0) * 2;
+    auto row_off = [&](uint32_t j, uint32_t b) {
+      return bt + (static_cast<uint64_t>(j) * p.d_out + col_base + b * kBlockN) * 2;
     };
-    uint32_t phys[2];
+    auto lookup = [&](uint32_t j, uint32_t b) -> uint32_t {
+      return (fast && j < r && b < nblk) ? __ldg(p.table + tile.table_off + static_cast<uint32_t>(row_off(j, b) >> p.log2_page)) : 0u;
+    };
+    uint32_t ph0 = lookup(wt, 0), ph1 = lookup(wt + kGatherThreads, 0);
+    for (uint32_t b = 0; b < nblk; ++b) {
+      const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
+      const uint32_t nx0 = lookup(wt, b + 1), nx1 = lookup(wt + kGatherThreads, b + 1);
+      ptx::mbar_wait(&b_empty[st], ph ^ 1u);
+      char* bs = smem + ESmem::b + st * 32768;
 #pragma unroll
-    for (uint32_t h = 0; h < 2; ++h) {
-      const uint32_t j = wt + h * kGatherThreads;
-      phys[h] = (fast && j < r) ? __ldg(p.table + tile.table_off + static_cast<uint32_t>(row_off(j) >> p.log2_page)) : 0u;
+      for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t j = wt + h * kGatherThreads;
+        if (j >= r16) continue;
+        const uint64_t off = row_off(j, b);
+        const char* base = p.arena + (static_cast<uint64_t>(h ? ph1 : ph0) << p.log2_page) + (off & pmask);
+#pragma unroll
+        for (uint32_t q = 0; q < 16; ++q) {
+          char* dst = bs + (q >> 3) * lbo + swz(j, q & 7);
+          if (j >= r)
+            ptx::cp_async_16(dst, p.arena, 0);
+          else if (fast)
+            ptx::cp_async_16(dst, base + q * 16, 16);
+          else
+            ptx::cp_async_16(dst, src.at(off + q * 16), 16);
+        }
+      }
+      ptx::cp_async_mbar_arrive_noinc(&b_full[st]);
+      ph0 = nx0;
+      ph1 = nx1;
     }
-#pragma unroll
-    for (uint32_t h = 0; h < 2; ++h) {
-      const uint32_t j = wt + h * kGatherThreads;
-      if (j >= r16) continue;
-      const uint64_t off = row_off(j);
-      const char* base = p.arena + (static_cast<uint64_t>(phys[h]) << p.log2_page) + (off & pmask);
-#pragma unroll
-      for (uint32_t q = 0; q < 16; ++q) {
-        const uint32_t g = q >> 3, c = q & 7;
-        char* dst = smem + ESmem::b + g * lbo + swz(j, c);
-        if (j >= r)
-          ptx::cp_async_16(dst, p.arena, 0);
-        else if (fast)
-          ptx::cp_async_16(dst, base + q * 16, 16);
-        else
-          ptx::cp_async_16(dst, src.at(off + q * 16), 16);
+  } else if (warp == 8) {
+    if (lane == 0) {
+      // ------------------------------------------------------- MMA issuer
+      const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, kBlockN, false, true);
+      const uint32_t vbase = ptx::smem_u32(smem + ESmem::v);
+      const uint32_t lbo = r16 * 128;
+      ptx::mbar_wait(v_full, 0);
+      for (uint32_t b = 0; b < nblk; ++b) {
+        const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
+        ptx::mbar_wait(&b_full[st], ph);
+        ptx::mbar_wait(&acc_empty[st], ph ^ 1u);
+        ptx::fence_proxy_async_shared();
+        ptx::tc_fence_after();
+        const uint32_t bbase = ptx::smem_u32(smem + ESmem::b + st * 32768);
+        for (uint32_t kk = 0; kk < r16 / 16; ++kk)
+          ptx::umma_f16(tmem + st * kBlockN,
+                        ptx::smem_desc_sw128(vbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                        ptx::smem_desc_sw128(bbase + kk * 2048, lbo, 1024), idesc, kk != 0);
+        ptx::umma_commit(&b_empty[st]);
+        ptx::umma_commit(&acc_full[st]);
       }
     }
-    ptx::cp_async_mbar_arrive_noinc(b_full);
   } else {
-    if (warp == 4 && lane == 0) {
-      // ------------------------------------------------------- MMA issuer
-      ptx::mbar_wait(in_full, 0);
-      ptx::mbar_wait(b_full, 0);
-      ptx::fence_proxy_async_shared();
-      ptx::tc_fence_after();
-      const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, kBlockN, false, true);
-      const uint32_t vbase = ptx::smem_u32(smem + ESmem::v), bbase = ptx::smem_u32(smem + ESmem::b);
-      const uint32_t lbo = r16 * 128;
-      for (uint32_t kk = 0; kk < r16 / 16; ++kk)
-        ptx::umma_f16(tmem, ptx::smem_desc_sw128(vbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                      ptx::smem_desc_sw128(bbase + kk * 2048, lbo, 1024), idesc, kk != 0);
-      ptx::umma_commit(acc_full);
-    }
-    __syncwarp();
     // ------------------------------------------------- epilogue (warps 4-7)
     const uint32_t m = (warp - 4) * 32 + lane;  // tile row == TMEM lane
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
-    ptx::mbar_wait(acc_full, 0);  // also implies in_full (the MMA waited on it)
-    ptx::tc_fence_after();
-    char* ys = smem + ESmem::y;
     const bool full_tile = tile.nrows == kTileM;
-    char* yrow = p.y + static_cast<uint64_t>(tile.row0 + m) * p.y_stride_b + static_cast<uint64_t>(col0) * 2;
+    for (uint32_t b = 0; b < nblk; ++b) {
+      const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
+      const uint32_t col0 = col_base + b * kBlockN;
+      char* ys = smem + ESmem::y + st * 32768;
+      char* yrow = p.y + static_cast<uint64_t>(tile.row0 + m) * p.y_stride_b + static_cast<uint64_t>(col0) * 2;
+      ptx::mbar_wait(&y_full[st], ph);
+      ptx::mbar_wait(&acc_full[st], ph);
+      ptx::tc_fence_after();
 #pragma unroll 1
-    for (uint32_t q = 0; q < kBlockN / 16; ++q) {  // 16 columns = two 16-byte chunks
-      uint32_t rv[16];
-      ptx::tmem_ld_32x32b_x16(tmem + lane_base + q * 16, rv);
-      ptx::tmem_ld_wait();
+      for (uint32_t q = 0; q < kBlockN / 16; ++q) {  // 16 columns = two 16-byte chunks
+        uint32_t rv[16];
+        ptx::tmem_ld_32x32b_x16(tmem + lane_base + st * kBlockN + q * 16, rv);
+        ptx::tmem_ld_wait();
 #pragma unroll
-      for (uint32_t hh = 0; hh < 2; ++hh) {
-        const uint32_t chunk = (q * 2 + hh) & 7, box = (q * 2 + hh) >> 3;
-        uint4* yp = reinterpret_cast<uint4*>(ys + box * 16384 + swz(m, chunk));
-        uint4 yv = *yp;
-        __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&yv);
+        for (uint32_t hh = 0; hh < 2; ++hh) {
+          const uint32_t chunk = (q * 2 + hh) & 7, box = (q * 2 + hh) >> 3;
+          uint4* yp = reinterpret_cast<uint4*>(ys + box * 16384 + swz(m, chunk));
+          uint4 yv = *yp;
+          __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&yv);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float2 f = __bfloat1622float2(hy[i]);
-          f.x = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i]), f.x);
-          f.y = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i + 1]), f.y);
-          hy[i] = __floats2bfloat162_rn(f.x, f.y);
+          for (int i = 0; i < 4; ++i) {
+            float2 f = __bfloat1622float2(hy[i]);
+            f.x = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i]), f.x);
+            f.y = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i + 1]), f.y);
+            hy[i] = __floats2bfloat162_rn(f.x, f.y);
+          }
+          if (full_tile)
+            *yp = yv;
+          else if (m < tile.nrows)  // rows past the run belong to the next one
+            reinterpret_cast<uint4*>(yrow)[q * 2 + hh] = yv;
         }
-        if (full_tile)
-          *yp = yv;
-        else if (m < tile.nrows)  // rows past the run belong to the next one
-          reinterpret_cast<uint4*>(yrow)[q * 2 + hh] = yv;
       }
-    }
-    if (full_tile) {
-      ptx::fence_proxy_async_shared();  // generic-proxy smem writes -> TMA store
+      ptx::tc_fence_before();
+      if (full_tile) ptx::fence_proxy_async_shared();  // generic-proxy smem writes -> TMA store
       ptx::named_bar_sync(1, 128);
       if (warp == 4 && lane == 0) {
-        for (uint32_t bx = 0; bx < 2; ++bx)
-          ptx::tma_store_2d(&tmap_y, static_cast<int32_t>(col0 + bx * 64),
-                            static_cast<int32_t>(tile.row0), ys + bx * 16384);
-        ptx::bulk_commit();
-        ptx::bulk_wait_all();
+        ptx::mbar_arrive(&acc_empty[st]);
+        if (full_tile) {
+          for (uint32_t bx = 0; bx < 2; ++bx)
+            ptx::tma_store_2d(&tmap_y, static_cast<int32_t>(col0 + bx * 64),
+                              static_cast<int32_t>(tile.row0), ys + bx * 16384);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read();  // the store has read the stage: it may be refilled
+        }
+        ptx::mbar_arrive(&y_empty[st]);
       }
     }
+    if (warp == 4 && lane == 0) ptx::bulk_wait_all();
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 4) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, kTmemCols);
+    ptx::tmem_dealloc(tmem, kETmemCols);
   }
 }
 
@@ -535,9 +587,10 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     ea.log2_page = st.log2_page;
     ea.d_in = din;
     ea.d_out = dout;
-    ea.nblk = dout / kBlockN;
+    ea.ngroups = (dout / kBlockN + kGroupBlocks - 1) / kGroupBlocks;
     ea.scale = scale;
-    cfg.gridDim = dim3(plan->n_tiles * ea.nblk);
+    cfg.gridDim = dim3(plan->n_tiles * ea.ngroups);
+    cfg.blockDim = dim3(kEThreads);
     cfg.dynamicSmemBytes = ESmem::alloc;
     PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y, tmap_v));
     count_launch();
