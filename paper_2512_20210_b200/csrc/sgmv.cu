@@ -60,7 +60,9 @@ constexpr uint32_t kChunkK = 64;   // shrink K per stage (one 128-byte swizzle r
 constexpr uint32_t kBlockN = 128;  // expand output columns per CTA
 constexpr uint32_t kMaxRank = 128;
 constexpr uint32_t kTmemCols = 128;
-constexpr int kGatherThreads = 96;  // warps 1-3
+constexpr int kGatherThreads = 96;   // expand: warps 1-3
+constexpr int kSGather = 192;       // shrink: warps 1-3 and 5-7 (5-7 are idle until the epilogue)
+constexpr int kEGather = 224;       // expand: warps 1-3 and 9-12
 
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
   // 128-byte swizzle inside an 8-row × 128-byte atom
@@ -126,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::pdl_launch_dependents();  // the expand may start gathering its weights
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSStages; ++s) {
-      ptx::mbar_init(&full[s], 1 + kGatherThreads);
+      ptx::mbar_init(&full[s], 1 + kSGather);
       ptx::mbar_init(&empty[s], 1);
     }
     ptx::mbar_init(v_full, 1);
@@ -152,15 +154,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                          &full[st]);
       }
     }
-  } else if (warp < 4) {
+  }
+  if (warp >= 1 && warp != 4) {
     // ----------------------------------------------- A gathers (paged rows)
     // Thread wt owns rank rows wt and wt + 96.  With pages >= 256 B a row's
     // 128-byte piece of a chunk lies in one page: one page-table lookup per
     // row per chunk, issued a chunk ahead (before the slot wait), so the
     // lookups never serialise the copies.  Smaller pages: per-piece lookups.
-    const uint32_t wt = threadIdx.x - 32;
+    const uint32_t wt = warp < 4 ? threadIdx.x - 32 : threadIdx.x - 160 + 96;
     const bool fast = p.log2_page >= 8;
-    const uint32_t n0 = wt, n1 = wt + kGatherThreads;
+    const uint32_t n0 = wt, n1 = wt + kSGather;
     auto row_off = [&](uint32_t n, uint32_t kc) {
       return blk + (static_cast<uint64_t>(n) * p.d_in + k0 + kc * kChunkK) * 2;
     };
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(&empty[st], ph ^ 1u);
       char* wdst = smem + SSmem::stages + st * kSStageBytes + kTileM * kChunkK * 2;
 #pragma unroll
-      for (uint32_t h = 0; h < 2; ++h) {
+      for (uint32_t h = 0; h < 1; ++h) {  // r16 <= 128 < 192 threads: one row each
         const uint32_t n = h ? n1 : n0;
         if (n >= r16) continue;
         if (n >= r) {
@@ -195,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ph0 = nx0;
       ph1 = nx1;
     }
-  } else {
+  }
+  if (warp >= 4) {
     if (warp == 4 && lane == 0) {
       // ------------------------------------------------------- MMA issuer
       const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, r16, false, false);
@@ -273,7 +277,7 @@ constexpr uint32_t kGroupBlocks = 4;
 constexpr uint32_t kETmemCols = 2 * kBlockN;
 // warps 0 TMA, 1-3 Bᵀ gathers, 4-7 epilogue, 8 MMA issuer (its own warp: the
 // epilogue releases the accumulators the MMA loop waits for)
-constexpr int kEThreads = 288;
+constexpr int kEThreads = 416;  // + warps 9-12: more Bᵀ gather threads
 
 struct ExpandArgs {
   const char* arena;
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&y_full[i], 1);
       ptx::mbar_init(&y_empty[i], 1);
-      ptx::mbar_init(&b_full[i], kGatherThreads);
+      ptx::mbar_init(&b_full[i], kEGather);
       ptx::mbar_init(&b_empty[i], 1);
       ptx::mbar_init(&acc_full[i], 1);
       ptx::mbar_init(&acc_empty[i], 1);
@@ -365,11 +369,11 @@ __global__ void __launch_bounds__(kEThreads, 1)
                            static_cast<int32_t>(tile.row0), &y_full[st]);
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 4 || warp >= 9) {
     // ----------------------------------- Bᵀ block gathers (paged rows)
     // Thread wt owns rank rows wt and wt + 96; with pages >= 256 B a row's
     // 256-byte block slice lies in one page (one lookup, issued a block ahead).
-    const uint32_t wt = threadIdx.x - 32;
+    const uint32_t wt = warp < 4 ? threadIdx.x - 32 : threadIdx.x - 288 + 96;
     const uint32_t lbo = r16 * 128;  // stride between the two 64-column groups
     const bool fast = p.log2_page >= 8;
     const uint64_t pmask = (1ull << p.log2_page) - 1;
@@ -379,15 +383,15 @@ __global__ void __launch_bounds__(kEThreads, 1)
     auto lookup = [&](uint32_t j, uint32_t b) -> uint32_t {
       return (fast && j < r && b < nblk) ? __ldg(p.table + tile.table_off + static_cast<uint32_t>(row_off(j, b) >> p.log2_page)) : 0u;
     };
-    uint32_t ph0 = lookup(wt, 0), ph1 = lookup(wt + kGatherThreads, 0);
+    uint32_t ph0 = lookup(wt, 0), ph1 = 0;
     for (uint32_t b = 0; b < nblk; ++b) {
       const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
-      const uint32_t nx0 = lookup(wt, b + 1), nx1 = lookup(wt + kGatherThreads, b + 1);
+      const uint32_t nx0 = lookup(wt, b + 1), nx1 = 0;
       ptx::mbar_wait(&b_empty[st], ph ^ 1u);
       char* bs = smem + ESmem::b + st * 32768;
 #pragma unroll
-      for (uint32_t h = 0; h < 2; ++h) {
-        const uint32_t j = wt + h * kGatherThreads;
+      for (uint32_t h = 0; h < 1; ++h) {  // r16 <= 128 < 224 gather threads: one row each
+        const uint32_t j = wt;
         if (j >= r16) continue;
         const uint64_t off = row_off(j, b);
         const char* base = p.arena + (static_cast<uint64_t>(h ? ph1 : ph0) << p.log2_page) + (off & pmask);
