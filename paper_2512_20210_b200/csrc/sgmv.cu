@@ -62,7 +62,7 @@ constexpr uint32_t kMaxRank = 128;
 constexpr uint32_t kTmemCols = 128;
 constexpr int kGatherThreads = 96;   // expand: warps 1-3
 constexpr int kSGather = 192;       // shrink: warps 1-3 and 5-7 (5-7 are idle until the epilogue)
-constexpr int kEGather = 224;       // expand: warps 1-3 and 9-12
+constexpr int kEGather = 96;        // expand: warps 1-3
 
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
   // 128-byte swizzle inside an 8-row × 128-byte atom
@@ -81,7 +81,7 @@ struct PagedSrc {
 };
 
 // ------------------------------------------------------------------ shrink
-constexpr int kSStages = 4;
+constexpr int kSStages = 4;  // a deep per-CTA ring beats more CTAs here (measured: 2 stages x3 CTAs 108 us, 3x2 92, 4x1 75)
 constexpr uint32_t kSStageBytes = 32768;  // X [128 × 64] 16 KiB + A [r16 × 64] <= 16 KiB
 
 struct ShrinkArgs {
@@ -273,11 +273,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // once; the Bᵀ block and y tile of block b go to stage b % 2 and the MMA to
 // TMEM accumulator b % 2, so the epilogue of block b overlaps the loads and
 // MMA of block b + 1.
-constexpr uint32_t kGroupBlocks = 4;
-constexpr uint32_t kETmemCols = 2 * kBlockN;
+constexpr uint32_t kEBlockN = 64;     // output columns per block (one 128-byte swizzle row)
+constexpr uint32_t kGroupBlocks = 8;  // blocks per CTA (512 columns)
+constexpr uint32_t kETmemCols = 2 * kEBlockN;
 // warps 0 TMA, 1-3 Bᵀ gathers, 4-7 epilogue, 8 MMA issuer (its own warp: the
 // epilogue releases the accumulators the MMA loop waits for)
-constexpr int kEThreads = 416;  // + warps 9-12: more Bᵀ gather threads
+constexpr int kEThreads = 288;
 
 struct ExpandArgs {
   const char* arena;
@@ -293,11 +294,11 @@ struct ExpandArgs {
   float scale;
 };
 
-struct ESmem {
+struct ESmem {  // ~97 KB: two expand CTAs per SM
   static constexpr uint32_t v = 0;                  // [2 atoms][128 rows × 128 B] SW128 (K-major)
-  static constexpr uint32_t y = v + 32768;          // [2 stages][2 boxes][128 rows × 128 B] SW128
-  static constexpr uint32_t b = y + 2 * 32768;      // [2 stages][2 col groups][r16 × 128 B] MN-major
-  static constexpr uint32_t bars = b + 2 * 32768;
+  static constexpr uint32_t y = v + 32768;          // [2 stages][128 rows × 128 B] SW128
+  static constexpr uint32_t b = y + 2 * 16384;      // [2 stages][r16 × 128 B] MN-major SW128
+  static constexpr uint32_t bars = b + 2 * 16384;
   // v_full, y_full[2], y_empty[2], b_full[2], b_empty[2], acc_full[2], acc_empty[2]
   static constexpr uint32_t n_bars = 13;
   static constexpr uint32_t tmem_slot = bars + n_bars * 8;
@@ -305,7 +306,7 @@ struct ESmem {
   static constexpr uint32_t alloc = total + 1024;
 };
 
-__global__ void __launch_bounds__(kEThreads, 1)
+__global__ void __launch_bounds__(kEThreads, 2)
     sgmv_expand_kernel(const ExpandArgs p, const __grid_constant__ CUtensorMap tmap_y,
                        const __grid_constant__ CUtensorMap tmap_v) {
   extern __shared__ char smem_raw[];
@@ -325,8 +326,8 @@ __global__ void __launch_bounds__(kEThreads, 1)
   const uint32_t r = tile.rank, r16 = (r + 15) & ~15u;
   const uint64_t bt = (static_cast<uint64_t>(r) * p.blk_mult + static_cast<uint64_t>(r) * p.d_in) * 2;
   const PagedSrc src{p.arena, p.table, tile.table_off, p.log2_page};
-  const uint32_t nblk = min(kGroupBlocks, p.d_out / kBlockN - grp * kGroupBlocks);
-  const uint32_t col_base = grp * kGroupBlocks * kBlockN;
+  const uint32_t nblk = min(kGroupBlocks, p.d_out / kEBlockN - grp * kGroupBlocks);
+  const uint32_t col_base = grp * kGroupBlocks * kEBlockN;
   const uint32_t vboxes = r16 > 64 ? 2 : 1;
 
   if (threadIdx.x == 0) {
@@ -362,42 +363,40 @@ __global__ void __launch_bounds__(kEThreads, 1)
       for (uint32_t b = 0; b < nblk; ++b) {
         const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
         ptx::mbar_wait(&y_empty[st], ph ^ 1u);
-        ptx::mbar_arrive_expect_tx(&y_full[st], 2 * 16384);
-        for (uint32_t bx = 0; bx < 2; ++bx)
-          ptx::tma_load_2d(smem + ESmem::y + st * 32768 + bx * 16384, &tmap_y,
-                           static_cast<int32_t>(col_base + b * kBlockN + bx * 64),
-                           static_cast<int32_t>(tile.row0), &y_full[st]);
+        ptx::mbar_arrive_expect_tx(&y_full[st], 16384);
+        ptx::tma_load_2d(smem + ESmem::y + st * 16384, &tmap_y,
+                         static_cast<int32_t>(col_base + b * kEBlockN),
+                         static_cast<int32_t>(tile.row0), &y_full[st]);
       }
     }
-  } else if (warp < 4 || warp >= 9) {
+  } else if (warp < 4) {
     // ----------------------------------- Bᵀ block gathers (paged rows)
     // Thread wt owns rank rows wt and wt + 96; with pages >= 256 B a row's
     // 256-byte block slice lies in one page (one lookup, issued a block ahead).
-    const uint32_t wt = warp < 4 ? threadIdx.x - 32 : threadIdx.x - 288 + 96;
-    const uint32_t lbo = r16 * 128;  // stride between the two 64-column groups
-    const bool fast = p.log2_page >= 8;
+    const uint32_t wt = threadIdx.x - 32;
+    const bool fast = p.log2_page >= 7;  // a row's 128-byte block slice lies in one page
     const uint64_t pmask = (1ull << p.log2_page) - 1;
     auto row_off = [&](uint32_t j, uint32_t b) {
-      return bt + (static_cast<uint64_t>(j) * p.d_out + col_base + b * kBlockN) * 2;
+      return bt + (static_cast<uint64_t>(j) * p.d_out + col_base + b * kEBlockN) * 2;
     };
     auto lookup = [&](uint32_t j, uint32_t b) -> uint32_t {
       return (fast && j < r && b < nblk) ? __ldg(p.table + tile.table_off + static_cast<uint32_t>(row_off(j, b) >> p.log2_page)) : 0u;
     };
-    uint32_t ph0 = lookup(wt, 0), ph1 = 0;
+    uint32_t ph0 = lookup(wt, 0), ph1 = lookup(wt + kEGather, 0);
     for (uint32_t b = 0; b < nblk; ++b) {
       const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
-      const uint32_t nx0 = lookup(wt, b + 1), nx1 = 0;
+      const uint32_t nx0 = lookup(wt, b + 1), nx1 = lookup(wt + kEGather, b + 1);
       ptx::mbar_wait(&b_empty[st], ph ^ 1u);
-      char* bs = smem + ESmem::b + st * 32768;
+      char* bs = smem + ESmem::b + st * 16384;
 #pragma unroll
-      for (uint32_t h = 0; h < 1; ++h) {  // r16 <= 128 < 224 gather threads: one row each
-        const uint32_t j = wt;
+      for (uint32_t h = 0; h < 2; ++h) {  // rows wt and wt + 96
+        const uint32_t j = wt + h * kEGather;
         if (j >= r16) continue;
         const uint64_t off = row_off(j, b);
         const char* base = p.arena + (static_cast<uint64_t>(h ? ph1 : ph0) << p.log2_page) + (off & pmask);
 #pragma unroll
-        for (uint32_t q = 0; q < 16; ++q) {
-          char* dst = bs + (q >> 3) * lbo + swz(j, q & 7);
+        for (uint32_t q = 0; q < 8; ++q) {
+          char* dst = bs + swz(j, q);
           if (j >= r)
             ptx::cp_async_16(dst, p.arena, 0);
           else if (fast)
@@ -413,9 +412,9 @@ __global__ void __launch_bounds__(kEThreads, 1)
   } else if (warp == 8) {
     if (lane == 0) {
       // ------------------------------------------------------- MMA issuer
-      const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, kBlockN, false, true);
+      const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, kEBlockN, false, true);
       const uint32_t vbase = ptx::smem_u32(smem + ESmem::v);
-      const uint32_t lbo = r16 * 128;
+      const uint32_t lbo = r16 * 128;  // unused with one 64-column group
       ptx::mbar_wait(v_full, 0);
       for (uint32_t b = 0; b < nblk; ++b) {
         const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
@@ -423,9 +422,9 @@ __global__ void __launch_bounds__(kEThreads, 1)
         ptx::mbar_wait(&acc_empty[st], ph ^ 1u);
         ptx::fence_proxy_async_shared();
         ptx::tc_fence_after();
-        const uint32_t bbase = ptx::smem_u32(smem + ESmem::b + st * 32768);
+        const uint32_t bbase = ptx::smem_u32(smem + ESmem::b + st * 16384);
         for (uint32_t kk = 0; kk < r16 / 16; ++kk)
-          ptx::umma_f16(tmem + st * kBlockN,
+          ptx::umma_f16(tmem + st * kEBlockN,
                         ptx::smem_desc_sw128(vbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                         ptx::smem_desc_sw128(bbase + kk * 2048, lbo, 1024), idesc, kk != 0);
         ptx::umma_commit(&b_empty[st]);
@@ -439,22 +438,24 @@ __global__ void __launch_bounds__(kEThreads, 1)
     const bool full_tile = tile.nrows == kTileM;
     for (uint32_t b = 0; b < nblk; ++b) {
       const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
-      const uint32_t col0 = col_base + b * kBlockN;
-      char* ys = smem + ESmem::y + st * 32768;
+      const uint32_t col0 = col_base + b * kEBlockN;
+      char* ys = smem + ESmem::y + st * 16384;
       char* yrow = p.y + static_cast<uint64_t>(tile.row0 + m) * p.y_stride_b + static_cast<uint64_t>(col0) * 2;
       ptx::mbar_wait(&y_full[st], ph);
       ptx::mbar_wait(&acc_full[st], ph);
       ptx::tc_fence_after();
 #pragma unroll 1
-      for (uint32_t q = 0; q < kBlockN / 16; ++q) {  // 16 columns = two 16-byte chunks
+      for (uint32_t q = 0; q < kEBlockN / 16; ++q) {  // 16 columns = two 16-byte chunks
         uint32_t rv[16];
-        ptx::tmem_ld_32x32b_x16(tmem + lane_base + st * kBlockN + q * 16, rv);
+        ptx::tmem_ld_32x32b_x16(tmem + lane_base + st * kEBlockN + q * 16, rv);
         ptx::tmem_ld_wait();
 #pragma unroll
         for (uint32_t hh = 0; hh < 2; ++hh) {
-          const uint32_t chunk = (q * 2 + hh) & 7, box = (q * 2 + hh) >> 3;
-          uint4* yp = reinterpret_cast<uint4*>(ys + box * 16384 + swz(m, chunk));
-          uint4 yv = *yp;
+          const uint32_t chunk = q * 2 + hh;
+          const uint32_t ya = ptx::smem_u32(ys + swz(m, chunk));
+          uint4 yv;
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(yv.x), "=r"(yv.y), "=r"(yv.z), "=r"(yv.w) : "r"(ya));
           __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&yv);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -464,9 +465,10 @@ __global__ void __launch_bounds__(kEThreads, 1)
             hy[i] = __floats2bfloat162_rn(f.x, f.y);
           }
           if (full_tile)
-            *yp = yv;
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ya), "r"(yv.x), "r"(yv.y),
+                         "r"(yv.z), "r"(yv.w) : "memory");
           else if (m < tile.nrows)  // rows past the run belong to the next one
-            reinterpret_cast<uint4*>(yrow)[q * 2 + hh] = yv;
+            reinterpret_cast<uint4*>(yrow)[chunk] = yv;
         }
       }
       ptx::tc_fence_before();
@@ -475,9 +477,7 @@ __global__ void __launch_bounds__(kEThreads, 1)
       if (warp == 4 && lane == 0) {
         ptx::mbar_arrive(&acc_empty[st]);
         if (full_tile) {
-          for (uint32_t bx = 0; bx < 2; ++bx)
-            ptx::tma_store_2d(&tmap_y, static_cast<int32_t>(col0 + bx * 64),
-                              static_cast<int32_t>(tile.row0), ys + bx * 16384);
+          ptx::tma_store_2d(&tmap_y, static_cast<int32_t>(col0), static_cast<int32_t>(tile.row0), ys);
           ptx::bulk_commit();
           ptx::bulk_wait_read();  // the store has read the stage: it may be refilled
         }
@@ -591,7 +591,7 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     ea.log2_page = st.log2_page;
     ea.d_in = din;
     ea.d_out = dout;
-    ea.ngroups = (dout / kBlockN + kGroupBlocks - 1) / kGroupBlocks;
+    ea.ngroups = (dout / kEBlockN + kGroupBlocks - 1) / kGroupBlocks;
     ea.scale = scale;
     cfg.gridDim = dim3(plan->n_tiles * ea.ngroups);
     cfg.blockDim = dim3(kEThreads);
