@@ -455,23 +455,44 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     if (tid == 0) trace_put(p, idx, 15);
     const uint32_t xa = ptx::smem_u32(smem + p.off_jb + (jord & 1u) * p.jb_bytes) + xoff;
     const uint32_t wa = ptx::smem_u32(smem + s * p.slot_bytes) + woff;
+    // Warp w takes k-step pairs w, w + kSWarps, ... (<= kPairs of them).  The
+    // schedule is software-pipelined by hand — pair j+1's fragment loads are
+    // issued before pair j's MMAs, into the other of two register sets (the
+    // asm statements keep program order; no register is copied while its
+    // load is in flight).
+    constexpr uint32_t kPairs = kMaxSlice / 32 / kSWarps;
     float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-    uint32_t k = 2 * w;
-#pragma unroll 2
-    for (; k + 1 < ksteps; k += 2 * kSWarps) {  // two k-steps per W fragment load
-      uint32_t a0[4], a1[4], b[4];
-      ptx::ldsm_x4(wa + k * 32, b);
-      ptx::ldsm_x4(xa + k * 32, a0);
-      ptx::ldsm_x4(xa + k * 32 + 32, a1);
-      if (half_tail && k + 1 == ksteps - 1) {  // k 8..15 of the last step lie past the slice
-        a1[2] = a1[3] = 0u;
-        b[3] = 0u;
+    float d2[4] = {0.f, 0.f, 0.f, 0.f}, d3[4] = {0.f, 0.f, 0.f, 0.f};  // shorter MMA chains
+    uint32_t fr[2][3][4];  // [set][W, x k-step 0, x k-step 1]
+#pragma unroll
+    for (uint32_t j = 0; j <= kPairs; ++j) {
+      const uint32_t kn = 2 * (w + j * kSWarps);
+      if (j < kPairs && kn + 1 < ksteps) {
+        ptx::ldsm_x4(wa + kn * 32, fr[j & 1][0]);
+        ptx::ldsm_x4(xa + kn * 32, fr[j & 1][1]);
+        ptx::ldsm_x4(xa + kn * 32 + 32, fr[j & 1][2]);
       }
-      const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
-      ptx::mma_bf16_16816(d0, a0, b0);
-      ptx::mma_bf16_16816(d1, a1, b1);
+      if (j > 0) {
+        const uint32_t kp = 2 * (w + (j - 1) * kSWarps);
+        uint32_t(&f)[3][4] = fr[(j - 1) & 1];
+        if (kp + 1 < ksteps) {
+          if (half_tail && kp + 1 == ksteps - 1) {  // k 8..15 of the last step lie past the slice
+            f[2][2] = f[2][3] = 0u;
+            f[0][3] = 0u;
+          }
+          const uint32_t b0[2] = {f[0][0], f[0][1]}, b1[2] = {f[0][2], f[0][3]};
+          ptx::mma_bf16_16816((j & 1) ? d0 : d2, f[1], b0);
+          ptx::mma_bf16_16816((j & 1) ? d1 : d3, f[2], b1);
+        }
+      }
     }
-    if (k < ksteps) {  // odd number of k-steps: the last one alone
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      d0[q] += d2[q];
+      d1[q] += d3[q];
+    }
+    if ((ksteps & 1u) && w == (ksteps / 2) % kSWarps) {  // odd number of k-steps: the last one
+      const uint32_t k = ksteps - 1;
       uint32_t a0[4], b[4];
       ptx::ldsm_x4(wa + k * 32, b);
       ptx::ldsm_x4(xa + k * 32, a0);
