@@ -73,12 +73,14 @@ __global__ void __launch_bounds__(128) tp_shrink_kernel(const TpArgs p) {
   const uint32_t row = p.tp_rank * rs + j;
   const uint64_t base = (static_cast<uint64_t>(job.rank) * p.blk_mult + static_cast<uint64_t>(row) * p.d_in) * 2;
   float acc[kJobTok] = {0.f, 0.f, 0.f, 0.f};
+  // unrolled so several (page-table lookup -> load) chains are in flight
+#pragma unroll 8
   for (uint32_t v8 = lane; v8 < p.d_in / 8; v8 += 32) {
-    const uint4 a = *reinterpret_cast<const uint4*>(paged(p, job.table_off, base + v8 * 16ull));
+    const uint4 a = __ldg(reinterpret_cast<const uint4*>(paged(p, job.table_off, base + v8 * 16ull)));
 #pragma unroll
     for (uint32_t t = 0; t < kJobTok; ++t) {
       if (t < job.ntok) {
-        const uint4 xv = *reinterpret_cast<const uint4*>(p.x + job.tok[t] * p.x_stride_b + v8 * 16ull);
+        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(p.x + job.tok[t] * p.x_stride_b + v8 * 16ull));
         acc[t] = fmaf(bf_lo(a.x), bf_lo(xv.x), acc[t]);
         acc[t] = fmaf(bf_hi(a.x), bf_hi(xv.x), acc[t]);
         acc[t] = fmaf(bf_lo(a.y), bf_lo(xv.y), acc[t]);
@@ -117,9 +119,10 @@ __global__ void __launch_bounds__(64) tp_expand_kernel(const TpArgs p) {
   if (c >= p.ncols) return;
   const uint64_t bt = (static_cast<uint64_t>(r) * p.blk_mult + static_cast<uint64_t>(r) * p.d_in) * 2;
   float acc[kJobTok][4] = {};
+#pragma unroll 8
   for (uint32_t jj = 0; jj < r; ++jj) {
     const uint64_t off = bt + (static_cast<uint64_t>(jj) * p.d_out + p.col0 + c) * 2;
-    const uint2 b = *reinterpret_cast<const uint2*>(paged(p, job.table_off, off));
+    const uint2 b = __ldg(reinterpret_cast<const uint2*>(paged(p, job.table_off, off)));
     const float b0 = bf_lo(b.x), b1 = bf_hi(b.x), b2 = bf_lo(b.y), b3 = bf_hi(b.y);
 #pragma unroll
     for (uint32_t t = 0; t < kJobTok; ++t) {
