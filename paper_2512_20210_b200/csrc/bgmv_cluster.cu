@@ -361,11 +361,12 @@ __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uin
     __syncwarp();
     const uint32_t* rw = recring + (idx % kRecRing) * 8;
     const Rec c(rw);
-    const uint32_t w = lane < 8 ? rw[lane] : 0u;
     ptx::mbar_wait(&bar.empty[s], ph ^ 1u);
-    if (lane < 8) hdr[s * 8 + lane] = w;  // the consumers read the record from here
-    __syncwarp();
-    if (lane == 0) {
+    if (lane == 0) {  // one thread writes the header and releases it with its arrival
+      const uint4* src = reinterpret_cast<const uint4*>(rw);
+      uint4* dst = reinterpret_cast<uint4*>(hdr + s * 8);
+      dst[0] = src[0];
+      dst[1] = src[1];
       ptx::mbar_arrive(&bar.full[s]);
       trace_put(p, idx, 13);
     }
