@@ -62,6 +62,7 @@ def lib() -> C.CDLL:
                                                P(u64)]),
             "ref_generate_catalog": (C.c_int, [u32, P(u32), P(dbl), u64, u64, u32, u32, u32,
                                                u32, P(u32), P(u64)]),
+            "ref_load_catalog_json": (i64, [C.c_char_p, P(u32), P(u64), u64]),
             "ref_generate_synthetic": (i64, [u32, dbl, dbl, dbl, u32, dbl, dbl, dbl, dbl, dbl,
                                              u64, P(dbl), P(u32), P(u32), P(u32), u64]),
         }
@@ -263,6 +264,18 @@ def generate_catalog(count, mix, seed, d=4096, k=4096, adapted=64, bpp=2):
     _check(lib().ref_generate_catalog(count, mr, mw, len(mix), seed, d, k, adapted, bpp, ranks,
                                       byts))
     return list(ranks), list(byts)
+
+
+def load_catalog_json(path, cap=4096):
+    """The reference's own load_catalog_json (base dims 4096/4096/64/bf16,
+    default size table): (ranks, bytes), or raises RefError with the code
+    (-1 ValidationError, -3 ConfigError, -5 ParseError)."""
+    ranks = (C.c_uint32 * cap)()
+    byts = (C.c_uint64 * cap)()
+    n = lib().ref_load_catalog_json(path.encode(), ranks, byts, cap)
+    if n < 0:
+        raise RefError(int(n), lib().ref_last_error().decode())
+    return list(ranks[:n]), list(byts[:n])
 
 
 def generate_synthetic(profile, duration_s, seed):

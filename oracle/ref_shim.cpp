@@ -29,12 +29,15 @@ using namespace lorasim;
 namespace {
 thread_local std::string g_err;
 
-// 0 ok; -1 ValidationError; -2 logic_error; -3 ConfigError; -4 other
+// 0 ok; -1 ValidationError; -2 logic_error; -3 ConfigError; -4 other; -5 ParseError
 template <class F>
 int guard(F&& f) {
   try {
     f();
     return 0;
+  } catch (const ParseError& e) {
+    g_err = e.what();
+    return -5;
   } catch (const ValidationError& e) {
     g_err = e.what();
     return -1;
@@ -236,6 +239,23 @@ int ref_generate_catalog(uint32_t count, const uint32_t* mix_ranks, const double
       bytes_out[i] = cat[i].weight_bytes;
     }
   });
+}
+
+// load_catalog_json over the reference's own parser: returns the entry count
+// (ranks / bytes filled up to cap) or a negative status (ref_last_error).
+int64_t ref_load_catalog_json(const char* path, uint32_t* ranks_out, uint64_t* bytes_out,
+                              uint64_t cap) {
+  int64_t n = -1;
+  const int rc = guard([&] {
+    LoraDims base{4096, 4096, 8, 64, 2};
+    auto cat = load_catalog_json(path, AdapterSizeTable{}, base);
+    n = static_cast<int64_t>(cat.size());
+    for (uint64_t i = 0; i < cat.size() && i < cap; ++i) {
+      ranks_out[i] = cat[i].dims.r;
+      bytes_out[i] = cat[i].weight_bytes;
+    }
+  });
+  return rc == 0 ? n : rc;
 }
 
 // ---- synthetic workload -------------------------------------------------------

@@ -7,8 +7,10 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass, field
 
+import json
+
 from . import _native as N
-from .errors import ValidationError
+from .errors import ConfigError, ParseError, ValidationError
 
 MiB = 1 << 20
 
@@ -112,4 +114,43 @@ def generate_catalog(count: int, mix: list[tuple[int, float]], seed: int,
     for i in range(count):
         dims = LoraDims(base.d, base.k, ranks[i], base.adapted_matrices, base.bytes_per_param)
         out.append(AdapterSpec(catalog_id(i, count), dims, nbytes[i], nbytes[i]))
+    return out
+
+
+def load_catalog_json(path: str, sizes: AdapterSizeTable | None = None,
+                      base: LoraDims | None = None) -> list[AdapterSpec]:
+    """load_catalog_json (src/adapter.cpp:81-108): a JSON array of
+    ``{"id": str, "rank": int[, "size_bytes": int]}``; sizes default to the
+    size table's bytes for the rank.  Errors as the reference raises them:
+    ConfigError (cannot open), ParseError (malformed / not an array / entry
+    without id or rank), ValidationError (empty catalog, invalid dims)."""
+    base = base if base is not None else LoraDims()
+    try:
+        with open(path) as f:
+            text = f.read()
+    except OSError:
+        raise ConfigError(f"cannot open adapter catalog: {path}") from None
+    try:
+        j = json.loads(text)
+    except json.JSONDecodeError as e:
+        raise ParseError(f"adapter catalog {path}: {e}") from None
+    if not isinstance(j, list):
+        raise ParseError("adapter catalog must be a JSON array")
+    out = []
+    for entry in j:
+        if not isinstance(entry, dict) or "id" not in entry or "rank" not in entry:
+            raise ParseError("catalog entry needs 'id' and 'rank'")
+        rank = entry["rank"]
+        if not isinstance(rank, int) or isinstance(rank, bool) or not 0 <= rank < 1 << 32:
+            raise ParseError(f"catalog entry {entry.get('id')!r}: rank must be an unsigned integer")
+        dims = LoraDims(base.d, base.k, rank, base.adapted_matrices, base.bytes_per_param)
+        if "size_bytes" in entry:
+            nbytes = entry["size_bytes"]
+            if not isinstance(nbytes, int) or isinstance(nbytes, bool) or nbytes < 0:
+                raise ParseError(f"catalog entry {entry['id']!r}: size_bytes must be an unsigned integer")
+        else:
+            nbytes = (sizes if sizes is not None else AdapterSizeTable()).bytes_for(rank)
+        out.append(AdapterSpec.sized(str(entry["id"]), dims, nbytes))
+    if not out:
+        raise ValidationError("adapter catalog is empty")
     return out

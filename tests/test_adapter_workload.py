@@ -89,3 +89,48 @@ def test_generate_synthetic_validation():
         generate_synthetic(SyntheticProfile(hot_set_size=0), 1.0, 1)
     with pytest.raises(ValidationError):
         generate_synthetic(SyntheticProfile(), -1.0, 1)
+
+
+CATALOGS = {
+    "golden": '[{"id": "alpha", "rank": 8}, {"id": "beta", "rank": 64, "size_bytes": 999}]',
+    "mixed": "[" + ", ".join(
+        f'{{"id": "a{i:03d}", "rank": {(8, 16, 32, 64, 128)[i % 5]}'
+        + (f', "size_bytes": {1 + 4096 * i}' if i % 3 == 0 else "") + "}" for i in range(40)) + "]",
+    "not_array": '{"id": "alpha", "rank": 8}',
+    "missing_rank": '[{"id": "alpha"}]',
+    "empty": "[]",
+    "malformed": '[{"id": "alpha", "rank": 8',
+    "zero_rank": '[{"id": "alpha", "rank": 0}]',
+}
+
+
+@pytest.mark.parametrize("name", sorted(CATALOGS))
+def test_load_catalog_json_matches_reference(ref, tmp_path, name):
+    """load_catalog_json (src/adapter.cpp:81-108) against the compiled
+    reference: the same specs, or the same error class."""
+    from paper_2512_20210_b200 import ConfigError, ParseError, ValidationError
+    from paper_2512_20210_b200.adapter import load_catalog_json
+    path = tmp_path / f"{name}.json"
+    path.write_text(CATALOGS[name])
+    codes = {ValidationError: -1, ConfigError: -3, ParseError: -5}
+    try:
+        want = ref.load_catalog_json(str(path))
+    except ref.RefError as e:
+        with pytest.raises(tuple(k for k, v in codes.items() if v == e.code)):
+            load_catalog_json(str(path))
+        return
+    got = load_catalog_json(str(path))
+    assert [s.dims.r for s in got] == want[0]
+    assert [s.weight_bytes for s in got] == want[1]
+    if name == "golden":  # tests/test_adapter.cpp:76-95
+        assert [s.id for s in got] == ["alpha", "beta"]
+        assert got[0].weight_bytes == 13 * (1 << 20)
+
+
+def test_load_catalog_json_missing_file_is_config_error(ref, tmp_path):
+    from paper_2512_20210_b200 import ConfigError
+    from paper_2512_20210_b200.adapter import load_catalog_json
+    with pytest.raises(ConfigError):
+        load_catalog_json(str(tmp_path / "does_not_exist.json"))
+    with pytest.raises(ref.RefError):
+        ref.load_catalog_json(str(tmp_path / "does_not_exist.json"))
