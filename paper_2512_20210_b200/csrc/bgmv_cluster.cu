@@ -102,7 +102,12 @@ struct Bars {
 };
 constexpr uint32_t kBarBytes = (2 * kMaxSlots + 4 + kX) * 8;
 constexpr uint32_t kHdrBytes = kMaxSlots * sizeof(ClusterChunk);
-constexpr uint32_t kPartBytes = 2 * kSWarps * kJobTok * kChunkRows * 4;  // shrink partials
+// The shrink group runs as two independent subgroups of kSubWarps warps on
+// alternating chunks: its per-chunk time is mostly fixed latency, so two
+// chunks in flight nearly double its throughput.
+constexpr uint32_t kSubWarps = 2;
+constexpr uint32_t kSubgroups = kSWarps / kSubWarps;
+constexpr uint32_t kPartBytes = kSubgroups * 2 * kSubWarps * kJobTok * kChunkRows * 4;  // shrink partials
 
 struct Slice {  // this CTA's input / output slice
   uint32_t k0, kb, n0, nb;  // first element, width (elements; may be 0 for tiny widths)
@@ -433,48 +438,46 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   const uint32_t xrow = (lane & 7) + ((lane >> 3) & 1) * 8;
   const uint32_t xoff = (xrow < kJobTok ? xrow : 0) * KSB + (lane >> 4) * 16;
   const uint32_t woff = (lane & 7) * KSB + (lane >> 3) * 16;
-  uint32_t jord = 0xffffffffu;
+  const uint32_t sg = w / kSubWarps, sw = w % kSubWarps;  // subgroup, warp within it
+  const bool lead = sw == 0 && lane == 0;
 #pragma unroll 1
-  for (uint32_t i = i0; i < i1; ++i) {
+  for (uint32_t i = i0 + sg; i < i1; i += kSubgroups) {  // this subgroup's chunks
     const uint32_t idx = i - i0, s = idx % p.slots, e = idx % kX;
-    if (tid == 0) trace_put(p, idx, 14);
+    if (lead) trace_put(p, idx, 14);
     ptx::mbar_wait(&bar.full[s], (idx / p.slots) & 1u);
-    if (tid == 0) trace_put(p, idx, 0);
+    if (lead) trace_put(p, idx, 0);
     const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
-    const uint32_t ntok = ch->ntok;
-    if (ch->flags & kChunkFirst) {
-      ++jord;
-      ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);
-    }
+    const uint32_t ntok = ch->ntok, jord = ch->jord;
+    if (ch->flags & kChunkFirst) ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);
     // Arm this chunk's exchange barrier: CS CTAs × kChunkRows rows × ntok
     // floats.  Peers' st.async may land before this (negative tx count is
     // fine: the phase also needs this arrival).  Aliasing bound: a peer's
     // shrink of chunk m needs its slot back, i.e. its expand of m - slots,
     // i.e. our partial of m - slots, i.e. our slot of that chunk, i.e. our
     // expand of m - 2·slots: kX >= 2·kMaxSlots keeps every live phase distinct.
-    if (tid == 0) ptx::mbar_arrive_expect_tx(&bar.xfull[e], p.cs * kChunkRows * ntok * 4);
-    if (tid == 0) trace_put(p, idx, 15);
+    if (lead) ptx::mbar_arrive_expect_tx(&bar.xfull[e], p.cs * kChunkRows * ntok * 4);
+    if (lead) trace_put(p, idx, 15);
     const uint32_t xa = ptx::smem_u32(smem + p.off_jb + (jord & 1u) * p.jb_bytes) + xoff;
     const uint32_t wa = ptx::smem_u32(smem + s * p.slot_bytes) + woff;
-    // Warp w takes k-step pairs w, w + kSWarps, ... (<= kPairs of them).  The
+    // Warp sw takes k-step pairs sw, sw + kSubWarps, ... (<= kPairs of them).  The
     // schedule is software-pipelined by hand — pair j+1's fragment loads are
     // issued before pair j's MMAs, into the other of two register sets (the
     // asm statements keep program order; no register is copied while its
     // load is in flight).
-    constexpr uint32_t kPairs = kMaxSlice / 32 / kSWarps;
+    constexpr uint32_t kPairs = kMaxSlice / 32 / kSubWarps;
     float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
     float d2[4] = {0.f, 0.f, 0.f, 0.f}, d3[4] = {0.f, 0.f, 0.f, 0.f};  // shorter MMA chains
     uint32_t fr[2][3][4];  // [set][W, x k-step 0, x k-step 1]
 #pragma unroll
     for (uint32_t j = 0; j <= kPairs; ++j) {
-      const uint32_t kn = 2 * (w + j * kSWarps);
+      const uint32_t kn = 2 * (sw + j * kSubWarps);
       if (j < kPairs && kn + 1 < ksteps) {
         ptx::ldsm_x4(wa + kn * 32, fr[j & 1][0]);
         ptx::ldsm_x4(xa + kn * 32, fr[j & 1][1]);
         ptx::ldsm_x4(xa + kn * 32 + 32, fr[j & 1][2]);
       }
       if (j > 0) {
-        const uint32_t kp = 2 * (w + (j - 1) * kSWarps);
+        const uint32_t kp = 2 * (sw + (j - 1) * kSubWarps);
         uint32_t(&f)[3][4] = fr[(j - 1) & 1];
         if (kp + 1 < ksteps) {
           if (half_tail && kp + 1 == ksteps - 1) {  // k 8..15 of the last step lie past the slice
@@ -492,7 +495,7 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
       d0[q] += d2[q];
       d1[q] += d3[q];
     }
-    if ((ksteps & 1u) && w == (ksteps / 2) % kSWarps) {  // odd number of k-steps: the last one
+    if ((ksteps & 1u) && sw == (ksteps / 2) % kSubWarps) {  // odd number of k-steps: the last one
       const uint32_t k = ksteps - 1;
       uint32_t a0[4], b[4];
       ptx::ldsm_x4(wa + k * 32, b);
@@ -504,23 +507,27 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
       const uint32_t b0[2] = {b[0], b[1]};
       ptx::mma_bf16_16816(d0, a0, b0);
     }
-    // d[0]/d[1] = (tok gq, rows 2cc, 2cc+1).  Partial buffers alternate by chunk
-    // parity: warp 0 reads buffer idx&1 before the next chunk's barrier, which
-    // every warp passes before writing that buffer again.
-    float* pb = part + (idx & 1u) * kSWarps * kJobTok * kChunkRows;
+    // d[0]/d[1] = (tok gq, rows 2cc, 2cc+1).  Each subgroup's partial buffers
+    // alternate by its chunk parity: the lead warp reads one before the
+    // subgroup's next barrier, which every warp of the subgroup passes before
+    // writing that buffer again.
+    float* pb = part + (sg * 2 + ((idx / kSubgroups) & 1u)) * kSubWarps * kJobTok * kChunkRows;
     if (gq < kJobTok) {
-      float* pw = pb + (w * kJobTok + gq) * kChunkRows + 2 * cc;
+      float* pw = pb + (sw * kJobTok + gq) * kChunkRows + 2 * cc;
       pw[0] = d0[0] + d1[0];
       pw[1] = d0[1] + d1[1];
     }
-    if (tid == 0) trace_put(p, idx, 8);
-    ptx::named_bar_sync(2, kSThreads);  // partials written; slot A rows read
-    if (tid == 0) trace_put(p, idx, 9);
-    if (w == 0) {
+    if (lead) trace_put(p, idx, 8);
+    if (sg == 0)  // partials written; slot A rows read (constant barrier ids)
+      ptx::named_bar_sync(2, kSubWarps * 32);
+    else
+      ptx::named_bar_sync(3, kSubWarps * 32);
+    if (lead) trace_put(p, idx, 9);
+    if (sw == 0) {
       if (lane < ntok * kChunkRows) {  // lane = tok · 8 + row: sum the warps, push
         float v = 0.f;
 #pragma unroll
-        for (uint32_t ww = 0; ww < kSWarps; ++ww) v += pb[ww * kJobTok * kChunkRows + lane];
+        for (uint32_t ww = 0; ww < kSubWarps; ++ww) v += pb[ww * kJobTok * kChunkRows + lane];
         const uint32_t t = lane / kChunkRows, r = lane % kChunkRows;
         const uint32_t local = xb0 + (e * kXSlotFloats + (t * kChunkRows + r) * kMaxCs + crank) * 4;
         const uint32_t lbar = ptx::smem_u32(&bar.xfull[e]);
@@ -549,15 +556,13 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   const bool tail8 = (sl.nb & 15u) != 0 && w == kEWarps - 1;  // a last 8-column tile
   ptx::pdl_wait();  // y is written below: the previous call must be complete
   float acc[kMaxTiles + 1][4];
-  uint32_t jord = 0xffffffffu;
 #pragma unroll 1
   for (uint32_t i = i0; i < i1; ++i) {
     const uint32_t idx = i - i0, s = idx % p.slots, e = idx % kX;
     ptx::mbar_wait(&bar.full[s], (idx / p.slots) & 1u);
     const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
-    const uint32_t ntok = ch->ntok, nrows = ch->nrows, flags = ch->flags;
+    const uint32_t ntok = ch->ntok, nrows = ch->nrows, flags = ch->flags, jord = ch->jord;
     if (flags & kChunkFirst) {
-      ++jord;
       ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);  // y rows of the job
 #pragma unroll
       for (uint32_t t = 0; t <= kMaxTiles; ++t)

@@ -206,14 +206,17 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       cw.cl_off = static_cast<uint32_t>(ccl_off.size());
       for (uint32_t c = 0; c < nc; ++c) {
         ccl_off.push_back(static_cast<uint32_t>(cchunks.size()) - cw.chunks_off);
+        uint32_t jord = 0;
         for (uint32_t w : lists[c]) {
           const ClusterJob& j = cjobs[w % nj];
+          const uint32_t this_job = jord++;
           for (uint32_t r0 = 0; r0 < j.rank; r0 += kChunkRows) {
             ClusterChunk ch{};
             ch.table_off = j.table_off;
             ch.rank = static_cast<uint16_t>(j.rank);
             ch.ntok = static_cast<uint8_t>(j.ntok);
             ch.proj = static_cast<uint8_t>(w / nj);
+            ch.jord = this_job;
             for (uint32_t t = 0; t < kJobTok; ++t) ch.tok[t] = j.tok[t];
             ch.row0 = static_cast<uint16_t>(r0);
             ch.nrows = static_cast<uint8_t>(std::min(kChunkRows, j.rank - r0));

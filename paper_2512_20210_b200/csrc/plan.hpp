@@ -121,7 +121,7 @@ struct ClusterChunk {
   uint16_t row0;
   uint8_t nrows;
   uint8_t proj;        // index into the launch's projection list (plora_bgmv_layer)
-  uint32_t pad1;
+  uint32_t jord;       // job ordinal within the cluster's list (job buffer jord & 1)
   uint32_t tok[kJobTok];  // x / y row of each job token
 };
 static_assert(sizeof(ClusterChunk) == 32, "ClusterChunk layout");
