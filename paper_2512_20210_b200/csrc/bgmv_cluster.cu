@@ -221,7 +221,7 @@ __device__ __forceinline__ void cp_async_wait_group() {
 // (Under a busy HBM a dependent global load takes ~1-1.5 µs.)
 constexpr int kAhead = 4;
 constexpr uint32_t kRecRing = 2 * kAhead;  // records, 32 bytes each
-constexpr uint32_t kRingBytes = kRecRing * 32 + kAhead * 32 * 4;
+constexpr uint32_t kRingBytes = kRecRing * 32 + kAhead * 32 * 4 * 3;  // records | entries | geometry
 
 // This lane's page piece of chunk c.  Aligned fast path (p.fast: every row
 // slice lies inside one page): producer warp pw owns rows 4·(pw&1) .. +3 of
@@ -258,6 +258,7 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
   Bars bar(smem, p.off_bar);
   uint32_t* recring = reinterpret_cast<uint32_t*>(smem + p.off_ring + pw * kRingBytes);  // [kRecRing][8]
   uint32_t* tblring = recring + kRecRing * 8;                                           // [kAhead][32]
+  uint2* georing = reinterpret_cast<uint2*>(tblring + kAhead * 32);  // [kAhead][32] {inpage, dst | len << 16}
   const uint32_t* recg = reinterpret_cast<const uint32_t*>(p.chunks);
   const Slice sl(p, crank);
   const uint64_t ef = ptx::policy_evict_first();
@@ -278,10 +279,12 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
   auto fetch_tbl = [&](uint32_t j) {  // page-table entry of this lane's piece of chunk j
     if (j >= n) return;
     const Rec c(recring + (j % kRecRing) * 8);
-    Piece x;
+    Piece x{};
     const uint32_t page = my_piece(p, sl, pg, c, pw, lane, x);
     if (x.len)
       cp_async_4(ptx::smem_u32(tblring + (j % kAhead) * 32 + lane), p.table + c.table_off + page);
+    // the piece's geometry rides along, so the issue step does not recompute it
+    georing[(j % kAhead) * 32 + lane] = make_uint2(x.inpage, x.len ? (x.dst | (x.len << 16)) : 0u);
   };
   // prologue: records 0 .. 2·kAhead-1 (waited), table entries 0 .. kAhead-1 (one group each)
   for (uint32_t j = 0; j < kRecRing; ++j) fetch_rec(j);
@@ -300,8 +303,11 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
     if (pw == 0 && lane == 0) trace_put(p, idx, 6);
     const Rec c(recring + (idx % kRecRing) * 8);
     char* sb = smem + s * p.slot_bytes;
+    const uint2 geo = georing[(idx % kAhead) * 32 + lane];
     Piece pc;
-    my_piece(p, sl, pg, c, pw, lane, pc);
+    pc.inpage = geo.x;
+    pc.dst = geo.y & 0xffffu;
+    pc.len = geo.y >> 16;
     const uint32_t phys = pc.len ? tblring[(idx % kAhead) * 32 + lane] : 0u;
     if (pw == 0 && lane == 0) trace_put(p, idx, 4);
     ptx::mbar_wait(&bar.empty[s], ph ^ 1u);
@@ -324,7 +330,13 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
       }
     }
     if (pw == 0 && lane == 0) trace_put(p, idx, 12);
-    bytes = __reduce_add_sync(0xffffffffu, bytes);
+    if (p.fast) {  // this warp's rows of the chunk × their slice bytes, no reduction needed
+      const uint32_t half = kChunkRows / 2, r0 = (pw & 1u) * half;
+      const uint32_t mine = c.nrows > r0 ? min(c.nrows - r0, half) : 0u;
+      bytes = mine * (pw >= 2 ? pg.NB : pg.KB);
+    } else {
+      bytes = __reduce_add_sync(0xffffffffu, bytes);
+    }
     if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.full[s], bytes);
     // ---- lookahead: table entries of idx + kAhead (its record landed), record of
     // idx + 2·kAhead into the ring slot idx just vacated
