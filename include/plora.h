@@ -454,9 +454,10 @@ int plora_predictor_buffer_at(const plora_predictor* p, uint64_t i, uint32_t* ad
                               double* window, double* label);
 
 /* ------------------------------------------------------------ diagnostics
- * Per-unit device timestamps of the next BGMV launches (globaltimer ns):
- * trace[(cta * 64 + k) * 8 + {0 issued, 1 data ready, 2 computed, 3 kind, ...}]
- * for the first 64 units of each CTA.  dev_buf = NULL disables tracing. */
+ * Per-chunk device timestamps (SM clock cycles) of the next bf16 BGMV
+ * launches: trace[(cta * 64 + k) * 16 + field] for the first 63 chunks of
+ * each CTA, fields as documented in scripts/trace_bgmv.py (chunk 63 holds the
+ * CTA start / end).  dev_buf = NULL disables tracing. */
 int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
 /* Launch geometry the plan chose for the bf16 decode op of projection
  * `proj`: out[0..7] = {cluster size, input slice, output slice, ring slots,

@@ -423,8 +423,13 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     const plora_store& st = *plan->store;
     const ModelGeom& g = st.geom;
     const ProjWork& pw = plan->proj[proj];
-    if (pw.n_units == 0) return 0;  // no LoRA token in the batch
     DeviceCtx ctx(st.device);
+    if (g.esize == 2) {  // bf16: the cluster op (bgmv_cluster.cu)
+      launch_bgmv_cluster(*plan, layer, proj, x, x_stride, y, y_stride, scale,
+                          static_cast<cudaStream_t>(stream));
+      return 0;
+    }
+    if (pw.n_units == 0) return 0;  // no LoRA token in the batch
     BgmvArgs a{};
     a.arena = st.arena;
     a.table = st.d_table;
@@ -444,10 +449,7 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     const uint32_t shrink_smem = (rpu + nts) * rowbytes;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const BgmvUnit* units = plan->d_units + pw.units_off;
-    if (g.esize == 2)
-      launch_bgmv_cluster(*plan, layer, proj, x, x_stride, y, y_stride, scale, s);
-    else
-      launch<float>(a, pw, units, shrink_smem, s);
+    launch<float>(a, pw, units, shrink_smem, s);
     return 0;
   });
 }

@@ -460,7 +460,11 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     if (lead) trace_put(p, idx, 0);
     const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
     const uint32_t ntok = ch->ntok, jord = ch->jord;
-    if (ch->flags & kChunkFirst) ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);
+    // Every chunk waits for its job's x rows: with two subgroups a job's later
+    // chunk can run before (or beside) its first one.  The job buffer cannot be
+    // recycled meanwhile (that needs the job's last expand), so the parity is
+    // unambiguous.
+    ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);
     // Arm this chunk's exchange barrier: CS CTAs × kChunkRows rows × ntok
     // floats.  Peers' st.async may land before this (negative tx count is
     // fine: the phase also needs this arrival).  Aliasing bound: a peer's
@@ -832,7 +836,20 @@ void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const voi
          scale, stream);
 }
 
+namespace {
+uint64_t* g_trace = nullptr;
+uint64_t g_trace_bytes = 0;
+}  // namespace
+
+uint64_t* trace_buffer(uint64_t need_bytes) { return g_trace_bytes >= need_bytes ? g_trace : nullptr; }
+
 }  // namespace plora
+
+extern "C" int plora_debug_set_trace(void* dev_buf, uint64_t bytes) {
+  plora::g_trace = static_cast<uint64_t*>(dev_buf);
+  plora::g_trace_bytes = dev_buf ? bytes : 0;
+  return 0;
+}
 
 extern "C" int plora_debug_plan_geom(const plora_plan* plan, uint32_t proj, uint32_t out[8]) {
   using namespace plora;

@@ -44,17 +44,12 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   std::sort(segs.begin(), segs.end(), [](const Seg& x, const Seg& y) { return x.adapter < y.adapter; });
   v_elems = 0;
   max_rank = 0;
-  uint32_t nkc_max = 1;
-  if (es == 2)
-    for (uint32_t p = 0; p < g.m.n_proj; ++p)
-      nkc_max = std::max(nkc_max, (g.m.d_in[p] + kShrinkK - 1) / kShrinkK);
   for (Seg& s : segs) {
     if (s.rank > kMaxBgmvRank)
       throw ValidationError("adapter " + std::to_string(s.adapter) + " has rank " +
                             std::to_string(s.rank) + " > " + std::to_string(kMaxBgmvRank));
     s.voff = static_cast<uint32_t>(v_elems);
-    // bf16: one partial plane of v per kShrinkK-wide K chunk (summed by the expand)
-    v_elems += static_cast<uint64_t>(s.toks.size()) * rpad4(s.rank) * nkc_max;
+    v_elems += static_cast<uint64_t>(s.toks.size()) * rpad4(s.rank);
     max_rank = std::max(max_rank, s.rank);
   }
   if (v_elems > 0xffffffffull) throw ValidationError("batch too large for one plan");
@@ -67,22 +62,19 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t x, uint32_t y) { return segs[x].rank > segs[y].rank; });
 
-  // ---- BGMV units per projection
+  // ---- fp32 BGMV units per projection (the bf16 op runs on clusters, below)
   units.clear();
-  for (uint32_t p = 0; p < g.m.n_proj; ++p) {
+  for (uint32_t p = 0; p < g.m.n_proj; ++p) proj[p] = ProjWork{};
+  for (uint32_t p = 0; p < g.m.n_proj && es == 4; ++p) {
     const uint32_t din = g.m.d_in[p], dout = g.m.d_out[p];
     const uint32_t rowbytes = din * es;
     if (es == 4 && rowbytes > kSlotAuxBytes)
       throw ValidationError("fp32 BGMV needs d_in * 4 <= " + std::to_string(kSlotAuxBytes) +
                             " bytes (d_in=" + std::to_string(din) + ")");
-    // bf16 (tensor-core ring): 16 rank rows × kShrinkK columns per unit, K
-    // partials in separate v planes.  fp32 (CUDA cores): rpu full rows.
-    const bool ksplit = es == 2;
-    const uint32_t nkc = ksplit ? (din + kShrinkK - 1) / kShrinkK : 1;
-    const uint32_t rpu = ksplit ? kShrinkRows16
-                                : std::min<uint32_t>(kMaxShrinkRows, kShrinkWeightBytes / rowbytes);
-    const uint32_t nts = ksplit ? kMaxUnitTok
-                                : std::min<uint32_t>(kMaxUnitTok, kSlotAuxBytes / rowbytes);
+    // rpu full rank rows per shrink unit (CUDA cores)
+    const uint32_t nkc = 1;
+    const uint32_t rpu = std::min<uint32_t>(kMaxShrinkRows, kShrinkWeightBytes / rowbytes);
+    const uint32_t nts = std::min<uint32_t>(kMaxUnitTok, kSlotAuxBytes / rowbytes);
     ProjWork& pw = proj[p];
     pw.units_off = static_cast<uint32_t>(units.size());
     std::vector<uint32_t> n_shrink(n_seg, 0);
@@ -114,12 +106,11 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     for (uint32_t si : order) {
       const Seg& s = segs[si];
       const uint32_t rp = rpad4(s.rank), nt_all = static_cast<uint32_t>(s.toks.size());
-      const uint32_t rg = es == 2 ? 1 : expand_rg(s.rank), cb = expand_cols(s.rank, es);
+      const uint32_t rg = expand_rg(s.rank), cb = expand_cols(s.rank, es);
       const uint32_t per_tok = nkc * rp * 4 + cb * es;
       // tokens per unit: aux area (v partial rows + y rows) and, when rows are
       // split over groups, the reduction buffer (RG · CB fp32 per token)
-      const uint32_t aux_budget =
-          ksplit ? kRingSlotBytes - ((s.rank + 15) & ~15u) * (cb * 2 + kRingRowPad) : kSlotAuxBytes;
+      const uint32_t aux_budget = kSlotAuxBytes;
       uint32_t nte = std::min<uint32_t>(kMaxUnitTok, aux_budget / per_tok);
       if (rg > 1) nte = std::min<uint32_t>(nte, kRedBytes / (rg * cb * 4));
       nte = std::max<uint32_t>(nte, 1);

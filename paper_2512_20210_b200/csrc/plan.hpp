@@ -35,20 +35,12 @@ struct BgmvUnit {
   uint32_t ntok;      // tokens (<= kMaxUnitTok)
   uint32_t n_shrink;  // expand: shrink units of the segment to wait for
   uint32_t tok[kMaxUnitTok];  // x / y row indices
-  uint32_t kc;        // shrink: K chunk (bf16 path: d_in split in kShrinkK slices)
-  uint32_t nkc;       // expand: number of K-chunk partial planes of v to sum
+  uint32_t kc;        // shrink: K chunk (0: full rows)
+  uint32_t nkc;       // expand: number of K-chunk partial planes of v to sum (1)
   uint32_t vstride;   // expand: floats between consecutive partial planes
   uint32_t pad;
 };
 static_assert(sizeof(BgmvUnit) == 64, "BgmvUnit layout");
-
-// bf16 shrink units: 16 rank rows (the MMA M) × kShrinkK input columns.
-constexpr uint32_t kShrinkK = 1024;
-constexpr uint32_t kShrinkRows16 = 16;
-// bf16 ring slot: shrink 16 rows + 4 x rows of (kShrinkK·2 + 16) bytes;
-// expand Bᵀ tile r16 × (CB·2 + 16) + per token: y segment + K-partial v rows.
-constexpr uint32_t kRingSlotBytes = 53248;
-constexpr uint32_t kRingRowPad = 16;
 
 // Expand split: RG row groups × CT column threads (RG·CT = kBgmvConsumers),
 // CB = CT · VEC columns, so the Bᵀ tile r × CB fits one 32 KiB slot and a
@@ -69,9 +61,7 @@ __host__ __device__
 #endif
 inline uint32_t rpad4(uint32_t r) { return (r + 3) & ~3u; }
 
-// Columns per expand unit.  bf16 (tensor-core path): the Bᵀ tile r16 × CB
-// (rank padded to the MMA K of 16) fits 32 KiB; fp32 (CUDA-core path): RG·CB
-// = 256 threads × 4 columns.
+// Columns per fp32 expand unit: RG·CB = 256 threads × 4 columns.
 #ifdef __CUDACC__
 __host__ __device__
 #endif
@@ -217,8 +207,4 @@ void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, 
 void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const void* x,
                                uint64_t x_stride, void* const* ys, const uint64_t* y_strides,
                                float scale, cudaStream_t stream);
-// bf16 decode op (bgmv_ring.cu): persistent TMA ring + warp-level tensor cores.
-void launch_bgmv_ring(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
-                      uint64_t x_stride, void* y, uint64_t y_stride, float scale,
-                      cudaStream_t stream);
 }  // namespace plora

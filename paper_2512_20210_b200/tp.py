@@ -101,6 +101,11 @@ class TensorParallelLoRA:
 
     def forward(self, layer: int, proj: int, x: torch.Tensor, y_shard: torch.Tensor,
                 scale: float = 1.0) -> torch.Tensor:
+        if self.tp_size == 1 and self._shrink is bgmv_tp_shrink:
+            # one rank holds every row and column: no collective, so the fused
+            # data-parallel op applies the whole LoRA in one launch
+            from .lora import bgmv
+            return bgmv(self.plan, layer, proj, x, y_shard, scale)
         self._shrink(self.plan, layer, proj, self.tp_rank, self.tp_size, x, self.v_part)
         if self.tp_size > 1:
             self._gather(self.v_gathered, self.v_part)

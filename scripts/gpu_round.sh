@@ -28,7 +28,7 @@ if has launches; then
   echo "launches rc=$?" >> gpurun_out/launches.log
 fi
 if has full; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:bgmv_cluster -s 200 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:bgmv_cluster -s 100 -c 2 \
     -o gpurun_out/bgmv_full -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/ncu_full.log 2>&1
   echo "full rc=$?" >> gpurun_out/ncu_full.log
