@@ -102,6 +102,24 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, int32_t c0, int32
       : "memory");
 }
 
+// 2-D TMA tensor tile reduce-add into global memory (the element type of the
+// tensor map; the add happens in L2), bulk async-group.
+__device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, int32_t c0, int32_t c1,
+                                                  const void* src) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          tmap),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
+
+// Wait until the smem sources of all but the newest `N` committed bulk groups
+// have been read.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read_n() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }

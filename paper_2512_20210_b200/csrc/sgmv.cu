@@ -21,13 +21,13 @@
 //          partial.  The last CTA of a tile (arrival counter) sums the KS
 //          partials in split order (deterministic) and writes V in bf16 — the
 //          rounding point between shrink and expand.
-//  expand  CTA (tile, 4 column blocks of 128): D[128 × 128] = V · Bᵀ[:, block]
+//  expand  CTA (tile, 8 column blocks of 64): D[128 × 64] = V · Bᵀ[:, block]
 //          (tcgen05, K = r16) per block, with the V tile loaded once by TMA,
-//          the Bᵀ blocks gathered from pages (MN-major SW128) and the y tiles
-//          TMA-loaded into a 2-stage ring, two TMEM accumulators; the
-//          epilogue adds D into the y tile in shared memory and TMA-stores
-//          it (rows of a partial tile, which belong to the next run, are
-//          stored per row).
+//          the Bᵀ blocks gathered from pages (MN-major SW128), two TMEM
+//          accumulators; the epilogue stages bf16(scale · D) in shared
+//          memory and TMA reduce-adds it into y (the read-modify-write happens
+//          in L2; rows of a partial tile that belong to the next run add 0).
+//          y therefore sees one extra bf16 rounding of the LoRA delta.
 // Rank <= 128; d_in % 64 == 0; d_out % 128 == 0; bf16 stores (otherwise the
 // exact CUDA-core BGMV path runs, see plora_sgmv).
 #include <cuda.h>
@@ -63,6 +63,11 @@ constexpr uint32_t kTmemCols = 128;
 constexpr int kGatherThreads = 96;   // expand: warps 1-3
 constexpr int kSGather = 192;       // shrink: warps 1-3 and 5-7 (5-7 are idle until the epilogue)
 constexpr int kEGather = 96;        // expand: warps 1-3
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
 
 __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
   // 128-byte swizzle inside an 8-row × 128-byte atom
@@ -269,10 +274,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ------------------------------------------------------------------ expand
-// CTA (tile, group of kGroupBlocks 128-column blocks): the V tile is loaded
-// once; the Bᵀ block and y tile of block b go to stage b % 2 and the MMA to
-// TMEM accumulator b % 2, so the epilogue of block b overlaps the loads and
-// MMA of block b + 1.
+// CTA (tile, group of kGroupBlocks 64-column blocks): the V tile is loaded
+// once; the Bᵀ block of block b goes to stage b % 2 and the MMA to TMEM
+// accumulator b % 2, so the epilogue of block b overlaps the gather and MMA
+// of block b + 1.  The epilogue never reads y: it stages bf16(scale · D) in
+// shared memory and TMA reduce-adds the tile into y (the add happens in L2),
+// with the rows of a partial tile that belong to the next run zeroed.
 constexpr uint32_t kEBlockN = 64;     // output columns per block (one 128-byte swizzle row)
 constexpr uint32_t kGroupBlocks = 8;  // blocks per CTA (512 columns)
 constexpr uint32_t kETmemCols = 2 * kEBlockN;
@@ -299,7 +306,7 @@ struct ESmem {  // ~97 KB: two expand CTAs per SM
   static constexpr uint32_t y = v + 32768;          // [2 stages][128 rows × 128 B] SW128
   static constexpr uint32_t b = y + 2 * 16384;      // [2 stages][r16 × 128 B] MN-major SW128
   static constexpr uint32_t bars = b + 2 * 16384;
-  // v_full, y_full[2], y_empty[2], b_full[2], b_empty[2], acc_full[2], acc_empty[2]
+  // v_full, (unused) [4], b_full[2], b_empty[2], acc_full[2], acc_empty[2]
   static constexpr uint32_t n_bars = 13;
   static constexpr uint32_t tmem_slot = bars + n_bars * 8;
   static constexpr uint32_t total = tmem_slot + 8;
@@ -353,21 +360,13 @@ __global__ void __launch_bounds__(kEThreads, 2)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ----------------------- TMA: V tile once, then the y tile of each block
+    // ----------------------------------------------- TMA: V tile once
     if (lane == 0) {
-      ptx::pdl_wait();  // V comes from the shrink; y from earlier kernels
+      ptx::pdl_wait();  // V comes from the shrink (and y may be read by earlier kernels)
       ptx::mbar_arrive_expect_tx(v_full, vboxes * 16384);
       for (uint32_t bx = 0; bx < vboxes; ++bx)
         ptx::tma_load_2d(smem + ESmem::v + bx * 16384, &tmap_v, static_cast<int32_t>(bx * 64),
                          static_cast<int32_t>(tile_i * kTileM), v_full);
-      for (uint32_t b = 0; b < nblk; ++b) {
-        const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
-        ptx::mbar_wait(&y_empty[st], ph ^ 1u);
-        ptx::mbar_arrive_expect_tx(&y_full[st], 16384);
-        ptx::tma_load_2d(smem + ESmem::y + st * 16384, &tmap_y,
-                         static_cast<int32_t>(col_base + b * kEBlockN),
-                         static_cast<int32_t>(tile.row0), &y_full[st]);
-      }
     }
   } else if (warp < 4) {
     // ----------------------------------- Bᵀ block gathers (paged rows)
@@ -435,13 +434,15 @@ __global__ void __launch_bounds__(kEThreads, 2)
     // ------------------------------------------------- epilogue (warps 4-7)
     const uint32_t m = (warp - 4) * 32 + lane;  // tile row == TMEM lane
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
-    const bool full_tile = tile.nrows == kTileM;
+    const bool live = m < tile.nrows;  // rows past the run belong to the next one: add 0
     for (uint32_t b = 0; b < nblk; ++b) {
       const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
       const uint32_t col0 = col_base + b * kEBlockN;
       char* ys = smem + ESmem::y + st * 16384;
-      char* yrow = p.y + static_cast<uint64_t>(tile.row0 + m) * p.y_stride_b + static_cast<uint64_t>(col0) * 2;
-      ptx::mbar_wait(&y_full[st], ph);
+      if (b >= 2) {  // the reduce-store of block b - 2 must have read stage st
+        if (warp == 4 && lane == 0) ptx::bulk_wait_read_n<1>();
+        ptx::named_bar_sync(1, 128);
+      }
       ptx::mbar_wait(&acc_full[st], ph);
       ptx::tc_fence_after();
 #pragma unroll 1
@@ -451,37 +452,24 @@ __global__ void __launch_bounds__(kEThreads, 2)
         ptx::tmem_ld_wait();
 #pragma unroll
         for (uint32_t hh = 0; hh < 2; ++hh) {
-          const uint32_t chunk = q * 2 + hh;
-          const uint32_t ya = ptx::smem_u32(ys + swz(m, chunk));
-          uint4 yv;
-          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(yv.x), "=r"(yv.y), "=r"(yv.z), "=r"(yv.w) : "r"(ya));
-          __nv_bfloat162* hy = reinterpret_cast<__nv_bfloat162*>(&yv);
+          const uint32_t ya = ptx::smem_u32(ys + swz(m, q * 2 + hh));
+          uint32_t o[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float2 f = __bfloat1622float2(hy[i]);
-            f.x = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i]), f.x);
-            f.y = fmaf(p.scale, __uint_as_float(rv[hh * 8 + 2 * i + 1]), f.y);
-            hy[i] = __floats2bfloat162_rn(f.x, f.y);
-          }
-          if (full_tile)
-            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ya), "r"(yv.x), "r"(yv.y),
-                         "r"(yv.z), "r"(yv.w) : "memory");
-          else if (m < tile.nrows)  // rows past the run belong to the next one
-            reinterpret_cast<uint4*>(yrow)[chunk] = yv;
+          for (int i = 0; i < 4; ++i)
+            o[i] = live ? pack_bf16x2(p.scale * __uint_as_float(rv[hh * 8 + 2 * i]),
+                                      p.scale * __uint_as_float(rv[hh * 8 + 2 * i + 1]))
+                        : 0u;
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ya), "r"(o[0]), "r"(o[1]),
+                       "r"(o[2]), "r"(o[3]) : "memory");
         }
       }
       ptx::tc_fence_before();
-      if (full_tile) ptx::fence_proxy_async_shared();  // generic-proxy smem writes -> TMA store
+      ptx::fence_proxy_async_shared();  // generic-proxy smem writes -> TMA
       ptx::named_bar_sync(1, 128);
       if (warp == 4 && lane == 0) {
         ptx::mbar_arrive(&acc_empty[st]);
-        if (full_tile) {
-          ptx::tma_store_2d(&tmap_y, static_cast<int32_t>(col0), static_cast<int32_t>(tile.row0), ys);
-          ptx::bulk_commit();
-          ptx::bulk_wait_read();  // the store has read the stage: it may be refilled
-        }
-        ptx::mbar_arrive(&y_empty[st]);
+        ptx::tma_reduce_add_2d(&tmap_y, static_cast<int32_t>(col0), static_cast<int32_t>(tile.row0), ys);
+        ptx::bulk_commit();
       }
     }
     if (warp == 4 && lane == 0) ptx::bulk_wait_all();
