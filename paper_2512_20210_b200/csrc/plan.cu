@@ -151,6 +151,32 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     t = e;
   }
   n_tiles = static_cast<uint32_t>(tiles.size());
+  sunits.clear();
+  for (uint32_t i = 0; i < n_tiles;) {
+    const bool pair = i + 1 < n_tiles && tiles[i].nrows == 128 &&
+                      tiles[i + 1].table_off == tiles[i].table_off &&
+                      tiles[i + 1].rank == tiles[i].rank && tiles[i + 1].row0 == tiles[i].row0 + 128;
+    sunits.push_back(i);
+    sunits.push_back(pair ? i + 1 : 0xffffffffu);
+    i += pair ? 2 : 1;
+  }
+  n_sunits = static_cast<uint32_t>(sunits.size() / 2);
+  {
+    // heaviest units (highest rank, pairs) first: CTAs are dispatched in
+    // blockIdx order, so the long ones start in the first wave
+    std::vector<uint32_t> order(n_sunits);
+    for (uint32_t u = 0; u < n_sunits; ++u) order[u] = u;
+    auto cost = [&](uint32_t u) {
+      return static_cast<uint64_t>(tiles[sunits[2 * u]].rank + 64) * (sunits[2 * u + 1] != 0xffffffffu ? 2 : 1);
+    };
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
+    std::vector<uint32_t> sorted(sunits.size());
+    for (uint32_t u = 0; u < n_sunits; ++u) {
+      sorted[2 * u] = sunits[2 * order[u]];
+      sorted[2 * u + 1] = sunits[2 * order[u] + 1];
+    }
+    sunits.swap(sorted);
+  }
 
   // ---- bf16 BGMV on clusters: jobs (<= kJobTok tokens of one adapter),
   // LPT-assigned to clusters by bytes, cut into kChunkRows-row chunks
@@ -241,7 +267,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   const uint64_t cch_b = align(cchunks.size() * sizeof(ClusterChunk));
   const uint64_t ccl_b = align(ccl_off.size() * sizeof(uint32_t));
   const uint64_t cjob_b = align(cjobs.size() * sizeof(ClusterJob));
-  const uint64_t total = std::max<uint64_t>(unit_b + tile_b + cch_b + ccl_b + cjob_b, 256);
+  const uint64_t sun_b = align(sunits.size() * sizeof(uint32_t));
+  const uint64_t total = std::max<uint64_t>(unit_b + tile_b + cch_b + ccl_b + cjob_b + sun_b, 256);
   DeviceCtx ctx(st.device);
   if (upload_done) PLORA_CUDA(cudaEventSynchronize(upload_done));  // pinned buffer reuse
   if (h_cap < total) {
@@ -271,6 +298,9 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   d_ccl_off = reinterpret_cast<uint32_t*>(d_buf + unit_b + tile_b + cch_b);
   std::memcpy(h_pinned + unit_b + tile_b + cch_b + ccl_b, cjobs.data(), cjobs.size() * sizeof(ClusterJob));
   d_cjobs = reinterpret_cast<ClusterJob*>(d_buf + unit_b + tile_b + cch_b + ccl_b);
+  std::memcpy(h_pinned + unit_b + tile_b + cch_b + ccl_b + cjob_b, sunits.data(),
+              sunits.size() * sizeof(uint32_t));
+  d_sunits = reinterpret_cast<uint32_t*>(d_buf + unit_b + tile_b + cch_b + ccl_b + cjob_b);
   PLORA_CUDA(cudaMemcpyAsync(d_buf, h_pinned, total, cudaMemcpyHostToDevice, stream));
   if (!upload_done) PLORA_CUDA(cudaEventCreateWithFlags(&upload_done, cudaEventDisableTiming));
   PLORA_CUDA(cudaEventRecord(upload_done, stream));

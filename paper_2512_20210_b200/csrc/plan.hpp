@@ -190,6 +190,11 @@ struct plora_plan {
   uint64_t vbuf_cap = 0;   // bytes
   uint32_t* d_tcnt = nullptr;
   uint64_t tcnt_cap = 0;
+  // SGMV shrink units: pairs of consecutive full tiles of one run (they share
+  // the adapter's A chunks), {tile, tile or ~0u}
+  std::vector<uint32_t> sunits;
+  uint32_t n_sunits = 0;
+  uint32_t* d_sunits = nullptr;
   cudaEvent_t upload_done = nullptr;
 
   void build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream);

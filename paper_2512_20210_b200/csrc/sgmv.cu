@@ -87,12 +87,14 @@ struct PagedSrc {
 
 // ------------------------------------------------------------------ shrink
 constexpr int kSStages = 4;  // a deep per-CTA ring beats more CTAs here (measured: 2 stages x3 CTAs 108 us, 3x2 92, 4x1 75)
-constexpr uint32_t kSStageBytes = 32768;  // X [128 × 64] 16 KiB + A [r16 × 64] <= 16 KiB
+constexpr uint32_t kSStageBytes = 49152;  // X [2 tiles][128 × 64] 32 KiB + A [r16 × 64] <= 16 KiB
+constexpr uint32_t kSTmemCols = 2 * kTmemCols;  // one accumulator per tile of the unit
 
 struct ShrinkArgs {
   const char* arena;
   const uint32_t* table;
   const SgmvTile* tiles;
+  const uint32_t* units;  // [unit] {tile, tile or ~0u}
   float* vpart;      // [tile][split][128][128] fp32
   __nv_bfloat16* vbuf;  // [tile][128][128] bf16
   uint32_t* tcnt;    // [tile] arrivals
@@ -122,8 +124,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SSmem::tmem_slot);
   volatile uint32_t* last_flag = reinterpret_cast<uint32_t*>(smem + SSmem::flag);
 
-  const uint32_t tile_i = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
-  const SgmvTile tile = p.tiles[tile_i];
+  const uint32_t unit = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
+  const uint32_t tile_a = p.units[2 * unit], tile_b = p.units[2 * unit + 1];
+  const uint32_t nt = tile_b != 0xffffffffu ? 2 : 1;  // tiles sharing the A chunks
+  const SgmvTile tile = p.tiles[tile_a];
+  const uint32_t row0_b = nt == 2 ? p.tiles[tile_b].row0 : 0;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r = tile.rank, r16 = (r + 15) & ~15u;
   const uint32_t kslice = p.d_in / p.splits, NK = kslice / kChunkK, k0 = split * kslice;
@@ -139,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(v_full, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 4) ptx::tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == 4) ptx::tmem_alloc(tmem_slot, kSTmemCols);
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
   ptx::tc_fence_before();
   __syncthreads();
@@ -153,10 +158,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t kc = 0; kc < NK; ++kc) {
         const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
         ptx::mbar_wait(&empty[st], ph ^ 1u);
-        ptx::mbar_arrive_expect_tx(&full[st], kTileM * kChunkK * 2);
+        ptx::mbar_arrive_expect_tx(&full[st], nt * kTileM * kChunkK * 2);
         ptx::tma_load_2d(smem + SSmem::stages + st * kSStageBytes, &tmap_x,
                          static_cast<int32_t>(k0 + kc * kChunkK), static_cast<int32_t>(tile.row0),
                          &full[st]);
+        if (nt == 2)
+          ptx::tma_load_2d(smem + SSmem::stages + st * kSStageBytes + kTileM * kChunkK * 2, &tmap_x,
+                           static_cast<int32_t>(k0 + kc * kChunkK), static_cast<int32_t>(row0_b),
+                           &full[st]);
       }
     }
   }
@@ -181,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
       const uint32_t nx0 = lookup(n0, kc + 1), nx1 = lookup(n1, kc + 1);  // next chunk, in flight
       ptx::mbar_wait(&empty[st], ph ^ 1u);
-      char* wdst = smem + SSmem::stages + st * kSStageBytes + kTileM * kChunkK * 2;
+      char* wdst = smem + SSmem::stages + st * kSStageBytes + 2 * kTileM * kChunkK * 2;
 #pragma unroll
       for (uint32_t h = 0; h < 1; ++h) {  // r16 <= 128 < 192 threads: one row each
         const uint32_t n = h ? n1 : n0;
@@ -214,11 +223,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(&full[st], ph);
         ptx::fence_proxy_async_shared();
         ptx::tc_fence_after();
-        const uint32_t xa = sbase + st * kSStageBytes, wa = xa + kTileM * kChunkK * 2;
+        const uint32_t xa = sbase + st * kSStageBytes, xb = xa + kTileM * kChunkK * 2;
+        const uint32_t wa = xa + 2 * kTileM * kChunkK * 2;
 #pragma unroll
-        for (uint32_t k = 0; k < kChunkK / 16; ++k)
-          ptx::umma_f16(tmem, ptx::smem_desc_sw128(xa + k * 32, 16, 1024),
-                        ptx::smem_desc_sw128(wa + k * 32, 16, 1024), idesc, (kc | k) != 0);
+        for (uint32_t k = 0; k < kChunkK / 16; ++k) {
+          const uint64_t wd = ptx::smem_desc_sw128(wa + k * 32, 16, 1024);
+          ptx::umma_f16(tmem, ptx::smem_desc_sw128(xa + k * 32, 16, 1024), wd, idesc, (kc | k) != 0);
+          if (nt == 2)
+            ptx::umma_f16(tmem + kTmemCols, ptx::smem_desc_sw128(xb + k * 32, 16, 1024), wd, idesc,
+                          (kc | k) != 0);
+        }
         ptx::umma_commit(&empty[st]);
       }
       ptx::umma_commit(v_full);
@@ -229,47 +243,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
     ptx::mbar_wait(v_full, 0);
     ptx::tc_fence_after();
-    float* vp = p.vpart + ((static_cast<uint64_t>(tile_i) * p.splits + split) * kTileM + m) * kMaxRank;
-    for (uint32_t cc = 0; cc < r16 / 16; ++cc) {
-      uint32_t rv[16];
-      ptx::tmem_ld_32x32b_x16(tmem + lane_base + cc * 16, rv);
-      ptx::tmem_ld_wait();
+    for (uint32_t t = 0; t < nt; ++t) {
+      const uint32_t tile_i = t ? tile_b : tile_a;
+      float* vp = p.vpart + ((static_cast<uint64_t>(tile_i) * p.splits + split) * kTileM + m) * kMaxRank;
+      for (uint32_t cc = 0; cc < r16 / 16; ++cc) {
+        uint32_t rv[16];
+        ptx::tmem_ld_32x32b_x16(tmem + lane_base + t * kTmemCols + cc * 16, rv);
+        ptx::tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        reinterpret_cast<uint4*>(vp + cc * 16)[i] = make_uint4(rv[4 * i], rv[4 * i + 1], rv[4 * i + 2], rv[4 * i + 3]);
-    }
-    // split-K reduction: the last CTA of the tile sums the partials in split order
-    __threadfence();
-    ptx::named_bar_sync(1, 128);
-    if (warp == 4 && lane == 0)
-      *last_flag = atomicAdd(p.tcnt + tile_i, 1u) == p.splits - 1;
-    ptx::named_bar_sync(1, 128);
-    if (*last_flag) {
-      __threadfence();
-      const float* v0 = p.vpart + (static_cast<uint64_t>(tile_i) * p.splits * kTileM + m) * kMaxRank;
-      __nv_bfloat16* vb = p.vbuf + (static_cast<uint64_t>(tile_i) * kTileM + m) * kMaxRank;
-      for (uint32_t c = 0; c < r16; c += 8) {
-        float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (uint32_t sp = 0; sp < p.splits; ++sp) {
-          const float4* q = reinterpret_cast<const float4*>(v0 + static_cast<uint64_t>(sp) * kTileM * kMaxRank + c);
-          const float4 lo = __ldcg(q), hi = __ldcg(q + 1);
-          a[0] += lo.x; a[1] += lo.y; a[2] += lo.z; a[3] += lo.w;
-          a[4] += hi.x; a[5] += hi.y; a[6] += hi.z; a[7] += hi.w;
-        }
-        uint4 o;
-        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
-        *reinterpret_cast<uint4*>(vb + c) = o;
+        for (int i = 0; i < 4; ++i)
+          reinterpret_cast<uint4*>(vp + cc * 16)[i] = make_uint4(rv[4 * i], rv[4 * i + 1], rv[4 * i + 2], rv[4 * i + 3]);
       }
-      if (warp == 4 && lane == 0) p.tcnt[tile_i] = 0;  // graph-replayable
+      // split-K reduction: the last CTA of the tile sums the partials in split order
+      __threadfence();
+      ptx::named_bar_sync(1, 128);
+      if (warp == 4 && lane == 0)
+        *last_flag = atomicAdd(p.tcnt + tile_i, 1u) == p.splits - 1;
+      ptx::named_bar_sync(1, 128);
+      if (*last_flag) {
+        __threadfence();
+        const float* v0 = p.vpart + (static_cast<uint64_t>(tile_i) * p.splits * kTileM + m) * kMaxRank;
+        __nv_bfloat16* vb = p.vbuf + (static_cast<uint64_t>(tile_i) * kTileM + m) * kMaxRank;
+        for (uint32_t c = 0; c < r16; c += 8) {
+          float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (uint32_t sp = 0; sp < p.splits; ++sp) {
+            const float4* q = reinterpret_cast<const float4*>(v0 + static_cast<uint64_t>(sp) * kTileM * kMaxRank + c);
+            const float4 lo = __ldcg(q), hi = __ldcg(q + 1);
+            a[0] += lo.x; a[1] += lo.y; a[2] += lo.z; a[3] += lo.w;
+            a[4] += hi.x; a[5] += hi.y; a[6] += hi.z; a[7] += hi.w;
+          }
+          uint4 o;
+          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
+          *reinterpret_cast<uint4*>(vb + c) = o;
+        }
+        if (warp == 4 && lane == 0) p.tcnt[tile_i] = 0;  // graph-replayable
+      }
+      ptx::named_bar_sync(1, 128);  // last_flag is reused by the next tile
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 4) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, kTmemCols);
+    ptx::tmem_dealloc(tmem, kSTmemCols);
   }
 }
 
@@ -552,6 +570,7 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     sa.arena = st.arena;
     sa.table = st.d_table;
     sa.tiles = plan->d_tiles;
+    sa.units = plan->d_sunits;
     sa.vpart = plan->d_vpart;
     sa.vbuf = reinterpret_cast<__nv_bfloat16*>(plan->d_vbuf);
     sa.tcnt = plan->d_tcnt;
@@ -560,7 +579,7 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     sa.d_in = din;
     sa.splits = splits;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(plan->n_tiles * splits);
+    cfg.gridDim = dim3(plan->n_sunits * splits);
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = SSmem::alloc;
     cfg.stream = s;
