@@ -463,6 +463,10 @@ int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
  * `proj`: out[0..7] = {cluster size, input slice, output slice, ring slots,
  * slot bytes, dynamic smem bytes, clusters, chunks}. */
 int plora_debug_plan_geom(const plora_plan* plan, uint32_t proj, uint32_t out[8]);
+/* Timing experiments only (results are wrong while set): the next SGMV
+ * shrink launches skip their 1 = weight gathers, 2 = MMAs, 4 = x loads,
+ * 16 = epilogue, 32 = split reduction; 8 = the expand launch is skipped.  0 restores the op. */
+int plora_debug_set_sgmv_flags(uint32_t flags);
 
 #ifdef __cplusplus
 }

@@ -237,6 +237,7 @@ _SIGS = {
     "plora_bgmv_tp_expand": (_int, [_vp, _u32, _u32, _u32, _u32, _vp, _vp, _u64, C.c_float, _vp]),
     "plora_debug_set_trace": (_int, [_vp, _u64]),
     "plora_debug_plan_geom": (_int, [_vp, _u32, _P(_u32)]),
+    "plora_debug_set_sgmv_flags": (_int, [_u32]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -52,7 +52,7 @@ constexpr uint32_t kX = 16;                    // exchange slots (>= 2 · kMaxSl
 constexpr uint32_t kMaxCs = 8;
 constexpr uint32_t kMaxSlots = 8;
 constexpr uint32_t kXSlotFloats = kJobTok * kChunkRows * kMaxCs;  // [t][row][src cta]
-constexpr uint32_t kSmemBudget = 200 * 1024;
+constexpr uint32_t kSmemBudget = 200 * 1024;  // 227 KiB (5 slots) measured no faster
 constexpr uint32_t kMaxSlice = 1024;  // elements per CTA slice (preferred)
 
 struct CArgs {

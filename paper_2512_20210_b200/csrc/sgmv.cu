@@ -54,6 +54,8 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
 
 namespace {
 
+uint32_t g_sgmv_dbg = 0;  // plora_debug_set_sgmv_flags
+
 constexpr int kThreads = 256;
 constexpr uint32_t kTileM = 128;
 constexpr uint32_t kChunkK = 64;   // shrink K per stage (one 128-byte swizzle row)
@@ -102,6 +104,7 @@ struct ShrinkArgs {
   uint32_t log2_page;
   uint32_t d_in;
   uint32_t splits;
+  uint32_t dbg;  // diagnostics (plora_debug_set_sgmv_flags): 1 no A gather, 2 no MMA, 4 no x load, 16 no epilogue, 32 no reduction
 };
 
 struct SSmem {
@@ -158,6 +161,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t kc = 0; kc < NK; ++kc) {
         const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
         ptx::mbar_wait(&empty[st], ph ^ 1u);
+        if (p.dbg & 4u) {
+          ptx::mbar_arrive(&full[st]);
+          continue;
+        }
         ptx::mbar_arrive_expect_tx(&full[st], nt * kTileM * kChunkK * 2);
         ptx::tma_load_2d(smem + SSmem::stages + st * kSStageBytes, &tmap_x,
                          static_cast<int32_t>(k0 + kc * kChunkK), static_cast<int32_t>(tile.row0),
@@ -194,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (uint32_t h = 0; h < 1; ++h) {  // r16 <= 128 < 192 threads: one row each
         const uint32_t n = h ? n1 : n0;
-        if (n >= r16) continue;
+        if (n >= r16 || (p.dbg & 1u)) continue;
         if (n >= r) {
 #pragma unroll
           for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), p.arena, 0);  // zero padding
@@ -221,6 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (uint32_t kc = 0; kc < NK; ++kc) {
         const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
         ptx::mbar_wait(&full[st], ph);
+        if (p.dbg & 2u) {
+          ptx::mbar_arrive(&empty[st]);
+          continue;
+        }
         ptx::fence_proxy_async_shared();
         ptx::tc_fence_after();
         const uint32_t xa = sbase + st * kSStageBytes, xb = xa + kTileM * kChunkK * 2;
@@ -238,49 +249,88 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::umma_commit(v_full);
     }
     __syncwarp();
-    // ------------------------------------------- epilogue (warps 4-7): partial
-    const uint32_t m = (warp - 4) * 32 + lane;  // tile row == TMEM lane
+  }
+  // --------------------------------------------- epilogue (all 8 warps)
+  // Warp w reads TMEM lanes 32·(w % 4) (its lane quarter), columns of half
+  // w / 4.  Partials are [tile][split] blocks of 128 × r16 fp32, rows of
+  // r16/4 16-byte chunks with chunk j of row m stored at j ^ (m & swm):
+  // staged through the (now idle) stage buffers without bank conflicts,
+  // written with one bulk copy, and read back coalesced by the reducing CTA.
+  ptx::mbar_wait(v_full, 0);
+  ptx::tc_fence_after();
+  {
+    const uint32_t m = (warp & 3) * 32 + lane;  // tile row == TMEM lane
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
-    ptx::mbar_wait(v_full, 0);
-    ptx::tc_fence_after();
-    for (uint32_t t = 0; t < nt; ++t) {
+    const uint32_t nch = r16 / 4, swm = min(8u, nch & (0u - nch)) - 1u;
+    const uint32_t tile_floats = kTileM * r16;
+    for (uint32_t t = 0; t < ((p.dbg & 16u) ? 0u : nt); ++t) {
       const uint32_t tile_i = t ? tile_b : tile_a;
-      float* vp = p.vpart + ((static_cast<uint64_t>(tile_i) * p.splits + split) * kTileM + m) * kMaxRank;
-      for (uint32_t cc = 0; cc < r16 / 16; ++cc) {
+      float* stg = reinterpret_cast<float*>(smem + SSmem::stages + t * kTileM * kMaxRank * 4);
+      for (uint32_t cc = warp >> 2; cc < r16 / 16; cc += 2) {
         uint32_t rv[16];
         ptx::tmem_ld_32x32b_x16(tmem + lane_base + t * kTmemCols + cc * 16, rv);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          reinterpret_cast<uint4*>(vp + cc * 16)[i] = make_uint4(rv[4 * i], rv[4 * i + 1], rv[4 * i + 2], rv[4 * i + 3]);
+        for (uint32_t i = 0; i < 4; ++i)
+          reinterpret_cast<uint4*>(stg + m * r16)[(cc * 4 + i) ^ (m & swm)] =
+              make_uint4(rv[4 * i], rv[4 * i + 1], rv[4 * i + 2], rv[4 * i + 3]);
       }
-      // split-K reduction: the last CTA of the tile sums the partials in split order
-      __threadfence();
-      ptx::named_bar_sync(1, 128);
-      if (warp == 4 && lane == 0)
-        *last_flag = atomicAdd(p.tcnt + tile_i, 1u) == p.splits - 1;
-      ptx::named_bar_sync(1, 128);
-      if (*last_flag) {
+      ptx::fence_proxy_async_shared();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float* dst = p.vpart + (static_cast<uint64_t>(tile_i) * p.splits + split) * kTileM * kMaxRank;
+        ptx::bulk_s2g(dst, stg, tile_floats * 4);
+        ptx::bulk_commit();
+        ptx::bulk_wait_all();  // written, not just read: the count below publishes it
+        ptx::fence_proxy_async_global();
         __threadfence();
-        const float* v0 = p.vpart + (static_cast<uint64_t>(tile_i) * p.splits * kTileM + m) * kMaxRank;
-        __nv_bfloat16* vb = p.vbuf + (static_cast<uint64_t>(tile_i) * kTileM + m) * kMaxRank;
-        for (uint32_t c = 0; c < r16; c += 8) {
-          float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          for (uint32_t sp = 0; sp < p.splits; ++sp) {
-            const float4* q = reinterpret_cast<const float4*>(v0 + static_cast<uint64_t>(sp) * kTileM * kMaxRank + c);
-            const float4 lo = __ldcg(q), hi = __ldcg(q + 1);
-            a[0] += lo.x; a[1] += lo.y; a[2] += lo.z; a[3] += lo.w;
-            a[4] += hi.x; a[5] += hi.y; a[6] += hi.z; a[7] += hi.w;
-          }
-          uint4 o;
-          __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
-          *reinterpret_cast<uint4*>(vb + c) = o;
-        }
-        if (warp == 4 && lane == 0) p.tcnt[tile_i] = 0;  // graph-replayable
+        *last_flag = atomicAdd(p.tcnt + tile_i, 1u) == p.splits - 1;
       }
-      ptx::named_bar_sync(1, 128);  // last_flag is reused by the next tile
+      __syncthreads();
+      if (*last_flag && !(p.dbg & 32u)) {
+        // split-K reduction by the tile's last CTA, in split order; 4 float4
+        // per thread and two splits per step keep 8 loads in flight
+        __threadfence();
+        constexpr uint32_t kU = 4;
+        constexpr uint32_t kSplitStride = kTileM * kMaxRank / 4;  // float4s
+        const float4* v0 = reinterpret_cast<const float4*>(
+            p.vpart + static_cast<uint64_t>(tile_i) * p.splits * kTileM * kMaxRank);
+        __nv_bfloat16* vb = p.vbuf + static_cast<uint64_t>(tile_i) * kTileM * kMaxRank;
+        const uint32_t n4 = tile_floats / 4;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint32_t f0 = threadIdx.x; f0 < n4; f0 += kU * kThreads) {
+          float4 acc[kU];
+#pragma unroll
+          for (uint32_t u = 0; u < kU; ++u) acc[u] = z;
+          for (uint32_t sp = 0; sp < p.splits; sp += 2) {
+            float4 q0[kU], q1[kU];
+#pragma unroll
+            for (uint32_t u = 0; u < kU; ++u) {
+              const uint32_t f = f0 + u * kThreads;
+              q0[u] = f < n4 ? __ldcg(v0 + sp * kSplitStride + f) : z;
+              q1[u] = f < n4 && sp + 1 < p.splits ? __ldcg(v0 + (sp + 1) * kSplitStride + f) : z;
+            }
+#pragma unroll
+            for (uint32_t u = 0; u < kU; ++u) {
+              acc[u].x += q0[u].x; acc[u].y += q0[u].y; acc[u].z += q0[u].z; acc[u].w += q0[u].w;
+              acc[u].x += q1[u].x; acc[u].y += q1[u].y; acc[u].z += q1[u].z; acc[u].w += q1[u].w;
+            }
+          }
+#pragma unroll
+          for (uint32_t u = 0; u < kU; ++u) {
+            const uint32_t f = f0 + u * kThreads;
+            if (f >= n4) continue;
+            const uint32_t row = f / nch, j = (f % nch) ^ (row & swm);
+            uint2 o;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+            h[0] = __floats2bfloat162_rn(acc[u].x, acc[u].y);
+            h[1] = __floats2bfloat162_rn(acc[u].z, acc[u].w);
+            *reinterpret_cast<uint2*>(vb + row * kMaxRank + j * 4) = o;
+          }
+        }
+        if (threadIdx.x == 0) p.tcnt[tile_i] = 0;  // graph-replayable
+      }
+      __syncthreads();  // last_flag and the staging buffer are reused by the next tile
     }
   }
   ptx::tc_fence_before();
@@ -531,6 +581,11 @@ void make_tmap_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows
 
 }  // namespace
 
+extern "C" int plora_debug_set_sgmv_flags(uint32_t flags) {
+  g_sgmv_dbg = flags;
+  return PLORA_OK;
+}
+
 extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                           uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                           plora_stream_t stream) {
@@ -578,6 +633,7 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     sa.log2_page = st.log2_page;
     sa.d_in = din;
     sa.splits = splits;
+    sa.dbg = g_sgmv_dbg;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(plan->n_sunits * splits);
     cfg.blockDim = dim3(kThreads);
@@ -587,6 +643,7 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     cfg.numAttrs = 1;
     PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_shrink_kernel, sa, tmap_x));
     count_launch();
+    if (g_sgmv_dbg & 8u) return 0;
 
     ExpandArgs ea{};
     ea.arena = st.arena;
