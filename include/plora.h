@@ -465,7 +465,7 @@ int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
 int plora_debug_plan_geom(const plora_plan* plan, uint32_t proj, uint32_t out[8]);
 /* Timing experiments only (results are wrong while set): the next SGMV
  * shrink launches skip their 1 = weight gathers, 2 = MMAs, 4 = x loads,
- * 16 = epilogue, 32 = split reduction; 8 = the expand launch is skipped.  0 restores the op. */
+ * 16 = epilogue; 32 = the split reduction launch, 8 = the expand launch.  0 restores the op. */
 int plora_debug_set_sgmv_flags(uint32_t flags);
 
 #ifdef __cplusplus

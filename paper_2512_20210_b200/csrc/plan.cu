@@ -1,5 +1,6 @@
 // Batch plan construction (host) and its C ABI.  See plan.hpp.
 #include <algorithm>
+#include <queue>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -161,21 +162,92 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     i += pair ? 2 : 1;
   }
   n_sunits = static_cast<uint32_t>(sunits.size() / 2);
-  {
-    // heaviest units (highest rank, pairs) first: CTAs are dispatched in
-    // blockIdx order, so the long ones start in the first wave
-    std::vector<uint32_t> order(n_sunits);
-    for (uint32_t u = 0; u < n_sunits; ++u) order[u] = u;
-    auto cost = [&](uint32_t u) {
-      return static_cast<uint64_t>(tiles[sunits[2 * u]].rank + 64) * (sunits[2 * u + 1] != 0xffffffffu ? 2 : 1);
-    };
-    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
-    std::vector<uint32_t> sorted(sunits.size());
-    for (uint32_t u = 0; u < n_sunits; ++u) {
-      sorted[2 * u] = sunits[2 * order[u]];
-      sorted[2 * u + 1] = sunits[2 * order[u] + 1];
+  // persistent shrink schedules (bf16 tensor-core path only)
+  sitems.clear();
+  scta.clear();
+  for (uint32_t p = 0; p < PLORA_MAX_PROJ; ++p) ssched[p] = SgmvSched{};
+  if (es == 2 && n_sunits > 0) {
+    const uint32_t n_sm = std::max(1, st.num_sms);
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) {
+      uint32_t same = p;
+      for (uint32_t q = 0; q < p; ++q)
+        if (g.m.d_in[q] == g.m.d_in[p]) same = q;
+      if (same != p) {
+        ssched[p] = ssched[same];
+        continue;
+      }
+      // Split-K factor: each candidate's LPT makespan (bytes the busiest
+      // CTA streams, at a per-SM share of HBM) plus the split reduction
+      // (partials written and read back); the cheapest
+      // wins.  Few splits for heavy uniform batches, more for mixed ranks.
+      const uint32_t d_in = g.m.d_in[p];
+      std::vector<std::vector<SgmvItem>> per, best_per;
+      uint32_t ks = 0;
+      double best = 0.0;
+      for (uint32_t cand = 1; cand <= 16; cand *= 2) {
+        if ((d_in / 64) % cand != 0 || (cand > 1 && d_in / cand < 256)) break;
+        const uint32_t kslice = d_in / cand;
+        std::vector<std::pair<uint64_t, SgmvItem>> items;  // (cost, item)
+        items.reserve(static_cast<size_t>(n_sunits) * cand);
+        uint64_t part_bytes = 0;
+        for (uint32_t u = 0; u < n_sunits; ++u) {
+          const uint64_t nt = sunits[2 * u + 1] != 0xffffffffu ? 2 : 1;
+          const SgmvTile& ta = tiles[sunits[2 * u]];
+          const uint64_t r16 = (ta.rank + 15) / 16 * 16;
+          // bytes streamed (x tiles + paged weights) plus the partial write-back
+          const uint64_t cost = 2ull * kslice * (nt * 128 + r16) + 4ull * nt * 128 * r16;
+          part_bytes += 8ull * nt * 128 * r16 * cand;
+          for (uint32_t sp = 0; sp < cand; ++sp) {
+            SgmvItem it{};
+            it.tile_a = sunits[2 * u];
+            it.tile_b = sunits[2 * u + 1];
+            it.row0_a = ta.row0;
+            it.row0_b = nt == 2 ? tiles[it.tile_b].row0 : 0;
+            it.table_off = ta.table_off;
+            it.rank = ta.rank;
+            it.split = sp;
+            items.emplace_back(cost, it);
+          }
+        }
+        std::stable_sort(items.begin(), items.end(),
+                         [](const auto& x, const auto& y) { return x.first > y.first; });
+        const uint32_t ctas = std::min<uint32_t>(n_sm, static_cast<uint32_t>(items.size()));
+        per.assign(ctas, {});
+        using Load = std::pair<uint64_t, uint32_t>;
+        std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+        for (uint32_t c = 0; c < ctas; ++c) heap.emplace(0, c);
+        uint64_t makespan = 0;
+        for (const auto& it : items) {
+          Load l = heap.top();
+          heap.pop();
+          per[l.second].push_back(it.second);
+          heap.emplace(l.first + it.first, l.second);
+          makespan = std::max(makespan, l.first + it.first);
+        }
+        constexpr double kSmBw = 45e9, kHbmBw = 5e12;
+        const double t = makespan / kSmBw + part_bytes / kHbmBw;
+        if (ks == 0 || t < best) {
+          ks = cand;
+          best = t;
+          best_per.swap(per);
+        }
+      }
+      per.swap(best_per);
+      const uint32_t ctas = static_cast<uint32_t>(per.size());
+      SgmvSched sc;
+      sc.splits = ks;
+      sc.ctas = ctas;
+      sc.item_off = static_cast<uint32_t>(sitems.size());
+      sc.cta_off = static_cast<uint32_t>(scta.size());
+      uint32_t n = 0;
+      for (uint32_t c = 0; c < ctas; ++c) {
+        scta.push_back(n);
+        for (const SgmvItem& v : per[c]) sitems.push_back(v);
+        n += static_cast<uint32_t>(per[c].size());
+      }
+      scta.push_back(n);
+      ssched[p] = sc;
     }
-    sunits.swap(sorted);
   }
 
   // ---- bf16 BGMV on clusters: jobs (<= kJobTok tokens of one adapter),
@@ -268,7 +340,10 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   const uint64_t ccl_b = align(ccl_off.size() * sizeof(uint32_t));
   const uint64_t cjob_b = align(cjobs.size() * sizeof(ClusterJob));
   const uint64_t sun_b = align(sunits.size() * sizeof(uint32_t));
-  const uint64_t total = std::max<uint64_t>(unit_b + tile_b + cch_b + ccl_b + cjob_b + sun_b, 256);
+  const uint64_t sit_b = align(sitems.size() * sizeof(SgmvItem));
+  const uint64_t sct_b = align(scta.size() * sizeof(uint32_t));
+  const uint64_t total =
+      std::max<uint64_t>(unit_b + tile_b + cch_b + ccl_b + cjob_b + sun_b + sit_b + sct_b, 256);
   DeviceCtx ctx(st.device);
   if (upload_done) PLORA_CUDA(cudaEventSynchronize(upload_done));  // pinned buffer reuse
   if (h_cap < total) {
@@ -301,6 +376,13 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   std::memcpy(h_pinned + unit_b + tile_b + cch_b + ccl_b + cjob_b, sunits.data(),
               sunits.size() * sizeof(uint32_t));
   d_sunits = reinterpret_cast<uint32_t*>(d_buf + unit_b + tile_b + cch_b + ccl_b + cjob_b);
+  {
+    const uint64_t o = unit_b + tile_b + cch_b + ccl_b + cjob_b + sun_b;
+    std::memcpy(h_pinned + o, sitems.data(), sitems.size() * sizeof(SgmvItem));
+    std::memcpy(h_pinned + o + sit_b, scta.data(), scta.size() * sizeof(uint32_t));
+    d_sitems = reinterpret_cast<SgmvItem*>(d_buf + o);
+    d_scta = reinterpret_cast<uint32_t*>(d_buf + o + sit_b);
+  }
   PLORA_CUDA(cudaMemcpyAsync(d_buf, h_pinned, total, cudaMemcpyHostToDevice, stream));
   if (!upload_done) PLORA_CUDA(cudaEventCreateWithFlags(&upload_done, cudaEventDisableTiming));
   PLORA_CUDA(cudaEventRecord(upload_done, stream));
@@ -317,24 +399,19 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   if (es == 2 && n_tiles > 0) {  // SGMV workspaces (see sgmv.cu)
     uint64_t parts = 0;
     for (uint32_t p = 0; p < g.m.n_proj; ++p)
-      parts = std::max<uint64_t>(parts, sgmv_splits(n_tiles, g.m.d_in[p]));
+      parts = std::max<uint64_t>(parts, ssched[p].splits);
     const uint64_t need_part = parts * n_tiles * 128ull * 128ull;
     const uint64_t need_vbuf = n_tiles * 128ull * 128ull * 2ull;
-    if (vpart_cap < need_part || vbuf_cap < need_vbuf || tcnt_cap < n_tiles) {
+    if (vpart_cap < need_part || vbuf_cap < need_vbuf) {
       PLORA_CUDA(cudaStreamSynchronize(stream));
       cudaFree(d_vpart);
       cudaFree(d_vbuf);
-      cudaFree(d_tcnt);
       d_vpart = nullptr;
       d_vbuf = nullptr;
-      d_tcnt = nullptr;
       vpart_cap = need_part;
       vbuf_cap = need_vbuf;
-      tcnt_cap = std::max<uint64_t>(n_tiles, 256);
       PLORA_CUDA(cudaMalloc(&d_vpart, vpart_cap * sizeof(float)));
       PLORA_CUDA(cudaMalloc(&d_vbuf, vbuf_cap));
-      PLORA_CUDA(cudaMalloc(&d_tcnt, tcnt_cap * sizeof(uint32_t)));
-      PLORA_CUDA(cudaMemsetAsync(d_tcnt, 0, tcnt_cap * sizeof(uint32_t), stream));
     }
   }
   if (sync_cap < 2ull + n_seg) {
@@ -388,7 +465,6 @@ void plora_plan_destroy(plora_plan* plan) {
   cudaFree(plan->d_sync);
   cudaFree(plan->d_vpart);
   cudaFree(plan->d_vbuf);
-  cudaFree(plan->d_tcnt);
   delete plan;
 }
 

@@ -142,13 +142,19 @@ struct SgmvTile {
   uint32_t rank;
 };
 
-// Split-K factor of the SGMV shrink: enough CTAs to cover the SMs twice,
-// K slices of >= 256 elements that divide d_in into 64-element chunks.
-inline uint32_t sgmv_splits(uint32_t n_tiles, uint32_t d_in) {
-  uint32_t ks = 1;
-  while (n_tiles * ks < 2 * 148 && (d_in / 64) % (ks * 2) == 0 && d_in / (ks * 2) >= 256) ks *= 2;
-  return ks;
-}
+// One SGMV shrink work item: a unit (one tile, or two consecutive full tiles
+// of one run, tile_b = ~0u otherwise) × one K slice, self-contained so the
+// kernel reads one 32-byte record per item.
+struct SgmvItem {
+  uint32_t tile_a, tile_b, row0_a, row0_b, table_off, rank, split, pad;
+};
+
+// Persistent SGMV shrink schedule of one projection: CTA c runs the work
+// items items[item_off + cta[cta_off + c] .. cta[cta_off + c + 1]), heaviest
+// first (LPT over the CTAs).
+struct SgmvSched {
+  uint32_t splits = 0, ctas = 0, item_off = 0, cta_off = 0;
+};
 
 }  // namespace plora
 
@@ -182,19 +188,21 @@ struct plora_plan {
   uint64_t v_cap = 0;
   uint32_t* d_sync = nullptr;  // [0] ticket, [1] exit count, [2..] per-segment shrink done
   uint64_t sync_cap = 0;
-  // SGMV: split-K partials of V (fp32), V tiles (bf16, 128 × 128 per tile),
-  // per-tile arrival counters of the split-K reduction (self-resetting)
+  // SGMV: split-K partials of V (fp32), V tiles (bf16, 128 × 128 per tile)
   float* d_vpart = nullptr;
   uint64_t vpart_cap = 0;  // floats
   char* d_vbuf = nullptr;
   uint64_t vbuf_cap = 0;   // bytes
-  uint32_t* d_tcnt = nullptr;
-  uint64_t tcnt_cap = 0;
   // SGMV shrink units: pairs of consecutive full tiles of one run (they share
   // the adapter's A chunks), {tile, tile or ~0u}
   std::vector<uint32_t> sunits;
   uint32_t n_sunits = 0;
   uint32_t* d_sunits = nullptr;
+  plora::SgmvSched ssched[PLORA_MAX_PROJ];
+  std::vector<plora::SgmvItem> sitems;
+  std::vector<uint32_t> scta;
+  plora::SgmvItem* d_sitems = nullptr;
+  uint32_t* d_scta = nullptr;
   cudaEvent_t upload_done = nullptr;
 
   void build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream);

@@ -56,14 +56,13 @@ namespace {
 
 uint32_t g_sgmv_dbg = 0;  // plora_debug_set_sgmv_flags
 
-constexpr int kThreads = 256;
 constexpr uint32_t kTileM = 128;
 constexpr uint32_t kChunkK = 64;   // shrink K per stage (one 128-byte swizzle row)
 constexpr uint32_t kBlockN = 128;  // expand output columns per CTA
 constexpr uint32_t kMaxRank = 128;
 constexpr uint32_t kTmemCols = 128;
 constexpr int kGatherThreads = 96;   // expand: warps 1-3
-constexpr int kSGather = 192;       // shrink: warps 1-3 and 5-7 (5-7 are idle until the epilogue)
+constexpr int kSGather = 192;       // shrink: warps 1-6
 constexpr int kEGather = 96;        // expand: warps 1-3
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -88,55 +87,86 @@ struct PagedSrc {
 };
 
 // ------------------------------------------------------------------ shrink
-constexpr int kSStages = 4;  // a deep per-CTA ring beats more CTAs here (measured: 2 stages x3 CTAs 108 us, 3x2 92, 4x1 75)
+// Persistent: one CTA per SM runs its LPT-scheduled work items, each a unit
+// (one tile, or two consecutive full tiles of one run that share every A
+// chunk) × one K slice.  The stage ring runs across items; the TMEM
+// accumulators are double-buffered, so the epilogue of item i (TMEM ->
+// shared -> bulk copy of the fp32 partial) overlaps the loads and MMAs of
+// item i + 1.  sgmv_reduce_kernel then sums the K-slice partials in split
+// order (deterministic) into the bf16 V tiles.
+//   warp 0      TMA producer of the x chunks (one 128 × 64 box per tile)
+//   warps 1-6   A gathers: rank row n of the chunk, page-table lookup a chunk ahead
+//   warp 7      MMA issuer (and TMEM allocator)
+//   warps 8-11  epilogue (warp 8 + q reads TMEM lanes 32q..32q+31)
+constexpr int kSStages = 4;
 constexpr uint32_t kSStageBytes = 49152;  // X [2 tiles][128 × 64] 32 KiB + A [r16 × 64] <= 16 KiB
-constexpr uint32_t kSTmemCols = 2 * kTmemCols;  // one accumulator per tile of the unit
+constexpr uint32_t kSThreads = 384;
+constexpr uint32_t kSEpiThreads = 128;
+constexpr uint32_t kStgBytes = 8192;  // per epilogue warp: 32 rows × 64 fp32
+constexpr uint32_t kSTmemCols = 512;  // [buffer][tile][128 columns]
 
 struct ShrinkArgs {
   const char* arena;
   const uint32_t* table;
   const SgmvTile* tiles;
-  const uint32_t* units;  // [unit] {tile, tile or ~0u}
-  float* vpart;      // [tile][split][128][128] fp32
-  __nv_bfloat16* vbuf;  // [tile][128][128] bf16
-  uint32_t* tcnt;    // [tile] arrivals
+  const SgmvItem* items;
+  const uint32_t* cta_items;  // [cta + 1] offsets into items
+  float* vpart;               // [tile][split] blocks of 128 × 128 fp32 (128 × r16 used)
   uint64_t blk_mult;
   uint32_t log2_page;
   uint32_t d_in;
   uint32_t splits;
-  uint32_t dbg;  // diagnostics (plora_debug_set_sgmv_flags): 1 no A gather, 2 no MMA, 4 no x load, 16 no epilogue, 32 no reduction
+  uint32_t dbg;  // diagnostics (plora_debug_set_sgmv_flags): 1 no A gather, 2 no MMA, 4 no x load, 16 no epilogue
 };
 
 struct SSmem {
   static constexpr uint32_t stages = 0;  // 1024-aligned
-  static constexpr uint32_t bars = stages + kSStages * kSStageBytes;
-  static constexpr uint32_t n_bars = 2 * kSStages + 1;  // full[4], empty[4], v_full
+  static constexpr uint32_t stg = stages + kSStages * kSStageBytes;
+  static constexpr uint32_t bars = stg + 4 * kStgBytes;
+  static constexpr uint32_t n_bars = 2 * kSStages + 4;  // full, empty, tfull[2], tempty[2]
   static constexpr uint32_t tmem_slot = bars + n_bars * 8;
-  static constexpr uint32_t flag = tmem_slot + 8;
-  static constexpr uint32_t total = flag + 8;
+  static constexpr uint32_t total = tmem_slot + 8;
   static constexpr uint32_t alloc = total + 1024;  // alignment slack
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+struct UnitInfo {
+  uint32_t tile_a, tile_b, nt, row0_a, row0_b, r, r16, table_off, split;
+};
+
+__device__ __forceinline__ UnitInfo unit_info(const SgmvItem* it) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(it));
+  const uint4 b = __ldg(reinterpret_cast<const uint4*>(it) + 1);
+  UnitInfo u;
+  u.tile_a = a.x;
+  u.tile_b = a.y;
+  u.nt = a.y != 0xffffffffu ? 2 : 1;
+  u.row0_a = a.z;
+  u.row0_b = a.w;
+  u.table_off = b.x;
+  u.r = b.y;
+  u.r16 = (b.y + 15) & ~15u;
+  u.split = b.z;
+  return u;
+}
+
+// Partial block layout (floats): [quarter q][pass][32 rows][pw], pass = 64
+// columns (pw = min(64, r16 - 64·pass)); 16-byte chunk j of row i stored at
+// j ^ (i & swm(pw)) so the staging writes are free of bank conflicts.
+__device__ __forceinline__ uint32_t part_swm(uint32_t pw4) { return min(8u, pw4 & (0u - pw4)) - 1u; }
+
+__global__ void __launch_bounds__(kSThreads, 1)
     sgmv_shrink_kernel(const ShrinkArgs p, const __grid_constant__ CUtensorMap tmap_x) {
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SSmem::bars);
   uint64_t* empty = full + kSStages;
-  uint64_t* v_full = full + 2 * kSStages;
+  uint64_t* tfull = full + 2 * kSStages;
+  uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + SSmem::tmem_slot);
-  volatile uint32_t* last_flag = reinterpret_cast<uint32_t*>(smem + SSmem::flag);
 
-  const uint32_t unit = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
-  const uint32_t tile_a = p.units[2 * unit], tile_b = p.units[2 * unit + 1];
-  const uint32_t nt = tile_b != 0xffffffffu ? 2 : 1;  // tiles sharing the A chunks
-  const SgmvTile tile = p.tiles[tile_a];
-  const uint32_t row0_b = nt == 2 ? p.tiles[tile_b].row0 : 0;
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t r = tile.rank, r16 = (r + 15) & ~15u;
-  const uint32_t kslice = p.d_in / p.splits, NK = kslice / kChunkK, k0 = split * kslice;
-  const uint64_t blk = static_cast<uint64_t>(r) * p.blk_mult * 2;  // A block, bytes
-  const PagedSrc src{p.arena, p.table, tile.table_off, p.log2_page};
+  const uint32_t it0 = p.cta_items[blockIdx.x], it1 = p.cta_items[blockIdx.x + 1];
+  const uint32_t kslice = p.d_in / p.splits, NK = kslice / kChunkK;
 
   ptx::pdl_launch_dependents();  // the expand may start gathering its weights
   if (threadIdx.x == 0) {
@@ -144,10 +174,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&full[s], 1 + kSGather);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(v_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 4);  // one arrival per epilogue warp
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 4) ptx::tmem_alloc(tmem_slot, kSTmemCols);
+  if (warp == 7) ptx::tmem_alloc(tmem_slot, kSTmemCols);
   if (warp == 0 && lane == 0) ptx::prefetch_tmap(&tmap_x);
   ptx::tc_fence_before();
   __syncthreads();
@@ -158,186 +191,215 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------ TMA producer (x chunks)
     if (lane == 0) {
       ptx::pdl_wait();  // x is written by earlier kernels in the stream
-      for (uint32_t kc = 0; kc < NK; ++kc) {
-        const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
-        ptx::mbar_wait(&empty[st], ph ^ 1u);
-        if (p.dbg & 4u) {
-          ptx::mbar_arrive(&full[st]);
-          continue;
+      uint32_t g = 0;
+      for (uint32_t it = it0; it < it1; ++it) {
+        const UnitInfo u = unit_info(p.items + it);
+        const uint32_t k0 = u.split * kslice;
+        for (uint32_t kc = 0; kc < NK; ++kc, ++g) {
+          const uint32_t st = g % kSStages, ph = (g / kSStages) & 1u;
+          ptx::mbar_wait(&empty[st], ph ^ 1u);
+          if (p.dbg & 4u) {
+            ptx::mbar_arrive(&full[st]);
+            continue;
+          }
+          char* xs = smem + SSmem::stages + st * kSStageBytes;
+          ptx::mbar_arrive_expect_tx(&full[st], u.nt * kTileM * kChunkK * 2);
+          ptx::tma_load_2d(xs, &tmap_x, static_cast<int32_t>(k0 + kc * kChunkK),
+                           static_cast<int32_t>(u.row0_a), &full[st]);
+          if (u.nt == 2)
+            ptx::tma_load_2d(xs + kTileM * kChunkK * 2, &tmap_x, static_cast<int32_t>(k0 + kc * kChunkK),
+                             static_cast<int32_t>(u.row0_b), &full[st]);
         }
-        ptx::mbar_arrive_expect_tx(&full[st], nt * kTileM * kChunkK * 2);
-        ptx::tma_load_2d(smem + SSmem::stages + st * kSStageBytes, &tmap_x,
-                         static_cast<int32_t>(k0 + kc * kChunkK), static_cast<int32_t>(tile.row0),
-                         &full[st]);
-        if (nt == 2)
-          ptx::tma_load_2d(smem + SSmem::stages + st * kSStageBytes + kTileM * kChunkK * 2, &tmap_x,
-                           static_cast<int32_t>(k0 + kc * kChunkK), static_cast<int32_t>(row0_b),
-                           &full[st]);
       }
     }
-  }
-  if (warp >= 1 && warp != 4) {
+  } else if (warp <= 6) {
     // ----------------------------------------------- A gathers (paged rows)
-    // Thread wt owns rank rows wt and wt + 96.  With pages >= 256 B a row's
-    // 128-byte piece of a chunk lies in one page: one page-table lookup per
-    // row per chunk, issued a chunk ahead (before the slot wait), so the
-    // lookups never serialise the copies.  Smaller pages: per-piece lookups.
-    const uint32_t wt = warp < 4 ? threadIdx.x - 32 : threadIdx.x - 160 + 96;
+    // Thread n owns rank row n (r16 <= 128 < 192).  A row's K slice spans
+    // few pages: the thread keeps the current page's frame and the next
+    // one's (looked up a page ahead), so a lookup never stalls a chunk.
+    // The next item's record is fetched one item ahead.
+    const uint32_t n = threadIdx.x - 32;
     const bool fast = p.log2_page >= 8;
-    const uint32_t n0 = wt, n1 = wt + kSGather;
-    auto row_off = [&](uint32_t n, uint32_t kc) {
-      return blk + (static_cast<uint64_t>(n) * p.d_in + k0 + kc * kChunkK) * 2;
-    };
-    auto lookup = [&](uint32_t n, uint32_t kc) -> uint32_t {
-      return (fast && n < r && kc < NK) ? __ldg(p.table + tile.table_off + static_cast<uint32_t>(row_off(n, kc) >> p.log2_page)) : 0u;
-    };
-    uint32_t ph0 = lookup(n0, 0), ph1 = lookup(n1, 0);
     const uint64_t pmask = (1ull << p.log2_page) - 1;
-    for (uint32_t kc = 0; kc < NK; ++kc) {
-      const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
-      const uint32_t nx0 = lookup(n0, kc + 1), nx1 = lookup(n1, kc + 1);  // next chunk, in flight
-      ptx::mbar_wait(&empty[st], ph ^ 1u);
-      char* wdst = smem + SSmem::stages + st * kSStageBytes + 2 * kTileM * kChunkK * 2;
-#pragma unroll
-      for (uint32_t h = 0; h < 1; ++h) {  // r16 <= 128 < 192 threads: one row each
-        const uint32_t n = h ? n1 : n0;
-        if (n >= r16 || (p.dbg & 1u)) continue;
-        if (n >= r) {
-#pragma unroll
-          for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), p.arena, 0);  // zero padding
-        } else if (fast) {
-          const uint64_t off = row_off(n, kc);
-          const char* base = p.arena + (static_cast<uint64_t>(h ? ph1 : ph0) << p.log2_page) + (off & pmask);
-#pragma unroll
-          for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), base + c * 16, 16);
-        } else {
-          for (uint32_t c = 0; c < 8; ++c)
-            ptx::cp_async_16(wdst + swz(n, c), src.at(row_off(n, kc) + c * 16), 16);
+    uint32_t g = 0;
+    UnitInfo un = it0 < it1 ? unit_info(p.items + it0) : UnitInfo{};
+    for (uint32_t it = it0; it < it1; ++it) {
+      const UnitInfo u = un;
+      if (it + 1 < it1) un = unit_info(p.items + it + 1);
+      const uint32_t k0 = u.split * kslice;
+      const uint64_t blk = static_cast<uint64_t>(u.r) * p.blk_mult * 2;  // A block, bytes
+      const PagedSrc src{p.arena, p.table, u.table_off, p.log2_page};
+      const uint64_t off0 = blk + (static_cast<uint64_t>(n) * p.d_in + k0) * 2;  // row n's slice
+      const bool live = fast && n < u.r;
+      const uint32_t lp_last = static_cast<uint32_t>((off0 + kslice * 2 - 1) >> p.log2_page);
+      uint32_t lp = static_cast<uint32_t>(off0 >> p.log2_page);
+      uint32_t e_cur = live ? __ldg(p.table + u.table_off + lp) : 0u;
+      uint32_t e_nxt = live && lp < lp_last ? __ldg(p.table + u.table_off + lp + 1) : 0u;
+      for (uint32_t kc = 0; kc < NK; ++kc, ++g) {
+        const uint32_t st = g % kSStages, ph = (g / kSStages) & 1u;
+        const uint64_t off = off0 + kc * kChunkK * 2;
+        if (live && (off >> p.log2_page) != lp) {  // crossed into the next page
+          lp = static_cast<uint32_t>(off >> p.log2_page);
+          e_cur = e_nxt;
+          e_nxt = lp < lp_last ? __ldg(p.table + u.table_off + lp + 1) : 0u;
         }
+        ptx::mbar_wait(&empty[st], ph ^ 1u);
+        char* wdst = smem + SSmem::stages + st * kSStageBytes + 2 * kTileM * kChunkK * 2;
+        if (n < u.r16 && !(p.dbg & 1u)) {
+          if (n >= u.r) {
+#pragma unroll
+            for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), p.arena, 0);  // zero padding
+          } else if (fast) {
+            const char* base = p.arena + (static_cast<uint64_t>(e_cur) << p.log2_page) + (off & pmask);
+#pragma unroll
+            for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), base + c * 16, 16);
+          } else {
+            for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), src.at(off + c * 16), 16);
+          }
+        }
+        ptx::cp_async_mbar_arrive_noinc(&full[st]);
       }
-      ptx::cp_async_mbar_arrive_noinc(&full[st]);
-      ph0 = nx0;
-      ph1 = nx1;
     }
-  }
-  if (warp >= 4) {
-    if (warp == 4 && lane == 0) {
-      // ------------------------------------------------------- MMA issuer
-      const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, r16, false, false);
+  } else if (warp == 7) {
+    // ------------------------------------------------------- MMA issuer
+    if (lane == 0) {
       const uint32_t sbase = ptx::smem_u32(smem + SSmem::stages);
-      for (uint32_t kc = 0; kc < NK; ++kc) {
-        const uint32_t st = kc % kSStages, ph = (kc / kSStages) & 1u;
-        ptx::mbar_wait(&full[st], ph);
-        if (p.dbg & 2u) {
-          ptx::mbar_arrive(&empty[st]);
-          continue;
-        }
-        ptx::fence_proxy_async_shared();
+      uint32_t g = 0;
+      for (uint32_t it = it0, i = 0; it < it1; ++it, ++i) {
+        const UnitInfo u = unit_info(p.items + it);
+        const uint32_t buf = i & 1u, tb = tmem + buf * 2 * kTmemCols;
+        const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, u.r16, false, false);
+        ptx::mbar_wait(&tempty[buf], ((i >> 1) & 1u) ^ 1u);  // epilogue of item i - 2 read it
         ptx::tc_fence_after();
-        const uint32_t xa = sbase + st * kSStageBytes, xb = xa + kTileM * kChunkK * 2;
-        const uint32_t wa = xa + 2 * kTileM * kChunkK * 2;
+        for (uint32_t kc = 0; kc < NK; ++kc, ++g) {
+          const uint32_t st = g % kSStages, ph = (g / kSStages) & 1u;
+          ptx::mbar_wait(&full[st], ph);
+          if (p.dbg & 2u) {
+            ptx::mbar_arrive(&empty[st]);
+            continue;
+          }
+          ptx::fence_proxy_async_shared();
+          ptx::tc_fence_after();
+          const uint32_t xa = sbase + st * kSStageBytes, xb = xa + kTileM * kChunkK * 2;
+          const uint32_t wa = xa + 2 * kTileM * kChunkK * 2;
 #pragma unroll
-        for (uint32_t k = 0; k < kChunkK / 16; ++k) {
-          const uint64_t wd = ptx::smem_desc_sw128(wa + k * 32, 16, 1024);
-          ptx::umma_f16(tmem, ptx::smem_desc_sw128(xa + k * 32, 16, 1024), wd, idesc, (kc | k) != 0);
-          if (nt == 2)
-            ptx::umma_f16(tmem + kTmemCols, ptx::smem_desc_sw128(xb + k * 32, 16, 1024), wd, idesc,
-                          (kc | k) != 0);
+          for (uint32_t k = 0; k < kChunkK / 16; ++k) {
+            const uint64_t wd = ptx::smem_desc_sw128(wa + k * 32, 16, 1024);
+            ptx::umma_f16(tb, ptx::smem_desc_sw128(xa + k * 32, 16, 1024), wd, idesc, (kc | k) != 0);
+            if (u.nt == 2)
+              ptx::umma_f16(tb + kTmemCols, ptx::smem_desc_sw128(xb + k * 32, 16, 1024), wd, idesc,
+                            (kc | k) != 0);
+          }
+          ptx::umma_commit(&empty[st]);
         }
-        ptx::umma_commit(&empty[st]);
+        ptx::umma_commit(&tfull[buf]);
       }
-      ptx::umma_commit(v_full);
     }
     __syncwarp();
-  }
-  // --------------------------------------------- epilogue (all 8 warps)
-  // Warp w reads TMEM lanes 32·(w % 4) (its lane quarter), columns of half
-  // w / 4.  Partials are [tile][split] blocks of 128 × r16 fp32, rows of
-  // r16/4 16-byte chunks with chunk j of row m stored at j ^ (m & swm):
-  // staged through the (now idle) stage buffers without bank conflicts,
-  // written with one bulk copy, and read back coalesced by the reducing CTA.
-  ptx::mbar_wait(v_full, 0);
-  ptx::tc_fence_after();
-  {
-    const uint32_t m = (warp & 3) * 32 + lane;  // tile row == TMEM lane
-    const uint32_t lane_base = ((warp & 3) * 32) << 16;
-    const uint32_t nch = r16 / 4, swm = min(8u, nch & (0u - nch)) - 1u;
-    const uint32_t tile_floats = kTileM * r16;
-    for (uint32_t t = 0; t < ((p.dbg & 16u) ? 0u : nt); ++t) {
-      const uint32_t tile_i = t ? tile_b : tile_a;
-      float* stg = reinterpret_cast<float*>(smem + SSmem::stages + t * kTileM * kMaxRank * 4);
-      for (uint32_t cc = warp >> 2; cc < r16 / 16; cc += 2) {
-        uint32_t rv[16];
-        ptx::tmem_ld_32x32b_x16(tmem + lane_base + t * kTmemCols + cc * 16, rv);
-        ptx::tmem_ld_wait();
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const uint32_t q = warp - 8;
+    const uint32_t lane_base = (q * 32) << 16;
+    float* stg = reinterpret_cast<float*>(smem + SSmem::stg + q * kStgBytes);
+    for (uint32_t it = it0, i = 0; it < it1; ++it, ++i) {
+      const UnitInfo u = unit_info(p.items + it);
+      const uint32_t buf = i & 1u, tb = tmem + buf * 2 * kTmemCols;
+      ptx::mbar_wait(&tfull[buf], (i >> 1) & 1u);
+      ptx::tc_fence_after();
+      const uint32_t ntw = (p.dbg & 16u) ? 0u : u.nt;
+      for (uint32_t t = 0; t < ntw; ++t) {
+        const uint32_t tile_i = t ? u.tile_b : u.tile_a;
+        float* blk = p.vpart + (static_cast<uint64_t>(tile_i) * p.splits + u.split) * kTileM * kMaxRank +
+                     q * 32 * u.r16;
+        for (uint32_t pass = 0; pass * 64 < u.r16; ++pass) {
+          const uint32_t pw = min(64u, u.r16 - pass * 64), pw4 = pw / 4, swm = part_swm(pw4);
+          if (lane == 0) ptx::bulk_wait_read_n<0>();  // the staging buffer's last copy has read it
+          __syncwarp();
+          for (uint32_t cc = 0; cc < pw / 16; ++cc) {
+            uint32_t rv[16];
+            ptx::tmem_ld_32x32b_x16(tb + lane_base + t * kTmemCols + pass * 64 + cc * 16, rv);
+            ptx::tmem_ld_wait();
 #pragma unroll
-        for (uint32_t i = 0; i < 4; ++i)
-          reinterpret_cast<uint4*>(stg + m * r16)[(cc * 4 + i) ^ (m & swm)] =
-              make_uint4(rv[4 * i], rv[4 * i + 1], rv[4 * i + 2], rv[4 * i + 3]);
-      }
-      ptx::fence_proxy_async_shared();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        float* dst = p.vpart + (static_cast<uint64_t>(tile_i) * p.splits + split) * kTileM * kMaxRank;
-        ptx::bulk_s2g(dst, stg, tile_floats * 4);
-        ptx::bulk_commit();
-        ptx::bulk_wait_all();  // written, not just read: the count below publishes it
-        ptx::fence_proxy_async_global();
-        __threadfence();
-        *last_flag = atomicAdd(p.tcnt + tile_i, 1u) == p.splits - 1;
-      }
-      __syncthreads();
-      if (*last_flag && !(p.dbg & 32u)) {
-        // split-K reduction by the tile's last CTA, in split order; 4 float4
-        // per thread and two splits per step keep 8 loads in flight
-        __threadfence();
-        constexpr uint32_t kU = 4;
-        constexpr uint32_t kSplitStride = kTileM * kMaxRank / 4;  // float4s
-        const float4* v0 = reinterpret_cast<const float4*>(
-            p.vpart + static_cast<uint64_t>(tile_i) * p.splits * kTileM * kMaxRank);
-        __nv_bfloat16* vb = p.vbuf + static_cast<uint64_t>(tile_i) * kTileM * kMaxRank;
-        const uint32_t n4 = tile_floats / 4;
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (uint32_t f0 = threadIdx.x; f0 < n4; f0 += kU * kThreads) {
-          float4 acc[kU];
-#pragma unroll
-          for (uint32_t u = 0; u < kU; ++u) acc[u] = z;
-          for (uint32_t sp = 0; sp < p.splits; sp += 2) {
-            float4 q0[kU], q1[kU];
-#pragma unroll
-            for (uint32_t u = 0; u < kU; ++u) {
-              const uint32_t f = f0 + u * kThreads;
-              q0[u] = f < n4 ? __ldcg(v0 + sp * kSplitStride + f) : z;
-              q1[u] = f < n4 && sp + 1 < p.splits ? __ldcg(v0 + (sp + 1) * kSplitStride + f) : z;
-            }
-#pragma unroll
-            for (uint32_t u = 0; u < kU; ++u) {
-              acc[u].x += q0[u].x; acc[u].y += q0[u].y; acc[u].z += q0[u].z; acc[u].w += q0[u].w;
-              acc[u].x += q1[u].x; acc[u].y += q1[u].y; acc[u].z += q1[u].z; acc[u].w += q1[u].w;
-            }
+            for (uint32_t c = 0; c < 4; ++c)
+              reinterpret_cast<uint4*>(stg + lane * pw)[(cc * 4 + c) ^ (lane & swm)] =
+                  make_uint4(rv[4 * c], rv[4 * c + 1], rv[4 * c + 2], rv[4 * c + 3]);
           }
-#pragma unroll
-          for (uint32_t u = 0; u < kU; ++u) {
-            const uint32_t f = f0 + u * kThreads;
-            if (f >= n4) continue;
-            const uint32_t row = f / nch, j = (f % nch) ^ (row & swm);
-            uint2 o;
-            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-            h[0] = __floats2bfloat162_rn(acc[u].x, acc[u].y);
-            h[1] = __floats2bfloat162_rn(acc[u].z, acc[u].w);
-            *reinterpret_cast<uint2*>(vb + row * kMaxRank + j * 4) = o;
+          ptx::fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::bulk_s2g(blk + pass * 32 * 64, stg, 32 * pw * 4);
+            ptx::bulk_commit();
           }
         }
-        if (threadIdx.x == 0) p.tcnt[tile_i] = 0;  // graph-replayable
       }
-      __syncthreads();  // last_flag and the staging buffer are reused by the next tile
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[buf]);  // TMEM buffer free for item i + 2
     }
+    if (lane == 0) ptx::bulk_wait_all();  // partials written before the grid completes
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 7) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, kSTmemCols);
+  }
+}
+
+// ------------------------------------------------------------------ reduce
+// V tile i = bf16(Σ_split partial[i][split]), summed in split order.  Block
+// (tile, quarter) reads its quarter's float4s of every split coalesced.
+constexpr uint32_t kRThreads = 256;
+
+struct ReduceArgs {
+  const SgmvTile* tiles;
+  const float* vpart;
+  __nv_bfloat16* vbuf;  // [tile][128][128] bf16
+  uint32_t splits;
+};
+
+__global__ void __launch_bounds__(kRThreads) sgmv_reduce_kernel(const ReduceArgs p) {
+  ptx::pdl_launch_dependents();
+  const uint32_t tile = blockIdx.x >> 2, qq = blockIdx.x & 3;
+  const uint32_t r16 = (p.tiles[tile].rank + 15) & ~15u, q4 = 8 * r16;  // float4s per quarter
+  constexpr uint32_t kSplitStride = kTileM * kMaxRank / 4;  // float4s
+  const float4* v0 = reinterpret_cast<const float4*>(p.vpart) +
+                     static_cast<uint64_t>(tile) * p.splits * kSplitStride + qq * q4;
+  __nv_bfloat16* vb = p.vbuf + static_cast<uint64_t>(tile) * kTileM * kMaxRank;
+  ptx::pdl_wait();  // the shrink's partials
+  constexpr uint32_t kU = 4;
+  for (uint32_t f0 = threadIdx.x; f0 < q4; f0 += kU * kRThreads) {
+    float4 acc[kU];
+#pragma unroll
+    for (uint32_t c = 0; c < kU; ++c) acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (uint32_t sp = 0; sp < p.splits; sp += 2) {
+      float4 a0[kU], a1[kU];
+#pragma unroll
+      for (uint32_t c = 0; c < kU; ++c) {
+        const uint32_t f = f0 + c * kRThreads;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        a0[c] = f < q4 ? __ldcg(v0 + sp * kSplitStride + f) : z;
+        a1[c] = f < q4 && sp + 1 < p.splits ? __ldcg(v0 + (sp + 1) * kSplitStride + f) : z;
+      }
+#pragma unroll
+      for (uint32_t c = 0; c < kU; ++c) {
+        acc[c].x += a0[c].x; acc[c].y += a0[c].y; acc[c].z += a0[c].z; acc[c].w += a0[c].w;
+        acc[c].x += a1[c].x; acc[c].y += a1[c].y; acc[c].z += a1[c].z; acc[c].w += a1[c].w;
+      }
+    }
+#pragma unroll
+    for (uint32_t c = 0; c < kU; ++c) {
+      const uint32_t f = f0 + c * kRThreads;
+      if (f >= q4) continue;
+      const uint32_t pass = f / 512, rem = f - pass * 512;
+      const uint32_t pw4 = min(16u, r16 / 4 - pass * 16), row = rem / pw4, jp = rem - row * pw4;
+      const uint32_t j = jp ^ (row & part_swm(pw4));
+      uint2 o;
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+      h[0] = __floats2bfloat162_rn(acc[c].x, acc[c].y);
+      h[1] = __floats2bfloat162_rn(acc[c].z, acc[c].w);
+      *reinterpret_cast<uint2*>(vb + (qq * 32 + row) * kMaxRank + pass * 64 + j * 4) = o;
+    }
   }
 }
 
@@ -603,7 +665,8 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     if (plan->n_tiles == 0) return 0;
     DeviceCtx ctx(st.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const uint32_t splits = sgmv_splits(plan->n_tiles, din);
+    const SgmvSched& sc = plan->ssched[proj];
+    const uint32_t splits = sc.splits;
     CUtensorMap tmap_x, tmap_y, tmap_v;
     make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kChunkK, kTileM);
     make_tmap_2d(&tmap_y, y, dout, plan->n_tokens, y_stride * 2, 64, kTileM);
@@ -625,24 +688,31 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     sa.arena = st.arena;
     sa.table = st.d_table;
     sa.tiles = plan->d_tiles;
-    sa.units = plan->d_sunits;
+    sa.items = plan->d_sitems + sc.item_off;
+    sa.cta_items = plan->d_scta + sc.cta_off;
     sa.vpart = plan->d_vpart;
-    sa.vbuf = reinterpret_cast<__nv_bfloat16*>(plan->d_vbuf);
-    sa.tcnt = plan->d_tcnt;
     sa.blk_mult = g.blk_mult(layer, proj);
     sa.log2_page = st.log2_page;
     sa.d_in = din;
     sa.splits = splits;
     sa.dbg = g_sgmv_dbg;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(plan->n_sunits * splits);
-    cfg.blockDim = dim3(kThreads);
+    cfg.gridDim = dim3(sc.ctas);
+    cfg.blockDim = dim3(kSThreads);
     cfg.dynamicSmemBytes = SSmem::alloc;
     cfg.stream = s;
     cfg.attrs = pdl;
     cfg.numAttrs = 1;
     PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_shrink_kernel, sa, tmap_x));
     count_launch();
+    if (!(g_sgmv_dbg & 32u)) {
+      ReduceArgs ra{plan->d_tiles, plan->d_vpart, reinterpret_cast<__nv_bfloat16*>(plan->d_vbuf), splits};
+      cfg.gridDim = dim3(plan->n_tiles * 4);
+      cfg.blockDim = dim3(kRThreads);
+      cfg.dynamicSmemBytes = 0;
+      PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_reduce_kernel, ra));
+      count_launch();
+    }
     if (g_sgmv_dbg & 8u) return 0;
 
     ExpandArgs ea{};
