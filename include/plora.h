@@ -465,7 +465,9 @@ int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
 int plora_debug_plan_geom(const plora_plan* plan, uint32_t proj, uint32_t out[8]);
 /* Timing experiments only (results are wrong while set): the next SGMV
  * shrink launches skip their 1 = weight gathers, 2 = MMAs, 4 = x loads,
- * 16 = epilogue; 32 = the split reduction launch, 8 = the expand launch.  0 restores the op. */
+ * 16 = epilogue; 32 = the split reduction launch, 8 = the expand launch;
+ * the expand skips its 64 = y reduce-adds, 128 = Bᵀ gathers, 256 = MMAs,
+ * 512 = everything after its prologue.  0 restores the op. */
 int plora_debug_set_sgmv_flags(uint32_t flags);
 
 #ifdef __cplusplus

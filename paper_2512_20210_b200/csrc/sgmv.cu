@@ -414,8 +414,10 @@ constexpr uint32_t kEBlockN = 64;     // output columns per block (one 128-byte 
 constexpr uint32_t kGroupBlocks = 8;  // blocks per CTA (512 columns)
 constexpr uint32_t kETmemCols = 2 * kEBlockN;
 // warps 0 TMA, 1-3 Bᵀ gathers, 4-7 epilogue, 8 MMA issuer (its own warp: the
-// epilogue releases the accumulators the MMA loop waits for)
+// epilogue releases the accumulators the MMA loop waits for).  (Eight
+// epilogue warps measured slower: the y stream, not the epilogue, bounds it.)
 constexpr int kEThreads = 288;
+constexpr uint32_t kEEpiThreads = 128;
 
 struct ExpandArgs {
   const char* arena;
@@ -429,6 +431,7 @@ struct ExpandArgs {
   uint32_t d_out;
   uint32_t ngroups;  // column groups per tile
   float scale;
+  uint32_t dbg;  // diagnostics: 64 no y reduce-add, 128 no Bᵀ gather, 256 no MMA, 512 prologue only
 };
 
 struct ESmem {  // ~97 KB: two expand CTAs per SM
@@ -489,7 +492,8 @@ __global__ void __launch_bounds__(kEThreads, 2)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (p.dbg & 512u) {
+  } else if (warp == 0) {
     // ----------------------------------------------- TMA: V tile once
     if (lane == 0) {
       ptx::pdl_wait();  // V comes from the shrink (and y may be read by earlier kernels)
@@ -500,29 +504,45 @@ __global__ void __launch_bounds__(kEThreads, 2)
     }
   } else if (warp < 4) {
     // ----------------------------------- Bᵀ block gathers (paged rows)
-    // Thread wt owns rank rows wt and wt + 96; with pages >= 256 B a row's
-    // 256-byte block slice lies in one page (one lookup, issued a block ahead).
+    // Thread wt owns rank rows wt and wt + 96.  A row's 1 KiB group slice
+    // spans few pages: the thread keeps each row's current page frame and
+    // the next one's (looked up a page ahead), so no block waits on a lookup.
     const uint32_t wt = threadIdx.x - 32;
     const bool fast = p.log2_page >= 7;  // a row's 128-byte block slice lies in one page
     const uint64_t pmask = (1ull << p.log2_page) - 1;
     auto row_off = [&](uint32_t j, uint32_t b) {
       return bt + (static_cast<uint64_t>(j) * p.d_out + col_base + b * kEBlockN) * 2;
     };
-    auto lookup = [&](uint32_t j, uint32_t b) -> uint32_t {
-      return (fast && j < r && b < nblk) ? __ldg(p.table + tile.table_off + static_cast<uint32_t>(row_off(j, b) >> p.log2_page)) : 0u;
-    };
-    uint32_t ph0 = lookup(wt, 0), ph1 = lookup(wt + kEGather, 0);
+    uint32_t lp[2], lp_last[2], e_cur[2], e_nxt[2];
+#pragma unroll
+    for (uint32_t h = 0; h < 2; ++h) {
+      const uint32_t j = wt + h * kEGather;
+      const bool live = fast && j < r && nblk > 0;
+      lp[h] = static_cast<uint32_t>(row_off(j, 0) >> p.log2_page);
+      lp_last[h] = live ? static_cast<uint32_t>((row_off(j, nblk - 1) + kEBlockN * 2 - 1) >> p.log2_page) : 0u;
+      e_cur[h] = live ? __ldg(p.table + tile.table_off + lp[h]) : 0u;
+      e_nxt[h] = live && lp[h] < lp_last[h] ? __ldg(p.table + tile.table_off + lp[h] + 1) : 0u;
+    }
     for (uint32_t b = 0; b < nblk; ++b) {
       const uint32_t st = b & 1u, ph = (b >> 1) & 1u;
-      const uint32_t nx0 = lookup(wt, b + 1), nx1 = lookup(wt + kEGather, b + 1);
+#pragma unroll
+      for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t j = wt + h * kEGather;
+        const uint32_t lpb = static_cast<uint32_t>(row_off(j, b) >> p.log2_page);
+        if (fast && j < r && lpb != lp[h]) {  // crossed into the next page
+          lp[h] = lpb;
+          e_cur[h] = e_nxt[h];
+          e_nxt[h] = lpb < lp_last[h] ? __ldg(p.table + tile.table_off + lpb + 1) : 0u;
+        }
+      }
       ptx::mbar_wait(&b_empty[st], ph ^ 1u);
       char* bs = smem + ESmem::b + st * 16384;
 #pragma unroll
       for (uint32_t h = 0; h < 2; ++h) {  // rows wt and wt + 96
         const uint32_t j = wt + h * kEGather;
-        if (j >= r16) continue;
+        if (j >= r16 || (p.dbg & 128u)) continue;
         const uint64_t off = row_off(j, b);
-        const char* base = p.arena + (static_cast<uint64_t>(h ? ph1 : ph0) << p.log2_page) + (off & pmask);
+        const char* base = p.arena + (static_cast<uint64_t>(e_cur[h]) << p.log2_page) + (off & pmask);
 #pragma unroll
         for (uint32_t q = 0; q < 8; ++q) {
           char* dst = bs + swz(j, q);
@@ -535,8 +555,6 @@ __global__ void __launch_bounds__(kEThreads, 2)
         }
       }
       ptx::cp_async_mbar_arrive_noinc(&b_full[st]);
-      ph0 = nx0;
-      ph1 = nx1;
     }
   } else if (warp == 8) {
     if (lane == 0) {
@@ -552,7 +570,7 @@ __global__ void __launch_bounds__(kEThreads, 2)
         ptx::fence_proxy_async_shared();
         ptx::tc_fence_after();
         const uint32_t bbase = ptx::smem_u32(smem + ESmem::b + st * 16384);
-        for (uint32_t kk = 0; kk < r16 / 16; ++kk)
+        for (uint32_t kk = 0; kk < ((p.dbg & 256u) ? 0u : r16 / 16); ++kk)
           ptx::umma_f16(tmem + st * kEBlockN,
                         ptx::smem_desc_sw128(vbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                         ptx::smem_desc_sw128(bbase + kk * 2048, lbo, 1024), idesc, kk != 0);
@@ -562,7 +580,7 @@ __global__ void __launch_bounds__(kEThreads, 2)
     }
   } else {
     // ------------------------------------------------- epilogue (warps 4-7)
-    const uint32_t m = (warp - 4) * 32 + lane;  // tile row == TMEM lane
+    const uint32_t m = (warp & 3) * 32 + lane;  // tile row == TMEM lane
     const uint32_t lane_base = ((warp & 3) * 32) << 16;
     const bool live = m < tile.nrows;  // rows past the run belong to the next one: add 0
     for (uint32_t b = 0; b < nblk; ++b) {
@@ -571,7 +589,7 @@ __global__ void __launch_bounds__(kEThreads, 2)
       char* ys = smem + ESmem::y + st * 16384;
       if (b >= 2) {  // the reduce-store of block b - 2 must have read stage st
         if (warp == 4 && lane == 0) ptx::bulk_wait_read_n<1>();
-        ptx::named_bar_sync(1, 128);
+        ptx::named_bar_sync(1, kEEpiThreads);
       }
       ptx::mbar_wait(&acc_full[st], ph);
       ptx::tc_fence_after();
@@ -595,10 +613,10 @@ __global__ void __launch_bounds__(kEThreads, 2)
       }
       ptx::tc_fence_before();
       ptx::fence_proxy_async_shared();  // generic-proxy smem writes -> TMA
-      ptx::named_bar_sync(1, 128);
+      ptx::named_bar_sync(1, kEEpiThreads);
       if (warp == 4 && lane == 0) {
         ptx::mbar_arrive(&acc_empty[st]);
-        ptx::tma_reduce_add_2d(&tmap_y, static_cast<int32_t>(col0), static_cast<int32_t>(tile.row0), ys);
+        if (!(p.dbg & 64u)) ptx::tma_reduce_add_2d(&tmap_y, static_cast<int32_t>(col0), static_cast<int32_t>(tile.row0), ys);
         ptx::bulk_commit();
       }
     }
@@ -727,6 +745,7 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     ea.d_out = dout;
     ea.ngroups = (dout / kEBlockN + kGroupBlocks - 1) / kGroupBlocks;
     ea.scale = scale;
+    ea.dbg = g_sgmv_dbg;
     cfg.gridDim = dim3(plan->n_tiles * ea.ngroups);
     cfg.blockDim = dim3(kEThreads);
     cfg.dynamicSmemBytes = ESmem::alloc;

@@ -29,7 +29,9 @@ for r in ranks:
     for name, flags in (("full op", 0), ("shrink only", 8), ("shrink, no gather", 9), ("shrink, no MMA", 10),
                         ("shrink, no x", 12), ("shrink, x only", 11), ("shrink, gather only", 14),
                         ("shrink, nothing", 15), ("shrink, no reduction", 40), ("shrink, no epilogue", 24),
-                        ("shrink, nothing at all", 31)):
+                        ("shrink, nothing at all", 31), ("expand, no y", 64), ("expand, no B", 128),
+                        ("expand, no MMA", 256), ("expand, only y", 384), ("expand, nothing", 448),
+                        ("expand prologue only", 512)):
         N.check(N.lib().plora_debug_set_sgmv_flags(flags))
         for _ in range(3):
             sgmv(plan, 1, 0, x, y)
