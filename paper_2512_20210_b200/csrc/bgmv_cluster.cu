@@ -54,12 +54,12 @@ constexpr uint32_t kMaxSlots = 8;
 constexpr uint32_t kXSlotFloats = kJobTok * kChunkRows * kMaxCs;  // [t][row][src cta]
 constexpr uint32_t kSmemBudget = 200 * 1024;  // 227 KiB (5 slots) measured no faster
 constexpr uint32_t kMaxSlice = 1024;  // elements per CTA slice (preferred)
+constexpr uint32_t kMaxClusters = 64;  // 148 SMs / clusters of >= 4
 
 struct CArgs {
   const char* arena;
   const uint32_t* table;
   const ClusterChunk* chunks;
-  const uint32_t* cl_off;
   const char* x;
   uint64_t x_stride_b;
   // per projection of the launch (chunk record field `proj`): output, its row
@@ -76,6 +76,9 @@ struct CArgs {
   uint32_t fast;  // every row slice lies inside one page (see my_piece)
   float scale;
   uint64_t* trace;  // diagnostics (plora_debug_set_trace) or nullptr
+  // cluster c runs chunks [cl_off[c], cl_off[c + 1]): a kernel parameter, so
+  // the prologue's first dependent load is the chunk record itself
+  uint32_t cl_off[kMaxClusters + 1];
 };
 
 constexpr uint32_t kTraceChunks = 64;
@@ -750,7 +753,7 @@ ClusterGeom cluster_geom(uint32_t d_in, uint32_t d_out, int device) {
     throw ValidationError("bf16 BGMV: d_in " + std::to_string(d_in) + " / d_out " +
                           std::to_string(d_out) + " leave fewer than 3 ring slots");
   g.smem = g.slots * g.slot_bytes + fixed;
-  g.n_clusters = static_cast<uint32_t>(max_clusters(device, g.cs, g.smem));
+  g.n_clusters = std::min<uint32_t>(kMaxClusters, static_cast<uint32_t>(max_clusters(device, g.cs, g.smem)));
   return g;
 }
 
@@ -767,7 +770,7 @@ void launch(const plora_plan& plan, const ClusterWork& cw, uint32_t layer, const
   a.arena = st.arena;
   a.table = st.d_table;
   a.chunks = plan.d_cchunks + cw.chunks_off;
-  a.cl_off = plan.d_ccl_off + cw.cl_off;
+  for (uint32_t c = 0; c <= g.n_clusters; ++c) a.cl_off[c] = plan.ccl_off[cw.cl_off + c];
   a.x = static_cast<const char*>(x);
   a.x_stride_b = x_stride * 2;
   a.log2_page = st.log2_page;

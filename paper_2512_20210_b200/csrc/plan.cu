@@ -331,19 +331,25 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     }
   }
 
-  // ---- upload units | tiles | cluster chunks | offsets in one copy
-  // from a pinned staging buffer
+  // ---- upload the device-side work lists in one copy from a pinned
+  // staging buffer (cluster chunk offsets travel as kernel parameters)
   auto align = [](uint64_t v) { return (v + 255) & ~255ull; };
-  const uint64_t unit_b = align(units.size() * sizeof(BgmvUnit));
-  const uint64_t tile_b = align(tiles.size() * sizeof(SgmvTile));
-  const uint64_t cch_b = align(cchunks.size() * sizeof(ClusterChunk));
-  const uint64_t ccl_b = align(ccl_off.size() * sizeof(uint32_t));
-  const uint64_t cjob_b = align(cjobs.size() * sizeof(ClusterJob));
-  const uint64_t sun_b = align(sunits.size() * sizeof(uint32_t));
-  const uint64_t sit_b = align(sitems.size() * sizeof(SgmvItem));
-  const uint64_t sct_b = align(scta.size() * sizeof(uint32_t));
-  const uint64_t total =
-      std::max<uint64_t>(unit_b + tile_b + cch_b + ccl_b + cjob_b + sun_b + sit_b + sct_b, 256);
+  struct Part {
+    const void* src;
+    uint64_t bytes;
+    void** dst;
+  };
+  const Part parts[] = {
+      {units.data(), units.size() * sizeof(BgmvUnit), reinterpret_cast<void**>(&d_units)},
+      {tiles.data(), tiles.size() * sizeof(SgmvTile), reinterpret_cast<void**>(&d_tiles)},
+      {cchunks.data(), cchunks.size() * sizeof(ClusterChunk), reinterpret_cast<void**>(&d_cchunks)},
+      {cjobs.data(), cjobs.size() * sizeof(ClusterJob), reinterpret_cast<void**>(&d_cjobs)},
+      {sitems.data(), sitems.size() * sizeof(SgmvItem), reinterpret_cast<void**>(&d_sitems)},
+      {scta.data(), scta.size() * sizeof(uint32_t), reinterpret_cast<void**>(&d_scta)},
+  };
+  uint64_t total = 0;
+  for (const Part& pt : parts) total += align(pt.bytes);
+  total = std::max<uint64_t>(total, 256);
   DeviceCtx ctx(st.device);
   if (upload_done) PLORA_CUDA(cudaEventSynchronize(upload_done));  // pinned buffer reuse
   if (h_cap < total) {
@@ -361,27 +367,11 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     PLORA_CUDA(cudaMalloc(&d_buf, total));
     d_cap = total;
   }
-  std::memcpy(h_pinned, units.data(), units.size() * sizeof(BgmvUnit));
-  std::memcpy(h_pinned + unit_b, tiles.data(), tiles.size() * sizeof(SgmvTile));
-  std::memcpy(h_pinned + unit_b + tile_b, cchunks.data(),
-              cchunks.size() * sizeof(ClusterChunk));
-  std::memcpy(h_pinned + unit_b + tile_b + cch_b, ccl_off.data(),
-              ccl_off.size() * sizeof(uint32_t));
-  d_units = reinterpret_cast<BgmvUnit*>(d_buf);
-  d_tiles = reinterpret_cast<SgmvTile*>(d_buf + unit_b);
-  d_cchunks = reinterpret_cast<ClusterChunk*>(d_buf + unit_b + tile_b);
-  d_ccl_off = reinterpret_cast<uint32_t*>(d_buf + unit_b + tile_b + cch_b);
-  std::memcpy(h_pinned + unit_b + tile_b + cch_b + ccl_b, cjobs.data(), cjobs.size() * sizeof(ClusterJob));
-  d_cjobs = reinterpret_cast<ClusterJob*>(d_buf + unit_b + tile_b + cch_b + ccl_b);
-  std::memcpy(h_pinned + unit_b + tile_b + cch_b + ccl_b + cjob_b, sunits.data(),
-              sunits.size() * sizeof(uint32_t));
-  d_sunits = reinterpret_cast<uint32_t*>(d_buf + unit_b + tile_b + cch_b + ccl_b + cjob_b);
-  {
-    const uint64_t o = unit_b + tile_b + cch_b + ccl_b + cjob_b + sun_b;
-    std::memcpy(h_pinned + o, sitems.data(), sitems.size() * sizeof(SgmvItem));
-    std::memcpy(h_pinned + o + sit_b, scta.data(), scta.size() * sizeof(uint32_t));
-    d_sitems = reinterpret_cast<SgmvItem*>(d_buf + o);
-    d_scta = reinterpret_cast<uint32_t*>(d_buf + o + sit_b);
+  uint64_t off = 0;
+  for (const Part& pt : parts) {
+    if (pt.bytes) std::memcpy(h_pinned + off, pt.src, pt.bytes);
+    *pt.dst = d_buf + off;
+    off += align(pt.bytes);
   }
   PLORA_CUDA(cudaMemcpyAsync(d_buf, h_pinned, total, cudaMemcpyHostToDevice, stream));
   if (!upload_done) PLORA_CUDA(cudaEventCreateWithFlags(&upload_done, cudaEventDisableTiming));

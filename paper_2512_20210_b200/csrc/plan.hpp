@@ -177,7 +177,6 @@ struct plora_plan {
   std::vector<uint32_t> ccl_off;
   plora::ClusterChunk* d_cchunks = nullptr;
   plora::ClusterJob* d_cjobs = nullptr;
-  uint32_t* d_ccl_off = nullptr;
   char* h_pinned = nullptr;
   uint64_t h_cap = 0;
   char* d_buf = nullptr;
@@ -197,7 +196,6 @@ struct plora_plan {
   // the adapter's A chunks), {tile, tile or ~0u}
   std::vector<uint32_t> sunits;
   uint32_t n_sunits = 0;
-  uint32_t* d_sunits = nullptr;
   plora::SgmvSched ssched[PLORA_MAX_PROJ];
   std::vector<plora::SgmvItem> sitems;
   std::vector<uint32_t> scta;
