@@ -590,6 +590,9 @@ int plora_engine_flush_predictor(plora_engine* e) {
     if (!e->svc) return 0;
     auto& sv = *e->svc;
     std::unique_lock<std::mutex> sl(sv.m);
+    // on_arrival wakes the worker only every 64 observations: wake it for
+    // the tail, or this wait would outlast a sleeping worker
+    sv.cv.notify_one();
     sv.idle.wait(sl, [&] { return sv.obs.empty() && !sv.round_req && !sv.busy; });
     if (!sv.error.empty()) throw ValidationError(sv.error);
     if (sv.have) {

@@ -38,7 +38,7 @@ if has cfg3; then
   echo "cfg3 rc=$?" >> gpurun_out/bench_cfg3.err
 fi
 if has fullsgmv; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgmv_ -s 70 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgmv_ -s 70 -c 3 \
     -o gpurun_out/sgmv_full -f python bench.py --workload cfg3 --steps 1 --warmup 3 --no-e2e --no-cpu \
     > gpurun_out/ncu_sgmv.log 2>&1
   echo "fullsgmv rc=$?" >> gpurun_out/ncu_sgmv.log

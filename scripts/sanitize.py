@@ -33,6 +33,10 @@ def main():
     xs = torch.randn(len(seg), 4096, device="cuda").to(torch.bfloat16)
     yss = torch.randn(len(seg), 4096, device="cuda").to(torch.bfloat16)
     sgmv(BatchPlan(s.store, seg), 1, 1, xs, yss)
+    seg2 = synth.segment_assignment(3, 300)  # runs of 300: tile pairs sharing the weight chunks
+    xs2 = torch.randn(len(seg2), 4096, device="cuda").to(torch.bfloat16)
+    ys2 = torch.randn(len(seg2), 4096, device="cuda").to(torch.bfloat16)
+    sgmv(BatchPlan(s.store, seg2), 1, 0, xs2, ys2)
     rs = tp_shard_rows(plan, 2)
     vp = torch.empty(2, T, rs, device="cuda")
     for i in range(2):
