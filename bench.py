@@ -359,7 +359,7 @@ def run_ours(args):
     avg_launch_ms = step_ms / (L * LPS)
     achieved = per_call / (avg_launch_ms / 1e3) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "bgmv_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "sgmv_traffic.json" if prefill else "bgmv_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
