@@ -290,6 +290,14 @@ int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x
 int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                plora_stream_t stream);
+/* Prefill with the base projection fused in: for every
+ * token row t of the plan (with or without an adapter)
+ *   y[t] = x[t] · W0ᵀ + bf16(scale · x[t] · A_{a(t)}ᵀ) · B_{a(t)}ᵀ
+ * w0: the base weight [d_out, d_in] (row stride w0_stride elements), y is
+ * overwritten.  bf16 store, rank <= 128, d_in % 64 == 0, d_out % 256 == 0. */
+int plora_sgmv_fused(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
+                     uint64_t x_stride, const void* w0, uint64_t w0_stride, void* y,
+                     uint64_t y_stride, float scale, plora_stream_t stream);
 
 /* ------------------- tensor-parallel decode (new; BASELINE cfg5) -----
  * The S-LoRA scheme for a column-parallel base projection (hidden-dim

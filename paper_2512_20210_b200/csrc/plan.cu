@@ -139,15 +139,25 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
 
   // ---- SGMV tiles: runs of consecutive tokens with the same adapter
   tiles.clear();
+  gtiles.clear();
   uint32_t t = 0;
   while (t < n) {
     const int32_t a = token_adapter[t];
     uint32_t e = t + 1;
     while (e < n && token_adapter[e] == a) ++e;
-    if (a >= 0) {
-      for (uint32_t r0 = t; r0 < e; r0 += 128)
-        tiles.push_back(SgmvTile{r0, std::min<uint32_t>(128, e - r0), st.h_dir[a].table_off,
-                                 st.h_dir[a].rank});
+    for (uint32_t r0 = t; r0 < e; r0 += 128) {
+      const uint32_t nr = std::min<uint32_t>(128, e - r0);
+      GemmTile gt{};
+      gt.row0 = r0;
+      gt.nrows = nr;
+      gt.vtile = 0xffffffffu;
+      if (a >= 0) {
+        gt.table_off = st.h_dir[a].table_off;
+        gt.rank = st.h_dir[a].rank;
+        gt.vtile = static_cast<uint32_t>(tiles.size());
+        tiles.push_back(SgmvTile{r0, nr, st.h_dir[a].table_off, st.h_dir[a].rank});
+      }
+      gtiles.push_back(gt);
     }
     t = e;
   }
@@ -342,6 +352,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   const Part parts[] = {
       {units.data(), units.size() * sizeof(BgmvUnit), reinterpret_cast<void**>(&d_units)},
       {tiles.data(), tiles.size() * sizeof(SgmvTile), reinterpret_cast<void**>(&d_tiles)},
+      {gtiles.data(), gtiles.size() * sizeof(GemmTile), reinterpret_cast<void**>(&d_gtiles)},
       {cchunks.data(), cchunks.size() * sizeof(ClusterChunk), reinterpret_cast<void**>(&d_cchunks)},
       {cjobs.data(), cjobs.size() * sizeof(ClusterJob), reinterpret_cast<void**>(&d_cjobs)},
       {sitems.data(), sitems.size() * sizeof(SgmvItem), reinterpret_cast<void**>(&d_sitems)},

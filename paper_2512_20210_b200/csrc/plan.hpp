@@ -142,6 +142,13 @@ struct SgmvTile {
   uint32_t rank;
 };
 
+// Fused base-GEMM + LoRA prefill (sgmv_fused.cu): every token row is in
+// exactly one 128-row tile of a run (adapter runs and runs of tokens without
+// an adapter); vtile indexes the run's SGMV tile (its V rows), ~0u for none.
+struct GemmTile {
+  uint32_t row0, nrows, table_off, rank, vtile, pad[3];
+};
+
 // One SGMV shrink work item: a unit (one tile, or two consecutive full tiles
 // of one run, tile_b = ~0u otherwise) × one K slice, self-contained so the
 // kernel reads one 32-byte record per item.
@@ -197,6 +204,8 @@ struct plora_plan {
   std::vector<uint32_t> sunits;
   uint32_t n_sunits = 0;
   plora::SgmvSched ssched[PLORA_MAX_PROJ];
+  std::vector<plora::GemmTile> gtiles;
+  plora::GemmTile* d_gtiles = nullptr;
   std::vector<plora::SgmvItem> sitems;
   std::vector<uint32_t> scta;
   plora::SgmvItem* d_sitems = nullptr;

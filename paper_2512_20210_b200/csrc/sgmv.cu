@@ -40,6 +40,7 @@
 
 #include "plan.hpp"
 #include "ptx.cuh"
+#include "tmap.cuh"
 
 using namespace plora;
 
@@ -53,6 +54,7 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
                           plora_stream_t stream);
 
 namespace {
+using namespace plora::tmap;
 
 uint32_t g_sgmv_dbg = 0;  // plora_debug_set_sgmv_flags
 
@@ -69,22 +71,6 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&h);
 }
-
-__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
-  // 128-byte swizzle inside an 8-row × 128-byte atom
-  return (row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4);
-}
-
-struct PagedSrc {
-  const char* arena;
-  const uint32_t* table;
-  uint32_t table_off;
-  uint32_t log2_page;
-  __device__ const char* at(uint64_t off) const {
-    const uint32_t phys = __ldg(table + table_off + static_cast<uint32_t>(off >> log2_page));
-    return arena + (static_cast<uint64_t>(phys) << log2_page) + (off & ((1ull << log2_page) - 1));
-  }
-};
 
 // ------------------------------------------------------------------ shrink
 // Persistent: one CTA per SM runs its LPT-scheduled work items, each a unit
@@ -356,6 +342,7 @@ struct ReduceArgs {
   const float* vpart;
   __nv_bfloat16* vbuf;  // [tile][128][128] bf16
   uint32_t splits;
+  float scale;  // V = bf16(scale · Σ partials): 1 for plora_sgmv, the LoRA scale when fused
 };
 
 __global__ void __launch_bounds__(kRThreads) sgmv_reduce_kernel(const ReduceArgs p) {
@@ -396,8 +383,8 @@ __global__ void __launch_bounds__(kRThreads) sgmv_reduce_kernel(const ReduceArgs
       const uint32_t j = jp ^ (row & part_swm(pw4));
       uint2 o;
       __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
-      h[0] = __floats2bfloat162_rn(acc[c].x, acc[c].y);
-      h[1] = __floats2bfloat162_rn(acc[c].z, acc[c].w);
+      h[0] = __floats2bfloat162_rn(p.scale * acc[c].x, p.scale * acc[c].y);
+      h[1] = __floats2bfloat162_rn(p.scale * acc[c].z, p.scale * acc[c].w);
       *reinterpret_cast<uint2*>(vb + (qq * 32 + row) * kMaxRank + pass * 64 + j * 4) = o;
     }
   }
@@ -630,41 +617,66 @@ __global__ void __launch_bounds__(kEThreads, 2)
   }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-  });
-  if (!fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
-  return fn;
-}
-
-
-void make_tmap_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
-                  uint64_t row_stride_b, uint32_t box_cols, uint32_t box_rows) {
-  const cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
-  const cuuint64_t strides[1] = {row_stride_b};
-  const cuuint32_t box[2] = {box_cols, box_rows};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string(cr));
-}
-
 }  // namespace
 
 extern "C" int plora_debug_set_sgmv_flags(uint32_t flags) {
   g_sgmv_dbg = flags;
   return PLORA_OK;
 }
+
+namespace plora {
+
+// Shrink + split reduction of one (layer, proj) call: V tiles (bf16, scaled
+// by v_scale) in plan->d_vbuf.  Shared by plora_sgmv and plora_sgmv_fused.
+void sgmv_shrink_reduce(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
+                        uint64_t x_stride, float v_scale, cudaStream_t s) {
+  const plora_store& st = *plan->store;
+  const ModelGeom& g = st.geom;
+  const uint32_t din = g.m.d_in[proj];
+  const SgmvSched& sc = plan->ssched[proj];
+  CUtensorMap tmap_x;
+  make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kChunkK, kTileM);
+  static bool attr = false;
+  if (!attr) {
+    PLORA_CUDA(cudaFuncSetAttribute(sgmv_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(SSmem::alloc)));
+    attr = true;
+  }
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  ShrinkArgs sa{};
+  sa.arena = st.arena;
+  sa.table = st.d_table;
+  sa.items = plan->d_sitems + sc.item_off;
+  sa.cta_items = plan->d_scta + sc.cta_off;
+  sa.vpart = plan->d_vpart;
+  sa.blk_mult = g.blk_mult(layer, proj);
+  sa.log2_page = st.log2_page;
+  sa.d_in = din;
+  sa.splits = sc.splits;
+  sa.dbg = g_sgmv_dbg;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sc.ctas);
+  cfg.blockDim = dim3(kSThreads);
+  cfg.dynamicSmemBytes = SSmem::alloc;
+  cfg.stream = s;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_shrink_kernel, sa, tmap_x));
+  count_launch();
+  if (!(g_sgmv_dbg & 32u)) {
+    ReduceArgs ra{plan->d_tiles, plan->d_vpart, reinterpret_cast<__nv_bfloat16*>(plan->d_vbuf),
+                  sc.splits, v_scale};
+    cfg.gridDim = dim3(plan->n_tiles * 4);
+    cfg.blockDim = dim3(kRThreads);
+    cfg.dynamicSmemBytes = 0;
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_reduce_kernel, ra));
+    count_launch();
+  }
+}
+
+}  // namespace plora
 
 extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                           uint64_t x_stride, void* y, uint64_t y_stride, float scale,
@@ -683,17 +695,15 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     if (plan->n_tiles == 0) return 0;
     DeviceCtx ctx(st.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const SgmvSched& sc = plan->ssched[proj];
-    const uint32_t splits = sc.splits;
-    CUtensorMap tmap_x, tmap_y, tmap_v;
-    make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kChunkK, kTileM);
+    sgmv_shrink_reduce(plan, layer, proj, x, x_stride, 1.0f, s);
+    if (g_sgmv_dbg & 8u) return 0;
+
+    CUtensorMap tmap_y, tmap_v;
     make_tmap_2d(&tmap_y, y, dout, plan->n_tokens, y_stride * 2, 64, kTileM);
     make_tmap_2d(&tmap_v, plan->d_vbuf, kMaxRank, static_cast<uint64_t>(plan->n_tiles) * kTileM,
                  kMaxRank * 2, 64, kTileM);
     static bool attr = false;
     if (!attr) {
-      PLORA_CUDA(cudaFuncSetAttribute(sgmv_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(SSmem::alloc)));
       PLORA_CUDA(cudaFuncSetAttribute(sgmv_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(ESmem::alloc)));
       attr = true;
@@ -701,38 +711,6 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
-
-    ShrinkArgs sa{};
-    sa.arena = st.arena;
-    sa.table = st.d_table;
-    sa.tiles = plan->d_tiles;
-    sa.items = plan->d_sitems + sc.item_off;
-    sa.cta_items = plan->d_scta + sc.cta_off;
-    sa.vpart = plan->d_vpart;
-    sa.blk_mult = g.blk_mult(layer, proj);
-    sa.log2_page = st.log2_page;
-    sa.d_in = din;
-    sa.splits = splits;
-    sa.dbg = g_sgmv_dbg;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(sc.ctas);
-    cfg.blockDim = dim3(kSThreads);
-    cfg.dynamicSmemBytes = SSmem::alloc;
-    cfg.stream = s;
-    cfg.attrs = pdl;
-    cfg.numAttrs = 1;
-    PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_shrink_kernel, sa, tmap_x));
-    count_launch();
-    if (!(g_sgmv_dbg & 32u)) {
-      ReduceArgs ra{plan->d_tiles, plan->d_vpart, reinterpret_cast<__nv_bfloat16*>(plan->d_vbuf), splits};
-      cfg.gridDim = dim3(plan->n_tiles * 4);
-      cfg.blockDim = dim3(kRThreads);
-      cfg.dynamicSmemBytes = 0;
-      PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_reduce_kernel, ra));
-      count_launch();
-    }
-    if (g_sgmv_dbg & 8u) return 0;
-
     ExpandArgs ea{};
     ea.arena = st.arena;
     ea.table = st.d_table;
@@ -746,9 +724,13 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     ea.ngroups = (dout / kEBlockN + kGroupBlocks - 1) / kGroupBlocks;
     ea.scale = scale;
     ea.dbg = g_sgmv_dbg;
+    cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(plan->n_tiles * ea.ngroups);
     cfg.blockDim = dim3(kEThreads);
     cfg.dynamicSmemBytes = ESmem::alloc;
+    cfg.stream = s;
+    cfg.attrs = pdl;
+    cfg.numAttrs = 1;
     PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y, tmap_v));
     count_launch();
     return 0;

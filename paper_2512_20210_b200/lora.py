@@ -280,5 +280,22 @@ def sgmv(plan: BatchPlan, layer: int, proj: int, x: torch.Tensor, y: torch.Tenso
     return y
 
 
+def sgmv_fused(plan: BatchPlan, layer: int, proj: int, x: torch.Tensor, w0: torch.Tensor,
+               y: torch.Tensor, scale: float = 1.0, stream: int | None = None) -> torch.Tensor:
+    """y = x · W0ᵀ + scale · (x · Aᵀ) · Bᵀ per token: the base projection with the
+    paged LoRA fused in (prefill, tensor cores); w0 is the base weight
+    [d_out, d_in], y is overwritten."""
+    _check_io(plan, proj, x, y)
+    if not w0.is_cuda or w0.dtype != torch.bfloat16 or w0.dim() != 2 or w0.stride(1) != 1:
+        raise N.ValidationError("w0 must be a 2-D bf16 CUDA tensor with unit column stride")
+    if w0.shape[0] != y.shape[1] or w0.shape[1] != x.shape[1]:
+        raise N.ValidationError("w0 must be [d_out, d_in]")
+    s = current_stream_handle(x.device) if stream is None else stream
+    N.check(N.lib().plora_sgmv_fused(plan.handle, layer, proj, x.data_ptr(), x.stride(0),
+                                     w0.data_ptr(), w0.stride(0), y.data_ptr(), y.stride(0),
+                                     scale, s))
+    return y
+
+
 def kernel_launch_count() -> int:
     return N.lib().plora_kernel_launch_count()
