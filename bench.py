@@ -44,11 +44,16 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def load_tensor_peak():
+def load_tensor_peak(sustained: bool = False):
+    """Dense bf16 TFLOP/s: the burst figure for a kernel timed alone, the
+    sustained one (4 s back to back, power-capped clocks) for a long step."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
-            return "measured", json.load(f).get("bf16_tflops", 1590.0)
+            d = json.load(f)
+        if sustained and "bf16_tflops_sustained" in d:
+            return "measured sustained", d["bf16_tflops_sustained"]
+        return "measured", d.get("bf16_tflops", 1590.0)
     return "fallback", 1590.0
 
 
@@ -692,6 +697,89 @@ def run_cfg5(args):
     print(json.dumps(line))
 
 
+def run_cfg3f(args):
+    """BASELINE configs[2] with the base projections fused in (SURVEY §8(f)
+    row 3): per (layer, proj) one plora_sgmv_fused call computes
+    y = x·W0ᵀ + scale·(x·Aᵀ)·Bᵀ for 32 segments × 512 tokens, r = 16/64/128,
+    Llama-7B q/v (4096 -> 4096), 32 layers × 2 per step, one CUDA graph.
+    Tensor-bound: the roofline is the measured dense bf16 peak."""
+    import torch
+
+    from paper_2512_20210_b200 import synth
+    from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, kernel_launch_count, sgmv_fused
+
+    dev = torch.device("cuda", 0)
+    cfg = synth.cfg3(page_bytes=args.page_bytes)
+    shape = cfg.shape
+    pool = synth.build_pool(cfg)
+    store = AdapterStore(pool, shape, cfg.n_adapters)
+    for a, r in enumerate(cfg.ranks):
+        store.register(a, r)
+        store.write_pages(a, synth.adapter_image(shape, r, a, device=dev).view(torch.uint8))
+        store.publish(a)
+    ta = synth.segment_assignment(32, 512)
+    T = len(ta)
+    L, NP = shape.n_layers, shape.n_proj
+    plan = BatchPlan(store, ta)
+    g = torch.Generator(device=dev).manual_seed(1234)
+    x = torch.randn(L, T, shape.d_in[0], device=dev, generator=g).to(torch.bfloat16)
+    w0 = [[(torch.randn(shape.d_out[p], shape.d_in[p], device=dev, generator=g) /
+            shape.d_in[p] ** 0.5).to(torch.bfloat16) for p in range(NP)] for _ in range(L)]
+    ys = [torch.empty(L, T, shape.d_out[p], device=dev, dtype=torch.bfloat16) for p in range(NP)]
+
+    def step():
+        for l in range(L):
+            for p in range(NP):
+                sgmv_fused(plan, l, p, x[l], w0[l][p], ys[p][l], 1.0)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    n_g0 = kernel_launch_count()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    per_replay = kernel_launch_count() - n_g0
+    graph.replay()
+    torch.cuda.synchronize()
+    K = args.steps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(K):
+            graph.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    calls = L * NP
+    flops = statistics.mean(2.0 * T * shape.d_in[p] * shape.d_out[p] +
+                            sum(2.0 * 512 * r * (shape.d_in[p] + shape.d_out[p]) for r in cfg.ranks)
+                            for p in range(NP))
+    kind, tpeak = load_tensor_peak(sustained=True)  # a 30 ms step of back-to-back GEMMs
+    call_ms = ms / calls
+    achieved = flops / (call_ms / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": T / (ms / 1e3), "unit": UNIT, "n_gpus": 1, "steps": K,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": ("cfg3 prefill with the base projection fused: y = x·W0ᵀ + "
+                                "(x·Aᵀ)·Bᵀ, 32 segments x 512 tokens, r=[16,64,128][s%3], "
+                                f"Llama-7B q/v 4096->4096, {L} layers x 2 calls per step "
+                                "(shrink + split reduction + fused tcgen05 GEMM per call)"),
+                   "page_bytes": args.page_bytes, "cuda_graph": True,
+                   "l2": "inputs > L2: 4 GiB of x, 2 GiB of base weights per step"},
+        "gpu_launches": per_replay * K,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
+                     "frac": achieved / tpeak, "traffic": None, "peak_kind": kind,
+                     "flops_per_launch": flops, "avg_launch_us": call_ms * 1e3,
+                     "launch_time": "step time / calls per step (each call = 3 launches)"},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -706,8 +794,9 @@ def main():
     ap.add_argument("--per-proj", action="store_true",
                     help="decode: one launch per (layer, proj) instead of one per layer")
     ap.add_argument("--cfg5-layers", type=int, default=80)
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg3f", "cfg4", "cfg5"],
                     help="cfg2 = decode BGMV (headline), cfg3 = prefill SGMV, "
+                         "cfg3f = prefill with the base projection GEMM fused in, "
                          "cfg4 = trace-driven decode with LSTM prefetch, "
                          "cfg5 = tensor-parallel 70B (run under torchrun for N > 1)")
     ap.add_argument("--cfg4-adapters", type=int, default=1000)
@@ -727,6 +816,8 @@ def main():
         run_cfg4(args)
     elif args.workload == "cfg5":
         run_cfg5(args)
+    elif args.workload == "cfg3f":
+        run_cfg3f(args)
     else:
         run_ours(args)
 

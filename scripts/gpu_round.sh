@@ -1,7 +1,7 @@
 #!/usr/bin/env bash
 # One GPU session: tests, smoke, bench, ncu launch list + one full capture.
 # Usage (from this container):  gpurun --timeout 2400 -- 'bash scripts/gpu_round.sh [stages]'
-# stages: any of test,smoke,bench,launches,full (default: all)
+# stages: any of test,smoke,bench,launches,full,cfg3,fullsgmv,fused (default: the first five)
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -44,3 +44,11 @@ if has fullsgmv; then
   echo "fullsgmv rc=$?" >> gpurun_out/ncu_sgmv.log
 fi
 ls -la gpurun_out
+if has fused; then
+  timeout 600 python bench.py --workload cfg3f --steps 5 --warmup 3 > gpurun_out/bench_cfg3f.json 2> gpurun_out/bench_cfg3f.err
+  echo "cfg3f rc=$?" >> gpurun_out/bench_cfg3f.err
+  timeout 300 python scripts/fused_bench.py > gpurun_out/fused_bench.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:sgmv_fused -s 20 -c 1 \
+    -o gpurun_out/fused_full -f python scripts/fused_bench.py > gpurun_out/ncu_fused.log 2>&1
+  echo "fused rc=$?" >> gpurun_out/ncu_fused.log
+fi
