@@ -6,21 +6,21 @@
 // reference bills this as cost_model.prefill_ms (cost_model.hpp:32-34,
 // src/engine.cpp:355).
 //
-// Two kernels per (layer, proj) call, chained by programmatic dependent
-// launch, each with enough CTAs to keep every SM streaming (a 128-token tile
-// is 1 MiB of x and 2 MiB of y read-modify-write; one CTA per tile would be
-// latency-bound on its own serial stream):
+// Three kernels per (layer, proj) call, chained by programmatic dependent
+// launch:
 //
-//  shrink  CTA (tile, k-split): V_part[128 × r16] = X[128, ks] · A[r, ks]ᵀ
-//          over a d_in/KS slice.  Warp 0 TMA-loads x chunks [128 × 64]
-//          (SWIZZLE_128B) into a 4-stage ring; warps 1-3 gather the
-//          adapter's A rows with 16-byte cp.async pieces, each translated
-//          through the device page table, straight into the UMMA K-major
-//          SW128 layout (rank zero-padded to 16 in smem only); warp 4 issues
-//          tcgen05.mma (M = 128, N = r16) into TMEM; warps 4-7 store the fp32
-//          partial.  The last CTA of a tile (arrival counter) sums the KS
-//          partials in split order (deterministic) and writes V in bf16 — the
-//          rounding point between shrink and expand.
+//  shrink  persistent, one CTA per SM: LPT-scheduled work items, each a
+//          unit (one 128-token tile, or two consecutive full tiles of one
+//          run sharing every A chunk) × one K slice.  Warp 0 TMA-loads x
+//          chunks [128 × 64] (SWIZZLE_128B) into a 4-stage ring; warps 1-6
+//          gather the adapter's A rows with 16-byte cp.async pieces, each
+//          translated through the device page table, straight into the UMMA
+//          K-major SW128 layout (rank zero-padded to 16 in smem only); warp 7
+//          issues tcgen05.mma (M = 128, N = r16) into one of two TMEM
+//          accumulator sets; warps 8-11 bulk-copy the fp32 partial out while
+//          the next item streams.
+//  reduce  sums the K-slice partials in split order (deterministic) and
+//          writes V in bf16 — the rounding point between shrink and expand.
 //  expand  CTA (tile, 8 column blocks of 64): D[128 × 64] = V · Bᵀ[:, block]
 //          (tcgen05, K = r16) per block, with the V tile loaded once by TMA,
 //          the Bᵀ blocks gathered from pages (MN-major SW128), two TMEM
