@@ -468,8 +468,8 @@ int plora_predictor_buffer_at(const plora_predictor* p, uint64_t i, uint32_t* ad
  * CTA start / end).  dev_buf = NULL disables tracing. */
 int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
 /* Launch geometry the plan chose for the bf16 decode op of projection
- * `proj`: out[0..7] = {cluster size, input slice, output slice, ring slots,
- * slot bytes, dynamic smem bytes, clusters, chunks}. */
+ * `proj`: out[0..7] = {cluster size, input slice, output slice, A-row ring
+ * slots, Bᵀ-row ring slots, dynamic smem bytes, clusters, chunks}. */
 int plora_debug_plan_geom(const plora_plan* plan, uint32_t proj, uint32_t out[8]);
 /* Timing experiments only (results are wrong while set): the next SGMV
  * shrink launches skip their 1 = weight gathers, 2 = MMAs, 4 = x loads,

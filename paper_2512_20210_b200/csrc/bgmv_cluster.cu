@@ -22,13 +22,15 @@
 // global-memory flags, no atomics; the only cross-CTA traffic is R·T floats
 // per chunk over DSMEM.
 //
-// Pipelining.  One producer warp per CTA issues 1-D TMA bulk copies (one per
-// page piece, L2 evict-first) into a ring of `slots` chunk slots; weights of
-// the next call are issued before griddepcontrol.wait (PDL), activations
-// after it.  Eight consumer warps: warp w dots rank row w of the chunk
-// (shrink) and all 256 threads share the expand columns.  The expand of
-// chunk i-1 runs after the shrink of chunk i, so the DSMEM round trip is
-// hidden behind a chunk of work.
+// Pipelining.  Page-producer warps issue 1-D TMA bulk copies (one per page
+// piece, L2 evict-first) into two rings: the chunk's A rows (read by the
+// shrink) and its Bᵀ rows (read by the expand, after the exchange) live in
+// separate slots, so an A slot is recycled as soon as the shrink is done and
+// a Bᵀ slot is only filled shortly before the expand needs it — each byte of
+// the ring is held for its own consumer's latency, not for the whole
+// shrink → exchange → expand chain.  Weights of the next call are issued
+// before griddepcontrol.wait (PDL), activations after it.  The shrink runs at
+// most kCredit chunks ahead of this CTA's expand (exchange-slot reuse).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -48,11 +50,13 @@ constexpr uint32_t kCWarps = kSWarps + kEWarps;
 constexpr uint32_t kCThreads = kCWarps * 32;
 constexpr uint32_t kPWarps = 4;                // page producer warps (TMA issue is per-lane serial)
 constexpr uint32_t kThreads = kCThreads + (kPWarps + 1) * 32;  // + one control warp
-constexpr uint32_t kX = 16;                    // exchange slots (>= 2 · kMaxSlots, see shrink_group)
+constexpr uint32_t kX = 16;                    // exchange slots (> 2 · kCredit + 1, see shrink_group)
+constexpr uint32_t kCredit = 6;                // shrink may lead this CTA's expand by this many chunks
+constexpr uint32_t kJobBufs = 4;               // x / y row buffers: jobs in flight (a job is often 1-2 chunks)
 constexpr uint32_t kMaxCs = 8;
-constexpr uint32_t kMaxSlots = 8;
+constexpr uint32_t kMaxSlots = 8;  // per ring (A rows / Bᵀ rows)
 constexpr uint32_t kXSlotFloats = kJobTok * kChunkRows * kMaxCs;  // [t][row][src cta]
-constexpr uint32_t kSmemBudget = 200 * 1024;  // 227 KiB (5 slots) measured no faster
+constexpr uint32_t kSmemBudget = 227 * 1024;  // the sm_100 opt-in maximum per CTA
 constexpr uint32_t kMaxSlice = 1024;  // elements per CTA slice (preferred)
 constexpr uint32_t kMaxClusters = 64;  // 148 SMs / clusters of >= 4
 
@@ -71,8 +75,8 @@ struct CArgs {
   uint32_t log2_page;
   uint32_t d_in, d_out;
   uint32_t cs, ks, ns;  // cluster size, slice widths (elements)
-  uint32_t slots, slot_bytes, jb_bytes;
-  uint32_t off_jb, off_xb, off_bar, off_hdr, off_part, off_ring;
+  uint32_t na, nbs, a_bytes, b_bytes, jb_bytes;  // ring depths and slot sizes (A rows, Bᵀ rows)
+  uint32_t off_b, off_jb, off_xb, off_bar, off_hdr, off_part, off_ring;
   uint32_t fast;  // every row slice lies inside one page (see my_piece)
   float scale;
   uint64_t* trace;  // diagnostics (plora_debug_set_trace) or nullptr
@@ -90,21 +94,27 @@ __device__ __forceinline__ void trace_put(const CArgs& p, uint32_t k, int field)
 }
 
 struct Bars {
-  uint64_t* full;    // [kMaxSlots] chunk weights landed
-  uint64_t* empty;   // [kMaxSlots] chunk slot free
-  uint64_t* jfull;   // [2] job x / y rows landed
-  uint64_t* jempty;  // [2] job buffer free
+  uint64_t* afull;   // [kMaxSlots] chunk A rows landed (+ header)
+  uint64_t* aempty;  // [kMaxSlots] A slot free (shrink done)
+  uint64_t* bfull;   // [kMaxSlots] chunk Bᵀ rows landed (+ header)
+  uint64_t* bempty;  // [kMaxSlots] Bᵀ slot free (expand done)
+  uint64_t* jfull;   // [kJobBufs] job x / y rows landed
+  uint64_t* jempty;  // [kJobBufs] job buffer free
   uint64_t* xfull;   // [kX] all CS partials of a chunk landed
   __device__ explicit Bars(char* smem, uint32_t off) {
-    full = reinterpret_cast<uint64_t*>(smem + off);
-    empty = full + kMaxSlots;
-    jfull = empty + kMaxSlots;
-    jempty = jfull + 2;
-    xfull = jempty + 2;
+    afull = reinterpret_cast<uint64_t*>(smem + off);
+    aempty = afull + kMaxSlots;
+    bfull = aempty + kMaxSlots;
+    bempty = bfull + kMaxSlots;
+    jfull = bempty + kMaxSlots;
+    jempty = jfull + kJobBufs;
+    xfull = jempty + kJobBufs;
   }
 };
-constexpr uint32_t kBarBytes = (2 * kMaxSlots + 4 + kX) * 8;
-constexpr uint32_t kHdrBytes = kMaxSlots * sizeof(ClusterChunk);
+constexpr uint32_t kBarBytes = (4 * kMaxSlots + 2 * kJobBufs + kX) * 8;
+// chunk records of the A slots, of the Bᵀ slots, then the expand's progress
+// counter (chunks done, read by the shrink's credit check)
+constexpr uint32_t kHdrBytes = 2 * kMaxSlots * sizeof(ClusterChunk) + 16;
 // The shrink group runs as two independent subgroups of kSubWarps warps on
 // alternating chunks: its per-chunk time is mostly fixed latency, so two
 // chunks in flight nearly double its throughput.
@@ -173,31 +183,29 @@ struct PieceGeom {
   uint32_t KB, NB, KSB, NSB, pprA, pprB;
 };
 
-// Piece q of chunk `c` (A rows first, then Bᵀ rows): logical page, offset in
-// the page, destination in the slot, length (0 = no piece).
+// Piece q of chunk `c`'s A rows (isb = false) or Bᵀ rows (isb = true):
+// logical page, offset in the page, destination in the slot, length (0 = no
+// piece).
 __device__ __forceinline__ uint32_t piece_geom(const CArgs& p, const Slice& sl,
-                                               const PieceGeom& pg, const Rec& c, uint32_t q,
-                                               Piece& out) {
+                                               const PieceGeom& pg, const Rec& c, bool isb,
+                                               uint32_t q, Piece& out) {
   out.len = 0;
-  const uint32_t nA = c.nrows * pg.pprA;
-  if (q >= nA + c.nrows * pg.pprB) return 0;
+  const uint32_t ppr = isb ? pg.pprB : pg.pprA;
+  if (q >= c.nrows * ppr) return 0;
   const uint32_t L = p.log2_page;
   const uint64_t a_base = static_cast<uint64_t>(c.rank) * p.blk_mult[c.proj];  // elements
+  const uint32_t r = q / ppr, k = q - r * ppr;
   uint64_t lo;
-  uint32_t len, dst, k;
-  if (q < nA) {
-    const uint32_t r = q / pg.pprA;
-    k = q - r * pg.pprA;
+  uint32_t len, dst;
+  if (!isb) {
     lo = (a_base + static_cast<uint64_t>(c.row0 + r) * p.d_in + sl.k0) * 2;
     len = pg.KB;
     dst = r * pg.KSB;
   } else {
-    const uint32_t qq = q - nA, r = qq / pg.pprB;
-    k = qq - r * pg.pprB;
     lo = (a_base + static_cast<uint64_t>(c.rank) * p.d_in +
           static_cast<uint64_t>(c.row0 + r) * p.d_out + sl.n0) * 2;
     len = pg.NB;
-    dst = kChunkRows * pg.KSB + r * pg.NSB;
+    dst = r * pg.NSB;
   }
   const uint64_t hi = lo + len, page = (lo >> L) + k;
   const uint64_t a = max(lo, page << L), b = min(hi, (page + 1) << L);
@@ -226,17 +234,18 @@ constexpr int kAhead = 4;
 constexpr uint32_t kRecRing = 2 * kAhead;  // records, 32 bytes each
 constexpr uint32_t kRingBytes = kRecRing * 32 + kAhead * 32 * 4 * 3;  // records | entries | geometry
 
-// This lane's page piece of chunk c.  Aligned fast path (p.fast: every row
-// slice lies inside one page): producer warp pw owns rows 4·(pw&1) .. +3 of
-// the A (pw < 2) or Bᵀ (pw >= 2) block, lanes 0..3 one row each — a shift,
-// no division.  Generic path: pieces [8·pw, 8·pw + 8) of piece_geom's
-// enumeration on lanes 0..7 (the rest go through the small-page loop).
+// This lane's page piece of chunk c.  Producer warps 0-1 stream the A rows,
+// warps 2-3 the Bᵀ rows; the two warps of a ring take alternate chunks.
+// Aligned fast path (p.fast: every row slice lies inside one page): lane r
+// < 8 copies row r — a shift, no division.  Generic path: pieces 0..31 of
+// the role's piece_geom enumeration on the 32 lanes (the rest go through
+// the small-page loop).
 __device__ __forceinline__ uint32_t my_piece(const CArgs& p, const Slice& sl, const PieceGeom& pg,
                                              const Rec& c, uint32_t pw, uint32_t lane, Piece& x) {
   x.len = 0;
   if (p.fast) {
-    const uint32_t r = (pw & 1u) * 4 + lane;
-    if (lane >= 4 || r >= c.nrows) return 0;
+    const uint32_t r = lane;
+    if (r >= c.nrows) return 0;
     const bool isb = pw >= 2;
     const uint64_t lo =
         (isb ? static_cast<uint64_t>(c.rank) * (p.blk_mult[c.proj] + p.d_in) +
@@ -244,18 +253,22 @@ __device__ __forceinline__ uint32_t my_piece(const CArgs& p, const Slice& sl, co
              : static_cast<uint64_t>(c.rank) * p.blk_mult[c.proj] +
                    static_cast<uint64_t>(c.row0 + r) * p.d_in + sl.k0) * 2;
     x.len = isb ? pg.NB : pg.KB;
-    x.dst = isb ? kChunkRows * pg.KSB + r * pg.NSB : r * pg.KSB;
+    x.dst = isb ? r * pg.NSB : r * pg.KSB;
     x.inpage = static_cast<uint32_t>(lo & ((1ull << p.log2_page) - 1));
     return static_cast<uint32_t>(lo >> p.log2_page);
   }
-  if (lane >= 8) return 0;
-  return piece_geom(p, sl, pg, c, pw * 8 + lane, x);
+  return piece_geom(p, sl, pg, c, pw >= 2, lane, x);
 }
 
-// Page warp pw of kPWarps: waits for the slot, issues its share of the
-// chunk's page pieces (my_piece) and arms the chunk barrier with exactly its
-// own bytes (arrive.expect_tx after the copies: the phase cannot complete
-// before this warp's arrival, so the order is safe).
+// Page warp pw of kPWarps (0-1: A ring, 2-3: Bᵀ ring) owns the chunks
+// idx ≡ pw (mod 2) of its ring: waits for the chunk's slot, issues all of the
+// chunk's page pieces of its ring (my_piece), publishes the chunk record in
+// the slot header and arms the slot barrier with the chunk's bytes
+// (arrive.expect_tx after the copies: the phase cannot complete before this
+// arrival, so the order is safe).  Alternating chunks halve each warp's
+// per-chunk issue and lookahead cost (the bulk copies of a warp issue
+// serially).  Both ring depths are even, so a slot's previous chunk was this
+// warp's own and its parity waits never run a lap ahead.
 __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl, uint32_t pw) {
   const uint32_t lane = threadIdx.x & 31;
   Bars bar(smem, p.off_bar);
@@ -274,12 +287,13 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
   pg.pprA = pg.KB ? ((pg.KB - 1) >> L) + 2 : 0;  // page pieces per row (upper bound)
   pg.pprB = pg.NB ? ((pg.NB - 1) >> L) + 2 : 0;
   const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
-  const uint32_t n = i1 - i0;
-  auto fetch_rec = [&](uint32_t j) {  // 32-byte record of chunk j: lanes 0, 1 copy 16 bytes each
+  const uint32_t w2 = pw & 1u;
+  const uint32_t n = (i1 - i0 + 1 - w2) / 2;  // this warp's chunks: idx = 2j + w2
+  auto fetch_rec = [&](uint32_t j) {  // 32-byte record of local chunk j: lanes 0, 1 copy 16 bytes each
     if (lane < 2 && j < n)
-      ptx::cp_async_16(recring + (j % kRecRing) * 8 + lane * 4, recg + (i0 + j) * 8 + lane * 4, 16);
+      ptx::cp_async_16(recring + (j % kRecRing) * 8 + lane * 4, recg + (i0 + 2 * j + w2) * 8 + lane * 4, 16);
   };
-  auto fetch_tbl = [&](uint32_t j) {  // page-table entry of this lane's piece of chunk j
+  auto fetch_tbl = [&](uint32_t j) {  // page-table entry of this lane's piece of local chunk j
     if (j >= n) return;
     const Rec c(recring + (j % kRecRing) * 8);
     Piece x{};
@@ -299,65 +313,80 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
     ptx::cp_async_commit();
   }
 #pragma unroll 1
-  for (uint32_t idx = 0; idx < n; ++idx) {
-    const uint32_t s = idx % p.slots, ph = (idx / p.slots) & 1u;
-    cp_async_wait_group<kAhead - 1>();  // table entries of idx, record of idx + kAhead
+  const bool isb = pw >= 2;
+  const uint32_t nslots = isb ? p.nbs : p.na;
+  uint64_t* fullb = isb ? bar.bfull : bar.afull;
+  uint64_t* emptyb = isb ? bar.bempty : bar.aempty;
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(smem + p.off_hdr) + (isb ? kMaxSlots * 8 : 0);
+  uint32_t s = w2, ph = 0;  // slot, its phase parity (no division per chunk)
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint32_t idx = 2 * j + w2;
+    cp_async_wait_group<kAhead - 1>();  // table entries of j, record of j + kAhead
     __syncwarp();
     if (pw == 0 && lane == 0) trace_put(p, idx, 6);
-    const Rec c(recring + (idx % kRecRing) * 8);
-    char* sb = smem + s * p.slot_bytes;
-    const uint2 geo = georing[(idx % kAhead) * 32 + lane];
+    const uint32_t* rw = recring + (j % kRecRing) * 8;
+    const Rec c(rw);
+    char* sb = smem + (isb ? p.off_b + s * p.b_bytes : s * p.a_bytes);
+    const uint2 geo = georing[(j % kAhead) * 32 + lane];
     Piece pc;
     pc.inpage = geo.x;
     pc.dst = geo.y & 0xffffu;
     pc.len = geo.y >> 16;
-    const uint32_t phys = pc.len ? tblring[(idx % kAhead) * 32 + lane] : 0u;
+    const uint32_t phys = pc.len ? tblring[(j % kAhead) * 32 + lane] : 0u;
     if (pw == 0 && lane == 0) trace_put(p, idx, 4);
-    ptx::mbar_wait(&bar.empty[s], ph ^ 1u);
+    ptx::mbar_wait(&emptyb[s], ph ^ 1u);
     if (pw == 0 && lane == 0) trace_put(p, idx, 5);
     uint32_t bytes = pc.len;
     if (pc.len)
       ptx::bulk_g2s_hint(sb + pc.dst, p.arena + (static_cast<uint64_t>(phys) << L) + pc.inpage,
-                         pc.len, &bar.full[s], ef);
-    if (!p.fast) {  // small pages: the pieces past the first 32, synchronous lookups
-      for (uint32_t q = 32 + pw * 32 + lane; q < c.nrows * (pg.pprA + pg.pprB); q += 32 * kPWarps) {
+                         pc.len, &fullb[s], ef);
+    if (!p.fast) {  // small pages: the role's pieces past the first 32, synchronous lookups
+      for (uint32_t q = 32 + lane; q < c.nrows * (isb ? pg.pprB : pg.pprA); q += 32) {
         Piece x;
-        const uint32_t page = piece_geom(p, sl, pg, c, q, x);
+        const uint32_t page = piece_geom(p, sl, pg, c, isb, q, x);
         if (x.len) {
           ptx::bulk_g2s_hint(sb + x.dst,
                              p.arena + (static_cast<uint64_t>(__ldg(p.table + c.table_off + page)) << L) +
                                  x.inpage,
-                             x.len, &bar.full[s], ef);
+                             x.len, &fullb[s], ef);
           bytes += x.len;
         }
       }
     }
     if (pw == 0 && lane == 0) trace_put(p, idx, 12);
-    if (p.fast) {  // this warp's rows of the chunk × their slice bytes, no reduction needed
-      const uint32_t half = kChunkRows / 2, r0 = (pw & 1u) * half;
-      const uint32_t mine = c.nrows > r0 ? min(c.nrows - r0, half) : 0u;
-      bytes = mine * (pw >= 2 ? pg.NB : pg.KB);
+    if (p.fast) {  // the chunk's rows × their slice bytes, no reduction needed
+      bytes = c.nrows * (isb ? pg.NB : pg.KB);
     } else {
       bytes = __reduce_add_sync(0xffffffffu, bytes);
     }
-    if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.full[s], bytes);
-    // ---- lookahead: table entries of idx + kAhead (its record landed), record of
-    // idx + 2·kAhead into the ring slot idx just vacated
-    fetch_tbl(idx + kAhead);
-    fetch_rec(idx + kRecRing);
+    if (lane == 0) {  // publish the record in the slot header, released by the arrival
+      const uint4* src = reinterpret_cast<const uint4*>(rw);
+      uint4* dst = reinterpret_cast<uint4*>(hdr + s * 8);
+      dst[0] = src[0];
+      dst[1] = src[1];
+      ptx::mbar_arrive_expect_tx(&fullb[s], bytes);
+    }
+    __syncwarp();  // the record ring slot is refilled below
+    s += 2;
+    if (s >= nslots) {
+      s -= nslots;
+      ph ^= 1u;
+    }
+    // ---- lookahead: table entries of j + kAhead (its record landed), record of
+    // j + 2·kAhead into the ring slot j just vacated
+    fetch_tbl(j + kAhead);
+    fetch_rec(j + kRecRing);
     ptx::cp_async_commit();
   }
   cp_async_wait_group<0>();
 }
 
-// Control warp: publishes each chunk's record in the slot header (its arrival
-// on the chunk barrier releases it to the consumers) and, at a job's first
-// chunk, loads the job's x / y slices — after griddepcontrol.wait, since the
-// activations are written by earlier kernels in the stream.
+// Control warp: at a job's first chunk, loads the job's x / y slices into a
+// job buffer — after griddepcontrol.wait, since the activations are written
+// by earlier kernels in the stream.
 __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uint32_t cl) {
   const uint32_t lane = threadIdx.x & 31;
   Bars bar(smem, p.off_bar);
-  uint32_t* hdr = reinterpret_cast<uint32_t*>(smem + p.off_hdr);
   uint32_t* recring = reinterpret_cast<uint32_t*>(smem + p.off_ring + kPWarps * kRingBytes);
   const uint32_t* recg = reinterpret_cast<const uint32_t*>(p.chunks);
   const Slice sl(p, crank);
@@ -376,22 +405,12 @@ __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uin
   bool waited = false;
 #pragma unroll 1
   for (uint32_t idx = 0; idx < n; ++idx) {
-    const uint32_t s = idx % p.slots, ph = (idx / p.slots) & 1u;
     cp_async_wait_group<kAhead - 1>();
     __syncwarp();
     const uint32_t* rw = recring + (idx % kRecRing) * 8;
     const Rec c(rw);
-    ptx::mbar_wait(&bar.empty[s], ph ^ 1u);
-    if (lane == 0) {  // one thread writes the header and releases it with its arrival
-      const uint4* src = reinterpret_cast<const uint4*>(rw);
-      uint4* dst = reinterpret_cast<uint4*>(hdr + s * 8);
-      dst[0] = src[0];
-      dst[1] = src[1];
-      ptx::mbar_arrive(&bar.full[s]);
-      trace_put(p, idx, 13);
-    }
     if (c.flags & kChunkFirst) {  // the job's x / y slices
-      const uint32_t jbuf = jord & 1u, jph = (jord >> 1) & 1u;
+      const uint32_t jbuf = jord % kJobBufs, jph = (jord / kJobBufs) & 1u;
       ++jord;
       char* jb = smem + p.off_jb + jbuf * p.jb_bytes;
       const uint32_t tokx = rw[4 + (lane & 3)];
@@ -445,7 +464,9 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   const bool half_tail = (sl.kb & 15u) != 0;
   const uint32_t xb0 = ptx::smem_u32(smem + p.off_xb);
   float* part = reinterpret_cast<float*>(smem + p.off_part);  // [2][warp][tok][row]
-  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(smem + p.off_hdr);
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(smem + p.off_hdr);  // A-slot records
+  const volatile uint32_t* edone =
+      reinterpret_cast<const volatile uint32_t*>(smem + p.off_hdr + 2 * kMaxSlots * sizeof(ClusterChunk));
   const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
   // ldmatrix lane addressing: A (x rows) = row (lane&7) + 8·((lane>>3)&1), k-half lane>>4
   // (rows >= kJobTok alias row 0: their D rows are discarded); B (W rows, x4 =
@@ -457,9 +478,11 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   const bool lead = sw == 0 && lane == 0;
 #pragma unroll 1
   for (uint32_t i = i0 + sg; i < i1; i += kSubgroups) {  // this subgroup's chunks
-    const uint32_t idx = i - i0, s = idx % p.slots, e = idx % kX;
+    // (p.na is even: a subgroup's previous chunk in slot s is idx - na, which
+    // it consumed itself, so its parity wait is never a ring lap ahead)
+    const uint32_t idx = i - i0, s = idx % p.na, e = idx % kX;
     if (lead) trace_put(p, idx, 14);
-    ptx::mbar_wait(&bar.full[s], (idx / p.slots) & 1u);
+    ptx::mbar_wait(&bar.afull[s], (idx / p.na) & 1u);
     if (lead) trace_put(p, idx, 0);
     const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
     const uint32_t ntok = ch->ntok, jord = ch->jord;
@@ -467,17 +490,22 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     // chunk can run before (or beside) its first one.  The job buffer cannot be
     // recycled meanwhile (that needs the job's last expand), so the parity is
     // unambiguous.
-    ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);
-    // Arm this chunk's exchange barrier: CS CTAs × kChunkRows rows × ntok
-    // floats.  Peers' st.async may land before this (negative tx count is
-    // fine: the phase also needs this arrival).  Aliasing bound: a peer's
-    // shrink of chunk m needs its slot back, i.e. its expand of m - slots,
-    // i.e. our partial of m - slots, i.e. our slot of that chunk, i.e. our
-    // expand of m - 2·slots: kX >= 2·kMaxSlots keeps every live phase distinct.
-    if (lead) ptx::mbar_arrive_expect_tx(&bar.xfull[e], p.cs * kChunkRows * ntok * 4);
+    ptx::mbar_wait(&bar.jfull[jord % kJobBufs], (jord / kJobBufs) & 1u);
+    // Credit: start chunk idx only once this CTA's expand has finished chunk
+    // idx - kCredit.  Then arm this chunk's exchange barrier: CS CTAs ×
+    // kChunkRows rows × ntok floats.  Peers' st.async may land before this
+    // (negative tx count is fine: the phase also needs this arrival).
+    // Aliasing bound: a peer's shrink of chunk m + kX needs its expand past
+    // m + kX - kCredit, i.e. our partial of that chunk, i.e. our expand past
+    // m + kX - 2·kCredit - 1 > m: kX > 2·kCredit + 1 keeps every live phase of
+    // an exchange slot distinct.
+    if (lead) {
+      while (idx >= *edone + kCredit) __nanosleep(32);
+      ptx::mbar_arrive_expect_tx(&bar.xfull[e], p.cs * kChunkRows * ntok * 4);
+    }
     if (lead) trace_put(p, idx, 15);
-    const uint32_t xa = ptx::smem_u32(smem + p.off_jb + (jord & 1u) * p.jb_bytes) + xoff;
-    const uint32_t wa = ptx::smem_u32(smem + s * p.slot_bytes) + woff;
+    const uint32_t xa = ptx::smem_u32(smem + p.off_jb + (jord % kJobBufs) * p.jb_bytes) + xoff;
+    const uint32_t wa = ptx::smem_u32(smem + s * p.a_bytes) + woff;
     // Warp sw takes k-step pairs sw, sw + kSubWarps, ... (<= kPairs of them).  The
     // schedule is software-pipelined by hand — pair j+1's fragment loads are
     // issued before pair j's MMAs, into the other of two register sets (the
@@ -555,7 +583,7 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
       }
       if (lane == 0) {
         trace_put(p, idx, 1);
-        ptx::mbar_arrive(&bar.empty[s]);  // shrink side of the slot is free
+        ptx::mbar_arrive(&bar.aempty[s]);  // A slot free
       }
     }
   }
@@ -567,7 +595,10 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   const Bars bar(smem, p.off_bar);
   const Slice sl(p, crank);
   const uint32_t NSB = row_stride(p.ns), KSB = row_stride(p.ks);
-  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(smem + p.off_hdr);
+  const uint32_t* hdr =
+      reinterpret_cast<const uint32_t*>(smem + p.off_hdr) + kMaxSlots * 8;  // Bᵀ-slot records
+  volatile uint32_t* edone =
+      reinterpret_cast<volatile uint32_t*>(smem + p.off_hdr + 2 * kMaxSlots * sizeof(ClusterChunk));
   const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
   // this warp's 16-column tiles [t0, t1) of the output slice
   const uint32_t ntiles = sl.nb / 16, tpw = (ntiles + kEWarps - 1) / kEWarps;
@@ -577,12 +608,12 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   float acc[kMaxTiles + 1][4];
 #pragma unroll 1
   for (uint32_t i = i0; i < i1; ++i) {
-    const uint32_t idx = i - i0, s = idx % p.slots, e = idx % kX;
-    ptx::mbar_wait(&bar.full[s], (idx / p.slots) & 1u);
+    const uint32_t idx = i - i0, s = idx % p.nbs, e = idx % kX;
+    ptx::mbar_wait(&bar.bfull[s], (idx / p.nbs) & 1u);
     const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
     const uint32_t ntok = ch->ntok, nrows = ch->nrows, flags = ch->flags, jord = ch->jord;
     if (flags & kChunkFirst) {
-      ptx::mbar_wait(&bar.jfull[jord & 1u], (jord >> 1) & 1u);  // y rows of the job
+      ptx::mbar_wait(&bar.jfull[jord % kJobBufs], (jord / kJobBufs) & 1u);  // y rows of the job
 #pragma unroll
       for (uint32_t t = 0; t <= kMaxTiles; ++t)
 #pragma unroll
@@ -619,7 +650,7 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     // Bᵀ rows >= nrows of the slot are stale: mask their halves of the A fragment
     const uint32_t amask =
         (2 * cc < nrows ? 0x0000ffffu : 0u) | (2 * cc + 1 < nrows ? 0xffff0000u : 0u);
-    const char* brow = smem + s * p.slot_bytes + kChunkRows * KSB;
+    const char* brow = smem + p.off_b + s * p.b_bytes;
     // ldmatrix.trans lane addressing: row (lane&7) of matrix lane>>3 = 8 columns
     const uint32_t brow0 = ptx::smem_u32(brow + (lane & 7) * NSB);
     const uint32_t baddr = brow0 + (lane >> 3) * 16;
@@ -645,7 +676,7 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     }
     if (tid == 0) trace_put(p, idx, 11);
     if ((flags & kChunkLast) && cc < ntok) {  // y[tok cc] += scale · (hi + lo), once per job
-      const char* yrow = smem + p.off_jb + (jord & 1u) * p.jb_bytes + kJobTok * KSB + cc * NSB;
+      const char* yrow = smem + p.off_jb + (jord % kJobBufs) * p.jb_bytes + kJobTok * KSB + cc * NSB;
       char* yg = p.y[ch->proj] + ch->tok[cc] * p.y_stride_b[ch->proj] + static_cast<uint64_t>(sl.n0) * 2;
       auto put = [&](uint32_t col, float v) {
         const float o = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(yrow + col * 2));
@@ -663,8 +694,10 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     ptx::named_bar_sync(1, kEThreads);  // slot (and job buffer) reads done
     if (tid == 0) {
       trace_put(p, idx, 3);
-      ptx::mbar_arrive(&bar.empty[s]);
-      if (flags & kChunkLast) ptx::mbar_arrive(&bar.jempty[jord & 1u]);
+      ptx::mbar_arrive(&bar.bempty[s]);
+      if (flags & kChunkLast) ptx::mbar_arrive(&bar.jempty[jord % kJobBufs]);
+      __threadfence_block();
+      *edone = idx + 1;  // credit for the shrink (its exchange slot is read)
     }
   }
 }
@@ -678,10 +711,13 @@ __global__ void __launch_bounds__(kThreads, 1) bgmv_cluster_kernel(const CArgs p
   if (threadIdx.x == 0) {
     Bars bar(smem, p.off_bar);
     for (uint32_t s = 0; s < kMaxSlots; ++s) {
-      ptx::mbar_init(&bar.full[s], kPWarps + 1);  // page warps + control warp
-      ptx::mbar_init(&bar.empty[s], 2);  // shrink group + expand group
+      ptx::mbar_init(&bar.afull[s], 1);   // the A page warp of the chunk
+      ptx::mbar_init(&bar.aempty[s], 1);  // the shrink subgroup of the chunk
+      ptx::mbar_init(&bar.bfull[s], 1);   // the Bᵀ page warp of the chunk
+      ptx::mbar_init(&bar.bempty[s], 1);           // the expand group
     }
-    for (int j = 0; j < 2; ++j) {
+    *reinterpret_cast<uint32_t*>(smem + p.off_hdr + 2 * kMaxSlots * sizeof(ClusterChunk)) = 0u;
+    for (uint32_t j = 0; j < kJobBufs; ++j) {
       ptx::mbar_init(&bar.jfull[j], 1);
       ptx::mbar_init(&bar.jempty[j], 1);
     }
@@ -745,14 +781,18 @@ ClusterGeom cluster_geom(uint32_t d_in, uint32_t d_out, int device) {
                           std::to_string(d_out) + " too wide (max " +
                           std::to_string(kMaxSlice * kMaxCs) + ")");
   auto up128 = [](uint32_t b) { return (b + 127) / 128 * 128; };
-  g.slot_bytes = up128(kChunkRows * (row_stride(g.ks) + row_stride(g.ns)));
+  g.a_bytes = up128(kChunkRows * row_stride(g.ks));
+  g.b_bytes = up128(kChunkRows * row_stride(g.ns));
   g.jb_bytes = up128(kJobTok * (row_stride(g.ks) + row_stride(g.ns)));
-  const uint32_t fixed = 2 * g.jb_bytes + kX * kXSlotFloats * 4 + kBarBytes + kHdrBytes + kPartBytes + (kPWarps + 1) * kRingBytes;
-  g.slots = fixed < kSmemBudget ? std::min<uint32_t>(kMaxSlots, (kSmemBudget - fixed) / g.slot_bytes) : 0;
-  if (g.slots < 3)
+  const uint32_t fixed = kJobBufs * g.jb_bytes + kX * kXSlotFloats * 4 + kBarBytes + kHdrBytes + kPartBytes + (kPWarps + 1) * kRingBytes;
+  // equal ring depths, the A ring even (two shrink subgroups alternate chunks)
+  const uint32_t pairs = fixed < kSmemBudget ? (kSmemBudget - fixed) / (g.a_bytes + g.b_bytes) : 0;
+  g.na = std::min<uint32_t>(kMaxSlots, pairs) & ~1u;
+  g.nbs = std::min<uint32_t>(kMaxSlots, pairs) & ~1u;  // even: the page warps alternate chunks
+  if (g.na < 2 || g.nbs < 2)
     throw ValidationError("bf16 BGMV: d_in " + std::to_string(d_in) + " / d_out " +
-                          std::to_string(d_out) + " leave fewer than 3 ring slots");
-  g.smem = g.slots * g.slot_bytes + fixed;
+                          std::to_string(d_out) + " leave fewer than 2 ring slots");
+  g.smem = g.na * g.a_bytes + g.nbs * g.b_bytes + fixed;
   g.n_clusters = std::min<uint32_t>(kMaxClusters, static_cast<uint32_t>(max_clusters(device, g.cs, g.smem)));
   return g;
 }
@@ -780,11 +820,14 @@ void launch(const plora_plan& plan, const ClusterWork& cw, uint32_t layer, const
   a.cs = g.cs;
   a.ks = g.ks;
   a.ns = g.ns;
-  a.slots = g.slots;
-  a.slot_bytes = g.slot_bytes;
+  a.na = g.na;
+  a.nbs = g.nbs;
+  a.a_bytes = g.a_bytes;
+  a.b_bytes = g.b_bytes;
   a.jb_bytes = g.jb_bytes;
-  a.off_jb = g.slots * g.slot_bytes;
-  a.off_xb = a.off_jb + 2 * g.jb_bytes;
+  a.off_b = g.na * g.a_bytes;
+  a.off_jb = a.off_b + g.nbs * g.b_bytes;
+  a.off_xb = a.off_jb + kJobBufs * g.jb_bytes;
   a.off_bar = a.off_xb + kX * kXSlotFloats * 4;
   a.off_hdr = a.off_bar + kBarBytes;
   a.off_part = a.off_hdr + kHdrBytes;
@@ -862,7 +905,7 @@ extern "C" int plora_debug_plan_geom(const plora_plan* plan, uint32_t proj, uint
     const ClusterWork& cw = plan->cwork[proj];
     const ClusterGeom& g = cw.geom;
     const uint32_t n = g.n_clusters ? plan->ccl_off[cw.cl_off + g.n_clusters] : 0;
-    const uint32_t v[8] = {g.cs, g.ks, g.ns, g.slots, g.slot_bytes, g.smem, g.n_clusters, n};
+    const uint32_t v[8] = {g.cs, g.ks, g.ns, g.na, g.nbs, g.smem, g.n_clusters, n};
     for (int i = 0; i < 8; ++i) out[i] = v[i];
     return 0;
   });

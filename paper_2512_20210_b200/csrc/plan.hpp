@@ -120,8 +120,9 @@ static_assert(sizeof(ClusterChunk) == 32, "ClusterChunk layout");
 struct ClusterGeom {
   uint32_t cs = 0;          // CTAs per cluster
   uint32_t ks = 0, ns = 0;  // input / output slice widths (elements)
-  uint32_t slots = 0;       // ring depth
-  uint32_t slot_bytes = 0, jb_bytes = 0, smem = 0;
+  uint32_t na = 0, nbs = 0;         // ring depths: A-row slots, Bᵀ-row slots
+  uint32_t a_bytes = 0, b_bytes = 0;  // slot sizes
+  uint32_t jb_bytes = 0, smem = 0;
   uint32_t n_clusters = 0;  // clusters launched (<= co-resident clusters)
 };
 ClusterGeom cluster_geom(uint32_t d_in, uint32_t d_out, int device);

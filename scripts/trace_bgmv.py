@@ -43,7 +43,7 @@ def main():
     fused = "--layer" in sys.argv  # q and v in one launch (plora_bgmv_layer)
     geom = (C.c_uint32 * 8)()
     N.check(N.lib().plora_debug_plan_geom(plan.handle, 0, geom))
-    names = ("cs", "ks", "ns", "slots", "slot_bytes", "smem", "clusters", "chunks")
+    names = ("cs", "ks", "ns", "a_slots", "b_slots", "smem", "clusters", "chunks")
     print("geometry:", dict(zip(names, list(geom))))
     x = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
     y = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
