@@ -358,15 +358,8 @@ __global__ void __launch_bounds__(kThreads) bgmv_expand_kernel(const BgmvArgs p)
 template <typename T>
 void launch(const BgmvArgs& a, const ProjWork& pw, const BgmvUnit* d_units, uint32_t shrink_smem,
             cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    PLORA_CUDA(cudaFuncSetAttribute(bgmv_shrink_kernel<T>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    PLORA_CUDA(cudaFuncSetAttribute(bgmv_expand_kernel<T>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(ExpandSmem::total)));
-    attr = true;
-  }
+  set_smem_once(reinterpret_cast<const void*>(bgmv_shrink_kernel<T>), 200 * 1024);
+  set_smem_once(reinterpret_cast<const void*>(bgmv_expand_kernel<T>), static_cast<int>(ExpandSmem::total));
   BgmvArgs sa = a;
   sa.units = d_units;
   if (pw.n_shrink) {

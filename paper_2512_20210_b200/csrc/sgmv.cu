@@ -636,12 +636,7 @@ void sgmv_shrink_reduce(plora_plan* plan, uint32_t layer, uint32_t proj, const v
   const SgmvSched& sc = plan->ssched[proj];
   CUtensorMap tmap_x;
   make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kChunkK, kTileM);
-  static bool attr = false;
-  if (!attr) {
-    PLORA_CUDA(cudaFuncSetAttribute(sgmv_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(SSmem::alloc)));
-    attr = true;
-  }
+  set_smem_once(reinterpret_cast<const void*>(sgmv_shrink_kernel), static_cast<int>(SSmem::alloc));
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
@@ -702,12 +697,7 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     make_tmap_2d(&tmap_y, y, dout, plan->n_tokens, y_stride * 2, 64, kTileM);
     make_tmap_2d(&tmap_v, plan->d_vbuf, kMaxRank, static_cast<uint64_t>(plan->n_tiles) * kTileM,
                  kMaxRank * 2, 64, kTileM);
-    static bool attr = false;
-    if (!attr) {
-      PLORA_CUDA(cudaFuncSetAttribute(sgmv_expand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(ESmem::alloc)));
-      attr = true;
-    }
+    set_smem_once(reinterpret_cast<const void*>(sgmv_expand_kernel), static_cast<int>(ESmem::alloc));
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;

@@ -345,12 +345,7 @@ extern "C" int plora_sgmv_fused(plora_plan* plan, uint32_t layer, uint32_t proj,
     make_tmap_2d(&tmap_v, plan->n_tiles ? plan->d_vbuf : x, kMaxRank,
                  std::max<uint64_t>(plan->n_tiles, 1) * kBM, kMaxRank * 2, kBK, kBM);
     make_tmap_2d(&tmap_y, y, dout, plan->n_tokens, y_stride * 2, 64, kBM);
-    static bool attr = false;
-    if (!attr) {
-      PLORA_CUDA(cudaFuncSetAttribute(sgmv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(FSmem::alloc)));
-      attr = true;
-    }
+    set_smem_once(reinterpret_cast<const void*>(sgmv_fused_kernel), static_cast<int>(FSmem::alloc));
     FArgs a{};
     a.arena = st.arena;
     a.table = st.d_table;

@@ -7,6 +7,8 @@
 // 250-288) and makes them usable at promotion (src/engine.cpp:406-414).
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <set>
 
 #include "store.hpp"
 
@@ -397,3 +399,18 @@ int plora_store_apply_relocations(plora_store* s, const plora_reloc* relocs, uin
 }
 
 }  // extern "C"
+
+namespace plora {
+
+void set_smem_once(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  int dev = 0;
+  PLORA_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, kernel})) return;
+  PLORA_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.insert({dev, kernel});
+}
+
+}  // namespace plora

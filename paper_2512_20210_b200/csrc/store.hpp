@@ -26,6 +26,11 @@ namespace plora {
       throw ::plora::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e));   \
   } while (0)
 
+// Opt a kernel into `bytes` of dynamic shared memory, once per (device,
+// kernel): the attribute belongs to the device's context, and several host
+// threads (the engine's pump, callers) may launch.
+void set_smem_once(const void* kernel, int bytes);
+
 // Directory entry for one adapter key, read by every kernel.  16 bytes.
 struct DevAdapter {
   uint32_t rank;
