@@ -202,7 +202,7 @@ def run_ours(args):
 
     from paper_2512_20210_b200 import synth
     from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, bgmv, bgmv_layer,
-                                            kernel_launch_count, sgmv)
+                                            kernel_launch_count, sgmv, sgmv_layer)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -236,17 +236,18 @@ def run_ours(args):
     y = torch.randn(L * NP, T, 4096, device=dev).to(torch.bfloat16)
     stream = torch.cuda.current_stream()
 
-    # decode: both projections of a layer (they read the same x) in one
-    # launch unless --per-proj; prefill: one launch pair per (layer, proj)
-    fused = not prefill and not args.per_proj
-    LPS = NP if not fused else 1  # launches per layer
+    # both projections of a layer (they read the same x) in one call unless
+    # --per-proj: decode one launch, prefill one shrink + reduction + expand
+    fused = not args.per_proj
+    LPS = NP if not fused else 1  # calls per layer
+    layer_op = sgmv_layer if prefill else bgmv_layer
 
     def step(ev=None):
         for l in range(L):
             if fused:
                 if ev is not None:
                     ev[2 * l].record()
-                bgmv_layer(plan, l, x[l], [y[l * NP + p] for p in range(NP)])
+                layer_op(plan, l, x[l], [y[l * NP + p] for p in range(NP)])
                 if ev is not None:
                     ev[2 * l + 1].record()
                 continue
@@ -397,8 +398,9 @@ def run_ours(args):
             (NP - 1) * T * shape.d_in[0] * shape.esize
     if prefill:  # every adapter serves one 512-token segment; weights read once per tile
         toks = cfg.tokens_per_adapter
-        flops = statistics.mean(sum(2 * toks * r * (shape.d_in[p] + shape.d_out[p])
-                                    for r in cfg.ranks) for p in range(NP))
+        per_proj_flops = [sum(2 * toks * r * (shape.d_in[p] + shape.d_out[p]) for r in cfg.ranks)
+                          for p in range(NP)]
+        flops = sum(per_proj_flops) if fused else statistics.mean(per_proj_flops)
     peak, peak_kind = load_peaks()
     # average launch duration over the timed region: the step is the L·NP
     # launches back to back (overlapping through PDL), nothing else
@@ -428,10 +430,12 @@ def run_ours(args):
         "warmup": max(args.warmup, 3), "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": ("cfg3 prefill SGMV (tcgen05): 32 segments x 512 tokens per GPU, "
-                                "r=[16,64,128][s%3], Llama-7B q/v (32 layers x 2 = 64 calls/step)")
+                                "r=[16,64,128][s%3], Llama-7B q/v (32 layers x 2 projections "
+                                "per step)")
                                if prefill else
                                ("cfg2 decode BGMV: 256 tokens / 128 adapters per GPU, "
-                                "r=[8,16,32,64][a%4], Llama-7B q/v (32 layers x 2 = 64 calls/step)"),
+                                "r=[8,16,32,64][a%4], Llama-7B q/v (32 layers x 2 projections "
+                                "per step)"),
                    "page_bytes": args.page_bytes, "tokens_per_step_per_gpu": T,
                    "parallelism": f"request-sharded x{world} (no collective)",
                    "cuda_graph": graph is not None,

@@ -290,6 +290,13 @@ int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x
 int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                plora_stream_t stream);
+/* Every projection of `layer` at once, prefill path (as plora_bgmv_layer):
+ * with two projections of equal shape the shrink reads each x chunk once
+ * for both and one expand launch covers both; otherwise one plora_sgmv
+ * call per projection. */
+int plora_sgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x_stride,
+                     void* const* ys, const uint64_t* y_strides, float scale,
+                     plora_stream_t stream);
 /* Prefill with the base projection fused in: for every
  * token row t of the plan (with or without an adapter)
  *   y[t] = x[t] · W0ᵀ + bf16(scale · x[t] · A_{a(t)}ᵀ) · B_{a(t)}ᵀ

@@ -176,87 +176,98 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   sitems.clear();
   scta.clear();
   for (uint32_t p = 0; p < PLORA_MAX_PROJ; ++p) ssched[p] = SgmvSched{};
-  if (es == 2 && n_sunits > 0) {
+  ssched_layer = SgmvSched{};
+  // units: {tile, tile or ~0u} pairs; np projections share each x chunk.
+  // Split-K factor: each candidate's LPT makespan (bytes the busiest CTA
+  // streams, at a per-SM share of HBM) plus the split reduction (partials
+  // written and read back); the cheapest wins.  Few splits for heavy uniform
+  // batches, more for mixed ranks.
+  auto build_sched = [&](const std::vector<uint32_t>& un, uint32_t d_in, uint32_t np) {
     const uint32_t n_sm = std::max(1, st.num_sms);
+    const uint32_t nu = static_cast<uint32_t>(un.size() / 2);
+    std::vector<std::vector<SgmvItem>> per, best_per;
+    uint32_t ks = 0;
+    double best = 0.0;
+    for (uint32_t cand = 1; cand <= 16; cand *= 2) {
+      if ((d_in / 64) % cand != 0 || (cand > 1 && d_in / cand < 256)) break;
+      const uint32_t kslice = d_in / cand;
+      std::vector<std::pair<uint64_t, SgmvItem>> items;  // (cost, item)
+      items.reserve(static_cast<size_t>(nu) * cand);
+      uint64_t part_bytes = 0;
+      for (uint32_t u = 0; u < nu; ++u) {
+        const uint64_t nt = un[2 * u + 1] != 0xffffffffu ? 2 : 1;
+        const SgmvTile& ta = tiles[un[2 * u]];
+        const uint64_t r16 = (ta.rank + 15) / 16 * 16;
+        // bytes streamed (x tiles + paged weights) plus the partial write-back
+        const uint64_t cost = 2ull * kslice * (nt * 128 + np * r16) + 4ull * nt * np * 128 * r16;
+        part_bytes += 8ull * nt * np * 128 * r16 * cand;
+        for (uint32_t sp = 0; sp < cand; ++sp) {
+          SgmvItem it{};
+          it.tile_a = un[2 * u];
+          it.tile_b = un[2 * u + 1];
+          it.row0_a = ta.row0;
+          it.row0_b = nt == 2 ? tiles[it.tile_b].row0 : 0;
+          it.table_off = ta.table_off;
+          it.rank = ta.rank;
+          it.split = sp;
+          items.emplace_back(cost, it);
+        }
+      }
+      std::stable_sort(items.begin(), items.end(),
+                       [](const auto& x, const auto& y) { return x.first > y.first; });
+      const uint32_t ctas = std::min<uint32_t>(n_sm, static_cast<uint32_t>(items.size()));
+      per.assign(ctas, {});
+      using Load = std::pair<uint64_t, uint32_t>;
+      std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+      for (uint32_t c = 0; c < ctas; ++c) heap.emplace(0, c);
+      uint64_t makespan = 0;
+      for (const auto& it : items) {
+        Load l = heap.top();
+        heap.pop();
+        per[l.second].push_back(it.second);
+        heap.emplace(l.first + it.first, l.second);
+        makespan = std::max(makespan, l.first + it.first);
+      }
+      constexpr double kSmBw = 45e9, kHbmBw = 5e12;
+      const double t = makespan / kSmBw + part_bytes / kHbmBw;
+      if (ks == 0 || t < best) {
+        ks = cand;
+        best = t;
+        best_per.swap(per);
+      }
+    }
+    SgmvSched sc;
+    sc.splits = ks;
+    sc.ctas = static_cast<uint32_t>(best_per.size());
+    sc.item_off = static_cast<uint32_t>(sitems.size());
+    sc.cta_off = static_cast<uint32_t>(scta.size());
+    uint32_t n = 0;
+    for (uint32_t c = 0; c < sc.ctas; ++c) {
+      scta.push_back(n);
+      for (const SgmvItem& v : best_per[c]) sitems.push_back(v);
+      n += static_cast<uint32_t>(best_per[c].size());
+    }
+    scta.push_back(n);
+    return sc;
+  };
+  if (es == 2 && n_sunits > 0) {
     for (uint32_t p = 0; p < g.m.n_proj; ++p) {
       uint32_t same = p;
       for (uint32_t q = 0; q < p; ++q)
         if (g.m.d_in[q] == g.m.d_in[p]) same = q;
-      if (same != p) {
-        ssched[p] = ssched[same];
-        continue;
+      ssched[p] = same != p ? ssched[same] : build_sched(sunits, g.m.d_in[p], 1);
+    }
+    // every projection of a layer from one x chunk (plora_sgmv_layer): single
+    // tiles, since a unit holds at most two accumulators
+    bool shared_x = g.m.n_proj == 2;
+    for (uint32_t p = 1; p < g.m.n_proj; ++p) shared_x = shared_x && g.m.d_in[p] == g.m.d_in[0];
+    if (shared_x) {
+      std::vector<uint32_t> singles;
+      for (uint32_t i = 0; i < n_tiles; ++i) {
+        singles.push_back(i);
+        singles.push_back(0xffffffffu);
       }
-      // Split-K factor: each candidate's LPT makespan (bytes the busiest
-      // CTA streams, at a per-SM share of HBM) plus the split reduction
-      // (partials written and read back); the cheapest
-      // wins.  Few splits for heavy uniform batches, more for mixed ranks.
-      const uint32_t d_in = g.m.d_in[p];
-      std::vector<std::vector<SgmvItem>> per, best_per;
-      uint32_t ks = 0;
-      double best = 0.0;
-      for (uint32_t cand = 1; cand <= 16; cand *= 2) {
-        if ((d_in / 64) % cand != 0 || (cand > 1 && d_in / cand < 256)) break;
-        const uint32_t kslice = d_in / cand;
-        std::vector<std::pair<uint64_t, SgmvItem>> items;  // (cost, item)
-        items.reserve(static_cast<size_t>(n_sunits) * cand);
-        uint64_t part_bytes = 0;
-        for (uint32_t u = 0; u < n_sunits; ++u) {
-          const uint64_t nt = sunits[2 * u + 1] != 0xffffffffu ? 2 : 1;
-          const SgmvTile& ta = tiles[sunits[2 * u]];
-          const uint64_t r16 = (ta.rank + 15) / 16 * 16;
-          // bytes streamed (x tiles + paged weights) plus the partial write-back
-          const uint64_t cost = 2ull * kslice * (nt * 128 + r16) + 4ull * nt * 128 * r16;
-          part_bytes += 8ull * nt * 128 * r16 * cand;
-          for (uint32_t sp = 0; sp < cand; ++sp) {
-            SgmvItem it{};
-            it.tile_a = sunits[2 * u];
-            it.tile_b = sunits[2 * u + 1];
-            it.row0_a = ta.row0;
-            it.row0_b = nt == 2 ? tiles[it.tile_b].row0 : 0;
-            it.table_off = ta.table_off;
-            it.rank = ta.rank;
-            it.split = sp;
-            items.emplace_back(cost, it);
-          }
-        }
-        std::stable_sort(items.begin(), items.end(),
-                         [](const auto& x, const auto& y) { return x.first > y.first; });
-        const uint32_t ctas = std::min<uint32_t>(n_sm, static_cast<uint32_t>(items.size()));
-        per.assign(ctas, {});
-        using Load = std::pair<uint64_t, uint32_t>;
-        std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-        for (uint32_t c = 0; c < ctas; ++c) heap.emplace(0, c);
-        uint64_t makespan = 0;
-        for (const auto& it : items) {
-          Load l = heap.top();
-          heap.pop();
-          per[l.second].push_back(it.second);
-          heap.emplace(l.first + it.first, l.second);
-          makespan = std::max(makespan, l.first + it.first);
-        }
-        constexpr double kSmBw = 45e9, kHbmBw = 5e12;
-        const double t = makespan / kSmBw + part_bytes / kHbmBw;
-        if (ks == 0 || t < best) {
-          ks = cand;
-          best = t;
-          best_per.swap(per);
-        }
-      }
-      per.swap(best_per);
-      const uint32_t ctas = static_cast<uint32_t>(per.size());
-      SgmvSched sc;
-      sc.splits = ks;
-      sc.ctas = ctas;
-      sc.item_off = static_cast<uint32_t>(sitems.size());
-      sc.cta_off = static_cast<uint32_t>(scta.size());
-      uint32_t n = 0;
-      for (uint32_t c = 0; c < ctas; ++c) {
-        scta.push_back(n);
-        for (const SgmvItem& v : per[c]) sitems.push_back(v);
-        n += static_cast<uint32_t>(per[c].size());
-      }
-      scta.push_back(n);
-      ssched[p] = sc;
+      ssched_layer = build_sched(singles, g.m.d_in[0], g.m.n_proj);
     }
   }
 
@@ -398,11 +409,13 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     PLORA_CUDA(cudaMalloc(&d_v, v_cap * sizeof(float)));
   }
   if (es == 2 && n_tiles > 0) {  // SGMV workspaces (see sgmv.cu)
-    uint64_t parts = 0;
+    // one region per projection (plora_sgmv_layer keeps both in flight)
+    uint64_t parts = ssched_layer.splits;
     for (uint32_t p = 0; p < g.m.n_proj; ++p)
       parts = std::max<uint64_t>(parts, ssched[p].splits);
-    const uint64_t need_part = parts * n_tiles * 128ull * 128ull;
-    const uint64_t need_vbuf = n_tiles * 128ull * 128ull * 2ull;
+    vpart_parts = static_cast<uint32_t>(parts);
+    const uint64_t need_part = g.m.n_proj * parts * n_tiles * 128ull * 128ull;
+    const uint64_t need_vbuf = g.m.n_proj * n_tiles * 128ull * 128ull * 2ull;
     if (vpart_cap < need_part || vbuf_cap < need_vbuf) {
       PLORA_CUDA(cudaStreamSynchronize(stream));
       cudaFree(d_vpart);

@@ -205,6 +205,8 @@ struct plora_plan {
   std::vector<uint32_t> sunits;
   uint32_t n_sunits = 0;
   plora::SgmvSched ssched[PLORA_MAX_PROJ];
+  plora::SgmvSched ssched_layer;  // both projections from one x chunk (splits 0: unavailable)
+  uint32_t vpart_parts = 0;       // K splits the partial regions are sized for
   std::vector<plora::GemmTile> gtiles;
   plora::GemmTile* d_gtiles = nullptr;
   std::vector<plora::SgmvItem> sitems;

@@ -63,7 +63,6 @@ constexpr uint32_t kChunkK = 64;   // shrink K per stage (one 128-byte swizzle r
 constexpr uint32_t kBlockN = 128;  // expand output columns per CTA
 constexpr uint32_t kMaxRank = 128;
 constexpr uint32_t kTmemCols = 128;
-constexpr int kGatherThreads = 96;   // expand: warps 1-3
 constexpr int kSGather = 192;       // shrink: warps 1-6
 constexpr int kEGather = 96;        // expand: warps 1-3
 
@@ -85,9 +84,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 //   warp 7      MMA issuer (and TMEM allocator)
 //   warps 8-11  epilogue (warp 8 + q reads TMEM lanes 32q..32q+31)
 constexpr int kSStages = 4;
-constexpr uint32_t kSStageBytes = 49152;  // X [2 tiles][128 × 64] 32 KiB + A [r16 × 64] <= 16 KiB
+constexpr uint32_t kSStageBytes = 49152;  // 16 KiB parts: x of each tile, then A of each projection
 constexpr uint32_t kSThreads = 384;
-constexpr uint32_t kSEpiThreads = 128;
 constexpr uint32_t kStgBytes = 8192;  // per epilogue warp: 32 rows × 64 fp32
 constexpr uint32_t kSTmemCols = 512;  // [buffer][tile][128 columns]
 
@@ -97,8 +95,10 @@ struct ShrinkArgs {
   const SgmvTile* tiles;
   const SgmvItem* items;
   const uint32_t* cta_items;  // [cta + 1] offsets into items
-  float* vpart;               // [tile][split] blocks of 128 × 128 fp32 (128 × r16 used)
-  uint64_t blk_mult;
+  float* vpart;               // [proj][tile][split] blocks of 128 × 128 fp32 (128 × r16 used)
+  uint64_t vpart_pstride;     // floats between projection regions
+  uint64_t blk_mult[2];       // per projection of the x chunk
+  uint32_t np;                // projections sharing each x chunk (nt · np <= 2)
   uint32_t log2_page;
   uint32_t d_in;
   uint32_t splits;
@@ -213,34 +213,48 @@ __global__ void __launch_bounds__(kSThreads, 1)
       const UnitInfo u = un;
       if (it + 1 < it1) un = unit_info(p.items + it + 1);
       const uint32_t k0 = u.split * kslice;
-      const uint64_t blk = static_cast<uint64_t>(u.r) * p.blk_mult * 2;  // A block, bytes
       const PagedSrc src{p.arena, p.table, u.table_off, p.log2_page};
-      const uint64_t off0 = blk + (static_cast<uint64_t>(n) * p.d_in + k0) * 2;  // row n's slice
       const bool live = fast && n < u.r;
-      const uint32_t lp_last = static_cast<uint32_t>((off0 + kslice * 2 - 1) >> p.log2_page);
-      uint32_t lp = static_cast<uint32_t>(off0 >> p.log2_page);
-      uint32_t e_cur = live ? __ldg(p.table + u.table_off + lp) : 0u;
-      uint32_t e_nxt = live && lp < lp_last ? __ldg(p.table + u.table_off + lp + 1) : 0u;
+      uint64_t off0[2];
+      uint32_t lp[2], lp_last[2], e_cur[2], e_nxt[2];
+#pragma unroll
+      for (uint32_t q = 0; q < 2; ++q) {  // this row of each projection's A block
+        const uint64_t blk = static_cast<uint64_t>(u.r) * (q ? p.blk_mult[1] : p.blk_mult[0]) * 2;
+        off0[q] = blk + (static_cast<uint64_t>(n) * p.d_in + k0) * 2;
+        lp_last[q] = static_cast<uint32_t>((off0[q] + kslice * 2 - 1) >> p.log2_page);
+        lp[q] = static_cast<uint32_t>(off0[q] >> p.log2_page);
+        const bool lq = live && q < p.np;
+        e_cur[q] = lq ? __ldg(p.table + u.table_off + lp[q]) : 0u;
+        e_nxt[q] = lq && lp[q] < lp_last[q] ? __ldg(p.table + u.table_off + lp[q] + 1) : 0u;
+      }
       for (uint32_t kc = 0; kc < NK; ++kc, ++g) {
         const uint32_t st = g % kSStages, ph = (g / kSStages) & 1u;
-        const uint64_t off = off0 + kc * kChunkK * 2;
-        if (live && (off >> p.log2_page) != lp) {  // crossed into the next page
-          lp = static_cast<uint32_t>(off >> p.log2_page);
-          e_cur = e_nxt;
-          e_nxt = lp < lp_last ? __ldg(p.table + u.table_off + lp + 1) : 0u;
+#pragma unroll
+        for (uint32_t q = 0; q < 2; ++q) {
+          const uint64_t off = off0[q] + kc * kChunkK * 2;
+          if (live && q < p.np && (off >> p.log2_page) != lp[q]) {  // crossed into the next page
+            lp[q] = static_cast<uint32_t>(off >> p.log2_page);
+            e_cur[q] = e_nxt[q];
+            e_nxt[q] = lp[q] < lp_last[q] ? __ldg(p.table + u.table_off + lp[q] + 1) : 0u;
+          }
         }
         ptx::mbar_wait(&empty[st], ph ^ 1u);
-        char* wdst = smem + SSmem::stages + st * kSStageBytes + 2 * kTileM * kChunkK * 2;
         if (n < u.r16 && !(p.dbg & 1u)) {
-          if (n >= u.r) {
 #pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), p.arena, 0);  // zero padding
-          } else if (fast) {
-            const char* base = p.arena + (static_cast<uint64_t>(e_cur) << p.log2_page) + (off & pmask);
+          for (uint32_t q = 0; q < 2; ++q) {
+            if (q >= p.np) break;
+            char* wdst = smem + SSmem::stages + st * kSStageBytes + (u.nt + q) * kTileM * kChunkK * 2;
+            const uint64_t off = off0[q] + kc * kChunkK * 2;
+            if (n >= u.r) {
 #pragma unroll
-            for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), base + c * 16, 16);
-          } else {
-            for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), src.at(off + c * 16), 16);
+              for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), p.arena, 0);  // zero padding
+            } else if (fast) {
+              const char* base = p.arena + (static_cast<uint64_t>(e_cur[q]) << p.log2_page) + (off & pmask);
+#pragma unroll
+              for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), base + c * 16, 16);
+            } else {
+              for (uint32_t c = 0; c < 8; ++c) ptx::cp_async_16(wdst + swz(n, c), src.at(off + c * 16), 16);
+            }
           }
         }
         ptx::cp_async_mbar_arrive_noinc(&full[st]);
@@ -266,15 +280,22 @@ __global__ void __launch_bounds__(kSThreads, 1)
           }
           ptx::fence_proxy_async_shared();
           ptx::tc_fence_after();
-          const uint32_t xa = sbase + st * kSStageBytes, xb = xa + kTileM * kChunkK * 2;
-          const uint32_t wa = xa + 2 * kTileM * kChunkK * 2;
+          // accumulators: tile t against the A chunk (np = 1), or the one tile
+          // against projection q's A chunk (np = 2), in TMEM columns 128 · (t | q)
+          const uint32_t xa = sbase + st * kSStageBytes;
+          constexpr uint32_t kPart = kTileM * kChunkK * 2;
+          const uint32_t wa = xa + u.nt * kPart;  // first A chunk
+          const bool second = u.nt == 2 || p.np == 2;
 #pragma unroll
           for (uint32_t k = 0; k < kChunkK / 16; ++k) {
-            const uint64_t wd = ptx::smem_desc_sw128(wa + k * 32, 16, 1024);
-            ptx::umma_f16(tb, ptx::smem_desc_sw128(xa + k * 32, 16, 1024), wd, idesc, (kc | k) != 0);
-            if (u.nt == 2)
-              ptx::umma_f16(tb + kTmemCols, ptx::smem_desc_sw128(xb + k * 32, 16, 1024), wd, idesc,
-                            (kc | k) != 0);
+            const uint64_t x0 = ptx::smem_desc_sw128(xa + k * 32, 16, 1024);
+            const uint64_t w0 = ptx::smem_desc_sw128(wa + k * 32, 16, 1024);
+            ptx::umma_f16(tb, x0, w0, idesc, (kc | k) != 0);
+            if (second) {
+              const uint64_t x1 = p.np == 2 ? x0 : ptx::smem_desc_sw128(xa + kPart + k * 32, 16, 1024);
+              const uint64_t w1 = p.np == 2 ? ptx::smem_desc_sw128(wa + kPart + k * 32, 16, 1024) : w0;
+              ptx::umma_f16(tb + kTmemCols, x1, w1, idesc, (kc | k) != 0);
+            }
           }
           ptx::umma_commit(&empty[st]);
         }
@@ -292,18 +313,19 @@ __global__ void __launch_bounds__(kSThreads, 1)
       const uint32_t buf = i & 1u, tb = tmem + buf * 2 * kTmemCols;
       ptx::mbar_wait(&tfull[buf], (i >> 1) & 1u);
       ptx::tc_fence_after();
-      const uint32_t ntw = (p.dbg & 16u) ? 0u : u.nt;
-      for (uint32_t t = 0; t < ntw; ++t) {
+      const uint32_t nacc = (p.dbg & 16u) ? 0u : u.nt * p.np;
+      for (uint32_t a = 0; a < nacc; ++a) {
+        const uint32_t t = a / p.np, pj = a - t * p.np;
         const uint32_t tile_i = t ? u.tile_b : u.tile_a;
-        float* blk = p.vpart + (static_cast<uint64_t>(tile_i) * p.splits + u.split) * kTileM * kMaxRank +
-                     q * 32 * u.r16;
+        float* blk = p.vpart + pj * p.vpart_pstride +
+                     (static_cast<uint64_t>(tile_i) * p.splits + u.split) * kTileM * kMaxRank + q * 32 * u.r16;
         for (uint32_t pass = 0; pass * 64 < u.r16; ++pass) {
           const uint32_t pw = min(64u, u.r16 - pass * 64), pw4 = pw / 4, swm = part_swm(pw4);
           if (lane == 0) ptx::bulk_wait_read_n<0>();  // the staging buffer's last copy has read it
           __syncwarp();
           for (uint32_t cc = 0; cc < pw / 16; ++cc) {
             uint32_t rv[16];
-            ptx::tmem_ld_32x32b_x16(tb + lane_base + t * kTmemCols + pass * 64 + cc * 16, rv);
+            ptx::tmem_ld_32x32b_x16(tb + lane_base + a * kTmemCols + pass * 64 + cc * 16, rv);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (uint32_t c = 0; c < 4; ++c)
@@ -340,19 +362,22 @@ constexpr uint32_t kRThreads = 256;
 struct ReduceArgs {
   const SgmvTile* tiles;
   const float* vpart;
-  __nv_bfloat16* vbuf;  // [tile][128][128] bf16
+  __nv_bfloat16* vbuf;  // [proj][tile][128][128] bf16
+  uint64_t vpart_pstride;  // floats between projection regions
+  uint32_t n_tiles;
   uint32_t splits;
   float scale;  // V = bf16(scale · Σ partials): 1 for plora_sgmv, the LoRA scale when fused
 };
 
 __global__ void __launch_bounds__(kRThreads) sgmv_reduce_kernel(const ReduceArgs p) {
   ptx::pdl_launch_dependents();
-  const uint32_t tile = blockIdx.x >> 2, qq = blockIdx.x & 3;
+  const uint32_t pj = blockIdx.x / (4 * p.n_tiles), rest = blockIdx.x - pj * 4 * p.n_tiles;
+  const uint32_t tile = rest >> 2, qq = rest & 3;
   const uint32_t r16 = (p.tiles[tile].rank + 15) & ~15u, q4 = 8 * r16;  // float4s per quarter
   constexpr uint32_t kSplitStride = kTileM * kMaxRank / 4;  // float4s
-  const float4* v0 = reinterpret_cast<const float4*>(p.vpart) +
+  const float4* v0 = reinterpret_cast<const float4*>(p.vpart + pj * p.vpart_pstride) +
                      static_cast<uint64_t>(tile) * p.splits * kSplitStride + qq * q4;
-  __nv_bfloat16* vb = p.vbuf + static_cast<uint64_t>(tile) * kTileM * kMaxRank;
+  __nv_bfloat16* vb = p.vbuf + (static_cast<uint64_t>(pj) * p.n_tiles + tile) * kTileM * kMaxRank;
   ptx::pdl_wait();  // the shrink's partials
   constexpr uint32_t kU = 4;
   for (uint32_t f0 = threadIdx.x; f0 < q4; f0 += kU * kRThreads) {
@@ -410,12 +435,11 @@ struct ExpandArgs {
   const char* arena;
   const uint32_t* table;
   const SgmvTile* tiles;
-  char* y;
-  uint64_t y_stride_b;
-  uint64_t blk_mult;
+  uint64_t blk_mult[2];  // per projection (CTA (proj, tile, group))
   uint32_t log2_page;
   uint32_t d_in;
   uint32_t d_out;
+  uint32_t n_tiles;
   uint32_t ngroups;  // column groups per tile
   float scale;
   uint32_t dbg;  // diagnostics: 64 no y reduce-add, 128 no Bᵀ gather, 256 no MMA, 512 prologue only
@@ -434,7 +458,8 @@ struct ESmem {  // ~97 KB: two expand CTAs per SM
 };
 
 __global__ void __launch_bounds__(kEThreads, 2)
-    sgmv_expand_kernel(const ExpandArgs p, const __grid_constant__ CUtensorMap tmap_y,
+    sgmv_expand_kernel(const ExpandArgs p, const __grid_constant__ CUtensorMap tmap_y0,
+                       const __grid_constant__ CUtensorMap tmap_y1,
                        const __grid_constant__ CUtensorMap tmap_v) {
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -447,11 +472,15 @@ __global__ void __launch_bounds__(kEThreads, 2)
   uint64_t* acc_empty = v_full + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + ESmem::tmem_slot);
 
-  const uint32_t tile_i = blockIdx.x / p.ngroups, grp = blockIdx.x % p.ngroups;
+  const uint32_t per_proj = p.n_tiles * p.ngroups;
+  const uint32_t pj = blockIdx.x / per_proj, tile_i = (blockIdx.x % per_proj) / p.ngroups,
+                 grp = blockIdx.x % p.ngroups;
+  const CUtensorMap* tmap_y = pj ? &tmap_y1 : &tmap_y0;
   const SgmvTile tile = p.tiles[tile_i];
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r = tile.rank, r16 = (r + 15) & ~15u;
-  const uint64_t bt = (static_cast<uint64_t>(r) * p.blk_mult + static_cast<uint64_t>(r) * p.d_in) * 2;
+  const uint64_t bt = (static_cast<uint64_t>(r) * (pj ? p.blk_mult[1] : p.blk_mult[0]) +
+                       static_cast<uint64_t>(r) * p.d_in) * 2;
   const PagedSrc src{p.arena, p.table, tile.table_off, p.log2_page};
   const uint32_t nblk = min(kGroupBlocks, p.d_out / kEBlockN - grp * kGroupBlocks);
   const uint32_t col_base = grp * kGroupBlocks * kEBlockN;
@@ -471,7 +500,7 @@ __global__ void __launch_bounds__(kEThreads, 2)
   }
   if (warp == 4) ptx::tmem_alloc(tmem_slot, kETmemCols);
   if (warp == 0 && lane == 0) {
-    ptx::prefetch_tmap(&tmap_y);
+    ptx::prefetch_tmap(tmap_y);
     ptx::prefetch_tmap(&tmap_v);
   }
   ptx::tc_fence_before();
@@ -487,7 +516,7 @@ __global__ void __launch_bounds__(kEThreads, 2)
       ptx::mbar_arrive_expect_tx(v_full, vboxes * 16384);
       for (uint32_t bx = 0; bx < vboxes; ++bx)
         ptx::tma_load_2d(smem + ESmem::v + bx * 16384, &tmap_v, static_cast<int32_t>(bx * 64),
-                         static_cast<int32_t>(tile_i * kTileM), v_full);
+                         static_cast<int32_t>((pj * p.n_tiles + tile_i) * kTileM), v_full);
     }
   } else if (warp < 4) {
     // ----------------------------------- Bᵀ block gathers (paged rows)
@@ -603,7 +632,7 @@ __global__ void __launch_bounds__(kEThreads, 2)
       ptx::named_bar_sync(1, kEEpiThreads);
       if (warp == 4 && lane == 0) {
         ptx::mbar_arrive(&acc_empty[st]);
-        if (!(p.dbg & 64u)) ptx::tma_reduce_add_2d(&tmap_y, static_cast<int32_t>(col0), static_cast<int32_t>(tile.row0), ys);
+        if (!(p.dbg & 64u)) ptx::tma_reduce_add_2d(tmap_y, static_cast<int32_t>(col0), static_cast<int32_t>(tile.row0), ys);
         ptx::bulk_commit();
       }
     }
@@ -626,27 +655,31 @@ extern "C" int plora_debug_set_sgmv_flags(uint32_t flags) {
 
 namespace plora {
 
-// Shrink + split reduction of one (layer, proj) call: V tiles (bf16, scaled
-// by v_scale) in plan->d_vbuf.  Shared by plora_sgmv and plora_sgmv_fused.
-void sgmv_shrink_reduce(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
-                        uint64_t x_stride, float v_scale, cudaStream_t s) {
+// Shrink + split reduction of `np` projections (<= 2) that share x: V tiles
+// (bf16, scaled by v_scale) in plan->d_vbuf, projection j's at tile offset
+// j · n_tiles.  np = 2 reads each x chunk once for both (plan->ssched_layer).
+void sgmv_shrink_reduce_n(plora_plan* plan, uint32_t layer, const uint32_t* projs, uint32_t np,
+                          const void* x, uint64_t x_stride, float v_scale, cudaStream_t s) {
   const plora_store& st = *plan->store;
   const ModelGeom& g = st.geom;
-  const uint32_t din = g.m.d_in[proj];
-  const SgmvSched& sc = plan->ssched[proj];
+  const uint32_t din = g.m.d_in[projs[0]];
+  const SgmvSched& sc = np == 1 ? plan->ssched[projs[0]] : plan->ssched_layer;
   CUtensorMap tmap_x;
   make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kChunkK, kTileM);
   set_smem_once(reinterpret_cast<const void*>(sgmv_shrink_kernel), static_cast<int>(SSmem::alloc));
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  const uint64_t pstride = static_cast<uint64_t>(plan->vpart_parts) * plan->n_tiles * kTileM * kMaxRank;
   ShrinkArgs sa{};
   sa.arena = st.arena;
   sa.table = st.d_table;
   sa.items = plan->d_sitems + sc.item_off;
   sa.cta_items = plan->d_scta + sc.cta_off;
   sa.vpart = plan->d_vpart;
-  sa.blk_mult = g.blk_mult(layer, proj);
+  sa.vpart_pstride = pstride;
+  for (uint32_t j = 0; j < 2; ++j) sa.blk_mult[j] = g.blk_mult(layer, projs[j < np ? j : 0]);
+  sa.np = np;
   sa.log2_page = st.log2_page;
   sa.d_in = din;
   sa.splits = sc.splits;
@@ -662,13 +695,71 @@ void sgmv_shrink_reduce(plora_plan* plan, uint32_t layer, uint32_t proj, const v
   count_launch();
   if (!(g_sgmv_dbg & 32u)) {
     ReduceArgs ra{plan->d_tiles, plan->d_vpart, reinterpret_cast<__nv_bfloat16*>(plan->d_vbuf),
-                  sc.splits, v_scale};
-    cfg.gridDim = dim3(plan->n_tiles * 4);
+                  pstride, plan->n_tiles, sc.splits, v_scale};
+    cfg.gridDim = dim3(np * plan->n_tiles * 4);
     cfg.blockDim = dim3(kRThreads);
     cfg.dynamicSmemBytes = 0;
     PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_reduce_kernel, ra));
     count_launch();
   }
+}
+
+void sgmv_shrink_reduce(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
+                        uint64_t x_stride, float v_scale, cudaStream_t s) {
+  sgmv_shrink_reduce_n(plan, layer, &proj, 1, x, x_stride, v_scale, s);
+}
+
+// The tensor-core SGMV of `np` projections sharing x (equal d_in, d_out):
+// one shrink + reduction, one expand launch over (proj, tile, group) CTAs.
+static void sgmv_run(plora_plan* plan, uint32_t layer, const uint32_t* projs, uint32_t np, const void* x,
+              uint64_t x_stride, void* const* ys, const uint64_t* y_strides, float scale,
+              cudaStream_t s) {
+  const plora_store& st = *plan->store;
+  const ModelGeom& g = st.geom;
+  const uint32_t din = g.m.d_in[projs[0]], dout = g.m.d_out[projs[0]];
+  sgmv_shrink_reduce_n(plan, layer, projs, np, x, x_stride, 1.0f, s);
+  if (g_sgmv_dbg & 8u) return;
+  CUtensorMap tmap_y[2], tmap_v;
+  for (uint32_t j = 0; j < 2; ++j) {
+    const uint32_t jj = j < np ? j : 0;
+    make_tmap_2d(&tmap_y[j], ys[jj], dout, plan->n_tokens, y_strides[jj] * 2, 64, kTileM);
+  }
+  make_tmap_2d(&tmap_v, plan->d_vbuf, kMaxRank, static_cast<uint64_t>(np) * plan->n_tiles * kTileM,
+               kMaxRank * 2, 64, kTileM);
+  set_smem_once(reinterpret_cast<const void*>(sgmv_expand_kernel), static_cast<int>(ESmem::alloc));
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  ExpandArgs ea{};
+  ea.arena = st.arena;
+  ea.table = st.d_table;
+  ea.tiles = plan->d_tiles;
+  for (uint32_t j = 0; j < 2; ++j) ea.blk_mult[j] = g.blk_mult(layer, projs[j < np ? j : 0]);
+  ea.log2_page = st.log2_page;
+  ea.d_in = din;
+  ea.d_out = dout;
+  ea.n_tiles = plan->n_tiles;
+  ea.ngroups = (dout / kEBlockN + kGroupBlocks - 1) / kGroupBlocks;
+  ea.scale = scale;
+  ea.dbg = g_sgmv_dbg;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(np * plan->n_tiles * ea.ngroups);
+  cfg.blockDim = dim3(kEThreads);
+  cfg.dynamicSmemBytes = ESmem::alloc;
+  cfg.stream = s;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y[0], tmap_y[1], tmap_v));
+  count_launch();
+}
+
+static bool tc_path(const plora_plan* plan, uint32_t proj) {
+  const ModelGeom& g = plan->store->geom;
+  // bf16, rank <= 128, d_in % 64 == 0, d_out % 128 == 0; anything else (fp32
+  // storage, wider ranks, odd widths) runs the exact CUDA-core BGMV path,
+  // which handles every segment length.
+  return g.esize == 2 && plan->max_rank <= kMaxRank && g.m.d_in[proj] % kChunkK == 0 &&
+         g.m.d_out[proj] % kBlockN == 0;
 }
 
 }  // namespace plora
@@ -679,50 +770,40 @@ extern "C" int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
   return guard([&] {
     if (!plan) throw ValidationError("null plan");
     check_io(plan, layer, proj, x, x_stride, y, y_stride);
-    const plora_store& st = *plan->store;
-    const ModelGeom& g = st.geom;
-    const uint32_t din = g.m.d_in[proj], dout = g.m.d_out[proj];
-    // The tensor-core path: bf16, rank <= 128, d_in % 64 == 0, d_out % 128 == 0.
-    // Anything else (fp32 storage, wider ranks, odd widths) runs the exact
-    // CUDA-core BGMV path, which handles every segment length.
-    if (g.esize != 2 || plan->max_rank > kMaxRank || din % kChunkK || dout % kBlockN)
+    if (!tc_path(plan, proj))
       return plora_bgmv(plan, layer, proj, x, x_stride, y, y_stride, scale, stream);
     if (plan->n_tiles == 0) return 0;
-    DeviceCtx ctx(st.device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    sgmv_shrink_reduce(plan, layer, proj, x, x_stride, 1.0f, s);
-    if (g_sgmv_dbg & 8u) return 0;
+    DeviceCtx ctx(plan->store->device);
+    void* ys[1] = {y};
+    const uint64_t ystr[1] = {y_stride};
+    sgmv_run(plan, layer, &proj, 1, x, x_stride, ys, ystr, scale, static_cast<cudaStream_t>(stream));
+    return 0;
+  });
+}
 
-    CUtensorMap tmap_y, tmap_v;
-    make_tmap_2d(&tmap_y, y, dout, plan->n_tokens, y_stride * 2, 64, kTileM);
-    make_tmap_2d(&tmap_v, plan->d_vbuf, kMaxRank, static_cast<uint64_t>(plan->n_tiles) * kTileM,
-                 kMaxRank * 2, 64, kTileM);
-    set_smem_once(reinterpret_cast<const void*>(sgmv_expand_kernel), static_cast<int>(ESmem::alloc));
-    cudaLaunchAttribute pdl[1];
-    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    ExpandArgs ea{};
-    ea.arena = st.arena;
-    ea.table = st.d_table;
-    ea.tiles = plan->d_tiles;
-    ea.y = static_cast<char*>(y);
-    ea.y_stride_b = y_stride * 2;
-    ea.blk_mult = g.blk_mult(layer, proj);
-    ea.log2_page = st.log2_page;
-    ea.d_in = din;
-    ea.d_out = dout;
-    ea.ngroups = (dout / kEBlockN + kGroupBlocks - 1) / kGroupBlocks;
-    ea.scale = scale;
-    ea.dbg = g_sgmv_dbg;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(plan->n_tiles * ea.ngroups);
-    cfg.blockDim = dim3(kEThreads);
-    cfg.dynamicSmemBytes = ESmem::alloc;
-    cfg.stream = s;
-    cfg.attrs = pdl;
-    cfg.numAttrs = 1;
-    PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y, tmap_v));
-    count_launch();
+extern "C" int plora_sgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x_stride,
+                                void* const* ys, const uint64_t* y_strides, float scale,
+                                plora_stream_t stream) {
+  return guard([&] {
+    if (!plan) throw ValidationError("null plan");
+    if (!ys || !y_strides) throw ValidationError("null ys / y_strides");
+    const ModelGeom& g = plan->store->geom;
+    const uint32_t np = g.m.n_proj;
+    for (uint32_t j = 0; j < np; ++j) check_io(plan, layer, j, x, x_stride, ys[j], y_strides[j]);
+    bool joint = np == 2 && plan->ssched_layer.splits != 0;
+    for (uint32_t j = 0; j < np; ++j)
+      joint = joint && tc_path(plan, j) && g.m.d_in[j] == g.m.d_in[0] && g.m.d_out[j] == g.m.d_out[0];
+    if (!joint) {  // one call per projection
+      for (uint32_t j = 0; j < np; ++j) {
+        const int rc = plora_sgmv(plan, layer, j, x, x_stride, ys[j], y_strides[j], scale, stream);
+        if (rc != 0) return rc;
+      }
+      return 0;
+    }
+    if (plan->n_tiles == 0) return 0;
+    DeviceCtx ctx(plan->store->device);
+    const uint32_t projs[2] = {0, 1};
+    sgmv_run(plan, layer, projs, 2, x, x_stride, ys, y_strides, scale, static_cast<cudaStream_t>(stream));
     return 0;
   });
 }

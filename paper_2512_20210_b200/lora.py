@@ -280,6 +280,24 @@ def sgmv(plan: BatchPlan, layer: int, proj: int, x: torch.Tensor, y: torch.Tenso
     return y
 
 
+def sgmv_layer(plan: BatchPlan, layer: int, x: torch.Tensor, ys: Sequence[torch.Tensor],
+               scale: float = 1.0, stream: int | None = None) -> Sequence[torch.Tensor]:
+    """Prefill path for every projection of `layer`: ys[p] += scale · (x · A_pᵀ) · B_pᵀ;
+    two projections of equal shape share each x chunk of the shrink and one
+    expand launch."""
+    shape = plan.store.shape
+    if len(ys) != shape.n_proj:
+        raise N.ValidationError(f"sgmv_layer needs {shape.n_proj} outputs, got {len(ys)}")
+    for p, y in enumerate(ys):
+        _check_io(plan, p, x, y)
+    ptrs = (C.c_void_p * shape.n_proj)(*[y.data_ptr() for y in ys])
+    strides = (C.c_uint64 * shape.n_proj)(*[y.stride(0) for y in ys])
+    s = current_stream_handle(x.device) if stream is None else stream
+    N.check(N.lib().plora_sgmv_layer(plan.handle, layer, x.data_ptr(), x.stride(0), ptrs, strides,
+                                     scale, s))
+    return ys
+
+
 def sgmv_fused(plan: BatchPlan, layer: int, proj: int, x: torch.Tensor, w0: torch.Tensor,
                y: torch.Tensor, scale: float = 1.0, stream: int | None = None) -> torch.Tensor:
     """y = x · W0ᵀ + scale · (x · Aᵀ) · Bᵀ per token: the base projection with the

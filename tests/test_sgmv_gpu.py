@@ -8,7 +8,7 @@ import torch
 from lora_harness import TOL_BF16, Setup, rel_err, to_np_bits
 from paper_2512_20210_b200 import synth
 from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, ModelShape, bgmv, sgmv,
-                                        kernel_launch_count)
+                                        kernel_launch_count, sgmv_layer)
 
 pytestmark = pytest.mark.gpu
 
@@ -93,3 +93,50 @@ def test_sgmv_fp32_store_routes_to_exact_path(cuda):
     ta = np.repeat(np.arange(2, dtype=np.int32), 40)
     yd, ref, _ = _sgmv_vs_oracle(s, ta, 0, 0)
     assert rel_err(yd, ref) <= 1e-5
+
+
+def test_sgmv_layer_matches_oracle_per_projection(cuda):
+    """plora_sgmv_layer (both projections from one x chunk, one expand launch)
+    against the oracle for each projection: runs with partial tiles and -1
+    gaps, ranks 1..128."""
+    shape = ModelShape(2, (4096, 4096), (2048, 2048), torch.bfloat16)
+    ranks = [16, 64, 128, 8, 3, 100, 32, 1]
+    cfg = synth.DecodeConfig("sgmv_layer", shape, ranks, 1, 2048)
+    s = Setup(cfg)
+    runs = [(0, 300), (1, 130), (-1, 5), (2, 128), (3, 1), (4, 77), (5, 129), (-1, 2), (6, 64),
+            (7, 9), (2, 40)]
+    ta = np.concatenate([np.full(n, a, np.int32) for a, n in runs])
+    T = len(ta)
+    x = synth.activations(T, 4096, shape.dtype, "x", salt=5)
+    y0 = [synth.activations(T, 2048, shape.dtype, "y", salt=5 + p) for p in range(2)]
+    ys = [y.cuda() for y in y0]
+    plan = BatchPlan(s.store, ta)
+    n0 = kernel_launch_count()
+    sgmv_layer(plan, 1, x.cuda(), ys, 0.5)
+    torch.cuda.synchronize()
+    assert kernel_launch_count() - n0 == 3  # joint shrink + reduction + expand
+    for p in range(2):
+        ref = s.oracle(1, p, x, y0[p], ta, scale=0.5, v_bf16=True)
+        assert rel_err(ys[p], ref) <= TOL_BF16, p
+        none = ta < 0
+        assert np.array_equal(to_np_bits(ys[p])[none], to_np_bits(y0[p])[none])
+
+
+def test_sgmv_layer_cfg3_agrees_with_per_projection(cuda):
+    """BASELINE config 3 call shape (6 segments × 512): the joint launch agrees
+    with two plora_sgmv calls within the bf16 tolerance."""
+    cfg = synth.cfg3(n_layers=2, n_segments=6)
+    s = Setup(cfg)
+    ta = synth.segment_assignment(6, 512)
+    plan = BatchPlan(s.store, ta)
+    x = torch.randn(len(ta), 4096, device="cuda").to(torch.bfloat16)
+    y0 = torch.randn(len(ta), 4096, device="cuda").to(torch.bfloat16)
+    a = [y0.clone(), y0.clone()]
+    b = [y0.clone(), y0.clone()]
+    sgmv_layer(plan, 1, x, a)
+    for p in range(2):
+        sgmv(plan, 1, p, x, b[p])
+    torch.cuda.synchronize()
+    for p in range(2):
+        err = (a[p].float() - b[p].float()).abs().max().item() / b[p].float().abs().max().item()
+        assert err <= TOL_BF16, (p, err)
