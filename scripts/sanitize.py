@@ -1,6 +1,7 @@
 """Small paged-LoRA calls for compute-sanitizer (memcheck / racecheck /
 synccheck): the cluster BGMV (per projection and fused per layer), the SGMV
-pair and the TP halves on a 2-layer cfg1 store.
+(per projection, per layer, fused with the base GEMM) and the TP halves on a
+2-layer cfg1 store.
 
 compute-sanitizer --tool memcheck python scripts/sanitize.py
 """
@@ -15,7 +16,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 from lora_harness import Setup  # noqa: E402
 from paper_2512_20210_b200 import synth  # noqa: E402
-from paper_2512_20210_b200.lora import BatchPlan, bgmv, bgmv_layer, sgmv  # noqa: E402
+from paper_2512_20210_b200.lora import BatchPlan, bgmv, bgmv_layer, sgmv, sgmv_fused, sgmv_layer  # noqa: E402
 from paper_2512_20210_b200.tp import bgmv_tp_expand, bgmv_tp_shrink, tp_shard_rows  # noqa: E402
 
 
@@ -37,6 +38,10 @@ def main():
     xs2 = torch.randn(len(seg2), 4096, device="cuda").to(torch.bfloat16)
     ys2 = torch.randn(len(seg2), 4096, device="cuda").to(torch.bfloat16)
     sgmv(BatchPlan(s.store, seg2), 1, 0, xs2, ys2)
+    plan2 = BatchPlan(s.store, seg2)
+    sgmv_layer(plan2, 1, xs2, [ys2, ys2.clone()])  # both projections from one x chunk
+    w0 = torch.randn(4096, 4096, device="cuda").to(torch.bfloat16)
+    sgmv_fused(plan2, 0, 0, xs2, w0, torch.empty_like(ys2))  # base GEMM + LoRA K-steps
     rs = tp_shard_rows(plan, 2)
     vp = torch.empty(2, T, rs, device="cuda")
     for i in range(2):
