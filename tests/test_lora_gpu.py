@@ -155,6 +155,22 @@ def test_edge_cases(cuda):
         assert torch.equal(y, y0)
 
 
+@pytest.mark.parametrize("page_bytes", [256, 512])
+def test_small_pages_wide_rows(cuda, page_bytes):
+    """Llama-7B row widths on pages smaller than a CTA's 2 KiB row slice (the
+    generic piece path; 72 / 40 page pieces per 8 A rows, past the 32 the
+    lookahead covers: the producer's synchronous small-page loop), ranks 3..64
+    with partial chunks."""
+    shape = ModelShape(2, (4096, 4096), (4096, 4096), torch.bfloat16)
+    ranks = [8, 16, 64, 3, 13]
+    cfg = synth.DecodeConfig("smallpage", shape, ranks, 2, page_bytes)
+    s = Setup(cfg)
+    ta = synth.token_assignment(len(ranks), 2)
+    for layer, proj in ((0, 1), (1, 0)):
+        yd, ref = _run(s, layer, proj, ta, scale=0.5, salt=layer)
+        assert rel_err(yd, ref) <= TOL_BF16, (page_bytes, layer, proj)
+
+
 def test_errors_are_loud(cuda):
     cfg = synth.cfg1(n_layers=1)
     s = Setup(cfg)
