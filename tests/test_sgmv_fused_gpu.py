@@ -94,3 +94,19 @@ def test_sgmv_fused_rejects_bad_shapes(cuda):
         sgmv_fused(plan, 0, 0, x, torch.zeros(4096, 4096, device="cuda"), y)  # fp32 weight
     with pytest.raises(N.ValidationError):
         sgmv_fused(plan, 0, 0, x, torch.zeros(2048, 4096, dtype=torch.bfloat16, device="cuda"), y)
+
+
+@pytest.mark.parametrize("page_bytes", [64, 256])
+def test_sgmv_fused_small_pages(cuda, page_bytes):
+    """Bᵀ row segments of a 256-column block straddle pages: the LoRA K-step
+    gathers translate every 16-byte piece through the page table."""
+    shape = ModelShape(2, (1024, 1024), (1024, 512), torch.bfloat16)
+    cfg = synth.DecodeConfig("fused_smallpage", shape, [16, 64, 128, 5], 1, page_bytes)
+    s = Setup(cfg)
+    runs = [(0, 200), (1, 128), (-1, 3), (2, 150), (3, 20)]
+    ta = np.concatenate([np.full(n, a, np.int32) for a, n in runs])
+    for proj in (0, 1):
+        w0 = torch.zeros(shape.d_out[proj], shape.d_in[proj], dtype=torch.bfloat16, device="cuda")
+        x, y, _ = _run(s, ta, 1, proj, w0, 0.5, proj)
+        ref = _delta(s, ta, 1, proj, x, 0.5)
+        assert rel_err(y, ref.numpy()) <= TOL_BF16, proj

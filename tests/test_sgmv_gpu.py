@@ -140,3 +140,27 @@ def test_sgmv_layer_cfg3_agrees_with_per_projection(cuda):
     for p in range(2):
         err = (a[p].float() - b[p].float()).abs().max().item() / b[p].float().abs().max().item()
         assert err <= TOL_BF16, (p, err)
+
+
+@pytest.mark.parametrize("page_bytes", [64, 256])
+def test_sgmv_small_pages(cuda, page_bytes):
+    """Pages smaller than a row segment of a K chunk / column block: the
+    gathers translate every 16-byte piece (64 B) or every 128-byte segment
+    (256 B) through the page table; per-projection and per-layer paths."""
+    shape = ModelShape(2, (1024, 1024), (1024, 1024), torch.bfloat16)
+    ranks = [16, 64, 128, 5]
+    cfg = synth.DecodeConfig("sgmv_smallpage", shape, ranks, 1, page_bytes)
+    s = Setup(cfg)
+    runs = [(0, 200), (1, 128), (-1, 3), (2, 150), (3, 20)]
+    ta = np.concatenate([np.full(n, a, np.int32) for a, n in runs])
+    yd, ref, _ = _sgmv_vs_oracle(s, ta, 1, 0, scale=0.5, salt=2)
+    assert rel_err(yd, ref) <= TOL_BF16
+    T = len(ta)
+    x = synth.activations(T, 1024, shape.dtype, "x", salt=3)
+    y0 = [synth.activations(T, 1024, shape.dtype, "y", salt=3 + p) for p in range(2)]
+    ys = [y.cuda() for y in y0]
+    sgmv_layer(BatchPlan(s.store, ta), 0, x.cuda(), ys)
+    torch.cuda.synchronize()
+    for p in range(2):
+        ref = s.oracle(0, p, x, y0[p], ta, v_bf16=True)
+        assert rel_err(ys[p], ref) <= TOL_BF16, p
