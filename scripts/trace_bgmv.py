@@ -11,7 +11,7 @@ comparable within a CTA only):
   4 producer: before slot wait      5 producer: slot free (issuing)
   6 producer: lookahead landed      (k = 63: 6 CTA start, 7 CTA end)
   8 shrink: MMAs done   9 shrink: partial barrier passed   10 expand: v built
-  11 expand: MMAs done  12 page warp 0: copies issued      13 control: header out
+  11 expand: MMAs done  12 page warp 0: copies issued      13 (unused)
   14 shrink: before the chunk wait  15 shrink: job x landed, barrier armed
 """
 import ctypes as C
@@ -89,10 +89,11 @@ def main():
     tstart = t[:, K - 1, 6].copy()
     t[:, K - 1, :] = 0
     wait_slot = (t[..., 5] - t[..., 4])[t[..., 4] > 0] / 1e3
-    m = (t[:, 1:, 6] > 0) & (t[:, :-1, 5] > 0)
-    work = (t[:, 1:, 6] - t[:, :-1, 5])[m] / 1e3
+    # page warp 0 takes every other chunk of its ring
+    m = (t[:, 2::2, 6] > 0) & (t[:, :-2:2, 5] > 0)
+    work = (t[:, 2::2, 6] - t[:, :-2:2, 5])[m] / 1e3
     pre = (t[..., 4] - t[..., 6])[(t[..., 4] > 0) & (t[..., 6] > 0)] / 1e3
-    print(f"producer: issue work (slot free -> next lookahead landed) median {np.median(work):.2f} us; "
+    print(f"producer: issue work (slot free -> its next chunk's lookahead landed) median {np.median(work):.2f} us; "
           f"lookahead-landed -> slot wait start median {np.median(pre):.2f} us")
     land = (t[..., 0] - t[..., 5])[(t[..., 0] > 0) & (t[..., 5] > 0)] / 1e3
     print(f"data latency (issued -> consumer saw it) median {np.median(land):.2f} us")
@@ -107,7 +108,7 @@ def main():
     print(f"shrink: wait {med(14, 0):.2f} | hdr->x ready {med(0, 15):.2f} | MMAs {med(15, 8):.2f} | barrier {med(8, 9):.2f} | "
           f"sum+send {med(9, 1):.2f} us")
     print(f"expand: xchg->v built {med(2, 10):.2f} | MMAs {med(10, 11):.2f} | y+barrier {med(11, 3):.2f} us")
-    print(f"page warp 0: slot free -> issued {med(5, 12):.2f} us; control: header after slot free {med(5, 13):.2f}")
+    print(f"page warp 0: slot free -> issued {med(5, 12):.2f} us")
     for c in (0, 1, 2, 3, ctas // 2):
         v = valid[c]
         c0 = tstart[c]
