@@ -140,4 +140,82 @@ class PagePool {
   plora_pool* p_ = nullptr;
 };
 
+// ------------------------------------------------------ device path (new)
+// The adapter pages in HBM behind a PagePool (which must outlive the store).
+class DeviceStore {
+ public:
+  DeviceStore(PagePool& pool, int device, const plora_model& model, std::uint32_t max_adapters) {
+    check(plora_store_create(pool.handle(), device, &model, max_adapters, &s_));
+  }
+  ~DeviceStore() { plora_store_destroy(s_); }
+  DeviceStore(const DeviceStore&) = delete;
+  DeviceStore& operator=(const DeviceStore&) = delete;
+
+  void register_adapter(AdapterKey a, std::uint32_t rank) { check(plora_store_register(s_, a, rank)); }
+  // H2D page scatter of the adapter's logical bytes (start_transfer, engine.cpp:250-259)
+  void write_pages(AdapterKey a, const void* host_src, std::uint64_t bytes,
+                   int mode = PLORA_COPY_CE, plora_stream_t stream = nullptr) {
+    check(plora_store_write_pages(s_, a, host_src, bytes, mode, stream));
+  }
+  // promotion (engine.cpp:406-414) / eviction (engine.cpp:294-304)
+  void publish(AdapterKey a, plora_stream_t stream = nullptr) { check(plora_store_publish(s_, a, stream)); }
+  void retire(AdapterKey a, plora_stream_t stream = nullptr) { check(plora_store_retire(s_, a, stream)); }
+  bool is_published(AdapterKey a) const { return plora_store_is_published(s_, a) != 0; }
+
+  plora_store* handle() const { return s_; }
+
+ private:
+  plora_store* s_ = nullptr;
+};
+
+// A batch's tokens grouped by adapter (reused for every (layer, proj) call).
+class BatchPlan {
+ public:
+  BatchPlan(DeviceStore& store, const std::vector<std::int32_t>& token_adapter,
+            plora_stream_t stream = nullptr) {
+    check(plora_plan_create(store.handle(), token_adapter.data(),
+                            static_cast<std::uint32_t>(token_adapter.size()), stream, &p_));
+  }
+  ~BatchPlan() { plora_plan_destroy(p_); }
+  BatchPlan(const BatchPlan&) = delete;
+  BatchPlan& operator=(const BatchPlan&) = delete;
+  void update(const std::vector<std::int32_t>& token_adapter, plora_stream_t stream = nullptr) {
+    check(plora_plan_update(p_, token_adapter.data(), static_cast<std::uint32_t>(token_adapter.size()),
+                            stream));
+  }
+  plora_plan* handle() const { return p_; }
+
+ private:
+  plora_plan* p_ = nullptr;
+};
+
+// y += scale · (x · Aᵀ) · Bᵀ per token; device pointers, strides in elements.
+inline void bgmv(BatchPlan& plan, std::uint32_t layer, std::uint32_t proj, const void* x,
+                 std::uint64_t ldx, void* y, std::uint64_t ldy, float scale = 1.f,
+                 plora_stream_t stream = nullptr) {
+  check(plora_bgmv(plan.handle(), layer, proj, x, ldx, y, ldy, scale, stream));
+}
+inline void sgmv(BatchPlan& plan, std::uint32_t layer, std::uint32_t proj, const void* x,
+                 std::uint64_t ldx, void* y, std::uint64_t ldy, float scale = 1.f,
+                 plora_stream_t stream = nullptr) {
+  check(plora_sgmv(plan.handle(), layer, proj, x, ldx, y, ldy, scale, stream));
+}
+// every projection of a layer (they share x): decode / prefill
+inline void bgmv_layer(BatchPlan& plan, std::uint32_t layer, const void* x, std::uint64_t ldx,
+                       void* const* ys, const std::uint64_t* ldys, float scale = 1.f,
+                       plora_stream_t stream = nullptr) {
+  check(plora_bgmv_layer(plan.handle(), layer, x, ldx, ys, ldys, scale, stream));
+}
+inline void sgmv_layer(BatchPlan& plan, std::uint32_t layer, const void* x, std::uint64_t ldx,
+                       void* const* ys, const std::uint64_t* ldys, float scale = 1.f,
+                       plora_stream_t stream = nullptr) {
+  check(plora_sgmv_layer(plan.handle(), layer, x, ldx, ys, ldys, scale, stream));
+}
+// y = x · W0ᵀ + scale · (x · Aᵀ) · Bᵀ (base projection fused, prefill)
+inline void sgmv_fused(BatchPlan& plan, std::uint32_t layer, std::uint32_t proj, const void* x,
+                       std::uint64_t ldx, const void* w0, std::uint64_t ldw, void* y,
+                       std::uint64_t ldy, float scale = 1.f, plora_stream_t stream = nullptr) {
+  check(plora_sgmv_fused(plan.handle(), layer, proj, x, ldx, w0, ldw, y, ldy, scale, stream));
+}
+
 }  // namespace plora
