@@ -744,14 +744,15 @@ def run_cfg5(args):
 
 def run_cfg3f(args):
     """BASELINE configs[2] with the base projections fused in (SURVEY §8(f)
-    row 3): per (layer, proj) one plora_sgmv_fused call computes
+    row 3): per layer one plora_sgmv_fused_layer call computes, for q and v,
     y = x·W0ᵀ + scale·(x·Aᵀ)·Bᵀ for 32 segments × 512 tokens, r = 16/64/128,
     Llama-7B q/v (4096 -> 4096), 32 layers × 2 per step, one CUDA graph.
     Tensor-bound: the roofline is the measured dense bf16 peak."""
     import torch
 
     from paper_2512_20210_b200 import synth
-    from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, kernel_launch_count, sgmv_fused
+    from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, kernel_launch_count,
+                                            sgmv_fused_layer)
 
     dev = torch.device("cuda", 0)
     cfg = synth.cfg3(page_bytes=args.page_bytes)
@@ -772,10 +773,9 @@ def run_cfg3f(args):
             shape.d_in[p] ** 0.5).to(torch.bfloat16) for p in range(NP)] for _ in range(L)]
     ys = [torch.empty(L, T, shape.d_out[p], device=dev, dtype=torch.bfloat16) for p in range(NP)]
 
-    def step():
+    def step():  # per layer: one shrink for q and v (x read once), then a fused GEMM each
         for l in range(L):
-            for p in range(NP):
-                sgmv_fused(plan, l, p, x[l], w0[l][p], ys[p][l], 1.0)
+            sgmv_fused_layer(plan, l, x[l], w0[l], [ys[p][l] for p in range(NP)], 1.0)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -812,14 +812,15 @@ def run_cfg3f(args):
         "config": {"workload": ("cfg3 prefill with the base projection fused: y = x·W0ᵀ + "
                                 "(x·Aᵀ)·Bᵀ, 32 segments x 512 tokens, r=[16,64,128][s%3], "
                                 f"Llama-7B q/v 4096->4096, {L} layers x 2 calls per step "
-                                "(shrink + split reduction + fused tcgen05 GEMM per call)"),
+                                "(per layer: one shrink + split reduction for both projections, "
+                                "then one fused tcgen05 GEMM each)"),
                    "page_bytes": args.page_bytes, "cuda_graph": True,
                    "l2": "inputs > L2: 4 GiB of x, 2 GiB of base weights per step"},
         "gpu_launches": per_replay * K,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tpeak, "unit": "TFLOP/s",
                      "frac": achieved / tpeak, "traffic": None, "peak_kind": kind,
                      "flops_per_launch": flops, "avg_launch_us": call_ms * 1e3,
-                     "launch_time": "step time / calls per step (each call = 3 launches)"},
+                     "launch_time": "step time / (layer, proj) calls per step (a layer = 4 launches)"},
         "clocks": clk.summary(),
     }
     print(json.dumps(line))

@@ -305,6 +305,12 @@ int plora_sgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x
 int plora_sgmv_fused(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                      uint64_t x_stride, const void* w0, uint64_t w0_stride, void* y,
                      uint64_t y_stride, float scale, plora_stream_t stream);
+/* Every projection of `layer` (they share x): one shrink for both when their
+ * shapes allow (x read once), then one fused GEMM per projection.
+ * w0s[p] / w0_strides[p]: projection p's base weight [d_out, d_in]. */
+int plora_sgmv_fused_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x_stride,
+                           const void* const* w0s, const uint64_t* w0_strides, void* const* ys,
+                           const uint64_t* y_strides, float scale, plora_stream_t stream);
 
 /* ------------------- tensor-parallel decode (new; BASELINE cfg5) -----
  * The S-LoRA scheme for a column-parallel base projection (hidden-dim

@@ -189,6 +189,8 @@ _SIGS = {
     "plora_sgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
     "plora_sgmv_layer": (_int, [_vp, _u32, _vp, _u64, _P(_vp), _P(_u64), C.c_float, _vp]),
     "plora_sgmv_fused": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, _vp, _u64, C.c_float, _vp]),
+    "plora_sgmv_fused_layer": (_int, [_vp, _u32, _vp, _u64, _P(_vp), _P(_u64), _P(_vp), _P(_u64),
+                                      C.c_float, _vp]),
     "plora_engine_config_default": (None, [_P(plora_engine_config)]),
     "plora_engine_create": (_int, [_vp, _P(plora_engine_config), _P(_vp)]),
     "plora_engine_destroy": (None, [_vp]),

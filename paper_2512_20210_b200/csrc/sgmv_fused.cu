@@ -38,6 +38,8 @@ void check_io(const plora_plan* plan, uint32_t layer, uint32_t proj, const void*
               uint64_t x_stride, void* y, uint64_t y_stride);
 void sgmv_shrink_reduce(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                         uint64_t x_stride, float v_scale, cudaStream_t s);
+void sgmv_shrink_reduce_n(plora_plan* plan, uint32_t layer, const uint32_t* projs, uint32_t np,
+                          const void* x, uint64_t x_stride, float v_scale, cudaStream_t s);
 }  // namespace plora
 
 namespace {
@@ -319,57 +321,107 @@ __global__ void __launch_bounds__(kFThreads, 1)
 
 }  // namespace
 
+namespace {
+
+void check_fused(const plora_plan* plan, uint32_t proj, const void* w0, uint64_t w0_stride) {
+  const ModelGeom& g = plan->store->geom;
+  const uint32_t din = g.m.d_in[proj], dout = g.m.d_out[proj];
+  if (!w0) throw ValidationError("null base weight");
+  if (g.esize != 2) throw ValidationError("plora_sgmv_fused needs a bf16 store");
+  if (plan->max_rank > kMaxRank) throw ValidationError("plora_sgmv_fused: rank > 128");
+  if (din % kBK || dout % kBN)
+    throw ValidationError("plora_sgmv_fused needs d_in % 64 == 0 and d_out % 256 == 0");
+  if (w0_stride < din) throw ValidationError("base weight row stride < d_in");
+}
+
+// The fused GEMM of one projection; its V tiles start at tile row v_tile0 of
+// the V buffer (projection j of a joint shrink: j · n_tiles).
+void launch_fused(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x, uint64_t x_stride,
+                  const void* w0, uint64_t w0_stride, void* y, uint64_t y_stride, uint64_t v_tile0,
+                  cudaStream_t s) {
+  const plora_store& st = *plan->store;
+  const ModelGeom& g = st.geom;
+  const uint32_t din = g.m.d_in[proj], dout = g.m.d_out[proj];
+  CUtensorMap tmap_x, tmap_w, tmap_v, tmap_y;
+  make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kBK, kBM);
+  make_tmap_2d(&tmap_w, w0, din, dout, w0_stride * 2, kBK, kBN);
+  const char* vbase = plan->n_tiles ? plan->d_vbuf + v_tile0 * kBM * kMaxRank * 2 : static_cast<const char*>(x);
+  make_tmap_2d(&tmap_v, vbase, kMaxRank, std::max<uint64_t>(plan->n_tiles, 1) * kBM, kMaxRank * 2, kBK, kBM);
+  make_tmap_2d(&tmap_y, y, dout, plan->n_tokens, y_stride * 2, 64, kBM);
+  set_smem_once(reinterpret_cast<const void*>(sgmv_fused_kernel), static_cast<int>(FSmem::alloc));
+  FArgs a{};
+  a.arena = st.arena;
+  a.table = st.d_table;
+  a.tiles = plan->d_gtiles;
+  a.y = static_cast<char*>(y);
+  a.y_stride_b = y_stride * 2;
+  a.bt_mult = g.blk_mult(layer, proj) + din;  // Bᵀ follows A (r · d_in elements)
+  a.log2_page = st.log2_page;
+  a.d_in = din;
+  a.d_out = dout;
+  a.nb = dout / kBN;
+  a.n_items = static_cast<uint32_t>(plan->gtiles.size()) * a.nb;
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min<uint32_t>(static_cast<uint32_t>(st.num_sms), a.n_items));
+  cfg.blockDim = dim3(kFThreads);
+  cfg.dynamicSmemBytes = FSmem::alloc;
+  cfg.stream = s;
+  cfg.attrs = pdl;
+  cfg.numAttrs = 1;
+  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_fused_kernel, a, tmap_x, tmap_w, tmap_v, tmap_y));
+  count_launch();
+}
+
+}  // namespace
+
 extern "C" int plora_sgmv_fused(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                                 uint64_t x_stride, const void* w0, uint64_t w0_stride, void* y,
                                 uint64_t y_stride, float scale, plora_stream_t stream) {
   return guard([&] {
     if (!plan) throw ValidationError("null plan");
     check_io(plan, layer, proj, x, x_stride, y, y_stride);
-    if (!w0) throw ValidationError("null base weight");
-    const plora_store& st = *plan->store;
-    const ModelGeom& g = st.geom;
-    const uint32_t din = g.m.d_in[proj], dout = g.m.d_out[proj];
-    if (g.esize != 2) throw ValidationError("plora_sgmv_fused needs a bf16 store");
-    if (plan->max_rank > kMaxRank) throw ValidationError("plora_sgmv_fused: rank > 128");
-    if (din % kBK || dout % kBN)
-      throw ValidationError("plora_sgmv_fused needs d_in % 64 == 0 and d_out % 256 == 0");
-    if (w0_stride < din) throw ValidationError("base weight row stride < d_in");
+    check_fused(plan, proj, w0, w0_stride);
     if (plan->gtiles.empty()) return 0;
-    DeviceCtx ctx(st.device);
+    DeviceCtx ctx(plan->store->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (plan->n_tiles) sgmv_shrink_reduce(plan, layer, proj, x, x_stride, scale, s);
+    launch_fused(plan, layer, proj, x, x_stride, w0, w0_stride, y, y_stride, 0, s);
+    return 0;
+  });
+}
 
-    CUtensorMap tmap_x, tmap_w, tmap_v, tmap_y;
-    make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kBK, kBM);
-    make_tmap_2d(&tmap_w, w0, din, dout, w0_stride * 2, kBK, kBN);
-    make_tmap_2d(&tmap_v, plan->n_tiles ? plan->d_vbuf : x, kMaxRank,
-                 std::max<uint64_t>(plan->n_tiles, 1) * kBM, kMaxRank * 2, kBK, kBM);
-    make_tmap_2d(&tmap_y, y, dout, plan->n_tokens, y_stride * 2, 64, kBM);
-    set_smem_once(reinterpret_cast<const void*>(sgmv_fused_kernel), static_cast<int>(FSmem::alloc));
-    FArgs a{};
-    a.arena = st.arena;
-    a.table = st.d_table;
-    a.tiles = plan->d_gtiles;
-    a.y = static_cast<char*>(y);
-    a.y_stride_b = y_stride * 2;
-    a.bt_mult = g.blk_mult(layer, proj) + din;  // Bᵀ follows A (r · d_in elements)
-    a.log2_page = st.log2_page;
-    a.d_in = din;
-    a.d_out = dout;
-    a.nb = dout / kBN;
-    a.n_items = static_cast<uint32_t>(plan->gtiles.size()) * a.nb;
-    cudaLaunchAttribute pdl[1];
-    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(std::min<uint32_t>(static_cast<uint32_t>(st.num_sms), a.n_items));
-    cfg.blockDim = dim3(kFThreads);
-    cfg.dynamicSmemBytes = FSmem::alloc;
-    cfg.stream = s;
-    cfg.attrs = pdl;
-    cfg.numAttrs = 1;
-    PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_fused_kernel, a, tmap_x, tmap_w, tmap_v, tmap_y));
-    count_launch();
+extern "C" int plora_sgmv_fused_layer(plora_plan* plan, uint32_t layer, const void* x,
+                                      uint64_t x_stride, const void* const* w0s,
+                                      const uint64_t* w0_strides, void* const* ys,
+                                      const uint64_t* y_strides, float scale, plora_stream_t stream) {
+  return guard([&] {
+    if (!plan) throw ValidationError("null plan");
+    if (!w0s || !w0_strides || !ys || !y_strides) throw ValidationError("null weight / output arrays");
+    const ModelGeom& g = plan->store->geom;
+    const uint32_t np = g.m.n_proj;
+    for (uint32_t j = 0; j < np; ++j) {
+      check_io(plan, layer, j, x, x_stride, ys[j], y_strides[j]);
+      check_fused(plan, j, w0s[j], w0_strides[j]);
+    }
+    if (plan->gtiles.empty()) return 0;
+    DeviceCtx ctx(plan->store->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool joint = np == 2 && plan->ssched_layer.splits != 0 && g.m.d_in[1] == g.m.d_in[0];
+    if (joint) {  // one shrink reads x once for both projections' V
+      const uint32_t projs[2] = {0, 1};
+      if (plan->n_tiles) sgmv_shrink_reduce_n(plan, layer, projs, 2, x, x_stride, scale, s);
+      for (uint32_t j = 0; j < 2; ++j)
+        launch_fused(plan, layer, j, x, x_stride, w0s[j], w0_strides[j], ys[j], y_strides[j],
+                     static_cast<uint64_t>(j) * plan->n_tiles, s);
+      return 0;
+    }
+    for (uint32_t j = 0; j < np; ++j) {
+      if (plan->n_tiles) sgmv_shrink_reduce(plan, layer, j, x, x_stride, scale, s);
+      launch_fused(plan, layer, j, x, x_stride, w0s[j], w0_strides[j], ys[j], y_strides[j], 0, s);
+    }
     return 0;
   });
 }

@@ -315,5 +315,30 @@ def sgmv_fused(plan: BatchPlan, layer: int, proj: int, x: torch.Tensor, w0: torc
     return y
 
 
+def sgmv_fused_layer(plan: BatchPlan, layer: int, x: torch.Tensor, w0s: Sequence[torch.Tensor],
+                     ys: Sequence[torch.Tensor], scale: float = 1.0,
+                     stream: int | None = None) -> Sequence[torch.Tensor]:
+    """ys[p] = x · W0_pᵀ + scale · (x · A_pᵀ) · B_pᵀ for every projection of
+    `layer`: one shrink for all (x read once), then one fused GEMM each."""
+    shape = plan.store.shape
+    if len(ys) != shape.n_proj or len(w0s) != shape.n_proj:
+        raise N.ValidationError(f"sgmv_fused_layer needs {shape.n_proj} weights and outputs")
+    for p, (w0, y) in enumerate(zip(w0s, ys)):
+        _check_io(plan, p, x, y)
+        if not w0.is_cuda or w0.dtype != torch.bfloat16 or w0.dim() != 2 or w0.stride(1) != 1:
+            raise N.ValidationError("w0 must be a 2-D bf16 CUDA tensor with unit column stride")
+        if w0.shape[0] != y.shape[1] or w0.shape[1] != x.shape[1]:
+            raise N.ValidationError("w0 must be [d_out, d_in]")
+    n = shape.n_proj
+    wp = (C.c_void_p * n)(*[w.data_ptr() for w in w0s])
+    ws = (C.c_uint64 * n)(*[w.stride(0) for w in w0s])
+    yp = (C.c_void_p * n)(*[y.data_ptr() for y in ys])
+    yst = (C.c_uint64 * n)(*[y.stride(0) for y in ys])
+    s = current_stream_handle(x.device) if stream is None else stream
+    N.check(N.lib().plora_sgmv_fused_layer(plan.handle, layer, x.data_ptr(), x.stride(0), wp, ws, yp,
+                                           yst, scale, s))
+    return ys
+
+
 def kernel_launch_count() -> int:
     return N.lib().plora_kernel_launch_count()

@@ -7,7 +7,8 @@ import torch
 
 from lora_harness import TOL_BF16, Setup, rel_err, to_f32
 from paper_2512_20210_b200 import _native as N, synth
-from paper_2512_20210_b200.lora import BatchPlan, ModelShape, kernel_launch_count, sgmv_fused
+from paper_2512_20210_b200.lora import (BatchPlan, ModelShape, kernel_launch_count, sgmv_fused,
+                                        sgmv_fused_layer)
 
 pytestmark = pytest.mark.gpu
 
@@ -110,3 +111,25 @@ def test_sgmv_fused_small_pages(cuda, page_bytes):
         x, y, _ = _run(s, ta, 1, proj, w0, 0.5, proj)
         ref = _delta(s, ta, 1, proj, x, 0.5)
         assert rel_err(y, ref.numpy()) <= TOL_BF16, proj
+
+
+def test_sgmv_fused_layer_matches_per_projection(cuda):
+    """plora_sgmv_fused_layer (one shrink for both projections, then one fused
+    GEMM each) against torch fp32 base GEMMs plus the oracle's deltas."""
+    shape = ModelShape(2, (1024, 1024), (1024, 1024), torch.bfloat16)
+    cfg = synth.DecodeConfig("fused_layer", shape, [16, 64, 128, 5], 1, 2048)
+    s = Setup(cfg)
+    runs = [(0, 200), (1, 128), (-1, 3), (2, 150), (3, 20)]
+    ta = np.concatenate([np.full(n, a, np.int32) for a, n in runs])
+    T = len(ta)
+    g = torch.Generator().manual_seed(77)
+    w0 = [(torch.randn(1024, 1024, generator=g) / 32).to(torch.bfloat16) for _ in range(2)]
+    x = synth.activations(T, 1024, shape.dtype, "x", salt=9)
+    ys = [torch.empty(T, 1024, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+    n0 = kernel_launch_count()
+    sgmv_fused_layer(BatchPlan(s.store, ta), 1, x.cuda(), [w.cuda() for w in w0], ys, 0.5)
+    torch.cuda.synchronize()
+    assert kernel_launch_count() - n0 == 4  # joint shrink + reduction + two fused GEMMs
+    for p in range(2):
+        ref = x.float() @ w0[p].float().t() + _delta(s, ta, 1, p, x, 0.5)
+        assert rel_err(ys[p].cpu(), ref.numpy()) <= TOL_BF16, p
