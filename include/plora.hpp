@@ -218,4 +218,12 @@ inline void sgmv_fused(BatchPlan& plan, std::uint32_t layer, std::uint32_t proj,
   check(plora_sgmv_fused(plan.handle(), layer, proj, x, ldx, w0, ldw, y, ldy, scale, stream));
 }
 
+// every projection of a layer with its base weight (x read once by the shrink)
+inline void sgmv_fused_layer(BatchPlan& plan, std::uint32_t layer, const void* x, std::uint64_t ldx,
+                             const void* const* w0s, const std::uint64_t* ldws, void* const* ys,
+                             const std::uint64_t* ldys, float scale = 1.f,
+                             plora_stream_t stream = nullptr) {
+  check(plora_sgmv_fused_layer(plan.handle(), layer, x, ldx, w0s, ldws, ys, ldys, scale, stream));
+}
+
 }  // namespace plora
