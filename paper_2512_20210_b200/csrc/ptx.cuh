@@ -84,6 +84,23 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
 }
 
 // 2-D TMA tensor tile load (tensor map in param/const space).
+// 2-D TMA gather of four rows r0..r3 (the tensor map's box is {cols, 1});
+// they land in four consecutive smem rows (swizzled by their smem address).
+__device__ __forceinline__ void tma_gather4(void* dst, const void* tmap, int32_t c0, int32_t r0,
+                                            int32_t r1, int32_t r2, int32_t r3, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Expect `bytes` more transaction bytes on `bar` without arriving.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int32_t c0, int32_t c1,
                                             uint64_t* bar) {
   asm volatile(

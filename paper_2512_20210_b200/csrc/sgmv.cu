@@ -103,6 +103,7 @@ struct ShrinkArgs {
   uint32_t d_in;
   uint32_t splits;
   uint32_t dbg;  // diagnostics (plora_debug_set_sgmv_flags): 1 no A gather, 2 no MMA, 4 no x load, 16 no epilogue
+  uint32_t g4;   // pages >= 256 B: A rows by TMA gather4 over the arena viewed as 128-byte rows
 };
 
 struct SSmem {
@@ -141,7 +142,8 @@ __device__ __forceinline__ UnitInfo unit_info(const SgmvItem* it) {
 __device__ __forceinline__ uint32_t part_swm(uint32_t pw4) { return min(8u, pw4 & (0u - pw4)) - 1u; }
 
 __global__ void __launch_bounds__(kSThreads, 1)
-    sgmv_shrink_kernel(const ShrinkArgs p, const __grid_constant__ CUtensorMap tmap_x) {
+    sgmv_shrink_kernel(const ShrinkArgs p, const __grid_constant__ CUtensorMap tmap_x,
+                       const __grid_constant__ CUtensorMap tmap_arena) {
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SSmem::bars);
@@ -239,7 +241,28 @@ __global__ void __launch_bounds__(kSThreads, 1)
           }
         }
         ptx::mbar_wait(&empty[st], ph ^ 1u);
-        if (n < u.r16 && !(p.dbg & 1u)) {
+        // Groups of four real rows go by one TMA gather4 (its row indices
+        // collected by the group's first lane); padding rows and the rows of
+        // a partial last group by 16-byte cp.async.
+        const bool g4 = p.g4 && (n | 3u) < u.r;
+        if (p.g4 && !(p.dbg & 1u)) {
+#pragma unroll
+          for (uint32_t q = 0; q < 2; ++q) {
+            if (q >= p.np) break;
+            const uint64_t off = off0[q] + kc * kChunkK * 2;
+            const int32_t row = static_cast<int32_t>(((static_cast<uint64_t>(e_cur[q]) << p.log2_page) +
+                                                      (off & pmask)) >> 7);
+            const uint32_t l0 = lane & ~3u;
+            const int32_t r0 = __shfl_sync(0xffffffffu, row, l0), r1 = __shfl_sync(0xffffffffu, row, l0 + 1);
+            const int32_t r2 = __shfl_sync(0xffffffffu, row, l0 + 2), r3 = __shfl_sync(0xffffffffu, row, l0 + 3);
+            if (g4 && (lane & 3u) == 0) {
+              char* wdst = smem + SSmem::stages + st * kSStageBytes + (u.nt + q) * kTileM * kChunkK * 2;
+              ptx::mbar_expect_tx(&full[st], 4 * kChunkK * 2);
+              ptx::tma_gather4(wdst + n * kChunkK * 2, &tmap_arena, 0, r0, r1, r2, r3, &full[st]);
+            }
+          }
+        }
+        if (n < u.r16 && !g4 && !(p.dbg & 1u)) {
 #pragma unroll
           for (uint32_t q = 0; q < 2; ++q) {
             if (q >= p.np) break;
@@ -664,8 +687,12 @@ void sgmv_shrink_reduce_n(plora_plan* plan, uint32_t layer, const uint32_t* proj
   const ModelGeom& g = st.geom;
   const uint32_t din = g.m.d_in[projs[0]];
   const SgmvSched& sc = np == 1 ? plan->ssched[projs[0]] : plan->ssched_layer;
-  CUtensorMap tmap_x;
+  CUtensorMap tmap_x, tmap_arena;
   make_tmap_2d(&tmap_x, x, din, plan->n_tokens, x_stride * 2, kChunkK, kTileM);
+  // the arena as rows of 128 bytes (64 bf16): TMA gather4 of A row segments
+  const uint64_t arena_rows = (static_cast<uint64_t>(st.pool->pool.total_pages()) << st.log2_page) >> 7;
+  const bool g4 = st.log2_page >= 8 && arena_rows < (1ull << 31);
+  make_tmap_2d(&tmap_arena, st.arena, kChunkK, g4 ? arena_rows : 1, kChunkK * 2, kChunkK, 1);
   set_smem_once(reinterpret_cast<const void*>(sgmv_shrink_kernel), static_cast<int>(SSmem::alloc));
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -684,6 +711,7 @@ void sgmv_shrink_reduce_n(plora_plan* plan, uint32_t layer, const uint32_t* proj
   sa.d_in = din;
   sa.splits = sc.splits;
   sa.dbg = g_sgmv_dbg;
+  sa.g4 = g4 ? 1u : 0u;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(sc.ctas);
   cfg.blockDim = dim3(kSThreads);
@@ -691,7 +719,7 @@ void sgmv_shrink_reduce_n(plora_plan* plan, uint32_t layer, const uint32_t* proj
   cfg.stream = s;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_shrink_kernel, sa, tmap_x));
+  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_shrink_kernel, sa, tmap_x, tmap_arena));
   count_launch();
   if (!(g_sgmv_dbg & 32u)) {
     ReduceArgs ra{plan->d_tiles, plan->d_vpart, reinterpret_cast<__nv_bfloat16*>(plan->d_vbuf),
