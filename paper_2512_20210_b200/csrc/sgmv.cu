@@ -466,6 +466,7 @@ struct ExpandArgs {
   uint32_t ngroups;  // column groups per tile
   float scale;
   uint32_t dbg;  // diagnostics: 64 no y reduce-add, 128 no Bᵀ gather, 256 no MMA, 512 prologue only
+  uint32_t g4;   // pages >= 256 B: Bᵀ rows by TMA gather4 (see ShrinkArgs::g4)
 };
 
 struct ESmem {  // ~97 KB: two expand CTAs per SM
@@ -483,7 +484,8 @@ struct ESmem {  // ~97 KB: two expand CTAs per SM
 __global__ void __launch_bounds__(kEThreads, 2)
     sgmv_expand_kernel(const ExpandArgs p, const __grid_constant__ CUtensorMap tmap_y0,
                        const __grid_constant__ CUtensorMap tmap_y1,
-                       const __grid_constant__ CUtensorMap tmap_v) {
+                       const __grid_constant__ CUtensorMap tmap_v,
+                       const __grid_constant__ CUtensorMap tmap_arena) {
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* v_full = reinterpret_cast<uint64_t*>(smem + ESmem::bars);
@@ -576,10 +578,29 @@ __global__ void __launch_bounds__(kEThreads, 2)
       }
       ptx::mbar_wait(&b_empty[st], ph ^ 1u);
       char* bs = smem + ESmem::b + st * 16384;
+      // groups of four real rows by TMA gather4 (row indices collected by the
+      // group's first lane), the rest by 16-byte cp.async
+      bool g4[2];
+#pragma unroll
+      for (uint32_t h = 0; h < 2; ++h) {
+        const uint32_t j = wt + h * kEGather;
+        g4[h] = p.g4 && (j | 3u) < r;
+        if (p.g4 && !(p.dbg & 128u)) {
+          const int32_t row = static_cast<int32_t>(
+              ((static_cast<uint64_t>(e_cur[h]) << p.log2_page) + (row_off(j, b) & pmask)) >> 7);
+          const uint32_t l0 = lane & ~3u;
+          const int32_t r0 = __shfl_sync(0xffffffffu, row, l0), r1 = __shfl_sync(0xffffffffu, row, l0 + 1);
+          const int32_t r2 = __shfl_sync(0xffffffffu, row, l0 + 2), r3 = __shfl_sync(0xffffffffu, row, l0 + 3);
+          if (g4[h] && (lane & 3u) == 0) {
+            ptx::mbar_expect_tx(&b_full[st], 4 * kEBlockN * 2);
+            ptx::tma_gather4(bs + j * kEBlockN * 2, &tmap_arena, 0, r0, r1, r2, r3, &b_full[st]);
+          }
+        }
+      }
 #pragma unroll
       for (uint32_t h = 0; h < 2; ++h) {  // rows wt and wt + 96
         const uint32_t j = wt + h * kEGather;
-        if (j >= r16 || (p.dbg & 128u)) continue;
+        if (j >= r16 || g4[h] || (p.dbg & 128u)) continue;
         const uint64_t off = row_off(j, b);
         const char* base = p.arena + (static_cast<uint64_t>(e_cur[h]) << p.log2_page) + (off & pmask);
 #pragma unroll
@@ -770,6 +791,11 @@ static void sgmv_run(plora_plan* plan, uint32_t layer, const uint32_t* projs, ui
   ea.ngroups = (dout / kEBlockN + kGroupBlocks - 1) / kGroupBlocks;
   ea.scale = scale;
   ea.dbg = g_sgmv_dbg;
+  CUtensorMap tmap_arena;
+  const uint64_t arena_rows = (static_cast<uint64_t>(st.pool->pool.total_pages()) << st.log2_page) >> 7;
+  const bool g4 = st.log2_page >= 8 && arena_rows < (1ull << 31);
+  make_tmap_2d(&tmap_arena, st.arena, kEBlockN, g4 ? arena_rows : 1, kEBlockN * 2, kEBlockN, 1);
+  ea.g4 = g4 ? 1u : 0u;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(np * plan->n_tiles * ea.ngroups);
   cfg.blockDim = dim3(kEThreads);
@@ -777,7 +803,7 @@ static void sgmv_run(plora_plan* plan, uint32_t layer, const uint32_t* projs, ui
   cfg.stream = s;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y[0], tmap_y[1], tmap_v));
+  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y[0], tmap_y[1], tmap_v, tmap_arena));
   count_launch();
 }
 
