@@ -66,6 +66,7 @@ struct FArgs {
   uint32_t log2_page;
   uint32_t d_in, d_out;
   uint32_t n_items, nb;  // items = tiles × nb column blocks, tile-major
+  uint32_t g4;           // Bᵀ rows by TMA gather4 over the arena viewed as 128-byte rows
 };
 
 struct FSmem {
@@ -92,7 +93,8 @@ __global__ void __launch_bounds__(kFThreads, 1)
     sgmv_fused_kernel(const FArgs p, const __grid_constant__ CUtensorMap tmap_x,
                       const __grid_constant__ CUtensorMap tmap_w,
                       const __grid_constant__ CUtensorMap tmap_v,
-                      const __grid_constant__ CUtensorMap tmap_y) {
+                      const __grid_constant__ CUtensorMap tmap_y,
+                      const __grid_constant__ CUtensorMap tmap_arena) {
   extern __shared__ char smem_raw[];
   char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + FSmem::bars);
@@ -158,7 +160,9 @@ __global__ void __launch_bounds__(kFThreads, 1)
   } else if (warp <= 4) {
     // ------------------------------------------- Bᵀ gathers (LoRA K-steps)
     // A LoRA chunk is 64 rank rows × 256 columns: piece (row, group) = one
-    // 128-byte row segment of a 64-column group, two pieces per thread.
+    // 128-byte row segment of a 64-column group, two pieces per thread; four
+    // consecutive lanes hold four consecutive rows of one group, so with
+    // pages >= 512 B a group of real rows goes by one TMA gather4.
     // The threads wait for every chunk's slot, base chunks included: a parity
     // wait must never run two ring laps ahead of the barrier.  Base chunks
     // arrive nowhere.
@@ -178,16 +182,36 @@ __global__ void __launch_bounds__(kFThreads, 1)
         uint64_t off[2];
 #pragma unroll
         for (uint32_t h = 0; h < 2; ++h) {  // page lookups before the slot wait
-          const uint32_t pc = tid + h * kFGather, krow = pc >> 2, grp = pc & 3, j = l * kBK + krow;
+          const uint32_t pc = tid + h * kFGather, krow = (pc & 3) + 4 * (pc >> 4), grp = (pc >> 2) & 3;
+          const uint32_t j = l * kBK + krow;
           off[h] = bt + (static_cast<uint64_t>(j) * p.d_out + n0 + grp * 64) * 2;
           phys[h] = (fast && j < r) ? __ldg(p.table + t.table_off + static_cast<uint32_t>(off[h] >> p.log2_page)) : 0u;
         }
         ptx::mbar_wait(&empty[st], ph ^ 1u);
         char* bs = smem + FSmem::stages + st * kFStageBytes + kXBytes;
+        bool g4[2];
 #pragma unroll
         for (uint32_t h = 0; h < 2; ++h) {
-          const uint32_t pc = tid + h * kFGather, krow = pc >> 2, grp = pc & 3, j = l * kBK + krow;
-          if (j >= r16) continue;  // the MMA stops at r16
+          const uint32_t pc = tid + h * kFGather, krow = (pc & 3) + 4 * (pc >> 4), grp = (pc >> 2) & 3;
+          const uint32_t j = l * kBK + krow;
+          g4[h] = p.g4 && fast && (j | 3u) < r;
+          if (p.g4 && fast) {
+            const int32_t row = static_cast<int32_t>(
+                ((static_cast<uint64_t>(phys[h]) << p.log2_page) + (off[h] & ((1ull << p.log2_page) - 1))) >> 7);
+            const uint32_t l0 = lane & ~3u;
+            const int32_t r0 = __shfl_sync(0xffffffffu, row, l0), r1 = __shfl_sync(0xffffffffu, row, l0 + 1);
+            const int32_t r2 = __shfl_sync(0xffffffffu, row, l0 + 2), r3 = __shfl_sync(0xffffffffu, row, l0 + 3);
+            if (g4[h] && (lane & 3u) == 0) {
+              ptx::mbar_expect_tx(&bfull[st], 4 * 128);
+              ptx::tma_gather4(bs + grp * 8192 + krow * 128, &tmap_arena, 0, r0, r1, r2, r3, &bfull[st]);
+            }
+          }
+        }
+#pragma unroll
+        for (uint32_t h = 0; h < 2; ++h) {
+          const uint32_t pc = tid + h * kFGather, krow = (pc & 3) + 4 * (pc >> 4), grp = (pc >> 2) & 3;
+          const uint32_t j = l * kBK + krow;
+          if (j >= r16 || g4[h]) continue;  // the MMA stops at r16
           char* dst = bs + grp * 8192;
           const char* base = p.arena + (static_cast<uint64_t>(phys[h]) << p.log2_page) +
                              (off[h] & ((1ull << p.log2_page) - 1));
@@ -361,6 +385,11 @@ void launch_fused(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x
   a.d_out = dout;
   a.nb = dout / kBN;
   a.n_items = static_cast<uint32_t>(plan->gtiles.size()) * a.nb;
+  CUtensorMap tmap_arena;
+  const uint64_t arena_rows = (static_cast<uint64_t>(st.pool->pool.total_pages()) << st.log2_page) >> 7;
+  const bool g4 = st.log2_page >= 9 && arena_rows < (1ull << 31);
+  make_tmap_2d(&tmap_arena, st.arena, 64, g4 ? arena_rows : 1, 128, 64, 1);
+  a.g4 = g4 ? 1u : 0u;
   cudaLaunchAttribute pdl[1];
   pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   pdl[0].val.programmaticStreamSerializationAllowed = 1;
@@ -371,7 +400,7 @@ void launch_fused(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x
   cfg.stream = s;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_fused_kernel, a, tmap_x, tmap_w, tmap_v, tmap_y));
+  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_fused_kernel, a, tmap_x, tmap_w, tmap_v, tmap_y, tmap_arena));
   count_launch();
 }
 
