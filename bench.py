@@ -115,82 +115,54 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- CPU arms
-class CpuOracle:
-    """The CPU oracle (port of the paged LoRA apply, all host threads) on cfg2
-    per-call shapes: a 2-layer image of the cfg2 catalog (per-call work is
-    identical to the 32-layer model; only the called block is read)."""
-
-    def __init__(self, nthreads: int):
-        import torch
-        from oracle import lora as OL
-        from paper_2512_20210_b200 import synth
-        self.OL = OL
-        cfg = synth.cfg2(n_layers=2)
-        pool = synth.build_pool(cfg)
-        self.P = cfg.page_bytes
-        self.arena = np.zeros(pool.total_pages() * self.P, np.uint8)
-        for a, r in enumerate(cfg.ranks):
-            img = synth.adapter_image(cfg.shape, r, a).view(torch.int16).numpy().view(np.uint16)
-            OL.scatter_pages(self.arena, self.P, pool.table(a), img)
-        self.tables = {a: pool.table(a) for a in range(cfg.n_adapters)}
-        self.m = OL.model(2, cfg.shape.d_in, cfg.shape.d_out, 2)
-        self.ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
-        bits = lambda t: t.view(torch.int16).numpy().view(np.uint16).copy()  # noqa: E731
-        self.x = bits(synth.activations(len(self.ta), 4096, torch.bfloat16, "x"))
-        self.y = bits(synth.activations(len(self.ta), 4096, torch.bfloat16, "y"))
-        self.ranks = dict(enumerate(cfg.ranks))
-        self.nthreads = nthreads
-        self.n = 0
-
-    def call(self):
-        self.OL.paged_lora_apply(self.m, self.arena, self.P, self.tables, self.ranks, self.n % 2,
-                                 (self.n // 2) % 2, self.x, self.y, self.ta, nthreads=self.nthreads)
-        self.n += 1
-
-    def sample(self, target_s: float, max_calls: int = 64):
-        """Seconds per call over a bounded sample; returns (s/call, calls)."""
-        n, t0 = 0, time.perf_counter()
-        while n < max_calls:
-            self.call()
-            n += 1
-            if time.perf_counter() - t0 >= target_s:
-                break
-        return (time.perf_counter() - t0) / n, n
+def cfg2_config(page_bytes: int, world: int) -> dict:
+    """The workload both arms print (identical dict: the driver compares them)."""
+    return {"workload": ("cfg2 decode BGMV: 256 tokens / 128 adapters per GPU, "
+                         "r=[8,16,32,64][a%4], Llama-7B q/v (32 layers x 2 projections "
+                         "per step)"),
+            "page_bytes": page_bytes, "tokens_per_step_per_gpu": 256,
+            "parallelism": f"request-sharded x{world} (no collective)",
+            "l2": "inputs > L2: 3.84 GB of adapter pages + 192 MiB activations per step"}
 
 
 def run_reference(args):
-    """--impl reference: the reference CPU path on this box's host cores."""
+    """--impl reference: the reference-side CPU path of the decode step on this
+    box's host cores — oracle/cpu_arm.py: every page table from the
+    reference's own PagePool (oracle/_ref/libref.so), the paged LoRA apply by
+    the C restatement with all host threads, all 64 (layer, proj) calls of
+    every step (no extrapolation).  The product package is never imported."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import cpu_arm
     nthreads = os.cpu_count() or 1
-    cpu = CpuOracle(nthreads)
-    # each step = a bounded sample of the workload: `calls_per_step` (layer, proj)
-    # calls, extrapolated to the 64-call decode step
-    per_call, _ = cpu.sample(2.0, max_calls=2)  # probe (also the first warm-up)
-    calls_per_step = max(1, min(16, int(4.0 / max(per_call, 1e-6))))
+    t0 = time.perf_counter()
+    cpu = cpu_arm.CpuDecodeStep(n_layers=32, page_bytes=args.page_bytes, nthreads=nthreads)
+    setup_s = time.perf_counter() - t0
     for _ in range(args.warmup):
-        cpu.call()
+        cpu.step()
     times = []
     for _ in range(args.steps):
-        t, n = cpu.sample(1e9, max_calls=calls_per_step)
-        times.append(t)
-    per_call = statistics.mean(times)
-    value = 256 / (per_call * 64)
-    sample = (f"cfg2 per-call shape (256 tok, 128 adapters, r in 8..64, 2 KiB pages): "
-              f"{calls_per_step} (layer,proj) calls per step, extrapolated to the 64-call step")
+        t = time.perf_counter()
+        cpu.step()
+        times.append(time.perf_counter() - t)
+    step_s = statistics.mean(times)
+    value = cpu.n_tokens / step_s
+    sample = (f"the full cfg2 decode step: 64 (layer, proj) calls over the 32-layer catalog "
+              f"(3.84 GB of 2 KiB pages laid out by the reference PagePool), every step")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_call * 64 * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "cfg2 decode BGMV: 256 tokens / 128 adapters, r=[8,16,32,64], "
-                               "Llama-7B q/v (32 layers x 2), 2 KiB pages"},
+        "config": cfg2_config(args.page_bytes, 1),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nthreads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_arm.cpu_model_name()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "the reference ships no LoRA arithmetic (SPEC.md:70,341); the CPU arm is the "
-                "oracle port reading weights through reference-identical page tables",
+        "setup_s": setup_s,
+        "note": "the reference ships no LoRA arithmetic (SPEC.md:70,341): the CPU arm is the "
+                "oracle port (oracle/lora_oracle.c) reading weights through page tables made by "
+                "the reference's own PagePool (oracle/_ref/libref.so); libplora.so is not loaded",
     }
     print(json.dumps(line))
 
@@ -414,10 +386,14 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not prefill:
+        from oracle import cpu_arm
         nthreads = os.cpu_count() or 1
-        per_call_s, n = CpuOracle(nthreads).sample(args.cpu_sample_s)
+        per_call_s, n = cpu_arm.CpuDecodeStep(n_layers=2, nthreads=nthreads).sample_calls(
+            args.cpu_sample_s)
         cpu = {"value": T / (per_call_s * L * NP), "unit": UNIT, "cores": nthreads, "kind": "port",
-               "sample": f"{n} cfg2 (layer,proj) calls of the CPU oracle, extrapolated to the "
+               "cpu_model": cpu_arm.cpu_model_name(),
+               "sample": f"{n} cfg2 (layer,proj) calls of the CPU oracle over reference-PagePool "
+                         f"tables (2-layer catalog: identical per-call work), scaled to the "
                          f"64-call step ({per_call_s * 1e3:.1f} ms/call)"}
 
     if world > 1:
@@ -429,20 +405,14 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": max(args.warmup, 3), "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": ("cfg3 prefill SGMV (tcgen05): 32 segments x 512 tokens per GPU, "
-                                "r=[16,64,128][s%3], Llama-7B q/v (32 layers x 2 projections "
-                                "per step)")
-                               if prefill else
-                               ("cfg2 decode BGMV: 256 tokens / 128 adapters per GPU, "
-                                "r=[8,16,32,64][a%4], Llama-7B q/v (32 layers x 2 projections "
-                                "per step)"),
-                   "page_bytes": args.page_bytes, "tokens_per_step_per_gpu": T,
-                   "parallelism": f"request-sharded x{world} (no collective)",
-                   "cuda_graph": graph is not None,
-                   "launches_per_layer": LPS,
-                   "l2": ("inputs > L2: 2.1 GiB of adapter pages + 12 GiB activations per step"
-                          if prefill else
-                          "inputs > L2: 3.84 GB of adapter pages + 192 MiB activations per step")},
+        "config": ({"workload": ("cfg3 prefill SGMV (tcgen05): 32 segments x 512 tokens per GPU, "
+                                 "r=[16,64,128][s%3], Llama-7B q/v (32 layers x 2 projections "
+                                 "per step)"),
+                    "page_bytes": args.page_bytes, "tokens_per_step_per_gpu": T,
+                    "parallelism": f"request-sharded x{world} (no collective)",
+                    "l2": "inputs > L2: 2.1 GiB of adapter pages + 12 GiB activations per step"}
+                   if prefill else cfg2_config(args.page_bytes, world)),
+        "impl_detail": {"cuda_graph": graph is not None, "launches_per_layer": LPS},
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

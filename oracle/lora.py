@@ -90,29 +90,39 @@ def gather_pages(arena: np.ndarray, page_bytes: int, entries, nbytes: int) -> np
     return out
 
 
+class PreparedTables:
+    """Page tables flattened once for repeated calls: entries, per-adapter
+    offsets into them, ranks."""
+
+    def __init__(self, tables: dict[int, list[int]], ranks: dict[int, int]):
+        self.n_adapters = max(list(ranks) + [-1]) + 1
+        self.offs = np.zeros(self.n_adapters, np.uint64)
+        self.rk = np.zeros(self.n_adapters, np.uint32)
+        parts, pos = [], 0
+        for a in range(self.n_adapters):
+            self.offs[a] = pos
+            if a in tables:
+                t = np.asarray(tables[a], np.uint32)
+                parts.append(t)
+                pos += len(t)
+                self.rk[a] = ranks[a]
+        self.ent = np.ascontiguousarray(np.concatenate(parts) if parts else np.zeros(1, np.uint32))
+
+
 def paged_lora_apply(m: OracleModel, arena: np.ndarray, page_bytes: int,
-                     tables: dict[int, list[int]], ranks: dict[int, int], layer: int, proj: int,
+                     tables, ranks: dict[int, int] | None, layer: int, proj: int,
                      x: np.ndarray, y: np.ndarray, token_adapter, scale: float = 1.0,
                      v_bf16: bool = False, nthreads: int = 1) -> np.ndarray:
     """Updates y in place (and returns it).  x/y: uint16 (bf16 bits) when
-    m.esize == 2, float32 when 4; rows = tokens."""
-    n_adapters = max(list(ranks) + [-1]) + 1
-    offs = np.zeros(n_adapters, np.uint64)
-    rk = np.zeros(n_adapters, np.uint32)
-    flat = []
-    pos = 0
-    for a in range(n_adapters):
-        offs[a] = pos
-        if a in tables:
-            flat.extend(tables[a])
-            pos += len(tables[a])
-            rk[a] = ranks[a]
-    ent, ep = _u32(flat if flat else [0])
+    m.esize == 2, float32 when 4; rows = tokens.  `tables` is a dict of page
+    tables (with `ranks`) or a PreparedTables."""
+    pt = tables if isinstance(tables, PreparedTables) else PreparedTables(tables, ranks)
     ta = np.ascontiguousarray(np.asarray(token_adapter, np.int32))
     assert x.flags.c_contiguous and y.flags.c_contiguous
     rc = lib().oracle_paged_lora_apply(
-        C.byref(m), arena.ctypes.data, page_bytes, ep, offs.ctypes.data_as(C.POINTER(C.c_uint64)),
-        rk.ctypes.data_as(C.POINTER(C.c_uint32)), n_adapters, layer, proj, x.ctypes.data,
+        C.byref(m), arena.ctypes.data, page_bytes, pt.ent.ctypes.data_as(C.POINTER(C.c_uint32)),
+        pt.offs.ctypes.data_as(C.POINTER(C.c_uint64)),
+        pt.rk.ctypes.data_as(C.POINTER(C.c_uint32)), pt.n_adapters, layer, proj, x.ctypes.data,
         y.ctypes.data, ta.ctypes.data_as(C.POINTER(C.c_int32)), len(ta), scale,
         1 if v_bf16 else 0, nthreads)
     if rc != 0:

@@ -152,6 +152,23 @@ static inline const uint8_t* paged_addr(const job_t* J, uint32_t a, uint64_t off
   return J->arena + (uint64_t)phys * J->page_bytes + off % J->page_bytes;
 }
 
+/* n consecutive elements of adapter a from logical byte `off`, translated
+ * once per page (every element lies inside one page: pages are multiples
+ * of the element size). */
+static void load_row(const job_t* J, uint32_t a, uint64_t off, uint32_t n, double* out) {
+  const uint32_t es = J->m->esize;
+  uint32_t k = 0;
+  while (k < n) {
+    const uint64_t o = off + (uint64_t)k * es;
+    const uint64_t in_page = o % J->page_bytes;
+    uint64_t m = (J->page_bytes - in_page) / es;
+    if (m > n - k) m = n - k;
+    const uint8_t* p = paged_addr(J, a, o);
+    for (uint64_t i = 0; i < m; ++i) out[k + i] = load_elem(p + i * es, es);
+    k += (uint32_t)m;
+  }
+}
+
 static void run_segment(job_t* J, uint32_t s) {
   const oracle_model* m = J->m;
   const uint32_t es = m->esize;
@@ -165,15 +182,19 @@ static void run_segment(job_t* J, uint32_t s) {
   double* v = (double*)calloc((size_t)nt * r, sizeof(double));
   double* acc = (double*)calloc((size_t)nt * dout, sizeof(double));
   double* row = (double*)malloc(sizeof(double) * (din > dout ? din : dout));
+  double* xs = (double*)malloc(sizeof(double) * (size_t)nt * din);
+  for (uint32_t i = 0; i < nt; ++i) { /* the segment's x rows, converted once */
+    const uint8_t* xt = J->x + (uint64_t)J->seg_tokens[t0 + i] * din * es;
+    for (uint32_t k = 0; k < din; ++k) xs[(uint64_t)i * din + k] = load_elem(xt + (uint64_t)k * es, es);
+  }
 
   /* shrink: v[t][j] = sum_k x[t][k] · A[j][k] */
   for (uint32_t j = 0; j < r; ++j) {
-    for (uint32_t k = 0; k < din; ++k)
-      row[k] = load_elem(paged_addr(J, a, blk + ((uint64_t)j * din + k) * es), es);
+    load_row(J, a, blk + (uint64_t)j * din * es, din, row);
     for (uint32_t i = 0; i < nt; ++i) {
-      const uint8_t* xt = J->x + (uint64_t)J->seg_tokens[t0 + i] * din * es;
+      const double* xt = xs + (uint64_t)i * din;
       double sum = 0.0;
-      for (uint32_t k = 0; k < din; ++k) sum += load_elem(xt + (uint64_t)k * es, es) * row[k];
+      for (uint32_t k = 0; k < din; ++k) sum += xt[k] * row[k];
       v[(uint64_t)i * r + j] = sum;
     }
   }
@@ -184,8 +205,7 @@ static void run_segment(job_t* J, uint32_t s) {
   }
   /* expand: acc[t][o] = sum_j v[t][j] · Bᵀ[j][o] */
   for (uint32_t j = 0; j < r; ++j) {
-    for (uint32_t o = 0; o < dout; ++o)
-      row[o] = load_elem(paged_addr(J, a, boff + ((uint64_t)j * dout + o) * es), es);
+    load_row(J, a, boff + (uint64_t)j * dout * es, dout, row);
     for (uint32_t i = 0; i < nt; ++i) {
       double vj = v[(uint64_t)i * r + j];
       double* at = acc + (uint64_t)i * dout;
@@ -203,6 +223,7 @@ static void run_segment(job_t* J, uint32_t s) {
   free(v);
   free(acc);
   free(row);
+  free(xs);
 }
 
 static void* worker(void* arg) {

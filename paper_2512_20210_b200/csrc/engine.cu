@@ -594,7 +594,11 @@ int plora_engine_flush_predictor(plora_engine* e) {
     // the tail, or this wait would outlast a sleeping worker
     sv.cv.notify_one();
     sv.idle.wait(sl, [&] { return sv.obs.empty() && !sv.round_req && !sv.busy; });
-    if (!sv.error.empty()) throw ValidationError(sv.error);
+    if (!sv.error.empty()) {  // report a worker failure once, then clear it
+      std::string msg;
+      msg.swap(sv.error);
+      throw ValidationError("predictor worker: " + msg);
+    }
     if (sv.have) {
       e->apply_predictions(sv.ids.data(), sv.probs.data(), static_cast<int64_t>(sv.ids.size()));
       sv.have = false;
@@ -638,7 +642,11 @@ int plora_engine_round(plora_engine* e, double now_ms, plora_stream_t compute) {
     if (e->svc) {  // apply the last completed round, request the next one
       auto& sv = *e->svc;
       std::lock_guard<std::mutex> sl(sv.m);
-      if (!sv.error.empty()) throw ValidationError(sv.error);
+      if (!sv.error.empty()) {  // report a worker failure once, then clear it
+      std::string msg;
+      msg.swap(sv.error);
+      throw ValidationError("predictor worker: " + msg);
+    }
       if (sv.have) {
         e->apply_predictions(sv.ids.data(), sv.probs.data(), static_cast<int64_t>(sv.ids.size()));
         sv.have = false;

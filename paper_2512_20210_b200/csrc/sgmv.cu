@@ -666,7 +666,7 @@ __global__ void __launch_bounds__(kEThreads, 2)
           for (int i = 0; i < 4; ++i)
             o[i] = live ? pack_bf16x2(p.scale * __uint_as_float(rv[hh * 8 + 2 * i]),
                                       p.scale * __uint_as_float(rv[hh * 8 + 2 * i + 1]))
-                        : 0u;
+                        : 0x80008000u;  // bf16 -0.0: the exact additive identity of the reduce-add
           asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ya), "r"(o[0]), "r"(o[1]),
                        "r"(o[2]), "r"(o[3]) : "memory");
         }
@@ -812,8 +812,12 @@ static bool tc_path(const plora_plan* plan, uint32_t proj) {
   // bf16, rank <= 128, d_in % 64 == 0, d_out % 128 == 0; anything else (fp32
   // storage, wider ranks, odd widths) runs the exact CUDA-core BGMV path,
   // which handles every segment length.
+  // The gathered rows are addressed as 128-byte arena rows (gather4 indices,
+  // 16-byte cp.async groups of 128 B): every (layer, proj) block of every
+  // rank must start on a 128-byte boundary, i.e. rank · blk_mult · 2 ≡ 0 mod
+  // 128 for rank 1 — blk_mult ≡ 0 (mod 64) for every layer.
   return g.esize == 2 && plan->max_rank <= kMaxRank && g.m.d_in[proj] % kChunkK == 0 &&
-         g.m.d_out[proj] % kBlockN == 0;
+         g.m.d_out[proj] % kBlockN == 0 && g.blocks_aligned_128(proj);
 }
 
 }  // namespace plora

@@ -356,6 +356,9 @@ void check_fused(const plora_plan* plan, uint32_t proj, const void* w0, uint64_t
   if (din % kBK || dout % kBN)
     throw ValidationError("plora_sgmv_fused needs d_in % 64 == 0 and d_out % 256 == 0");
   if (w0_stride < din) throw ValidationError("base weight row stride < d_in");
+  if (!g.blocks_aligned_128(proj))
+    throw ValidationError("plora_sgmv_fused needs every (layer, proj) block on a 128-byte boundary "
+                          "(sum of the projection widths and their prefixes multiples of 64)");
 }
 
 // The fused GEMM of one projection; its V tiles start at tile row v_tile0 of

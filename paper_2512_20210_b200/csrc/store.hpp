@@ -51,6 +51,12 @@ struct ModelGeom {
   uint64_t blk_mult(uint32_t layer, uint32_t proj) const {
     return static_cast<uint64_t>(layer) * per_layer_unit + prefix[proj];
   }
+  // Every (layer, proj) A and Bᵀ block of projection `proj` starts on a
+  // 128-byte boundary of the adapter for every rank (the tensor-core paths
+  // address pages as 128-byte rows).
+  bool blocks_aligned_128(uint32_t proj) const {
+    return per_layer_unit % 64 == 0 && prefix[proj] % 64 == 0 && m.d_in[proj] % 64 == 0;
+  }
   uint64_t adapter_bytes(uint32_t rank) const {
     return static_cast<uint64_t>(rank) * per_layer_unit * m.n_layers * esize;
   }

@@ -93,11 +93,28 @@ class TensorParallelLoRA:
         self._shrink = shrink or bgmv_tp_shrink
         self._expand = expand or bgmv_tp_expand
         self._gather = all_gather or (lambda out, inp: _all_gather(out, inp, group))
-        self.rs = shard_rows if shard_rows is not None else tp_shard_rows(plan, tp_size)
-        self.n_tokens = n_tokens if n_tokens is not None else plan.n_tokens
-        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.v_part = torch.empty(self.n_tokens, self.rs, dtype=torch.float32, device=dev)
-        self.v_gathered = torch.empty(tp_size, self.n_tokens, self.rs, dtype=torch.float32, device=dev)
+        # fixed sizes only when injected (emulated ranks); otherwise they follow
+        # the plan, which BatchPlan.update may change between calls
+        self._fixed_rs, self._fixed_t = shard_rows, n_tokens
+        self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self._buf = torch.empty(0, dtype=torch.float32, device=self.device)
+        self._gbuf = torch.empty(0, dtype=torch.float32, device=self.device)
+        self._views()
+
+    def _views(self):
+        """v_part [T, rs] and v_gathered [N, T, rs] as contiguous prefix views
+        of the buffers, sized from the plan as it is now: the expand kernel
+        reads rank block i at i·T·rs of the CURRENT plan, so the gathered
+        layout must be rebuilt whenever T or rs changes."""
+        rs = self._fixed_rs if self._fixed_rs is not None else tp_shard_rows(self.plan, self.tp_size)
+        t = self._fixed_t if self._fixed_t is not None else self.plan.n_tokens
+        need = max(t * rs, 1)
+        if self._buf.numel() < need:
+            self._buf = torch.empty(need, dtype=torch.float32, device=self.device)
+            self._gbuf = torch.empty(self.tp_size * need, dtype=torch.float32, device=self.device)
+        self.rs, self.n_tokens = rs, t
+        self.v_part = self._buf[:t * rs].view(t, rs)
+        self.v_gathered = self._gbuf[:self.tp_size * t * rs].view(self.tp_size, t, rs)
 
     def forward(self, layer: int, proj: int, x: torch.Tensor, y_shard: torch.Tensor,
                 scale: float = 1.0) -> torch.Tensor:
@@ -106,6 +123,7 @@ class TensorParallelLoRA:
             # data-parallel op applies the whole LoRA in one launch
             from .lora import bgmv
             return bgmv(self.plan, layer, proj, x, y_shard, scale)
+        self._views()
         self._shrink(self.plan, layer, proj, self.tp_rank, self.tp_size, x, self.v_part)
         if self.tp_size > 1:
             self._gather(self.v_gathered, self.v_part)

@@ -25,6 +25,16 @@ def to_f32(a: np.ndarray) -> np.ndarray:
     return OL.bf16_bits_to_f32(a) if a.dtype == np.uint16 else a.astype(np.float32)
 
 
+def delta_rel_err(y_gpu: torch.Tensor, y_ref: np.ndarray, y0: torch.Tensor) -> float:
+    """Normwise error of the LoRA delta alone: max|Δy_gpu - Δy_ref| / max|Δy_ref|
+    (y0 subtracted in fp64), so a systematic error in the delta cannot hide
+    under |y0|."""
+    g = to_f32(to_np_bits(y_gpu)).astype(np.float64)
+    r = to_f32(y_ref).astype(np.float64)
+    b = to_f32(to_np_bits(y0)).astype(np.float64)
+    return float(np.abs((g - b) - (r - b)).max() / max(np.abs(r - b).max(), 1e-30))
+
+
 def rel_err(y_gpu: torch.Tensor, y_ref: np.ndarray) -> float:
     g = to_f32(to_np_bits(y_gpu)).astype(np.float64)
     r = to_f32(y_ref).astype(np.float64)
@@ -56,6 +66,30 @@ class Setup:
             OL.scatter_pages(self.arena, P, self.pool.table(a), to_np_bits(img))
         torch.cuda.synchronize()
         self.m = OL.model(cfg.shape.n_layers, cfg.shape.d_in, cfg.shape.d_out, cfg.shape.esize)
+
+    @classmethod
+    def on_device(cls, cfg: synth.DecodeConfig, device: int = 0, pool=None):
+        """Full-size configs: images generated on the GPU (torch CUDA
+        generator), scattered device-to-device, and copied once to the host
+        arena the oracle reads — no host copy of the images is kept."""
+        self = cls.__new__(cls)
+        self.cfg, self.shape = cfg, cfg.shape
+        self.pool = pool if pool is not None else synth.build_pool(cfg)
+        self.store = AdapterStore(self.pool, cfg.shape, max_adapters=cfg.n_adapters,
+                                  device=device)
+        P = cfg.page_bytes
+        self.arena = np.zeros(self.pool.total_pages() * P, np.uint8)
+        self.images = {}
+        for a, r in enumerate(cfg.ranks):
+            img = synth.adapter_image(cfg.shape, r, a, device=f"cuda:{device}")
+            self.store.register(a, r)
+            self.store.write_pages(a, img.view(torch.uint8))
+            self.store.publish(a)
+            OL.scatter_pages(self.arena, P, self.pool.table(a), to_np_bits(img))
+            del img
+        torch.cuda.synchronize()
+        self.m = OL.model(cfg.shape.n_layers, cfg.shape.d_in, cfg.shape.d_out, cfg.shape.esize)
+        return self
 
     def tables(self):
         return {a: self.pool.table(a) for a in range(self.cfg.n_adapters)}

@@ -1,0 +1,197 @@
+"""Full-size parity against the CPU oracle (oracle/lora_oracle.c) at the
+BASELINE configs themselves — not reduced shapes — plus skewed decode batches
+and delta-only (y0 = 0) runs so the 1e-2 bound measures the LoRA delta alone.
+
+  * cfg3 at full size: 32 segments × 512 tokens, r = [16,64,128][s % 3],
+    32 layers; plora_sgmv and plora_sgmv_layer at the first and last layer.
+  * cfg2 at full depth: layer 31 of the 32-layer catalog, both projections,
+    plora_bgmv and plora_bgmv_layer.
+  * skewed decode: 128 adapters with Zipf-distributed token counts (the hot
+    adapter holds >= 64 tokens), r in {8..128}, Llama-7B widths.
+"""
+import numpy as np
+import pytest
+import torch
+
+from lora_harness import TOL_BF16, Setup, delta_rel_err, rel_err, to_np_bits
+from paper_2512_20210_b200 import synth
+from paper_2512_20210_b200.lora import (BatchPlan, ModelShape, bgmv, bgmv_layer,
+                                        kernel_launch_count, sgmv, sgmv_layer)
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(T, d_in, d_out, salt, zero_y=False, n_out=1):
+    x = synth.activations(T, d_in, torch.bfloat16, "x", salt=salt)
+    ys = [torch.zeros(T, d_out, dtype=torch.bfloat16) if zero_y else
+          synth.activations(T, d_out, torch.bfloat16, "y", salt=salt + p) for p in range(n_out)]
+    return x, ys
+
+
+@pytest.fixture(scope="module")
+def cfg3_full(cuda):
+    s = Setup.on_device(synth.cfg3())
+    yield s
+    del s
+
+
+@pytest.mark.parametrize("layer,proj", [(0, 0), (31, 1)])
+def test_sgmv_full_cfg3_vs_oracle(cfg3_full, layer, proj):
+    s = cfg3_full
+    ta = synth.segment_assignment(32, 512)
+    T = len(ta)
+    for zero_y in (False, True):
+        x, (y0,) = _inputs(T, 4096, 4096, salt=40 + layer, zero_y=zero_y)
+        yd = y0.cuda()
+        sgmv(BatchPlan(s.store, ta), layer, proj, x.cuda(), yd, 0.5)
+        torch.cuda.synchronize()
+        ref = s.oracle(layer, proj, x, y0, ta, scale=0.5, v_bf16=True, nthreads=32)
+        err = delta_rel_err(yd, ref, y0)
+        assert err <= TOL_BF16, (layer, proj, zero_y, err)
+        assert rel_err(yd, ref) <= TOL_BF16
+
+
+def test_sgmv_layer_full_cfg3_vs_oracle(cfg3_full):
+    s = cfg3_full
+    ta = synth.segment_assignment(32, 512)
+    T = len(ta)
+    for layer in (31, 7):
+        x, y0 = _inputs(T, 4096, 4096, salt=60 + layer, zero_y=layer == 7, n_out=2)
+        ys = [y.cuda() for y in y0]
+        n0 = kernel_launch_count()
+        sgmv_layer(BatchPlan(s.store, ta), layer, x.cuda(), ys)
+        torch.cuda.synchronize()
+        assert kernel_launch_count() - n0 == 3
+        for p in range(2):
+            ref = s.oracle(layer, p, x, y0[p], ta, v_bf16=True, nthreads=32)
+            err = delta_rel_err(ys[p], ref, y0[p])
+            assert err <= TOL_BF16, (layer, p, err)
+
+
+@pytest.fixture(scope="module")
+def cfg2_full(cuda):
+    s = Setup.on_device(synth.cfg2())
+    yield s
+    del s
+
+
+def test_bgmv_full_cfg2_last_layer_vs_oracle(cfg2_full):
+    """Layer 31 of the full 32-layer cfg2 catalog (the last block of every
+    adapter: the highest logical pages of every table)."""
+    s = cfg2_full
+    ta = synth.token_assignment(128, 2)
+    T = len(ta)
+    for proj in (0, 1):
+        for zero_y in (False, True):
+            x, (y0,) = _inputs(T, 4096, 4096, salt=31 * 2 + proj, zero_y=zero_y)
+            yd = y0.cuda()
+            bgmv(BatchPlan(s.store, ta), 31, proj, x.cuda(), yd)
+            torch.cuda.synchronize()
+            ref = s.oracle(31, proj, x, y0, ta, nthreads=32)
+            assert delta_rel_err(yd, ref, y0) <= TOL_BF16, (proj, zero_y)
+            assert rel_err(yd, ref) <= TOL_BF16
+
+
+def test_bgmv_layer_full_cfg2_last_layer_vs_oracle(cfg2_full):
+    s = cfg2_full
+    ta = synth.token_assignment(128, 2)
+    T = len(ta)
+    x, y0 = _inputs(T, 4096, 4096, salt=99, zero_y=True, n_out=2)
+    ys = [y.cuda() for y in y0]
+    bgmv_layer(BatchPlan(s.store, ta), 31, x.cuda(), ys, 0.75)
+    torch.cuda.synchronize()
+    for p in range(2):
+        ref = s.oracle(31, p, x, y0[p], ta, scale=0.75, nthreads=32)
+        assert delta_rel_err(ys[p], ref, y0[p]) <= TOL_BF16, p
+
+
+def skewed_assignment(n_adapters=128, n_tokens=512, hot=64, seed=17):
+    """Zipf(1.1) token counts over the adapters, the hottest holding >= `hot`
+    tokens, every adapter at least one token; shuffled (decode order)."""
+    w = 1.0 / np.arange(1, n_adapters + 1) ** 1.1
+    cnt = np.maximum(1, np.floor(w / w.sum() * n_tokens)).astype(int)
+    cnt[0] = max(cnt[0], hot)
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n_adapters)  # the hot adapter is not key 0
+    ta = np.concatenate([np.full(c, perm[i], np.int32) for i, c in enumerate(cnt)])
+    rng.shuffle(ta)
+    return ta
+
+
+@pytest.fixture(scope="module")
+def skew_setup(cuda):
+    shape = ModelShape(2, (4096, 4096), (4096, 4096), torch.bfloat16)
+    ranks = [(8, 16, 32, 64, 128)[a % 5] for a in range(128)]
+    s = Setup.on_device(synth.DecodeConfig("skew", shape, ranks, 1, 2048))
+    yield s
+    del s
+
+
+@pytest.mark.parametrize("zero_y", [False, True])
+def test_bgmv_skewed_batch_vs_oracle(skew_setup, zero_y):
+    s = skew_setup
+    ta = skewed_assignment()
+    counts = np.bincount(ta, minlength=128)
+    assert counts.max() >= 64 and (counts > 0).all()
+    T = len(ta)
+    for layer, proj in ((0, 1), (1, 0)):
+        x, (y0,) = _inputs(T, 4096, 4096, salt=layer * 3 + proj, zero_y=zero_y)
+        yd = y0.cuda()
+        bgmv(BatchPlan(s.store, ta), layer, proj, x.cuda(), yd, 0.5)
+        torch.cuda.synchronize()
+        ref = s.oracle(layer, proj, x, y0, ta, scale=0.5, nthreads=32)
+        assert delta_rel_err(yd, ref, y0) <= TOL_BF16, (layer, proj)
+        assert rel_err(yd, ref) <= TOL_BF16
+
+
+def test_bgmv_layer_skewed_batch_vs_oracle(skew_setup):
+    s = skew_setup
+    ta = skewed_assignment(seed=23, hot=96)
+    T = len(ta)
+    x, y0 = _inputs(T, 4096, 4096, salt=5, zero_y=True, n_out=2)
+    ys = [y.cuda() for y in y0]
+    bgmv_layer(BatchPlan(s.store, ta), 1, x.cuda(), ys)
+    torch.cuda.synchronize()
+    for p in range(2):
+        ref = s.oracle(1, p, x, y0[p], ta, nthreads=32)
+        assert delta_rel_err(ys[p], ref, y0[p]) <= TOL_BF16, p
+
+
+def test_delta_only_small_configs(cuda):
+    """y0 = 0 for the per-call ops at cfg1 (so the normwise bound is on Δy)."""
+    cfg = synth.cfg1(n_layers=2)
+    s = Setup(cfg)
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    T = len(ta)
+    x, (y0,) = _inputs(T, 4096, 4096, salt=3, zero_y=True)
+    for op, vb in ((bgmv, False), (sgmv, True)):
+        yd = y0.cuda()
+        op(BatchPlan(s.store, ta), 1, 0, x.cuda(), yd)
+        torch.cuda.synchronize()
+        ref = s.oracle(1, 0, x, y0, ta, v_bf16=vb)
+        assert delta_rel_err(yd, ref, y0) <= TOL_BF16, op.__name__
+
+
+def test_sgmv_mixed_width_misaligned_blocks(cuda):
+    """A projection width that puts later (layer, proj) blocks off a 128-byte
+    boundary (d_out 4104): the tensor-core path must not run on it (it
+    addresses pages as 128-byte rows); results match the oracle on every
+    layer and projection."""
+    shape = ModelShape(2, (4096, 4096), (4096, 4104), torch.bfloat16)
+    ranks = [4, 3, 16]
+    cfg = synth.DecodeConfig("misaligned", shape, ranks, 1, 2048)
+    s = Setup(cfg)
+    runs = [(0, 130), (1, 40), (2, 200)]
+    ta = np.concatenate([np.full(n, a, np.int32) for a, n in runs])
+    T = len(ta)
+    for layer in (0, 1):
+        for proj in (0, 1):
+            x, (y0,) = _inputs(T, 4096, shape.d_out[proj], salt=layer * 2 + proj)
+            yd = y0.cuda()
+            sgmv(BatchPlan(s.store, ta), layer, proj, x.cuda(), yd)
+            torch.cuda.synchronize()
+            ref_f = s.oracle(layer, proj, x, y0, ta)
+            ref_b = s.oracle(layer, proj, x, y0, ta, v_bf16=True)
+            err = min(delta_rel_err(yd, ref_f, y0), delta_rel_err(yd, ref_b, y0))
+            assert err <= TOL_BF16, (layer, proj, err)
+            assert np.array_equal(to_np_bits(yd)[ta < 0], to_np_bits(y0)[ta < 0])

@@ -97,7 +97,7 @@ def test_sgmv_fused_rejects_bad_shapes(cuda):
         sgmv_fused(plan, 0, 0, x, torch.zeros(2048, 4096, dtype=torch.bfloat16, device="cuda"), y)
 
 
-@pytest.mark.parametrize("page_bytes", [64, 256])
+@pytest.mark.parametrize("page_bytes", [64, 256, 512, 1024])
 def test_sgmv_fused_small_pages(cuda, page_bytes):
     """Bᵀ row segments of a 256-column block straddle pages: the LoRA K-step
     gathers translate every 16-byte piece through the page table."""
