@@ -214,7 +214,22 @@ def run_ours(args):
     LPS = NP if not fused else 1  # calls per layer
     layer_op = sgmv_layer if prefill else bgmv_layer
 
+    mlp = max(1, args.layers_per_launch) if not prefill else 1
+    if mlp > 1:
+        from paper_2512_20210_b200.lora import bgmv_layers
+        yv = y.view(L, NP, T, 4096)
+        LPS = 1.0 / mlp  # launches per layer
+
     def step(ev=None):
+        if mlp > 1:
+            for i, l0 in enumerate(range(0, L, mlp)):
+                if ev is not None:
+                    ev[2 * i].record()
+                n = min(mlp, L - l0)
+                bgmv_layers(plan, l0, x[l0:l0 + n], [yv[l0:l0 + n, p] for p in range(NP)])
+                if ev is not None:
+                    ev[2 * i + 1].record()
+            return
         for l in range(L):
             if fused:
                 if ev is not None:
@@ -277,11 +292,11 @@ def run_ours(args):
         for _ in range(3):  # per-launch durations (separate, serialised replays)
             tgraph.replay()
             torch.cuda.synchronize()
-            kern_ms += [gevs[2 * i].elapsed_time(gevs[2 * i + 1]) for i in range(L * LPS)]
+            kern_ms += [gevs[2 * i].elapsed_time(gevs[2 * i + 1]) for i in range(int(L * LPS))]
     else:
         launches = kernel_launch_count() - n0
         kern_ms = [evs[k][2 * i].elapsed_time(evs[k][2 * i + 1])
-                   for k in range(K) for i in range(L * LPS)]
+                   for k in range(K) for i in range(int(L * LPS))]
     step_ms = start.elapsed_time(end) / K
     mean_kern_ms = statistics.mean(kern_ms)
     if world > 1:
@@ -377,6 +392,8 @@ def run_ours(args):
     # average launch duration over the timed region: the step is the L·NP
     # launches back to back (overlapping through PDL), nothing else
     avg_launch_ms = step_ms / (L * LPS)
+    if mlp > 1:  # one launch serves mlp layers: its bytes are mlp layers' worth
+        per_call *= mlp
     achieved = per_call / (avg_launch_ms / 1e3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "sgmv_traffic.json" if prefill else "bgmv_traffic.json")
@@ -807,6 +824,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the 64 calls eagerly")
+    ap.add_argument("--layers-per-launch", type=int, default=1,
+                    help="decode: layers served by one plora_bgmv_layers launch (1 = one "
+                         "plora_bgmv_layer launch per layer)")
     ap.add_argument("--per-proj", action="store_true",
                     help="decode: one launch per (layer, proj) instead of one per layer")
     ap.add_argument("--cfg5-layers", type=int, default=80)

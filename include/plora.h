@@ -285,6 +285,18 @@ int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
 int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x_stride,
                      void* const* ys, const uint64_t* y_strides, float scale,
                      plora_stream_t stream);
+/* Layers [layer0, layer0 + n_layers) of plora_bgmv_layer in one launch, for
+ * inputs that are all ready (a LoRA-only decode step, speculative/multi-layer
+ * batching): the decode clusters stay resident and stream layer l+1's pages
+ * right behind layer l's, so the per-launch prologue / drain / CTA
+ * turnaround is paid once.  Layer layer0 + i reads x + i·x_layer_stride and
+ * updates ys[p] + i·y_layer_strides[p] (all strides in elements).  Results
+ * are bit-identical to n_layers plora_bgmv_layer calls.  bf16 stores with
+ * equal projection shapes; otherwise one plora_bgmv_layer per layer. */
+int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_layers, const void* x,
+                      uint64_t x_stride, uint64_t x_layer_stride, void* const* ys,
+                      const uint64_t* y_strides, const uint64_t* y_layer_strides, float scale,
+                      plora_stream_t stream);
 /* Same contract, prefill path (tcgen05 tensor cores; v rounded to the
  * storage dtype between shrink and expand). */
 int plora_sgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,

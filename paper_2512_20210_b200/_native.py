@@ -186,6 +186,8 @@ _SIGS = {
     "plora_plan_num_segments": (_u32, [_vp]),
     "plora_bgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
     "plora_bgmv_layer": (_int, [_vp, _u32, _vp, _u64, _P(_vp), _P(_u64), C.c_float, _vp]),
+    "plora_bgmv_layers": (_int, [_vp, _u32, _u32, _vp, _u64, _u64, _P(_vp), _P(_u64), _P(_u64),
+                                 C.c_float, _vp]),
     "plora_sgmv": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, C.c_float, _vp]),
     "plora_sgmv_layer": (_int, [_vp, _u32, _vp, _u64, _P(_vp), _P(_u64), C.c_float, _vp]),
     "plora_sgmv_fused": (_int, [_vp, _u32, _u32, _vp, _u64, _vp, _u64, _vp, _u64, C.c_float, _vp]),

@@ -447,6 +447,48 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
   });
 }
 
+extern "C" int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_layers,
+                                 const void* x, uint64_t x_stride, uint64_t x_layer_stride,
+                                 void* const* ys, const uint64_t* y_strides,
+                                 const uint64_t* y_layer_strides, float scale,
+                                 plora_stream_t stream) {
+  return guard([&] {
+    if (!plan) throw ValidationError("null plan");
+    if (!ys || !y_strides || !y_layer_strides) throw ValidationError("null ys / strides");
+    if (n_layers == 0) return 0;
+    const plora_store& st = *plan->store;
+    const ModelGeom& g = st.geom;
+    if (layer0 + static_cast<uint64_t>(n_layers) > g.m.n_layers)
+      throw ValidationError("layers [" + std::to_string(layer0) + ", " +
+                            std::to_string(layer0 + n_layers) + ") out of range");
+    const uint32_t vec = 16 / g.esize;
+    if (x_layer_stride % vec) throw ValidationError("layer strides must be multiples of 16 bytes");
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) {
+      if (g.m.d_in[p] != g.m.d_in[0])
+        throw ValidationError("plora_bgmv_layers: projections read different input widths");
+      if (y_layer_strides[p] % vec) throw ValidationError("layer strides must be multiples of 16 bytes");
+      check_io(plan, layer0, p, x, x_stride, ys[p], y_strides[p]);
+    }
+    const bool one = g.esize == 2 && plan->n_layer_proj == g.m.n_proj &&
+                     n_layers * g.m.n_proj <= 256;
+    if (one) {
+      DeviceCtx ctx(st.device);
+      launch_bgmv_cluster_layers(*plan, layer0, n_layers, x, x_stride, x_layer_stride, ys,
+                                 y_strides, y_layer_strides, scale, static_cast<cudaStream_t>(stream));
+      return 0;
+    }
+    std::vector<void*> yl(g.m.n_proj);
+    for (uint32_t i = 0; i < n_layers; ++i) {
+      for (uint32_t p = 0; p < g.m.n_proj; ++p)
+        yl[p] = static_cast<char*>(ys[p]) + i * y_layer_strides[p] * g.esize;
+      const int rc = plora_bgmv_layer(plan, layer0 + i, static_cast<const char*>(x) + i * x_layer_stride * g.esize,
+                                      x_stride, yl.data(), y_strides, scale, stream);
+      if (rc < 0) return rc;
+    }
+    return 0;
+  });
+}
+
 extern "C" int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x,
                                 uint64_t x_stride, void* const* ys, const uint64_t* y_strides,
                                 float scale, plora_stream_t stream) {

@@ -72,6 +72,14 @@ struct CArgs {
   char* y[PLORA_MAX_PROJ];
   uint64_t y_stride_b[PLORA_MAX_PROJ];
   uint64_t blk_mult[PLORA_MAX_PROJ];
+  // multi-layer launch (plora_bgmv_layers): every cluster's chunk list runs
+  // n_layers times; pass li of it serves layer layer0 + li, whose x / y rows
+  // are li·x_lstride_b / li·y_lstride_b[proj] bytes further and whose blocks
+  // start li·plu elements further (per unit of rank)
+  uint32_t n_layers, np;
+  uint64_t x_lstride_b;
+  uint64_t y_lstride_b[PLORA_MAX_PROJ];
+  uint64_t plu;
   uint32_t log2_page;
   uint32_t d_in, d_out;
   uint32_t cs, ks, ns;  // cluster size, slice widths (elements)
@@ -83,7 +91,18 @@ struct CArgs {
   // cluster c runs chunks [cl_off[c], cl_off[c + 1]): a kernel parameter, so
   // the prologue's first dependent load is the chunk record itself
   uint32_t cl_off[kMaxClusters + 1];
+  uint32_t cl_jobs[kMaxClusters];  // jobs in cluster c's list (virtual job ordinals across passes)
 };
+
+// Position of virtual chunk v of a cluster's n_layers-fold list: the pass
+// (layer offset) and the chunk record's global index.
+struct VPos {
+  uint32_t li, gi;
+};
+__device__ __forceinline__ VPos vpos(uint32_t v, uint32_t i0, uint32_t nch) {
+  const uint32_t li = v / nch;
+  return VPos{li, i0 + (v - li * nch)};
+}
 
 constexpr uint32_t kTraceChunks = 64;
 __device__ __forceinline__ uint64_t now_ns() {  // SM cycles (cheap; %globaltimer is not)
@@ -167,8 +186,9 @@ struct Piece {
 };
 
 struct Rec {  // chunk record fields (ClusterChunk), read from a smem ring
-  uint32_t table_off, rank, ntok, flags, row0, nrows, proj;
-  __device__ explicit Rec(const uint32_t* w) {
+  uint32_t table_off, rank, ntok, flags, row0, nrows, proj, li;
+  uint64_t blk;  // block offset multiplier of this chunk's (layer, proj): A starts at rank · blk
+  __device__ Rec(const uint32_t* w, const CArgs& p, uint32_t pass) {
     table_off = w[0];
     rank = w[1] & 0xffffu;
     ntok = (w[1] >> 16) & 0xffu;
@@ -176,6 +196,8 @@ struct Rec {  // chunk record fields (ClusterChunk), read from a smem ring
     row0 = w[2] & 0xffffu;
     nrows = (w[2] >> 16) & 0xffu;
     proj = w[2] >> 24;
+    li = pass;
+    blk = p.blk_mult[proj] + static_cast<uint64_t>(pass) * p.plu;
   }
 };
 
@@ -193,7 +215,7 @@ __device__ __forceinline__ uint32_t piece_geom(const CArgs& p, const Slice& sl,
   const uint32_t ppr = isb ? pg.pprB : pg.pprA;
   if (q >= c.nrows * ppr) return 0;
   const uint32_t L = p.log2_page;
-  const uint64_t a_base = static_cast<uint64_t>(c.rank) * p.blk_mult[c.proj];  // elements
+  const uint64_t a_base = static_cast<uint64_t>(c.rank) * c.blk;  // elements
   const uint32_t r = q / ppr, k = q - r * ppr;
   uint64_t lo;
   uint32_t len, dst;
@@ -248,9 +270,9 @@ __device__ __forceinline__ uint32_t my_piece(const CArgs& p, const Slice& sl, co
     if (r >= c.nrows) return 0;
     const bool isb = pw >= 2;
     const uint64_t lo =
-        (isb ? static_cast<uint64_t>(c.rank) * (p.blk_mult[c.proj] + p.d_in) +
+        (isb ? static_cast<uint64_t>(c.rank) * (c.blk + p.d_in) +
                    static_cast<uint64_t>(c.row0 + r) * p.d_out + sl.n0
-             : static_cast<uint64_t>(c.rank) * p.blk_mult[c.proj] +
+             : static_cast<uint64_t>(c.rank) * c.blk +
                    static_cast<uint64_t>(c.row0 + r) * p.d_in + sl.k0) * 2;
     x.len = isb ? pg.NB : pg.KB;
     x.dst = isb ? r * pg.NSB : r * pg.KSB;
@@ -286,16 +308,18 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
   pg.NSB = row_stride(p.ns);
   pg.pprA = pg.KB ? ((pg.KB - 1) >> L) + 2 : 0;  // page pieces per row (upper bound)
   pg.pprB = pg.NB ? ((pg.NB - 1) >> L) + 2 : 0;
-  const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
+  const uint32_t i0 = p.cl_off[cl], nch = p.cl_off[cl + 1] - i0;
   const uint32_t w2 = pw & 1u;
-  const uint32_t n = (i1 - i0 + 1 - w2) / 2;  // this warp's chunks: idx = 2j + w2
+  const uint32_t n = (nch * p.n_layers + 1 - w2) / 2;  // this warp's chunks: idx = 2j + w2
+  const uint32_t njobs = p.cl_jobs[cl];
   auto fetch_rec = [&](uint32_t j) {  // 32-byte record of local chunk j: lanes 0, 1 copy 16 bytes each
     if (lane < 2 && j < n)
-      ptx::cp_async_16(recring + (j % kRecRing) * 8 + lane * 4, recg + (i0 + 2 * j + w2) * 8 + lane * 4, 16);
+      ptx::cp_async_16(recring + (j % kRecRing) * 8 + lane * 4,
+                       recg + vpos(2 * j + w2, i0, nch).gi * 8 + lane * 4, 16);
   };
   auto fetch_tbl = [&](uint32_t j) {  // page-table entry of this lane's piece of local chunk j
     if (j >= n) return;
-    const Rec c(recring + (j % kRecRing) * 8);
+    const Rec c(recring + (j % kRecRing) * 8, p, vpos(2 * j + w2, i0, nch).li);
     Piece x{};
     const uint32_t page = my_piece(p, sl, pg, c, pw, lane, x);
     if (x.len)
@@ -325,7 +349,7 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
     __syncwarp();
     if (pw == 0 && lane == 0) trace_put(p, idx, 6);
     const uint32_t* rw = recring + (j % kRecRing) * 8;
-    const Rec c(rw);
+    const Rec c(rw, p, vpos(idx, i0, nch).li);
     char* sb = smem + (isb ? p.off_b + s * p.b_bytes : s * p.a_bytes);
     const uint2 geo = georing[(j % kAhead) * 32 + lane];
     Piece pc;
@@ -360,9 +384,14 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
       bytes = __reduce_add_sync(0xffffffffu, bytes);
     }
     if (lane == 0) {  // publish the record in the slot header, released by the arrival
+      // (virtual fields for the consumers: proj byte = pass · np + proj, jord
+      // = pass · jobs + jord, so job buffers cycle across passes)
       const uint4* src = reinterpret_cast<const uint4*>(rw);
       uint4* dst = reinterpret_cast<uint4*>(hdr + s * 8);
-      dst[0] = src[0];
+      uint4 w0 = src[0];
+      w0.z = (w0.z & 0x00ffffffu) | ((c.li * p.np + c.proj) << 24);
+      w0.w += c.li * njobs;
+      dst[0] = w0;
       dst[1] = src[1];
       ptx::mbar_arrive_expect_tx(&fullb[s], bytes);
     }
@@ -391,11 +420,11 @@ __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uin
   const uint32_t* recg = reinterpret_cast<const uint32_t*>(p.chunks);
   const Slice sl(p, crank);
   const uint32_t KB = sl.kb * 2, NB = sl.nb * 2, KSB = row_stride(p.ks), NSB = row_stride(p.ns);
-  const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
-  const uint32_t n = i1 - i0;
+  const uint32_t i0 = p.cl_off[cl], nch = p.cl_off[cl + 1] - i0;
+  const uint32_t n = nch * p.n_layers;
   auto fetch_rec = [&](uint32_t j) {
     if (lane < 2 && j < n)
-      ptx::cp_async_16(recring + (j % kRecRing) * 8 + lane * 4, recg + (i0 + j) * 8 + lane * 4, 16);
+      ptx::cp_async_16(recring + (j % kRecRing) * 8 + lane * 4, recg + vpos(j, i0, nch).gi * 8 + lane * 4, 16);
   };
   for (uint32_t j = 0; j < kAhead; ++j) {
     fetch_rec(j);
@@ -408,7 +437,7 @@ __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uin
     cp_async_wait_group<kAhead - 1>();
     __syncwarp();
     const uint32_t* rw = recring + (idx % kRecRing) * 8;
-    const Rec c(rw);
+    const Rec c(rw, p, vpos(idx, i0, nch).li);
     if (c.flags & kChunkFirst) {  // the job's x / y slices
       const uint32_t jbuf = jord % kJobBufs, jph = (jord / kJobBufs) & 1u;
       ++jord;
@@ -422,10 +451,11 @@ __device__ void control_producer(const CArgs& p, char* smem, uint32_t crank, uin
       if (lane == 0) ptx::mbar_arrive_expect_tx(&bar.jfull[jbuf], c.ntok * (KB + NB));
       __syncwarp();
       if (lane < c.ntok && KB)
-        ptx::bulk_g2s(jb + lane * KSB, p.x + tokx * p.x_stride_b + sl.k0 * 2, KB, &bar.jfull[jbuf]);
+        ptx::bulk_g2s(jb + lane * KSB, p.x + c.li * p.x_lstride_b + tokx * p.x_stride_b + sl.k0 * 2, KB,
+                      &bar.jfull[jbuf]);
       else if (lane >= 16 && lane - 16 < c.ntok && NB)
         ptx::bulk_g2s(jb + kJobTok * KSB + (lane - 16) * NSB,
-                      p.y[c.proj] + tokx * p.y_stride_b[c.proj] + sl.n0 * 2,
+                      p.y[c.proj] + c.li * p.y_lstride_b[c.proj] + tokx * p.y_stride_b[c.proj] + sl.n0 * 2,
                       NB, &bar.jfull[jbuf]);
     }
     __syncwarp();
@@ -467,7 +497,7 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   const uint32_t* hdr = reinterpret_cast<const uint32_t*>(smem + p.off_hdr);  // A-slot records
   const volatile uint32_t* edone =
       reinterpret_cast<const volatile uint32_t*>(smem + p.off_hdr + 2 * kMaxSlots * sizeof(ClusterChunk));
-  const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
+  const uint32_t n = (p.cl_off[cl + 1] - p.cl_off[cl]) * p.n_layers;
   // ldmatrix lane addressing: A (x rows) = row (lane&7) + 8·((lane>>3)&1), k-half lane>>4
   // (rows >= kJobTok alias row 0: their D rows are discarded); B (W rows, x4 =
   // two k-steps) = row lane&7, k-quarter lane>>3
@@ -477,10 +507,10 @@ __device__ void shrink_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   const uint32_t sg = w / kSubWarps, sw = w % kSubWarps;  // subgroup, warp within it
   const bool lead = sw == 0 && lane == 0;
 #pragma unroll 1
-  for (uint32_t i = i0 + sg; i < i1; i += kSubgroups) {  // this subgroup's chunks
+  for (uint32_t idx = sg; idx < n; idx += kSubgroups) {  // this subgroup's chunks
     // (p.na is even: a subgroup's previous chunk in slot s is idx - na, which
     // it consumed itself, so its parity wait is never a ring lap ahead)
-    const uint32_t idx = i - i0, s = idx % p.na, e = idx % kX;
+    const uint32_t s = idx % p.na, e = idx % kX;
     if (lead) trace_put(p, idx, 14);
     ptx::mbar_wait(&bar.afull[s], (idx / p.na) & 1u);
     if (lead) trace_put(p, idx, 0);
@@ -599,7 +629,7 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
       reinterpret_cast<const uint32_t*>(smem + p.off_hdr) + kMaxSlots * 8;  // Bᵀ-slot records
   volatile uint32_t* edone =
       reinterpret_cast<volatile uint32_t*>(smem + p.off_hdr + 2 * kMaxSlots * sizeof(ClusterChunk));
-  const uint32_t i0 = p.cl_off[cl], i1 = p.cl_off[cl + 1];
+  const uint32_t n = (p.cl_off[cl + 1] - p.cl_off[cl]) * p.n_layers;
   // this warp's 16-column tiles [t0, t1) of the output slice
   const uint32_t ntiles = sl.nb / 16, tpw = (ntiles + kEWarps - 1) / kEWarps;
   const uint32_t t0 = w * tpw, t1 = min(t0 + tpw, ntiles);
@@ -607,8 +637,8 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
   ptx::pdl_wait();  // y is written below: the previous call must be complete
   float acc[kMaxTiles + 1][4];
 #pragma unroll 1
-  for (uint32_t i = i0; i < i1; ++i) {
-    const uint32_t idx = i - i0, s = idx % p.nbs, e = idx % kX;
+  for (uint32_t idx = 0; idx < n; ++idx) {
+    const uint32_t s = idx % p.nbs, e = idx % kX;
     ptx::mbar_wait(&bar.bfull[s], (idx / p.nbs) & 1u);
     const ClusterChunk* ch = reinterpret_cast<const ClusterChunk*>(hdr + s * 8);
     const uint32_t ntok = ch->ntok, nrows = ch->nrows, flags = ch->flags, jord = ch->jord;
@@ -677,7 +707,9 @@ __device__ void expand_group(const CArgs& p, char* smem, uint32_t crank, uint32_
     if (tid == 0) trace_put(p, idx, 11);
     if ((flags & kChunkLast) && cc < ntok) {  // y[tok cc] += scale · (hi + lo), once per job
       const char* yrow = smem + p.off_jb + (jord % kJobBufs) * p.jb_bytes + kJobTok * KSB + cc * NSB;
-      char* yg = p.y[ch->proj] + ch->tok[cc] * p.y_stride_b[ch->proj] + static_cast<uint64_t>(sl.n0) * 2;
+      const uint32_t li = ch->proj / p.np, pj = ch->proj - li * p.np;  // virtual proj byte
+      char* yg = p.y[pj] + li * p.y_lstride_b[pj] + ch->tok[cc] * p.y_stride_b[pj] +
+                 static_cast<uint64_t>(sl.n0) * 2;
       auto put = [&](uint32_t col, float v) {
         const float o = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(yrow + col * 2));
         *reinterpret_cast<__nv_bfloat16*>(yg + col * 2) = __float2bfloat16_rn(fmaf(p.scale, v, o));
@@ -801,7 +833,8 @@ namespace {
 
 void launch(const plora_plan& plan, const ClusterWork& cw, uint32_t layer, const uint32_t* projs,
             uint32_t np, const void* x, uint64_t x_stride, void* const* ys,
-            const uint64_t* y_strides, float scale, cudaStream_t stream) {
+            const uint64_t* y_strides, float scale, cudaStream_t stream, uint32_t n_layers = 1,
+            uint64_t x_lstride = 0, const uint64_t* y_lstrides = nullptr) {
   const plora_store& st = *plan.store;
   const ModelGeom& gm = st.geom;
   const ClusterGeom& g = cw.geom;
@@ -811,6 +844,13 @@ void launch(const plora_plan& plan, const ClusterWork& cw, uint32_t layer, const
   a.table = st.d_table;
   a.chunks = plan.d_cchunks + cw.chunks_off;
   for (uint32_t c = 0; c <= g.n_clusters; ++c) a.cl_off[c] = plan.ccl_off[cw.cl_off + c];
+  for (uint32_t c = 0; c < g.n_clusters; ++c) a.cl_jobs[c] = plan.ccl_jobs[cw.cl_off + c];
+  if (n_layers == 0 || n_layers * np > 256)
+    throw ValidationError("bf16 BGMV: n_layers x projections must be in [1, 256] per launch");
+  a.n_layers = n_layers;
+  a.np = np;
+  a.x_lstride_b = x_lstride * 2;
+  a.plu = gm.per_layer_unit;
   a.x = static_cast<const char*>(x);
   a.x_stride_b = x_stride * 2;
   a.log2_page = st.log2_page;
@@ -839,8 +879,10 @@ void launch(const plora_plan& plan, const ClusterWork& cw, uint32_t layer, const
   for (uint32_t i = 0; i < np; ++i) {
     a.y[i] = static_cast<char*>(ys[i]);
     a.y_stride_b[i] = y_strides[i] * 2;
+    a.y_lstride_b[i] = y_lstrides ? y_lstrides[i] * 2 : 0;
     a.blk_mult[i] = gm.blk_mult(layer, projs[i]);
-    a.fast = a.fast && a.blk_mult[i] % a.ks == 0 && (a.blk_mult[i] + a.d_in) % a.ns == 0;
+    a.fast = a.fast && a.blk_mult[i] % a.ks == 0 && (a.blk_mult[i] + a.d_in) % a.ns == 0 &&
+             (n_layers == 1 || a.plu % a.ks == 0);
   }
   a.trace = trace_buffer(g.n_clusters * g.cs * kTraceChunks * 128);
   cudaLaunchConfig_t cfg{};
@@ -880,6 +922,16 @@ void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const voi
   for (uint32_t i = 0; i < plan.n_layer_proj; ++i) projs[i] = i;
   launch(plan, plan.cwork_layer, layer, projs, plan.n_layer_proj, x, x_stride, ys, y_strides,
          scale, stream);
+}
+
+void launch_bgmv_cluster_layers(const plora_plan& plan, uint32_t layer0, uint32_t n_layers,
+                                const void* x, uint64_t x_stride, uint64_t x_lstride,
+                                void* const* ys, const uint64_t* y_strides,
+                                const uint64_t* y_lstrides, float scale, cudaStream_t stream) {
+  uint32_t projs[PLORA_MAX_PROJ];
+  for (uint32_t i = 0; i < plan.n_layer_proj; ++i) projs[i] = i;
+  launch(plan, plan.cwork_layer, layer0, projs, plan.n_layer_proj, x, x_stride, ys, y_strides,
+         scale, stream, n_layers, x_lstride, y_lstrides);
 }
 
 namespace {

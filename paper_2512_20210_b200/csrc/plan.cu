@@ -276,6 +276,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   cjobs.clear();
   cchunks.clear();
   ccl_off.clear();
+  ccl_jobs.clear();
   if (es == 2) {
     for (const Seg& s : segs)
       for (uint32_t tc = 0; tc < s.toks.size(); tc += kJobTok) {
@@ -335,8 +336,10 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
             cchunks.push_back(ch);
           }
         }
+        ccl_jobs.push_back(jord);
       }
       ccl_off.push_back(static_cast<uint32_t>(cchunks.size()) - cw.chunks_off);
+      ccl_jobs.push_back(0);  // keeps ccl_jobs indexed like ccl_off
     };
     for (uint32_t p = 0; p < g.m.n_proj; ++p) build(cwork[p], &p, 1);
     n_layer_proj = 0;

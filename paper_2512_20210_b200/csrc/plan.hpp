@@ -183,6 +183,7 @@ struct plora_plan {
   std::vector<plora::ClusterJob> cjobs;
   std::vector<plora::ClusterChunk> cchunks;
   std::vector<uint32_t> ccl_off;
+  std::vector<uint32_t> ccl_jobs;  // jobs per cluster list (indexed like ccl_off; 0 at each list's end entry)
   plora::ClusterChunk* d_cchunks = nullptr;
   plora::ClusterJob* d_cjobs = nullptr;
   char* h_pinned = nullptr;
@@ -230,4 +231,12 @@ void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, 
 void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const void* x,
                                uint64_t x_stride, void* const* ys, const uint64_t* y_strides,
                                float scale, cudaStream_t stream);
+// Layers [layer0, layer0 + n_layers), every projection, in one launch: the
+// clusters stay resident and stream layer l + 1's pages right behind layer
+// l's.  Layer l's x rows start l·x_lstride elements after x, projection p's
+// y rows y_lstrides[p] elements after the previous layer's.
+void launch_bgmv_cluster_layers(const plora_plan& plan, uint32_t layer0, uint32_t n_layers,
+                                const void* x, uint64_t x_stride, uint64_t x_lstride,
+                                void* const* ys, const uint64_t* y_strides,
+                                const uint64_t* y_lstrides, float scale, cudaStream_t stream);
 }  // namespace plora

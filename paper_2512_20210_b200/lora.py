@@ -270,6 +270,28 @@ def bgmv_layer(plan: BatchPlan, layer: int, x: torch.Tensor, ys: Sequence[torch.
     return ys
 
 
+def bgmv_layers(plan: BatchPlan, layer0: int, x: torch.Tensor, ys: Sequence[torch.Tensor],
+                scale: float = 1.0, stream: int | None = None) -> Sequence[torch.Tensor]:
+    """Layers [layer0, layer0 + n) of bgmv_layer in one launch, n = x.shape[0]:
+    x is [n, T, d_in] (layer i's rows at x[i]), ys[p] is [n, T, d_out[p]].
+    For inputs that are all ready at once; bit-identical to n bgmv_layer calls."""
+    shape = plan.store.shape
+    if len(ys) != shape.n_proj:
+        raise N.ValidationError(f"bgmv_layers needs {shape.n_proj} outputs, got {len(ys)}")
+    if x.dim() != 3 or any(y.dim() != 3 or y.shape[0] != x.shape[0] for y in ys):
+        raise N.ValidationError("bgmv_layers: x and every y must be [n_layers, T, d]")
+    for p, y in enumerate(ys):
+        _check_io(plan, p, x[0], y[0])
+    n = x.shape[0]
+    ptrs = (C.c_void_p * shape.n_proj)(*[y.data_ptr() for y in ys])
+    strides = (C.c_uint64 * shape.n_proj)(*[y.stride(1) for y in ys])
+    lstrides = (C.c_uint64 * shape.n_proj)(*[y.stride(0) for y in ys])
+    s = current_stream_handle(x.device) if stream is None else stream
+    N.check(N.lib().plora_bgmv_layers(plan.handle, layer0, n, x.data_ptr(), x.stride(1),
+                                      x.stride(0), ptrs, strides, lstrides, scale, s))
+    return ys
+
+
 def sgmv(plan: BatchPlan, layer: int, proj: int, x: torch.Tensor, y: torch.Tensor,
          scale: float = 1.0, stream: int | None = None) -> torch.Tensor:
     """y += scale · (x · Aᵀ) · Bᵀ per token (prefill path, tensor cores)."""

@@ -25,7 +25,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from paper_2512_20210_b200 import _native as N, synth  # noqa: E402
-from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, bgmv, bgmv_layer  # noqa: E402
+from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, bgmv, bgmv_layer,  # noqa: E402
+                                        bgmv_layers)
 
 K = 64
 
@@ -49,6 +50,10 @@ def main():
     y = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
     y2 = torch.randn(256, 4096, device="cuda").to(torch.bfloat16)
     call = (lambda: bgmv_layer(plan, 1, x, [y, y2])) if fused else (lambda: bgmv(plan, 1, 0, x, y))
+    if "--layers" in sys.argv:  # both layers in one launch (plora_bgmv_layers)
+        xl = torch.randn(2, 256, 4096, device="cuda").to(torch.bfloat16)
+        yl = torch.randn(2, 2, 256, 4096, device="cuda").to(torch.bfloat16)
+        call = lambda: bgmv_layers(plan, 0, xl, [yl[:, 0], yl[:, 1]])  # noqa: E731
     for _ in range(3):
         call()
     ctas = geom[0] * geom[6]

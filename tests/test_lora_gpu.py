@@ -315,3 +315,30 @@ def test_bgmv_layer_fused_equals_per_projection(cuda, page_bytes):
         assert torch.equal(fused[p], sep[p])
     ref = s.oracle(1, 1, x.cpu(), y0[1].cpu(), ta, scale=0.75)
     assert rel_err(fused[1], ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("page_bytes", [2048, 256])
+def test_bgmv_layers_multi_layer_launch_bit_identical(cuda, page_bytes):
+    """plora_bgmv_layers (several layers per launch, the clusters' chunk lists
+    repeated per layer) computes exactly what per-layer bgmv_layer calls do,
+    on strided per-layer views, and matches the oracle."""
+    from paper_2512_20210_b200.lora import bgmv_layer, bgmv_layers
+    cfg = synth.cfg2(n_layers=4, page_bytes=page_bytes)
+    s = Setup(cfg)
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    T = len(ta)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(3, T, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    y0 = torch.randn(3, 2, T, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    plan = BatchPlan(s.store, ta)
+    ref = y0.clone()
+    for i in range(3):
+        bgmv_layer(plan, 1 + i, x[i], [ref[i, 0], ref[i, 1]], 0.5)
+    got = y0.clone()
+    n0 = kernel_launch_count()
+    bgmv_layers(plan, 1, x, [got[:, 0], got[:, 1]], 0.5)
+    torch.cuda.synchronize()
+    assert kernel_launch_count() - n0 == 1
+    assert torch.equal(got, ref)
+    o = s.oracle(3, 1, x[2].cpu(), y0[2, 1].cpu(), ta, scale=0.5)
+    assert rel_err(got[2, 1], o) <= TOL_BF16
