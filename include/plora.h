@@ -492,6 +492,13 @@ int plora_predictor_buffer_at(const plora_predictor* p, uint64_t i, uint32_t* ad
  * each CTA, fields as documented in scripts/trace_bgmv.py (chunk 63 holds the
  * CTA start / end).  dev_buf = NULL disables tracing. */
 int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
+/* Diagnostics: the bf16 decode kernel behind plora_bgmv* — 0 thread-block
+ * clusters (bgmv_cluster.cu, default), 1 the streaming kernel
+ * (bgmv_stream.cu; measured alternative). */
+int plora_debug_set_bgmv_impl(int impl);
+/* Diagnostics for the streaming kernel: 1 consumers skip the math, 2 no
+ * weight copies (results are then wrong; timing ablation only). */
+int plora_debug_set_bgmv_flags(uint32_t flags);
 /* Launch geometry the plan chose for the bf16 decode op of projection
  * `proj`: out[0..7] = {cluster size, input slice, output slice, A-row ring
  * slots, Bᵀ-row ring slots, dynamic smem bytes, clusters, chunks}. */

@@ -407,6 +407,15 @@ void check_io(const plora_plan* plan, uint32_t layer, uint32_t proj, const void*
 
 }  // namespace plora
 
+namespace {
+int g_bgmv_impl = 0;  // bf16 decode kernel: 0 clusters (bgmv_cluster.cu), 1 streaming (bgmv_stream.cu)
+}  // namespace
+
+extern "C" int plora_debug_set_bgmv_impl(int impl) {
+  g_bgmv_impl = impl;
+  return 0;
+}
+
 extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                           uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                           plora_stream_t stream) {
@@ -417,9 +426,16 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     const ModelGeom& g = st.geom;
     const ProjWork& pw = plan->proj[proj];
     DeviceCtx ctx(st.device);
-    if (g.esize == 2) {  // bf16: the cluster op (bgmv_cluster.cu)
-      launch_bgmv_cluster(*plan, layer, proj, x, x_stride, y, y_stride, scale,
-                          static_cast<cudaStream_t>(stream));
+    if (g.esize == 2) {  // bf16: the streaming op (bgmv_stream.cu) or the cluster op
+      if (g_bgmv_impl != 1) {
+        launch_bgmv_cluster(*plan, layer, proj, x, x_stride, y, y_stride, scale,
+                            static_cast<cudaStream_t>(stream));
+      } else {
+        void* ys[1] = {y};
+        const uint64_t yst[1] = {y_stride};
+        launch_bgmv_stream(*plan, plan->swork[proj], layer, 1, x, x_stride, 0, ys, yst, nullptr,
+                           scale, static_cast<cudaStream_t>(stream));
+      }
       return 0;
     }
     if (pw.n_units == 0) return 0;  // no LoRA token in the batch
@@ -469,6 +485,12 @@ extern "C" int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_l
       if (y_layer_strides[p] % vec) throw ValidationError("layer strides must be multiples of 16 bytes");
       check_io(plan, layer0, p, x, x_stride, ys[p], y_strides[p]);
     }
+    if (g.esize == 2 && g_bgmv_impl == 1 && plan->swork_layer.np == g.m.n_proj) {
+      DeviceCtx ctx(st.device);
+      launch_bgmv_stream(*plan, plan->swork_layer, layer0, n_layers, x, x_stride, x_layer_stride,
+                         ys, y_strides, y_layer_strides, scale, static_cast<cudaStream_t>(stream));
+      return 0;
+    }
     const bool one = g.esize == 2 && plan->n_layer_proj == g.m.n_proj &&
                      n_layers * g.m.n_proj <= 256;
     if (one) {
@@ -501,6 +523,13 @@ extern "C" int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x,
       if (g.m.d_in[p] != g.m.d_in[0])
         throw ValidationError("plora_bgmv_layer: projections read different input widths");
       check_io(plan, layer, p, x, x_stride, ys[p], y_strides[p]);
+    }
+    if (g.esize == 2 && g_bgmv_impl == 1 && plan->swork_layer.np == g.m.n_proj) {
+      DeviceCtx ctx(st.device);
+      const uint64_t zero[PLORA_MAX_PROJ] = {};
+      launch_bgmv_stream(*plan, plan->swork_layer, layer, 1, x, x_stride, 0, ys, y_strides, zero,
+                         scale, static_cast<cudaStream_t>(stream));
+      return 0;
     }
     if (g.esize == 2 && plan->n_layer_proj == g.m.n_proj) {
       DeviceCtx ctx(st.device);

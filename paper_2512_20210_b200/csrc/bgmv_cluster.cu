@@ -299,7 +299,7 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
   uint2* georing = reinterpret_cast<uint2*>(tblring + kAhead * 32);  // [kAhead][32] {inpage, dst | len << 16}
   const uint32_t* recg = reinterpret_cast<const uint32_t*>(p.chunks);
   const Slice sl(p, crank);
-  const uint64_t ef = ptx::policy_evict_first();
+  const uint64_t ef = ptx::policy_evict_first(), el = ptx::policy_evict_last();
   const uint32_t L = p.log2_page;
   PieceGeom pg;
   pg.KB = sl.kb * 2;
@@ -361,9 +361,10 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
     ptx::mbar_wait(&emptyb[s], ph ^ 1u);
     if (pw == 0 && lane == 0) trace_put(p, idx, 5);
     uint32_t bytes = pc.len;
+    const uint64_t pol = (c.flags & kChunkReuse) ? el : ef;  // pages read again by later jobs stay in L2
     if (pc.len)
       ptx::bulk_g2s_hint(sb + pc.dst, p.arena + (static_cast<uint64_t>(phys) << L) + pc.inpage,
-                         pc.len, &fullb[s], ef);
+                         pc.len, &fullb[s], pol);
     if (!p.fast) {  // small pages: the role's pieces past the first 32, synchronous lookups
       for (uint32_t q = 32 + lane; q < c.nrows * (isb ? pg.pprB : pg.pprA); q += 32) {
         Piece x;
@@ -372,7 +373,7 @@ __device__ void page_producer(const CArgs& p, char* smem, uint32_t crank, uint32
           ptx::bulk_g2s_hint(sb + x.dst,
                              p.arena + (static_cast<uint64_t>(__ldg(p.table + c.table_off + page)) << L) +
                                  x.inpage,
-                             x.len, &fullb[s], ef);
+                             x.len, &fullb[s], pol);
           bytes += x.len;
         }
       }

@@ -288,6 +288,14 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
         cjobs.push_back(j);
       }
     const uint32_t nj = static_cast<uint32_t>(cjobs.size());
+    std::vector<uint8_t> multi(nj, 0);  // the job's adapter has more than one job
+    {
+      uint32_t k = 0;
+      for (const Seg& s : segs) {
+        const uint32_t n_j = (static_cast<uint32_t>(s.toks.size()) + kJobTok - 1) / kJobTok;
+        for (uint32_t q = 0; q < n_j; ++q) multi[k++] = n_j > 1;
+      }
+    }
     // One chunk list per launch: the jobs of the given projections (tagged
     // with their index in the launch) LPT-assigned to clusters by bytes
     // (heaviest first onto the least-loaded cluster, ties: lowest index).
@@ -332,7 +340,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
             ch.row0 = static_cast<uint16_t>(r0);
             ch.nrows = static_cast<uint8_t>(std::min(kChunkRows, j.rank - r0));
             ch.flags = static_cast<uint8_t>((r0 == 0 ? kChunkFirst : 0) |
-                                            (r0 + kChunkRows >= j.rank ? kChunkLast : 0));
+                                            (r0 + kChunkRows >= j.rank ? kChunkLast : 0) |
+                                            (multi[w % nj] ? kChunkReuse : 0));
             cchunks.push_back(ch);
           }
         }
@@ -355,6 +364,139 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     }
   }
 
+  // ---- bf16 streaming BGMV (bgmv_stream.cu): jobs of <= s_jt tokens, S / E
+  // items, list-scheduled over one CTA per SM
+  stitems.clear();
+  stcta.clear();
+  for (uint32_t p = 0; p < PLORA_MAX_PROJ; ++p) swork[p] = StreamWork{};
+  swork_layer = StreamWork{};
+  s_njobs = 0;
+  s_vplane = 0;
+  if (es == 2) {
+    uint32_t maxtok = 0;
+    for (const Seg& sg : segs) maxtok = std::max<uint32_t>(maxtok, static_cast<uint32_t>(sg.toks.size()));
+    s_jt = maxtok > 4 ? 8 : 4;
+    struct SJob {
+      uint32_t rank, table_off, ntok, v_off, tok[8];
+    };
+    std::vector<SJob> jobs;
+    uint64_t voff = 0;
+    for (uint32_t si : order) {  // largest rank first
+      const Seg& sg = segs[si];
+      for (uint32_t tc = 0; tc < sg.toks.size(); tc += s_jt) {
+        SJob j{};
+        j.rank = sg.rank;
+        j.table_off = sg.table_off;
+        j.ntok = std::min<uint32_t>(s_jt, static_cast<uint32_t>(sg.toks.size()) - tc);
+        for (uint32_t t = 0; t < j.ntok; ++t) j.tok[t] = sg.toks[tc + t];
+        j.v_off = static_cast<uint32_t>(voff);
+        voff += static_cast<uint64_t>((sg.rank + 15) & ~15u) * s_jt;  // rows padded to 16 (kept zero)
+        jobs.push_back(j);
+      }
+    }
+    if (voff > 0xffffffffull) throw ValidationError("batch too large for one plan");
+    s_njobs = static_cast<uint32_t>(jobs.size());
+    s_vplane = (voff + 3) & ~3ull;
+    const uint32_t max_ctas = stream_max_ctas(st.device, s_jt);
+    auto build_sw = [&](StreamWork& w, const uint32_t* projs, uint32_t np) {
+      w = StreamWork{};
+      w.np = np;
+      for (uint32_t i = 0; i < np; ++i) w.projs[i] = projs[i];
+      if (jobs.empty()) return;
+      const uint32_t din = g.m.d_in[projs[0]], dout = g.m.d_out[projs[0]];
+      const uint32_t ne = (dout + kStreamKC - 1) / kStreamKC;
+      // cost model: bytes streamed per SM (x / y rows counted at L2 / HBM
+      // weight) plus a fixed per-item overhead
+      const double ovh = 4096.0;
+      struct Cand {
+        StreamItem it;
+        double cost;
+        uint32_t key;  // job · np + launch projection
+      };
+      std::vector<Cand> sc, ec;
+      for (uint32_t jn = 0; jn < jobs.size(); ++jn) {
+        const SJob& j = jobs[jn];
+        const uint32_t ns = j.rank * j.ntok;  // v elements: each released on its own
+        for (uint32_t i = 0; i < np; ++i) {
+          StreamItem base{};
+          base.job = jn;
+          base.table_off = j.table_off;
+          base.rank_ntok = j.rank | (j.ntok << 16);
+          base.v_off = j.v_off;
+          base.ns_ne = ns | (ne << 16);
+          for (uint32_t t = 0; t < 8; ++t) base.tok[t] = t < j.ntok ? j.tok[t] : 0u;
+          for (uint32_t r0 = 0; r0 < j.rank; r0 += 16) {
+            Cand c{base, 0.0, jn * np + i};
+            c.it.kind = i;
+            c.it.off = r0;
+            c.it.n = std::min<uint32_t>(16, j.rank - r0);
+            c.cost = 2.0 * c.it.n * din + 1.0 * j.ntok * din + ovh;
+            sc.push_back(c);
+          }
+          for (uint32_t c0 = 0; c0 < dout; c0 += kStreamKC) {
+            Cand c{base, 0.0, jn * np + i};
+            c.it.kind = kStreamExpand | i;
+            c.it.off = c0;
+            c.it.n = std::min<uint32_t>(kStreamKC, dout - c0);
+            c.cost = 2.0 * j.rank * c.it.n + 4.0 * j.ntok * c.it.n + ovh;
+            ec.push_back(c);
+          }
+        }
+      }
+      const uint32_t ctas = std::min<uint32_t>(max_ctas, static_cast<uint32_t>(sc.size() + ec.size()));
+      std::vector<double> load(ctas, 0.0);
+      std::vector<std::vector<uint32_t>> lists_s(ctas), lists_e(ctas);
+      std::vector<double> ready(jobs.size() * np, 0.0);
+      using Load = std::pair<double, uint32_t>;
+      std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+      for (uint32_t c = 0; c < ctas; ++c) heap.emplace(0.0, c);
+      for (uint32_t k = 0; k < sc.size(); ++k) {  // S items in job order onto the least-loaded CTA
+        Load l = heap.top();
+        heap.pop();
+        const double fin = l.first + sc[k].cost;
+        lists_s[l.second].push_back(k);
+        ready[sc[k].key] = std::max(ready[sc[k].key], fin);
+        heap.emplace(fin, l.second);
+      }
+      // E items by the simulated readiness of their job (the producer runs
+      // about a ring ahead of the consumers: margin), heaviest first
+      const double margin = 160.0 * 1024;
+      std::vector<uint32_t> eo(ec.size());
+      std::iota(eo.begin(), eo.end(), 0u);
+      std::stable_sort(eo.begin(), eo.end(), [&](uint32_t a, uint32_t b) {
+        const double ra = ready[ec[a].key], rb = ready[ec[b].key];
+        return ra != rb ? ra < rb : ec[a].cost > ec[b].cost;
+      });
+      for (uint32_t k : eo) {
+        Load l = heap.top();
+        heap.pop();
+        const double start = std::max(l.first, ready[ec[k].key] + margin);
+        lists_e[l.second].push_back(k);
+        heap.emplace(start + ec[k].cost, l.second);
+      }
+      w.items_off = static_cast<uint32_t>(stitems.size());
+      w.cta_off = static_cast<uint32_t>(stcta.size());
+      w.ctas = ctas;
+      uint32_t n = 0;
+      for (uint32_t c = 0; c < ctas; ++c) {
+        stcta.push_back(n);
+        for (uint32_t k : lists_s[c]) stitems.push_back(sc[k].it);
+        for (uint32_t k : lists_e[c]) stitems.push_back(ec[k].it);
+        n += static_cast<uint32_t>(lists_s[c].size() + lists_e[c].size());
+      }
+      stcta.push_back(n);
+    };
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) build_sw(swork[p], &p, 1);
+    bool same = g.m.n_proj > 1;
+    for (uint32_t p = 1; p < g.m.n_proj; ++p)
+      same = same && g.m.d_in[p] == g.m.d_in[0] && g.m.d_out[p] == g.m.d_out[0];
+    if (same) {
+      uint32_t all[PLORA_MAX_PROJ];
+      for (uint32_t p = 0; p < g.m.n_proj; ++p) all[p] = p;
+      build_sw(swork_layer, all, g.m.n_proj);
+    }
+  }
+
   // ---- upload the device-side work lists in one copy from a pinned
   // staging buffer (cluster chunk offsets travel as kernel parameters)
   auto align = [](uint64_t v) { return (v + 255) & ~255ull; };
@@ -371,6 +513,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       {cjobs.data(), cjobs.size() * sizeof(ClusterJob), reinterpret_cast<void**>(&d_cjobs)},
       {sitems.data(), sitems.size() * sizeof(SgmvItem), reinterpret_cast<void**>(&d_sitems)},
       {scta.data(), scta.size() * sizeof(uint32_t), reinterpret_cast<void**>(&d_scta)},
+      {stitems.data(), stitems.size() * sizeof(StreamItem), reinterpret_cast<void**>(&d_stitems)},
+      {stcta.data(), stcta.size() * sizeof(uint32_t), reinterpret_cast<void**>(&d_stcta)},
   };
   uint64_t total = 0;
   for (const Part& pt : parts) total += align(pt.bytes);
@@ -431,6 +575,25 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       PLORA_CUDA(cudaMalloc(&d_vbuf, vbuf_cap));
     }
   }
+  if (es == 2 && s_njobs > 0) {  // streaming BGMV: v planes and counters for every (layer, proj)
+    const uint64_t planes = static_cast<uint64_t>(g.m.n_layers) * g.m.n_proj;
+    const uint64_t need_v = planes * s_vplane, need_c = planes * 2ull * s_njobs;
+    if (sv_cap < need_v || scnt_cap < need_c) {
+      PLORA_CUDA(cudaStreamSynchronize(stream));
+      cudaFree(d_sv);
+      cudaFree(d_scnt);
+      d_sv = nullptr;
+      d_scnt = nullptr;
+      sv_cap = std::max(need_v, sv_cap);
+      scnt_cap = std::max(need_c, scnt_cap);
+      PLORA_CUDA(cudaMalloc(&d_sv, sv_cap * sizeof(float)));
+      PLORA_CUDA(cudaMalloc(&d_scnt, scnt_cap * sizeof(uint32_t)));
+      // v pad rows (rank .. rank rounded up to 16) are never written: zero them once
+      PLORA_CUDA(cudaMemsetAsync(d_sv, 0, sv_cap * sizeof(float), stream));
+    }
+    // every call leaves the counters at zero; a rebuilt plan starts from zero too
+    PLORA_CUDA(cudaMemsetAsync(d_scnt, 0, need_c * sizeof(uint32_t), stream));
+  }
   if (sync_cap < 2ull + n_seg) {
     if (d_sync) {
       PLORA_CUDA(cudaStreamSynchronize(stream));
@@ -479,6 +642,8 @@ void plora_plan_destroy(plora_plan* plan) {
   cudaFreeHost(plan->h_pinned);
   cudaFree(plan->d_buf);
   cudaFree(plan->d_v);
+  cudaFree(plan->d_sv);
+  cudaFree(plan->d_scnt);
   cudaFree(plan->d_sync);
   cudaFree(plan->d_vpart);
   cudaFree(plan->d_vbuf);

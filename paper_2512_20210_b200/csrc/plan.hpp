@@ -90,6 +90,10 @@ struct ProjWork {
 constexpr uint32_t kJobTok = 4;
 constexpr uint32_t kChunkRows = 8;
 constexpr uint32_t kChunkFirst = 1, kChunkLast = 2;
+// the job's adapter has further jobs in the batch (more than kJobTok tokens):
+// its pages are read again, so they are kept in L2 (evict_last) instead of
+// streamed through it (evict_first)
+constexpr uint32_t kChunkReuse = 4;
 
 struct ClusterJob {  // 32 bytes; uploaded for the tensor-parallel path (tp.cu)
   uint32_t table_off;
@@ -131,6 +135,37 @@ struct ClusterWork {
   ClusterGeom geom;
   uint32_t chunks_off = 0;  // into the chunk array
   uint32_t cl_off = 0;      // into the cluster offset array (n_clusters + 1 entries)
+};
+
+// ------------------------------------------------ bf16 BGMV (streaming)
+// bgmv_stream.cu: persistent, one CTA per SM, no cross-CTA exchange.  A job
+// is <= JT tokens of one adapter at one (layer, proj).  Its shrink is cut
+// into S items (<= 16 rank rows, full K: v = x·A[rows]ᵀ exact in fp32, written
+// to a v plane) and its expand into E items (one column block of <= 1024
+// output columns, all rank rows: y[:, block] += scale · v · Bᵀ[:, block]);
+// an E item waits (acquire) on its job's v counter.  Every item streams
+// 16 weight rows × <= 1024 elements per stage.
+constexpr uint32_t kStreamKC = 1024;     // elements per stage row segment
+constexpr uint32_t kStreamExpand = 0x80000000u;
+struct StreamItem {  // 64 bytes, fully resolved on the host
+  uint32_t kind;       // kStreamExpand | launch projection index
+  uint32_t job;        // job index (counter slot within a (layer, proj) plane)
+  uint32_t table_off;  // adapter's first entry in the device page table
+  uint32_t rank_ntok;  // rank | ntok << 16
+  uint32_t off;        // S: first rank row; E: first output column
+  uint32_t n;          // S: rank rows (<= 16); E: columns (<= kStreamKC)
+  uint32_t v_off;      // floats into a v plane: the job's [rank][JT] block
+  uint32_t ns_ne;      // v elements of the job (rank · ntok, each released by its own store) | E items << 16
+  uint32_t tok[8];     // x / y rows of the job's tokens
+};
+static_assert(sizeof(StreamItem) == 64, "StreamItem layout");
+
+struct StreamWork {  // one launch variant (a projection, or every projection of a layer)
+  uint32_t items_off = 0;  // into the item array
+  uint32_t cta_off = 0;    // into the CTA offset array (ctas + 1 entries)
+  uint32_t ctas = 0;
+  uint32_t np = 0;
+  uint32_t projs[PLORA_MAX_PROJ] = {};
 };
 
 // ---------------------------------------------------------------- SGMV
@@ -214,6 +249,22 @@ struct plora_plan {
   std::vector<uint32_t> scta;
   plora::SgmvItem* d_sitems = nullptr;
   uint32_t* d_scta = nullptr;
+  // bf16 streaming BGMV (bgmv_stream.cu)
+  uint32_t s_jt = 4;       // tokens per job (4 or 8)
+  uint32_t s_njobs = 0;    // jobs per (layer, proj) plane
+  uint64_t s_vplane = 0;   // floats per (layer, proj) v plane
+  plora::StreamWork swork[PLORA_MAX_PROJ];
+  plora::StreamWork swork_layer;  // every projection of a layer (equal shapes), ctas 0: none
+  std::vector<plora::StreamItem> stitems;
+  std::vector<uint32_t> stcta;
+  plora::StreamItem* d_stitems = nullptr;
+  uint32_t* d_stcta = nullptr;
+  float* d_sv = nullptr;       // v planes: n_layers · n_proj · s_vplane floats
+  uint64_t sv_cap = 0;
+  uint32_t* d_scnt = nullptr;  // per plane: s_njobs S-item counters, then s_njobs E-done counters
+  uint64_t scnt_cap = 0;
+  void build_stream(const std::vector<std::vector<uint32_t>>& seg_toks,
+                    const std::vector<uint32_t>& seg_rank, const std::vector<uint32_t>& seg_table);
   cudaEvent_t upload_done = nullptr;
 
   void build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream);
@@ -227,6 +278,14 @@ uint64_t* trace_buffer(uint64_t need_bytes);
 void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, const void* x,
                          uint64_t x_stride, void* y, uint64_t y_stride, float scale,
                          cudaStream_t stream);
+// Streaming bf16 BGMV (bgmv_stream.cu): the projections `w` was built for,
+// layers [layer0, layer0 + n_layers); layer layer0 + i reads x + i·x_lstride
+// and updates ys[j] + i·y_lstrides[j] (elements).
+void launch_bgmv_stream(const plora_plan& plan, const StreamWork& w, uint32_t layer0,
+                        uint32_t n_layers, const void* x, uint64_t x_stride, uint64_t x_lstride,
+                        void* const* ys, const uint64_t* y_strides, const uint64_t* y_lstrides,
+                        float scale, cudaStream_t stream);
+uint32_t stream_max_ctas(int device, uint32_t jt);
 // Every projection of `layer` (they read the same x) in one launch.
 void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const void* x,
                                uint64_t x_stride, void* const* ys, const uint64_t* y_strides,

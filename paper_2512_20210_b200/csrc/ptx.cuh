@@ -83,6 +83,12 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
 // 2-D TMA tensor tile load (tensor map in param/const space).
 // 2-D TMA gather of four rows r0..r3 (the tensor map's box is {cols, 1});
 // they land in four consecutive smem rows (swizzled by their smem address).

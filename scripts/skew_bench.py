@@ -34,7 +34,10 @@ def main():
         store.register(a, r)
         store.write_pages(a, synth.adapter_image(shape, r, a, device="cuda").view(torch.uint8))
         store.publish(a)
-    out = {}
+    from paper_2512_20210_b200 import _native as N
+    impl = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    N.check(N.lib().plora_debug_set_bgmv_impl(impl))
+    out = {"impl": impl}
     for name, ta in (("skewed", skewed_assignment(hot=hot)),
                      ("uniform", synth.token_assignment(128, 4))):
         T = len(ta)

@@ -342,3 +342,36 @@ def test_bgmv_layers_multi_layer_launch_bit_identical(cuda, page_bytes):
     assert torch.equal(got, ref)
     o = s.oracle(3, 1, x[2].cpu(), y0[2, 1].cpu(), ta, scale=0.5)
     assert rel_err(got[2, 1], o) <= TOL_BF16
+
+
+@pytest.mark.parametrize("tokens_per_adapter", [2, 6])
+def test_streaming_kernel_parity(cuda, tokens_per_adapter):
+    """The alternative streaming decode kernel (bgmv_stream.cu, selected with
+    plora_debug_set_bgmv_impl(1)): per-call, per-layer and multi-layer
+    launches against the oracle, 4- and 8-token jobs."""
+    from paper_2512_20210_b200 import _native as N
+    from paper_2512_20210_b200.lora import bgmv_layer, bgmv_layers
+    cfg = synth.cfg2(n_layers=3)
+    s = Setup(cfg)
+    ta = synth.token_assignment(cfg.n_adapters, tokens_per_adapter)
+    T = len(ta)
+    x = synth.activations(T, 4096, torch.bfloat16, "x", salt=4)
+    y0 = synth.activations(T, 4096, torch.bfloat16, "y", salt=4)
+    N.check(N.lib().plora_debug_set_bgmv_impl(1))
+    try:
+        plan = BatchPlan(s.store, ta)
+        yd = y0.cuda()
+        bgmv(plan, 2, 1, x.cuda(), yd, 0.5)
+        torch.cuda.synchronize()
+        assert rel_err(yd, s.oracle(2, 1, x, y0, ta, scale=0.5)) <= TOL_BF16
+        xl = x.cuda().unsqueeze(0).repeat(2, 1, 1)
+        yl = y0.cuda().view(1, 1, T, 4096).repeat(2, 2, 1, 1)
+        ref = yl.clone()
+        for i in range(2):
+            bgmv_layer(plan, 1 + i, xl[i], [ref[i, 0], ref[i, 1]])
+        bgmv_layers(plan, 1, xl, [yl[:, 0], yl[:, 1]])
+        torch.cuda.synchronize()
+        assert torch.equal(yl, ref)
+        assert rel_err(yl[1, 0], s.oracle(2, 0, x, y0, ta)) <= TOL_BF16
+    finally:
+        N.check(N.lib().plora_debug_set_bgmv_impl(0))
