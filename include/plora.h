@@ -471,6 +471,11 @@ int plora_predictor_roll_to(plora_predictor* p, double t_ms);
 int plora_predictor_train_step(plora_predictor* p, double* loss);
 /* Predictions for every known adapter in key order; returns the count (may
  * exceed cap; only cap entries written) or a negative status. */
+/* Run predict_all's LSTM forward on CUDA device `device` (FP64, the same
+ * summation order as the host path; differs only by exp/tanh rounding), or
+ * on the host threads (device = -1, the default).  New for the 100 ms
+ * prediction round at production adapter counts. */
+int plora_predictor_set_device(plora_predictor* p, int device);
 int64_t plora_predictor_predict_all(plora_predictor* p, double now_ms, uint32_t* adapters,
                                     double* probs, uint64_t cap);
 int plora_predictor_window(const plora_predictor* p, uint32_t adapter, double* out);

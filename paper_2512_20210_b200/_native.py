@@ -233,6 +233,7 @@ _SIGS = {
     "plora_predictor_observe": (_int, [_vp, _u32, _dbl]),
     "plora_predictor_roll_to": (_int, [_vp, _dbl]),
     "plora_predictor_train_step": (_int, [_vp, _P(_dbl)]),
+    "plora_predictor_set_device": (_int, [_vp, C.c_int]),
     "plora_predictor_predict_all": (_i64, [_vp, _dbl, _P(_u32), _P(_dbl), _u64]),
     "plora_predictor_window": (_int, [_vp, _u32, _P(_dbl)]),
     "plora_predictor_known": (_int, [_vp, _u32]),

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "predictor_gpu.hpp"
 
 namespace plora {
 namespace {
@@ -35,6 +36,38 @@ double sigmoid(double x) {  // lstm.cpp:12-16
 double clamped_ce(double p, double y) {  // lstm.cpp:22-25
   double q = std::min(1.0 - kClamp, std::max(kClamp, p));
   return -(y * std::log(q) + (1.0 - y) * std::log(1.0 - q));
+}
+
+// z[r] = b[r] + Σ_k W[k·G + r]·x[k] + Σ_k U[k·G + r]·h[k] for the G = 4H gate
+// rows, summed in that order (blocks of 32 rows kept in registers across k).
+// Cloned per host ISA; with -ffp-contract=off every clone rounds identically.
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void gate_sums(const double* b, const double* W, const double* U, const double* x,
+               const double* h, std::size_t in, std::size_t H, double* z) {
+  constexpr std::size_t kRB = 32;
+  const std::size_t G = 4 * H;
+  std::size_t r0 = 0;
+  for (; r0 + kRB <= G; r0 += kRB) {
+    double acc[kRB];
+    for (std::size_t i = 0; i < kRB; ++i) acc[i] = b[r0 + i];
+    for (std::size_t k = 0; k < in; ++k) {
+      const double xv = x[k];
+      const double* col = W + k * G + r0;
+      for (std::size_t i = 0; i < kRB; ++i) acc[i] += col[i] * xv;
+    }
+    for (std::size_t k = 0; k < H; ++k) {
+      const double hv = h[k];
+      const double* col = U + k * G + r0;
+      for (std::size_t i = 0; i < kRB; ++i) acc[i] += col[i] * hv;
+    }
+    for (std::size_t i = 0; i < kRB; ++i) z[r0 + i] = acc[i];
+  }
+  for (std::size_t r = r0; r < G; ++r) {  // a last partial block
+    double a = b[r];
+    for (std::size_t k = 0; k < in; ++k) a += W[k * G + r] * x[k];
+    for (std::size_t k = 0; k < H; ++k) a += U[k * G + r] * h[k];
+    z[r] = a;
+  }
 }
 
 template <class F>
@@ -99,6 +132,22 @@ class Lstm {
   }
 
   const plora_lstm_config& cfg() const { return c_; }
+  GpuLstmShape gpu_shape() const {
+    GpuLstmShape s{};
+    s.hidden = c_.hidden;
+    s.embedding_dim = c_.embedding_dim;
+    s.window = c_.window;
+    s.layers = c_.layers;
+    for (uint32_t l = 0; l < c_.layers && l < 4; ++l) {
+      s.w_off[l] = w_off_[l];
+      s.u_off[l] = u_off_[l];
+      s.b_off[l] = b_off_[l];
+    }
+    s.head_w = head_w_off_;
+    s.head_b = head_b_off_;
+    s.emb = emb_off_;
+    return s;
+  }
   std::vector<double>& theta() { return theta_; }
   const std::vector<double>& theta() const { return theta_; }
 
@@ -172,11 +221,66 @@ class Lstm {
     return logit;
   }
 
+  // Inference over many examples (predict_all): examples in chunks of kFwdChunk
+  // share every pass over W / U (the reference's batched Eigen products,
+  // lstm.cpp:130-161), the gate sums of each example accumulated in the same
+  // order as logit_one, so the result is bit-identical to it.
+  static constexpr std::size_t kFwdChunk = 16;
+  void logits_chunk(const Example* ex, std::size_t n, double* out) const {
+    const std::size_t H = c_.hidden, E = c_.embedding_dim, T = c_.window, G = 4 * H;
+    const std::size_t in_max = std::max<std::size_t>(in0_, H);
+    std::vector<double> x(n * T * in_max), xn(n * T * H), z(n * G), h(n * H), c(n * H);
+    for (std::size_t e = 0; e < n; ++e)
+      for (std::size_t t = 0; t < T; ++t) {
+        double* xt = x.data() + (e * T + t) * in0_;
+        xt[0] = ex[e].window[t];
+        for (std::size_t q = 0; q < E; ++q) xt[1 + q] = theta_[emb_off_ + ex[e].adapter * E + q];
+      }
+    std::size_t in = in0_;
+    for (uint32_t l = 0; l < c_.layers; ++l) {
+      const double* W = theta_.data() + w_off_[l];
+      const double* U = theta_.data() + u_off_[l];
+      const double* b = theta_.data() + b_off_[l];
+      std::fill(h.begin(), h.end(), 0.0);
+      std::fill(c.begin(), c.end(), 0.0);
+      for (std::size_t t = 0; t < T; ++t) {
+        // z = b + W·x_t + U·h, per (example, gate row) summed over k in order
+        for (std::size_t e = 0; e < n; ++e)
+          gate_sums(b, W, U, x.data() + (e * T + t) * in, h.data() + e * H, in, H, z.data() + e * G);
+        for (std::size_t e = 0; e < n; ++e) {
+          const double* ze = z.data() + e * G;
+          double* he = h.data() + e * H;
+          double* ce = c.data() + e * H;
+          for (std::size_t j = 0; j < H; ++j) {
+            const double gi = sigmoid(ze[j]), gf = sigmoid(ze[H + j]);
+            const double gg = std::tanh(ze[2 * H + j]), go = sigmoid(ze[3 * H + j]);
+            const double ct = gf * ce[j] + gi * gg, ht = go * std::tanh(ct);
+            ce[j] = ct;
+            he[j] = ht;
+            xn[(e * T + t) * H + j] = ht;  // feeds the next layer
+          }
+        }
+      }
+      x.swap(xn);
+      in = H;
+    }
+    for (std::size_t e = 0; e < n; ++e) {
+      double logit = theta_[head_b_off_];
+      for (std::size_t j = 0; j < H; ++j) logit += theta_[head_w_off_ + j] * h[e * H + j];
+      out[e] = logit;
+    }
+  }
+
   std::vector<double> forward(const std::vector<Example>& batch) const {
     validate_batch(batch);
     std::vector<double> out(batch.size());
-    parallel_for(batch.size(), 32, [&](std::size_t lo, std::size_t hi) {
-      for (std::size_t i = lo; i < hi; ++i) out[i] = sigmoid(logit_one(batch[i], nullptr));
+    const std::size_t nch = (batch.size() + kFwdChunk - 1) / kFwdChunk;
+    parallel_for(nch, 1, [&](std::size_t lo, std::size_t hi) {
+      for (std::size_t q = lo; q < hi; ++q) {
+        const std::size_t b0 = q * kFwdChunk, n = std::min(kFwdChunk, batch.size() - b0);
+        logits_chunk(batch.data() + b0, n, out.data() + b0);
+        for (std::size_t i = b0; i < b0 + n; ++i) out[i] = sigmoid(out[i]);
+      }
     });
     return out;
   }
@@ -369,6 +473,12 @@ class Online {
   }
 
   Lstm& model() { return model_; }
+  // predict_all's forward on a GPU (device >= 0) or on the host (-1)
+  void set_device(int device) {
+    gpu_.reset(device >= 0 ? new GpuLstm(device) : nullptr);
+    cache_interval_ = -1;  // recompute on the next call
+  }
+  int device() const { return gpu_ ? gpu_->device() : -1; }
 
   void observe(uint32_t adapter, double t_ms) {  // predictor.cpp:86-98
     if (adapter >= series_.size()) throw ValidationError("adapter index out of range in observe()");
@@ -416,7 +526,18 @@ class Online {
       batch.push_back(std::move(ex));
       ids.push_back(a);
     }
-    const auto probs = model_.forward(batch);
+    std::vector<double> probs;
+    if (gpu_) {  // FP64 forward on the device (plora_predictor_set_device)
+      const std::size_t T = model_.cfg().window;
+      std::vector<double> win(batch.size() * T);
+      for (std::size_t i = 0; i < batch.size(); ++i)
+        std::copy(batch[i].window.begin(), batch[i].window.end(), win.begin() + i * T);
+      probs.resize(batch.size());
+      gpu_->forward(model_.gpu_shape(), model_.theta().data(), model_.theta().size(), ids.data(),
+                    win.data(), ids.size(), probs.data());
+    } else {
+      probs = model_.forward(batch);
+    }
     cache_.resize(ids.size());
     for (std::size_t i = 0; i < ids.size(); ++i)
       cache_[i] = {ids[i], std::min(1.0 - kProbEps, std::max(kProbEps, probs[i]))};
@@ -507,6 +628,7 @@ class Online {
 
   plora_predictor_config cfg_;
   Lstm model_;
+  std::unique_ptr<GpuLstm> gpu_;
   std::vector<Series> series_;
   int64_t interval_ = 0;
   uint64_t observed_ = 0, train_steps_ = 0, known_ = 0;
@@ -672,11 +794,32 @@ int plora_predictor_train_step(plora_predictor* p, double* loss) {
   return guard([&] { return p->p.train_step(loss) ? 1 : 0; });
 }
 
+int plora_predictor_set_device(plora_predictor* p, int device) {
+  return guard([&] {
+    if (!p) throw ValidationError("null predictor");
+    try {
+      p->p.set_device(device);
+    } catch (const std::runtime_error& e) {
+      throw CudaError(e.what());
+    }
+    return 0;
+  });
+}
+
 int64_t plora_predictor_predict_all(plora_predictor* p, double now_ms, uint32_t* adapters,
                                     double* probs, uint64_t cap) {
   int64_t n = 0;
   const int rc = guard([&] {
-    const auto& v = p->p.predict_all(now_ms);
+    const std::vector<std::pair<uint32_t, double>>* vp = nullptr;
+    try {
+      vp = &p->p.predict_all(now_ms);
+    } catch (const std::runtime_error& e) {  // GPU forward failures are CUDA errors
+      if (dynamic_cast<const ValidationError*>(&e) || dynamic_cast<const ConfigError*>(&e) ||
+          dynamic_cast<const ParseError*>(&e) || dynamic_cast<const CudaError*>(&e))
+        throw;
+      throw CudaError(e.what());
+    }
+    const auto& v = *vp;
     n = static_cast<int64_t>(v.size());
     for (uint64_t i = 0; i < v.size() && i < cap; ++i) {
       adapters[i] = v[i].first;

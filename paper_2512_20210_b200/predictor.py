@@ -242,6 +242,10 @@ class OnlinePredictor:
     def roll_to(self, t_ms: float) -> None:
         N.check(N.lib().plora_predictor_roll_to(self._h, t_ms))
 
+    def set_device(self, device: int) -> None:
+        """predict_all's LSTM forward on CUDA `device` (FP64), or the host (-1)."""
+        N.check(N.lib().plora_predictor_set_device(self._h, int(device)))
+
     def predict_arrays(self, now_ms: float):
         """(adapters uint32[k], probabilities f64[k]) for every known adapter."""
         n = N.lib().plora_predictor_predict_all(

@@ -357,15 +357,21 @@ def test_online_predictions_match_numpy_oracle():
 
 
 def test_predict_all_production_scale_speed():
-    # 1000 known adapters at the production shape: one predict_all must stay
-    # well inside the reference's 100 ms prefetch interval budget
+    # 1000 known adapters at the production shape: a steady-state predict_all
+    # (the round after warm-up) must fit the reference's 100 ms prediction
+    # interval on the host threads; the GPU forward
+    # (plora_predictor_set_device, tests/test_predictor_gpu.py) is the 5 ms path
+    import statistics
     import time
     cfg = OnlinePredictorConfig(model=PredictorConfig(num_adapters=1000), train_every=10 ** 9)
     pred = OnlinePredictor(cfg, 1)
     for a in range(1000):
         pred.observe(a, float(a))
-    t0 = time.perf_counter()
-    ids, p = pred.predict_arrays(1500.0)
-    dt = time.perf_counter() - t0
-    assert len(ids) == 1000 and np.all((p > 0) & (p < 1))
-    assert dt < float(os.environ.get("PLORA_PREDICT_BUDGET_S", "5.0"))
+    times = []
+    for i in range(7):  # a new interval each call: no cached round
+        t0 = time.perf_counter()
+        ids, p = pred.predict_arrays(1500.0 + 1000.0 * i)
+        times.append(time.perf_counter() - t0)
+        assert len(ids) == 1000 and np.all((p > 0) & (p < 1))
+    budget = float(os.environ.get("PLORA_PREDICT_BUDGET_S", "0.1"))
+    assert statistics.median(times[2:]) < budget, times
