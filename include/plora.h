@@ -374,7 +374,26 @@ typedef struct { /* MetricsReport counters (include/lorasim/engine.hpp:66-98) */
   double predictor_ms;       /* async predictor worker busy time */
   uint64_t in_flight, staged, resident;
   int32_t copy_mode, reserved;
+  /* per-interval prediction accuracy (engine.cpp:598-633): Σ tp/(tp+fp+fn)
+   * over the scored intervals, their count, and the summed tp / fp / fn */
+  double acc_sum;
+  uint64_t acc_intervals, acc_tp, acc_fp, acc_fn;
 } plora_engine_stats;
+/* One decision-log row (DecisionLogRow, include/lorasim/engine.hpp:61;
+ * engine.cpp:304, 330, 412, 435, 495): action, adapter (0xffffffff: none),
+ * time, score (eviction score / prefetch probability) and a detail value
+ * (bytes for loads, relocations for compact). */
+#define PLORA_DECISION_EVICT 0
+#define PLORA_DECISION_PREFETCH 1
+#define PLORA_DECISION_DEMAND_LOAD 2
+#define PLORA_DECISION_PROMOTE 3
+#define PLORA_DECISION_ADMISSION_FAILURE 4
+#define PLORA_DECISION_COMPACT 5
+typedef struct {
+  double t_ms, score;
+  uint32_t adapter, action;
+  uint64_t detail;
+} plora_decision;
 typedef struct plora_engine plora_engine;
 typedef struct plora_predictor plora_predictor;
 void plora_engine_config_default(plora_engine_config* c);
@@ -422,6 +441,13 @@ int plora_engine_release_many(plora_engine* e, const uint32_t* adapters, uint64_
 int plora_engine_sync(plora_engine* e); /* wait for every issued copy */
 int plora_engine_status(const plora_engine* e, uint32_t adapter, plora_dynamics* out);
 void plora_engine_get_stats(const plora_engine* e, plora_engine_stats* out);
+/* Decision log rows [start, start + cap) into out; returns the total count. */
+uint64_t plora_engine_decisions(const plora_engine* e, uint64_t start, plora_decision* out,
+                                uint64_t cap);
+int plora_engine_set_decision_log(plora_engine* e, int enabled); /* default on; off clears */
+/* Interval length and warm-up of the accuracy scoring (predictor interval_ms,
+ * run.warmup_s); defaults 1000 ms and 0. */
+int plora_engine_set_accuracy_interval(plora_engine* e, double interval_ms, double warmup_ms);
 int plora_engine_streams(const plora_engine* e, plora_stream_t* demand, plora_stream_t* prefetch);
 
 /* ----------------------------------------------- demand predictor (host) ---

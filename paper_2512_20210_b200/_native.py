@@ -92,7 +92,14 @@ class plora_engine_stats(C.Structure):
         + [("transfer_ms", C.c_double), ("demand_transfer_ms", C.c_double),
            ("predictor_ms", C.c_double)]
         + [(n, C.c_uint64) for n in ("in_flight", "staged", "resident")]
-        + [("copy_mode", C.c_int32), ("reserved", C.c_int32)])
+        + [("copy_mode", C.c_int32), ("reserved", C.c_int32)]
+        + [("acc_sum", C.c_double)]
+        + [(n, C.c_uint64) for n in ("acc_intervals", "acc_tp", "acc_fp", "acc_fn")])
+
+
+class plora_decision(C.Structure):
+    _fields_ = [("t_ms", C.c_double), ("score", C.c_double), ("adapter", C.c_uint32),
+                ("action", C.c_uint32), ("detail", C.c_uint64)]
 
 
 class plora_lstm_config(C.Structure):
@@ -211,6 +218,9 @@ _SIGS = {
     "plora_engine_admit": (_int, [_vp, _P(_u32), _u64, _dbl, _vp, _int, _P(_i32)]),
     "plora_engine_release_many": (_int, [_vp, _P(_u32), _u64]),
     "plora_engine_status": (_int, [_vp, _u32, _P(plora_dynamics)]),
+    "plora_engine_decisions": (_u64, [_vp, _u64, _P(plora_decision), _u64]),
+    "plora_engine_set_decision_log": (_int, [_vp, C.c_int]),
+    "plora_engine_set_accuracy_interval": (_int, [_vp, C.c_double, C.c_double]),
     "plora_engine_get_stats": (None, [_vp, _P(plora_engine_stats)]),
     "plora_engine_streams": (_int, [_vp, _P(_vp), _P(_vp)]),
     "plora_lstm_config_default": (None, [_P(plora_lstm_config)]),

@@ -21,6 +21,7 @@
 //     (it sleeps on the oldest in-flight chunk's event); every entry point
 //     and the pump serialise on one mutex — one owner thread per engine as
 //     in the reference, the pump being the engine's own.
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -85,6 +86,63 @@ struct plora_engine {
 
   plora_predictor* predictor = nullptr;
   plora_engine_stats st{};
+
+  // ---- decision log (engine.cpp:635-640, written as decisions.csv by
+  // report.cpp:106-113): every evict / prefetch / demand_load / promote /
+  // admission_failure / compact with its time and score
+  std::vector<plora_decision> decisions;
+  bool log_decisions = true;
+  void log(double t, uint32_t action, uint32_t adapter, double score, uint64_t detail = 0) {
+    if (log_decisions) decisions.push_back(plora_decision{t, score, adapter, action, detail});
+  }
+
+  // ---- per-interval prediction accuracy (engine.cpp:547-561 snapshots the
+  // predicted set {p > theta} of the known adapters when an interval starts;
+  // :598-633 scores each closed interval as tp / (tp + fp + fn))
+  double acc_interval_ms = 1000.0, acc_warmup_ms = 0.0;
+  std::vector<uint8_t> seen;
+  int64_t last_snapshot = -1;
+  std::map<int64_t, std::pair<std::vector<uint32_t>, std::vector<uint32_t>>> snapshots;  // known, predicted
+  std::map<int64_t, std::set<uint32_t>> actual;
+  int64_t interval_of(double t) const { return static_cast<int64_t>(std::floor(t / acc_interval_ms)); }
+  void snapshot(double now) {
+    const int64_t k = interval_of(now);
+    if (k <= last_snapshot) return;
+    last_snapshot = k;
+    auto& sn = snapshots[k];
+    for (uint32_t a = 0; a < A; ++a) {
+      if (!seen[a]) continue;
+      sn.first.push_back(a);
+      if (probs[a] > policy.theta) sn.second.push_back(a);
+    }
+  }
+  void evaluate(double now) {
+    const int64_t cur = interval_of(now);
+    while (!snapshots.empty() && snapshots.begin()->first < cur) {
+      const int64_t k = snapshots.begin()->first;
+      const auto& [known, predicted] = snapshots.begin()->second;
+      std::set<uint32_t> act;
+      auto it = actual.find(k);
+      if (it != actual.end())
+        for (uint32_t a : it->second)
+          if (std::binary_search(known.begin(), known.end(), a)) act.insert(a);
+      uint64_t tp = 0, fp = 0, fn = 0;
+      for (uint32_t a : predicted) (act.count(a) ? tp : fp) += 1;
+      for (uint32_t a : act)
+        if (!std::binary_search(predicted.begin(), predicted.end(), a)) ++fn;
+      if (tp + fp + fn > 0 && static_cast<double>(k) * acc_interval_ms >= acc_warmup_ms) {
+        st.acc_sum += static_cast<double>(tp) / static_cast<double>(tp + fp + fn);
+        ++st.acc_intervals;
+        st.acc_tp += tp;
+        st.acc_fp += fp;
+        st.acc_fn += fn;
+      }
+      snapshots.erase(snapshots.begin());
+    }
+    while (!actual.empty() && actual.begin()->first < cur &&
+           (snapshots.empty() || actual.begin()->first < snapshots.begin()->first))
+      actual.erase(actual.begin());
+  }
 
   // Asynchronous predictor service: observations are queued to a worker
   // thread that owns the predictor (observe -> periodic train_step,
@@ -163,6 +221,7 @@ struct plora_engine {
     }
   }
 
+  double now_ms = 0.0;  // time of the current API call (decision log)
   mutable std::mutex mu;
   std::condition_variable cv;
   std::thread pump;
@@ -335,12 +394,12 @@ struct plora_engine {
     dyn[a].status = PLORA_NOT_RESIDENT;
     staged_ready.erase(a);
     ++st.evictions;
+    log(now_ms, PLORA_DECISION_EVICT, a, score);
     // pages of `a` may still be read by kernels already on the compute
     // stream: order every later copy after them
     PLORA_CUDA(cudaEventRecord(fence, compute));
     PLORA_CUDA(cudaStreamWaitEvent(demand_stream, fence, 0));
     PLORA_CUDA(cudaStreamWaitEvent(prefetch_stream, fence, 0));
-    (void)score;
   }
 
   // engine.cpp:310-333
@@ -370,8 +429,12 @@ struct plora_engine {
       if (!found) return false;
       evict(victim, vs, compute);
     }
+    nvtxRangePushA(for_prefetch ? "plora.transfer.prefetch" : "plora.transfer.demand");
     start_transfer(a, !for_prefetch);
+    nvtxRangePop();
     if (!for_prefetch) ++st.demand_loads;
+    log(now, for_prefetch ? PLORA_DECISION_PREFETCH : PLORA_DECISION_DEMAND_LOAD, a,
+        for_prefetch ? candidate_p : 0.0, bytes[a]);
     return true;
   }
 
@@ -380,6 +443,7 @@ struct plora_engine {
       dyn[a].status = PLORA_RESIDENT;
       prefetch_staged.erase(a);
       ++st.promotions;
+      log(now_ms, PLORA_DECISION_PROMOTE, a, 0.0);
       publish(a, compute);
     }
     staged_ready.clear();
@@ -416,6 +480,7 @@ struct plora_engine {
       throw CudaError(std::string("relocation failed: ") + plora_last_error());
     st.relocations += moved;
     ++st.compactions;
+    log(now_ms, PLORA_DECISION_COMPACT, 0xffffffffu, 0.0, moved);
     PLORA_CUDA(cudaEventRecord(fence, compute));
     PLORA_CUDA(cudaStreamWaitEvent(demand_stream, fence, 0));
     PLORA_CUDA(cudaStreamWaitEvent(prefetch_stream, fence, 0));
@@ -500,6 +565,7 @@ int plora_engine_create(plora_store* s, const plora_engine_config* cfg, plora_en
     e->dyn.resize(e->A);
     for (auto& d : e->dyn) plora_dynamics_init(&d);
     e->probs.assign(e->A, -1.0);
+    e->seen.assign(e->A, 0);
     e->bytes.assign(e->A, 0);
     e->units.assign(e->A, 0);
     e->src.assign(e->A, nullptr);
@@ -613,9 +679,13 @@ int plora_engine_on_arrival(plora_engine* e, uint32_t adapter, double now_ms,
     E(e)->check_key(adapter);
     std::lock_guard<std::mutex> lk(e->mu);
     DeviceCtx ctx(e->store->device);
+    nvtxRangePushA("plora.arrival");
+    e->now_ms = now_ms;
     plora_dynamics& d = e->dyn[adapter];
     const bool hit = d.status == PLORA_RESIDENT;
     ++e->st.arrivals;
+    e->seen[adapter] = 1;
+    e->actual[e->interval_of(now_ms)].insert(adapter);
     if (hit) ++e->st.hits;
     plora_record_access(&d, now_ms, e->policy.freq_half_life_ms);
     if (e->svc) {
@@ -629,6 +699,7 @@ int plora_engine_on_arrival(plora_engine* e, uint32_t adapter, double now_ms,
     // reactive demand path: absent adapters start loading at arrival
     if (d.status == PLORA_NOT_RESIDENT && !d.transfer_active)
       e->ensure_loading(adapter, false, 0.0, now_ms, static_cast<cudaStream_t>(compute));
+    nvtxRangePop();
     return hit ? 1 : 0;
   });
 }
@@ -639,6 +710,17 @@ int plora_engine_round(plora_engine* e, double now_ms, plora_stream_t compute) {
     std::lock_guard<std::mutex> lk(e->mu);
     if (!e->predictor) throw ValidationError("no predictor attached");
     ++e->st.prediction_rounds;
+    e->now_ms = now_ms;
+    nvtxRangePushA("plora.round");
+    struct Pop {
+      plora_engine* e;
+      double now;
+      ~Pop() {
+        e->snapshot(now);
+        e->evaluate(now);
+        nvtxRangePop();
+      }
+    } pop{e, now_ms};
     if (e->svc) {  // apply the last completed round, request the next one
       auto& sv = *e->svc;
       std::lock_guard<std::mutex> sl(sv.m);
@@ -678,6 +760,8 @@ int plora_engine_set_predictions(plora_engine* e, const double* probs, uint64_t 
       e->dyn[a].prediction = probs[a];
     }
     ++e->st.prediction_rounds;
+    e->snapshot(e->now_ms);
+    e->evaluate(e->now_ms);
     return 0;
   });
 }
@@ -690,9 +774,11 @@ int plora_engine_acquire(plora_engine* e, uint32_t adapter, double now_ms,
     DeviceCtx ctx(e->store->device);
     cudaStream_t compute = static_cast<cudaStream_t>(compute_);
     plora_dynamics& d = e->dyn[adapter];
+    e->now_ms = now_ms;
     if (d.status == PLORA_NOT_RESIDENT && !d.transfer_active) {
       if (!e->ensure_loading(adapter, false, 0.0, now_ms, compute)) {
         ++e->st.admission_failures;
+        e->log(now_ms, PLORA_DECISION_ADMISSION_FAILURE, adapter, 0.0);
         return PLORA_ADMIT_FAILED;
       }
     }
@@ -767,11 +853,15 @@ int plora_engine_boundary(plora_engine* e, double now_ms, plora_stream_t compute
     DeviceCtx ctx(e->store->device);
     cudaStream_t compute = static_cast<cudaStream_t>(compute_);
     if (e->pump_error) throw CudaError("prefetch pump failed (see CUDA error state)");
+    nvtxRangePushA("plora.boundary");
+    e->now_ms = now_ms;
     const int done = e->poll_transfers(compute);
     e->promote_staged(compute);
     e->issue_prefetches(now_ms, compute);
     e->maybe_compact(compute);
+    e->evaluate(now_ms);
     e->cv.notify_one();
+    nvtxRangePop();
     return done;
   });
 }
@@ -856,6 +946,39 @@ void plora_engine_get_stats(const plora_engine* e, plora_engine_stats* out) {
     std::lock_guard<std::mutex> sl(e->svc->m);
     out->predictor_ms = e->svc->busy_ms;
   }
+}
+
+uint64_t plora_engine_decisions(const plora_engine* e, uint64_t start, plora_decision* out,
+                                uint64_t cap) {
+  if (!e) return 0;
+  std::lock_guard<std::mutex> lk(e->mu);
+  const uint64_t n = e->decisions.size();
+  for (uint64_t i = start; i < n && i - start < cap && out; ++i) out[i - start] = e->decisions[i];
+  return n;
+}
+
+int plora_engine_set_decision_log(plora_engine* e, int enabled) {
+  return guard([&] {
+    E(e);
+    std::lock_guard<std::mutex> lk(e->mu);
+    e->log_decisions = enabled != 0;
+    if (!enabled) e->decisions.clear();
+    return 0;
+  });
+}
+
+int plora_engine_set_accuracy_interval(plora_engine* e, double interval_ms, double warmup_ms) {
+  return guard([&] {  // cfg_.predictor.interval_ms, cfg_.run.warmup_s (engine.cpp:598-633)
+    E(e);
+    if (!(interval_ms > 0)) throw ValidationError("accuracy interval must be positive");
+    std::lock_guard<std::mutex> lk(e->mu);
+    e->acc_interval_ms = interval_ms;
+    e->acc_warmup_ms = warmup_ms;
+    e->snapshots.clear();
+    e->actual.clear();
+    e->last_snapshot = -1;
+    return 0;
+  });
 }
 
 int plora_engine_streams(const plora_engine* e, plora_stream_t* demand, plora_stream_t* prefetch) {

@@ -158,6 +158,27 @@ class PrefetchEngine:
         N.lib().plora_engine_get_stats(self._h, C.byref(s))
         return {n: getattr(s, n) for n, _ in N.plora_engine_stats._fields_ if n != "reserved"}
 
+    DECISION_ACTIONS = ("evict", "prefetch", "demand_load", "promote", "admission_failure",
+                        "compact")
+
+    def decisions(self, start: int = 0) -> list:
+        """Decision-log rows (time_ms, action, adapter, score, detail) from
+        `start` on — the reference's decisions.csv (src/report.cpp:106-113)."""
+        n = int(N.lib().plora_engine_decisions(self._h, start, None, 0))
+        if n <= start:
+            return []
+        buf = (N.plora_decision * (n - start))()
+        N.lib().plora_engine_decisions(self._h, start, buf, n - start)
+        return [(r.t_ms, self.DECISION_ACTIONS[r.action], None if r.adapter == 0xFFFFFFFF else r.adapter,
+                 r.score, r.detail) for r in buf]
+
+    def set_decision_log(self, enabled: bool) -> None:
+        N.check(N.lib().plora_engine_set_decision_log(self._h, int(enabled)))
+
+    def set_accuracy_interval(self, interval_ms: float, warmup_ms: float = 0.0) -> None:
+        """Per-interval prediction accuracy bookkeeping (engine.cpp:598-633)."""
+        N.check(N.lib().plora_engine_set_accuracy_interval(self._h, interval_ms, warmup_ms))
+
     def streams(self):
         d, p = C.c_void_p(), C.c_void_p()
         N.check(N.lib().plora_engine_streams(self._h, C.byref(d), C.byref(p)))

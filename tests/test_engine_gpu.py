@@ -247,3 +247,30 @@ def test_engine_errors():
         rig.eng.release(0)  # release without acquire -> logic error
     with pytest.raises(Exception):
         rig.eng.set_source(0, torch.zeros(10, dtype=torch.uint8))  # wrong size
+
+
+def test_decision_log_and_interval_accuracy():
+    """Every decision is logged with its time (engine.cpp:304-495 -> decisions.csv),
+    and each closed interval is scored tp / (tp + fp + fn) over the known
+    adapters, the predicted set snapshotted when the interval's first
+    prediction arrives (engine.cpp:547-561, 598-633)."""
+    rig = Rig([4, 4, 4], pool_pages=400)
+    eng = rig.eng
+    eng.set_accuracy_interval(100.0)
+    for a in range(3):
+        eng.on_arrival(a, 10.0)
+    rig.settle(20.0)
+    eng.on_arrival(0, 120.0)  # interval 1: adapters 0, 1 arrive
+    eng.set_predictions([0.01, 0.99, 0.01])  # predicted {1}
+    eng.on_arrival(1, 150.0)
+    eng.boundary(210.0)  # closes interval 1
+    st = eng.stats()
+    assert st["acc_intervals"] == 1
+    assert (st["acc_tp"], st["acc_fp"], st["acc_fn"]) == (1, 0, 1)
+    assert abs(st["acc_sum"] - 0.5) < 1e-12
+    rows = eng.decisions()
+    loads = [r for r in rows if r[1] == "demand_load"]
+    assert [r[2] for r in loads[:3]] == [0, 1, 2] and all(r[0] == 10.0 for r in loads[:3])
+    assert loads[0][4] == SHAPE.adapter_bytes(4)
+    eng.set_decision_log(False)
+    assert eng.decisions() == []
