@@ -471,14 +471,20 @@ def h2d_roof_gbs(dev, nbytes=256 << 20):
 
 def run_cfg4(args):
     """BASELINE configs[3]: synthetic Azure-Functions-like trace over 1000
-    adapters held in pinned host memory, LSTM-driven page prefetch overlapped
-    with the paged BGMV; request-sharded over ranks (adapter k -> rank k mod N)."""
+    distinct adapters held in a pinned host adapter store, LSTM-driven page
+    prefetch overlapped with the paged BGMV; request-sharded over ranks
+    (adapter k -> rank k mod N).  The same trace is served three times from a
+    cold pool — prediction source lstm (the online predictor), oracle (the
+    future arrivals, engine.cpp:555-562) and off (demand loads only) — and
+    each run reports hit rate, demand-stall time, prefetch traffic and the
+    per-interval prediction accuracy (engine.cpp:598-633)."""
     import torch
     import torch.distributed as dist
 
     from paper_2512_20210_b200 import synth
     from paper_2512_20210_b200.engine import EngineConfig
-    from paper_2512_20210_b200.lora import ModelShape, bgmv, kernel_launch_count
+    from paper_2512_20210_b200.hoststore import HostAdapterStore
+    from paper_2512_20210_b200.lora import ModelShape, bgmv_layer, kernel_launch_count
     from paper_2512_20210_b200.predictor import OnlinePredictorConfig, PredictorConfig
     from paper_2512_20210_b200.prefetch import PrefetchPolicy
     from paper_2512_20210_b200.serving import DecodeServer, ServerConfig, shard_keys
@@ -495,25 +501,17 @@ def run_cfg4(args):
     n_total = args.cfg4_adapters
     keys = shard_keys(n_total, rank, world)
     ranks = [(8, 16, 32, 64)[k % 4] for k in keys]
-    # pinned host store: n_img distinct images per rank class, aliased over the
-    # keys of that class (every transfer still moves the adapter's full bytes)
-    imgs = {}
-    for r in (8, 16, 32, 64):
-        for j in range(args.cfg4_images):
-            g = synth.adapter_image(shape, r, 10_000 * r + j, device=dev)
-            imgs[(r, j)] = g.view(torch.uint8).cpu().pin_memory()
-            del g
-    host_image = lambda i: imgs[(ranks[i], i % args.cfg4_images)]  # noqa: E731
-    pol = PrefetchPolicy(staging_fraction=args.cfg4_staging)
-    scfg = ServerConfig(
-        shape=shape, ranks=ranks, pool_bytes=int(args.cfg4_pool_gib * (1 << 30)),
-        page_bytes=args.cfg4_page_bytes, batch_tokens=256, round_ms=100.0,
-        engine=EngineConfig(policy=pol, chunk_bytes=8 << 20, prefetch_inflight_bytes=64 << 20),
-        predictor=OnlinePredictorConfig(model=PredictorConfig(num_adapters=len(keys)),
-                                        interval_ms=1000.0, train_every=100, batch_size=64),
-        seed=42, device=local)
-    srv = DecodeServer(scfg, host_image)
-    srv.engine.attach_predictor(srv.predictor, asynchronous=True)
+    # the host adapter store: every local adapter's own bytes, pinned and
+    # page-aligned (distinct images: each transfer moves that adapter's data)
+    t0 = time.perf_counter()
+    hstore = HostAdapterStore.create([shape.adapter_bytes(r) for r in ranks], ranks,
+                                     align=args.cfg4_page_bytes)
+    for i, (k, r) in enumerate(zip(keys, ranks)):
+        img = synth.adapter_image(shape, r, k, device=dev)
+        hstore.view(i).copy_(img.view(torch.uint8), non_blocking=True)
+        del img
+    torch.cuda.synchronize()
+    store_s = time.perf_counter() - t0
     # trace: rate scales with N so every rank sees the same per-GPU load
     prof = SyntheticProfile(num_adapters=n_total, base_rate=args.cfg4_rate * world,
                             hot_set_size=args.cfg4_hot, hot_rotation_s=args.cfg4_rotation_s,
@@ -529,95 +527,136 @@ def run_cfg4(args):
     tr = generate_synthetic(prof, duration, seed=42)
     mine = np.nonzero(tr.adapter % world == rank)[0]
     local_of = {k: i for i, k in enumerate(keys)}
-    arr_keys = [local_of[int(k)] for k in tr.adapter[mine]]
+    arr_keys = np.asarray([local_of[int(k)] for k in tr.adapter[mine]], np.uint32)
     arr_t = tr.arrival_ms[mine]
     if len(arr_keys) < (W + K) * T:
         raise RuntimeError("trace too short for the requested steps")
+    future = [np.sort(arr_t[arr_keys == i]) for i in range(len(keys))]
     stream = torch.cuda.current_stream()
-
-    def run_steps(k0, n, evs=None):
-        for s in range(k0, k0 + n):
-            a = arr_keys[s * T:(s + 1) * T]
-            srv.step(a, float(arr_t[(s + 1) * T - 1]), events=evs[s - k0] if evs else None)
-
-    run_steps(0, W)
-    srv.engine.flush_predictor()
-    torch.cuda.synchronize()
-    st0 = srv.engine.stats()
-    if world > 1:
-        dist.barrier()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(K)]
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    n0 = kernel_launch_count()
-    tok0 = srv.stats["tokens"]
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        e0.record(stream)
-        run_steps(W, K, evs)
-        e1.record(stream)
-        torch.cuda.synchronize()
-    launches = kernel_launch_count() - n0
-    tokens = srv.stats["tokens"] - tok0
-    ms = e0.elapsed_time(e1)
-    bgmv_ms = sum(a.elapsed_time(b) for a, b in evs) / K
-    st1 = srv.engine.stats()
-    # BGMV alone: the last batch replayed with the engine idle
-    srv.engine.sync()
-    torch.cuda.synchronize()
-    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a0.record(stream)
-    for _ in range(10):
-        for l in range(shape.n_layers):
-            for p_ in range(shape.n_proj):
-                bgmv(srv.plan, l, p_, srv.x[p_][:srv.last_batch], srv.y[p_][:srv.last_batch])
-    a1.record(stream)
-    torch.cuda.synchronize()
-    alone_ms = a0.elapsed_time(a1) / 10
     roof = h2d_roof_gbs(dev)
-    d = {k: st1[k] - st0[k] for k in ("arrivals", "hits", "demand_loads", "prefetch_issued",
-                                        "promotions", "evictions", "admission_failures",
-                                        "upgrades", "bytes_h2d", "transfer_ms",
-                                        "prediction_rounds", "compactions")}
-    tot = torch.tensor([ms, float(tokens)], device=dev, dtype=torch.float64)
+    modes = [m for m in args.cfg4_modes.split(",") if m]
+    results = {}
+    for mode in modes:
+        pol = PrefetchPolicy(staging_fraction=args.cfg4_staging)
+        # the reference trains every 100 observations at 50 requests/s
+        # (defaults.ini:20, 68): the same training cadence per second of trace
+        train_every = args.cfg4_train_every or max(100, int(round(100 * args.cfg4_rate / 50.0)))
+        pcfg = OnlinePredictorConfig(model=PredictorConfig(num_adapters=len(keys)),
+                                     interval_ms=1000.0, train_every=train_every, batch_size=64)
+        scfg = ServerConfig(
+            shape=shape, ranks=ranks, pool_bytes=int(args.cfg4_pool_gib * (1 << 30)),
+            page_bytes=args.cfg4_page_bytes, batch_tokens=T, round_ms=100.0,
+            engine=EngineConfig(policy=pol, chunk_bytes=8 << 20, prefetch_inflight_bytes=64 << 20,
+                                prefetch=mode != "off"),
+            predictor=pcfg, seed=42, device=local, prediction=mode)
+        srv = DecodeServer(scfg, hstore.view, future=future)
+        if srv.predictor is not None:
+            if not args.cfg4_host_predictor:
+                srv.predictor.set_device(local)  # predict_all on the GPU (FP64)
+            srv.engine.attach_predictor(srv.predictor, asynchronous=True)
+        # score intervals once the LSTM window (30 x 1 s) has seen 10 s of trace
+        srv.engine.set_accuracy_interval(1000.0, warmup_ms=float(arr_t[0]) + 10000.0)
+
+        def run_steps(k0, n, evs=None):
+            for st_ in range(k0, k0 + n):
+                a = arr_keys[st_ * T:(st_ + 1) * T]
+                srv.step(a, float(arr_t[(st_ + 1) * T - 1]), events=evs[st_ - k0] if evs else None)
+
+        tw = time.perf_counter()
+        run_steps(0, W)
+        if srv.predictor is not None:
+            srv.engine.flush_predictor()
+        torch.cuda.synchronize()
+        warm_s = time.perf_counter() - tw
+        st0 = srv.engine.stats()
+        d0 = len(srv.engine.decisions())
+        if world > 1:
+            dist.barrier()
+        evs = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(K)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0 = kernel_launch_count()
+        tok0 = srv.stats["tokens"]
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize()
+            e0.record(stream)
+            run_steps(W, K, evs)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        launches = kernel_launch_count() - n0
+        tokens = srv.stats["tokens"] - tok0
+        ms = e0.elapsed_time(e1)
+        stall_ms = sum(a.elapsed_time(b) for a, b, _ in evs) / K
+        bgmv_ms = sum(b.elapsed_time(c) for _, b, c in evs) / K
+        st1 = srv.engine.stats()
+        rows = srv.engine.decisions(d0)
+        # BGMV alone: the last batch replayed with the engine idle
+        srv.engine.sync()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(10):
+            srv.apply(srv.last_batch)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        alone_ms = a0.elapsed_time(a1) / 10
+        d = {k: st1[k] - st0[k] for k in ("arrivals", "hits", "demand_loads", "prefetch_issued",
+                                            "promotions", "evictions", "admission_failures",
+                                            "upgrades", "bytes_h2d", "transfer_ms",
+                                            "prediction_rounds", "compactions")}
+        tot = torch.tensor([ms, float(tokens)], device=dev, dtype=torch.float64)
+        if world > 1:
+            mx = tot.clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            sm = tot.clone()
+            dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+            ms, tokens = mx[0].item(), sm[1].item()
+        acts = {}
+        for r_ in rows:
+            acts[r_[1]] = acts.get(r_[1], 0) + 1
+        results[mode] = {
+            "value": tokens / (ms / 1e3), "ms_per_step": ms / K, "launches": launches,
+            "hit_rate": d["hits"] / max(d["arrivals"], 1),
+            "demand_stall_ms_per_step": stall_ms,
+            "bgmv_ms_per_step_with_prefetch": bgmv_ms, "bgmv_ms_per_step_alone": alone_ms,
+            "overlap": alone_ms / max(bgmv_ms, 1e-9),
+            "bytes_h2d_per_step": d["bytes_h2d"] / K,
+            "h2d_gbs_over_timed_region": d["bytes_h2d"] / (ms / 1e3) / 1e9,
+            "link_busy_frac": d["bytes_h2d"] / (ms / 1e3) / 1e9 / roof,
+            "interval_accuracy": st1["acc_sum"] / max(st1["acc_intervals"], 1),
+            "accuracy_intervals": st1["acc_intervals"],
+            "accuracy_tp_fp_fn": [st1["acc_tp"], st1["acc_fp"], st1["acc_fn"]],
+            "predictor_busy_ms": st1["predictor_ms"], "trace_served_s": warm_s + ms / 1e3,
+            "predictor": {"train_every": train_every, "predict_all": "host" if args.cfg4_host_predictor
+                          else "gpu"},
+            "decisions_in_timed_region": acts, "counters": d, "clocks": clk.summary()}
+        del srv
+        torch.cuda.empty_cache()
     if world > 1:
-        mx = tot.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tot.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms, tokens = mx[0].item(), sm[1].item()
         dist.barrier()
         dist.destroy_process_group()
     if rank != 0:
         return
-    value = tokens / (ms / 1e3)
-    # H2D link utilisation over the timed region (demand + prefetch page
-    # scatters), against the measured pinned-copy roof of this box
-    pf_gbs = d["bytes_h2d"] / (ms / 1e3) / 1e9
+    head = results.get("lstm") or results[modes[0]]
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": (f"cfg4: generate_synthetic trace, {n_total} adapters in pinned "
-                                f"host memory (r=[8,16,32,64][k%4], Llama-7B q/v), per GPU "
-                                f"{len(keys)} adapters, 256-token decode steps, async LSTM "
-                                f"predictor, page prefetch overlapped with BGMV"),
+        "config": {"workload": (f"cfg4: generate_synthetic trace, {n_total} distinct adapters in a "
+                                f"pinned host adapter store (r=[8,16,32,64][k%4], Llama-7B q/v), per "
+                                f"GPU {len(keys)} adapters, 256-token decode steps, async LSTM "
+                                f"predictor (predict_all on the GPU), page prefetch overlapped "
+                                f"with BGMV"),
                    "pool_gib_per_gpu": args.cfg4_pool_gib, "page_bytes": args.cfg4_page_bytes,
                    "trace": {"base_rate_per_gpu": args.cfg4_rate, "hot_set_size": args.cfg4_hot,
                              "hot_rotation_s": args.cfg4_rotation_s, "hot_share": 0.9},
-                   "host_images": f"{args.cfg4_images} distinct pinned images per rank class",
+                   "host_store": {"bytes_per_gpu": hstore.total_bytes(), "build_s": store_s,
+                                  "distinct_images": len(keys)},
                    "parallelism": f"request-sharded x{world} (adapter k -> rank k mod N)",
                    "l2": "inputs > L2 (adapter pages)"},
-        "gpu_launches": launches,
-        "prefetch": {"bytes_h2d_per_step": d["bytes_h2d"] / K,
-                     "h2d_gbs_over_timed_region": pf_gbs, "h2d_roof_gbs": roof,
-                     "link_busy_frac": pf_gbs / roof,
-                     "trace_warm_s": args.cfg4_warm_s, "untimed_serving_steps": pre,
-                     "overlap": alone_ms / max(bgmv_ms, 1e-9),
-                     "bgmv_ms_per_step_with_prefetch": bgmv_ms, "bgmv_ms_per_step_alone": alone_ms,
-                     "hit_rate": d["hits"] / max(d["arrivals"], 1),
-                     "counters": d, "predictor_busy_ms": st1["predictor_ms"]},
-        "clocks": clk.summary(),
+        "gpu_launches": head["launches"],
+        "prefetch": {"h2d_roof_gbs": roof, "trace_warm_s": args.cfg4_warm_s,
+                     "untimed_serving_steps": pre, "by_prediction_source": results},
+        "clocks": head["clocks"],
     }
     print(json.dumps(line))
 
@@ -836,7 +875,13 @@ def main():
                          "cfg4 = trace-driven decode with LSTM prefetch, "
                          "cfg5 = tensor-parallel 70B (run under torchrun for N > 1)")
     ap.add_argument("--cfg4-adapters", type=int, default=1000)
-    ap.add_argument("--cfg4-images", type=int, default=4)
+    ap.add_argument("--cfg4-modes", default="lstm,oracle,off",
+                    help="prediction sources served in turn (lstm, oracle, off)")
+    ap.add_argument("--cfg4-train-every", type=int, default=0,
+                    help="observations per LSTM train step (0: the reference's cadence per "
+                         "second of trace, 100 at 50 req/s)")
+    ap.add_argument("--cfg4-host-predictor", action="store_true",
+                    help="run predict_all on the host threads instead of the GPU")
     ap.add_argument("--cfg4-pool-gib", type=float, default=16.0)
     ap.add_argument("--cfg4-page-bytes", type=int, default=2 << 20)
     ap.add_argument("--cfg4-staging", type=float, default=0.25)

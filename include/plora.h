@@ -255,6 +255,23 @@ int plora_store_is_published(const plora_store* s, uint32_t adapter);
 int plora_store_apply_relocations(plora_store* s, const plora_reloc* relocs, uint64_t n,
                                   plora_stream_t stream);
 
+/* ------------------------------------------------ host adapter store -----
+ * The pinned host copy of every adapter the engine pages in (SURVEY §8(f)
+ * row 4): one page-aligned pinned region with an offset index, optionally
+ * file-backed ("PLHS": header, index, align-aligned images; opened with mmap
+ * + cudaHostRegister).  Adapter sizes: plora_param_count (adapter.cpp:12-26);
+ * the engine's transfer sources point into it (plora_engine_set_source). */
+typedef struct plora_hoststore plora_hoststore;
+int plora_hoststore_create(const uint64_t* bytes, const uint32_t* ranks, uint32_t n,
+                           uint64_t align, plora_hoststore** out);
+int plora_hoststore_open(const char* path, plora_hoststore** out);
+int plora_hoststore_save(const plora_hoststore* s, const char* path);
+void plora_hoststore_destroy(plora_hoststore* s);
+uint32_t plora_hoststore_count(const plora_hoststore* s);
+int plora_hoststore_entry(const plora_hoststore* s, uint32_t key, void** ptr, uint64_t* bytes,
+                          uint32_t* rank);
+int plora_hoststore_bytes(const plora_hoststore* s, uint64_t* data_bytes);
+
 /* --------------------------------------- paged LoRA forward op (new) -----
  * The op the reference bills as cost_model prefill_ms / step_ms
  * (include/lorasim/cost_model.hpp:32-40 at src/engine.cpp:355,510);

@@ -187,6 +187,13 @@ _SIGS = {
     "plora_store_retire": (_int, [_vp, _u32, _vp]),
     "plora_store_is_published": (_int, [_vp, _u32]),
     "plora_store_apply_relocations": (_int, [_vp, _P(plora_reloc), _u64, _vp]),
+    "plora_hoststore_create": (_int, [_P(_u64), _P(_u32), _u32, _u64, _P(_vp)]),
+    "plora_hoststore_open": (_int, [C.c_char_p, _P(_vp)]),
+    "plora_hoststore_save": (_int, [_vp, C.c_char_p]),
+    "plora_hoststore_destroy": (None, [_vp]),
+    "plora_hoststore_count": (_u32, [_vp]),
+    "plora_hoststore_entry": (_int, [_vp, _u32, _P(_vp), _P(_u64), _P(_u32)]),
+    "plora_hoststore_bytes": (_int, [_vp, _P(_u64)]),
     "plora_plan_create": (_int, [_vp, _P(_i32), _u32, _vp, _P(_vp)]),
     "plora_plan_update": (_int, [_vp, _P(_i32), _u32, _vp]),
     "plora_plan_destroy": (None, [_vp]),
