@@ -740,6 +740,30 @@ def run_cfg5(args):
         return
     # per-rank algorithmic bytes of one (layer, proj) call: its A rows, its Bᵀ
     # columns, x, its y shard RMW
+    split = None
+    if world == 1:  # the per-rank halves themselves (shrink, copy, expand) at TP = 1
+        tps = TensorParallelLoRA(plan, 0, 1, force_split=True)
+
+        def step_split():
+            for l in range(L):
+                for p in range(NP):
+                    tps(l, p, x[l], ys[p][l])
+
+        for _ in range(3):
+            step_split()
+        torch.cuda.synchronize()
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g2):
+            step_split()
+        g2.replay()
+        torch.cuda.synchronize()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(K):
+            g2.replay()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        split = s0.elapsed_time(s1) / K
     per_call = statistics.mean(
         sum((r // world) * shape.d_in[p] + r * (shape.d_out[p] // world) for r in cfg.ranks) * 2
         + T * shape.d_in[p] * 2 + 2 * T * (shape.d_out[p] // world) * 2 for p in range(NP))
@@ -763,6 +787,11 @@ def run_cfg5(args):
                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": per_call,
                      "avg_launch_us": avg_call_ms * 1e3,
                      "note": "per (layer, proj) call = shrink + all-gather + expand on one rank"},
+        "tp_halves_at_tp1": None if split is None else {
+            "ms_per_step": split, "us_per_call": split * 1e3 / (L * NP),
+            "hbm_frac": per_call / (split / (L * NP) / 1e3) / 1e9 / peak,
+            "note": "tp_shrink + v copy + tp_expand forced at TP=1 (the per-rank kernels of the "
+                    "N>1 path; value above uses the fused data-parallel op at TP=1)"},
         "clocks": clk.summary(),
     }
     print(json.dumps(line))

@@ -86,10 +86,14 @@ class TensorParallelLoRA:
     def __init__(self, plan, tp_rank: int, tp_size: int, group=None,
                  shrink: Optional[Callable] = None, expand: Optional[Callable] = None,
                  all_gather: Optional[Callable] = None, shard_rows: Optional[int] = None,
-                 n_tokens: Optional[int] = None, device=None):
+                 n_tokens: Optional[int] = None, device=None, force_split: bool = False):
+        """force_split: run the shrink / expand halves even at tp_size 1
+        (timing of the per-rank kernels; otherwise one rank uses the fused
+        data-parallel op)."""
         if tp_size < 1 or not 0 <= tp_rank < tp_size:
             raise N.ValidationError("tp_rank must be in [0, tp_size)")
         self.plan, self.tp_rank, self.tp_size, self.group = plan, tp_rank, tp_size, group
+        self.force_split = force_split
         self._shrink = shrink or bgmv_tp_shrink
         self._expand = expand or bgmv_tp_expand
         self._gather = all_gather or (lambda out, inp: _all_gather(out, inp, group))
@@ -118,7 +122,7 @@ class TensorParallelLoRA:
 
     def forward(self, layer: int, proj: int, x: torch.Tensor, y_shard: torch.Tensor,
                 scale: float = 1.0) -> torch.Tensor:
-        if self.tp_size == 1 and self._shrink is bgmv_tp_shrink:
+        if self.tp_size == 1 and self._shrink is bgmv_tp_shrink and not self.force_split:
             # one rank holds every row and column: no collective, so the fused
             # data-parallel op applies the whole LoRA in one launch
             from .lora import bgmv
