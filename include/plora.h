@@ -67,6 +67,18 @@ void plora_size_table_destroy(plora_size_table* t);
 int plora_size_table_set(plora_size_table* t, uint32_t rank, uint64_t bytes); /* adapter.cpp:37-40 */
 int plora_size_table_bytes_for(const plora_size_table* t, uint32_t rank,
                                uint64_t* out); /* adapter.cpp:43-50 */
+/* load_catalog_json (adapter.cpp:81-108): a JSON array of {"id": string,
+ * "rank": uint[, "size_bytes": uint]}; bytes default to sizes (NULL = the
+ * default table) at the rank; base dims d, k, adapted, bytes_per_param.
+ * Fills up to cap entries (ranks, bytes, and ids as NUL-terminated strings
+ * of at most id_stride - 1 bytes at ids_out + i·id_stride; any output may be
+ * NULL) and returns the catalog size, or a negative status: ConfigError
+ * (cannot open), ParseError (malformed, not an array, entry without id or
+ * rank), ValidationError (empty catalog, invalid dims). */
+int64_t plora_load_catalog_json(const char* path, const plora_size_table* sizes, uint32_t d,
+                                uint32_t k, uint32_t adapted, uint32_t bytes_per_param,
+                                uint32_t* ranks_out, uint64_t* bytes_out, char* ids_out,
+                                uint64_t id_stride, uint64_t cap);
 /* generate_catalog (adapter.cpp:110-144): ranks/bytes of `count` adapters
  * keyed 0..count-1 (ids "a000".. in catalog order).  sizes NULL = default table. */
 int plora_generate_catalog(uint32_t count, const uint32_t* mix_ranks, const double* mix_weights,

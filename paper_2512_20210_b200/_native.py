@@ -136,6 +136,8 @@ _SIGS = {
     "plora_size_table_destroy": (None, [_vp]),
     "plora_size_table_set": (_int, [_vp, _u32, _u64]),
     "plora_size_table_bytes_for": (_int, [_vp, _u32, _P(_u64)]),
+    "plora_load_catalog_json": (_i64, [C.c_char_p, _vp, _u32, _u32, _u32, _u32, _P(_u32),
+                                        _P(_u64), C.c_char_p, _u64, _u64]),
     "plora_generate_catalog": (_int, [_u32, _P(_u32), _P(_dbl), _u64, _u64, _vp, _u32, _u32,
                                       _u32, _u32, _P(_u32), _P(_u64)]),
     "plora_pool_create": (_int, [_u64, _u32, _P(_vp)]),

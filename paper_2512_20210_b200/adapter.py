@@ -119,38 +119,26 @@ def generate_catalog(count: int, mix: list[tuple[int, float]], seed: int,
 
 def load_catalog_json(path: str, sizes: AdapterSizeTable | None = None,
                       base: LoraDims | None = None) -> list[AdapterSpec]:
-    """load_catalog_json (src/adapter.cpp:81-108): a JSON array of
-    ``{"id": str, "rank": int[, "size_bytes": int]}``; sizes default to the
-    size table's bytes for the rank.  Errors as the reference raises them:
-    ConfigError (cannot open), ParseError (malformed / not an array / entry
-    without id or rank), ValidationError (empty catalog, invalid dims)."""
+    """load_catalog_json (src/adapter.cpp:81-108) through the C ABI
+    (plora_load_catalog_json): a JSON array of ``{"id": str, "rank": int[,
+    "size_bytes": int]}``; sizes default to the size table's bytes for the
+    rank.  Errors as the reference raises them: ConfigError (cannot open),
+    ParseError (malformed / not an array / entry without id or rank),
+    ValidationError (empty catalog, invalid dims)."""
     base = base if base is not None else LoraDims()
-    try:
-        with open(path) as f:
-            text = f.read()
-    except OSError:
-        raise ConfigError(f"cannot open adapter catalog: {path}") from None
-    try:
-        j = json.loads(text)
-    except json.JSONDecodeError as e:
-        raise ParseError(f"adapter catalog {path}: {e}") from None
-    if not isinstance(j, list):
-        raise ParseError("adapter catalog must be a JSON array")
+    sz = sizes if sizes is not None else AdapterSizeTable()
+    L = N.lib()
+    args = (path.encode(), sz._h, base.d, base.k, base.adapted_matrices, base.bytes_per_param)
+    n = L.plora_load_catalog_json(*args, None, None, None, 0, 0)
+    N.check(n)
+    ranks = (C.c_uint32 * n)()
+    nbytes = (C.c_uint64 * n)()
+    stride = 256
+    ids = C.create_string_buffer(n * stride)
+    N.check(L.plora_load_catalog_json(*args, ranks, nbytes, ids, stride, n))
     out = []
-    for entry in j:
-        if not isinstance(entry, dict) or "id" not in entry or "rank" not in entry:
-            raise ParseError("catalog entry needs 'id' and 'rank'")
-        rank = entry["rank"]
-        if not isinstance(rank, int) or isinstance(rank, bool) or not 0 <= rank < 1 << 32:
-            raise ParseError(f"catalog entry {entry.get('id')!r}: rank must be an unsigned integer")
-        dims = LoraDims(base.d, base.k, rank, base.adapted_matrices, base.bytes_per_param)
-        if "size_bytes" in entry:
-            nbytes = entry["size_bytes"]
-            if not isinstance(nbytes, int) or isinstance(nbytes, bool) or nbytes < 0:
-                raise ParseError(f"catalog entry {entry['id']!r}: size_bytes must be an unsigned integer")
-        else:
-            nbytes = (sizes if sizes is not None else AdapterSizeTable()).bytes_for(rank)
-        out.append(AdapterSpec.sized(str(entry["id"]), dims, nbytes))
-    if not out:
-        raise ValidationError("adapter catalog is empty")
+    for i in range(n):
+        ident = C.string_at(C.addressof(ids) + i * stride).decode("utf-8", "replace")
+        dims = LoraDims(base.d, base.k, ranks[i], base.adapted_matrices, base.bytes_per_param)
+        out.append(AdapterSpec.sized(ident, dims, nbytes[i]))
     return out

@@ -10,6 +10,9 @@
 #include <string>
 #include <vector>
 
+#include <fstream>
+#include <cctype>
+#include <iterator>
 #include "common.hpp"
 #include "pagepool.hpp"
 #include "store.hpp"
@@ -59,6 +62,244 @@ struct plora_size_table {
     return anchor_bytes * rank / anchor_rank;
   }
 };
+
+// ---- catalog JSON (load_catalog_json, adapter.cpp:81-108): a minimal JSON
+// reader for the catalog's grammar — an array of objects whose "id" is a
+// string and "rank" / "size_bytes" unsigned integers; every other value of
+// any JSON type is skipped.  Malformed input is a ParseError, as the
+// reference's nlohmann parse failure is.
+namespace {
+
+struct CatalogEntry {
+  std::string id;
+  bool has_id = false, has_rank = false, has_size = false;
+  uint64_t rank = 0, size = 0;
+};
+
+class JsonReader {
+ public:
+  JsonReader(const std::string& text, const std::string& path) : s_(text), path_(path) {}
+  std::vector<CatalogEntry> catalog() {
+    ws();
+    if (peek() != '[') throw ParseError("adapter catalog must be a JSON array");
+    ++i_;
+    std::vector<CatalogEntry> out;
+    ws();
+    if (peek() == ']') {
+      ++i_;
+    } else {
+      while (true) {
+        out.push_back(entry());
+        ws();
+        const char c = next();
+        if (c == ']') break;
+        if (c != ',') fail("expected ',' or ']'");
+      }
+    }
+    ws();
+    if (i_ != s_.size()) fail("trailing characters");
+    return out;
+  }
+
+ private:
+  CatalogEntry entry() {
+    ws();
+    if (peek() != '{') {  // a non-object entry has no 'id' / 'rank'
+      skip_value();
+      return CatalogEntry{};
+    }
+    ++i_;
+    CatalogEntry e;
+    ws();
+    if (peek() == '}') {
+      ++i_;
+      return e;
+    }
+    while (true) {
+      ws();
+      const std::string key = string();
+      ws();
+      if (next() != ':') fail("expected ':'");
+      ws();
+      if (key == "id" && peek() == '"') {
+        e.id = string();
+        e.has_id = true;
+      } else if (key == "id") {  // nlohmann's get<std::string> on a non-string
+        skip_value();
+        throw ParseError("adapter catalog " + path_ + ": catalog entry 'id' must be a string");
+      } else if (key == "rank" || key == "size_bytes") {
+        const uint64_t v = unsigned_int(key);
+        if (key == "rank") {
+          if (v > 0xffffffffull) throw ParseError("adapter catalog " + path_ + ": rank out of range");
+          e.rank = v;
+          e.has_rank = true;
+        } else {
+          e.size = v;
+          e.has_size = true;
+        }
+      } else {
+        skip_value();
+      }
+      ws();
+      const char c = next();
+      if (c == '}') break;
+      if (c != ',') fail("expected ',' or '}'");
+    }
+    return e;
+  }
+  uint64_t unsigned_int(const std::string& key) {
+    const std::size_t b = i_;
+    if (peek() == '-' || !std::isdigit(static_cast<unsigned char>(peek()))) {
+      skip_value();
+      throw ParseError("adapter catalog " + path_ + ": '" + key + "' must be an unsigned integer");
+    }
+    uint64_t v = 0;
+    while (i_ < s_.size() && std::isdigit(static_cast<unsigned char>(s_[i_]))) {
+      const uint64_t d = static_cast<uint64_t>(s_[i_++] - '0');
+      if (v > (~0ull - d) / 10) fail("integer overflow");
+      v = v * 10 + d;
+    }
+    if (i_ < s_.size() && (s_[i_] == '.' || s_[i_] == 'e' || s_[i_] == 'E')) {
+      i_ = b;
+      skip_value();
+      throw ParseError("adapter catalog " + path_ + ": '" + key + "' must be an unsigned integer");
+    }
+    return v;
+  }
+  std::string string() {
+    if (next() != '"') fail("expected a string");
+    std::string out;
+    while (true) {
+      if (i_ >= s_.size()) fail("unterminated string");
+      const char c = s_[i_++];
+      if (c == '"') break;
+      if (static_cast<unsigned char>(c) < 0x20) fail("control character in string");
+      if (c != '\\') {
+        out.push_back(c);
+        continue;
+      }
+      if (i_ >= s_.size()) fail("unterminated escape");
+      const char e = s_[i_++];
+      switch (e) {
+        case '"': out.push_back('"'); break;
+        case '\\': out.push_back('\\'); break;
+        case '/': out.push_back('/'); break;
+        case 'b': out.push_back('\b'); break;
+        case 'f': out.push_back('\f'); break;
+        case 'n': out.push_back('\n'); break;
+        case 'r': out.push_back('\r'); break;
+        case 't': out.push_back('\t'); break;
+        case 'u': {  // BMP code point -> UTF-8 (surrogate pairs combined)
+          uint32_t cp = hex4();
+          if (cp >= 0xD800 && cp <= 0xDBFF) {
+            if (i_ + 1 >= s_.size() || s_[i_] != '\\' || s_[i_ + 1] != 'u') fail("lone surrogate");
+            i_ += 2;
+            const uint32_t lo = hex4();
+            if (lo < 0xDC00 || lo > 0xDFFF) fail("bad surrogate pair");
+            cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+          }
+          if (cp < 0x80) {
+            out.push_back(static_cast<char>(cp));
+          } else if (cp < 0x800) {
+            out.push_back(static_cast<char>(0xC0 | (cp >> 6)));
+            out.push_back(static_cast<char>(0x80 | (cp & 0x3F)));
+          } else if (cp < 0x10000) {
+            out.push_back(static_cast<char>(0xE0 | (cp >> 12)));
+            out.push_back(static_cast<char>(0x80 | ((cp >> 6) & 0x3F)));
+            out.push_back(static_cast<char>(0x80 | (cp & 0x3F)));
+          } else {
+            out.push_back(static_cast<char>(0xF0 | (cp >> 18)));
+            out.push_back(static_cast<char>(0x80 | ((cp >> 12) & 0x3F)));
+            out.push_back(static_cast<char>(0x80 | ((cp >> 6) & 0x3F)));
+            out.push_back(static_cast<char>(0x80 | (cp & 0x3F)));
+          }
+          break;
+        }
+        default: fail("bad escape");
+      }
+    }
+    return out;
+  }
+  uint32_t hex4() {
+    if (i_ + 4 > s_.size()) fail("short \\u escape");
+    uint32_t v = 0;
+    for (int q = 0; q < 4; ++q) {
+      const char c = s_[i_++];
+      v <<= 4;
+      if (c >= '0' && c <= '9') v |= static_cast<uint32_t>(c - '0');
+      else if (c >= 'a' && c <= 'f') v |= static_cast<uint32_t>(c - 'a' + 10);
+      else if (c >= 'A' && c <= 'F') v |= static_cast<uint32_t>(c - 'A' + 10);
+      else fail("bad \\u escape");
+    }
+    return v;
+  }
+  void skip_value(int depth = 0) {
+    if (depth > 512) fail("nesting too deep");
+    ws();
+    const char c = peek();
+    if (c == '"') {
+      string();
+    } else if (c == '{' || c == '[') {
+      const char close = c == '{' ? '}' : ']';
+      ++i_;
+      ws();
+      if (peek() == close) {
+        ++i_;
+        return;
+      }
+      while (true) {
+        ws();
+        if (c == '{') {
+          string();
+          ws();
+          if (next() != ':') fail("expected ':'");
+        }
+        skip_value(depth + 1);
+        ws();
+        const char d = next();
+        if (d == close) break;
+        if (d != ',') fail("expected ','");
+      }
+    } else if (s_.compare(i_, 4, "true") == 0 || s_.compare(i_, 4, "null") == 0) {
+      i_ += 4;
+    } else if (s_.compare(i_, 5, "false") == 0) {
+      i_ += 5;
+    } else if (c == '-' || std::isdigit(static_cast<unsigned char>(c))) {
+      if (c == '-') ++i_;
+      if (!std::isdigit(static_cast<unsigned char>(peek()))) fail("bad number");
+      while (std::isdigit(static_cast<unsigned char>(peek()))) ++i_;
+      if (peek() == '.') {
+        ++i_;
+        if (!std::isdigit(static_cast<unsigned char>(peek()))) fail("bad number");
+        while (std::isdigit(static_cast<unsigned char>(peek()))) ++i_;
+      }
+      if (peek() == 'e' || peek() == 'E') {
+        ++i_;
+        if (peek() == '+' || peek() == '-') ++i_;
+        if (!std::isdigit(static_cast<unsigned char>(peek()))) fail("bad number");
+        while (std::isdigit(static_cast<unsigned char>(peek()))) ++i_;
+      }
+    } else {
+      fail("unexpected character");
+    }
+  }
+  void ws() {
+    while (i_ < s_.size() && (s_[i_] == ' ' || s_[i_] == '\t' || s_[i_] == '\n' || s_[i_] == '\r')) ++i_;
+  }
+  char peek() const { return i_ < s_.size() ? s_[i_] : '\0'; }
+  char next() {
+    if (i_ >= s_.size()) fail("unexpected end of input");
+    return s_[i_++];
+  }
+  [[noreturn]] void fail(const std::string& what) const {
+    throw ParseError("adapter catalog " + path_ + ": " + what + " at byte " + std::to_string(i_));
+  }
+  const std::string& s_;
+  std::string path_;
+  std::size_t i_ = 0;
+};
+
+}  // namespace
 
 
 extern "C" {
@@ -115,6 +356,46 @@ int plora_size_table_bytes_for(const plora_size_table* t, uint32_t rank, uint64_
     *out = t->bytes_for(rank);
     return 0;
   });
+}
+
+int64_t plora_load_catalog_json(const char* path, const plora_size_table* sizes, uint32_t d,
+                                uint32_t k, uint32_t adapted, uint32_t bpp, uint32_t* ranks_out,
+                                uint64_t* bytes_out, char* ids_out, uint64_t id_stride,
+                                uint64_t cap) {
+  int64_t n = 0;
+  const int rc = guard([&] {  // load_catalog_json, adapter.cpp:81-108
+    if (!path) throw ValidationError("null path");
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw ConfigError(std::string("cannot open adapter catalog: ") + path);
+    std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+    const std::vector<CatalogEntry> cat = JsonReader(text, path).catalog();
+    plora_size_table def;
+    const plora_size_table& st = sizes ? *sizes : def;
+    std::vector<std::pair<uint32_t, uint64_t>> out;
+    for (const CatalogEntry& e : cat) {
+      if (!e.has_id || !e.has_rank) throw ParseError("catalog entry needs 'id' and 'rank'");
+      const uint32_t r = static_cast<uint32_t>(e.rank);
+      const uint64_t bytes = e.has_size ? e.size : st.bytes_for(r);
+      // AdapterSpec::sized -> validate (adapter.cpp:61-79)
+      validate_dims(d, k, r, adapted, bpp);
+      if (bytes == 0) throw ValidationError("adapter weight_bytes must be > 0");
+      out.emplace_back(r, bytes);
+    }
+    if (out.empty()) throw ValidationError("adapter catalog is empty");
+    for (uint64_t i = 0; i < out.size() && i < cap; ++i) {
+      if (ranks_out) ranks_out[i] = out[i].first;
+      if (bytes_out) bytes_out[i] = out[i].second;
+      if (ids_out && id_stride) {
+        const std::string& id = cat[i].id;
+        const uint64_t m = std::min<uint64_t>(id.size(), id_stride - 1);
+        std::memcpy(ids_out + i * id_stride, id.data(), m);
+        ids_out[i * id_stride + m] = '\0';
+      }
+    }
+    n = static_cast<int64_t>(out.size());
+    return 0;
+  });
+  return rc < 0 ? rc : n;
 }
 
 int plora_generate_catalog(uint32_t count, const uint32_t* mix_ranks, const double* mix_weights,
