@@ -89,7 +89,7 @@ struct SArgs {
 
 constexpr uint32_t kTraceStages = 512;
 __device__ __forceinline__ void tput(const SArgs& p, uint32_t gs, uint32_t f, uint64_t v) {
-  if (p.trace && gs < kTraceStages) p.trace[(blockIdx.x * kTraceStages + gs) * 8 + f] = v;
+  if (p.trace && gs < kTraceStages) p.trace[(blockIdx.x * kTraceStages + gs) * 12 + f] = v;
 }
 
 // Smem slot: [16 weight rows][JT activation rows (S: x, E: y)][v: 16 × JT fp32];
@@ -388,6 +388,7 @@ __device__ void consumers(const SArgs& p, char* smem) {
     const uint32_t job = h0.y, ntok = h0.z, width = h0.w;
     const uint32_t v_off = h1.x, off = h1.y, plane = h1.z, li_n = h1.w;
     const uint32_t sbase = ptx::smem_u32(smem + s * p.slot_bytes);
+    if (tid == 0) tput(p, gs, 8, (expand << 2) | (first << 1) | last);
     if (p.dbg & 1u) {
       // diagnostics: release the slot without the math (S items still publish v)
       if (!expand && last && w == 0 && lane == 0)
@@ -489,31 +490,40 @@ __device__ void consumers(const SArgs& p, char* smem) {
         if (w + j * kCWarps < ntiles)
 #pragma unroll
           for (uint32_t q = 0; q < NT; ++q) ptx::mma_bf16_16816(acc[j][q], a[j], bv[q]);
+      if (tid == 0) tput(p, gs, 9, clock64());
       if (last && !(p.dbg & 16u)) {  // y[tok][c0 + col] = bf16(y + scale · (hi + lo)), once per item
+        // the new values overwrite the staged y rows in place (each warp
+        // owns its 16-column tiles), then go out as 16-byte stores
         const uint32_t li = li_n >> 16;
-        const char* ysm = smem + s * p.slot_bytes + Slot<JT>::aux;
+        char* ysm = smem + s * p.slot_bytes + Slot<JT>::aux;
         const uint32_t* toks = hdr + s * kHdrWords + 8;
 #pragma unroll
         for (uint32_t q = 0; q < NT; ++q) {
           const uint32_t tok = q * 4 + cc;
           if (tok < ntok) {
-            const char* yrow = ysm + tok * kRowB;
-            char* yg = p.y[pj] + li * p.y_lstride_b[pj] + toks[tok] * p.y_stride_b[pj] +
-                       static_cast<uint64_t>(off) * 2;
-            auto put = [&](uint32_t col, float val) {
-              if (col < width) {
-                const float o = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(yrow + col * 2));
-                *reinterpret_cast<__nv_bfloat16*>(yg + col * 2) = __float2bfloat16_rn(fmaf(p.scale, val, o));
-              }
-            };
+            __nv_bfloat16* yrow = reinterpret_cast<__nv_bfloat16*>(ysm + tok * kRowB);
 #pragma unroll
             for (uint32_t j = 0; j < kTiles; ++j) {
               const uint32_t t = w + j * kCWarps;
               if (t < ntiles) {
-                put(t * 16 + gq, acc[j][q][0] + acc[j][q][1]);
-                put(t * 16 + gq + 8, acc[j][q][2] + acc[j][q][3]);
+                const uint32_t c = t * 16 + gq;
+                yrow[c] = __float2bfloat16_rn(fmaf(p.scale, acc[j][q][0] + acc[j][q][1], __bfloat162float(yrow[c])));
+                yrow[c + 8] = __float2bfloat16_rn(fmaf(p.scale, acc[j][q][2] + acc[j][q][3], __bfloat162float(yrow[c + 8])));
               }
             }
+          }
+        }
+        __syncwarp();
+        // this warp's tiles of every token: (token, tile, 16-byte half) per lane
+        const uint32_t nchunks = ntok * kTiles * 2;
+        for (uint32_t e = lane; e < nchunks; e += 32) {
+          const uint32_t tok = e / (kTiles * 2), j = (e / 2) % kTiles, hh = e & 1u;
+          const uint32_t t = w + j * kCWarps, c = t * 16 + hh * 8;
+          if (t < ntiles && c < width) {
+            const uint4 v = *reinterpret_cast<const uint4*>(ysm + tok * kRowB + c * 2);
+            char* yg = p.y[pj] + li * p.y_lstride_b[pj] + toks[tok] * p.y_stride_b[pj] +
+                       (static_cast<uint64_t>(off) + c) * 2;
+            *reinterpret_cast<uint4*>(yg) = v;
           }
         }
       }
@@ -693,7 +703,7 @@ void launch_jt(const plora_plan& plan, const StreamWork& w, uint32_t layer0, uin
   for (uint32_t i = 0; i < w.np; ++i) fast = fast && gm.prefix[w.projs[i]] % kKC == 0;
   a.fast = fast ? 1u : 0u;
   a.scale = scale;
-  a.trace = trace_buffer(static_cast<uint64_t>(w.ctas) * kTraceStages * 64);
+  a.trace = trace_buffer(static_cast<uint64_t>(w.ctas) * kTraceStages * 96);
   a.dbg = g_stream_dbg;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(w.ctas);

@@ -42,9 +42,9 @@ def main():
     per_layer = lambda: [bgmv_layer(plan, l, x[l], [y[l, 0], y[l, 1]]) for l in range(32)]  # noqa: E731
     multi = lambda: bgmv_layers(plan, 0, x, [y[:, 0], y[:, 1]])  # noqa: E731
     alg = 136314880
-    for impl in (0, 1):
+    for impl in (1, 0):  # 1 streaming, 0 clusters
         N.check(N.lib().plora_debug_set_bgmv_impl(impl))
-        for flags in ((0, 1, 2, 3, 4, 8, 16, 28) if impl == 0 else (0,)):
+        for flags in ((0, 1, 2, 3, 4, 8, 16, 28) if impl == 1 else (0,)):
             N.check(N.lib().plora_debug_set_bgmv_flags(flags))
             a = timeit(per_layer, 5) / 32
             b = timeit(multi, 5) / 32

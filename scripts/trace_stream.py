@@ -39,7 +39,7 @@ def main():
     for _ in range(3):
         call()
     ctas = 148
-    buf = torch.zeros(ctas * S * 8, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(ctas * S * 12, dtype=torch.int64, device="cuda")
     N.check(N.lib().plora_debug_set_trace(buf.data_ptr(), buf.numel() * 8))
     torch.cuda.synchronize()
     call()
@@ -52,7 +52,7 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     print(f"untraced {e0.elapsed_time(e1) * 1e3 / 20:.1f} us/launch")
-    t = buf.view(ctas, S, 8).cpu().numpy().astype(np.float64) / 1.965e3  # us
+    t = buf.view(ctas, S, 12).cpu().numpy().astype(np.float64) / 1.965e3  # us
     for c in range(ctas):
         v = t[c, :, 1] > 0
         if not v.any():
@@ -70,6 +70,19 @@ def main():
     w = wait[wait > 0]
     print(f"counter waits: n={len(w)} median {np.median(w) / 1.0 if len(w) else 0:.2f} us "
           f"p90 {np.percentile(w, 90) if len(w) else 0:.2f} max {w.max() if len(w) else 0:.2f}")
+    kind = buf.view(ctas, S, 12)[..., 8].cpu().numpy()
+    for kk, name in ((0, "S mid"), (1, "S last"), (2, "S first"), (4, "E mid"), (5, "E last"),
+                     (6, "E first"), (7, "E first+last")):
+        m = (kind == kk) & valid
+        if m.any():
+            x = (done - seen)[m]
+            print(f"consumer {name}: n={m.sum()} seen->released median {np.median(x):.3f} "
+                  f"p90 {np.percentile(x, 90):.3f} us")
+    m = valid & (t[..., 9] > 0)
+    if m.any():
+        print(f"E: seen -> math done median {np.median((t[..., 9] - seen)[m]):.3f} us; "
+              f"math done -> released median {np.median((done - t[..., 9])[m]):.3f} us")
+
     def d(a, b):
         m = (t[..., a] > 0) & (t[..., b] > 0)
         x = (t[..., b] - t[..., a])[m]
