@@ -374,7 +374,8 @@ __device__ void consumers(const SArgs& p, char* smem) {
   uint32_t s_items = 0, s = 0, ph = 0;
 #pragma unroll 1
   for (uint32_t gs = 0;; ++gs) {
-    ptx::mbar_wait(&full[s], ph);
+    if (p.dbg & 32u) ptx::mbar_wait(&full[s], ph);
+    else ptx::mbar_wait_spin(&full[s], ph);
     if (tid == 0) tput(p, gs, 1, clock64());
     const uint4 h0 = *reinterpret_cast<const uint4*>(hdr + s * kHdrWords);
     const uint4 h1 = *reinterpret_cast<const uint4*>(hdr + s * kHdrWords + 4);

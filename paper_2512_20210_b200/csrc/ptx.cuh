@@ -49,6 +49,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// Non-suspending probe (mbarrier.test_wait): a spin on it never sleeps past
+// the phase completion (try_wait may suspend the warp for a system-defined
+// time when the phase is not yet complete).
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test_wait(bar, parity)) {
+  }
+}
+
 // cp.async (LDGSTS) completion arrives on an mbarrier without incrementing
 // its pending count (the init count must include these arrivals).
 __device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
