@@ -12,7 +12,8 @@ import os
 from .errors import ConfigError, LogicError, ParseError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libplora.so")
+# PLORA_LIB: diagnostics only (A/B builds of the same ABI, scripts/); default in-tree
+LIB_PATH = os.environ.get("PLORA_LIB", os.path.join(_HERE, "libplora.so"))
 
 PLORA_OK = 0
 PLORA_E_VALIDATION = -1

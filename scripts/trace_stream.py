@@ -86,16 +86,20 @@ def main():
     def d(a, b):
         m = (t[..., a] > 0) & (t[..., b] > 0)
         x = (t[..., b] - t[..., a])[m]
+        if not len(x):
+            return "n/a"
         return f"median {np.median(x):.3f} p90 {np.percentile(x, 90):.3f}"
     print("producer: before slot wait -> slot free", d(4, 0))
     print("producer: slot free -> copies issued", d(0, 5))
-    print("producer: item start -> lookahead landed", d(6, 7))
-    print("producer: lookahead landed -> first stage's slot wait", d(7, 4))
-    for c in (0, 1, 70, 147):
+    for c in (0, 70):
         v = valid[c]
-        rows = [(round(issued[c, k] - base[c, 0], 2), round(seen[c, k] - base[c, 0], 2),
-                 round(done[c, k] - base[c, 0], 2), round(wait[c, k], 2)) for k in range(S) if v[k]]
-        print(f"CTA {c}:", rows[:40])
+        print(f"CTA {c}: stage kind issue seen released (us from the CTA's first issue)")
+        for k in range(S):
+            if v[k]:
+                print(f"  {k:3d} {int(kind[c, k]):d} {issued[c, k] - base[c, 0]:7.2f} "
+                      f"{seen[c, k] - base[c, 0]:7.2f} {done[c, k] - base[c, 0]:7.2f}")
+            if k > 60:
+                break
     np.savez(os.path.join(ROOT, "gpurun_out", "trace_stream.npz"), t=t)
 
 
