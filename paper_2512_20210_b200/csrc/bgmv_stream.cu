@@ -245,7 +245,7 @@ __device__ void producer(const SArgs& p, char* smem, uint32_t pw) {
     for (uint32_t st = st0, j = 0; st < nst; st += kPW, ++j) {
       const uint32_t gs = g + st;
       if (lane == 0) tput(p, gs, 4, clock64());
-      ptx::mbar_wait(&empty[pw], ph ^ 1u);
+      ptx::mbar_wait_backoff(&empty[pw], ph ^ 1u, 64);
       if (lane == 0) tput(p, gs, 0, clock64());
       const uint32_t rows = stage_rows(it, st);
       uint32_t bytes = 0;
@@ -566,6 +566,7 @@ __device__ void publisher(const SArgs& p, char* smem) {
     // wait for the partials, or for the consumers' exit (they raise the stop word)
     bool done = false;
     while (!ptx::mbar_try_wait(&pready[pbuf], (i / kPubBufs<JT>) & 1u)) {
+      __nanosleep(128);
       if (*reinterpret_cast<const volatile uint32_t*>(hdr + p.nslots * kHdrWords) != 0u) {
         // every consumer arrival precedes the exit word: one more look, then stop
         done = !ptx::mbar_try_wait(&pready[pbuf], (i / kPubBufs<JT>) & 1u);

@@ -44,7 +44,7 @@ def main():
     alg = 136314880
     for impl in (1, 0):  # 1 streaming, 0 clusters
         N.check(N.lib().plora_debug_set_bgmv_impl(impl))
-        for flags in ((0, 32, 1, 2) if impl == 1 else (0,)):
+        for flags in ((0, 128, 1, 2) if impl == 1 else (0,)):
             N.check(N.lib().plora_debug_set_bgmv_flags(flags))
             a = timeit(per_layer, 5) / 32
             b = timeit(multi, 5) / 32

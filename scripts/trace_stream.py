@@ -78,6 +78,11 @@ def main():
             x = (done - seen)[m]
             print(f"consumer {name}: n={m.sum()} seen->released median {np.median(x):.3f} "
                   f"p90 {np.percentile(x, 90):.3f} us")
+    m = valid & (t[..., 10] > 0) & (t[..., 11] > 0)
+    if m.any():
+        print(f"S: seen -> math start median {np.median((t[..., 10] - seen)[m]):.3f} us; math "
+              f"median {np.median((t[..., 11] - t[..., 10])[m]):.3f} us; math end -> released "
+              f"median {np.median((done - t[..., 11])[m]):.3f} us")
     m = valid & (t[..., 9] > 0)
     if m.any():
         print(f"E: seen -> math done median {np.median((t[..., 9] - seen)[m]):.3f} us; "
