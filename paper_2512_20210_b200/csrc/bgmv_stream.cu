@@ -381,7 +381,7 @@ __device__ void consumers(const SArgs& p, char* smem) {
     const uint4 h1 = *reinterpret_cast<const uint4*>(hdr + s * kHdrWords + 4);
     if (h0.x == kStop) {  // after every consumer warp handed off its last partials: tell the publisher
       ptx::named_bar_sync(1, kCThreads);
-      if (tid == 0) *reinterpret_cast<volatile uint32_t*>(const_cast<uint32_t*>(hdr) + p.nslots * kHdrWords) = 1u;
+      if (tid == 0) ptx::mbar_arrive(empty + p.nslots + 2 * kPubBufs<JT>);  // cdone
       break;
     }
     const uint32_t expand = h0.x >> 31, first = (h0.x >> 30) & 1u, last = (h0.x >> 29) & 1u;
@@ -443,8 +443,7 @@ __device__ void consumers(const SArgs& p, char* smem) {
           meta[3] = ntok;
           meta[4] = job;
         }
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&pready[pbuf]);
+        ptx::mbar_arrive(&pready[pbuf]);  // every consumer thread: its own writes precede it
         ++s_items;
       }
     } else {
@@ -529,10 +528,9 @@ __device__ void consumers(const SArgs& p, char* smem) {
         }
       }
     }
-    __syncwarp();  // this warp's slot reads are done
+    ptx::mbar_arrive(&empty[s]);  // every consumer thread releases its own reads of the slot
     if (lane == 0) {
       if (w == 0) tput(p, gs, 2, clock64());
-      ptx::mbar_arrive(&empty[s]);  // one arrival per consumer warp
       if (w == 0 && expand && last) {  // the job's last E item resets its counters for the next call
         uint32_t* c = p.cnt + static_cast<uint64_t>(plane) * 2 * p.njobs;
         const uint32_t ne = li_n & 0xffffu;
@@ -559,7 +557,7 @@ __device__ void publisher(const SArgs& p, char* smem) {
   uint64_t* pfree = pready + kPubBufs<JT>;
   const float* part = reinterpret_cast<const float*>(smem + p.off_part);
   const uint32_t* metas = reinterpret_cast<const uint32_t*>(part + kPubBufs<JT> * kCWarps * kWRows * JT);
-  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(smem + p.off_hdr);
+  uint64_t* cdone = pfree + kPubBufs<JT>;  // the consumers have exited
   ptx::pdl_wait();
   for (uint32_t i = 0;; ++i) {
     const uint32_t pbuf = i % kPubBufs<JT>;
@@ -567,8 +565,8 @@ __device__ void publisher(const SArgs& p, char* smem) {
     bool done = false;
     while (!ptx::mbar_try_wait(&pready[pbuf], (i / kPubBufs<JT>) & 1u)) {
       __nanosleep(128);
-      if (*reinterpret_cast<const volatile uint32_t*>(hdr + p.nslots * kHdrWords) != 0u) {
-        // every consumer arrival precedes the exit word: one more look, then stop
+      if (ptx::mbar_test_wait(cdone, 0)) {
+        // every consumer arrival precedes cdone: one more look, then stop
         done = !ptx::mbar_try_wait(&pready[pbuf], (i / kPubBufs<JT>) & 1u);
         break;
       }
@@ -610,13 +608,13 @@ __global__ void __launch_bounds__(Slot<JT>::threads, 1) bgmv_stream_kernel(const
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
     for (uint32_t s = 0; s < p.nslots; ++s) {
       ptx::mbar_init(&full[s], 1);             // the slot's producer warp (+ tx bytes)
-      ptx::mbar_init(&full[p.nslots + s], kCWarps);  // empty: every consumer warp's release
+      ptx::mbar_init(&full[p.nslots + s], kCThreads);  // empty: every consumer thread's release
     }
     for (uint32_t b = 0; b < kPubBufs<JT>; ++b) {
-      ptx::mbar_init(&full[2 * p.nslots + b], kCWarps);       // partials of an S item written
+      ptx::mbar_init(&full[2 * p.nslots + b], kCThreads);     // partials of an S item written
       ptx::mbar_init(&full[2 * p.nslots + kPubBufs<JT> + b], 1);  // publisher done with the buffer
     }
-    *reinterpret_cast<volatile uint32_t*>(smem + p.off_hdr + p.nslots * kHdrWords * 4) = 0u;  // consumers' exit word
+    ptx::mbar_init(&full[2 * p.nslots + 2 * kPubBufs<JT>], 1);  // cdone: the consumers have exited
     ptx::fence_mbar_init();
   }
   __syncthreads();
@@ -646,7 +644,7 @@ Geom geom() {
   (void)per_slot;
   g.off_hdr = g.nslots * g.slot_bytes;
   g.off_bar = g.off_hdr + (g.nslots + 1) * kHdrWords * 4;  // + the consumers' exit word
-  g.off_ring = (g.off_bar + (2 * g.nslots + 2 * kPubBufs<JT>) * 8 + 127) / 128 * 128;
+  g.off_ring = (g.off_bar + (2 * g.nslots + 2 * kPubBufs<JT> + 1) * 8 + 127) / 128 * 128;
   g.off_part = g.off_ring + ring;
   g.smem = g.off_part + part;
   return g;

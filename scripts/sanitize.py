@@ -1,7 +1,8 @@
 """Small paged-LoRA calls for compute-sanitizer (memcheck / racecheck /
-synccheck): the cluster BGMV (per projection and fused per layer), the SGMV
-(per projection, per layer, fused with the base GEMM) and the TP halves on a
-2-layer cfg1 store.
+synccheck): the cluster BGMV (per projection, fused per layer, multi-layer),
+the streaming BGMV (4- and 8-token jobs), the SGMV (per projection, per layer,
+fused with the base GEMM, 512 B and 1 KiB pages), the TP halves, the GPU
+predict_all and a host-store-fed engine on small stores.
 
 compute-sanitizer --tool memcheck python scripts/sanitize.py
 """
@@ -48,6 +49,42 @@ def main():
         bgmv_tp_shrink(plan, 0, 0, i, 2, x, vp[i])
     for i in range(2):
         bgmv_tp_expand(plan, 0, 0, i, 2, vp, ys[0][:, i * 2048:(i + 1) * 2048])
+    # multi-layer launch
+    from paper_2512_20210_b200.lora import bgmv_layers
+    xl = torch.randn(2, T, 4096, device="cuda").to(torch.bfloat16)
+    yl = torch.randn(2, 2, T, 4096, device="cuda").to(torch.bfloat16)
+    bgmv_layers(plan, 0, xl, [yl[:, 0], yl[:, 1]])
+    # streaming decode kernel, 4- and 8-token jobs
+    from paper_2512_20210_b200 import _native as N
+    N.check(N.lib().plora_debug_set_bgmv_impl(1))
+    bgmv_layer(plan, 1, x, ys)
+    ta8 = synth.token_assignment(cfg.n_adapters, 6)
+    x8 = torch.randn(len(ta8), 4096, device="cuda").to(torch.bfloat16)
+    y8 = [torch.randn(len(ta8), 4096, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    plan8 = BatchPlan(s.store, ta8)
+    bgmv_layer(plan8, 0, x8, y8)
+    bgmv_layers(plan, 0, xl, [yl[:, 0], yl[:, 1]])
+    N.check(N.lib().plora_debug_set_bgmv_impl(0))
+    # fused prefill on 512 B / 1 KiB pages (the gather4 thresholds)
+    from paper_2512_20210_b200.lora import ModelShape
+    for page in (512, 1024):
+        shape = ModelShape(2, (1024, 1024), (1024, 512), torch.bfloat16)
+        cs = synth.DecodeConfig("san", shape, [16, 64, 128, 5], 1, page)
+        ss = Setup(cs)
+        sg = synth.segment_assignment(4, 150)
+        xx = torch.randn(len(sg), 1024, device="cuda").to(torch.bfloat16)
+        pf = BatchPlan(ss.store, sg)
+        sgmv_fused(pf, 1, 0, xx, torch.randn(1024, 1024, device="cuda").to(torch.bfloat16),
+                   torch.empty(len(sg), 1024, device="cuda", dtype=torch.bfloat16))
+        sgmv(pf, 1, 1, xx, torch.randn(len(sg), 512, device="cuda").to(torch.bfloat16))
+    # predict_all on the GPU
+    from paper_2512_20210_b200.predictor import OnlinePredictor, OnlinePredictorConfig, PredictorConfig
+    pred = OnlinePredictor(OnlinePredictorConfig(model=PredictorConfig(num_adapters=50),
+                                                 train_every=10 ** 9), 1)
+    for a in range(50):
+        pred.observe(a, float(a))
+    pred.set_device(0)
+    pred.predict_arrays(2000.0)
     torch.cuda.synchronize()
     print("sanitize run ok")
 
