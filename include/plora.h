@@ -319,9 +319,14 @@ int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x
  * batching): the decode clusters stay resident and stream layer l+1's pages
  * right behind layer l's, so the per-launch prologue / drain / CTA
  * turnaround is paid once.  Layer layer0 + i reads x + i·x_layer_stride and
- * updates ys[p] + i·y_layer_strides[p] (all strides in elements).  Results
- * are bit-identical to n_layers plora_bgmv_layer calls.  bf16 stores with
- * equal projection shapes; otherwise one plora_bgmv_layer per layer. */
+ * updates ys[p] + i·y_layer_strides[p] (all strides in elements).  On GPUs
+ * whose SM count leaves SMs outside the 4-CTA clusters (148 - 132 on B200)
+ * the plan gives a byte-proportional share of the adapters to the streaming
+ * kernel, which runs on those SMs concurrently (an internal aux stream, fork /
+ * join by events, so `stream` orders after both).  Deterministic; equal to
+ * n_layers plora_bgmv_layer calls within the bf16 tolerance, bit for bit
+ * with plora_debug_set_bgmv_impl(2) (clusters only).  bf16 stores with equal
+ * projection shapes; otherwise one plora_bgmv_layer per layer. */
 int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_layers, const void* x,
                       uint64_t x_stride, uint64_t x_layer_stride, void* const* ys,
                       const uint64_t* y_strides, const uint64_t* y_layer_strides, float scale,
@@ -553,12 +558,16 @@ int plora_predictor_buffer_at(const plora_predictor* p, uint64_t i, uint32_t* ad
  * CTA start / end).  dev_buf = NULL disables tracing. */
 int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
 /* Diagnostics: the bf16 decode kernel behind plora_bgmv* — 0 thread-block
- * clusters (bgmv_cluster.cu, default), 1 the streaming kernel
- * (bgmv_stream.cu; measured alternative). */
+ * clusters (bgmv_cluster.cu), with the hybrid streaming share for
+ * plora_bgmv_layers (default); 1 the streaming kernel alone (bgmv_stream.cu);
+ * 2 clusters only.  Applies to plans built afterwards for the hybrid split. */
 int plora_debug_set_bgmv_impl(int impl);
 /* Diagnostics for the streaming kernel: 1 consumers skip the math, 2 no
  * weight copies (results are then wrong; timing ablation only). */
 int plora_debug_set_bgmv_flags(uint32_t flags);
+/* Diagnostics: plans built afterwards give the streaming kernel at most
+ * `ctas` CTAs (0 = one per SM). */
+int plora_debug_set_stream_ctas(uint32_t ctas);
 /* Launch geometry the plan chose for the bf16 decode op of projection
  * `proj`: out[0..7] = {cluster size, input slice, output slice, A-row ring
  * slots, Bᵀ-row ring slots, dynamic smem bytes, clusters, chunks}. */

@@ -408,8 +408,15 @@ void check_io(const plora_plan* plan, uint32_t layer, uint32_t proj, const void*
 }  // namespace plora
 
 namespace {
-int g_bgmv_impl = 0;  // bf16 decode kernel: 0 clusters (bgmv_cluster.cu), 1 streaming (bgmv_stream.cu)
+// bf16 decode kernel: 0 clusters (bgmv_cluster.cu), and for multi-layer
+// launches the hybrid with a streaming share on the idle SMs; 1 the streaming
+// kernel alone (bgmv_stream.cu); 2 clusters only
+int g_bgmv_impl = 0;
 }  // namespace
+
+namespace plora {
+bool hybrid_enabled() { return g_bgmv_impl == 0; }
+}  // namespace plora
 
 extern "C" int plora_debug_set_bgmv_impl(int impl) {
   g_bgmv_impl = impl;
@@ -489,6 +496,28 @@ extern "C" int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_l
       DeviceCtx ctx(st.device);
       launch_bgmv_stream(*plan, plan->swork_layer, layer0, n_layers, x, x_stride, x_layer_stride,
                          ys, y_strides, y_layer_strides, scale, static_cast<cudaStream_t>(stream));
+      return 0;
+    }
+    if (g.esize == 2 && g_bgmv_impl == 0 && plan->hyb_spare && plan->n_layer_proj == g.m.n_proj &&
+        n_layers * g.m.n_proj <= 256) {
+      // hybrid: the streaming share forks onto the plan's aux stream, the
+      // clusters run on `stream`, and `stream` joins the aux stream (the two
+      // shares touch disjoint adapters and y rows)
+      DeviceCtx ctx(st.device);
+      cudaStream_t s = static_cast<cudaStream_t>(stream);
+      if (!plan->aux_stream) {
+        PLORA_CUDA(cudaStreamCreateWithFlags(&plan->aux_stream, cudaStreamNonBlocking));
+        PLORA_CUDA(cudaEventCreateWithFlags(&plan->ev_fork, cudaEventDisableTiming));
+        PLORA_CUDA(cudaEventCreateWithFlags(&plan->ev_join, cudaEventDisableTiming));
+      }
+      PLORA_CUDA(cudaEventRecord(plan->ev_fork, s));
+      PLORA_CUDA(cudaStreamWaitEvent(plan->aux_stream, plan->ev_fork, 0));
+      launch_bgmv_cluster_layers(*plan, layer0, n_layers, x, x_stride, x_layer_stride, ys, y_strides,
+                                 y_layer_strides, scale, s, &plan->cwork_hyb);
+      launch_bgmv_stream(*plan, plan->swork_hyb, layer0, n_layers, x, x_stride, x_layer_stride, ys,
+                         y_strides, y_layer_strides, scale, plan->aux_stream);
+      PLORA_CUDA(cudaEventRecord(plan->ev_join, plan->aux_stream));
+      PLORA_CUDA(cudaStreamWaitEvent(s, plan->ev_join, 0));
       return 0;
     }
     const bool one = g.esize == 2 && plan->n_layer_proj == g.m.n_proj &&

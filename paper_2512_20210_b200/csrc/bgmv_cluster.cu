@@ -928,11 +928,12 @@ void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const voi
 void launch_bgmv_cluster_layers(const plora_plan& plan, uint32_t layer0, uint32_t n_layers,
                                 const void* x, uint64_t x_stride, uint64_t x_lstride,
                                 void* const* ys, const uint64_t* y_strides,
-                                const uint64_t* y_lstrides, float scale, cudaStream_t stream) {
+                                const uint64_t* y_lstrides, float scale, cudaStream_t stream,
+                                const ClusterWork* work) {
   uint32_t projs[PLORA_MAX_PROJ];
   for (uint32_t i = 0; i < plan.n_layer_proj; ++i) projs[i] = i;
-  launch(plan, plan.cwork_layer, layer0, projs, plan.n_layer_proj, x, x_stride, ys, y_strides,
-         scale, stream, n_layers, x_lstride, y_lstrides);
+  launch(plan, work ? *work : plan.cwork_layer, layer0, projs, plan.n_layer_proj, x, x_stride, ys,
+         y_strides, scale, stream, n_layers, x_lstride, y_lstrides);
 }
 
 namespace {

@@ -627,6 +627,7 @@ __global__ void __launch_bounds__(Slot<JT>::threads, 1) bgmv_stream_kernel(const
 }
 
 uint32_t g_stream_dbg = 0;
+uint32_t g_stream_ctas = 0;  // plora_debug_set_stream_ctas
 
 struct Geom {
   uint32_t nslots, slot_bytes, off_hdr, off_bar, off_ring, off_part, smem;
@@ -751,7 +752,13 @@ uint32_t stream_max_ctas(int device, uint32_t jt) {
     it = sms.emplace(device, n).first;
   }
   (void)jt;
-  return static_cast<uint32_t>(it->second);
+  const uint32_t n = static_cast<uint32_t>(it->second);
+  return g_stream_ctas ? std::min(n, g_stream_ctas) : n;
+}
+
+extern "C" int plora_debug_set_stream_ctas(uint32_t ctas) {
+  g_stream_ctas = ctas;  // plans built afterwards use at most `ctas` CTAs (0: one per SM)
+  return 0;
 }
 
 }  // namespace plora

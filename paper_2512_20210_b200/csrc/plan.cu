@@ -271,15 +271,56 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     }
   }
 
+  // ---- decode step in one launch (plora_bgmv_layers), hybrid: the 4-CTA
+  // clusters fit on 4·n_clusters SMs (132 of 148 on B200); the streaming
+  // kernel (bgmv_stream.cu) runs a share of the adapters on the SMs they
+  // leave idle, concurrently, sized by SM count (both stream ~31 GB/s per SM
+  // at cfg2, profiles/r02g_hybrid_probe.txt)
+  seg_hyb.assign(segs.size(), 0);
+  hyb_spare = 0;
+  bool layer_same = g.m.n_proj > 1;
+  for (uint32_t p = 1; p < g.m.n_proj; ++p)
+    layer_same = layer_same && g.m.d_in[p] == g.m.d_in[0] && g.m.d_out[p] == g.m.d_out[0];
+  if (es == 2 && layer_same && hybrid_enabled() && !segs.empty()) {
+    const ClusterGeom cg = cluster_geom(g.m.d_in[0], g.m.d_out[0], st.device);
+    const uint32_t sms = static_cast<uint32_t>(std::max(1, st.num_sms));
+    const uint32_t used = cg.n_clusters * cg.cs;
+    if (sms > used + 3) {
+      hyb_spare = sms - used;
+      uint64_t total = 0;
+      for (const Seg& sg : segs) total += static_cast<uint64_t>(sg.rank) * sg.toks.size();
+      std::vector<uint32_t> by(segs.size());
+      std::iota(by.begin(), by.end(), 0u);
+      auto bytes_of = [&](uint32_t i) {  // weight rows streamed per token group (rank per job)
+        return static_cast<uint64_t>(segs[i].rank) * ((segs[i].toks.size() + kJobTok - 1) / kJobTok);
+      };
+      uint64_t all = 0;
+      for (uint32_t i = 0; i < segs.size(); ++i) all += bytes_of(i);
+      std::stable_sort(by.begin(), by.end(), [&](uint32_t a, uint32_t b) { return bytes_of(a) > bytes_of(b); });
+      const double target = static_cast<double>(all) * hyb_spare / sms * 0.95;
+      uint64_t acc = 0;
+      for (uint32_t i : by)
+        if (static_cast<double>(acc + bytes_of(i)) <= target) {
+          seg_hyb[i] = 1;
+          acc += bytes_of(i);
+        }
+      if (acc == 0) hyb_spare = 0;
+      (void)total;
+    }
+  }
+
   // ---- bf16 BGMV on clusters: jobs (<= kJobTok tokens of one adapter),
   // LPT-assigned to clusters by bytes, cut into kChunkRows-row chunks
   cjobs.clear();
   cchunks.clear();
   ccl_off.clear();
   ccl_jobs.clear();
+  std::vector<uint8_t> cjob_hyb;
   if (es == 2) {
-    for (const Seg& s : segs)
+    for (uint32_t si = 0; si < segs.size(); ++si) {
+      const Seg& s = segs[si];
       for (uint32_t tc = 0; tc < s.toks.size(); tc += kJobTok) {
+        cjob_hyb.push_back(seg_hyb[si]);
         ClusterJob j{};
         j.table_off = s.table_off;
         j.rank = s.rank;
@@ -287,6 +328,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
         for (uint32_t t = 0; t < j.ntok; ++t) j.tok[t] = s.toks[tc + t];
         cjobs.push_back(j);
       }
+    }
     const uint32_t nj = static_cast<uint32_t>(cjobs.size());
     std::vector<uint8_t> multi(nj, 0);  // the job's adapter has more than one job
     {
@@ -299,16 +341,19 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     // One chunk list per launch: the jobs of the given projections (tagged
     // with their index in the launch) LPT-assigned to clusters by bytes
     // (heaviest first onto the least-loaded cluster, ties: lowest index).
-    auto build = [&](ClusterWork& cw, const uint32_t* projs, uint32_t np) {
+    // exclude_hyb: leave out the jobs of the streaming share (hybrid launch)
+    auto build = [&](ClusterWork& cw, const uint32_t* projs, uint32_t np, bool exclude_hyb = false) {
       cw = ClusterWork{};
       if (nj == 0) return;
       const uint32_t din = g.m.d_in[projs[0]], dout = g.m.d_out[projs[0]];
       cw.geom = cluster_geom(din, dout, st.device);
-      const uint32_t nw = nj * np;
+      std::vector<uint32_t> jo;  // work item w = job w % nj of projection w / nj
+      for (uint32_t w = 0; w < nj * np; ++w)
+        if (!exclude_hyb || !cjob_hyb[w % nj]) jo.push_back(w);
+      const uint32_t nw = static_cast<uint32_t>(jo.size());
+      if (nw == 0) return;
       const uint32_t nc = std::min(cw.geom.n_clusters, nw);
       cw.geom.n_clusters = nc;
-      std::vector<uint32_t> jo(nw);  // work item w = job w % nj of projection w / nj
-      std::iota(jo.begin(), jo.end(), 0u);
       auto cost = [&](uint32_t w) {
         const ClusterJob& j = cjobs[w % nj];
         return static_cast<uint64_t>(j.rank + j.ntok) * (din + dout);
@@ -361,6 +406,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       for (uint32_t p = 0; p < g.m.n_proj; ++p) all[p] = p;
       build(cwork_layer, all, g.m.n_proj);
       n_layer_proj = g.m.n_proj;
+      cwork_hyb = ClusterWork{};
+      if (hyb_spare) build(cwork_hyb, all, g.m.n_proj, true);
     }
   }
 
@@ -378,6 +425,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     s_jt = maxtok > 4 ? 8 : 4;
     struct SJob {
       uint32_t rank, table_off, ntok, v_off, tok[8];
+      uint8_t hyb;  // the adapter belongs to the hybrid launch's streaming share
     };
     std::vector<SJob> jobs;
     uint64_t voff = 0;
@@ -390,6 +438,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
         j.ntok = std::min<uint32_t>(s_jt, static_cast<uint32_t>(sg.toks.size()) - tc);
         for (uint32_t t = 0; t < j.ntok; ++t) j.tok[t] = sg.toks[tc + t];
         j.v_off = static_cast<uint32_t>(voff);
+        j.hyb = seg_hyb[si];
         voff += static_cast<uint64_t>((sg.rank + 15) & ~15u) * s_jt;  // rows padded to 16 (kept zero)
         jobs.push_back(j);
       }
@@ -398,7 +447,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     s_njobs = static_cast<uint32_t>(jobs.size());
     s_vplane = (voff + 3) & ~3ull;
     const uint32_t max_ctas = stream_max_ctas(st.device, s_jt);
-    auto build_sw = [&](StreamWork& w, const uint32_t* projs, uint32_t np) {
+    auto build_sw = [&](StreamWork& w, const uint32_t* projs, uint32_t np, uint32_t cta_cap = 0,
+                        bool only_hyb = false) {
       w = StreamWork{};
       w.np = np;
       for (uint32_t i = 0; i < np; ++i) w.projs[i] = projs[i];
@@ -416,6 +466,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       std::vector<Cand> sc, ec;
       for (uint32_t jn = 0; jn < jobs.size(); ++jn) {
         const SJob& j = jobs[jn];
+        if (only_hyb && !j.hyb) continue;
         const uint32_t ns = j.rank * j.ntok;  // v elements: each released on its own
         for (uint32_t i = 0; i < np; ++i) {
           StreamItem base{};
@@ -443,7 +494,9 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
           }
         }
       }
-      const uint32_t ctas = std::min<uint32_t>(max_ctas, static_cast<uint32_t>(sc.size() + ec.size()));
+      if (sc.empty() && ec.empty()) return;
+      const uint32_t ctas = std::min<uint32_t>(cta_cap ? std::min(cta_cap, max_ctas) : max_ctas,
+                                               static_cast<uint32_t>(sc.size() + ec.size()));
       std::vector<double> load(ctas, 0.0);
       std::vector<std::vector<uint32_t>> lists_s(ctas), lists_e(ctas);
       std::vector<double> ready(jobs.size() * np, 0.0);
@@ -494,6 +547,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       uint32_t all[PLORA_MAX_PROJ];
       for (uint32_t p = 0; p < g.m.n_proj; ++p) all[p] = p;
       build_sw(swork_layer, all, g.m.n_proj);
+      swork_hyb = StreamWork{};
+      if (hyb_spare) build_sw(swork_hyb, all, g.m.n_proj, hyb_spare, true);
     }
   }
 
@@ -644,6 +699,9 @@ void plora_plan_destroy(plora_plan* plan) {
   cudaFree(plan->d_v);
   cudaFree(plan->d_sv);
   cudaFree(plan->d_scnt);
+  if (plan->aux_stream) cudaStreamDestroy(plan->aux_stream);
+  if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
+  if (plan->ev_join) cudaEventDestroy(plan->ev_join);
   cudaFree(plan->d_sync);
   cudaFree(plan->d_vpart);
   cudaFree(plan->d_vbuf);

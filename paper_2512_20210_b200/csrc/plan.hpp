@@ -265,6 +265,15 @@ struct plora_plan {
   uint64_t scnt_cap = 0;
   void build_stream(const std::vector<std::vector<uint32_t>>& seg_toks,
                     const std::vector<uint32_t>& seg_rank, const std::vector<uint32_t>& seg_table);
+  // hybrid decode launch (plora_bgmv_layers): the clusters' share and the
+  // streaming kernel's share on the SMs the clusters leave idle, run
+  // concurrently on `stream` and `aux_stream` (fork / join by events)
+  std::vector<uint8_t> seg_hyb;
+  uint32_t hyb_spare = 0;             // SMs the streaming share runs on (0: no hybrid)
+  plora::ClusterWork cwork_hyb;
+  plora::StreamWork swork_hyb;
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t upload_done = nullptr;
 
   void build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream);
@@ -286,6 +295,7 @@ void launch_bgmv_stream(const plora_plan& plan, const StreamWork& w, uint32_t la
                         void* const* ys, const uint64_t* y_strides, const uint64_t* y_lstrides,
                         float scale, cudaStream_t stream);
 uint32_t stream_max_ctas(int device, uint32_t jt);
+bool hybrid_enabled();  // plora_debug_set_bgmv_impl: 0 (default) = clusters + streaming share
 // Every projection of `layer` (they read the same x) in one launch.
 void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const void* x,
                                uint64_t x_stride, void* const* ys, const uint64_t* y_strides,
@@ -297,5 +307,6 @@ void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const voi
 void launch_bgmv_cluster_layers(const plora_plan& plan, uint32_t layer0, uint32_t n_layers,
                                 const void* x, uint64_t x_stride, uint64_t x_lstride,
                                 void* const* ys, const uint64_t* y_strides,
-                                const uint64_t* y_lstrides, float scale, cudaStream_t stream);
+                                const uint64_t* y_lstrides, float scale, cudaStream_t stream,
+                                const ClusterWork* work = nullptr);  // default: plan.cwork_layer
 }  // namespace plora

@@ -334,14 +334,33 @@ def test_bgmv_layers_multi_layer_launch_bit_identical(cuda, page_bytes):
     ref = y0.clone()
     for i in range(3):
         bgmv_layer(plan, 1 + i, x[i], [ref[i, 0], ref[i, 1]], 0.5)
-    got = y0.clone()
+    from paper_2512_20210_b200 import _native as N
+    N.check(N.lib().plora_debug_set_bgmv_impl(2))  # clusters only: the same chunks as bgmv_layer
+    try:
+        got = y0.clone()
+        n0 = kernel_launch_count()
+        bgmv_layers(BatchPlan(s.store, ta), 1, x, [got[:, 0], got[:, 1]], 0.5)
+        torch.cuda.synchronize()
+        assert kernel_launch_count() - n0 == 1
+        assert torch.equal(got, ref)
+    finally:
+        N.check(N.lib().plora_debug_set_bgmv_impl(0))
+    # default: the hybrid launch (clusters + a streaming share on the idle SMs)
+    hyb = y0.clone()
+    plan_h = BatchPlan(s.store, ta)
     n0 = kernel_launch_count()
-    bgmv_layers(plan, 1, x, [got[:, 0], got[:, 1]], 0.5)
+    bgmv_layers(plan_h, 1, x, [hyb[:, 0], hyb[:, 1]], 0.5)
     torch.cuda.synchronize()
-    assert kernel_launch_count() - n0 == 1
-    assert torch.equal(got, ref)
-    o = s.oracle(3, 1, x[2].cpu(), y0[2, 1].cpu(), ta, scale=0.5)
-    assert rel_err(got[2, 1], o) <= TOL_BF16
+    assert kernel_launch_count() - n0 == 2
+    again = y0.clone()
+    bgmv_layers(plan_h, 1, x, [again[:, 0], again[:, 1]], 0.5)
+    torch.cuda.synchronize()
+    assert torch.equal(hyb, again)  # deterministic
+    for i in range(3):
+        for p in range(2):
+            o = s.oracle(1 + i, p, x[i].cpu(), y0[i, p].cpu(), ta, scale=0.5)
+            assert rel_err(hyb[i, p], o) <= TOL_BF16, (i, p)
+            assert rel_err(got[i, p], o) <= TOL_BF16, (i, p)
 
 
 @pytest.mark.parametrize("tokens_per_adapter", [2, 6])
