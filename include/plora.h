@@ -568,6 +568,11 @@ int plora_debug_set_bgmv_flags(uint32_t flags);
 /* Diagnostics: plans built afterwards give the streaming kernel at most
  * `ctas` CTAs (0 = one per SM). */
 int plora_debug_set_stream_ctas(uint32_t ctas);
+/* Diagnostics: the hybrid decode launch's streaming share = spare SMs / SMs ×
+ * factor of the weight rows (default 0.95; plans built afterwards), and a
+ * plan's split: {spare SMs, share fraction, clusters, streaming CTAs}. */
+int plora_debug_set_hybrid_share(double factor);
+int plora_debug_plan_hybrid(const plora_plan* plan, double out[4]);
 /* Launch geometry the plan chose for the bf16 decode op of projection
  * `proj`: out[0..7] = {cluster size, input slice, output slice, A-row ring
  * slots, Bᵀ-row ring slots, dynamic smem bytes, clusters, chunks}. */

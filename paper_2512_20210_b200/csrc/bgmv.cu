@@ -416,7 +416,26 @@ int g_bgmv_impl = 0;
 
 namespace plora {
 bool hybrid_enabled() { return g_bgmv_impl == 0; }
+double g_hybrid_factor = 0.95;
+double hybrid_share_factor() { return g_hybrid_factor; }
 }  // namespace plora
+
+extern "C" int plora_debug_set_hybrid_share(double factor) {
+  plora::g_hybrid_factor = factor;  // plans built afterwards
+  return 0;
+}
+
+extern "C" int plora_debug_plan_hybrid(const plora_plan* plan, double out[4]) {
+  using namespace plora;
+  return guard([&] {
+    if (!plan || !out) throw ValidationError("null plan or out");
+    out[0] = plan->hyb_spare;                       // SMs the streaming share runs on (0: none)
+    out[1] = plan->hyb_frac;                        // its fraction of the step's weight rows
+    out[2] = plan->cwork_hyb.geom.n_clusters;       // clusters of the cluster share
+    out[3] = plan->swork_hyb.ctas;                  // CTAs of the streaming share
+    return 0;
+  });
+}
 
 extern "C" int plora_debug_set_bgmv_impl(int impl) {
   g_bgmv_impl = impl;

@@ -278,10 +278,15 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   // at cfg2, profiles/r02g_hybrid_probe.txt)
   seg_hyb.assign(segs.size(), 0);
   hyb_spare = 0;
+  hyb_frac = 0.0;
   bool layer_same = g.m.n_proj > 1;
   for (uint32_t p = 1; p < g.m.n_proj; ++p)
     layer_same = layer_same && g.m.d_in[p] == g.m.d_in[0] && g.m.d_out[p] == g.m.d_out[0];
-  if (es == 2 && layer_same && hybrid_enabled() && !segs.empty()) {
+  uint32_t seg_maxtok = 0;
+  for (const Seg& sg : segs) seg_maxtok = std::max<uint32_t>(seg_maxtok, static_cast<uint32_t>(sg.toks.size()));
+  // (batches with an adapter of more than 4 tokens would run the streaming
+  // share with 8-token jobs, which measured 2x slower: clusters only then)
+  if (es == 2 && layer_same && hybrid_enabled() && !segs.empty() && seg_maxtok <= kJobTok) {
     const ClusterGeom cg = cluster_geom(g.m.d_in[0], g.m.d_out[0], st.device);
     const uint32_t sms = static_cast<uint32_t>(std::max(1, st.num_sms));
     const uint32_t used = cg.n_clusters * cg.cs;
@@ -297,7 +302,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       uint64_t all = 0;
       for (uint32_t i = 0; i < segs.size(); ++i) all += bytes_of(i);
       std::stable_sort(by.begin(), by.end(), [&](uint32_t a, uint32_t b) { return bytes_of(a) > bytes_of(b); });
-      const double target = static_cast<double>(all) * hyb_spare / sms * 0.95;
+      const double target = static_cast<double>(all) * hyb_spare / sms * hybrid_share_factor();
       uint64_t acc = 0;
       for (uint32_t i : by)
         if (static_cast<double>(acc + bytes_of(i)) <= target) {
@@ -305,6 +310,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
           acc += bytes_of(i);
         }
       if (acc == 0) hyb_spare = 0;
+      hyb_frac = all ? static_cast<double>(acc) / static_cast<double>(all) : 0.0;
       (void)total;
     }
   }

@@ -270,6 +270,7 @@ struct plora_plan {
   // concurrently on `stream` and `aux_stream` (fork / join by events)
   std::vector<uint8_t> seg_hyb;
   uint32_t hyb_spare = 0;             // SMs the streaming share runs on (0: no hybrid)
+  double hyb_frac = 0.0;              // the streaming share's fraction of the weight rows
   plora::ClusterWork cwork_hyb;
   plora::StreamWork swork_hyb;
   cudaStream_t aux_stream = nullptr;
@@ -296,6 +297,7 @@ void launch_bgmv_stream(const plora_plan& plan, const StreamWork& w, uint32_t la
                         float scale, cudaStream_t stream);
 uint32_t stream_max_ctas(int device, uint32_t jt);
 bool hybrid_enabled();  // plora_debug_set_bgmv_impl: 0 (default) = clusters + streaming share
+double hybrid_share_factor();  // streaming share = spare SMs / SMs × this (of the weight bytes)
 // Every projection of `layer` (they read the same x) in one launch.
 void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const void* x,
                                uint64_t x_stride, void* const* ys, const uint64_t* y_strides,
