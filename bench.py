@@ -468,6 +468,17 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
+    if mlp > 1 and not prefill:  # the decode launch's split (plora_bgmv_layers)
+        import ctypes as C
+        from paper_2512_20210_b200 import _native as N
+        info = (C.c_double * 4)()
+        N.check(N.lib().plora_debug_plan_hybrid(plan.handle, info))
+        if info[0] > 0:
+            line["roofline"]["kernels"] = (
+                f"the launch pair of plora_bgmv_layers: bgmv_cluster_kernel ({int(info[2])} 4-CTA "
+                f"clusters, {1 - info[1]:.3f} of the weight rows) and, concurrently on the "
+                f"{int(info[0])} SMs the clusters leave idle, bgmv_stream_kernel ({int(info[3])} CTAs, "
+                f"{info[1]:.3f}); achieved = the step's algorithmic bytes / the pair's time")
     if per_layer_ms is not None:
         lb = per_call / mlp  # one layer's bytes
         line["per_layer_launch"] = {

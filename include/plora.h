@@ -573,6 +573,8 @@ int plora_debug_set_stream_ctas(uint32_t ctas);
  * plan's split: {spare SMs, share fraction, clusters, streaming CTAs}. */
 int plora_debug_set_hybrid_share(double factor);
 int plora_debug_plan_hybrid(const plora_plan* plan, double out[4]);
+/* Diagnostics: also run plora_bgmv_layer (one layer) as the hybrid pair. */
+int plora_debug_set_hybrid_per_layer(int on);
 /* Launch geometry the plan chose for the bf16 decode op of projection
  * `proj`: out[0..7] = {cluster size, input slice, output slice, A-row ring
  * slots, Bᵀ-row ring slots, dynamic smem bytes, clusters, chunks}. */

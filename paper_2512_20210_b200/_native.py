@@ -268,6 +268,7 @@ _SIGS = {
     "plora_debug_set_stream_ctas": (_int, [_u32]),
     "plora_debug_set_hybrid_share": (_int, [C.c_double]),
     "plora_debug_plan_hybrid": (_int, [_vp, _P(C.c_double)]),
+    "plora_debug_set_hybrid_per_layer": (_int, [C.c_int]),
     "plora_debug_plan_geom": (_int, [_vp, _u32, _P(_u32)]),
     "plora_debug_set_sgmv_flags": (_int, [_u32]),
 }

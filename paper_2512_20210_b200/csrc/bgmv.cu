@@ -408,6 +408,7 @@ void check_io(const plora_plan* plan, uint32_t layer, uint32_t proj, const void*
 }  // namespace plora
 
 namespace {
+int g_hybrid_per_layer = 0;  // plora_debug_set_hybrid_per_layer
 // bf16 decode kernel: 0 clusters (bgmv_cluster.cu), and for multi-layer
 // launches the hybrid with a streaming share on the idle SMs; 1 the streaming
 // kernel alone (bgmv_stream.cu); 2 clusters only
@@ -419,6 +420,34 @@ bool hybrid_enabled() { return g_bgmv_impl == 0; }
 double g_hybrid_factor = 0.95;
 double hybrid_share_factor() { return g_hybrid_factor; }
 }  // namespace plora
+
+namespace plora {
+// The hybrid decode launch: the streaming share forks onto the plan's aux
+// stream, the clusters run on `stream`, and `stream` joins the aux stream
+// (the two shares touch disjoint adapters and y rows).
+void launch_hybrid(plora_plan* plan, uint32_t layer0, uint32_t n_layers, const void* x,
+                   uint64_t x_stride, uint64_t x_lstride, void* const* ys, const uint64_t* y_strides,
+                   const uint64_t* y_lstrides, float scale, cudaStream_t s) {
+  if (!plan->aux_stream) {
+    PLORA_CUDA(cudaStreamCreateWithFlags(&plan->aux_stream, cudaStreamNonBlocking));
+    PLORA_CUDA(cudaEventCreateWithFlags(&plan->ev_fork, cudaEventDisableTiming));
+    PLORA_CUDA(cudaEventCreateWithFlags(&plan->ev_join, cudaEventDisableTiming));
+  }
+  PLORA_CUDA(cudaEventRecord(plan->ev_fork, s));
+  PLORA_CUDA(cudaStreamWaitEvent(plan->aux_stream, plan->ev_fork, 0));
+  launch_bgmv_cluster_layers(*plan, layer0, n_layers, x, x_stride, x_lstride, ys, y_strides, y_lstrides,
+                             scale, s, &plan->cwork_hyb);
+  launch_bgmv_stream(*plan, plan->swork_hyb, layer0, n_layers, x, x_stride, x_lstride, ys, y_strides,
+                     y_lstrides, scale, plan->aux_stream);
+  PLORA_CUDA(cudaEventRecord(plan->ev_join, plan->aux_stream));
+  PLORA_CUDA(cudaStreamWaitEvent(s, plan->ev_join, 0));
+}
+}  // namespace plora
+
+extern "C" int plora_debug_set_hybrid_per_layer(int on) {
+  g_hybrid_per_layer = on;
+  return 0;
+}
 
 extern "C" int plora_debug_set_hybrid_share(double factor) {
   plora::g_hybrid_factor = factor;  // plans built afterwards
@@ -519,24 +548,9 @@ extern "C" int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_l
     }
     if (g.esize == 2 && g_bgmv_impl == 0 && plan->hyb_spare && plan->n_layer_proj == g.m.n_proj &&
         n_layers * g.m.n_proj <= 256) {
-      // hybrid: the streaming share forks onto the plan's aux stream, the
-      // clusters run on `stream`, and `stream` joins the aux stream (the two
-      // shares touch disjoint adapters and y rows)
       DeviceCtx ctx(st.device);
-      cudaStream_t s = static_cast<cudaStream_t>(stream);
-      if (!plan->aux_stream) {
-        PLORA_CUDA(cudaStreamCreateWithFlags(&plan->aux_stream, cudaStreamNonBlocking));
-        PLORA_CUDA(cudaEventCreateWithFlags(&plan->ev_fork, cudaEventDisableTiming));
-        PLORA_CUDA(cudaEventCreateWithFlags(&plan->ev_join, cudaEventDisableTiming));
-      }
-      PLORA_CUDA(cudaEventRecord(plan->ev_fork, s));
-      PLORA_CUDA(cudaStreamWaitEvent(plan->aux_stream, plan->ev_fork, 0));
-      launch_bgmv_cluster_layers(*plan, layer0, n_layers, x, x_stride, x_layer_stride, ys, y_strides,
-                                 y_layer_strides, scale, s, &plan->cwork_hyb);
-      launch_bgmv_stream(*plan, plan->swork_hyb, layer0, n_layers, x, x_stride, x_layer_stride, ys,
-                         y_strides, y_layer_strides, scale, plan->aux_stream);
-      PLORA_CUDA(cudaEventRecord(plan->ev_join, plan->aux_stream));
-      PLORA_CUDA(cudaStreamWaitEvent(s, plan->ev_join, 0));
+      launch_hybrid(plan, layer0, n_layers, x, x_stride, x_layer_stride, ys, y_strides, y_layer_strides,
+                    scale, static_cast<cudaStream_t>(stream));
       return 0;
     }
     const bool one = g.esize == 2 && plan->n_layer_proj == g.m.n_proj &&
@@ -577,6 +591,14 @@ extern "C" int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x,
       const uint64_t zero[PLORA_MAX_PROJ] = {};
       launch_bgmv_stream(*plan, plan->swork_layer, layer, 1, x, x_stride, 0, ys, y_strides, zero,
                          scale, static_cast<cudaStream_t>(stream));
+      return 0;
+    }
+    if (g.esize == 2 && g_bgmv_impl == 0 && g_hybrid_per_layer && plan->hyb_spare &&
+        plan->n_layer_proj == g.m.n_proj) {
+      DeviceCtx ctx(st.device);
+      const uint64_t zero[PLORA_MAX_PROJ] = {};
+      launch_hybrid(plan, layer, 1, x, x_stride, 0, ys, y_strides, zero, scale,
+                    static_cast<cudaStream_t>(stream));
       return 0;
     }
     if (g.esize == 2 && plan->n_layer_proj == g.m.n_proj) {
