@@ -783,6 +783,7 @@ def run_cfg5(args):
     # per-rank algorithmic bytes of one (layer, proj) call: its A rows, its Bᵀ
     # columns, x, its y shard RMW
     split = None
+    rank0 = {}
     if world == 1:  # the per-rank halves themselves (shrink, copy, expand) at TP = 1
         tps = TensorParallelLoRA(plan, 0, 1, force_split=True)
 
@@ -806,6 +807,45 @@ def run_cfg5(args):
         s1.record(stream)
         torch.cuda.synchronize()
         split = s0.elapsed_time(s1) / K
+        # one rank's halves at TP = 2, 4, 8 (the collective excluded: rank 0
+        # expands from a gathered buffer filled once by every rank's shrink)
+        from paper_2512_20210_b200.tp import bgmv_tp_expand, bgmv_tp_shrink, tp_shard_rows
+        rank0 = {}
+        for n in (2, 4, 8):
+            rs = tp_shard_rows(plan, n)
+            vg = torch.zeros(NP, n, T, rs, dtype=torch.float32, device=dev)
+            ysh = [torch.randn(L, T, shape.d_out[p] // n, device=dev).to(torch.bfloat16) for p in range(NP)]
+            for p in range(NP):
+                for i in range(n):
+                    bgmv_tp_shrink(plan, 0, p, i, n, x[0], vg[p, i])
+
+            def step_rank0(n=n, vg=vg, ysh=ysh):
+                for l in range(L):
+                    for p in range(NP):
+                        bgmv_tp_shrink(plan, l, p, 0, n, x[l], vg[p, 0])
+                        bgmv_tp_expand(plan, l, p, 0, n, vg[p], ysh[p][l])
+
+            for _ in range(3):
+                step_rank0()
+            torch.cuda.synchronize()
+            g3 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g3):
+                step_rank0()
+            g3.replay()
+            torch.cuda.synchronize()
+            s0.record(stream)
+            for _ in range(K):
+                g3.replay()
+            s1.record(stream)
+            torch.cuda.synchronize()
+            t_ms = s0.elapsed_time(s1) / K
+            b_call = statistics.mean(
+                sum((r // n) * shape.d_in[p] + r * (shape.d_out[p] // n) for r in cfg.ranks) * 2
+                + T * shape.d_in[p] * 2 + 2 * T * (shape.d_out[p] // n) * 2 for p in range(NP))
+            rank0[f"tp{n}"] = {"us_per_call": t_ms * 1e3 / (L * NP),
+                               "alg_bytes_per_call": b_call,
+                               "hbm_frac": b_call / (t_ms / (L * NP) / 1e3) / 1e9 / load_peaks()[0]}
+            del vg, ysh, g3
     per_call = statistics.mean(
         sum((r // world) * shape.d_in[p] + r * (shape.d_out[p] // world) for r in cfg.ranks) * 2
         + T * shape.d_in[p] * 2 + 2 * T * (shape.d_out[p] // world) * 2 for p in range(NP))
@@ -832,8 +872,12 @@ def run_cfg5(args):
         "tp_halves_at_tp1": None if split is None else {
             "ms_per_step": split, "us_per_call": split * 1e3 / (L * NP),
             "hbm_frac": per_call / (split / (L * NP) / 1e3) / 1e9 / peak,
-            "note": "tp_shrink + v copy + tp_expand forced at TP=1 (the per-rank kernels of the "
-                    "N>1 path; value above uses the fused data-parallel op at TP=1)"},
+            "note": "tp_shrink + tp_expand forced at TP=1 (the per-rank kernels of the N>1 path; "
+                    "value above uses the fused data-parallel op at TP=1)"},
+        "tp_rank0_halves": None if split is None else {
+            **rank0,
+            "note": "rank 0's shrink + expand per (layer, proj) call at TP = N on one GPU, the "
+                    "all-gather excluded (its v_gathered filled once by every rank's shrink)"},
         "clocks": clk.summary(),
     }
     print(json.dumps(line))

@@ -565,6 +565,10 @@ int plora_debug_set_bgmv_impl(int impl);
 /* Diagnostics for the streaming kernel: 1 consumers skip the math, 2 no
  * weight copies (results are then wrong; timing ablation only). */
 int plora_debug_set_bgmv_flags(uint32_t flags);
+/* Diagnostics: L2 bulk prefetch of the streaming decode kernel's weight rows
+ * two items ahead of its shared-memory ring (1) or off (0, the default:
+ * measured slower, profiles/r02i_stream_prefetch_ablation.txt). */
+int plora_debug_set_stream_prefetch(uint32_t on);
 /* Diagnostics: plans built afterwards give the streaming kernel at most
  * `ctas` CTAs (0 = one per SM). */
 int plora_debug_set_stream_ctas(uint32_t ctas);

@@ -265,6 +265,7 @@ _SIGS = {
     "plora_debug_set_trace": (_int, [_vp, _u64]),
     "plora_debug_set_bgmv_impl": (_int, [C.c_int]),
     "plora_debug_set_bgmv_flags": (_int, [_u32]),
+    "plora_debug_set_stream_prefetch": (_int, [_u32]),
     "plora_debug_set_stream_ctas": (_int, [_u32]),
     "plora_debug_set_hybrid_share": (_int, [C.c_double]),
     "plora_debug_plan_hybrid": (_int, [_vp, _P(C.c_double)]),

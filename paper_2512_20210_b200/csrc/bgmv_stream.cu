@@ -58,6 +58,7 @@ template <uint32_t JT>
 constexpr uint32_t kPubBufs = JT == 4 ? 4 : 2;  // S-item partial buffers between the consumers and the publisher
 constexpr uint32_t kLook = 4;             // producer lookahead (items)
 constexpr uint32_t kRecRing = 2 * kLook;  // item records in flight
+constexpr uint32_t kPf = 2;               // L2 prefetch distance (items; <= kLook - 1)
 constexpr uint32_t kSmemBudget = 227 * 1024;
 constexpr uint32_t kStop = 0xffffffffu;
 constexpr uint32_t kHdrWords = 16;
@@ -85,6 +86,14 @@ struct SArgs {
   float scale;
   uint64_t* trace;  // diagnostics (plora_debug_set_trace): [cta][stage][4] SM clocks, or nullptr
   uint32_t dbg;     // diagnostics (plora_debug_set_bgmv_flags): 1 consumers skip the math, 2 no weight copies
+  uint32_t pf;      // L2 prefetch of the weight rows kPf items ahead (fast path)
+  // tensor-parallel halves (tp.cu; 0: the data-parallel op).  1 = shrink: S
+  // items only, v stored as fp32 tp_v[tok][v_off + row] (the v_part layout);
+  // 2 = expand: E items only, v read from the all-gathered tp_vg[N][T][rs_max]
+  // (row j of a rank-r adapter lives in rank block j / (r/N)).  No counters.
+  uint32_t tp, tp_size, tp_T, tp_rsmax;
+  float* tp_v;
+  const float* tp_vg;
 };
 
 constexpr uint32_t kTraceStages = 512;
@@ -221,9 +230,28 @@ __device__ void producer(const SArgs& p, char* smem, uint32_t pw) {
   }
   ptx::pdl_wait();  // activations, v planes and counters belong to the previous call until here
   uint32_t ph = 0, g = 0;  // parity of this warp's slot; global stage number
+  // L2 prefetch of this warp's stages kPf items ahead: DRAM -> L2 runs that
+  // far ahead of the shared-memory ring, whose depth the smem budget caps
+  auto prefetch_item = [&](uint32_t vp, uint32_t gp) {
+    const Item ip(recring + (vp % kRecRing) * 16, p, vp / nc);
+    const uint32_t* entp = entring + (vp % kLook) * kEntPW;
+    const uint32_t nstp = ip.stages(p);
+    for (uint32_t st = (pw + kPW - gp % kPW) % kPW, j = 0; st < nstp; st += kPW, ++j) {
+      if (lane < stage_rows(ip, st)) {
+        uint64_t lo;
+        uint32_t len;
+        row_seg(p, ip, st, lane, lo, len);
+        ptx::bulk_prefetch_l2(p.arena + (static_cast<uint64_t>(entp[j * kWRows + lane]) << L) + (lo & pmask), len);
+      }
+    }
+  };
+  uint32_t g_pf = 0;  // first global stage of item v + kPf
+  if (p.fast && p.pf) {
+    for (uint32_t v = 0; v < kPf && v < nv; ++v) g_pf += Item(recring + (v % kRecRing) * 16, p, v / nc).stages(p);
+  }
 #pragma unroll 1
   for (uint32_t v = 0; v < nv; ++v) {
-    cp_async_wait_group<kLook - 1>();  // entries of v, record of v + kLook
+    cp_async_wait_group<kLook - 1 - kPf>();  // entries of v + kPf, record of v + kLook
     __syncwarp();
     const uint32_t* rw = recring + (v % kRecRing) * 16;
     const Item it(rw, p, v / nc);
@@ -231,7 +259,11 @@ __device__ void producer(const SArgs& p, char* smem, uint32_t pw) {
     const uint32_t nst = it.stages(p);
     const uint32_t plane = it.plane(p);
     const uint32_t st0 = (pw + kPW - g % kPW) % kPW;  // this warp's first stage of the item
-    if (it.expand && st0 < nst) {  // v of the job must be complete
+    if (p.fast && p.pf && v + kPf < nv) {
+      prefetch_item(v + kPf, g_pf);
+      g_pf += Item(recring + ((v + kPf) % kRecRing) * 16, p, (v + kPf) / nc).stages(p);
+    }
+    if (it.expand && st0 < nst && p.tp == 0) {  // v of the job must be complete
       if (lane == 0) {
         const uint64_t tw = clock64();
         const uint32_t* c = p.cnt + static_cast<uint64_t>(plane) * 2 * p.njobs + it.job;
@@ -289,11 +321,35 @@ __device__ void producer(const SArgs& p, char* smem, uint32_t pw) {
                         kb, &full[pw]);
         bytes += it.ntok * kb;
       } else {
-        if (lane == 24)
-          ptx::bulk_g2s(sb + Slot<JT>::vrows,
-                        p.v + static_cast<uint64_t>(plane) * p.vplane + it.v_off + st * kWRows * JT,
-                        kWRows * JT * 4, &full[pw]);  // the job's v block is padded to 16 rows
-        bytes += kWRows * JT * 4;
+        if (p.tp == 2) {
+          // v rows st·16 .. st·16 + 15 of the job from the gathered shards,
+          // split into the fragment words the consumers read (as the
+          // publisher stores them): word ((row pair)·JT + tok)·2 + {hi, lo}
+          uint32_t* vw = reinterpret_cast<uint32_t*>(sb + Slot<JT>::vrows);
+          const uint32_t rs = it.rank / p.tp_size;
+          for (uint32_t e = lane; e < kWRows * JT; e += 32) {
+            const uint32_t rp = e / (2 * JT), t = (e / 2) % JT, part = e & 1u;
+            float v2[2];
+#pragma unroll
+            for (uint32_t q = 0; q < 2; ++q) {
+              const uint32_t j = st * kWRows + 2 * rp + q;
+              v2[q] = (j < it.rank && t < it.ntok)
+                          ? __ldg(p.tp_vg + (static_cast<uint64_t>(j / rs) * p.tp_T + rw[8 + t]) * p.tp_rsmax + j % rs)
+                          : 0.f;
+            }
+            const __nv_bfloat16 h0 = __float2bfloat16_rn(v2[0]), h1 = __float2bfloat16_rn(v2[1]);
+            vw[e] = part ? pack_bf16x2(v2[0] - __bfloat162float(h0), v2[1] - __bfloat162float(h1))
+                         : (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16) | __bfloat16_as_ushort(h0);
+          }
+          __threadfence_block();  // ordered before lane 0's arrival on the slot's full barrier
+          __syncwarp();
+        } else {
+          if (lane == 24)
+            ptx::bulk_g2s(sb + Slot<JT>::vrows,
+                          p.v + static_cast<uint64_t>(plane) * p.vplane + it.v_off + st * kWRows * JT,
+                          kWRows * JT * 4, &full[pw]);  // the job's v block is padded to 16 rows
+          bytes += kWRows * JT * 4;
+        }
         if (last) {
           if (lane >= 16 && lane - 16 < it.ntok)
             ptx::bulk_g2s(sb + Slot<JT>::aux + (lane - 16) * kRowB,
@@ -436,12 +492,14 @@ __device__ void consumers(const SArgs& p, char* smem) {
           pw[(gq + 8) * JT + 2 * cc + 1] = sd[0][3] + sd[1][3];
         }
         if (w == 0 && lane == 0) {  // the item's coordinates
-          uint32_t* meta = reinterpret_cast<uint32_t*>(part + kPubBufs<JT> * kCWarps * kWRows * JT) + pbuf * 8;
+          uint32_t* meta = reinterpret_cast<uint32_t*>(part + kPubBufs<JT> * kCWarps * kWRows * JT) + pbuf * 16;
           meta[0] = plane;
-          meta[1] = v_off + off * JT;
+          meta[1] = p.tp ? v_off : v_off + off * JT;  // TP: the item's first shard row
           meta[2] = rows;
           meta[3] = ntok;
           meta[4] = job;
+#pragma unroll
+          for (uint32_t t = 0; t < 8; ++t) meta[8 + t] = hdr[s * kHdrWords + 8 + t];
         }
         ptx::mbar_arrive(&pready[pbuf]);  // every consumer thread: its own writes precede it
         ++s_items;
@@ -531,7 +589,7 @@ __device__ void consumers(const SArgs& p, char* smem) {
     ptx::mbar_arrive(&empty[s]);  // every consumer thread releases its own reads of the slot
     if (lane == 0) {
       if (w == 0) tput(p, gs, 2, clock64());
-      if (w == 0 && expand && last) {  // the job's last E item resets its counters for the next call
+      if (w == 0 && expand && last && p.tp == 0) {  // the job's last E item resets its counters for the next call
         uint32_t* c = p.cnt + static_cast<uint64_t>(plane) * 2 * p.njobs;
         const uint32_t ne = li_n & 0xffffu;
         if (atomicAdd(c + p.njobs + job, 1u) + 1 == ne) {
@@ -572,9 +630,21 @@ __device__ void publisher(const SArgs& p, char* smem) {
       }
     }
     if (done) return;
-    const uint32_t* meta = metas + pbuf * 8;
+    const uint32_t* meta = metas + pbuf * 16;
     const uint32_t plane = meta[0], vbase = meta[1], rows = meta[2], ntok = meta[3], job = meta[4];
     const float* pb = part + pbuf * kCWarps * kWRows * JT;
+    if (p.tp == 1) {  // tensor-parallel shrink: v_part[tok][shard row] in fp32
+      for (uint32_t e = lane; e < kWRows * JT; e += 32) {
+        const uint32_t r = e / JT, t = e % JT;
+        float vv = 0.f;
+#pragma unroll
+        for (uint32_t ww = 0; ww < kCWarps; ++ww) vv += pb[ww * kWRows * JT + e];
+        if (t < ntok && r < rows) p.tp_v[static_cast<uint64_t>(meta[8 + t]) * p.tp_rsmax + vbase + r] = vv;
+      }
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&pfree[pbuf]);
+      continue;
+    }
     // v is stored as the expand's B fragments want it: per row pair, token and
     // part (bf16 hi / lo of the fp32 value), a 32-bit word holding rows 2i, 2i+1
     __nv_bfloat16* vg = reinterpret_cast<__nv_bfloat16*>(p.v + static_cast<uint64_t>(plane) * p.vplane + vbase);
@@ -627,6 +697,7 @@ __global__ void __launch_bounds__(Slot<JT>::threads, 1) bgmv_stream_kernel(const
 }
 
 uint32_t g_stream_dbg = 0;
+uint32_t g_stream_pf = 0;  // plora_debug_set_stream_prefetch (measured slower: off)
 uint32_t g_stream_ctas = 0;  // plora_debug_set_stream_ctas
 
 struct Geom {
@@ -638,7 +709,7 @@ Geom geom() {
   Geom g{};
   g.slot_bytes = Slot<JT>::bytes;
   const uint32_t ring = Slot<JT>::n * (kRecRing * 16 + kLook * kEntPW) * 4;
-  const uint32_t part = kPubBufs<JT> * (kCWarps * JT * kWRows + 8) * 4;
+  const uint32_t part = kPubBufs<JT> * (kCWarps * JT * kWRows + 16) * 4;
   const uint32_t per_slot = g.slot_bytes + kHdrWords * 4 + 16;
   const uint32_t fixed = ring + part + kHdrWords * 4 + 4 * kPubBufs<JT> * 8 + 256;
   g.nslots = Slot<JT>::n;
@@ -655,7 +726,7 @@ template <uint32_t JT>
 void launch_jt(const plora_plan& plan, const StreamWork& w, uint32_t layer0, uint32_t n_layers,
                const void* x, uint64_t x_stride, uint64_t x_lstride, void* const* ys,
                const uint64_t* y_strides, const uint64_t* y_lstrides, float scale,
-               cudaStream_t stream) {
+               cudaStream_t stream, const StreamTp* tp = nullptr) {
   const plora_store& st = *plan.store;
   const ModelGeom& gm = st.geom;
   const Geom g = geom<JT>();
@@ -668,8 +739,16 @@ void launch_jt(const plora_plan& plan, const StreamWork& w, uint32_t layer0, uin
   SArgs a{};
   a.arena = st.arena;
   a.table = st.d_table;
-  a.items = plan.d_stitems + w.items_off;
-  a.cta_off = plan.d_stcta + w.cta_off;
+  a.items = (tp ? tp->items : plan.d_stitems) + w.items_off;
+  a.cta_off = (tp ? tp->cta_off : plan.d_stcta) + w.cta_off;
+  if (tp) {
+    a.tp = tp->mode;
+    a.tp_size = tp->tp_size;
+    a.tp_T = tp->n_tokens;
+    a.tp_rsmax = tp->rs_max;
+    a.tp_v = tp->v_out;
+    a.tp_vg = tp->v_in;
+  }
   a.x = static_cast<const char*>(x);
   a.x_stride_b = x_stride * 2;
   a.x_lstride_b = x_lstride * 2;
@@ -706,6 +785,7 @@ void launch_jt(const plora_plan& plan, const StreamWork& w, uint32_t layer0, uin
   a.scale = scale;
   a.trace = trace_buffer(static_cast<uint64_t>(w.ctas) * kTraceStages * 96);
   a.dbg = g_stream_dbg;
+  a.pf = g_stream_pf;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(w.ctas);
   cfg.blockDim = dim3(Slot<JT>::threads);
@@ -733,6 +813,20 @@ void launch_bgmv_stream(const plora_plan& plan, const StreamWork& w, uint32_t la
     launch_jt<8>(plan, w, layer0, n_layers, x, x_stride, x_lstride, ys, y_strides, y_lstrides, scale, stream);
   else
     launch_jt<4>(plan, w, layer0, n_layers, x, x_stride, x_lstride, ys, y_strides, y_lstrides, scale, stream);
+}
+
+void launch_bgmv_stream_tp(const plora_plan& plan, const StreamWork& w, const StreamTp& tp,
+                           uint32_t layer, const void* x, uint64_t x_stride, void* y,
+                           uint64_t y_stride, float scale, cudaStream_t stream) {
+  if (w.ctas == 0) return;
+  void* ys[1] = {y};
+  const uint64_t yst[1] = {y_stride};
+  launch_jt<4>(plan, w, layer, 1, x, x_stride, 0, ys, yst, nullptr, scale, stream, &tp);
+}
+
+extern "C" int plora_debug_set_stream_prefetch(uint32_t on) {
+  g_stream_pf = on;
+  return 0;
 }
 
 extern "C" int plora_debug_set_bgmv_flags(uint32_t flags) {

@@ -18,7 +18,18 @@ struct Seg {
 
 }  // namespace
 
+void plora_plan::drop_tp() {
+  if (tpw.empty()) return;
+  DeviceCtx ctx(store->device);
+  for (auto& kv : tpw) {
+    cudaFree(kv.second.d_items);  // implicit device synchronisation: no TP launch still reads it
+    cudaFreeHost(kv.second.h_stage);
+  }
+  tpw.clear();
+}
+
 void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream) {
+  drop_tp();  // TP item lists follow the batch
   const plora_store& st = *store;
   const ModelGeom& g = st.geom;
   const uint32_t es = g.esize, vec = 16 / es;
@@ -700,6 +711,7 @@ void plora_plan_destroy(plora_plan* plan) {
     cudaEventDestroy(plan->upload_done);
   }
   cudaDeviceSynchronize();
+  plan->drop_tp();
   cudaFreeHost(plan->h_pinned);
   cudaFree(plan->d_buf);
   cudaFree(plan->d_v);

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <vector>
 
 #include "store.hpp"
@@ -160,6 +161,15 @@ struct StreamItem {  // 64 bytes, fully resolved on the host
 };
 static_assert(sizeof(StreamItem) == 64, "StreamItem layout");
 
+struct StreamTp {  // a tensor-parallel half on the streaming kernel (tp.cu)
+  uint32_t mode;      // 1 shrink (S items; v -> v_out), 2 expand (E items; v from v_in)
+  uint32_t tp_size, n_tokens, rs_max;
+  float* v_out;
+  const float* v_in;
+  const StreamItem* items;
+  const uint32_t* cta_off;
+};
+
 struct StreamWork {  // one launch variant (a projection, or every projection of a layer)
   uint32_t items_off = 0;  // into the item array
   uint32_t cta_off = 0;    // into the CTA offset array (ctas + 1 entries)
@@ -276,6 +286,16 @@ struct plora_plan {
   cudaStream_t aux_stream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t upload_done = nullptr;
+  // tensor-parallel halves (tp.cu): streaming-kernel item lists per
+  // (tp_rank, tp_size, proj, half), built on first use, dropped on rebuild
+  struct TpWork {
+    plora::StreamWork w;
+    plora::StreamItem* d_items = nullptr;  // items, then the CTA offsets
+    uint32_t* d_cta = nullptr;
+    char* h_stage = nullptr;               // pinned source of the upload
+  };
+  std::map<uint64_t, TpWork> tpw;
+  void drop_tp();
 
   void build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream);
 };
@@ -291,6 +311,11 @@ void launch_bgmv_cluster(const plora_plan& plan, uint32_t layer, uint32_t proj, 
 // Streaming bf16 BGMV (bgmv_stream.cu): the projections `w` was built for,
 // layers [layer0, layer0 + n_layers); layer layer0 + i reads x + i·x_lstride
 // and updates ys[j] + i·y_lstrides[j] (elements).
+// One tensor-parallel half (single projection `w.projs[0]`, one layer); y is
+// pre-shifted by the caller so that column c of the output is y + c.
+void launch_bgmv_stream_tp(const plora_plan& plan, const StreamWork& w, const StreamTp& tp,
+                           uint32_t layer, const void* x, uint64_t x_stride, void* y,
+                           uint64_t y_stride, float scale, cudaStream_t stream);
 void launch_bgmv_stream(const plora_plan& plan, const StreamWork& w, uint32_t layer0,
                         uint32_t n_layers, const void* x, uint64_t x_stride, uint64_t x_lstride,
                         void* const* ys, const uint64_t* y_strides, const uint64_t* y_lstrides,

@@ -17,166 +17,143 @@
 // the HBM traffic per GPU is 1/N of the adapter.  Math: PAPER.md:64-69; the
 // reference has no multi-GPU path.
 //
-// Both kernels are plain streaming kernels (HBM-bound, ~1.8 flop/B): the
-// work per rank at 70B shapes is small and the all-gather message is T·r/N
-// fp32 per rank (4-32 KiB in total), so the call is latency-bound.
+// Both halves run on the streaming decode kernel (bgmv_stream.cu): one
+// persistent CTA per SM, weight rows moved page by page with 1-D TMA bulk
+// copies into a multi-slot shared-memory ring, mma.sync consumers.
+//   shrink  = its S items restricted to the shard rows (<= 16 rows, full K
+//             each); the publisher warp stores v_part in fp32.
+//   expand  = its E items restricted to the column shard (<= 1024 columns,
+//             cut at 1024-column boundaries so every row piece stays in one
+//             page); the producer builds the bf16 hi / lo fragments of v from
+//             v_gathered while the slot's weight rows are in flight.
+// No counters: v is complete before either launch.  The item lists depend
+// on (batch, proj, tp_rank, tp_size) only; they are built and uploaded on a
+// plan's first call for that key (outside stream capture) and reused by
+// every layer.
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstddef>
+#include <cstring>
+#include <numeric>
+#include <queue>
 
 #include "plan.hpp"
 
 using namespace plora;
 
-namespace plora {
-void check_io(const plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
-              uint64_t x_stride, void* y, uint64_t y_stride);
-}
-
 namespace {
 
-struct TpArgs {
-  const char* arena;
-  const uint32_t* table;
-  const ClusterJob* jobs;
-  const char* x;       // shrink: [T, d_in]
-  uint64_t x_stride_b;
-  float* v;            // shrink: v_part [T, rs_max]; expand: v_gathered [N][T][rs_max]
-  char* y;             // expand: [T, d_out / N] (this rank's column shard)
-  uint64_t y_stride_b;
-  uint64_t blk_mult;
-  uint32_t log2_page;
-  uint32_t d_in, d_out;
-  uint32_t tp_rank, tp_size;
-  uint32_t rs_max;     // row stride of v_part (floats)
-  uint32_t n_tokens;
-  uint32_t col0, ncols;
-  float scale;
+struct TpGeom {
+  uint32_t d_in, d_out, rs_max, ncols, col0;
 };
 
-__device__ __forceinline__ const char* paged(const TpArgs& p, uint32_t table_off, uint64_t off) {
-  const uint32_t phys = __ldg(p.table + table_off + static_cast<uint32_t>(off >> p.log2_page));
-  return p.arena + (static_cast<uint64_t>(phys) << p.log2_page) + (off & ((1ull << p.log2_page) - 1));
-}
-
-__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
-
-// One warp per (job, shard row): lanes stride the row in 16-byte vectors
-// (each vector inside one page: pages are >= 16 B and 16-byte aligned).
-__global__ void __launch_bounds__(128) tp_shrink_kernel(const TpArgs p) {
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const ClusterJob job = p.jobs[blockIdx.x];
-  const uint32_t rs = job.rank / p.tp_size;
-  const uint32_t j = blockIdx.y * 4 + warp;
-  if (j >= rs) return;
-  const uint32_t row = p.tp_rank * rs + j;
-  const uint64_t base = (static_cast<uint64_t>(job.rank) * p.blk_mult + static_cast<uint64_t>(row) * p.d_in) * 2;
-  float acc[kJobTok] = {0.f, 0.f, 0.f, 0.f};
-  // unrolled so several (page-table lookup -> load) chains are in flight
-#pragma unroll 8
-  for (uint32_t v8 = lane; v8 < p.d_in / 8; v8 += 32) {
-    const uint4 a = __ldg(reinterpret_cast<const uint4*>(paged(p, job.table_off, base + v8 * 16ull)));
-#pragma unroll
-    for (uint32_t t = 0; t < kJobTok; ++t) {
-      if (t < job.ntok) {
-        const uint4 xv = __ldg(reinterpret_cast<const uint4*>(p.x + job.tok[t] * p.x_stride_b + v8 * 16ull));
-        acc[t] = fmaf(bf_lo(a.x), bf_lo(xv.x), acc[t]);
-        acc[t] = fmaf(bf_hi(a.x), bf_hi(xv.x), acc[t]);
-        acc[t] = fmaf(bf_lo(a.y), bf_lo(xv.y), acc[t]);
-        acc[t] = fmaf(bf_hi(a.y), bf_hi(xv.y), acc[t]);
-        acc[t] = fmaf(bf_lo(a.z), bf_lo(xv.z), acc[t]);
-        acc[t] = fmaf(bf_hi(a.z), bf_hi(xv.z), acc[t]);
-        acc[t] = fmaf(bf_lo(a.w), bf_lo(xv.w), acc[t]);
-        acc[t] = fmaf(bf_hi(a.w), bf_hi(xv.w), acc[t]);
-      }
-    }
-  }
-#pragma unroll
-  for (uint32_t t = 0; t < kJobTok; ++t) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
-    if (lane == 0 && t < job.ntok) p.v[static_cast<uint64_t>(job.tok[t]) * p.rs_max + j] = acc[t];
-  }
-}
-
-// One CTA per (job, 256-column block of the shard): thread = 4 columns; v of
-// the job's tokens staged in shared memory from the gathered buffer.
-constexpr uint32_t kExpCols = 256;
-constexpr uint32_t kMaxTpRank = 256;
-
-__global__ void __launch_bounds__(64) tp_expand_kernel(const TpArgs p) {
-  __shared__ float vs[kJobTok][kMaxTpRank];
-  const ClusterJob job = p.jobs[blockIdx.x];
-  const uint32_t r = job.rank, rs = r / p.tp_size;
-  for (uint32_t i = threadIdx.x; i < kJobTok * r; i += blockDim.x) {
-    const uint32_t t = i / r, jj = i - t * r;
-    vs[t][jj] = t < job.ntok ? p.v[(static_cast<uint64_t>(jj / rs) * p.n_tokens + job.tok[t]) * p.rs_max + jj % rs]
-                             : 0.f;
-  }
-  __syncthreads();
-  const uint32_t c = blockIdx.y * kExpCols + threadIdx.x * 4;  // column within the shard
-  if (c >= p.ncols) return;
-  const uint64_t bt = (static_cast<uint64_t>(r) * p.blk_mult + static_cast<uint64_t>(r) * p.d_in) * 2;
-  float acc[kJobTok][4] = {};
-#pragma unroll 8
-  for (uint32_t jj = 0; jj < r; ++jj) {
-    const uint64_t off = bt + (static_cast<uint64_t>(jj) * p.d_out + p.col0 + c) * 2;
-    const uint2 b = __ldg(reinterpret_cast<const uint2*>(paged(p, job.table_off, off)));
-    const float b0 = bf_lo(b.x), b1 = bf_hi(b.x), b2 = bf_lo(b.y), b3 = bf_hi(b.y);
-#pragma unroll
-    for (uint32_t t = 0; t < kJobTok; ++t) {
-      const float v = vs[t][jj];
-      acc[t][0] = fmaf(v, b0, acc[t][0]);
-      acc[t][1] = fmaf(v, b1, acc[t][1]);
-      acc[t][2] = fmaf(v, b2, acc[t][2]);
-      acc[t][3] = fmaf(v, b3, acc[t][3]);
-    }
-  }
-#pragma unroll
-  for (uint32_t t = 0; t < kJobTok; ++t) {
-    if (t >= job.ntok) continue;
-    uint2* yp = reinterpret_cast<uint2*>(p.y + job.tok[t] * p.y_stride_b + c * 2ull);
-    uint2 yo = *yp;
-    __nv_bfloat162 lo = __floats2bfloat162_rn(fmaf(p.scale, acc[t][0], bf_lo(yo.x)),
-                                              fmaf(p.scale, acc[t][1], bf_hi(yo.x)));
-    __nv_bfloat162 hi = __floats2bfloat162_rn(fmaf(p.scale, acc[t][2], bf_lo(yo.y)),
-                                              fmaf(p.scale, acc[t][3], bf_hi(yo.y)));
-    yo.x = *reinterpret_cast<uint32_t*>(&lo);
-    yo.y = *reinterpret_cast<uint32_t*>(&hi);
-    *yp = yo;
-  }
-}
-
-TpArgs tp_args(const plora_plan& plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
-               uint32_t tp_size) {
+TpGeom tp_check(const plora_plan& plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
+                uint32_t tp_size) {
   const plora_store& st = *plan.store;
   const ModelGeom& g = st.geom;
   if (g.esize != 2) throw ValidationError("tensor-parallel LoRA needs a bf16 store");
   if (layer >= g.m.n_layers || proj >= g.m.n_proj) throw ValidationError("layer / proj out of range");
   if (tp_size == 0 || tp_rank >= tp_size) throw ValidationError("tp_rank must be < tp_size");
   const uint32_t din = g.m.d_in[proj], dout = g.m.d_out[proj];
-  if (din % 8 || dout % (4 * tp_size)) throw ValidationError("d_in % 8 and d_out % (4 tp_size) must be 0");
-  if (plan.max_rank > kMaxTpRank) throw ValidationError("tensor-parallel LoRA: rank > 256");
+  if (din % 8 || dout % (8 * tp_size)) throw ValidationError("d_in % 8 and d_out % (8 tp_size) must be 0");
+  if (plan.max_rank > 256) throw ValidationError("tensor-parallel LoRA: rank > 256");
   for (const ClusterJob& j : plan.cjobs)
     if (j.rank % tp_size)
       throw ValidationError("adapter rank " + std::to_string(j.rank) + " is not divisible by tp_size " +
                             std::to_string(tp_size));
-  TpArgs a{};
-  a.arena = st.arena;
-  a.table = st.d_table;
-  a.jobs = plan.d_cjobs;
-  a.blk_mult = g.blk_mult(layer, proj);
-  a.log2_page = st.log2_page;
-  a.d_in = din;
-  a.d_out = dout;
-  a.tp_rank = tp_rank;
-  a.tp_size = tp_size;
-  a.rs_max = (plan.max_rank + tp_size - 1) / tp_size;
-  a.n_tokens = plan.n_tokens;
-  a.ncols = dout / tp_size;
-  a.col0 = tp_rank * a.ncols;
-  return a;
+  TpGeom t{};
+  t.d_in = din;
+  t.d_out = dout;
+  t.rs_max = (plan.max_rank + tp_size - 1) / tp_size;
+  t.ncols = dout / tp_size;
+  t.col0 = tp_rank * t.ncols;
+  return t;
+}
+
+// The item list of one half for (proj, tp_rank, tp_size): items are
+// LPT-assigned by streamed bytes to one CTA per SM.
+plora_plan::TpWork& tp_work(plora_plan& plan, uint32_t proj, uint32_t tp_rank, uint32_t tp_size,
+                            uint32_t half, const TpGeom& tg, cudaStream_t stream) {
+  const uint64_t key = (static_cast<uint64_t>(half) << 48) | (static_cast<uint64_t>(proj) << 40) |
+                       (static_cast<uint64_t>(tp_size) << 20) | tp_rank;
+  auto found = plan.tpw.find(key);
+  if (found != plan.tpw.end()) return found->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  PLORA_CUDA(cudaStreamIsCapturing(stream, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    throw ValidationError("the first tensor-parallel call of a plan for (proj, tp_rank, tp_size) uploads its "
+                          "item list and must run outside stream capture");
+  struct Cand {
+    StreamItem it;
+    double cost;
+  };
+  std::vector<Cand> cands;
+  const double ovh = 4096.0;  // per-item overhead in byte equivalents (as plan.cu)
+  for (uint32_t jn = 0; jn < plan.cjobs.size(); ++jn) {
+    const ClusterJob& j = plan.cjobs[jn];
+    StreamItem base{};
+    base.job = jn;
+    base.table_off = j.table_off;
+    base.rank_ntok = j.rank | (j.ntok << 16);
+    for (uint32_t t = 0; t < kJobTok; ++t) base.tok[t] = t < j.ntok ? j.tok[t] : 0u;
+    if (half == 1) {
+      const uint32_t rs = j.rank / tp_size;
+      for (uint32_t r0 = 0; r0 < rs; r0 += 16) {
+        Cand c{base, 0.0};
+        c.it.kind = 0;
+        c.it.off = tp_rank * rs + r0;  // absolute A row
+        c.it.n = std::min<uint32_t>(16, rs - r0);
+        c.it.v_off = r0;  // shard row of v_part
+        c.cost = 2.0 * c.it.n * tg.d_in + 1.0 * j.ntok * tg.d_in + ovh;
+        cands.push_back(c);
+      }
+    } else {
+      for (uint32_t c0 = tg.col0; c0 < tg.col0 + tg.ncols;) {
+        const uint32_t c1 = std::min(tg.col0 + tg.ncols, (c0 / kStreamKC + 1) * kStreamKC);
+        Cand c{base, 0.0};
+        c.it.kind = kStreamExpand;
+        c.it.off = c0;  // absolute output column
+        c.it.n = c1 - c0;
+        c.cost = 2.0 * j.rank * c.it.n + 4.0 * j.ntok * c.it.n + ovh;
+        cands.push_back(c);
+        c0 = c1;
+      }
+    }
+  }
+  std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.cost > b.cost; });
+  const uint32_t ctas =
+      std::min<uint32_t>(stream_max_ctas(plan.store->device, 4), static_cast<uint32_t>(cands.size()));
+  std::vector<std::vector<uint32_t>> lists(ctas);
+  using Load = std::pair<double, uint32_t>;
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (uint32_t c = 0; c < ctas; ++c) heap.emplace(0.0, c);
+  for (uint32_t k = 0; k < cands.size(); ++k) {
+    Load l = heap.top();
+    heap.pop();
+    lists[l.second].push_back(k);
+    heap.emplace(l.first + cands[k].cost, l.second);
+  }
+  std::vector<StreamItem> items;
+  std::vector<uint32_t> cta_off;
+  for (uint32_t c = 0; c < ctas; ++c) {
+    cta_off.push_back(static_cast<uint32_t>(items.size()));
+    for (uint32_t k : lists[c]) items.push_back(cands[k].it);
+  }
+  cta_off.push_back(static_cast<uint32_t>(items.size()));
+  plora_plan::TpWork w;
+  w.w.ctas = ctas;
+  w.w.np = 1;
+  w.w.projs[0] = proj;
+  const uint64_t ib = items.size() * sizeof(StreamItem), cb = cta_off.size() * sizeof(uint32_t);
+  DeviceCtx ctx(plan.store->device);
+  PLORA_CUDA(cudaMalloc(&w.d_items, ib + cb));
+  w.d_cta = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(w.d_items) + ib);
+  PLORA_CUDA(cudaMallocHost(&w.h_stage, ib + cb));
+  std::memcpy(w.h_stage, items.data(), ib);
+  std::memcpy(w.h_stage + ib, cta_off.data(), cb);
+  PLORA_CUDA(cudaMemcpyAsync(w.d_items, w.h_stage, ib + cb, cudaMemcpyHostToDevice, stream));
+  return plan.tpw.emplace(key, w).first->second;
 }
 
 }  // namespace
@@ -193,20 +170,23 @@ int plora_bgmv_tp_shrink(plora_plan* plan, uint32_t layer, uint32_t proj, uint32
                          plora_stream_t stream) {
   return guard([&] {
     if (!plan) throw ValidationError("null plan");
-    TpArgs a = tp_args(*plan, layer, proj, tp_rank, tp_size);
+    const TpGeom tg = tp_check(*plan, layer, proj, tp_rank, tp_size);
     if (plan->cjobs.empty()) return 0;
     if (!x || !v_part) throw ValidationError("null x or v_part");
-    if (x_stride < a.d_in || x_stride % 8 || reinterpret_cast<uintptr_t>(x) % 16)
+    if (x_stride < tg.d_in || x_stride % 8 || reinterpret_cast<uintptr_t>(x) % 16)
       throw ValidationError("x must be 16-byte aligned with a row stride >= d_in, multiple of 8");
     DeviceCtx ctx(plan->store->device);
-    a.x = static_cast<const char*>(x);
-    a.x_stride_b = x_stride * 2;
-    a.v = v_part;
-    const uint32_t rows = a.rs_max;
-    tp_shrink_kernel<<<dim3(static_cast<uint32_t>(plan->cjobs.size()), (rows + 3) / 4), 128, 0,
-                       static_cast<cudaStream_t>(stream)>>>(a);
-    PLORA_CUDA(cudaGetLastError());
-    count_launch();
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const plora_plan::TpWork& w = tp_work(*plan, proj, tp_rank, tp_size, 1, tg, s);
+    StreamTp tp{};
+    tp.mode = 1;
+    tp.tp_size = tp_size;
+    tp.n_tokens = plan->n_tokens;
+    tp.rs_max = tg.rs_max;
+    tp.v_out = v_part;
+    tp.items = w.d_items;
+    tp.cta_off = w.d_cta;
+    launch_bgmv_stream_tp(*plan, w.w, tp, layer, x, x_stride, nullptr, 0, 1.f, s);
     return 0;
   });
 }
@@ -216,20 +196,25 @@ int plora_bgmv_tp_expand(plora_plan* plan, uint32_t layer, uint32_t proj, uint32
                          uint64_t y_stride, float scale, plora_stream_t stream) {
   return guard([&] {
     if (!plan) throw ValidationError("null plan");
-    TpArgs a = tp_args(*plan, layer, proj, tp_rank, tp_size);
+    const TpGeom tg = tp_check(*plan, layer, proj, tp_rank, tp_size);
     if (plan->cjobs.empty()) return 0;
     if (!v_gathered || !y_shard) throw ValidationError("null v_gathered or y_shard");
-    if (y_stride < a.ncols || y_stride % 4 || reinterpret_cast<uintptr_t>(y_shard) % 8)
-      throw ValidationError("y_shard must be 8-byte aligned with a row stride >= d_out/tp_size, multiple of 4");
+    if (y_stride < tg.ncols || y_stride % 8 || reinterpret_cast<uintptr_t>(y_shard) % 16)
+      throw ValidationError("y_shard must be 16-byte aligned with a row stride >= d_out/tp_size, multiple of 8");
     DeviceCtx ctx(plan->store->device);
-    a.v = const_cast<float*>(v_gathered);
-    a.y = static_cast<char*>(y_shard);
-    a.y_stride_b = y_stride * 2;
-    a.scale = scale;
-    tp_expand_kernel<<<dim3(static_cast<uint32_t>(plan->cjobs.size()), (a.ncols + kExpCols - 1) / kExpCols),
-                       64, 0, static_cast<cudaStream_t>(stream)>>>(a);
-    PLORA_CUDA(cudaGetLastError());
-    count_launch();
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const plora_plan::TpWork& w = tp_work(*plan, proj, tp_rank, tp_size, 2, tg, s);
+    StreamTp tp{};
+    tp.mode = 2;
+    tp.tp_size = tp_size;
+    tp.n_tokens = plan->n_tokens;
+    tp.rs_max = tg.rs_max;
+    tp.v_in = v_gathered;
+    tp.items = w.d_items;
+    tp.cta_off = w.d_cta;
+    // the kernel addresses output column c (absolute in d_out) at y + c
+    char* y = static_cast<char*>(y_shard) - static_cast<ptrdiff_t>(tg.col0) * 2;
+    launch_bgmv_stream_tp(*plan, w.w, tp, layer, nullptr, 0, y, y_stride, scale, s);
     return 0;
   });
 }

@@ -117,8 +117,9 @@ class TensorParallelLoRA:
             self._buf = torch.empty(need, dtype=torch.float32, device=self.device)
             self._gbuf = torch.empty(self.tp_size * need, dtype=torch.float32, device=self.device)
         self.rs, self.n_tokens = rs, t
-        self.v_part = self._buf[:t * rs].view(t, rs)
         self.v_gathered = self._gbuf[:self.tp_size * t * rs].view(self.tp_size, t, rs)
+        # one rank: the shrink writes the "gathered" buffer directly (no copy)
+        self.v_part = self.v_gathered[0] if self.tp_size == 1 else self._buf[:t * rs].view(t, rs)
 
     def forward(self, layer: int, proj: int, x: torch.Tensor, y_shard: torch.Tensor,
                 scale: float = 1.0) -> torch.Tensor:
@@ -131,8 +132,6 @@ class TensorParallelLoRA:
         self._shrink(self.plan, layer, proj, self.tp_rank, self.tp_size, x, self.v_part)
         if self.tp_size > 1:
             self._gather(self.v_gathered, self.v_part)
-        else:
-            self.v_gathered[0].copy_(self.v_part)
         return self._expand(self.plan, layer, proj, self.tp_rank, self.tp_size, self.v_gathered,
                             y_shard, scale)
 

@@ -42,14 +42,19 @@ def main():
     per_layer = lambda: [bgmv_layer(plan, l, x[l], [y[l, 0], y[l, 1]]) for l in range(32)]  # noqa: E731
     multi = lambda: bgmv_layers(plan, 0, x, [y[:, 0], y[:, 1]])  # noqa: E731
     alg = 136314880
-    for impl in (1, 0):  # 1 streaming, 0 clusters
+    flag_sets = [int(f) for f in os.environ.get("ABLATE_FLAGS", "0,1,2").split(",")]
+    for impl in (1, 0):  # 1 streaming, 0 clusters (+ the hybrid streaming share for the 32-layer launch)
         N.check(N.lib().plora_debug_set_bgmv_impl(impl))
-        for flags in ((0, 128, 1, 2) if impl == 1 else (0,)):
-            N.check(N.lib().plora_debug_set_bgmv_flags(flags))
-            a = timeit(per_layer, 5) / 32
-            b = timeit(multi, 5) / 32
-            print(f"impl {impl} flags {flags}: per-layer launch {a:.1f} us ({alg / a / 1e3:.0f} GB/s), "
-                  f"32-layer launch {b:.1f} us/layer ({alg / b / 1e3:.0f} GB/s)")
+        plan.update(ta)  # the hybrid split is decided at plan build
+        for pf in (1, 0):  # L2 prefetch of the streaming kernel's weight rows
+            N.check(N.lib().plora_debug_set_stream_prefetch(pf))
+            for flags in (flag_sets if impl == 1 else (0,)):
+                N.check(N.lib().plora_debug_set_bgmv_flags(flags))
+                a = timeit(per_layer, 5) / 32
+                b = timeit(multi, 5) / 32
+                print(f"impl {impl} prefetch {pf} flags {flags}: per-layer launch {a:.1f} us "
+                      f"({alg / a / 1e3:.0f} GB/s), 32-layer launch {b:.1f} us/layer ({alg / b / 1e3:.0f} GB/s)")
+    N.check(N.lib().plora_debug_set_stream_prefetch(0))
     N.check(N.lib().plora_debug_set_bgmv_flags(0))
     N.check(N.lib().plora_debug_set_bgmv_impl(0))
 
