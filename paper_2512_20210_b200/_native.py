@@ -266,6 +266,8 @@ _SIGS = {
     "plora_debug_set_bgmv_impl": (_int, [C.c_int]),
     "plora_debug_set_bgmv_flags": (_int, [_u32]),
     "plora_debug_set_stream_prefetch": (_int, [_u32]),
+    "plora_debug_set_route_tokens": (_int, [_u32]),
+    "plora_debug_plan_routed": (_int, [C.c_void_p, C.POINTER(_u32)]),
     "plora_debug_set_stream_ctas": (_int, [_u32]),
     "plora_debug_set_hybrid_share": (_int, [C.c_double]),
     "plora_debug_plan_hybrid": (_int, [_vp, _P(C.c_double)]),

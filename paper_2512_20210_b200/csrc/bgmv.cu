@@ -444,6 +444,137 @@ void launch_hybrid(plora_plan* plan, uint32_t layer0, uint32_t n_layers, const v
 }
 }  // namespace plora
 
+namespace {
+// ---- many-token adapters on the tensor-core path (plan.cu: plan->route)
+uint32_t g_route_min = 48;  // plora_debug_set_route_tokens (profiles/r02j_route_sweep.txt)
+
+// xg[i, :] = x[perm[i], :]: the routed tokens' rows, in adapter order
+__global__ void route_gather_kernel(const char* __restrict__ x, uint64_t x_stride_b,
+                                    const uint32_t* __restrict__ perm, uint32_t n, uint32_t row_v,
+                                    uint4* __restrict__ xg) {
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < static_cast<uint64_t>(n) * row_v;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t i = static_cast<uint32_t>(e / row_v), c = static_cast<uint32_t>(e - static_cast<uint64_t>(i) * row_v);
+    xg[e] = __ldg(reinterpret_cast<const uint4*>(x + perm[i] * x_stride_b) + c);
+  }
+}
+
+// y[perm[i], :] = bf16(y + yg[i, :]) for every projection (blockIdx.y): yg
+// holds bf16(scale · delta), the value the SGMV expand reduce-adds into y
+struct ScatterArgs {
+  const uint4* yg[PLORA_MAX_PROJ];
+  char* y[PLORA_MAX_PROJ];
+  uint64_t y_stride_b[PLORA_MAX_PROJ];
+  uint32_t row_v[PLORA_MAX_PROJ];
+  const uint32_t* perm;
+  uint32_t n;
+};
+__global__ void route_scatter_kernel(const ScatterArgs a) {
+  const uint32_t p = blockIdx.y, row_v = a.row_v[p];
+  for (uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; e < static_cast<uint64_t>(a.n) * row_v;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t i = static_cast<uint32_t>(e / row_v), c = static_cast<uint32_t>(e - static_cast<uint64_t>(i) * row_v);
+    uint4* yp = reinterpret_cast<uint4*>(a.y[p] + a.perm[i] * a.y_stride_b[p]) + c;
+    const uint4 d = a.yg[p][e];
+    uint4 v = *yp;
+    uint32_t* vw = reinterpret_cast<uint32_t*>(&v);
+    const uint32_t* dw = reinterpret_cast<const uint32_t*>(&d);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const __nv_bfloat162 o = __floats2bfloat162_rn(__uint_as_float(vw[k] << 16) + __uint_as_float(dw[k] << 16),
+                                                     __uint_as_float(vw[k] & 0xffff0000u) +
+                                                         __uint_as_float(dw[k] & 0xffff0000u));
+      vw[k] = *reinterpret_cast<const uint32_t*>(&o);
+    }
+    *yp = v;
+  }
+}
+}  // namespace
+
+namespace plora {
+uint32_t route_min_tokens() { return g_route_min; }
+
+// The routed adapters of layers [layer0, layer0 + n_layers), projections
+// `projs`, forked onto the plan's route stream: per layer, gather their x
+// rows, run the tensor-core SGMV (plora_sgmv / plora_sgmv_layer on the child
+// plan) into zeroed bf16 deltas, and add the deltas into their y rows.  The
+// caller joins with join_routed after its own launches (the decode kernels
+// touch the other tokens' rows only).  Returns false if nothing is routed.
+bool launch_routed(plora_plan* plan, uint32_t layer0, uint32_t n_layers, const uint32_t* projs,
+                   uint32_t np, const void* x, uint64_t x_stride, uint64_t x_lstride, void* const* ys,
+                   const uint64_t* y_strides, const uint64_t* y_lstrides, float scale, cudaStream_t s) {
+  if (!plan->route || plan->n_route == 0) return false;
+  const ModelGeom& g = plan->store->geom;
+  if (!plan->route_stream) {
+    PLORA_CUDA(cudaStreamCreateWithFlags(&plan->route_stream, cudaStreamNonBlocking));
+    PLORA_CUDA(cudaEventCreateWithFlags(&plan->ev_rfork, cudaEventDisableTiming));
+    PLORA_CUDA(cudaEventCreateWithFlags(&plan->ev_rjoin, cudaEventDisableTiming));
+  }
+  cudaStream_t rs = plan->route_stream;
+  PLORA_CUDA(cudaEventRecord(plan->ev_rfork, s));
+  PLORA_CUDA(cudaStreamWaitEvent(rs, plan->ev_rfork, 0));
+  const uint32_t n = plan->n_route, din = g.m.d_in[projs[0]];
+  char* xg = plan->d_route_ws;
+  char* yg[PLORA_MAX_PROJ];
+  uint64_t ygs[PLORA_MAX_PROJ];
+  uint64_t ybytes = 0;
+  char* yb = xg + static_cast<uint64_t>(n) * din * 2;
+  for (uint32_t j = 0; j < np; ++j) {
+    yg[j] = yb + ybytes;
+    ygs[j] = g.m.d_out[projs[j]];
+    ybytes += static_cast<uint64_t>(n) * g.m.d_out[projs[j]] * 2;
+  }
+  const uint32_t blocks = std::min<uint32_t>(1024, (n * (din / 8) + 255) / 256);
+  for (uint32_t l = 0; l < n_layers; ++l) {
+    route_gather_kernel<<<blocks, 256, 0, rs>>>(static_cast<const char*>(x) + l * x_lstride * 2, x_stride * 2,
+                                                plan->d_route_perm, n, din / 8, reinterpret_cast<uint4*>(xg));
+    PLORA_CUDA(cudaGetLastError());
+    count_launch();
+    PLORA_CUDA(cudaMemsetAsync(yb, 0, ybytes, rs));
+    int rc;
+    if (np == g.m.n_proj && np > 1)
+      rc = plora_sgmv_layer(plan->route, layer0 + l, xg, din, reinterpret_cast<void* const*>(yg), ygs, scale, rs);
+    else
+      rc = plora_sgmv(plan->route, layer0 + l, projs[0], xg, din, yg[0], ygs[0], scale, rs);
+    if (rc < 0) throw CudaError(std::string("routed SGMV: ") + plora_last_error());
+    ScatterArgs sa{};
+    uint32_t vmax = 0;
+    for (uint32_t j = 0; j < np; ++j) {
+      sa.yg[j] = reinterpret_cast<const uint4*>(yg[j]);
+      sa.y[j] = static_cast<char*>(ys[j]) + (y_lstrides ? l * y_lstrides[j] * 2 : 0);
+      sa.y_stride_b[j] = y_strides[j] * 2;
+      sa.row_v[j] = g.m.d_out[projs[j]] / 8;
+      vmax = std::max(vmax, sa.row_v[j]);
+    }
+    sa.perm = plan->d_route_perm;
+    sa.n = n;
+    route_scatter_kernel<<<dim3(std::min<uint32_t>(1024, (n * vmax + 255) / 256), np), 256, 0, rs>>>(sa);
+    PLORA_CUDA(cudaGetLastError());
+    count_launch();
+  }
+  PLORA_CUDA(cudaEventRecord(plan->ev_rjoin, rs));
+  return true;
+}
+
+void join_routed(plora_plan* plan, cudaStream_t s) {
+  PLORA_CUDA(cudaStreamWaitEvent(s, plan->ev_rjoin, 0));
+}
+}  // namespace plora
+
+extern "C" int plora_debug_set_route_tokens(uint32_t min_tokens) {
+  g_route_min = min_tokens;  // plans built afterwards
+  return 0;
+}
+
+extern "C" int plora_debug_plan_routed(const plora_plan* plan, uint32_t* n_tokens) {
+  using namespace plora;
+  return guard([&] {
+    if (!plan || !n_tokens) throw ValidationError("null plan or n_tokens");
+    *n_tokens = plan->route ? plan->n_route : 0u;
+    return 0;
+  });
+}
+
 extern "C" int plora_debug_set_hybrid_per_layer(int on) {
   g_hybrid_per_layer = on;
   return 0;
@@ -482,15 +613,15 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
     const ProjWork& pw = plan->proj[proj];
     DeviceCtx ctx(st.device);
     if (g.esize == 2) {  // bf16: the streaming op (bgmv_stream.cu) or the cluster op
-      if (g_bgmv_impl != 1) {
-        launch_bgmv_cluster(*plan, layer, proj, x, x_stride, y, y_stride, scale,
-                            static_cast<cudaStream_t>(stream));
-      } else {
-        void* ys[1] = {y};
-        const uint64_t yst[1] = {y_stride};
-        launch_bgmv_stream(*plan, plan->swork[proj], layer, 1, x, x_stride, 0, ys, yst, nullptr,
-                           scale, static_cast<cudaStream_t>(stream));
-      }
+      cudaStream_t s = static_cast<cudaStream_t>(stream);
+      void* ys[1] = {y};
+      const uint64_t yst[1] = {y_stride};
+      const bool routed = launch_routed(plan, layer, 1, &proj, 1, x, x_stride, 0, ys, yst, nullptr, scale, s);
+      if (g_bgmv_impl != 1)
+        launch_bgmv_cluster(*plan, layer, proj, x, x_stride, y, y_stride, scale, s);
+      else
+        launch_bgmv_stream(*plan, plan->swork[proj], layer, 1, x, x_stride, 0, ys, yst, nullptr, scale, s);
+      if (routed) join_routed(plan, s);
       return 0;
     }
     if (pw.n_units == 0) return 0;  // no LoRA token in the batch
@@ -540,25 +671,38 @@ extern "C" int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_l
       if (y_layer_strides[p] % vec) throw ValidationError("layer strides must be multiples of 16 bytes");
       check_io(plan, layer0, p, x, x_stride, ys[p], y_strides[p]);
     }
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t all[PLORA_MAX_PROJ];
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) all[p] = p;
+    auto routed = [&] {
+      return launch_routed(plan, layer0, n_layers, all, g.m.n_proj, x, x_stride, x_layer_stride, ys,
+                           y_strides, y_layer_strides, scale, s);
+    };
     if (g.esize == 2 && g_bgmv_impl == 1 && plan->swork_layer.np == g.m.n_proj) {
       DeviceCtx ctx(st.device);
+      const bool r = routed();
       launch_bgmv_stream(*plan, plan->swork_layer, layer0, n_layers, x, x_stride, x_layer_stride,
-                         ys, y_strides, y_layer_strides, scale, static_cast<cudaStream_t>(stream));
+                         ys, y_strides, y_layer_strides, scale, s);
+      if (r) join_routed(plan, s);
       return 0;
     }
     if (g.esize == 2 && g_bgmv_impl == 0 && plan->hyb_spare && plan->n_layer_proj == g.m.n_proj &&
         n_layers * g.m.n_proj <= 256) {
       DeviceCtx ctx(st.device);
+      const bool r = routed();
       launch_hybrid(plan, layer0, n_layers, x, x_stride, x_layer_stride, ys, y_strides, y_layer_strides,
-                    scale, static_cast<cudaStream_t>(stream));
+                    scale, s);
+      if (r) join_routed(plan, s);
       return 0;
     }
     const bool one = g.esize == 2 && plan->n_layer_proj == g.m.n_proj &&
                      n_layers * g.m.n_proj <= 256;
     if (one) {
       DeviceCtx ctx(st.device);
+      const bool r = routed();
       launch_bgmv_cluster_layers(*plan, layer0, n_layers, x, x_stride, x_layer_stride, ys,
-                                 y_strides, y_layer_strides, scale, static_cast<cudaStream_t>(stream));
+                                 y_strides, y_layer_strides, scale, s);
+      if (r) join_routed(plan, s);
       return 0;
     }
     std::vector<void*> yl(g.m.n_proj);
@@ -586,25 +730,34 @@ extern "C" int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x,
         throw ValidationError("plora_bgmv_layer: projections read different input widths");
       check_io(plan, layer, p, x, x_stride, ys[p], y_strides[p]);
     }
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    uint32_t all[PLORA_MAX_PROJ];
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) all[p] = p;
+    auto routed = [&] {
+      return launch_routed(plan, layer, 1, all, g.m.n_proj, x, x_stride, 0, ys, y_strides, nullptr, scale, s);
+    };
     if (g.esize == 2 && g_bgmv_impl == 1 && plan->swork_layer.np == g.m.n_proj) {
       DeviceCtx ctx(st.device);
       const uint64_t zero[PLORA_MAX_PROJ] = {};
-      launch_bgmv_stream(*plan, plan->swork_layer, layer, 1, x, x_stride, 0, ys, y_strides, zero,
-                         scale, static_cast<cudaStream_t>(stream));
+      const bool r = routed();
+      launch_bgmv_stream(*plan, plan->swork_layer, layer, 1, x, x_stride, 0, ys, y_strides, zero, scale, s);
+      if (r) join_routed(plan, s);
       return 0;
     }
     if (g.esize == 2 && g_bgmv_impl == 0 && g_hybrid_per_layer && plan->hyb_spare &&
         plan->n_layer_proj == g.m.n_proj) {
       DeviceCtx ctx(st.device);
       const uint64_t zero[PLORA_MAX_PROJ] = {};
-      launch_hybrid(plan, layer, 1, x, x_stride, 0, ys, y_strides, zero, scale,
-                    static_cast<cudaStream_t>(stream));
+      const bool r = routed();
+      launch_hybrid(plan, layer, 1, x, x_stride, 0, ys, y_strides, zero, scale, s);
+      if (r) join_routed(plan, s);
       return 0;
     }
     if (g.esize == 2 && plan->n_layer_proj == g.m.n_proj) {
       DeviceCtx ctx(st.device);
-      launch_bgmv_cluster_layer(*plan, layer, x, x_stride, ys, y_strides, scale,
-                                static_cast<cudaStream_t>(stream));
+      const bool r = routed();
+      launch_bgmv_cluster_layer(*plan, layer, x, x_stride, ys, y_strides, scale, s);
+      if (r) join_routed(plan, s);
       return 0;
     }
     for (uint32_t p = 0; p < g.m.n_proj; ++p) {  // shapes differ: one launch per projection

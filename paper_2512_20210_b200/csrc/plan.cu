@@ -74,6 +74,54 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   std::stable_sort(order.begin(), order.end(),
                    [&](uint32_t x, uint32_t y) { return segs[x].rank > segs[y].rank; });
 
+  // ---- many-token adapters -> the tensor-core SGMV path on a child plan
+  // (bgmv.cu launch_routed): bf16 stores, rank <= 128 and the SGMV geometry
+  // for every projection
+  seg_route.assign(segs.size(), 0);
+  route_perm.clear();
+  n_route = 0;
+  {
+    bool tc_ok = es == 2 && !no_route && route_min_tokens() > 0;
+    for (uint32_t p = 0; p < g.m.n_proj && tc_ok; ++p)
+      tc_ok = g.m.d_in[p] % 64 == 0 && g.m.d_out[p] % 128 == 0 && g.blocks_aligned_128(p);
+    std::vector<int32_t> child_ta;
+    for (uint32_t si = 0; si < segs.size() && tc_ok; ++si) {
+      const Seg& sg = segs[si];
+      if (sg.toks.size() < route_min_tokens() || sg.rank > 128) continue;
+      seg_route[si] = 1;
+      for (uint32_t tk : sg.toks) {
+        route_perm.push_back(tk);
+        child_ta.push_back(static_cast<int32_t>(sg.adapter));
+      }
+    }
+    n_route = static_cast<uint32_t>(route_perm.size());
+    if (n_route) {
+      if (!route) {
+        route = new plora_plan;
+        route->store = store;
+        route->no_route = true;
+      }
+      route->build(child_ta.data(), n_route, stream);
+      uint32_t dmax = 0;
+      uint64_t yb = 0;
+      for (uint32_t p = 0; p < g.m.n_proj; ++p) {
+        dmax = std::max(dmax, g.m.d_in[p]);
+        yb += static_cast<uint64_t>(n_route) * g.m.d_out[p] * 2;
+      }
+      const uint64_t need = static_cast<uint64_t>(n_route) * dmax * 2 + yb;
+      if (route_ws_cap < need) {
+        DeviceCtx ctx(st.device);
+        if (d_route_ws) {
+          PLORA_CUDA(cudaStreamSynchronize(stream));
+          cudaFree(d_route_ws);
+        }
+        d_route_ws = nullptr;
+        PLORA_CUDA(cudaMalloc(&d_route_ws, need));
+        route_ws_cap = need;
+      }
+    }
+  }
+
   // ---- fp32 BGMV units per projection (the bf16 op runs on clusters, below)
   units.clear();
   for (uint32_t p = 0; p < g.m.n_proj; ++p) proj[p] = ProjWork{};
@@ -293,11 +341,15 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   bool layer_same = g.m.n_proj > 1;
   for (uint32_t p = 1; p < g.m.n_proj; ++p)
     layer_same = layer_same && g.m.d_in[p] == g.m.d_in[0] && g.m.d_out[p] == g.m.d_out[0];
-  uint32_t seg_maxtok = 0;
-  for (const Seg& sg : segs) seg_maxtok = std::max<uint32_t>(seg_maxtok, static_cast<uint32_t>(sg.toks.size()));
+  uint32_t seg_maxtok = 0, n_kept = 0;  // over the adapters the decode kernels keep
+  for (uint32_t si = 0; si < segs.size(); ++si)
+    if (!seg_route[si]) {
+      seg_maxtok = std::max<uint32_t>(seg_maxtok, static_cast<uint32_t>(segs[si].toks.size()));
+      ++n_kept;
+    }
   // (batches with an adapter of more than 4 tokens would run the streaming
   // share with 8-token jobs, which measured 2x slower: clusters only then)
-  if (es == 2 && layer_same && hybrid_enabled() && !segs.empty() && seg_maxtok <= kJobTok) {
+  if (es == 2 && layer_same && hybrid_enabled() && n_kept && seg_maxtok <= kJobTok) {
     const ClusterGeom cg = cluster_geom(g.m.d_in[0], g.m.d_out[0], st.device);
     const uint32_t sms = static_cast<uint32_t>(std::max(1, st.num_sms));
     const uint32_t used = cg.n_clusters * cg.cs;
@@ -308,7 +360,8 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       std::vector<uint32_t> by(segs.size());
       std::iota(by.begin(), by.end(), 0u);
       auto bytes_of = [&](uint32_t i) {  // weight rows streamed per token group (rank per job)
-        return static_cast<uint64_t>(segs[i].rank) * ((segs[i].toks.size() + kJobTok - 1) / kJobTok);
+        return seg_route[i] ? 0ull
+                            : static_cast<uint64_t>(segs[i].rank) * ((segs[i].toks.size() + kJobTok - 1) / kJobTok);
       };
       uint64_t all = 0;
       for (uint32_t i = 0; i < segs.size(); ++i) all += bytes_of(i);
@@ -316,7 +369,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       const double target = static_cast<double>(all) * hyb_spare / sms * hybrid_share_factor();
       uint64_t acc = 0;
       for (uint32_t i : by)
-        if (static_cast<double>(acc + bytes_of(i)) <= target) {
+        if (bytes_of(i) && static_cast<double>(acc + bytes_of(i)) <= target) {
           seg_hyb[i] = 1;
           acc += bytes_of(i);
         }
@@ -332,12 +385,13 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   cchunks.clear();
   ccl_off.clear();
   ccl_jobs.clear();
-  std::vector<uint8_t> cjob_hyb;
+  std::vector<uint8_t> cjob_hyb, cjob_route;
   if (es == 2) {
     for (uint32_t si = 0; si < segs.size(); ++si) {
       const Seg& s = segs[si];
       for (uint32_t tc = 0; tc < s.toks.size(); tc += kJobTok) {
         cjob_hyb.push_back(seg_hyb[si]);
+        cjob_route.push_back(seg_route[si]);  // kept in cjobs (the TP halves serve every token)
         ClusterJob j{};
         j.table_off = s.table_off;
         j.rank = s.rank;
@@ -366,9 +420,12 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       cw.geom = cluster_geom(din, dout, st.device);
       std::vector<uint32_t> jo;  // work item w = job w % nj of projection w / nj
       for (uint32_t w = 0; w < nj * np; ++w)
-        if (!exclude_hyb || !cjob_hyb[w % nj]) jo.push_back(w);
+        if ((!exclude_hyb || !cjob_hyb[w % nj]) && !cjob_route[w % nj]) jo.push_back(w);
       const uint32_t nw = static_cast<uint32_t>(jo.size());
-      if (nw == 0) return;
+      if (nw == 0) {
+        cw.geom.n_clusters = 0;  // every job left this launch
+        return;
+      }
       const uint32_t nc = std::min(cw.geom.n_clusters, nw);
       cw.geom.n_clusters = nc;
       auto cost = [&](uint32_t w) {
@@ -437,9 +494,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
   s_njobs = 0;
   s_vplane = 0;
   if (es == 2) {
-    uint32_t maxtok = 0;
-    for (const Seg& sg : segs) maxtok = std::max<uint32_t>(maxtok, static_cast<uint32_t>(sg.toks.size()));
-    s_jt = maxtok > 4 ? 8 : 4;
+    s_jt = seg_maxtok > 4 ? 8 : 4;
     struct SJob {
       uint32_t rank, table_off, ntok, v_off, tok[8];
       uint8_t hyb;  // the adapter belongs to the hybrid launch's streaming share
@@ -448,6 +503,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     uint64_t voff = 0;
     for (uint32_t si : order) {  // largest rank first
       const Seg& sg = segs[si];
+      if (seg_route[si]) continue;
       for (uint32_t tc = 0; tc < sg.toks.size(); tc += s_jt) {
         SJob j{};
         j.rank = sg.rank;
@@ -587,6 +643,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       {scta.data(), scta.size() * sizeof(uint32_t), reinterpret_cast<void**>(&d_scta)},
       {stitems.data(), stitems.size() * sizeof(StreamItem), reinterpret_cast<void**>(&d_stitems)},
       {stcta.data(), stcta.size() * sizeof(uint32_t), reinterpret_cast<void**>(&d_stcta)},
+      {route_perm.data(), route_perm.size() * sizeof(uint32_t), reinterpret_cast<void**>(&d_route_perm)},
   };
   uint64_t total = 0;
   for (const Part& pt : parts) total += align(pt.bytes);
@@ -712,6 +769,11 @@ void plora_plan_destroy(plora_plan* plan) {
   }
   cudaDeviceSynchronize();
   plan->drop_tp();
+  if (plan->route) plora_plan_destroy(plan->route);
+  cudaFree(plan->d_route_ws);
+  if (plan->route_stream) cudaStreamDestroy(plan->route_stream);
+  if (plan->ev_rfork) cudaEventDestroy(plan->ev_rfork);
+  if (plan->ev_rjoin) cudaEventDestroy(plan->ev_rjoin);
   cudaFreeHost(plan->h_pinned);
   cudaFree(plan->d_buf);
   cudaFree(plan->d_v);

@@ -296,6 +296,20 @@ struct plora_plan {
   };
   std::map<uint64_t, TpWork> tpw;
   void drop_tp();
+  // Many-token adapters (>= route_min_tokens() tokens in the batch) leave the
+  // decode kernels: their tokens, gathered in adapter order, form a child
+  // plan that runs the tensor-core SGMV path (bgmv.cu launch_routed), on its
+  // own stream, concurrently with the decode kernels over the other adapters.
+  std::vector<uint8_t> seg_route;    // per segment (adapter) of the batch
+  plora_plan* route = nullptr;       // the child plan (never routes itself)
+  bool no_route = false;
+  uint32_t n_route = 0;              // routed tokens (0: none this batch)
+  std::vector<uint32_t> route_perm;  // routed row i -> the batch's token row
+  uint32_t* d_route_perm = nullptr;  // (in d_buf)
+  char* d_route_ws = nullptr;        // one layer: gathered x, then y deltas per projection
+  uint64_t route_ws_cap = 0;
+  cudaStream_t route_stream = nullptr;
+  cudaEvent_t ev_rfork = nullptr, ev_rjoin = nullptr;
 
   void build(const int32_t* token_adapter, uint32_t n, cudaStream_t stream);
 };
@@ -322,6 +336,7 @@ void launch_bgmv_stream(const plora_plan& plan, const StreamWork& w, uint32_t la
                         float scale, cudaStream_t stream);
 uint32_t stream_max_ctas(int device, uint32_t jt);
 bool hybrid_enabled();  // plora_debug_set_bgmv_impl: 0 (default) = clusters + streaming share
+uint32_t route_min_tokens();  // plora_debug_set_route_tokens (0: never route)
 double hybrid_share_factor();  // streaming share = spare SMs / SMs × this (of the weight bytes)
 // Every projection of `layer` (they read the same x) in one launch.
 void launch_bgmv_cluster_layer(const plora_plan& plan, uint32_t layer, const void* x,

@@ -36,8 +36,10 @@ def main():
         store.publish(a)
     from paper_2512_20210_b200 import _native as N
     impl = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    route = int(sys.argv[4]) if len(sys.argv) > 4 else 16  # many-token adapters -> SGMV (0: off)
     N.check(N.lib().plora_debug_set_bgmv_impl(impl))
-    out = {"impl": impl}
+    N.check(N.lib().plora_debug_set_route_tokens(route))
+    out = {"impl": impl, "route_min_tokens": route}
     for name, ta in (("skewed", skewed_assignment(hot=hot)),
                      ("uniform", synth.token_assignment(128, 4))):
         T = len(ta)
