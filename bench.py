@@ -739,7 +739,7 @@ def run_cfg5(args):
     T = len(ta)
     L, NP = shape.n_layers, shape.n_proj
     plan = BatchPlan(store, ta)
-    tp = TensorParallelLoRA(plan, rank, world)
+    tp = TensorParallelLoRA(plan, rank, world, allgather=args.cfg5_allgather)
     x = torch.randn(L, T, shape.d_in[0], device=dev).to(torch.bfloat16)
     ys = [torch.randn(L, T, shape.d_out[p] // world, device=dev).to(torch.bfloat16)
           for p in range(NP)]
@@ -783,6 +783,7 @@ def run_cfg5(args):
     # per-rank algorithmic bytes of one (layer, proj) call: its A rows, its Bᵀ
     # columns, x, its y shard RMW
     split = None
+    fused_ms = None
     rank0 = {}
     if world == 1:  # the per-rank halves themselves (shrink, copy, expand) at TP = 1
         tps = TensorParallelLoRA(plan, 0, 1, force_split=True)
@@ -807,6 +808,29 @@ def run_cfg5(args):
         s1.record(stream)
         torch.cuda.synchronize()
         split = s0.elapsed_time(s1) / K
+        # the same halves with the all-gather fused into the shrink (peer-write
+        # + arrival flags; at TP = 1 the peer is this GPU)
+        tpf = TensorParallelLoRA(plan, 0, 1, force_split=True, allgather="fused")
+
+        def step_fused():
+            for l in range(L):
+                for p in range(NP):
+                    tpf(l, p, x[l], ys[p][l])
+
+        for _ in range(3):
+            step_fused()
+        torch.cuda.synchronize()
+        g4 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g4):
+            step_fused()
+        g4.replay()
+        torch.cuda.synchronize()
+        s0.record(stream)
+        for _ in range(K):
+            g4.replay()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        fused_ms = s0.elapsed_time(s1) / K
         # one rank's halves at TP = 2, 4, 8 (the collective excluded: rank 0
         # expands from a gathered buffer filled once by every rank's shrink)
         from paper_2512_20210_b200.tp import bgmv_tp_expand, bgmv_tp_shrink, tp_shard_rows
@@ -859,7 +883,8 @@ def run_cfg5(args):
         "config": {"workload": (f"cfg5 tensor-parallel LoRA, Llama-2-70B q/v (q 8192->8192, "
                                 f"v 8192->1024), {L} layers x 2 per step, 256 tokens / "
                                 f"{cfg.n_adapters} adapters, r=[8,16,64][a%3], TP={world}"),
-                   "page_bytes": args.page_bytes, "parallelism": f"tp{world} (S-LoRA all-gather)",
+                   "page_bytes": args.page_bytes,
+                   "parallelism": f"tp{world} (S-LoRA all-gather: {args.cfg5_allgather})",
                    "cuda_graph": True, "all_gather_bytes_per_call": gather_bytes,
                    "l2": "inputs > L2: adapter pages of 160 (layer, proj) blocks per step"},
         "gpu_launches": per_replay * K,
@@ -874,6 +899,11 @@ def run_cfg5(args):
             "hbm_frac": per_call / (split / (L * NP) / 1e3) / 1e9 / peak,
             "note": "tp_shrink + tp_expand forced at TP=1 (the per-rank kernels of the N>1 path; "
                     "value above uses the fused data-parallel op at TP=1)"},
+        "tp_fused_allgather_at_tp1": None if split is None else {
+            "ms_per_step": fused_ms, "us_per_call": fused_ms * 1e3 / (L * NP),
+            "hbm_frac": per_call / (fused_ms / (L * NP) / 1e3) / 1e9 / peak,
+            "note": "plora_bgmv_tp_shrink_push + plora_bgmv_tp_expand_wait (peer-write all-gather, "
+                    "arrival flags) forced at TP=1"},
         "tp_rank0_halves": None if split is None else {
             **rank0,
             "note": "rank 0's shrink + expand per (layer, proj) call at TP = N on one GPU, the "
@@ -984,6 +1014,8 @@ def main():
     ap.add_argument("--per-proj", action="store_true",
                     help="decode: one launch per (layer, proj) instead of one per layer")
     ap.add_argument("--cfg5-layers", type=int, default=80)
+    ap.add_argument("--cfg5-allgather", default="nccl", choices=["nccl", "fused"],
+                    help="TP all-gather: NCCL between the halves, or fused into the shrink (peer-write)")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg3f", "cfg4", "cfg5"],
                     help="cfg2 = decode BGMV (headline), cfg3 = prefill SGMV, "
                          "cfg3f = prefill with the base projection GEMM fused in, "

@@ -375,6 +375,26 @@ int plora_bgmv_tp_shrink(plora_plan* plan, uint32_t layer, uint32_t proj, uint32
 int plora_bgmv_tp_expand(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
                          uint32_t tp_size, const float* v_gathered, void* y_shard,
                          uint64_t y_stride, float scale, plora_stream_t stream);
+/* The all-gather fused into the shrink (peer-write, no collective call).
+ * Each rank holds v_gathered [tp_size][n_tokens][rs] fp32 and a flag array of
+ * tp_size uint32 (zero-initialised), both in memory every rank can address
+ * (CUDA IPC / symmetric memory over NVLink; peer_*[d] = rank d's copy).
+ * shrink_push stores this rank's v rows straight into every rank's
+ * v_gathered (block tp_rank) as they are produced; its last CTA then adds 1
+ * to slot tp_rank of every rank's flag array (release, system scope).
+ * expand_wait waits until every slot of the local flag array is >= 1
+ * (acquire), expands, and its last CTA takes 1 from every slot — so the
+ * protocol is the same on every call and CUDA-graph replays are safe.  A
+ * rank's v_gathered may be rewritten by a peer's next call once that peer
+ * passed this rank's expand: callers alternate two buffers by call parity
+ * (an even number of calls per captured graph).  tp_size <= 8. */
+int plora_bgmv_tp_shrink_push(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
+                              uint32_t tp_size, const void* x, uint64_t x_stride,
+                              float* const* peer_v_gathered, uint32_t* const* peer_flags,
+                              plora_stream_t stream);
+int plora_bgmv_tp_expand_wait(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
+                              uint32_t tp_size, const float* v_gathered, uint32_t* flags,
+                              void* y_shard, uint64_t y_stride, float scale, plora_stream_t stream);
 
 /* ------------------------------------ loading / prefetch engine (new) -----
  * The reference simulator's residency control restated on CUDA streams and

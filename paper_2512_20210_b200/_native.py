@@ -262,6 +262,9 @@ _SIGS = {
     "plora_tp_shard_rows": (_u32, [_vp, _u32]),
     "plora_bgmv_tp_shrink": (_int, [_vp, _u32, _u32, _u32, _u32, _vp, _u64, _vp, _vp]),
     "plora_bgmv_tp_expand": (_int, [_vp, _u32, _u32, _u32, _u32, _vp, _vp, _u64, C.c_float, _vp]),
+    "plora_bgmv_tp_shrink_push": (_int, [_vp, _u32, _u32, _u32, _u32, _vp, _u64, _vp, _vp, _vp]),
+    "plora_bgmv_tp_expand_wait": (_int, [_vp, _u32, _u32, _u32, _u32, _vp, _vp, _vp, _u64,
+                                         C.c_float, _vp]),
     "plora_debug_set_trace": (_int, [_vp, _u64]),
     "plora_debug_set_bgmv_impl": (_int, [C.c_int]),
     "plora_debug_set_bgmv_flags": (_int, [_u32]),

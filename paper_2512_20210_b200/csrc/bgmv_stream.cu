@@ -94,6 +94,13 @@ struct SArgs {
   uint32_t tp, tp_size, tp_T, tp_rsmax;
   float* tp_v;
   const float* tp_vg;
+  // fused peer-write all-gather (StreamTp): shrink destinations and flags,
+  // expand wait
+  uint32_t tp_ndst;
+  float* tp_dst[kMaxTp];
+  uint32_t* tp_flags[kMaxTp];
+  uint32_t* tp_done;
+  uint32_t* tp_wait;  // [tp_size] per-source arrivals (expand)
 };
 
 constexpr uint32_t kTraceStages = 512;
@@ -229,6 +236,12 @@ __device__ void producer(const SArgs& p, char* smem, uint32_t pw) {
     ptx::cp_async_commit();
   }
   ptx::pdl_wait();  // activations, v planes and counters belong to the previous call until here
+  if (p.tp_wait) {  // fused all-gather: every rank's v rows of this call have landed
+    if (lane == 0)
+      for (uint32_t r = 0; r < p.tp_size; ++r)
+        while (ptx::ld_acquire_sys(p.tp_wait + r) == 0u) __nanosleep(128);
+    __syncwarp();
+  }
   uint32_t ph = 0, g = 0;  // parity of this warp's slot; global stage number
   // L2 prefetch of this warp's stages kPf items ahead: DRAM -> L2 runs that
   // far ahead of the shared-memory ring, whose depth the smem budget caps
@@ -333,8 +346,8 @@ __device__ void producer(const SArgs& p, char* smem, uint32_t pw) {
 #pragma unroll
             for (uint32_t q = 0; q < 2; ++q) {
               const uint32_t j = st * kWRows + 2 * rp + q;
-              v2[q] = (j < it.rank && t < it.ntok)
-                          ? __ldg(p.tp_vg + (static_cast<uint64_t>(j / rs) * p.tp_T + rw[8 + t]) * p.tp_rsmax + j % rs)
+              v2[q] = (j < it.rank && t < it.ntok)  // L2 (peers write it during the call's lifetime)
+                          ? __ldcg(p.tp_vg + (static_cast<uint64_t>(j / rs) * p.tp_T + rw[8 + t]) * p.tp_rsmax + j % rs)
                           : 0.f;
             }
             const __nv_bfloat16 h0 = __float2bfloat16_rn(v2[0]), h1 = __float2bfloat16_rn(v2[1]);
@@ -639,7 +652,11 @@ __device__ void publisher(const SArgs& p, char* smem) {
         float vv = 0.f;
 #pragma unroll
         for (uint32_t ww = 0; ww < kCWarps; ++ww) vv += pb[ww * kWRows * JT + e];
-        if (t < ntok && r < rows) p.tp_v[static_cast<uint64_t>(meta[8 + t]) * p.tp_rsmax + vbase + r] = vv;
+        if (t < ntok && r < rows) {
+          const uint64_t o = static_cast<uint64_t>(meta[8 + t]) * p.tp_rsmax + vbase + r;
+          if (p.tp_v) p.tp_v[o] = vv;
+          for (uint32_t d = 0; d < p.tp_ndst; ++d) p.tp_dst[d][o] = vv;  // peer stores over NVLink
+        }
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&pfree[pbuf]);
@@ -694,6 +711,21 @@ __global__ void __launch_bounds__(Slot<JT>::threads, 1) bgmv_stream_kernel(const
     producer<JT>(p, smem, (threadIdx.x - kCThreads) >> 5);
   else
     consumers<JT>(p, smem);
+  if (p.tp_ndst || p.tp_wait) {  // fused all-gather: the last CTA to finish signals
+    __syncthreads();  // this CTA's peer stores (or flag reads) precede thread 0's atomic
+    if (threadIdx.x == 0) {
+      if (p.tp_ndst) ptx::fence_acq_rel_sys();  // the peer stores, before this CTA's count
+      if (atomicAdd(p.tp_done, 1u) + 1 == gridDim.x) {
+        *p.tp_done = 0u;  // for the next call (stream-ordered after this grid)
+        if (p.tp_ndst) {  // shrink: one arrival in this rank's slot of every rank's flags
+          ptx::fence_acq_rel_sys();  // every CTA's stores (observed through the count) first
+          for (uint32_t d = 0; d < p.tp_ndst; ++d) ptx::red_release_sys_add(p.tp_flags[d], 1u);
+        }
+        if (p.tp_wait)  // expand: consume this call's arrival from every source
+          for (uint32_t r = 0; r < p.tp_size; ++r) ptx::red_relaxed_sys_add(p.tp_wait + r, 0xffffffffu);
+      }
+    }
+  }
 }
 
 uint32_t g_stream_dbg = 0;
@@ -748,6 +780,13 @@ void launch_jt(const plora_plan& plan, const StreamWork& w, uint32_t layer0, uin
     a.tp_rsmax = tp->rs_max;
     a.tp_v = tp->v_out;
     a.tp_vg = tp->v_in;
+    a.tp_ndst = tp->n_dst;
+    for (uint32_t d = 0; d < tp->n_dst; ++d) {
+      a.tp_dst[d] = tp->dst[d];
+      a.tp_flags[d] = tp->flags[d];
+    }
+    a.tp_done = tp->done;
+    a.tp_wait = tp->wait;
   }
   a.x = static_cast<const char*>(x);
   a.x_stride_b = x_stride * 2;

@@ -161,6 +161,7 @@ struct StreamItem {  // 64 bytes, fully resolved on the host
 };
 static_assert(sizeof(StreamItem) == 64, "StreamItem layout");
 
+constexpr uint32_t kMaxTp = 8;  // TP ranks of the fused peer-write all-gather
 struct StreamTp {  // a tensor-parallel half on the streaming kernel (tp.cu)
   uint32_t mode;      // 1 shrink (S items; v -> v_out), 2 expand (E items; v from v_in)
   uint32_t tp_size, n_tokens, rs_max;
@@ -168,6 +169,16 @@ struct StreamTp {  // a tensor-parallel half on the streaming kernel (tp.cu)
   const float* v_in;
   const StreamItem* items;
   const uint32_t* cta_off;
+  // fused all-gather.  Shrink: v rows also go straight into every rank's
+  // gathered buffer (peer memory; rank block already applied), then the last
+  // CTA adds 1 to this rank's slot of every rank's flag array.  Expand: wait
+  // until every slot of the local flag array is >= 1, and the last CTA takes
+  // 1 from each (consumed: graph replays see the same protocol).
+  uint32_t n_dst;
+  float* dst[kMaxTp];
+  uint32_t* flags[kMaxTp];  // shrink: &flag_array_of_rank_d[tp_rank]
+  uint32_t* done;           // this launch's CTA-completion counter (zero between calls)
+  uint32_t* wait;           // expand: the local flag array [tp_size]
 };
 
 struct StreamWork {  // one launch variant (a projection, or every projection of a layer)
@@ -292,6 +303,7 @@ struct plora_plan {
     plora::StreamWork w;
     plora::StreamItem* d_items = nullptr;  // items, then the CTA offsets
     uint32_t* d_cta = nullptr;
+    uint32_t* d_done = nullptr;            // fused all-gather: CTAs of the shrink done (zero between calls)
     char* h_stage = nullptr;               // pinned source of the upload
   };
   std::map<uint64_t, TpWork> tpw;

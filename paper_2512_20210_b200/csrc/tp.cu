@@ -39,6 +39,7 @@
 #include <queue>
 
 #include "plan.hpp"
+#include "ptx.cuh"
 
 using namespace plora;
 
@@ -147,15 +148,80 @@ plora_plan::TpWork& tp_work(plora_plan& plan, uint32_t proj, uint32_t tp_rank, u
   w.w.projs[0] = proj;
   const uint64_t ib = items.size() * sizeof(StreamItem), cb = cta_off.size() * sizeof(uint32_t);
   DeviceCtx ctx(plan.store->device);
-  PLORA_CUDA(cudaMalloc(&w.d_items, ib + cb));
+  // items, CTA offsets, then the fused all-gather's CTA-completion counter
+  const uint64_t db = (ib + cb + 15) / 16 * 16;
+  PLORA_CUDA(cudaMalloc(&w.d_items, db + 16));
   w.d_cta = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(w.d_items) + ib);
-  PLORA_CUDA(cudaMallocHost(&w.h_stage, ib + cb));
+  w.d_done = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(w.d_items) + db);
+  PLORA_CUDA(cudaMallocHost(&w.h_stage, db + 16));
+  std::memset(w.h_stage, 0, db + 16);
   std::memcpy(w.h_stage, items.data(), ib);
   std::memcpy(w.h_stage + ib, cta_off.data(), cb);
-  PLORA_CUDA(cudaMemcpyAsync(w.d_items, w.h_stage, ib + cb, cudaMemcpyHostToDevice, stream));
+  PLORA_CUDA(cudaMemcpyAsync(w.d_items, w.h_stage, db + 16, cudaMemcpyHostToDevice, stream));
   return plan.tpw.emplace(key, w).first->second;
 }
 
+struct TpFlags {
+  uint32_t* flags[kMaxTp];
+  uint32_t n;
+};
+// A rank with no LoRA token still completes its share of the fused all-gather.
+__global__ void tp_flag_bump_kernel(const TpFlags f) {
+  if (threadIdx.x < f.n) ptx::red_release_sys_add(f.flags[threadIdx.x], 1u);
+}
+
+__global__ void tp_flag_consume_kernel(uint32_t* flags, uint32_t n) {
+  if (threadIdx.x < n) {
+    while (ptx::ld_acquire_sys(flags + threadIdx.x) == 0u) __nanosleep(128);
+    ptx::red_relaxed_sys_add(flags + threadIdx.x, 0xffffffffu);
+  }
+}
+
+}  // namespace
+
+// One rank's expand; flags != nullptr: first wait for the fused all-gather
+// (every rank's shrink_push of this call has added 1 to its slot), and
+// consume those arrivals at the end.
+namespace {
+int tp_expand(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank, uint32_t tp_size,
+              const float* v_gathered, uint32_t* flags, void* y_shard, uint64_t y_stride, float scale,
+              plora_stream_t stream) {
+  if (!plan) throw ValidationError("null plan");
+  const TpGeom tg = tp_check(*plan, layer, proj, tp_rank, tp_size);
+  if (plan->cjobs.empty()) {
+    if (flags) {  // no LoRA token: still take this call's arrivals
+      if (tp_size > kMaxTp) throw ValidationError("fused all-gather: tp_size > " + std::to_string(kMaxTp));
+      DeviceCtx ctx(plan->store->device);
+      tp_flag_consume_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(flags, tp_size);
+      PLORA_CUDA(cudaGetLastError());
+      count_launch();
+    }
+    return 0;
+  }
+  if (!v_gathered || !y_shard) throw ValidationError("null v_gathered or y_shard");
+  if (y_stride < tg.ncols || y_stride % 8 || reinterpret_cast<uintptr_t>(y_shard) % 16)
+    throw ValidationError("y_shard must be 16-byte aligned with a row stride >= d_out/tp_size, multiple of 8");
+  DeviceCtx ctx(plan->store->device);
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const plora_plan::TpWork& w = tp_work(*plan, proj, tp_rank, tp_size, 2, tg, s);
+  StreamTp tp{};
+  tp.mode = 2;
+  tp.tp_size = tp_size;
+  tp.n_tokens = plan->n_tokens;
+  tp.rs_max = tg.rs_max;
+  tp.v_in = v_gathered;
+  tp.items = w.d_items;
+  tp.cta_off = w.d_cta;
+  // the kernel addresses output column c (absolute in d_out) at y + c
+  char* y = static_cast<char*>(y_shard) - static_cast<ptrdiff_t>(tg.col0) * 2;
+  if (flags) {
+    if (tp_size > kMaxTp) throw ValidationError("fused all-gather: tp_size > " + std::to_string(kMaxTp));
+    tp.wait = flags;
+    tp.done = w.d_done;
+  }
+  launch_bgmv_stream_tp(*plan, w.w, tp, layer, nullptr, 0, y, y_stride, scale, s);
+  return 0;
+}
 }  // namespace
 
 extern "C" {
@@ -191,31 +257,65 @@ int plora_bgmv_tp_shrink(plora_plan* plan, uint32_t layer, uint32_t proj, uint32
   });
 }
 
+int plora_bgmv_tp_shrink_push(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
+                              uint32_t tp_size, const void* x, uint64_t x_stride,
+                              float* const* peer_v_gathered, uint32_t* const* peer_flags,
+                              plora_stream_t stream) {
+  return guard([&] {
+    if (!plan) throw ValidationError("null plan");
+    const TpGeom tg = tp_check(*plan, layer, proj, tp_rank, tp_size);
+    if (tp_size > kMaxTp) throw ValidationError("fused all-gather: tp_size > " + std::to_string(kMaxTp));
+    if (!peer_v_gathered || !peer_flags) throw ValidationError("null peer buffers");
+    for (uint32_t d = 0; d < tp_size; ++d)
+      if (!peer_v_gathered[d] || !peer_flags[d]) throw ValidationError("null peer buffer " + std::to_string(d));
+    if (!x) throw ValidationError("null x");
+    if (x_stride < tg.d_in || x_stride % 8 || reinterpret_cast<uintptr_t>(x) % 16)
+      throw ValidationError("x must be 16-byte aligned with a row stride >= d_in, multiple of 8");
+    DeviceCtx ctx(plan->store->device);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    StreamTp tp{};
+    tp.mode = 1;
+    tp.tp_size = tp_size;
+    tp.n_tokens = plan->n_tokens;
+    tp.rs_max = tg.rs_max;
+    tp.n_dst = tp_size;
+    const uint64_t block = static_cast<uint64_t>(tp_rank) * plan->n_tokens * tg.rs_max;  // this rank's rows
+    for (uint32_t d = 0; d < tp_size; ++d) {
+      tp.dst[d] = peer_v_gathered[d] + block;
+      tp.flags[d] = peer_flags[d] + tp_rank;  // this rank's slot of rank d's flag array
+    }
+    if (plan->cjobs.empty()) {  // nothing to write: still tell every rank this call is done
+      TpFlags f{};
+      f.n = tp_size;
+      for (uint32_t d = 0; d < tp_size; ++d) f.flags[d] = peer_flags[d] + tp_rank;
+      tp_flag_bump_kernel<<<1, 32, 0, s>>>(f);
+      PLORA_CUDA(cudaGetLastError());
+      count_launch();
+      return 0;
+    }
+    const plora_plan::TpWork& w = tp_work(*plan, proj, tp_rank, tp_size, 1, tg, s);
+    tp.items = w.d_items;
+    tp.cta_off = w.d_cta;
+    tp.done = w.d_done;
+    launch_bgmv_stream_tp(*plan, w.w, tp, layer, x, x_stride, nullptr, 0, 1.f, s);
+    return 0;
+  });
+}
+
+int plora_bgmv_tp_expand_wait(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
+                              uint32_t tp_size, const float* v_gathered, uint32_t* flags,
+                              void* y_shard, uint64_t y_stride, float scale, plora_stream_t stream) {
+  return guard([&] {
+    if (!flags) throw ValidationError("null flags");
+    return tp_expand(plan, layer, proj, tp_rank, tp_size, v_gathered, flags, y_shard, y_stride, scale, stream);
+  });
+}
+
 int plora_bgmv_tp_expand(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
                          uint32_t tp_size, const float* v_gathered, void* y_shard,
                          uint64_t y_stride, float scale, plora_stream_t stream) {
   return guard([&] {
-    if (!plan) throw ValidationError("null plan");
-    const TpGeom tg = tp_check(*plan, layer, proj, tp_rank, tp_size);
-    if (plan->cjobs.empty()) return 0;
-    if (!v_gathered || !y_shard) throw ValidationError("null v_gathered or y_shard");
-    if (y_stride < tg.ncols || y_stride % 8 || reinterpret_cast<uintptr_t>(y_shard) % 16)
-      throw ValidationError("y_shard must be 16-byte aligned with a row stride >= d_out/tp_size, multiple of 8");
-    DeviceCtx ctx(plan->store->device);
-    const cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const plora_plan::TpWork& w = tp_work(*plan, proj, tp_rank, tp_size, 2, tg, s);
-    StreamTp tp{};
-    tp.mode = 2;
-    tp.tp_size = tp_size;
-    tp.n_tokens = plan->n_tokens;
-    tp.rs_max = tg.rs_max;
-    tp.v_in = v_gathered;
-    tp.items = w.d_items;
-    tp.cta_off = w.d_cta;
-    // the kernel addresses output column c (absolute in d_out) at y + c
-    char* y = static_cast<char*>(y_shard) - static_cast<ptrdiff_t>(tg.col0) * 2;
-    launch_bgmv_stream_tp(*plan, w.w, tp, layer, nullptr, 0, y, y_stride, scale, s);
-    return 0;
+    return tp_expand(plan, layer, proj, tp_rank, tp_size, v_gathered, nullptr, y_shard, y_stride, scale, stream);
   });
 }
 

@@ -68,3 +68,77 @@ def test_tp_module_single_rank_and_errors(setup70):
         bgmv_tp_shrink(plan, 0, 0, 0, 16, x, torch.empty(T, 8, dtype=torch.float32, device="cuda"))
     with pytest.raises(ValidationError):
         bgmv_tp_shrink(plan, 0, 0, 3, 2, x, torch.empty(T, 64, dtype=torch.float32, device="cuda"))
+
+
+@pytest.mark.parametrize("tp_size", [1, 2, 4, 8])
+def test_fused_allgather_emulated_ranks_bit_identical(setup70, tp_size):
+    """The peer-write all-gather (plora_bgmv_tp_shrink_push / _expand_wait):
+    N ranks emulated in one process, each with its own pair of gathered
+    buffers and arrival flags, every rank's shrink storing into all of them.
+    Three calls (buffer parities 0, 1, 0) must equal the unfused halves bit
+    for bit, and leave every flag at zero (arrivals consumed)."""
+    from paper_2512_20210_b200.tp import bgmv_tp_expand_wait, bgmv_tp_shrink_push
+    s = setup70
+    cfg = s.cfg
+    ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
+    T = len(ta)
+    plan = BatchPlan(s.store, ta)
+    rs = tp_shard_rows(plan, tp_size)
+    vg = [torch.zeros(2, tp_size, T, rs, dtype=torch.float32, device="cuda") for _ in range(tp_size)]
+    flags = [torch.zeros(tp_size, dtype=torch.int32, device="cuda") for _ in range(tp_size)]
+    for call, (layer, proj) in enumerate(((0, 0), (1, 1), (1, 0))):
+        din, dout = cfg.shape.d_in[proj], cfg.shape.d_out[proj]
+        ncols = dout // tp_size
+        x = synth.activations(T, din, torch.bfloat16, "x", salt=call).cuda()
+        y0 = synth.activations(T, dout, torch.bfloat16, "y", salt=call).cuda()
+        par = call & 1
+        y_f, y_u = y0.clone(), y0.clone()
+        for r in range(tp_size):
+            bgmv_tp_shrink_push(plan, layer, proj, r, tp_size, x, [vg[d][par].data_ptr() for d in range(tp_size)],
+                                [flags[d].data_ptr() for d in range(tp_size)])
+        for r in range(tp_size):
+            bgmv_tp_expand_wait(plan, layer, proj, r, tp_size, vg[r][par], flags[r],
+                                y_f[:, r * ncols:(r + 1) * ncols], 0.5)
+        parts = [bgmv_tp_shrink(plan, layer, proj, r, tp_size, x,  # (zeros: rows past r/N stay unwritten)
+                                torch.zeros(T, rs, dtype=torch.float32, device="cuda")) for r in range(tp_size)]
+        vu = torch.stack(parts).contiguous()
+        for r in range(tp_size):
+            bgmv_tp_expand(plan, layer, proj, r, tp_size, vu, y_u[:, r * ncols:(r + 1) * ncols], 0.5)
+        torch.cuda.synchronize()
+        for r in range(tp_size):  # every rank's gathered buffer holds every rank's rows
+            assert torch.equal(vg[r][par], vu), (call, r)
+        assert torch.equal(y_f, y_u), call
+        assert all(int(f.abs().sum()) == 0 for f in flags)
+
+
+def test_fused_allgather_module_tp1_and_graph(setup70):
+    s = setup70
+    ta = synth.token_assignment(s.cfg.n_adapters, s.cfg.tokens_per_adapter)
+    plan = BatchPlan(s.store, ta)
+    T = len(ta)
+    x = synth.activations(T, 8192, torch.bfloat16, "x").cuda()
+    y0 = synth.activations(T, 8192, torch.bfloat16, "y").cuda()
+    fused = TensorParallelLoRA(plan, 0, 1, force_split=True, allgather="fused")
+    plain = TensorParallelLoRA(plan, 0, 1, force_split=True)
+    ya, yb = y0.clone(), y0.clone()
+    for layer in (0, 1):
+        fused(layer, 0, x, ya)
+        plain(layer, 0, x, yb)
+    torch.cuda.synchronize()
+    assert torch.equal(ya, yb)
+    # a captured step of two calls (even: the buffer parity repeats per replay)
+    yg = y0.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fused(0, 0, x, yg)
+        fused(1, 0, x, yg)
+    yg.copy_(y0)
+    g.replay()
+    g.replay()
+    yc = y0.clone()
+    for _ in range(2):
+        for layer in (0, 1):
+            plain(layer, 0, x, yc)
+    torch.cuda.synchronize()
+    assert torch.equal(yg, yc)
+    assert int(fused._ff.abs().sum()) == 0
