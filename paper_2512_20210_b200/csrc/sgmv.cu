@@ -244,7 +244,16 @@ __global__ void __launch_bounds__(kSThreads, 1)
         // Groups of four real rows go by one TMA gather4 (its row indices
         // collected by the group's first lane); padding rows and the rows of
         // a partial last group by 16-byte cp.async.
-        const bool g4 = p.g4 && (n | 3u) < u.r;
+        // Every other group of four goes by cp.async instead: the TMA unit
+        // (gather4 moves 512 B per op) and the LSU pipes then share the rows
+        // (profiles/r02l_sgmv_g4_split.txt: shrink 60.2 -> 54.4 us at cfg3).
+        // Diagnostics: 16384 all by gather4, 4096 one in four by cp.async,
+        // 8192 three in four, 2048 all.
+        const uint32_t gi = (n >> 2) & 3u;
+        const bool by_lsu = (p.dbg & 2048u) || ((p.dbg & 4096u) ? gi == 3u
+                                               : (p.dbg & 8192u) ? gi != 0u
+                                               : !(p.dbg & 16384u) && (gi & 1u));
+        const bool g4 = p.g4 && (n | 3u) < u.r && !by_lsu;
         if (p.g4 && !(p.dbg & 1u)) {
 #pragma unroll
           for (uint32_t q = 0; q < 2; ++q) {
