@@ -354,8 +354,7 @@ __device__ void producer(const SArgs& p, char* smem, uint32_t pw) {
             vw[e] = part ? pack_bf16x2(v2[0] - __bfloat162float(h0), v2[1] - __bfloat162float(h1))
                          : (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16) | __bfloat16_as_ushort(h0);
           }
-          __threadfence_block();  // ordered before lane 0's arrival on the slot's full barrier
-          __syncwarp();
+          if (lane != 0) ptx::mbar_arrive(&full[pw]);  // each lane releases its own words (count 32)
         } else {
           if (lane == 24)
             ptx::bulk_g2s(sb + Slot<JT>::vrows,
@@ -401,10 +400,8 @@ __device__ void producer(const SArgs& p, char* smem, uint32_t pw) {
   // the stop marker goes to the owner of stage g
   if (g % kPW == pw) {
     ptx::mbar_wait(&empty[pw], ph ^ 1u);
-    if (lane == 0) {
-      hdr[0] = kStop;
-      ptx::mbar_arrive(&full[pw]);
-    }
+    if (lane == 0) hdr[0] = kStop;
+    if (lane == 0 || p.tp == 2) ptx::mbar_arrive(&full[pw]);  // (TP expand: the full count is 32)
   }
   cp_async_wait_group<0>();
 }
@@ -694,7 +691,7 @@ __global__ void __launch_bounds__(Slot<JT>::threads, 1) bgmv_stream_kernel(const
   if (threadIdx.x == 0) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.off_bar);
     for (uint32_t s = 0; s < p.nslots; ++s) {
-      ptx::mbar_init(&full[s], 1);             // the slot's producer warp (+ tx bytes)
+      ptx::mbar_init(&full[s], p.tp == 2 ? 32 : 1);  // the slot's producer (every lane in TP expand) + tx
       ptx::mbar_init(&full[p.nslots + s], kCThreads);  // empty: every consumer thread's release
     }
     for (uint32_t b = 0; b < kPubBufs<JT>; ++b) {

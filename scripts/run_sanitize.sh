@@ -4,5 +4,3 @@ for tool in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize.py > gpurun_out/sanitize_$tool.log 2>&1
   echo "$tool rc=$?" >> gpurun_out/sanitize_$tool.log
 done
-timeout 300 python -m pytest tests/test_lora_gpu.py -q -x -k streaming > gpurun_out/t.log 2>&1
-timeout 300 python scripts/stream_ablate.py > gpurun_out/ablate.txt 2>&1

@@ -1,8 +1,9 @@
 """Small paged-LoRA calls for compute-sanitizer (memcheck / racecheck /
 synccheck): the cluster BGMV (per projection, fused per layer, multi-layer),
 the streaming BGMV (4- and 8-token jobs), the SGMV (per projection, per layer,
-fused with the base GEMM, 512 B and 1 KiB pages), the TP halves, the GPU
-predict_all and a host-store-fed engine on small stores.
+fused with the base GEMM, 512 B and 1 KiB pages), the TP halves (NCCL-style
+and with the fused peer-write all-gather), decode batches with a routed
+many-token adapter, and the GPU predict_all.
 
 compute-sanitizer --tool memcheck python scripts/sanitize.py
 """
@@ -77,6 +78,27 @@ def main():
         sgmv_fused(pf, 1, 0, xx, torch.randn(1024, 1024, device="cuda").to(torch.bfloat16),
                    torch.empty(len(sg), 1024, device="cuda", dtype=torch.bfloat16))
         sgmv(pf, 1, 1, xx, torch.randn(len(sg), 512, device="cuda").to(torch.bfloat16))
+    # many-token adapters routed to the SGMV path (child plan, second stream)
+    import numpy as np
+    N.check(N.lib().plora_debug_set_route_tokens(16))
+    tr = np.concatenate([np.full(20, 1, np.int32), np.arange(2, cfg.n_adapters, dtype=np.int32)])
+    xr = torch.randn(len(tr), 4096, device="cuda").to(torch.bfloat16)
+    yr = [torch.randn(len(tr), 4096, device="cuda").to(torch.bfloat16) for _ in range(2)]
+    pr = BatchPlan(s.store, tr)
+    bgmv(pr, 1, 0, xr, yr[0])
+    bgmv_layer(pr, 0, xr, yr)
+    xrl = torch.randn(2, len(tr), 4096, device="cuda").to(torch.bfloat16)
+    yrl = torch.randn(2, 2, len(tr), 4096, device="cuda").to(torch.bfloat16)
+    bgmv_layers(pr, 0, xrl, [yrl[:, 0], yrl[:, 1]])
+    N.check(N.lib().plora_debug_set_route_tokens(48))
+    # TP halves with the fused peer-write all-gather, two emulated ranks
+    from paper_2512_20210_b200.tp import bgmv_tp_expand_wait, bgmv_tp_shrink_push
+    vgs = [torch.zeros(2, T, rs, device="cuda") for _ in range(2)]
+    fl = [torch.zeros(2, dtype=torch.int32, device="cuda") for _ in range(2)]
+    for i in range(2):
+        bgmv_tp_shrink_push(plan, 0, 1, i, 2, x, [v.data_ptr() for v in vgs], [f.data_ptr() for f in fl])
+    for i in range(2):
+        bgmv_tp_expand_wait(plan, 0, 1, i, 2, vgs[i], fl[i], ys[1][:, i * 2048:(i + 1) * 2048])
     # predict_all on the GPU
     from paper_2512_20210_b200.predictor import OnlinePredictor, OnlinePredictorConfig, PredictorConfig
     pred = OnlinePredictor(OnlinePredictorConfig(model=PredictorConfig(num_adapters=50),
