@@ -25,10 +25,7 @@ plan = BatchPlan(store, synth.segment_assignment(32, 512))
 x = torch.randn(32 * 512, 4096, device="cuda").to(torch.bfloat16)
 ys = [torch.randn(32 * 512, 4096, device="cuda").to(torch.bfloat16) for _ in range(2)]
 for g4 in (16384, 4096, 0, 8192, 2048):  # 0 = the default (half by cp.async)
-    for name, extra in (("layer call", 0), ("shrink only", 40), ("shrink no A", 41), ("shrink no x", 44),
-                        ("shrink no MMA", 42), ("shrink no epi", 56), ("shrink nothing", 63)):
-        if g4 and extra not in (0, 40):
-            continue
+    for name, extra in (("layer call", 0), ("shrink only", 40), ("expand no y", 64), ("expand no B", 128)):
         N.check(N.lib().plora_debug_set_sgmv_flags(g4 | extra))
         for _ in range(3):
             sgmv_layer(plan, 1, x, ys)
