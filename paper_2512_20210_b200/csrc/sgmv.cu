@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(kEThreads, 2)
       ptx::mbar_init(&b_full[i], kEGather);
       ptx::mbar_init(&b_empty[i], 1);
       ptx::mbar_init(&acc_full[i], 1);
-      ptx::mbar_init(&acc_empty[i], 1);
+      ptx::mbar_init(&acc_empty[i], kEEpiThreads / 32);  // each epilogue warp, once its TMEM reads are done
     }
     ptx::fence_mbar_init();
   }
@@ -664,29 +664,34 @@ __global__ void __launch_bounds__(kEThreads, 2)
       }
       ptx::mbar_wait(&acc_full[st], ph);
       ptx::tc_fence_after();
-#pragma unroll 1
+      // the warp's 32 rows × 64 columns in one TMEM round trip, then the
+      // accumulator goes back to the MMA warp before the smem writes
+      uint32_t rv[kEBlockN / 16][16];
+#pragma unroll
+      for (uint32_t q = 0; q < kEBlockN / 16; ++q)
+        ptx::tmem_ld_32x32b_x16(tmem + lane_base + st * kEBlockN + q * 16, rv[q]);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[st]);  // one arrival per epilogue warp
+#pragma unroll
       for (uint32_t q = 0; q < kEBlockN / 16; ++q) {  // 16 columns = two 16-byte chunks
-        uint32_t rv[16];
-        ptx::tmem_ld_32x32b_x16(tmem + lane_base + st * kEBlockN + q * 16, rv);
-        ptx::tmem_ld_wait();
 #pragma unroll
         for (uint32_t hh = 0; hh < 2; ++hh) {
           const uint32_t ya = ptx::smem_u32(ys + swz(m, q * 2 + hh));
           uint32_t o[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            o[i] = live ? pack_bf16x2(p.scale * __uint_as_float(rv[hh * 8 + 2 * i]),
-                                      p.scale * __uint_as_float(rv[hh * 8 + 2 * i + 1]))
+            o[i] = live ? pack_bf16x2(p.scale * __uint_as_float(rv[q][hh * 8 + 2 * i]),
+                                      p.scale * __uint_as_float(rv[q][hh * 8 + 2 * i + 1]))
                         : 0x80008000u;  // bf16 -0.0: the exact additive identity of the reduce-add
           asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ya), "r"(o[0]), "r"(o[1]),
                        "r"(o[2]), "r"(o[3]) : "memory");
         }
       }
-      ptx::tc_fence_before();
       ptx::fence_proxy_async_shared();  // generic-proxy smem writes -> TMA
       ptx::named_bar_sync(1, kEEpiThreads);
       if (warp == 4 && lane == 0) {
-        ptx::mbar_arrive(&acc_empty[st]);
         if (!(p.dbg & 64u)) ptx::tma_reduce_add_2d(tmap_y, static_cast<int32_t>(col0), static_cast<int32_t>(tile.row0), ys);
         ptx::bulk_commit();
       }
