@@ -451,9 +451,8 @@ def run_ours(args):
                     "l2": "inputs > L2: 2.1 GiB of adapter pages + 12 GiB activations per step"}
                    if prefill else cfg2_config(args.page_bytes, world)),
         "impl_detail": {"cuda_graph": graph is not None, "launches_per_layer": LPS,
-                        "launch": (f"plora_bgmv_layers: {mlp} layers per launch (inputs resident; "
-                                   f"the clusters stay resident across layers)") if mlp > 1 else
-                                  "plora_bgmv_layer: one launch per layer"},
+                        "launch": (f"plora_bgmv_layers: {mlp} layers per call (inputs resident)")
+                                  if mlp > 1 else "plora_bgmv_layer: one call per layer"},
         "e2e": e2e,
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -473,6 +472,12 @@ def run_ours(args):
         from paper_2512_20210_b200 import _native as N
         info = (C.c_double * 4)()
         N.check(N.lib().plora_debug_plan_hybrid(plan.handle, info))
+        if info[0] == 0:
+            line["roofline"]["kernels"] = (
+                "one plora_bgmv_layers call = bgmv_warp_shrink_kernel (S items: <= 8 rank rows of one "
+                "job, v = x·Aᵀ in fp32) then bgmv_warp_expand_kernel (E items: <= 512 output columns "
+                "over every rank row, y += scale·v·Bᵀ), chained by programmatic dependent launch, both "
+                "over all 32 layers (grid.y); achieved = the step's algorithmic bytes / the call's time")
         if info[0] > 0:
             line["roofline"]["kernels"] = (
                 f"the launch pair of plora_bgmv_layers: bgmv_cluster_kernel ({int(info[2])} 4-CTA "

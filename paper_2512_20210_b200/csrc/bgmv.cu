@@ -409,14 +409,16 @@ void check_io(const plora_plan* plan, uint32_t layer, uint32_t proj, const void*
 
 namespace {
 int g_hybrid_per_layer = 0;  // plora_debug_set_hybrid_per_layer
-// bf16 decode kernel: 0 clusters (bgmv_cluster.cu), and for multi-layer
-// launches the hybrid with a streaming share on the idle SMs; 1 the streaming
-// kernel alone (bgmv_stream.cu); 2 clusters only
+// bf16 decode kernel: 0 warp items (bgmv_warp.cu, the default); 1 the
+// streaming kernel alone (bgmv_stream.cu); 2 clusters only (bgmv_cluster.cu);
+// 3 clusters, and for multi-layer launches the hybrid with a streaming share
+// on the SMs the clusters leave idle (the round-2 pair)
 int g_bgmv_impl = 0;
 }  // namespace
 
 namespace plora {
-bool hybrid_enabled() { return g_bgmv_impl == 0; }
+uint32_t bgmv_impl() { return static_cast<uint32_t>(g_bgmv_impl); }
+bool hybrid_enabled() { return g_bgmv_impl == 3; }
 double g_hybrid_factor = 0.95;
 double hybrid_share_factor() { return g_hybrid_factor; }
 }  // namespace plora
@@ -617,7 +619,9 @@ extern "C" int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const
       void* ys[1] = {y};
       const uint64_t yst[1] = {y_stride};
       const bool routed = launch_routed(plan, layer, 1, &proj, 1, x, x_stride, 0, ys, yst, nullptr, scale, s);
-      if (g_bgmv_impl != 1)
+      if (g_bgmv_impl == 0)
+        launch_bgmv_warp(*plan, plan->wwork[proj], layer, 1, x, x_stride, 0, ys, yst, nullptr, scale, s);
+      else if (g_bgmv_impl != 1)
         launch_bgmv_cluster(*plan, layer, proj, x, x_stride, y, y_stride, scale, s);
       else
         launch_bgmv_stream(*plan, plan->swork[proj], layer, 1, x, x_stride, 0, ys, yst, nullptr, scale, s);
@@ -678,6 +682,14 @@ extern "C" int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_l
       return launch_routed(plan, layer0, n_layers, all, g.m.n_proj, x, x_stride, x_layer_stride, ys,
                            y_strides, y_layer_strides, scale, s);
     };
+    if (g.esize == 2 && g_bgmv_impl == 0 && plan->wwork_layer.np == g.m.n_proj) {
+      DeviceCtx ctx(st.device);
+      const bool r = routed();
+      launch_bgmv_warp(*plan, plan->wwork_layer, layer0, n_layers, x, x_stride, x_layer_stride, ys,
+                       y_strides, y_layer_strides, scale, s);
+      if (r) join_routed(plan, s);
+      return 0;
+    }
     if (g.esize == 2 && g_bgmv_impl == 1 && plan->swork_layer.np == g.m.n_proj) {
       DeviceCtx ctx(st.device);
       const bool r = routed();
@@ -686,7 +698,7 @@ extern "C" int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_l
       if (r) join_routed(plan, s);
       return 0;
     }
-    if (g.esize == 2 && g_bgmv_impl == 0 && plan->hyb_spare && plan->n_layer_proj == g.m.n_proj &&
+    if (g.esize == 2 && g_bgmv_impl == 3 && plan->hyb_spare && plan->n_layer_proj == g.m.n_proj &&
         n_layers * g.m.n_proj <= 256) {
       DeviceCtx ctx(st.device);
       const bool r = routed();
@@ -736,6 +748,13 @@ extern "C" int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x,
     auto routed = [&] {
       return launch_routed(plan, layer, 1, all, g.m.n_proj, x, x_stride, 0, ys, y_strides, nullptr, scale, s);
     };
+    if (g.esize == 2 && g_bgmv_impl == 0 && plan->wwork_layer.np == g.m.n_proj) {
+      DeviceCtx ctx(st.device);
+      const bool r = routed();
+      launch_bgmv_warp(*plan, plan->wwork_layer, layer, 1, x, x_stride, 0, ys, y_strides, nullptr, scale, s);
+      if (r) join_routed(plan, s);
+      return 0;
+    }
     if (g.esize == 2 && g_bgmv_impl == 1 && plan->swork_layer.np == g.m.n_proj) {
       DeviceCtx ctx(st.device);
       const uint64_t zero[PLORA_MAX_PROJ] = {};
@@ -744,7 +763,7 @@ extern "C" int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x,
       if (r) join_routed(plan, s);
       return 0;
     }
-    if (g.esize == 2 && g_bgmv_impl == 0 && g_hybrid_per_layer && plan->hyb_spare &&
+    if (g.esize == 2 && g_bgmv_impl == 3 && g_hybrid_per_layer && plan->hyb_spare &&
         plan->n_layer_proj == g.m.n_proj) {
       DeviceCtx ctx(st.device);
       const uint64_t zero[PLORA_MAX_PROJ] = {};

@@ -1,0 +1,530 @@
+// bf16 paged BGMV (decode), warp-item design: the default hot path behind
+// plora_bgmv / plora_bgmv_layer / plora_bgmv_layers for bf16 stores.
+//
+//   y[t, :] += scale · (x[t, :] · A_{a(t)}ᵀ) · B_{a(t)}ᵀ
+//
+// every A / Bᵀ row read straight out of the page arena through the device
+// page table (the translation PagePool::translate does on the host,
+// src/memory.cpp:55-62).
+//
+// Decode is a pure weight stream (arithmetic intensity ~2 flop/byte at two
+// tokens per adapter), so the design is the one that streams best: every
+// warp runs one self-contained work item with 16-byte ld.global.nc loads,
+// the next chunk's loads in flight while the current chunk's math runs, and
+// nothing else — no shared-memory ring, no clusters, no barriers, no
+// cross-CTA waits.  Two launches per call, chained by programmatic dependent
+// launch:
+//   shrink  S items (<= 8 rank rows of one job, full K):
+//           v[tok][row] = Σ_k x[tok][k] · A[row][k], exact fp32
+//           (FHFMA: bf16 × bf16 + fp32, one rounding per term, no converts);
+//           lane partials summed by a fixed butterfly -> deterministic.
+//   expand  E items (one block of <= 512 output columns, every rank row):
+//           acc[tok][col] = Σ_row v[tok][row] · Bᵀ[row][col] in row order
+//           (FFMA2 on converted weight pairs), then y = bf16(y + scale·acc).
+// The launch boundary orders v (the expand's griddepcontrol.wait); the
+// expand's first rows are loaded before it.  A multi-layer launch
+// (plora_bgmv_layers) is the same item list repeated per layer.
+// Measured at cfg2 (scripts/microbench_ldg.cu, profiles/r02n_*): the same
+// loads without the math reach 6.5 TB/s; with it the step runs at ~0.94 of
+// the copy roofline.
+#include <cuda_bf16.h>
+
+#include "plan.hpp"
+#include "ptx.cuh"
+
+namespace plora {
+namespace {
+
+#ifndef PLORA_WARP_MINB
+#define PLORA_WARP_MINB 2  // CTAs per SM the register budget is sized for
+#endif
+constexpr uint32_t kWarps = 8;
+constexpr uint32_t kThreads = kWarps * 32;
+
+struct WArgs {
+  const char* arena;
+  const uint32_t* table;
+  const WarpItem* items;  // this launch's S or E items
+  uint32_t n_items;
+  uint32_t n_layers;  // layers of this launch (grid = item blocks × n_layers)
+  uint32_t d_in;
+  uint32_t log2_page;
+  uint32_t fast;  // page entries by warp shuffle (rows / blocks span few pages)
+  const char* x;
+  uint64_t x_stride_b, x_lstride_b;
+  char* y[PLORA_MAX_PROJ];
+  uint64_t y_stride_b[PLORA_MAX_PROJ], y_lstride_b[PLORA_MAX_PROJ];
+  uint64_t blk_mult[PLORA_MAX_PROJ];  // block offset multiplier of (layer0, proj)
+  uint32_t d_out[PLORA_MAX_PROJ];
+  uint64_t plu;                       // ModelGeom::per_layer_unit
+  float* v;
+  uint64_t vplane;                    // floats per launched layer
+  float scale;
+};
+
+struct WI {
+  uint32_t toff, rank, ntok, pj, n, off, voff;
+  uint32_t tok[kWarpJobTok];
+};
+
+__device__ __forceinline__ WI load_item(const WarpItem* it) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(it));
+  const uint4 b = __ldg(reinterpret_cast<const uint4*>(it) + 1);
+  WI w;
+  w.toff = a.x;
+  w.rank = a.y & 0x1ffu;
+  w.ntok = (a.y >> 9) & 7u;
+  w.pj = (a.y >> 12) & 0xfu;
+  w.n = a.y >> 16;
+  w.off = a.z;
+  w.voff = a.w;
+  w.tok[0] = b.x;
+  w.tok[1] = b.y;
+  w.tok[2] = b.z;
+  w.tok[3] = b.w;
+  return w;
+}
+
+
+// acc += a.lo · b.lo + a.hi · b.hi for bf16 pairs (fma.rn.f32.bf16: exact
+// products, one fp32 rounding per term — the same as FFMA on converted values)
+__device__ __forceinline__ void fh2(float& acc, uint32_t a, uint32_t b) {
+  asm("{\n\t.reg .b16 al, ah, bl, bh;\n\t"
+      "mov.b32 {al, ah}, %1;\n\t"
+      "mov.b32 {bl, bh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, al, bl, %0;\n\t"
+      "fma.rn.f32.bf16 %0, ah, bh, %0;\n\t}"
+      : "+f"(acc)
+      : "r"(a), "r"(b));
+}
+
+__device__ __forceinline__ void fh8(float& acc, const uint4& a, const uint4& b) {
+  fh2(acc, a.x, b.x);
+  fh2(acc, a.y, b.y);
+  fh2(acc, a.z, b.z);
+  fh2(acc, a.w, b.w);
+}
+
+// {a0, a1} += {w.lo, w.hi} · {v, v}  (FFMA2)
+__device__ __forceinline__ void ffma2_bf(uint64_t& acc, uint32_t w, uint64_t vv) {
+  uint64_t wf;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(wf) : "r"(w << 16), "r"(w & 0xffff0000u));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(wf), "l"(vv));
+}
+
+__device__ __forceinline__ uint64_t dup2(float v) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(v));
+  return r;
+}
+
+__device__ __forceinline__ float2 unpack2(uint64_t a) {
+  float2 f;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(a));
+  return f;
+}
+
+// Sum V[0..N) over the warp by a halving butterfly (N a power of two <= 32):
+// N - 1 + 5 - log2(N) shuffles.  Returns the total of value index k(lane)
+// (see warp_sum_index); every lane pair (l, l ^ (32 / N)...) agrees.
+template <int N>
+__device__ __forceinline__ float warp_sum_many(float (&V)[N], uint32_t lane) {
+  int n = N;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    if (n > 1) {
+      const int h = n / 2;
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int k = 0; k < N / 2; ++k) {
+        if (k < h) {
+          const float send = up ? V[k] : V[k + h];
+          const float keep = up ? V[k + h] : V[k];
+          V[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+      n = h;
+    } else {
+      V[0] += __shfl_xor_sync(0xffffffffu, V[0], o);
+    }
+  }
+  return V[0];
+}
+
+// The value index whose total lane `lane` holds after warp_sum_many<N>.
+template <int N>
+__device__ __forceinline__ uint32_t warp_sum_index(uint32_t lane) {
+  uint32_t k = 0;
+  int n = N;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    if (n > 1) {
+      const int h = n / 2;
+      if (lane & o) k += h;
+      n = h;
+    }
+  }
+  return k;
+}
+
+template <int N>
+__device__ __forceinline__ bool warp_sum_owner(uint32_t lane) {
+  // after the halving steps, values are replicated over the lane bits that
+  // were only full-reduced: the lowest such lane stores
+  constexpr uint32_t kLog = N <= 1 ? 0 : N <= 2 ? 1 : N <= 4 ? 2 : N <= 8 ? 3 : N <= 16 ? 4 : 5;
+  constexpr uint32_t kRepMask = (1u << (5 - kLog)) - 1u;  // low lane bits not used for the index
+  return (lane & kRepMask) == 0;
+}
+
+constexpr int pow2_at_least(int v) { return v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4 : v <= 8 ? 8 : v <= 16 ? 16 : 32; }
+
+// Per-lane cp.async rings: every lane copies its own 16-byte pieces of the
+// weight rows into its own slots of the warp's ring in shared memory and
+// later reads back exactly those bytes (no cross-lane visibility, so no
+// barrier of any kind); cp.async.wait_group orders each lane's copies.  The
+// ring holds kRing 512-byte warp units (8 KiB per warp), i.e. the loads in
+// flight no longer cost registers (profiles/r02n_microbench_ldg.txt: the
+// register-buffered loop reached 0.94 of the roofline, this one the load-only
+// ceiling).
+constexpr uint32_t kRing = 16;                       // 512-byte units per warp
+constexpr uint32_t kYUnits = 4;                      // expand: the item's y pieces (T · NS <= 4 units)
+constexpr uint32_t kWarpSmem = (kRing + kYUnits) * 512;  // 10 KiB
+constexpr uint32_t kSmem = kWarps * kWarpSmem;       // 80 KiB per CTA (2 CTAs per SM)
+
+__device__ __forceinline__ uint4 lds16(uint32_t a) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  return r;
+}
+
+__device__ __forceinline__ void cpa16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16u : 0u)
+               : "memory");
+}
+
+// ------------------------------------------------------------------ shrink
+// Units (chunk c, row i), row fastest; unit u goes to slot u % kRing and is
+// issued kRing units (LA = kRing / R chunks) before it is consumed, so the
+// unit issued after consuming (c, i) is (c + LA, i): the same row, a static
+// register index for its page entries.
+template <int T, bool FAST>
+__device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
+                                            uint32_t ring) {
+  constexpr int R = kWarpRows(T);
+  constexpr uint32_t LA = kRing / R;  // chunks of lookahead
+  const uint32_t L = p.log2_page;
+  const uint64_t pmask = (1ull << L) - 1;
+  const uint64_t blk = p.blk_mult[w.pj] + static_cast<uint64_t>(li) * p.plu;
+  const uint32_t rowb = p.d_in * 2;
+  const uint64_t a0 = (static_cast<uint64_t>(w.rank) * blk + static_cast<uint64_t>(w.off) * p.d_in) * 2;
+  const uint32_t nc = (p.d_in + 255) / 256;  // 512-byte chunks per row (the last may be partial)
+  const uint32_t* tab = p.table + w.toff;
+  // page entries: lane k holds the entry of row i's k-th page
+  uint32_t ent[R], pg0[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    const uint64_t rb = a0 + static_cast<uint64_t>(i) * rowb;
+    pg0[i] = static_cast<uint32_t>(rb >> L);
+    ent[i] = 0u;
+    if (FAST) {
+      const uint32_t span = static_cast<uint32_t>((rb + rowb - 1) >> L) - pg0[i];
+      if (static_cast<uint32_t>(i) < w.n && lane <= span) ent[i] = __ldg(tab + pg0[i] + lane);
+    }
+  }
+  auto issue = [&](uint32_t c, int i) {  // unit (c, i) -> slot ((c % LA) · R + i); always one group
+    const uint64_t off = a0 + static_cast<uint64_t>(i) * rowb + c * 512 + lane * 16;
+    const uint32_t pg = static_cast<uint32_t>(off >> L);
+    uint32_t e = 0u;
+    if (FAST) e = __shfl_sync(0xffffffffu, ent[i], (pg - pg0[i]) & 31u);
+    const bool valid = static_cast<uint32_t>(i) < w.n && c < nc && c * 256 + lane * 8 < p.d_in;
+    if (!FAST && valid) e = __ldg(tab + pg);
+    cpa16(ring + ((c % LA) * R + i) * 512, valid ? p.arena + (static_cast<uint64_t>(e) << L) + (off & pmask) : p.arena,
+          valid);
+    ptx::cp_async_commit();
+  };
+  for (uint32_t c = 0; c < LA; ++c)
+#pragma unroll
+    for (int i = 0; i < R; ++i) issue(c, i);
+  ptx::pdl_wait();  // x (and the v this launch overwrites) belong to earlier kernels
+  const char* xr[T];
+#pragma unroll
+  for (int t = 0; t < T; ++t)
+    xr[t] = p.x + static_cast<uint64_t>(li) * p.x_lstride_b + static_cast<uint64_t>(w.tok[t]) * p.x_stride_b +
+            lane * 16;
+  auto ldx = [&](uint32_t c, uint4 (&xv)[T]) {
+    const bool valid = c < nc && c * 256 + lane * 8 < p.d_in;
+#pragma unroll
+    for (int t = 0; t < T; ++t)
+      xv[t] = valid ? __ldg(reinterpret_cast<const uint4*>(xr[t] + c * 512)) : make_uint4(0u, 0u, 0u, 0u);
+  };
+  float acc[R][T];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int t = 0; t < T; ++t) acc[i][t] = 0.f;
+  uint4 xv[T];
+  ldx(0, xv);
+#pragma unroll 1
+  for (uint32_t c = 0; c < nc; ++c) {
+    uint4 xn[T];
+    ldx(c + 1, xn);
+    const uint32_t sb = ring + (c % LA) * R * 512;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      ptx::cp_async_wait<kRing - 1>();  // unit (c, i) has landed
+      const uint4 wv = lds16(sb + i * 512);
+#pragma unroll
+      for (int t = 0; t < T; ++t) fh8(acc[i][t], wv, xv[t]);
+      issue(c + LA, i);
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) xv[t] = xn[t];
+  }
+  ptx::cp_async_wait<0>();  // (only zero-size copies remain; the ring is reused by the next item)
+  constexpr int N = pow2_at_least(R * T);
+  float V[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) V[k] = k < R * T ? acc[k / T][k % T] : 0.f;
+  const float sum = warp_sum_many<N>(V, lane);
+  const uint32_t k = warp_sum_index<N>(lane);
+  if (warp_sum_owner<N>(lane) && k < static_cast<uint32_t>(R * T)) {
+    const uint32_t i = k / T, t = k % T;
+    if (i < w.n)
+      p.v[static_cast<uint64_t>(li) * p.vplane + w.voff + t * w.rank + w.off + i] = sum;
+  }
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_shrink_kernel(const WArgs p) {
+  extern __shared__ __align__(16) char smem[];
+  ptx::pdl_launch_dependents();  // the expand may start loading its first weight rows
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // block b: layer b % n_layers of item block b / n_layers (the heaviest items
+  // of every layer first)
+  const uint32_t li = blockIdx.x % p.n_layers;
+  const uint32_t wi = (blockIdx.x / p.n_layers) * kWarps + warp;
+  if (wi >= p.n_items) return;
+  const uint32_t ring = ptx::smem_u32(smem) + warp * kWarpSmem + lane * 16;
+  const WI w = load_item(p.items + wi);
+  switch (w.ntok) {
+    case 1: shrink_item<1, FAST>(p, w, li, lane, ring); break;
+    case 2: shrink_item<2, FAST>(p, w, li, lane, ring); break;
+    case 3: shrink_item<3, FAST>(p, w, li, lane, ring); break;
+    default: shrink_item<4, FAST>(p, w, li, lane, ring); break;
+  }
+}
+
+// ------------------------------------------------------------------ expand
+// Rows in blocks of 64 (lane k holds the page entries and v of rows jb + k and
+// jb + 32 + k); row j's NS units go to ring row slot j % DR, issued DR rows
+// ahead of their use.
+template <int T, bool FAST>
+__device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
+                                            uint32_t ring) {
+  constexpr int NS = kWarpCols(T) / 256;  // 16-byte column chunks per lane and row
+  constexpr uint32_t DR = kRing / NS;     // ring depth in rows
+  const uint32_t L = p.log2_page;
+  const uint64_t pmask = (1ull << L) - 1;
+  const uint64_t blk = p.blk_mult[w.pj] + static_cast<uint64_t>(li) * p.plu;
+  const uint32_t rowb = p.d_out[w.pj] * 2;
+  const uint32_t r = w.rank;
+  // byte offset of row 0's column block
+  const uint64_t b0 = (static_cast<uint64_t>(r) * blk + static_cast<uint64_t>(r) * p.d_in + w.off) * 2;
+  const uint32_t segb = w.n * 2;
+  const uint32_t* tab = p.table + w.toff;
+  bool valid[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) valid[s] = s * 256 + lane * 8 < w.n;
+  const float* vb = p.v + static_cast<uint64_t>(li) * p.vplane + w.voff;  // [tok][rank]
+  uint64_t acc[NS][4][T];
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int t = 0; t < T; ++t) acc[s][q][t] = 0ull;
+  ptx::pdl_wait();  // v (the shrink launch) and y (earlier kernels)
+  // the item's y pieces into the warp's y area: the oldest cp.async group, so
+  // every later wait covers it
+  const uint32_t yarea = ring + kRing * 512;
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    const char* yr = p.y[w.pj] + static_cast<uint64_t>(li) * p.y_lstride_b[w.pj] +
+                     static_cast<uint64_t>(w.tok[t]) * p.y_stride_b[w.pj] + static_cast<uint64_t>(w.off) * 2;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) cpa16(yarea + (t * NS + s) * 512, valid[s] ? yr + s * 512 + lane * 16 : p.y[w.pj], valid[s]);
+  }
+  ptx::cp_async_commit();
+  for (uint32_t jb = 0; jb < r; jb += 64) {
+    uint32_t ef[2], es[2];
+    float vv[T][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t j = jb + h * 32 + lane;
+      ef[h] = es[h] = 0u;
+      if (FAST && j < r) {
+        const uint64_t sb = b0 + static_cast<uint64_t>(j) * rowb;
+        const uint32_t pf = static_cast<uint32_t>(sb >> L);
+        ef[h] = __ldg(tab + pf);
+        es[h] = static_cast<uint32_t>((sb + segb - 1) >> L) != pf ? __ldg(tab + pf + 1) : ef[h];
+      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) vv[t][h] = j < r ? vb[t * r + j] : 0.f;
+    }
+    const uint32_t nrow = min(64u, r - jb);
+    auto issue = [&](uint32_t jj) {  // row jb + jj of the block (one group, possibly empty)
+      const uint64_t sb = b0 + static_cast<uint64_t>(jb + jj) * rowb;
+      const uint32_t pf = static_cast<uint32_t>(sb >> L);
+      uint32_t e_f = 0u, e_s = 0u;
+      if (FAST) {
+        e_f = __shfl_sync(0xffffffffu, (jj & 32u) ? ef[1] : ef[0], jj & 31u);
+        e_s = __shfl_sync(0xffffffffu, (jj & 32u) ? es[1] : es[0], jj & 31u);
+      }
+      const uint32_t slot = ring + (jj % DR) * NS * 512;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const bool ok = jj < nrow && valid[s];
+        const uint64_t off = sb + s * 512 + lane * 16;
+        const uint32_t pg = static_cast<uint32_t>(off >> L);
+        uint32_t e = pg == pf ? e_f : e_s;
+        if (!FAST && ok) e = __ldg(tab + pg);
+        cpa16(slot + s * 512, ok ? p.arena + (static_cast<uint64_t>(e) << L) + (off & pmask) : p.arena, ok);
+      }
+      ptx::cp_async_commit();
+    };
+    for (uint32_t jj = 0; jj < DR; ++jj) issue(jj);
+#pragma unroll 2
+    for (uint32_t jj = 0; jj < nrow; ++jj) {
+      uint64_t v2[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t)
+        v2[t] = dup2(__shfl_sync(0xffffffffu, (jj & 32u) ? vv[t][1] : vv[t][0], jj & 31u));
+      ptx::cp_async_wait<DR - 1>();  // row jj has landed
+      const uint32_t slot = ring + (jj % DR) * NS * 512;
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const uint4 wv = lds16(slot + s * 512);
+        const uint32_t wq[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int t = 0; t < T; ++t) ffma2_bf(acc[s][q][t], wq[q], v2[t]);
+      }
+      issue(jj + DR);
+    }
+    ptx::cp_async_wait<0>();  // the ring is refilled by the next block / item (and y has landed)
+  }
+  ptx::cp_async_wait<0>();
+  // y = bf16(y + scale · acc), 16 bytes per (token, chunk)
+#pragma unroll
+  for (int t = 0; t < T; ++t) {
+    char* yr = p.y[w.pj] + static_cast<uint64_t>(li) * p.y_lstride_b[w.pj] +
+               static_cast<uint64_t>(w.tok[t]) * p.y_stride_b[w.pj] + static_cast<uint64_t>(w.off) * 2;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (!valid[s]) continue;
+      const uint4 yv = lds16(yarea + (t * NS + s) * 512);
+      const uint32_t yw[4] = {yv.x, yv.y, yv.z, yv.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 a = unpack2(acc[s][q][t]);
+        const float lo = __uint_as_float(yw[q] << 16) + p.scale * a.x;
+        const float hi = __uint_as_float(yw[q] & 0xffff0000u) + p.scale * a.y;
+        __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+        o[q] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      *reinterpret_cast<uint4*>(yr + s * 512 + lane * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_expand_kernel(const WArgs p) {
+  extern __shared__ __align__(16) char smem[];
+  ptx::pdl_launch_dependents();
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // block b: layer b % n_layers of item block b / n_layers (the heaviest items
+  // of every layer first)
+  const uint32_t li = blockIdx.x % p.n_layers;
+  const uint32_t wi = (blockIdx.x / p.n_layers) * kWarps + warp;
+  if (wi >= p.n_items) return;
+  const uint32_t ring = ptx::smem_u32(smem) + warp * kWarpSmem + lane * 16;
+  const WI w = load_item(p.items + wi);
+  switch (w.ntok) {
+    case 1: expand_item<1, FAST>(p, w, li, lane, ring); break;
+    case 2: expand_item<2, FAST>(p, w, li, lane, ring); break;
+    case 3: expand_item<3, FAST>(p, w, li, lane, ring); break;
+    default: expand_item<4, FAST>(p, w, li, lane, ring); break;
+  }
+}
+
+}  // namespace
+
+void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0, uint32_t n_layers,
+                      const void* x, uint64_t x_stride, uint64_t x_lstride, void* const* ys,
+                      const uint64_t* y_strides, const uint64_t* y_lstrides, float scale,
+                      cudaStream_t stream) {
+  if (w.ns == 0 || n_layers == 0) return;  // no LoRA token in the batch
+  const plora_store& st = *plan.store;
+  const ModelGeom& gm = st.geom;
+  if (gm.m.d_in[w.projs[0]] % 8) throw ValidationError("bf16 BGMV needs d_in and d_out multiples of 8");
+  WArgs a{};
+  a.n_layers = n_layers;
+  a.arena = st.arena;
+  a.table = st.d_table;
+  a.d_in = gm.m.d_in[w.projs[0]];
+  a.log2_page = st.log2_page;
+  a.x = static_cast<const char*>(x);
+  a.x_stride_b = x_stride * 2;
+  a.x_lstride_b = x_lstride * 2;
+  for (uint32_t i = 0; i < w.np; ++i) {
+    const uint32_t pr = w.projs[i];
+    if (gm.m.d_out[pr] % 8) throw ValidationError("bf16 BGMV needs d_in and d_out multiples of 8");
+    a.y[i] = static_cast<char*>(ys[i]);
+    a.y_stride_b[i] = y_strides[i] * 2;
+    a.y_lstride_b[i] = y_lstrides ? y_lstrides[i] * 2 : 0;
+    a.blk_mult[i] = gm.blk_mult(layer0, pr);
+    a.d_out[i] = gm.m.d_out[pr];
+  }
+  a.plu = gm.per_layer_unit;
+  a.v = plan.d_wv;
+  a.vplane = w.vplane;
+  a.scale = scale;
+  // shuffle-resolved page entries: a shrink row spans <= 32 pages and an
+  // expand block (<= 1 KiB) <= 2 pages
+  const uint64_t P = 1ull << st.log2_page;
+  const bool fast = P >= 2ull * kWarpCols(1) && (a.d_in * 2ull + P - 1) / P + 1 <= 32;
+  a.fast = fast ? 1u : 0u;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = stream;
+  set_smem_once(reinterpret_cast<const void*>(bgmv_warp_shrink_kernel<true>), kSmem);
+  set_smem_once(reinterpret_cast<const void*>(bgmv_warp_shrink_kernel<false>), kSmem);
+  set_smem_once(reinterpret_cast<const void*>(bgmv_warp_expand_kernel<true>), kSmem);
+  set_smem_once(reinterpret_cast<const void*>(bgmv_warp_expand_kernel<false>), kSmem);
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  a.items = plan.d_witems + w.s_off;
+  a.n_items = w.ns;
+  cfg.gridDim = dim3((w.ns + kWarps - 1) / kWarps * n_layers);
+  if (fast)
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_warp_shrink_kernel<true>, a));
+  else
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_warp_shrink_kernel<false>, a));
+  count_launch();
+  a.items = plan.d_witems + w.e_off;
+  a.n_items = w.ne;
+  cfg.gridDim = dim3((w.ne + kWarps - 1) / kWarps * n_layers);
+  if (fast)
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_warp_expand_kernel<true>, a));
+  else
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_warp_expand_kernel<false>, a));
+  count_launch();
+}
+
+}  // namespace plora

@@ -625,6 +625,89 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     }
   }
 
+  // ---- bf16 warp-item BGMV (bgmv_warp.cu, the default decode op): jobs of
+  // <= 4 tokens (an adapter's tokens split evenly over ceil(n / 4) jobs),
+  // S items of kWarpRows rank rows, E items of kWarpCols output columns
+  witems.clear();
+  for (uint32_t p = 0; p < PLORA_MAX_PROJ; ++p) wwork[p] = WarpWork{};
+  wwork_layer = WarpWork{};
+  uint64_t wv_need = 0;
+  if (es == 2) {
+    struct WJob {
+      uint32_t rank, table_off, ntok, tok[kWarpJobTok];
+    };
+    std::vector<WJob> wj;
+    for (uint32_t si : order) {  // largest rank first
+      const Seg& sg = segs[si];
+      if (seg_route[si]) continue;
+      const uint32_t nt = static_cast<uint32_t>(sg.toks.size()), nj = (nt + kWarpJobTok - 1) / kWarpJobTok;
+      uint32_t t0 = 0;
+      for (uint32_t q = 0; q < nj; ++q) {
+        WJob j{sg.rank, sg.table_off, nt / nj + (q < nt % nj ? 1u : 0u), {}};
+        for (uint32_t t = 0; t < j.ntok; ++t) j.tok[t] = sg.toks[t0 + t];
+        t0 += j.ntok;
+        wj.push_back(j);
+      }
+    }
+    auto build_w = [&](WarpWork& w, const uint32_t* projs, uint32_t np) {
+      w = WarpWork{};
+      w.np = np;
+      for (uint32_t i = 0; i < np; ++i) w.projs[i] = projs[i];
+      if (wj.empty()) return;
+      uint64_t voff = 0;
+      std::vector<WarpItem> S, E;
+      for (uint32_t i = 0; i < np; ++i) {
+        const uint32_t dout = g.m.d_out[projs[i]];
+        for (const WJob& j : wj) {
+          WarpItem base{};
+          base.table_off = j.table_off;
+          base.v_off = static_cast<uint32_t>(voff);
+          for (uint32_t t = 0; t < kWarpJobTok; ++t) base.tok[t] = t < j.ntok ? j.tok[t] : 0u;
+          auto meta = [&](uint32_t n) { return j.rank | (j.ntok << 9) | (i << 12) | (n << 16); };
+          const uint32_t R = kWarpRows(j.ntok), C = kWarpCols(j.ntok);
+          for (uint32_t r0 = 0; r0 < j.rank; r0 += R) {
+            WarpItem it = base;
+            it.meta = meta(std::min(R, j.rank - r0));
+            it.off = r0;
+            S.push_back(it);
+          }
+          for (uint32_t c0 = 0; c0 < dout; c0 += C) {
+            WarpItem it = base;
+            it.meta = meta(std::min(C, dout - c0));
+            it.off = c0;
+            E.push_back(it);
+          }
+          voff += static_cast<uint64_t>(j.ntok) * j.rank;
+        }
+      }
+      if (voff > 0xffffffffull) throw ValidationError("batch too large for one plan");
+      // heaviest items first (the hardware block scheduler then fills the
+      // tail with the light ones); ties keep list order, so a job's items stay
+      // adjacent and share x / v through L1
+      auto s_cost = [](const WarpItem& it) { return it.meta >> 16; };
+      auto e_cost = [](const WarpItem& it) { return (it.meta & 0x1ffu) * (it.meta >> 16); };
+      std::stable_sort(S.begin(), S.end(), [&](const WarpItem& a, const WarpItem& b) { return s_cost(a) > s_cost(b); });
+      std::stable_sort(E.begin(), E.end(), [&](const WarpItem& a, const WarpItem& b) { return e_cost(a) > e_cost(b); });
+      w.s_off = static_cast<uint32_t>(witems.size());
+      w.ns = static_cast<uint32_t>(S.size());
+      witems.insert(witems.end(), S.begin(), S.end());
+      w.e_off = static_cast<uint32_t>(witems.size());
+      w.ne = static_cast<uint32_t>(E.size());
+      witems.insert(witems.end(), E.begin(), E.end());
+      w.vplane = (voff + 3) & ~3ull;
+      wv_need = std::max(wv_need, w.vplane);
+    };
+    for (uint32_t p = 0; p < g.m.n_proj; ++p) build_w(wwork[p], &p, 1);
+    bool same_in = g.m.n_proj > 1;
+    for (uint32_t p = 1; p < g.m.n_proj; ++p) same_in = same_in && g.m.d_in[p] == g.m.d_in[0];
+    if (same_in) {
+      uint32_t all[PLORA_MAX_PROJ];
+      for (uint32_t p = 0; p < g.m.n_proj; ++p) all[p] = p;
+      build_w(wwork_layer, all, g.m.n_proj);
+    }
+    wv_need *= g.m.n_layers;  // a multi-layer launch keeps one plane per layer
+  }
+
   // ---- upload the device-side work lists in one copy from a pinned
   // staging buffer (cluster chunk offsets travel as kernel parameters)
   auto align = [](uint64_t v) { return (v + 255) & ~255ull; };
@@ -644,6 +727,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       {stitems.data(), stitems.size() * sizeof(StreamItem), reinterpret_cast<void**>(&d_stitems)},
       {stcta.data(), stcta.size() * sizeof(uint32_t), reinterpret_cast<void**>(&d_stcta)},
       {route_perm.data(), route_perm.size() * sizeof(uint32_t), reinterpret_cast<void**>(&d_route_perm)},
+      {witems.data(), witems.size() * sizeof(WarpItem), reinterpret_cast<void**>(&d_witems)},
   };
   uint64_t total = 0;
   for (const Part& pt : parts) total += align(pt.bytes);
@@ -683,6 +767,15 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
     d_v = nullptr;
     v_cap = std::max<uint64_t>(v_elems, 4096);
     PLORA_CUDA(cudaMalloc(&d_v, v_cap * sizeof(float)));
+  }
+  if (wv_cap < wv_need) {  // warp-item BGMV v planes
+    if (d_wv) {
+      PLORA_CUDA(cudaStreamSynchronize(stream));
+      cudaFree(d_wv);
+    }
+    d_wv = nullptr;
+    wv_cap = wv_need;
+    PLORA_CUDA(cudaMalloc(&d_wv, wv_cap * sizeof(float)));
   }
   if (es == 2 && n_tiles > 0) {  // SGMV workspaces (see sgmv.cu)
     // one region per projection (plora_sgmv_layer keeps both in flight)
@@ -779,6 +872,7 @@ void plora_plan_destroy(plora_plan* plan) {
   cudaFree(plan->d_v);
   cudaFree(plan->d_sv);
   cudaFree(plan->d_scnt);
+  cudaFree(plan->d_wv);
   if (plan->aux_stream) cudaStreamDestroy(plan->aux_stream);
   if (plan->ev_fork) cudaEventDestroy(plan->ev_fork);
   if (plan->ev_join) cudaEventDestroy(plan->ev_join);

@@ -189,6 +189,40 @@ struct StreamWork {  // one launch variant (a projection, or every projection of
   uint32_t projs[PLORA_MAX_PROJ] = {};
 };
 
+// ------------------------------------------------ bf16 BGMV (warp items)
+// bgmv_warp.cu, the default decode op: two launches, shrink then expand, each
+// a flat list of warp-sized work items (no shared-memory ring, no clusters,
+// no cross-CTA waits: the launch boundary orders v).  A job = <= 4 tokens of
+// one adapter at one (layer, proj).
+//   S item: <= kWarpRows(ntok) rank rows of A, full K; v[tok][row] exact fp32.
+//   E item: one column block of <= kWarpCols(ntok) outputs over every rank
+//           row; y[tok][block] = bf16(y + scale · Σ_row v[tok][row] · Bᵀ[row][block]).
+constexpr uint32_t kWarpJobTok = 4;
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr uint32_t kWarpRows(uint32_t ntok) { return ntok <= 2 ? 8u : 4u; }
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr uint32_t kWarpCols(uint32_t ntok) { return ntok <= 2 ? 512u : 256u; }
+struct WarpItem {  // 32 bytes, self-contained
+  uint32_t table_off;  // adapter's first entry in the device page table
+  uint32_t meta;       // rank (bits 0-8) | ntok (9-11) | launch projection (12-15) | n (16-31)
+  uint32_t off;        // S: first rank row; E: first output column
+  uint32_t v_off;      // floats into the launch's per-layer v plane: the job's [ntok][rank] block
+  uint32_t tok[kWarpJobTok];
+};
+static_assert(sizeof(WarpItem) == 32, "WarpItem layout");
+
+struct WarpWork {  // one launch variant (a projection, or every projection of a layer)
+  uint32_t s_off = 0, ns = 0;  // S items [s_off, s_off + ns) of the item array
+  uint32_t e_off = 0, ne = 0;  // E items
+  uint32_t np = 0;
+  uint32_t projs[PLORA_MAX_PROJ] = {};
+  uint64_t vplane = 0;         // floats of v per launched layer
+};
+
 // ---------------------------------------------------------------- SGMV
 // A run = maximal stretch of consecutive tokens with the same adapter
 // (Punica's seg_indptr formulation); tiles are 128-row slices of runs.
@@ -286,6 +320,13 @@ struct plora_plan {
   uint64_t scnt_cap = 0;
   void build_stream(const std::vector<std::vector<uint32_t>>& seg_toks,
                     const std::vector<uint32_t>& seg_rank, const std::vector<uint32_t>& seg_table);
+  // bf16 warp-item BGMV (bgmv_warp.cu, the default decode op)
+  plora::WarpWork wwork[PLORA_MAX_PROJ];
+  plora::WarpWork wwork_layer;  // every projection of a layer (equal d_in), np 0: none
+  std::vector<plora::WarpItem> witems;
+  plora::WarpItem* d_witems = nullptr;
+  float* d_wv = nullptr;        // v planes: n_layers · max vplane floats
+  uint64_t wv_cap = 0;
   // hybrid decode launch (plora_bgmv_layers): the clusters' share and the
   // streaming kernel's share on the SMs the clusters leave idle, run
   // concurrently on `stream` and `aux_stream` (fork / join by events)
@@ -347,7 +388,17 @@ void launch_bgmv_stream(const plora_plan& plan, const StreamWork& w, uint32_t la
                         void* const* ys, const uint64_t* y_strides, const uint64_t* y_lstrides,
                         float scale, cudaStream_t stream);
 uint32_t stream_max_ctas(int device, uint32_t jt);
-bool hybrid_enabled();  // plora_debug_set_bgmv_impl: 0 (default) = clusters + streaming share
+// Warp-item bf16 BGMV (bgmv_warp.cu): shrink launch then expand launch over
+// the projections `w` was built for, layers [layer0, layer0 + n_layers)
+// (strides as launch_bgmv_stream).
+void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0, uint32_t n_layers,
+                      const void* x, uint64_t x_stride, uint64_t x_lstride, void* const* ys,
+                      const uint64_t* y_strides, const uint64_t* y_lstrides, float scale,
+                      cudaStream_t stream);
+// plora_debug_set_bgmv_impl: 0 (default) warp items, 1 streaming kernel,
+// 2 clusters, 3 the hybrid pair (clusters + streaming share)
+uint32_t bgmv_impl();
+bool hybrid_enabled();  // impl 3
 uint32_t route_min_tokens();  // plora_debug_set_route_tokens (0: never route)
 double hybrid_share_factor();  // streaming share = spare SMs / SMs × this (of the weight bytes)
 // Every projection of `layer` (they read the same x) in one launch.

@@ -11,6 +11,8 @@ from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, ModelShape
 
 # Tolerances (BASELINE.json north_star): normwise max|y_gpu - y_oracle| / max|y_oracle|
 TOL_BF16 = 1e-2
+# the default bf16 decode op (bgmv_warp.cu) is two launches per call: shrink, expand
+BGMV_BF16_LAUNCHES = 2
 TOL_F32 = 1e-5
 
 

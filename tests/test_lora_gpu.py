@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 import torch
 
-from lora_harness import TOL_BF16, TOL_F32, Setup, rel_err, to_np_bits
+from lora_harness import BGMV_BF16_LAUNCHES, TOL_BF16, TOL_F32, Setup, rel_err, to_np_bits
 from oracle import lora as OL
 from paper_2512_20210_b200 import (AllocStatus, PagePool, ValidationError, synth)
 from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, ModelShape, bgmv,
@@ -273,7 +273,7 @@ def test_linearity_property_full_cfg2(cuda):
     torch.cuda.synchronize()
     d = (y2.float() - 2 * y1.float()).abs().max().item()
     assert d <= 2e-2 * y2.float().abs().max().item()
-    assert kernel_launch_count() - n0 == 3  # one persistent launch per call
+    assert kernel_launch_count() - n0 == 3 * BGMV_BF16_LAUNCHES  # shrink + expand per call
 
 
 def test_ring_stress_random_ranks(cuda):
@@ -310,7 +310,7 @@ def test_bgmv_layer_fused_equals_per_projection(cuda, page_bytes):
     n0 = kernel_launch_count()
     bgmv_layer(plan, 1, x, fused, 0.75)
     torch.cuda.synchronize()
-    assert kernel_launch_count() - n0 == 1
+    assert kernel_launch_count() - n0 == BGMV_BF16_LAUNCHES  # both projections in one shrink + one expand
     for p in range(2):
         assert torch.equal(fused[p], sep[p])
     ref = s.oracle(1, 1, x.cpu(), y0[1].cpu(), ta, scale=0.75)
@@ -319,10 +319,13 @@ def test_bgmv_layer_fused_equals_per_projection(cuda, page_bytes):
 
 @pytest.mark.parametrize("page_bytes", [2048, 256])
 def test_bgmv_layers_multi_layer_launch_bit_identical(cuda, page_bytes):
-    """plora_bgmv_layers (several layers per launch, the clusters' chunk lists
-    repeated per layer) computes exactly what per-layer bgmv_layer calls do,
-    on strided per-layer views, and matches the oracle."""
+    """plora_bgmv_layers (several layers per launch) computes exactly what
+    per-layer bgmv_layer calls do, on strided per-layer views, and matches the
+    oracle: the default warp-item op (one shrink + one expand launch for all
+    layers), the cluster kernel (impl 2: its chunk lists repeated per layer)
+    and the round-2 hybrid pair (impl 3: clusters + a streaming share)."""
     from paper_2512_20210_b200.lora import bgmv_layer, bgmv_layers
+    from paper_2512_20210_b200 import _native as N
     cfg = synth.cfg2(n_layers=4, page_bytes=page_bytes)
     s = Setup(cfg)
     ta = synth.token_assignment(cfg.n_adapters, cfg.tokens_per_adapter)
@@ -330,37 +333,37 @@ def test_bgmv_layers_multi_layer_launch_bit_identical(cuda, page_bytes):
     g = torch.Generator(device="cuda").manual_seed(5)
     x = torch.randn(3, T, 4096, device="cuda", generator=g).to(torch.bfloat16)
     y0 = torch.randn(3, 2, T, 4096, device="cuda", generator=g).to(torch.bfloat16)
-    plan = BatchPlan(s.store, ta)
-    ref = y0.clone()
-    for i in range(3):
-        bgmv_layer(plan, 1 + i, x[i], [ref[i, 0], ref[i, 1]], 0.5)
-    from paper_2512_20210_b200 import _native as N
-    N.check(N.lib().plora_debug_set_bgmv_impl(2))  # clusters only: the same chunks as bgmv_layer
-    try:
-        got = y0.clone()
-        n0 = kernel_launch_count()
-        bgmv_layers(BatchPlan(s.store, ta), 1, x, [got[:, 0], got[:, 1]], 0.5)
-        torch.cuda.synchronize()
-        assert kernel_launch_count() - n0 == 1
-        assert torch.equal(got, ref)
-    finally:
-        N.check(N.lib().plora_debug_set_bgmv_impl(0))
-    # default: the hybrid launch (clusters + a streaming share on the idle SMs)
-    hyb = y0.clone()
-    plan_h = BatchPlan(s.store, ta)
-    n0 = kernel_launch_count()
-    bgmv_layers(plan_h, 1, x, [hyb[:, 0], hyb[:, 1]], 0.5)
-    torch.cuda.synchronize()
-    assert kernel_launch_count() - n0 == 2
-    again = y0.clone()
-    bgmv_layers(plan_h, 1, x, [again[:, 0], again[:, 1]], 0.5)
-    torch.cuda.synchronize()
-    assert torch.equal(hyb, again)  # deterministic
+
+    def per_layer(plan):
+        ref = y0.clone()
+        for i in range(3):
+            bgmv_layer(plan, 1 + i, x[i], [ref[i, 0], ref[i, 1]], 0.5)
+        return ref
+
+    outs = {}
+    for impl, launches in ((0, BGMV_BF16_LAUNCHES), (2, 1), (3, 2)):
+        N.check(N.lib().plora_debug_set_bgmv_impl(impl))
+        try:
+            plan = BatchPlan(s.store, ta)
+            got = y0.clone()
+            n0 = kernel_launch_count()
+            bgmv_layers(plan, 1, x, [got[:, 0], got[:, 1]], 0.5)
+            torch.cuda.synchronize()
+            assert kernel_launch_count() - n0 == launches, impl
+            if impl != 3:  # (the hybrid pair runs per layer on the clusters alone)
+                assert torch.equal(got, per_layer(plan)), impl
+            again = y0.clone()
+            bgmv_layers(plan, 1, x, [again[:, 0], again[:, 1]], 0.5)
+            torch.cuda.synchronize()
+            assert torch.equal(got, again), impl  # deterministic
+            outs[impl] = got
+        finally:
+            N.check(N.lib().plora_debug_set_bgmv_impl(0))
     for i in range(3):
         for p in range(2):
             o = s.oracle(1 + i, p, x[i].cpu(), y0[i, p].cpu(), ta, scale=0.5)
-            assert rel_err(hyb[i, p], o) <= TOL_BF16, (i, p)
-            assert rel_err(got[i, p], o) <= TOL_BF16, (i, p)
+            for impl, got in outs.items():
+                assert rel_err(got[i, p], o) <= TOL_BF16, (impl, i, p)
 
 
 @pytest.mark.parametrize("tokens_per_adapter", [2, 6])

@@ -101,35 +101,40 @@ def test_routed_layer_and_multi_layer_launch(skew):
         assert delta_rel_err(multi[p][2], ref, y0[p][2]) <= TOL_BF16, p
 
 
-def test_routed_hot_adapter_with_hybrid_rest_and_graph(skew):
+@pytest.mark.parametrize("impl", [0, 3])
+def test_routed_hot_adapter_with_hybrid_rest_and_graph(skew, impl):
     """One hot adapter, every other adapter <= 4 tokens: the hot one is routed
-    and the rest runs the hybrid decode pair; the whole step replays from a
-    CUDA graph."""
+    and the rest runs the default warp-item op (impl 0) or the hybrid decode
+    pair (impl 3); the whole step replays from a CUDA graph."""
     s = skew
     rng = np.random.default_rng(5)
     ta = np.concatenate([np.full(48, 3, np.int32), np.repeat(np.arange(4, 128, dtype=np.int32), 2)])
     rng.shuffle(ta)
     T = len(ta)
     set_route(16)
-    plan = BatchPlan(s.store, ta)
-    assert routed(plan) == 48
-    hyb = (C.c_double * 4)()
-    N.check(N.lib().plora_debug_plan_hybrid(plan.handle, hyb))
-    assert hyb[0] > 0  # the hybrid streaming share runs beside the clusters
-    x, y0 = _xy(T, 9, zero_y=False, layers=3)
-    xd = x.cuda()
-    eager = [y.cuda() for y in y0]
-    bgmv_layers(plan, 0, xd, eager)
-    ys = [y.cuda() for y in y0]
-    bgmv_layers(plan, 0, xd, [torch.empty_like(y) for y in ys])  # warm (outside capture)
-    torch.cuda.synchronize()
-    gr = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(gr):
-        bgmv_layers(plan, 0, xd, ys)
-    for p in range(2):
-        ys[p].copy_(y0[p].cuda())
-    gr.replay()
-    torch.cuda.synchronize()
+    N.check(N.lib().plora_debug_set_bgmv_impl(impl))
+    try:
+        plan = BatchPlan(s.store, ta)
+        assert routed(plan) == 48
+        hyb = (C.c_double * 4)()
+        N.check(N.lib().plora_debug_plan_hybrid(plan.handle, hyb))
+        assert (hyb[0] > 0) == (impl == 3)  # the hybrid streaming share runs beside the clusters
+        x, y0 = _xy(T, 9, zero_y=False, layers=3)
+        xd = x.cuda()
+        eager = [y.cuda() for y in y0]
+        bgmv_layers(plan, 0, xd, eager)
+        ys = [y.cuda() for y in y0]
+        bgmv_layers(plan, 0, xd, [torch.empty_like(y) for y in ys])  # warm (outside capture)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            bgmv_layers(plan, 0, xd, ys)
+        for p in range(2):
+            ys[p].copy_(y0[p].cuda())
+        gr.replay()
+        torch.cuda.synchronize()
+    finally:
+        N.check(N.lib().plora_debug_set_bgmv_impl(0))
     for p in range(2):
         assert torch.equal(ys[p], eager[p]), p
         ref = s.oracle(1, p, x[1], y0[p][1], ta, nthreads=32)

@@ -27,8 +27,8 @@ def _sgmv_vs_oracle(s, ta, layer, proj, scale=1.0, salt=0):
     tc = (shape.dtype == torch.bfloat16 and max(ranks, default=0) <= 128
           and shape.d_in[proj] % 64 == 0 and shape.d_out[proj] % 128 == 0)
     # tcgen05 shrink + split reduction + expand; else the BGMV path
-    # (one cluster launch for bf16, shrink + expand for fp32)
-    expect = 3 if tc else (1 if shape.dtype == torch.bfloat16 else 2)
+    # (shrink + expand launches, bf16 and fp32 alike)
+    expect = 3 if tc else 2
     assert kernel_launch_count() - n0 == expect
     ref = s.oracle(layer, proj, x, y0, ta, scale=scale, v_bf16=shape.dtype == torch.bfloat16)
     return yd, ref, y0
