@@ -654,6 +654,10 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       w.np = np;
       for (uint32_t i = 0; i < np; ++i) w.projs[i] = projs[i];
       if (wj.empty()) return;
+      // K slices of the S items: 1 (splitting a 4096-wide 8-row item in two
+      // measured slower for the 32-layer step, 0.339 vs 0.320 ms of shrink,
+      // and barely faster per layer, profiles/r02n_warp_variants.txt)
+      w.ks = 1;
       uint64_t voff = 0;
       std::vector<WarpItem> S, E;
       for (uint32_t i = 0; i < np; ++i) {
@@ -664,20 +668,24 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
           base.v_off = static_cast<uint32_t>(voff);
           for (uint32_t t = 0; t < kWarpJobTok; ++t) base.tok[t] = t < j.ntok ? j.tok[t] : 0u;
           auto meta = [&](uint32_t n) { return j.rank | (j.ntok << 9) | (i << 12) | (n << 16); };
-          const uint32_t R = kWarpRows(j.ntok), C = kWarpCols(j.ntok);
-          for (uint32_t r0 = 0; r0 < j.rank; r0 += R) {
-            WarpItem it = base;
-            it.meta = meta(std::min(R, j.rank - r0));
-            it.off = r0;
-            S.push_back(it);
-          }
+          const uint32_t R = kWarpRows(j.ntok);
+          // (256-column blocks for wide adapters measured slower: 515 vs 367 us
+          // of expand per 32-layer step, profiles/r02n_warp_variants.txt)
+          const uint32_t C = kWarpCols(j.ntok);
+          for (uint32_t k = 0; k < w.ks; ++k)
+            for (uint32_t r0 = 0; r0 < j.rank; r0 += R) {
+              WarpItem it = base;
+              it.meta = meta(std::min(R, j.rank - r0));
+              it.off = r0 | (k << 16);
+              S.push_back(it);
+            }
           for (uint32_t c0 = 0; c0 < dout; c0 += C) {
             WarpItem it = base;
             it.meta = meta(std::min(C, dout - c0));
             it.off = c0;
             E.push_back(it);
           }
-          voff += static_cast<uint64_t>(j.ntok) * j.rank;
+          voff += static_cast<uint64_t>(w.ks) * j.ntok * j.rank;
         }
       }
       if (voff > 0xffffffffull) throw ValidationError("batch too large for one plan");

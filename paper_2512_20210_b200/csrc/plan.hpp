@@ -194,9 +194,12 @@ struct StreamWork {  // one launch variant (a projection, or every projection of
 // a flat list of warp-sized work items (no shared-memory ring, no clusters,
 // no cross-CTA waits: the launch boundary orders v).  A job = <= 4 tokens of
 // one adapter at one (layer, proj).
-//   S item: <= kWarpRows(ntok) rank rows of A, full K; v[tok][row] exact fp32.
+//   S item: <= kWarpRows(ntok) rank rows of A over one of the list's `ks`
+//           K slices; its fp32 partial of v[tok][row] goes to that slice's
+//           plane of the job's v block [ks][ntok][rank].
 //   E item: one column block of <= kWarpCols(ntok) outputs over every rank
-//           row; y[tok][block] = bf16(y + scale · Σ_row v[tok][row] · Bᵀ[row][block]).
+//           row; y[tok][block] = bf16(y + scale · Σ_row v[tok][row] · Bᵀ[row][block])
+//           with v = the K-slice partials summed in slice order.
 constexpr uint32_t kWarpJobTok = 4;
 #ifdef __CUDACC__
 __host__ __device__
@@ -209,7 +212,7 @@ constexpr uint32_t kWarpCols(uint32_t ntok) { return ntok <= 2 ? 512u : 256u; }
 struct WarpItem {  // 32 bytes, self-contained
   uint32_t table_off;  // adapter's first entry in the device page table
   uint32_t meta;       // rank (bits 0-8) | ntok (9-11) | launch projection (12-15) | n (16-31)
-  uint32_t off;        // S: first rank row; E: first output column
+  uint32_t off;        // S: first rank row | K slice << 16; E: first output column
   uint32_t v_off;      // floats into the launch's per-layer v plane: the job's [ntok][rank] block
   uint32_t tok[kWarpJobTok];
 };
@@ -220,6 +223,7 @@ struct WarpWork {  // one launch variant (a projection, or every projection of a
   uint32_t e_off = 0, ne = 0;  // E items
   uint32_t np = 0;
   uint32_t projs[PLORA_MAX_PROJ] = {};
+  uint32_t ks = 1;             // K slices of the S items (v partial planes per job)
   uint64_t vplane = 0;         // floats of v per launched layer
 };
 
