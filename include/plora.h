@@ -577,10 +577,11 @@ int plora_predictor_buffer_at(const plora_predictor* p, uint64_t i, uint32_t* ad
  * each CTA, fields as documented in scripts/trace_bgmv.py (chunk 63 holds the
  * CTA start / end).  dev_buf = NULL disables tracing. */
 int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
-/* Diagnostics: the bf16 decode kernel behind plora_bgmv* — 0 thread-block
- * clusters (bgmv_cluster.cu), with the hybrid streaming share for
- * plora_bgmv_layers (default); 1 the streaming kernel alone (bgmv_stream.cu);
- * 2 clusters only.  Applies to plans built afterwards for the hybrid split. */
+/* Diagnostics: the bf16 decode kernel behind plora_bgmv* — 0 warp items
+ * (bgmv_warp.cu, the default); 1 the streaming kernel alone (bgmv_stream.cu);
+ * 2 thread-block clusters only (bgmv_cluster.cu); 3 clusters with the hybrid
+ * streaming share for plora_bgmv_layers (the round-2 pair).  Applies to plans
+ * built afterwards for the hybrid split. */
 int plora_debug_set_bgmv_impl(int impl);
 /* Diagnostics for the streaming kernel: 1 consumers skip the math, 2 no
  * weight copies (results are then wrong; timing ablation only). */

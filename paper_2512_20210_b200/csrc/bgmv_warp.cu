@@ -35,10 +35,11 @@
 namespace plora {
 namespace {
 
-#ifndef PLORA_WARP_MINB
-#define PLORA_WARP_MINB 2  // CTAs per SM the register budget is sized for
+#ifndef PLORA_WARP_CTA
+#define PLORA_WARP_CTA 2  // warps (work items) per CTA
 #endif
-constexpr uint32_t kWarps = 8;
+constexpr uint32_t kWarps = PLORA_WARP_CTA;
+#define PLORA_WARP_MINB (16 / PLORA_WARP_CTA)  // 16 warps per SM: <= 128 registers
 constexpr uint32_t kThreads = kWarps * 32;
 
 struct WArgs {
@@ -47,7 +48,6 @@ struct WArgs {
   const WarpItem* items;  // this launch's S or E items
   uint32_t n_items;
   uint32_t n_layers;  // layers of this launch (grid = item blocks × n_layers)
-  uint32_t ks;        // K slices of the S items (v partial planes per job)
   uint32_t d_in;
   uint32_t log2_page;
   uint32_t fast;  // page entries by warp shuffle (rows / blocks span few pages)
@@ -187,10 +187,16 @@ constexpr int pow2_at_least(int v) { return v <= 1 ? 1 : v <= 2 ? 2 : v <= 4 ? 4
 // flight no longer cost registers (profiles/r02n_microbench_ldg.txt: the
 // register-buffered loop reached 0.94 of the roofline, this one the load-only
 // ceiling).
-constexpr uint32_t kRing = 16;                       // 512-byte units per warp
-constexpr uint32_t kYUnits = 4;                      // expand: the item's y pieces (T · NS <= 4 units)
-constexpr uint32_t kWarpSmem = (kRing + kYUnits) * 512;  // 10 KiB
-constexpr uint32_t kSmem = kWarps * kWarpSmem;       // 80 KiB per CTA (2 CTAs per SM)
+// Ring depth: 16 units (8 KiB per warp, 16 warps per SM) for multi-layer
+// launches, which have items for every SM many times over; 32 units (16 KiB
+// per warp, 12 warps per SM) for a single layer's call, whose few items each
+// stream for longer (profiles/r02n_warp_variants.txt: per-layer 45.0 ->
+// 36.5 us; the 32-layer step 0.661 -> 0.766 ms with the deep ring, so both).
+constexpr uint32_t kRing = 16;
+constexpr uint32_t kDeepRing = 32;
+constexpr uint32_t kYUnits = 4;  // expand: the item's y pieces (T · NS <= 4 units)
+__host__ __device__ constexpr uint32_t warp_smem(uint32_t ring) { return (ring + kYUnits) * 512; }
+__host__ __device__ constexpr uint32_t cta_smem(uint32_t ring) { return kWarps * warp_smem(ring); }
 
 __device__ __forceinline__ uint4 lds16(uint32_t a) {
   uint4 r;
@@ -208,22 +214,19 @@ __device__ __forceinline__ void cpa16(uint32_t dst, const void* src, bool valid)
 // issued kRing units (LA = kRing / R chunks) before it is consumed, so the
 // unit issued after consuming (c, i) is (c + LA, i): the same row, a static
 // register index for its page entries.
-template <int T, bool FAST>
+template <int T, bool FAST, uint32_t RG>
 __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
                                             uint32_t ring) {
   constexpr int R = kWarpRows(T);
-  constexpr uint32_t LA = kRing / R;  // chunks of lookahead
+  constexpr uint32_t LA = RG / R;  // chunks of lookahead
   const uint32_t L = p.log2_page;
   const uint64_t pmask = (1ull << L) - 1;
   const uint64_t blk = p.blk_mult[w.pj] + static_cast<uint64_t>(li) * p.plu;
   const uint32_t rowb = p.d_in * 2;
-  const uint32_t row0 = w.off & 0xffffu, slice = w.off >> 16;
-  const uint32_t ncall = (p.d_in + 255) / 256;  // 512-byte chunks per row (the last may be partial)
-  const uint32_t cps = (ncall + p.ks - 1) / p.ks;
-  const uint32_t c0 = slice * cps, nc = min(ncall, c0 + cps) - c0;  // this item's chunks [c0, c0 + nc)
-  const uint64_t a0 = (static_cast<uint64_t>(w.rank) * blk + static_cast<uint64_t>(row0) * p.d_in + c0 * 256ull) * 2;
+  const uint64_t a0 = (static_cast<uint64_t>(w.rank) * blk + static_cast<uint64_t>(w.off) * p.d_in) * 2;
+  const uint32_t nc = (p.d_in + 255) / 256;  // 512-byte chunks per row (the last may be partial)
   const uint32_t* tab = p.table + w.toff;
-  // page entries: lane k holds the entry of row i's k-th page (of the slice)
+  // page entries: lane k holds the entry of row i's k-th page
   uint32_t ent[R], pg0[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
@@ -231,7 +234,7 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
     pg0[i] = static_cast<uint32_t>(rb >> L);
     ent[i] = 0u;
     if (FAST) {
-      const uint32_t span = static_cast<uint32_t>((rb + min(rowb, nc * 512u) - 1) >> L) - pg0[i];
+      const uint32_t span = static_cast<uint32_t>((rb + rowb - 1) >> L) - pg0[i];
       if (static_cast<uint32_t>(i) < w.n && lane <= span) ent[i] = __ldg(tab + pg0[i] + lane);
     }
   }
@@ -240,7 +243,7 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
     const uint32_t pg = static_cast<uint32_t>(off >> L);
     uint32_t e = 0u;
     if (FAST) e = __shfl_sync(0xffffffffu, ent[i], (pg - pg0[i]) & 31u);
-    const bool valid = static_cast<uint32_t>(i) < w.n && c < nc && (c0 + c) * 256 + lane * 8 < p.d_in;
+    const bool valid = static_cast<uint32_t>(i) < w.n && c < nc && c * 256 + lane * 8 < p.d_in;
     if (!FAST && valid) e = __ldg(tab + pg);
     cpa16(ring + ((c % LA) * R + i) * 512, valid ? p.arena + (static_cast<uint64_t>(e) << L) + (off & pmask) : p.arena,
           valid);
@@ -254,9 +257,9 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
 #pragma unroll
   for (int t = 0; t < T; ++t)
     xr[t] = p.x + static_cast<uint64_t>(li) * p.x_lstride_b + static_cast<uint64_t>(w.tok[t]) * p.x_stride_b +
-            c0 * 512 + lane * 16;
+            lane * 16;
   auto ldx = [&](uint32_t c, uint4 (&xv)[T]) {
-    const bool valid = c < nc && (c0 + c) * 256 + lane * 8 < p.d_in;
+    const bool valid = c < nc && c * 256 + lane * 8 < p.d_in;
 #pragma unroll
     for (int t = 0; t < T; ++t)
       xv[t] = valid ? __ldg(reinterpret_cast<const uint4*>(xr[t] + c * 512)) : make_uint4(0u, 0u, 0u, 0u);
@@ -275,7 +278,7 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
     const uint32_t sb = ring + (c % LA) * R * 512;
 #pragma unroll
     for (int i = 0; i < R; ++i) {
-      ptx::cp_async_wait<kRing - 1>();  // unit (c, i) has landed
+      ptx::cp_async_wait<RG - 1>();  // unit (c, i) has landed
       const uint4 wv = lds16(sb + i * 512);
 #pragma unroll
       for (int t = 0; t < T; ++t) fh8(acc[i][t], wv, xv[t]);
@@ -294,11 +297,11 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
   if (warp_sum_owner<N>(lane) && k < static_cast<uint32_t>(R * T)) {
     const uint32_t i = k / T, t = k % T;
     if (i < w.n)
-      p.v[static_cast<uint64_t>(li) * p.vplane + w.voff + (slice * w.ntok + t) * w.rank + row0 + i] = sum;
+      p.v[static_cast<uint64_t>(li) * p.vplane + w.voff + t * w.rank + w.off + i] = sum;
   }
 }
 
-template <bool FAST>
+template <bool FAST, uint32_t RG>
 __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_shrink_kernel(const WArgs p) {
   extern __shared__ __align__(16) char smem[];
   ptx::pdl_launch_dependents();  // the expand may start loading its first weight rows
@@ -308,13 +311,13 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_shrink_ke
   const uint32_t li = blockIdx.x % p.n_layers;
   const uint32_t wi = (blockIdx.x / p.n_layers) * kWarps + warp;
   if (wi >= p.n_items) return;
-  const uint32_t ring = ptx::smem_u32(smem) + warp * kWarpSmem + lane * 16;
+  const uint32_t ring = ptx::smem_u32(smem) + warp * warp_smem(RG) + lane * 16;
   const WI w = load_item(p.items + wi);
   switch (w.ntok) {
-    case 1: shrink_item<1, FAST>(p, w, li, lane, ring); break;
-    case 2: shrink_item<2, FAST>(p, w, li, lane, ring); break;
-    case 3: shrink_item<3, FAST>(p, w, li, lane, ring); break;
-    default: shrink_item<4, FAST>(p, w, li, lane, ring); break;
+    case 1: shrink_item<1, FAST, RG>(p, w, li, lane, ring); break;
+    case 2: shrink_item<2, FAST, RG>(p, w, li, lane, ring); break;
+    case 3: shrink_item<3, FAST, RG>(p, w, li, lane, ring); break;
+    default: shrink_item<4, FAST, RG>(p, w, li, lane, ring); break;
   }
 }
 
@@ -322,11 +325,11 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_shrink_ke
 // Rows in blocks of 64 (lane k holds the page entries and v of rows jb + k and
 // jb + 32 + k); row j's NS units go to ring row slot j % DR, issued DR rows
 // ahead of their use.
-template <int T, int NS, bool FAST>
+template <int T, bool FAST, uint32_t RG>
 __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
                                             uint32_t ring) {
-  // NS: 16-byte column chunks per lane and row (the item's <= 256 · NS columns)
-  constexpr uint32_t DR = kRing / NS;     // ring depth in rows
+  constexpr int NS = kWarpCols(T) / 256;  // 16-byte column chunks per lane and row
+  constexpr uint32_t DR = RG / NS;        // ring depth in rows
   const uint32_t L = p.log2_page;
   const uint64_t pmask = (1ull << L) - 1;
   const uint64_t blk = p.blk_mult[w.pj] + static_cast<uint64_t>(li) * p.plu;
@@ -350,7 +353,7 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
   ptx::pdl_wait();  // v (the shrink launch) and y (earlier kernels)
   // the item's y pieces into the warp's y area: the oldest cp.async group, so
   // every later wait covers it
-  const uint32_t yarea = ring + kRing * 512;
+  const uint32_t yarea = ring + RG * 512;
 #pragma unroll
   for (int t = 0; t < T; ++t) {
     const char* yr = p.y[w.pj] + static_cast<uint64_t>(li) * p.y_lstride_b[w.pj] +
@@ -373,11 +376,7 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
         es[h] = static_cast<uint32_t>((sb + segb - 1) >> L) != pf ? __ldg(tab + pf + 1) : ef[h];
       }
 #pragma unroll
-      for (int t = 0; t < T; ++t) {
-        float v = 0.f;
-        for (uint32_t k = 0; k < p.ks && j < r; ++k) v += vb[(k * T + t) * r + j];  // slice order
-        vv[t][h] = v;
-      }
+      for (int t = 0; t < T; ++t) vv[t][h] = j < r ? vb[t * r + j] : 0.f;
     }
     const uint32_t nrow = min(64u, r - jb);
     auto issue = [&](uint32_t jj) {  // row jb + jj of the block (one group, possibly empty)
@@ -447,7 +446,7 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
   }
 }
 
-template <bool FAST>
+template <bool FAST, uint32_t RG>
 __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_expand_kernel(const WArgs p) {
   extern __shared__ __align__(16) char smem[];
   ptx::pdl_launch_dependents();
@@ -457,20 +456,13 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_expand_ke
   const uint32_t li = blockIdx.x % p.n_layers;
   const uint32_t wi = (blockIdx.x / p.n_layers) * kWarps + warp;
   if (wi >= p.n_items) return;
-  const uint32_t ring = ptx::smem_u32(smem) + warp * kWarpSmem + lane * 16;
+  const uint32_t ring = ptx::smem_u32(smem) + warp * warp_smem(RG) + lane * 16;
   const WI w = load_item(p.items + wi);
-  const bool narrow = w.n <= 256;
   switch (w.ntok) {
-    case 1:
-      if (narrow) expand_item<1, 1, FAST>(p, w, li, lane, ring);
-      else expand_item<1, 2, FAST>(p, w, li, lane, ring);
-      break;
-    case 2:
-      if (narrow) expand_item<2, 1, FAST>(p, w, li, lane, ring);
-      else expand_item<2, 2, FAST>(p, w, li, lane, ring);
-      break;
-    case 3: expand_item<3, 1, FAST>(p, w, li, lane, ring); break;
-    default: expand_item<4, 1, FAST>(p, w, li, lane, ring); break;
+    case 1: expand_item<1, FAST, RG>(p, w, li, lane, ring); break;
+    case 2: expand_item<2, FAST, RG>(p, w, li, lane, ring); break;
+    case 3: expand_item<3, FAST, RG>(p, w, li, lane, ring); break;
+    default: expand_item<4, FAST, RG>(p, w, li, lane, ring); break;
   }
 }
 
@@ -505,7 +497,6 @@ void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0
   a.plu = gm.per_layer_unit;
   a.v = plan.d_wv;
   a.vplane = w.vplane;
-  a.ks = w.ks;
   a.scale = scale;
   // shuffle-resolved page entries: a shrink row spans <= 32 pages and an
   // expand block (<= 1 KiB) <= 2 pages
@@ -517,30 +508,34 @@ void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cudaLaunchConfig_t cfg{};
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = stream;
-  set_smem_once(reinterpret_cast<const void*>(bgmv_warp_shrink_kernel<true>), kSmem);
-  set_smem_once(reinterpret_cast<const void*>(bgmv_warp_shrink_kernel<false>), kSmem);
-  set_smem_once(reinterpret_cast<const void*>(bgmv_warp_expand_kernel<true>), kSmem);
-  set_smem_once(reinterpret_cast<const void*>(bgmv_warp_expand_kernel<false>), kSmem);
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  a.items = plan.d_witems + w.s_off;
-  a.n_items = w.ns;
-  cfg.gridDim = dim3((w.ns + kWarps - 1) / kWarps * n_layers);
-  if (fast)
-    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_warp_shrink_kernel<true>, a));
-  else
-    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_warp_shrink_kernel<false>, a));
-  count_launch();
-  a.items = plan.d_witems + w.e_off;
-  a.n_items = w.ne;
-  cfg.gridDim = dim3((w.ne + kWarps - 1) / kWarps * n_layers);
-  if (fast)
-    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_warp_expand_kernel<true>, a));
-  else
-    PLORA_CUDA(cudaLaunchKernelEx(&cfg, bgmv_warp_expand_kernel<false>, a));
-  count_launch();
+  const bool deep = n_layers == 1;
+  cfg.dynamicSmemBytes = cta_smem(deep ? kDeepRing : kRing);
+  auto launch = [&](auto k16, auto k32, uint32_t n_items, const WarpItem* items) {
+    a.items = items;
+    a.n_items = n_items;
+    cfg.gridDim = dim3((n_items + kWarps - 1) / kWarps * n_layers);
+    const void* k = deep ? reinterpret_cast<const void*>(k32) : reinterpret_cast<const void*>(k16);
+    set_smem_once(k, static_cast<int>(cfg.dynamicSmemBytes));
+    if (deep)
+      PLORA_CUDA(cudaLaunchKernelEx(&cfg, k32, a));
+    else
+      PLORA_CUDA(cudaLaunchKernelEx(&cfg, k16, a));
+    count_launch();
+  };
+  if (fast) {
+    launch(bgmv_warp_shrink_kernel<true, kRing>, bgmv_warp_shrink_kernel<true, kDeepRing>, w.ns,
+           plan.d_witems + w.s_off);
+    launch(bgmv_warp_expand_kernel<true, kRing>, bgmv_warp_expand_kernel<true, kDeepRing>, w.ne,
+           plan.d_witems + w.e_off);
+  } else {
+    launch(bgmv_warp_shrink_kernel<false, kRing>, bgmv_warp_shrink_kernel<false, kDeepRing>, w.ns,
+           plan.d_witems + w.s_off);
+    launch(bgmv_warp_expand_kernel<false, kRing>, bgmv_warp_expand_kernel<false, kDeepRing>, w.ne,
+           plan.d_witems + w.e_off);
+  }
 }
 
 }  // namespace plora

@@ -9,7 +9,7 @@ rows=[r for r in csv.reader(open('gpurun_out/l.csv')) if len(r)>5]
 h=rows[0]; ki=h.index('Kernel Name'); vi=h.index('Metric Value'); gi=h.index('Grid Size')
 dd=collections.defaultdict(list)
 for r in rows[1:]:
-    try: dd[(r[ki][30:58], r[gi])].append(float(r[vi].replace(',','')))
+    try: dd[(r[ki][25:60], r[gi])].append(float(r[vi].replace(',','')))
     except: pass
 for k,v in dd.items(): print(k, len(v), round(sum(v)/len(v)/1000,2), 'us')
 PY
