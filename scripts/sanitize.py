@@ -1,5 +1,7 @@
 """Small paged-LoRA calls for compute-sanitizer (memcheck / racecheck /
-synccheck): the cluster BGMV (per projection, fused per layer, multi-layer),
+synccheck): the warp-item BGMV (the default: per projection, per layer,
+multi-layer; 1-4 token jobs; 256 B pages, odd widths), the cluster BGMV and
+the hybrid pair (per projection, fused per layer, multi-layer),
 the streaming BGMV (4- and 8-token jobs), the SGMV (per projection, per layer,
 fused with the base GEMM, 512 B and 1 KiB pages), the TP halves (NCCL-style
 and with the fused peer-write all-gather), decode batches with a routed
@@ -55,8 +57,30 @@ def main():
     xl = torch.randn(2, T, 4096, device="cuda").to(torch.bfloat16)
     yl = torch.randn(2, 2, T, 4096, device="cuda").to(torch.bfloat16)
     bgmv_layers(plan, 0, xl, [yl[:, 0], yl[:, 1]])
-    # streaming decode kernel, 4- and 8-token jobs
     from paper_2512_20210_b200 import _native as N
+    # warp items: jobs of 1..4 tokens (6 tokens per adapter -> 3 + 3), 256 B
+    # pages (page entries by table loads) and widths that are not multiples
+    # of 256 / 512
+    from paper_2512_20210_b200.lora import ModelShape
+    for tpa in (1, 3, 6):
+        tan = synth.token_assignment(cfg.n_adapters, tpa)
+        xn = torch.randn(len(tan), 4096, device="cuda").to(torch.bfloat16)
+        yn = [torch.randn(len(tan), 4096, device="cuda").to(torch.bfloat16) for _ in range(2)]
+        bgmv_layer(BatchPlan(s.store, tan), 1, xn, yn)
+    shp = ModelShape(2, (1000, 1000), (520, 1048), torch.bfloat16)
+    sw = Setup(synth.DecodeConfig("san_w", shp, [5, 16, 64, 33], 2, 256))
+    taw = synth.token_assignment(4, 2)
+    xw = torch.randn(len(taw), 1000, device="cuda").to(torch.bfloat16)
+    bgmv_layer(BatchPlan(sw.store, taw), 1, xw, [torch.randn(len(taw), 520, device="cuda").to(torch.bfloat16),
+                                                torch.randn(len(taw), 1048, device="cuda").to(torch.bfloat16)])
+    # cluster kernel and the hybrid pair
+    for impl in (2, 3):
+        N.check(N.lib().plora_debug_set_bgmv_impl(impl))
+        pc = BatchPlan(s.store, ta)
+        bgmv(pc, 1, 0, x, ys[0])
+        bgmv_layer(pc, 0, x, ys)
+        bgmv_layers(pc, 0, xl, [yl[:, 0], yl[:, 1]])
+    # streaming decode kernel, 4- and 8-token jobs
     N.check(N.lib().plora_debug_set_bgmv_impl(1))
     bgmv_layer(plan, 1, x, ys)
     ta8 = synth.token_assignment(cfg.n_adapters, 6)
