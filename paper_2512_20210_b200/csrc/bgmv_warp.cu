@@ -48,6 +48,7 @@ struct WArgs {
   const WarpItem* items;  // this launch's S or E items
   uint32_t n_items;
   uint32_t n_layers;  // layers of this launch (grid = item blocks × n_layers)
+  uint32_t ks;        // K slices of the S items (v partial planes per job)
   uint32_t d_in;
   uint32_t log2_page;
   uint32_t fast;  // page entries by warp shuffle (rows / blocks span few pages)
@@ -223,8 +224,12 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
   const uint64_t pmask = (1ull << L) - 1;
   const uint64_t blk = p.blk_mult[w.pj] + static_cast<uint64_t>(li) * p.plu;
   const uint32_t rowb = p.d_in * 2;
-  const uint64_t a0 = (static_cast<uint64_t>(w.rank) * blk + static_cast<uint64_t>(w.off) * p.d_in) * 2;
-  const uint32_t nc = (p.d_in + 255) / 256;  // 512-byte chunks per row (the last may be partial)
+  const uint32_t row0 = w.off & 0xffffu, slice = w.off >> 16;
+  const uint32_t ncall = (p.d_in + 255) / 256;  // 512-byte chunks per row (the last may be partial)
+  const uint32_t cps = (ncall + p.ks - 1) / p.ks;
+  const uint32_t c0 = slice * cps, nc = min(ncall, c0 + cps) - c0;  // this item's chunks [c0, c0 + nc)
+  const uint32_t kin = min(p.d_in, (c0 + nc) * 256) - c0 * 256;     // its inputs
+  const uint64_t a0 = (static_cast<uint64_t>(w.rank) * blk + static_cast<uint64_t>(row0) * p.d_in + c0 * 256ull) * 2;
   const uint32_t* tab = p.table + w.toff;
   // page entries: lane k holds the entry of row i's k-th page
   uint32_t ent[R], pg0[R];
@@ -234,7 +239,7 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
     pg0[i] = static_cast<uint32_t>(rb >> L);
     ent[i] = 0u;
     if (FAST) {
-      const uint32_t span = static_cast<uint32_t>((rb + rowb - 1) >> L) - pg0[i];
+      const uint32_t span = static_cast<uint32_t>((rb + kin * 2 - 1) >> L) - pg0[i];
       if (static_cast<uint32_t>(i) < w.n && lane <= span) ent[i] = __ldg(tab + pg0[i] + lane);
     }
   }
@@ -243,7 +248,7 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
     const uint32_t pg = static_cast<uint32_t>(off >> L);
     uint32_t e = 0u;
     if (FAST) e = __shfl_sync(0xffffffffu, ent[i], (pg - pg0[i]) & 31u);
-    const bool valid = static_cast<uint32_t>(i) < w.n && c < nc && c * 256 + lane * 8 < p.d_in;
+    const bool valid = static_cast<uint32_t>(i) < w.n && c < nc && c * 256 + lane * 8 < kin;
     if (!FAST && valid) e = __ldg(tab + pg);
     cpa16(ring + ((c % LA) * R + i) * 512, valid ? p.arena + (static_cast<uint64_t>(e) << L) + (off & pmask) : p.arena,
           valid);
@@ -257,9 +262,9 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
 #pragma unroll
   for (int t = 0; t < T; ++t)
     xr[t] = p.x + static_cast<uint64_t>(li) * p.x_lstride_b + static_cast<uint64_t>(w.tok[t]) * p.x_stride_b +
-            lane * 16;
+            c0 * 512 + lane * 16;
   auto ldx = [&](uint32_t c, uint4 (&xv)[T]) {
-    const bool valid = c < nc && c * 256 + lane * 8 < p.d_in;
+    const bool valid = c < nc && c * 256 + lane * 8 < kin;
 #pragma unroll
     for (int t = 0; t < T; ++t)
       xv[t] = valid ? __ldg(reinterpret_cast<const uint4*>(xr[t] + c * 512)) : make_uint4(0u, 0u, 0u, 0u);
@@ -297,7 +302,7 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
   if (warp_sum_owner<N>(lane) && k < static_cast<uint32_t>(R * T)) {
     const uint32_t i = k / T, t = k % T;
     if (i < w.n)
-      p.v[static_cast<uint64_t>(li) * p.vplane + w.voff + t * w.rank + w.off + i] = sum;
+      p.v[static_cast<uint64_t>(li) * p.vplane + w.voff + (slice * w.ntok + t) * w.rank + row0 + i] = sum;
   }
 }
 
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_shrink_ke
 // Rows in blocks of 64 (lane k holds the page entries and v of rows jb + k and
 // jb + 32 + k); row j's NS units go to ring row slot j % DR, issued DR rows
 // ahead of their use.
-template <int T, bool FAST, uint32_t RG>
+template <int T, bool FAST, uint32_t RG, uint32_t KS>
 __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
                                             uint32_t ring) {
   constexpr int NS = kWarpCols(T) / 256;  // 16-byte column chunks per lane and row
@@ -377,6 +382,18 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
       }
 #pragma unroll
       for (int t = 0; t < T; ++t) vv[t][h] = j < r ? vb[t * r + j] : 0.f;
+      // the K-slice partials of v, summed in slice order (KS: compile-time
+      // slice count, 0 = the launch's p.ks; the expand's code is sensitive to
+      // anything around these loads, so the one-slice body has none)
+      if (KS == 2 && j < r) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) vv[t][h] += vb[(T + t) * r + j];
+      }
+      if (KS == 0 && j < r) {
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+          for (uint32_t k = 1; k < p.ks; ++k) vv[t][h] += vb[(k * T + t) * r + j];
+      }
     }
     const uint32_t nrow = min(64u, r - jb);
     auto issue = [&](uint32_t jj) {  // row jb + jj of the block (one group, possibly empty)
@@ -446,7 +463,7 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
   }
 }
 
-template <bool FAST, uint32_t RG>
+template <bool FAST, uint32_t RG, uint32_t KS>
 __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_expand_kernel(const WArgs p) {
   extern __shared__ __align__(16) char smem[];
   ptx::pdl_launch_dependents();
@@ -459,10 +476,10 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_expand_ke
   const uint32_t ring = ptx::smem_u32(smem) + warp * warp_smem(RG) + lane * 16;
   const WI w = load_item(p.items + wi);
   switch (w.ntok) {
-    case 1: expand_item<1, FAST, RG>(p, w, li, lane, ring); break;
-    case 2: expand_item<2, FAST, RG>(p, w, li, lane, ring); break;
-    case 3: expand_item<3, FAST, RG>(p, w, li, lane, ring); break;
-    default: expand_item<4, FAST, RG>(p, w, li, lane, ring); break;
+    case 1: expand_item<1, FAST, RG, KS>(p, w, li, lane, ring); break;
+    case 2: expand_item<2, FAST, RG, KS>(p, w, li, lane, ring); break;
+    case 3: expand_item<3, FAST, RG, KS>(p, w, li, lane, ring); break;
+    default: expand_item<4, FAST, RG, KS>(p, w, li, lane, ring); break;
   }
 }
 
@@ -497,6 +514,7 @@ void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0
   a.plu = gm.per_layer_unit;
   a.v = plan.d_wv;
   a.vplane = w.vplane;
+  a.ks = w.ks;
   a.scale = scale;
   // shuffle-resolved page entries: a shrink row spans <= 32 pages and an
   // expand block (<= 1 KiB) <= 2 pages
@@ -525,17 +543,23 @@ void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0
       PLORA_CUDA(cudaLaunchKernelEx(&cfg, k16, a));
     count_launch();
   };
-  if (fast) {
+  if (fast)
     launch(bgmv_warp_shrink_kernel<true, kRing>, bgmv_warp_shrink_kernel<true, kDeepRing>, w.ns,
            plan.d_witems + w.s_off);
-    launch(bgmv_warp_expand_kernel<true, kRing>, bgmv_warp_expand_kernel<true, kDeepRing>, w.ne,
-           plan.d_witems + w.e_off);
-  } else {
+  else
     launch(bgmv_warp_shrink_kernel<false, kRing>, bgmv_warp_shrink_kernel<false, kDeepRing>, w.ns,
            plan.d_witems + w.s_off);
-    launch(bgmv_warp_expand_kernel<false, kRing>, bgmv_warp_expand_kernel<false, kDeepRing>, w.ne,
-           plan.d_witems + w.e_off);
-  }
+  const WarpItem* ei = plan.d_witems + w.e_off;
+  if (fast && w.ks == 1)
+    launch(bgmv_warp_expand_kernel<true, kRing, 1>, bgmv_warp_expand_kernel<true, kDeepRing, 1>, w.ne, ei);
+  else if (fast && w.ks == 2)
+    launch(bgmv_warp_expand_kernel<true, kRing, 2>, bgmv_warp_expand_kernel<true, kDeepRing, 2>, w.ne, ei);
+  else if (fast)
+    launch(bgmv_warp_expand_kernel<true, kRing, 0>, bgmv_warp_expand_kernel<true, kDeepRing, 0>, w.ne, ei);
+  else if (w.ks == 1)
+    launch(bgmv_warp_expand_kernel<false, kRing, 1>, bgmv_warp_expand_kernel<false, kDeepRing, 1>, w.ne, ei);
+  else
+    launch(bgmv_warp_expand_kernel<false, kRing, 0>, bgmv_warp_expand_kernel<false, kDeepRing, 0>, w.ne, ei);
 }
 
 }  // namespace plora

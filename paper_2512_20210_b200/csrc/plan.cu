@@ -658,6 +658,10 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       // measured slower for the 32-layer step, 0.339 vs 0.320 ms of shrink,
       // and barely faster per layer, profiles/r02n_warp_variants.txt)
       w.ks = 1;
+      // K slices of <= 4096 inputs (16 chunks of 512 bytes per lane row):
+      // 8-row items of at most 64 KiB, so wide layers still give every SM
+      // several items (cfg5's 8192-wide q / v: two slices)
+      w.ks = (g.m.d_in[projs[0]] + 4095) / 4096;
       uint64_t voff = 0;
       std::vector<WarpItem> S, E;
       for (uint32_t i = 0; i < np; ++i) {
@@ -668,10 +672,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
           base.v_off = static_cast<uint32_t>(voff);
           for (uint32_t t = 0; t < kWarpJobTok; ++t) base.tok[t] = t < j.ntok ? j.tok[t] : 0u;
           auto meta = [&](uint32_t n) { return j.rank | (j.ntok << 9) | (i << 12) | (n << 16); };
-          const uint32_t R = kWarpRows(j.ntok);
-          // (256-column blocks for wide adapters measured slower: 515 vs 367 us
-          // of expand per 32-layer step, profiles/r02n_warp_variants.txt)
-          const uint32_t C = kWarpCols(j.ntok);
+          const uint32_t R = kWarpRows(j.ntok), C = kWarpCols(j.ntok);
           for (uint32_t k = 0; k < w.ks; ++k)
             for (uint32_t r0 = 0; r0 < j.rank; r0 += R) {
               WarpItem it = base;

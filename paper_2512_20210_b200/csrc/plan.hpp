@@ -213,7 +213,7 @@ struct WarpItem {  // 32 bytes, self-contained
   uint32_t table_off;  // adapter's first entry in the device page table
   uint32_t meta;       // rank (bits 0-8) | ntok (9-11) | launch projection (12-15) | n (16-31)
   uint32_t off;        // S: first rank row | K slice << 16; E: first output column
-  uint32_t v_off;      // floats into the launch's per-layer v plane: the job's [ntok][rank] block
+  uint32_t v_off;      // floats into the launch's per-layer v plane: the job's [ks][ntok][rank] block
   uint32_t tok[kWarpJobTok];
 };
 static_assert(sizeof(WarpItem) == 32, "WarpItem layout");

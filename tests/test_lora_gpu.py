@@ -397,3 +397,36 @@ def test_streaming_kernel_parity(cuda, tokens_per_adapter):
         assert rel_err(yl[1, 0], s.oracle(2, 0, x, y0, ta)) <= TOL_BF16
     finally:
         N.check(N.lib().plora_debug_set_bgmv_impl(0))
+
+
+@pytest.mark.parametrize("page_bytes", [256, 2048])
+def test_warp_items_token_counts_and_odd_widths(cuda, page_bytes):
+    """The default warp-item op (bgmv_warp.cu): adapters with 1..7 tokens
+    (jobs of 1-4 tokens: the four shrink / expand bodies, and a 5-7-token
+    adapter split evenly over two jobs), widths that are not multiples of 256
+    (partial 512-byte chunks) or of the expand block, ranks 1..80, 256-byte
+    pages (page entries by table loads) and 2 KiB pages (by shuffle); -1
+    tokens untouched; bgmv and bgmv_layer agree bit for bit."""
+    from paper_2512_20210_b200.lora import bgmv_layer
+    shape = ModelShape(3, (1000, 1000), (520, 1048), torch.bfloat16)
+    ranks = [1, 5, 16, 33, 64, 80, 8, 24]
+    s = Setup(synth.DecodeConfig("warp_edge", shape, ranks, 1, page_bytes))
+    rng = np.random.default_rng(7)
+    ta = np.concatenate([np.full(1 + a % 7, a, np.int32) for a in range(len(ranks))] + [np.full(5, -1, np.int32)])
+    rng.shuffle(ta)
+    T = len(ta)
+    x = synth.activations(T, 1000, torch.bfloat16, "x", salt=3)
+    y0 = [synth.activations(T, shape.d_out[p], torch.bfloat16, "y", salt=3 + p) for p in range(2)]
+    plan = BatchPlan(s.store, ta)
+    ys = [y.cuda() for y in y0]
+    bgmv_layer(plan, 2, x.cuda(), ys, 0.5)
+    sep = [y.cuda() for y in y0]
+    for p in range(2):
+        bgmv(plan, 2, p, x.cuda(), sep[p], 0.5)
+    torch.cuda.synchronize()
+    for p in range(2):
+        assert torch.equal(ys[p], sep[p]), p
+        ref = s.oracle(2, p, x, y0[p], ta, scale=0.5)
+        assert rel_err(ys[p], ref) <= TOL_BF16, p
+        none = ta < 0
+        assert np.array_equal(to_np_bits(ys[p])[none], to_np_bits(y0[p])[none])
