@@ -309,24 +309,22 @@ int plora_bgmv(plora_plan* plan, uint32_t layer, uint32_t proj, const void* x,
                plora_stream_t stream);
 /* Every projection p of `layer` at once (they read the same x, as q/k/v of
  * an attention block do): ys[p] += scale · (x · A_pᵀ) · B_pᵀ with row stride
- * y_strides[p].  One launch when the projections have equal shapes (the
- * per-call fixed cost is paid once per layer), else one per projection. */
+ * y_strides[p].  bf16 stores with equal input widths: one shrink launch and
+ * one expand launch for all projections (bgmv_warp.cu), bit-identical to
+ * per-projection plora_bgmv calls; else one plora_bgmv per projection. */
 int plora_bgmv_layer(plora_plan* plan, uint32_t layer, const void* x, uint64_t x_stride,
                      void* const* ys, const uint64_t* y_strides, float scale,
                      plora_stream_t stream);
-/* Layers [layer0, layer0 + n_layers) of plora_bgmv_layer in one launch, for
+/* Layers [layer0, layer0 + n_layers) of plora_bgmv_layer in one call, for
  * inputs that are all ready (a LoRA-only decode step, speculative/multi-layer
- * batching): the decode clusters stay resident and stream layer l+1's pages
- * right behind layer l's, so the per-launch prologue / drain / CTA
- * turnaround is paid once.  Layer layer0 + i reads x + i·x_layer_stride and
- * updates ys[p] + i·y_layer_strides[p] (all strides in elements).  On GPUs
- * whose SM count leaves SMs outside the 4-CTA clusters (148 - 132 on B200)
- * the plan gives a byte-proportional share of the adapters to the streaming
- * kernel, which runs on those SMs concurrently (an internal aux stream, fork /
- * join by events, so `stream` orders after both).  Deterministic; equal to
- * n_layers plora_bgmv_layer calls within the bf16 tolerance, bit for bit
- * with plora_debug_set_bgmv_impl(2) (clusters only).  bf16 stores with equal
- * projection shapes; otherwise one plora_bgmv_layer per layer. */
+ * batching): one shrink launch and one expand launch cover every layer
+ * (bgmv_warp.cu; the layers' work items interleaved, heaviest first), so the
+ * per-launch ramp and drain are paid once.  Layer layer0 + i reads
+ * x + i·x_layer_stride and updates ys[p] + i·y_layer_strides[p] (all strides
+ * in elements).  Deterministic and bit for bit equal to n_layers
+ * plora_bgmv_layer calls.  bf16 stores with equal input widths; otherwise one
+ * plora_bgmv_layer per layer.  (plora_debug_set_bgmv_impl selects the
+ * cluster kernel or the round-2 hybrid pair of clusters + streaming kernel.) */
 int plora_bgmv_layers(plora_plan* plan, uint32_t layer0, uint32_t n_layers, const void* x,
                       uint64_t x_stride, uint64_t x_layer_stride, void* const* ys,
                       const uint64_t* y_strides, const uint64_t* y_layer_strides, float scale,
