@@ -57,6 +57,7 @@ namespace {
 using namespace plora::tmap;
 
 uint32_t g_sgmv_dbg = 0;  // plora_debug_set_sgmv_flags
+constexpr uint32_t kDbgPersistentExpand = 1u << 20;  // run the persistent expand (measured slower) instead of the tiled one
 
 constexpr uint32_t kTileM = 128;
 constexpr uint32_t kChunkK = 64;   // shrink K per stage (one 128-byte swizzle row)
@@ -473,6 +474,8 @@ struct ExpandArgs {
   uint32_t d_out;
   uint32_t n_tiles;
   uint32_t ngroups;  // column groups per tile
+  uint32_t np;       // projections of the call (persistent expand)
+  uint64_t* trace;   // diagnostics (plora_debug_set_trace): [cta][block < kPTrace][8] SM clocks, or nullptr
   float scale;
   uint32_t dbg;  // diagnostics: 64 no y reduce-add, 128 no Bᵀ gather, 256 no MMA, 512 prologue only
   uint32_t g4;   // pages >= 256 B: Bᵀ rows by TMA gather4 (see ShrinkArgs::g4)
@@ -706,6 +709,322 @@ __global__ void __launch_bounds__(kEThreads, 2)
   }
 }
 
+// ------------------------------------------------------- persistent expand
+// An alternative to sgmv_expand_kernel, selected by plora_debug_set_sgmv_flags
+// bit 20 and measured SLOWER at cfg3 (layer call 173 vs 165 us,
+// profiles/r02o_sgmv_persistent_expand.txt): its per-block pipeline (Bᵀ
+// gather4 latency ~1.6 us under load, ~0.45 us of epilogue per block on the
+// critical chain) ends up serial per SM, where the tiled grid's two resident
+// CTAs per SM overlap one CTA's setup and drain with the other's blocks.
+// One CTA per SM walks a contiguous range of the call's
+// 64-column output blocks, ordered (proj, tile, block) — ~111 blocks per SM at
+// cfg3 — so the per-CTA setup (barriers, TMEM, the first V load) and the final
+// drain are paid once per SM instead of once per 512 columns, and the block
+// pipeline runs kPStages deep across tile boundaries:
+//   warp 0      TMA of the V tiles, two stages (the next tile's V streams
+//               while the current tile's blocks run)
+//   warps 1-8   Bᵀ block gathers into kPStages stages: groups of four rows
+//               by TMA gather4, spread round-robin over the eight warps (a
+//               warp issues its lanes' TMA ops one after another, ~84 cycles
+//               each), the remaining rows by 16-byte cp.async
+//   warps 9-16  epilogue, two groups of four warps taking alternate blocks:
+//               TMEM -> bf16(scale · D) -> staging buffer -> TMA reduce-add
+//               into y
+//   warp 17     MMA issuer into kPStages TMEM accumulators of 64 columns
+// Same arithmetic as sgmv_expand_kernel (bit-identical y).
+constexpr uint32_t kPStages = 6;      // Bᵀ block stages (gather4 latency under load is ~1.6 us)
+constexpr uint32_t kPAcc = 4;         // TMEM accumulators of 64 columns (k % 4; group k % 2)
+constexpr uint32_t kPGatherWarps = 8;
+constexpr uint32_t kPGather = kPGatherWarps * 32;
+constexpr uint32_t kPEpi0 = 1 + kPGatherWarps;  // first epilogue warp
+constexpr uint32_t kPMma = kPEpi0 + 8;
+constexpr int kPThreads = (kPMma + 1) * 32;
+constexpr uint32_t kPVStages = 3;  // V tiles in flight: a unit's V loads two units ahead
+struct PSmem {  // ~225 KB: one CTA per SM
+  static constexpr uint32_t v = 0;                        // [kPVStages][2 atoms][128 rows × 128 B] SW128
+  static constexpr uint32_t y = v + kPVStages * 32768;    // [8 epilogue warps][32 rows × 128 B] SW128
+  static constexpr uint32_t b = y + 8 * 4096;             // [kPStages][r16 × 128 B] MN-major SW128
+  static constexpr uint32_t bars = b + kPStages * 16384;
+  // v_full[V], v_empty[V], b_full[S], b_empty[S], acc_full[A], acc_empty[A]
+  static constexpr uint32_t n_bars = 2 * kPVStages + 2 * kPStages + 2 * kPAcc;
+  static constexpr uint32_t tmem_slot = bars + n_bars * 8;
+  static constexpr uint32_t total = tmem_slot + 8;
+  static constexpr uint32_t alloc = total + 1024;
+};
+static_assert(PSmem::alloc <= 232448, "persistent expand shared memory");
+constexpr uint32_t kPTrace = 128;
+__device__ __forceinline__ void ptrace(const ExpandArgs& p, uint32_t k, int f) {
+  if (p.trace && k < kPTrace) p.trace[(blockIdx.x * kPTrace + k) * 8 + f] = clock64();
+}
+
+// Work units: (proj, tile, group of kPUnitBlocks 64-column blocks), dealt
+// round-robin to the CTAs (unit i to CTA i mod grid), so at any moment the
+// CTAs work on a window of ~grid consecutive units — a few segments, whose
+// Bᵀ rows the neighbouring CTAs read from L2 — as the round-1 tiled grid did
+// (dealing contiguous ranges spread the CTAs over every tile at once and
+// tripled the gather time).
+constexpr uint32_t kPUnitBlocks = 4;
+struct Unit {
+  uint32_t tile, pj, b0, b1;  // tile, projection, block range [b0, b1)
+  __device__ void set(uint32_t ui, uint32_t ngrp, uint32_t nbt, uint32_t n_tiles) {
+    const uint32_t tu = ui / ngrp, grp = ui - tu * ngrp;
+    pj = tu / n_tiles;
+    tile = tu - pj * n_tiles;
+    b0 = grp * kPUnitBlocks;
+    b1 = min(nbt, b0 + kPUnitBlocks);
+  }
+};
+
+__global__ void __launch_bounds__(kPThreads, 1)
+    sgmv_expand_persistent_kernel(const ExpandArgs p, const __grid_constant__ CUtensorMap tmap_y0,
+                                  const __grid_constant__ CUtensorMap tmap_y1,
+                                  const __grid_constant__ CUtensorMap tmap_v,
+                                  const __grid_constant__ CUtensorMap tmap_arena) {
+  extern __shared__ char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* v_full = reinterpret_cast<uint64_t*>(smem + PSmem::bars);
+  uint64_t* v_empty = v_full + kPVStages;
+  uint64_t* b_full = v_empty + kPVStages;
+  uint64_t* b_empty = b_full + kPStages;
+  uint64_t* acc_full = b_empty + kPStages;
+  uint64_t* acc_empty = acc_full + kPAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + PSmem::tmem_slot);
+
+  const uint32_t nbt = p.d_out / kEBlockN;  // blocks per tile row
+  const uint32_t ngrp = (nbt + kPUnitBlocks - 1) / kPUnitBlocks;
+  const uint32_t n_units = p.np * p.n_tiles * ngrp;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < kPVStages; ++i) {
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
+    }
+    for (uint32_t i = 0; i < kPStages; ++i) {
+      // gather4 mode: one arrival per gather warp (after its lanes' expect_tx);
+      // otherwise every gather thread's cp.async completion arrives
+      ptx::mbar_init(&b_full[i], p.g4 ? kPGatherWarps : kPGather);
+      ptx::mbar_init(&b_empty[i], 1);
+    }
+    for (uint32_t i = 0; i < kPAcc; ++i) {
+      ptx::mbar_init(&acc_full[i], 1);
+      ptx::mbar_init(&acc_empty[i], kEEpiThreads / 32);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == kPEpi0) ptx::tmem_alloc(tmem_slot, kPAcc * kEBlockN);
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmap_y0);
+    ptx::prefetch_tmap(&tmap_y1);
+    ptx::prefetch_tmap(&tmap_v);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  Unit un;
+
+  if (p.dbg & 512u) {
+  } else if (warp == 0) {
+    // ------------------------------------ TMA: the V tile of each unit
+    if (lane == 0) {
+      ptx::pdl_wait();  // V comes from the shrink (and y may be read by earlier kernels)
+      uint32_t vi = 0;
+      for (uint32_t ui = blockIdx.x; ui < n_units; ui += gridDim.x, ++vi) {
+        un.set(ui, ngrp, nbt, p.n_tiles);
+        const uint32_t vs = vi % kPVStages, vph = (vi / kPVStages) & 1u;
+        const uint32_t r16 = (p.tiles[un.tile].rank + 15) & ~15u;
+        const uint32_t vboxes = r16 > 64 ? 2 : 1;
+        ptx::mbar_wait(&v_empty[vs], vph ^ 1u);
+        ptx::mbar_arrive_expect_tx(&v_full[vs], vboxes * 16384);
+        for (uint32_t bx = 0; bx < vboxes; ++bx)
+          ptx::tma_load_2d(smem + PSmem::v + vs * 32768 + bx * 16384, &tmap_v, static_cast<int32_t>(bx * 64),
+                           static_cast<int32_t>((un.pj * p.n_tiles + un.tile) * kTileM), &v_full[vs]);
+      }
+    }
+  } else if (warp <= kPGatherWarps) {
+    // ----------------------------------- Bᵀ block gathers (paged rows)
+    // gather4 mode (pages >= 256 B): lane l of gather warp w issues the
+    // gather4 of row group q = l · 8 + w (rows 4q..4q+3, looked up by itself;
+    // a warp issues its lanes' TMA ops one after another, so the groups are
+    // spread over all eight warps).  Rows r..r16-1 (zero V columns) get
+    // copies of row r - 1: finite values, so they add exact zeros.
+    // Completion is all transaction bytes plus one arrival per warp.
+    // Otherwise thread gt copies row gt by cp.async (zero-filled padding) and
+    // every thread's completion arrives.  Page entries are cached per row and
+    // logical page (a 2 KiB page holds 16 blocks of a row).
+    const uint32_t gt = threadIdx.x - 32, gw = warp - 1;
+    const uint32_t q = lane * kPGatherWarps + gw;
+    const bool fast = p.log2_page >= 7;  // a row's 128-byte block slice lies in one page
+    const uint64_t pmask = (1ull << p.log2_page) - 1;
+    uint64_t rowoff[5];  // the rows' offsets at block 0: group q's four, row gt
+    uint32_t lp[5], le[5];
+    uint32_t k = 0;
+    for (uint32_t ui = blockIdx.x; ui < n_units; ui += gridDim.x) {
+      un.set(ui, ngrp, nbt, p.n_tiles);
+      const SgmvTile t = p.tiles[un.tile];
+      const uint32_t r = t.rank, r16 = (r + 15) & ~15u;
+      const uint64_t bt = (static_cast<uint64_t>(r) * (un.pj ? p.blk_mult[1] : p.blk_mult[0]) +
+                           static_cast<uint64_t>(r) * p.d_in) * 2;
+#pragma unroll
+      for (uint32_t i = 0; i < 4; ++i) rowoff[i] = bt + static_cast<uint64_t>(min(q * 4 + i, r - 1)) * p.d_out * 2;
+      rowoff[4] = bt + static_cast<uint64_t>(gt) * p.d_out * 2;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) lp[i] = ~0u;
+      auto entry = [&](int i, uint64_t off) {
+        const uint32_t pg = static_cast<uint32_t>(off >> p.log2_page);
+        if (pg != lp[i]) {
+          lp[i] = pg;
+          le[i] = __ldg(p.table + t.table_off + pg);
+        }
+        return le[i];
+      };
+      for (uint32_t b = un.b0; b < un.b1; ++b, ++k) {
+        const uint32_t st = k % kPStages, ph = (k / kPStages) & 1u;
+        const uint32_t cb = b * kEBlockN * 2;  // the block's byte offset in a row
+        int32_t row[4];
+        if (p.g4 && q * 4 < r16) {  // (looked up before the stage wait)
+#pragma unroll
+          for (uint32_t i = 0; i < 4; ++i) {
+            const uint64_t off = rowoff[i] + cb;
+            row[i] = static_cast<int32_t>(((static_cast<uint64_t>(entry(i, off)) << p.log2_page) + (off & pmask)) >> 7);
+          }
+        }
+        ptx::mbar_wait(&b_empty[st], ph ^ 1u);
+        if (gt == 0) ptrace(p, k, 0);
+        char* bs = smem + PSmem::b + st * 16384;
+        if (p.g4) {
+          if (q * 4 < r16 && !(p.dbg & 128u)) {
+            ptx::mbar_expect_tx(&b_full[st], 4 * kEBlockN * 2);
+            ptx::tma_gather4(bs + q * 4 * kEBlockN * 2, &tmap_arena, 0, row[0], row[1], row[2], row[3], &b_full[st]);
+          }
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&b_full[st]);
+        } else {
+          const uint32_t j = gt;
+          if (j < r16 && !(p.dbg & 128u)) {
+            const uint64_t off = rowoff[4] + cb;
+            const PagedSrc src{p.arena, p.table, t.table_off, p.log2_page};
+            const char* base = fast && j < r ? p.arena + (static_cast<uint64_t>(entry(4, off)) << p.log2_page) + (off & pmask)
+                                             : p.arena;
+#pragma unroll
+            for (uint32_t c = 0; c < 8; ++c) {
+              char* dst = bs + swz(j, c);
+              if (j >= r)
+                ptx::cp_async_16(dst, p.arena, 0);
+              else if (fast)
+                ptx::cp_async_16(dst, base + c * 16, 16);
+              else
+                ptx::cp_async_16(dst, src.at(off + c * 16), 16);
+            }
+          }
+          ptx::cp_async_mbar_arrive_noinc(&b_full[st]);
+        }
+        if (gt == 0) ptrace(p, k, 1);
+      }
+    }
+  } else if (warp == kPMma) {
+    if (lane == 0) {
+      // ------------------------------------------------------- MMA issuer
+      const uint32_t idesc = ptx::idesc_bf16_f32(kTileM, kEBlockN, false, true);
+      uint32_t k = 0, vi = 0;
+      for (uint32_t ui = blockIdx.x; ui < n_units; ui += gridDim.x, ++vi) {
+        un.set(ui, ngrp, nbt, p.n_tiles);
+        const uint32_t r16 = (p.tiles[un.tile].rank + 15) & ~15u, vs = vi % kPVStages;
+        ptx::mbar_wait(&v_full[vs], (vi / kPVStages) & 1u);
+        const uint32_t vbase = ptx::smem_u32(smem + PSmem::v + vs * 32768);
+        for (uint32_t b = un.b0; b < un.b1; ++b, ++k) {
+          const uint32_t st = k % kPStages, ph = (k / kPStages) & 1u;
+          const uint32_t as = k % kPAcc, aph = (k / kPAcc) & 1u;
+          ptx::mbar_wait(&b_full[st], ph);
+          ptrace(p, k, 2);
+          ptx::mbar_wait(&acc_empty[as], aph ^ 1u);
+          ptrace(p, k, 3);
+          ptx::fence_proxy_async_shared();
+          ptx::tc_fence_after();
+          const uint32_t bbase = ptx::smem_u32(smem + PSmem::b + st * 16384);
+          for (uint32_t kk = 0; kk < ((p.dbg & 256u) ? 0u : r16 / 16); ++kk)
+            ptx::umma_f16(tmem + as * kEBlockN, ptx::smem_desc_sw128(vbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                          ptx::smem_desc_sw128(bbase + kk * 2048, r16 * 128, 1024), idesc, kk != 0);
+          ptx::umma_commit(&b_empty[st]);
+          ptx::umma_commit(&acc_full[as]);
+        }
+        ptx::umma_commit(&v_empty[vs]);  // the unit's last block: its V stage is free
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (two groups)
+    // Every warp stages its own 32 rows and reduce-adds them itself (a 64 × 32
+    // box): no barrier across the group, and each warp waits only for its own
+    // earlier reduce-add before reusing its staging buffer.
+    const uint32_t quad = warp & 3;             // TMEM lane quadrant (each group covers all four)
+    const uint32_t m = quad * 32 + lane;        // tile row == TMEM lane
+    const uint32_t lane_base = (quad * 32) << 16;
+    const uint32_t eg = (warp - kPEpi0) >> 2;   // group: blocks k ≡ eg (mod 2)
+    char* ys = smem + PSmem::y + (warp - kPEpi0) * 4096;
+    uint32_t k = 0, n = 0;
+    for (uint32_t ui = blockIdx.x; ui < n_units; ui += gridDim.x) {
+      un.set(ui, ngrp, nbt, p.n_tiles);
+      const SgmvTile tile = p.tiles[un.tile];
+      const bool live = m < tile.nrows;  // rows past the run belong to the next one: add -0
+      const bool any = quad * 32 < tile.nrows;
+      for (uint32_t b = un.b0; b < un.b1; ++b, ++k) {
+        if ((k & 1u) != eg) continue;
+        const uint32_t as = k % kPAcc, aph = (k / kPAcc) & 1u;
+        if (n >= 1) {  // this warp's previous reduce-add must have read the buffer
+          if (lane == 0) ptx::bulk_wait_read_n<0>();
+          __syncwarp();
+        }
+        ++n;
+        if (lane == 0 && quad == 0) ptrace(p, k, 7);
+        ptx::mbar_wait(&acc_full[as], aph);
+        if (lane == 0 && quad == 0) ptrace(p, k, 4);
+        ptx::tc_fence_after();
+        uint32_t rv[kEBlockN / 16][16];
+#pragma unroll
+        for (uint32_t c = 0; c < kEBlockN / 16; ++c)
+          ptx::tmem_ld_32x32b_x16(tmem + lane_base + as * kEBlockN + c * 16, rv[c]);
+        ptx::tmem_ld_wait();
+        if (lane == 0 && quad == 0) ptrace(p, k, 5);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&acc_empty[as]);
+#pragma unroll
+        for (uint32_t c = 0; c < kEBlockN / 16; ++c) {
+#pragma unroll
+          for (uint32_t hh = 0; hh < 2; ++hh) {
+            const uint32_t ya = ptx::smem_u32(ys + swz(lane, c * 2 + hh));
+            uint32_t o[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o[i] = live ? pack_bf16x2(p.scale * __uint_as_float(rv[c][hh * 8 + 2 * i]),
+                                        p.scale * __uint_as_float(rv[c][hh * 8 + 2 * i + 1]))
+                          : 0x80008000u;  // bf16 -0.0: the exact additive identity of the reduce-add
+            asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(ya), "r"(o[0]), "r"(o[1]),
+                         "r"(o[2]), "r"(o[3]) : "memory");
+          }
+        }
+        ptx::fence_proxy_async_shared();  // generic-proxy smem writes -> TMA
+        __syncwarp();
+        if (lane == 0) {
+          if (quad == 0) ptrace(p, k, 6);
+          if (any && !(p.dbg & 64u))  // (a warp whose rows all belong to the next run adds nothing)
+            ptx::tma_reduce_add_2d(un.pj ? &tmap_y1 : &tmap_y0, static_cast<int32_t>(b * kEBlockN),
+                                   static_cast<int32_t>(tile.row0 + quad * 32), ys);
+          ptx::bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) ptx::bulk_wait_all();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == kPEpi0) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, kPAcc * kEBlockN);
+  }
+}
+
 }  // namespace
 
 extern "C" int plora_debug_set_sgmv_flags(uint32_t flags) {
@@ -805,6 +1124,7 @@ static void sgmv_run(plora_plan* plan, uint32_t layer, const uint32_t* projs, ui
   ea.d_out = dout;
   ea.n_tiles = plan->n_tiles;
   ea.ngroups = (dout / kEBlockN + kGroupBlocks - 1) / kGroupBlocks;
+  ea.np = np;
   ea.scale = scale;
   ea.dbg = g_sgmv_dbg;
   CUtensorMap tmap_arena;
@@ -813,13 +1133,29 @@ static void sgmv_run(plora_plan* plan, uint32_t layer, const uint32_t* projs, ui
   make_tmap_2d(&tmap_arena, st.arena, kEBlockN, g4 ? arena_rows : 1, kEBlockN * 2, kEBlockN, 1);
   ea.g4 = g4 ? 1u : 0u;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(np * plan->n_tiles * ea.ngroups);
   cfg.blockDim = dim3(kEThreads);
-  cfg.dynamicSmemBytes = ESmem::alloc;
   cfg.stream = s;
   cfg.attrs = pdl;
   cfg.numAttrs = 1;
-  PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y[0], tmap_y[1], tmap_v, tmap_arena));
+  if (!(g_sgmv_dbg & kDbgPersistentExpand)) {  // the default: one CTA per (proj, tile, 512 columns)
+    cfg.gridDim = dim3(np * plan->n_tiles * ea.ngroups);
+    cfg.dynamicSmemBytes = ESmem::alloc;
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_kernel, ea, tmap_y[0], tmap_y[1], tmap_v, tmap_arena));
+  } else {
+    for (uint32_t j = 0; j < 2; ++j) {  // 64 × 32 boxes: every epilogue warp reduce-adds its own rows
+      const uint32_t jj = j < np ? j : 0;
+      make_tmap_2d(&tmap_y[j], ys[jj], dout, plan->n_tokens, y_strides[jj] * 2, 64, 32);
+    }
+    set_smem_once(reinterpret_cast<const void*>(sgmv_expand_persistent_kernel), static_cast<int>(PSmem::alloc));
+    cfg.blockDim = dim3(kPThreads);
+    const uint64_t units = static_cast<uint64_t>(np) * plan->n_tiles *
+                           ((dout / kEBlockN + kPUnitBlocks - 1) / kPUnitBlocks);
+    cfg.gridDim = dim3(static_cast<uint32_t>(std::min<uint64_t>(std::max(1, st.num_sms), units)));
+    cfg.dynamicSmemBytes = PSmem::alloc;
+    ea.trace = trace_buffer(static_cast<uint64_t>(cfg.gridDim.x) * kPTrace * 64);
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, sgmv_expand_persistent_kernel, ea, tmap_y[0], tmap_y[1], tmap_v,
+                                  tmap_arena));
+  }
   count_launch();
 }
 

@@ -164,3 +164,34 @@ def test_sgmv_small_pages(cuda, page_bytes):
     for p in range(2):
         ref = s.oracle(0, p, x, y0[p], ta, v_bf16=True)
         assert rel_err(ys[p], ref) <= TOL_BF16, p
+
+
+@pytest.mark.parametrize("page_bytes", [64, 256, 2048])
+def test_sgmv_persistent_expand_bit_identical(cuda, page_bytes):
+    """The persistent expand (plora_debug_set_sgmv_flags bit 20, a measured
+    alternative) gives the tiled expand's y bit for bit: mixed ranks incl. a
+    rank with gather4 tail/padding rows (5), partial tiles, adapter-less
+    tokens, gather4 (>= 256 B pages) and cp.async (64 B) modes."""
+    from paper_2512_20210_b200 import _native as N
+    shape = ModelShape(2, (1024, 1024), (1024, 1024), torch.bfloat16)
+    cfg = synth.DecodeConfig("sgmv_persist", shape, [16, 64, 128, 5], 1, page_bytes)
+    s = Setup(cfg)
+    runs = [(0, 200), (1, 128), (-1, 3), (2, 150), (3, 20), (2, 300)]
+    ta = np.concatenate([np.full(n, a, np.int32) for a, n in runs])
+    T = len(ta)
+    x = synth.activations(T, 1024, shape.dtype, "x", salt=5).cuda()
+    y0 = [synth.activations(T, 1024, shape.dtype, "y", salt=6 + p).cuda() for p in range(2)]
+    plan = BatchPlan(s.store, ta)
+    outs = []
+    try:
+        for flags in (0, 1 << 20):
+            N.check(N.lib().plora_debug_set_sgmv_flags(flags))
+            ys = [y.clone() for y in y0]
+            sgmv_layer(plan, 1, x, ys, scale=0.75)
+            torch.cuda.synchronize()
+            outs.append(ys)
+    finally:
+        N.check(N.lib().plora_debug_set_sgmv_flags(0))
+    for p in range(2):
+        assert torch.equal(outs[0][p], outs[1][p]), p
+        assert not torch.equal(outs[0][p], y0[p])
