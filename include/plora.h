@@ -594,7 +594,7 @@ int plora_debug_set_stream_ctas(uint32_t ctas);
 /* Adapters with at least `min_tokens` tokens in a decode batch leave the
  * decode kernels for the tensor-core SGMV path (their tokens gathered into a
  * child plan, run concurrently on a second stream).  Applies to plans built
- * afterwards; 0 disables.  Default 48 (profiles/r02j_route_sweep.txt). */
+ * afterwards; 0 disables.  Default 160 (profiles/r02o_route_warp.txt). */
 int plora_debug_set_route_tokens(uint32_t min_tokens);
 /* Tokens of the plan's batch that take the routed SGMV path. */
 int plora_debug_plan_routed(const plora_plan* plan, uint32_t* n_tokens);

@@ -448,7 +448,12 @@ void launch_hybrid(plora_plan* plan, uint32_t layer0, uint32_t n_layers, const v
 
 namespace {
 // ---- many-token adapters on the tensor-core path (plan.cu: plan->route)
-uint32_t g_route_min = 48;  // plora_debug_set_route_tokens (profiles/r02j_route_sweep.txt)
+// plora_debug_set_route_tokens.  160: with the warp-item decode kernels the
+// routed SGMV side costs ~100 us per layer call however few tiles it has (its
+// persistent shrink needs whole SMs, which the decode CTAs hold), so routing
+// pays only for adapters of >= ~160 tokens (profiles/r02o_route_warp.txt;
+// the cluster kernel's break-even was 48, profiles/r02j_route_sweep.txt).
+uint32_t g_route_min = 160;
 
 // xg[i, :] = x[perm[i], :]: the routed tokens' rows, in adapter order
 __global__ void route_gather_kernel(const char* __restrict__ x, uint64_t x_stride_b,
