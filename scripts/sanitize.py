@@ -102,6 +102,16 @@ def main():
         sgmv_fused(pf, 1, 0, xx, torch.randn(1024, 1024, device="cuda").to(torch.bfloat16),
                    torch.empty(len(sg), 1024, device="cuda", dtype=torch.bfloat16))
         sgmv(pf, 1, 1, xx, torch.randn(len(sg), 512, device="cuda").to(torch.bfloat16))
+    # the persistent SGMV expand (a measured alternative, flag bit 20): gather4 pages, 64 B pages (cp.async)
+    for page in (2048, 64):
+        shape = ModelShape(2, (1024, 1024), (1024, 1024), torch.bfloat16)
+        ss = Setup(synth.DecodeConfig("san", shape, [16, 64, 128, 5], 1, page))
+        sg = synth.segment_assignment(4, 150)
+        xx = torch.randn(len(sg), 1024, device="cuda").to(torch.bfloat16)
+        N.check(N.lib().plora_debug_set_sgmv_flags(1 << 20))
+        sgmv_layer(BatchPlan(ss.store, sg), 1, xx, [torch.randn(len(sg), 1024, device="cuda").to(torch.bfloat16)
+                                                    for _ in range(2)])
+        N.check(N.lib().plora_debug_set_sgmv_flags(0))
     # many-token adapters routed to the SGMV path (child plan, second stream)
     import numpy as np
     N.check(N.lib().plora_debug_set_route_tokens(16))
@@ -114,7 +124,7 @@ def main():
     xrl = torch.randn(2, len(tr), 4096, device="cuda").to(torch.bfloat16)
     yrl = torch.randn(2, 2, len(tr), 4096, device="cuda").to(torch.bfloat16)
     bgmv_layers(pr, 0, xrl, [yrl[:, 0], yrl[:, 1]])
-    N.check(N.lib().plora_debug_set_route_tokens(48))
+    N.check(N.lib().plora_debug_set_route_tokens(160))
     # TP halves with the fused peer-write all-gather, two emulated ranks
     from paper_2512_20210_b200.tp import bgmv_tp_expand_wait, bgmv_tp_shrink_push
     vgs = [torch.zeros(2, T, rs, device="cuda") for _ in range(2)]
