@@ -39,6 +39,7 @@ namespace {
 #define PLORA_WARP_CTA 2  // warps (work items) per CTA
 #endif
 constexpr uint32_t kWarps = PLORA_WARP_CTA;
+static_assert(kWarps % 2 == 0, "split E pairs are the two warps (2c, 2c + 1) of a CTA");
 #define PLORA_WARP_MINB (16 / PLORA_WARP_CTA)  // 16 warps per SM: <= 128 registers
 constexpr uint32_t kThreads = kWarps * 32;
 
@@ -65,7 +66,7 @@ struct WArgs {
 };
 
 struct WI {
-  uint32_t toff, rank, ntok, pj, n, off, voff;
+  uint32_t toff, rank, ntok, pj, n, off, voff, flags;
   uint32_t tok[kWarpJobTok];
 };
 
@@ -77,7 +78,8 @@ __device__ __forceinline__ WI load_item(const WarpItem* it) {
   w.rank = a.y & 0x1ffu;
   w.ntok = (a.y >> 9) & 7u;
   w.pj = (a.y >> 12) & 0xfu;
-  w.n = a.y >> 16;
+  w.n = (a.y >> 16) & 0x3ffu;
+  w.flags = a.y & (kWarpSplit | kWarpSecond);
   w.off = a.z;
   w.voff = a.w;
   w.tok[0] = b.x;
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_shrink_ke
 // ahead of their use.
 template <int T, bool FAST, uint32_t RG, uint32_t KS>
 __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
-                                            uint32_t ring) {
+                                            uint32_t ring, uint32_t partner) {
   constexpr int NS = kWarpCols(T) / 256;  // 16-byte column chunks per lane and row
   constexpr uint32_t DR = RG / NS;        // ring depth in rows
   const uint32_t L = p.log2_page;
@@ -344,6 +346,13 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
   const uint64_t b0 = (static_cast<uint64_t>(r) * blk + static_cast<uint64_t>(r) * p.d_in + w.off) * 2;
   const uint32_t segb = w.n * 2;
   const uint32_t* tab = p.table + w.toff;
+  // rank rows [j0, j1) of this warp: all of them, or one half of a split pair
+  // (single-layer calls only: multi-layer launches have no pairs, and their
+  // kernels are compiled without the pair code)
+  const bool split = RG == kDeepRing && (w.flags & kWarpSplit) != 0;
+  const bool second = split && (w.flags & kWarpSecond) != 0;
+  const uint32_t hr = (r + 1) / 2;
+  const uint32_t j0 = split && second ? hr : 0u, j1 = split && !second ? hr : r;
   bool valid[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) valid[s] = s * 256 + lane * 8 < w.n;
@@ -399,22 +408,26 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
   // slower with it: profiles/r02o_expand_prefetch.txt).
   constexpr bool kPre = RG == kDeepRing;
   if (kPre) {
-    entries(0);
-    for (uint32_t jj = 0; jj < DR; ++jj) issue(0, min(64u, r), jj);
+    entries(j0);
+    for (uint32_t jj = 0; jj < DR; ++jj) issue(j0, min(64u, j1 - j0), jj);
   }
   ptx::pdl_wait();  // v (the shrink launch) and y (earlier kernels)
   // the item's y pieces into the warp's y area (the oldest group, or with kPre
-  // the one after the first block's rows: every wait from row 1 on covers it)
+  // the one after the first block's rows: every wait from row 1 on covers it);
+  // a pair's second half does not touch y
   const uint32_t yarea = ring + RG * 512;
 #pragma unroll
   for (int t = 0; t < T; ++t) {
     const char* yr = p.y[w.pj] + static_cast<uint64_t>(li) * p.y_lstride_b[w.pj] +
                      static_cast<uint64_t>(w.tok[t]) * p.y_stride_b[w.pj] + static_cast<uint64_t>(w.off) * 2;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) cpa16(yarea + (t * NS + s) * 512, valid[s] ? yr + s * 512 + lane * 16 : p.y[w.pj], valid[s]);
+    for (int s = 0; s < NS; ++s) {
+      const bool ok = valid[s] && !second;
+      cpa16(yarea + (t * NS + s) * 512, ok ? yr + s * 512 + lane * 16 : p.y[w.pj], ok);
+    }
   }
   ptx::cp_async_commit();
-  for (uint32_t jb = 0; jb < r; jb += 64) {
+  for (uint32_t jb = j0; jb < j1; jb += 64) {
     float vv[T][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -434,8 +447,8 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
           for (uint32_t k = 1; k < p.ks; ++k) vv[t][h] += vb[(k * T + t) * r + j];
       }
     }
-    const uint32_t nrow = min(64u, r - jb);
-    if (!kPre || jb > 0) {
+    const uint32_t nrow = min(64u, j1 - jb);
+    if (!kPre || jb > j0) {
       entries(jb);
       for (uint32_t jj = 0; jj < DR; ++jj) issue(jb, nrow, jj);
     }
@@ -461,6 +474,34 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
     ptx::cp_async_wait<0>();  // the ring is refilled by the next block / item (and y has landed)
   }
   ptx::cp_async_wait<0>();
+  if (split) {  // combine the pair: acc(rows [0, h)) + acc(rows [h, r)), in that order
+    constexpr int K = NS * 4 * T;
+    if (second) {  // its own ring is idle now: stage the partial sums there
+#pragma unroll
+      for (int s = 0; s < NS; ++s)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int t = 0; t < T; ++t)
+            asm volatile("st.shared.u64 [%0], %1;" ::"r"(ring - lane * 16 + (((s * 4 + q) * T + t) * 32 + lane) * 8),
+                         "l"(acc[s][q][t]) : "memory");
+      asm volatile("bar.sync 1, 64;" ::: "memory");
+      return;
+    }
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    static_assert(K * 256 <= 16 * 512, "pair partial sums fit the partner's ring");
+#pragma unroll
+    for (int s = 0; s < NS; ++s)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+          uint64_t o;
+          asm volatile("ld.shared.u64 %0, [%1];" : "=l"(o) : "r"(partner + (((s * 4 + q) * T + t) * 32 + lane) * 8) : "memory");
+          const float2 a = unpack2(acc[s][q][t]), b = unpack2(o);
+          asm("mov.b64 %0, {%1, %2};" : "=l"(acc[s][q][t]) : "f"(a.x + b.x), "f"(a.y + b.y));
+        }
+  }
   // y = bf16(y + scale · acc), 16 bytes per (token, chunk)
 #pragma unroll
   for (int t = 0; t < T; ++t) {
@@ -496,12 +537,13 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_expand_ke
   const uint32_t wi = (blockIdx.x / p.n_layers) * kWarps + warp;
   if (wi >= p.n_items) return;
   const uint32_t ring = ptx::smem_u32(smem) + warp * warp_smem(RG) + lane * 16;
+  const uint32_t partner = ptx::smem_u32(smem) + (warp ^ 1u) * warp_smem(RG);  // a split pair's other warp
   const WI w = load_item(p.items + wi);
   switch (w.ntok) {
-    case 1: expand_item<1, FAST, RG, KS>(p, w, li, lane, ring); break;
-    case 2: expand_item<2, FAST, RG, KS>(p, w, li, lane, ring); break;
-    case 3: expand_item<3, FAST, RG, KS>(p, w, li, lane, ring); break;
-    default: expand_item<4, FAST, RG, KS>(p, w, li, lane, ring); break;
+    case 1: expand_item<1, FAST, RG, KS>(p, w, li, lane, ring, partner); break;
+    case 2: expand_item<2, FAST, RG, KS>(p, w, li, lane, ring, partner); break;
+    case 3: expand_item<3, FAST, RG, KS>(p, w, li, lane, ring, partner); break;
+    default: expand_item<4, FAST, RG, KS>(p, w, li, lane, ring, partner); break;
   }
 }
 
@@ -571,17 +613,19 @@ void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0
   else
     launch(bgmv_warp_shrink_kernel<false, kRing>, bgmv_warp_shrink_kernel<false, kDeepRing>, w.ns,
            plan.d_witems + w.s_off);
-  const WarpItem* ei = plan.d_witems + w.e_off;
+  // single-layer calls: the item list with split pairs for the widest adapters
+  const WarpItem* ei = plan.d_witems + (deep ? w.e1_off : w.e_off);
+  const uint32_t ne = deep ? w.ne1 : w.ne;
   if (fast && w.ks == 1)
-    launch(bgmv_warp_expand_kernel<true, kRing, 1>, bgmv_warp_expand_kernel<true, kDeepRing, 1>, w.ne, ei);
+    launch(bgmv_warp_expand_kernel<true, kRing, 1>, bgmv_warp_expand_kernel<true, kDeepRing, 1>, ne, ei);
   else if (fast && w.ks == 2)
-    launch(bgmv_warp_expand_kernel<true, kRing, 2>, bgmv_warp_expand_kernel<true, kDeepRing, 2>, w.ne, ei);
+    launch(bgmv_warp_expand_kernel<true, kRing, 2>, bgmv_warp_expand_kernel<true, kDeepRing, 2>, ne, ei);
   else if (fast)
-    launch(bgmv_warp_expand_kernel<true, kRing, 0>, bgmv_warp_expand_kernel<true, kDeepRing, 0>, w.ne, ei);
+    launch(bgmv_warp_expand_kernel<true, kRing, 0>, bgmv_warp_expand_kernel<true, kDeepRing, 0>, ne, ei);
   else if (w.ks == 1)
-    launch(bgmv_warp_expand_kernel<false, kRing, 1>, bgmv_warp_expand_kernel<false, kDeepRing, 1>, w.ne, ei);
+    launch(bgmv_warp_expand_kernel<false, kRing, 1>, bgmv_warp_expand_kernel<false, kDeepRing, 1>, ne, ei);
   else
-    launch(bgmv_warp_expand_kernel<false, kRing, 0>, bgmv_warp_expand_kernel<false, kDeepRing, 0>, w.ne, ei);
+    launch(bgmv_warp_expand_kernel<false, kRing, 0>, bgmv_warp_expand_kernel<false, kDeepRing, 0>, ne, ei);
 }
 
 }  // namespace plora

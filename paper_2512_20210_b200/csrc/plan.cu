@@ -663,7 +663,7 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       // several items (cfg5's 8192-wide q / v: two slices)
       w.ks = (g.m.d_in[projs[0]] + 4095) / 4096;
       uint64_t voff = 0;
-      std::vector<WarpItem> S, E;
+      std::vector<WarpItem> S, E, E1, EP;  // E: multi-layer; E1 + EP (split pairs): single-layer
       for (uint32_t i = 0; i < np; ++i) {
         const uint32_t dout = g.m.d_out[projs[i]];
         for (const WJob& j : wj) {
@@ -685,6 +685,14 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
             it.meta = meta(std::min(C, dout - c0));
             it.off = c0;
             E.push_back(it);
+            if (j.rank >= kWarpSplitRows) {  // a pair: rows [0, h) and [h, r), one CTA
+              it.meta |= kWarpSplit;
+              EP.push_back(it);
+              it.meta |= kWarpSecond;
+              EP.push_back(it);
+            } else {
+              E1.push_back(it);
+            }
           }
           voff += static_cast<uint64_t>(w.ks) * j.ntok * j.rank;
         }
@@ -694,15 +702,33 @@ void plora_plan::build(const int32_t* token_adapter, uint32_t n, cudaStream_t st
       // tail with the light ones); ties keep list order, so a job's items stay
       // adjacent and share x / v through L1
       auto s_cost = [](const WarpItem& it) { return it.meta >> 16; };
-      auto e_cost = [](const WarpItem& it) { return (it.meta & 0x1ffu) * (it.meta >> 16); };
+      auto e_cost = [](const WarpItem& it) { return (it.meta & 0x1ffu) * ((it.meta >> 16) & 0x3ffu); };
       std::stable_sort(S.begin(), S.end(), [&](const WarpItem& a, const WarpItem& b) { return s_cost(a) > s_cost(b); });
       std::stable_sort(E.begin(), E.end(), [&](const WarpItem& a, const WarpItem& b) { return e_cost(a) > e_cost(b); });
+      std::stable_sort(E1.begin(), E1.end(), [&](const WarpItem& a, const WarpItem& b) { return e_cost(a) > e_cost(b); });
+      {  // split pairs first, heaviest first, each pair on an even position (one CTA of two warps)
+        std::vector<uint32_t> pi(EP.size() / 2);
+        std::iota(pi.begin(), pi.end(), 0u);
+        std::stable_sort(pi.begin(), pi.end(),
+                         [&](uint32_t a, uint32_t b) { return e_cost(EP[2 * a]) > e_cost(EP[2 * b]); });
+        std::vector<WarpItem> all;
+        all.reserve(EP.size() + E.size());
+        for (uint32_t k : pi) {
+          all.push_back(EP[2 * k]);
+          all.push_back(EP[2 * k + 1]);
+        }
+        all.insert(all.end(), E1.begin(), E1.end());
+        E1.swap(all);
+      }
       w.s_off = static_cast<uint32_t>(witems.size());
       w.ns = static_cast<uint32_t>(S.size());
       witems.insert(witems.end(), S.begin(), S.end());
       w.e_off = static_cast<uint32_t>(witems.size());
       w.ne = static_cast<uint32_t>(E.size());
       witems.insert(witems.end(), E.begin(), E.end());
+      w.e1_off = static_cast<uint32_t>(witems.size());
+      w.ne1 = static_cast<uint32_t>(E1.size());
+      witems.insert(witems.end(), E1.begin(), E1.end());
       w.vplane = (voff + 3) & ~3ull;
       wv_need = std::max(wv_need, w.vplane);
     };

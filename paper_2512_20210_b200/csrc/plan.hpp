@@ -209,9 +209,21 @@ constexpr uint32_t kWarpRows(uint32_t ntok) { return ntok <= 2 ? 8u : 4u; }
 __host__ __device__
 #endif
 constexpr uint32_t kWarpCols(uint32_t ntok) { return ntok <= 2 ? 512u : 256u; }
+// Single-layer calls (plora_bgmv / plora_bgmv_layer): E items of jobs with
+// >= kWarpSplitRows rank rows come in pairs — the two warps of one CTA take
+// rows [0, h) and [h, r) of the same column block (h = ceil(r / 2)) and the
+// first adds the second's partial sums (shared memory, fixed order) before
+// the y epilogue: half the stream per warp for the widest adapters, which set
+// the tail of a single layer's call (cfg2 34.6 -> 32.5 us).  Multi-layer
+// launches keep whole items (the pairs measured 3 % slower there,
+// profiles/r02o_warp_split.txt), so the two launch forms differ in the fp32
+// summation order of those adapters' rows (<= 1 bf16 ulp of y).
+constexpr uint32_t kWarpSplitRows = 64;
+constexpr uint32_t kWarpSplit = 1u << 26;   // meta: a member of a split pair
+constexpr uint32_t kWarpSecond = 1u << 27;  // meta: the pair's second half (rows [h, r))
 struct WarpItem {  // 32 bytes, self-contained
   uint32_t table_off;  // adapter's first entry in the device page table
-  uint32_t meta;       // rank (bits 0-8) | ntok (9-11) | launch projection (12-15) | n (16-31)
+  uint32_t meta;       // rank (bits 0-8) | ntok (9-11) | launch projection (12-15) | n (16-25) | flags (26-27)
   uint32_t off;        // S: first rank row | K slice << 16; E: first output column
   uint32_t v_off;      // floats into the launch's per-layer v plane: the job's [ks][ntok][rank] block
   uint32_t tok[kWarpJobTok];
@@ -220,7 +232,8 @@ static_assert(sizeof(WarpItem) == 32, "WarpItem layout");
 
 struct WarpWork {  // one launch variant (a projection, or every projection of a layer)
   uint32_t s_off = 0, ns = 0;  // S items [s_off, s_off + ns) of the item array
-  uint32_t e_off = 0, ne = 0;  // E items
+  uint32_t e_off = 0, ne = 0;  // E items (multi-layer launches)
+  uint32_t e1_off = 0, ne1 = 0;  // E items of single-layer calls (split pairs)
   uint32_t np = 0;
   uint32_t projs[PLORA_MAX_PROJ] = {};
   uint32_t ks = 1;             // K slices of the S items (v partial planes per job)

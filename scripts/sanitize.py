@@ -68,8 +68,8 @@ def main():
         yn = [torch.randn(len(tan), 4096, device="cuda").to(torch.bfloat16) for _ in range(2)]
         bgmv_layer(BatchPlan(s.store, tan), 1, xn, yn)
     shp = ModelShape(2, (1000, 1000), (520, 1048), torch.bfloat16)
-    sw = Setup(synth.DecodeConfig("san_w", shp, [5, 16, 64, 33], 2, 256))
-    taw = synth.token_assignment(4, 2)
+    sw = Setup(synth.DecodeConfig("san_w", shp, [5, 16, 64, 33, 80], 2, 256))
+    taw = synth.token_assignment(5, 3)  # (rank 64 / 80: split expand pairs in single-layer calls)
     xw = torch.randn(len(taw), 1000, device="cuda").to(torch.bfloat16)
     bgmv_layer(BatchPlan(sw.store, taw), 1, xw, [torch.randn(len(taw), 520, device="cuda").to(torch.bfloat16),
                                                 torch.randn(len(taw), 1048, device="cuda").to(torch.bfloat16)])

@@ -319,11 +319,13 @@ def test_bgmv_layer_fused_equals_per_projection(cuda, page_bytes):
 
 @pytest.mark.parametrize("page_bytes", [2048, 256])
 def test_bgmv_layers_multi_layer_launch_bit_identical(cuda, page_bytes):
-    """plora_bgmv_layers (several layers per launch) computes exactly what
-    per-layer bgmv_layer calls do, on strided per-layer views, and matches the
-    oracle: the default warp-item op (one shrink + one expand launch for all
-    layers), the cluster kernel (impl 2: its chunk lists repeated per layer)
-    and the round-2 hybrid pair (impl 3: clusters + a streaming share)."""
+    """plora_bgmv_layers (several layers per launch) computes what per-layer
+    bgmv_layer calls do, on strided per-layer views, and matches the oracle:
+    the default warp-item op (one shrink + one expand launch for all layers;
+    within one bf16 ulp of the per-layer calls, whose widest adapters' expand
+    items are split pairs), the cluster kernel (impl 2: its chunk lists
+    repeated per layer; bit for bit) and the round-2 hybrid pair (impl 3:
+    clusters + a streaming share)."""
     from paper_2512_20210_b200.lora import bgmv_layer, bgmv_layers
     from paper_2512_20210_b200 import _native as N
     cfg = synth.cfg2(n_layers=4, page_bytes=page_bytes)
@@ -350,8 +352,16 @@ def test_bgmv_layers_multi_layer_launch_bit_identical(cuda, page_bytes):
             bgmv_layers(plan, 1, x, [got[:, 0], got[:, 1]], 0.5)
             torch.cuda.synchronize()
             assert kernel_launch_count() - n0 == launches, impl
-            if impl != 3:  # (the hybrid pair runs per layer on the clusters alone)
+            if impl == 2:
                 assert torch.equal(got, per_layer(plan)), impl
+            elif impl == 0:
+                # single-layer calls split the rank-64 adapters' expand items over two warps (another
+                # fp32 summation order of their rows): at most one bf16 ulp of y apart, mostly identical
+                ref = per_layer(plan)
+                d = (got.float() - ref.float()).abs()
+                # (<= one ulp of y, or of the delta's fp32 rounding where y0 + delta cancels)
+                assert (d <= ref.float().abs() * 2.0 ** -7 + ref.float().abs().max() * 2.0 ** -12).all(), impl
+                assert (d > 0).float().mean().item() < 0.05, impl
             again = y0.clone()
             bgmv_layers(plan, 1, x, [again[:, 0], again[:, 1]], 0.5)
             torch.cuda.synchronize()

@@ -96,7 +96,11 @@ def test_routed_layer_and_multi_layer_launch(skew):
     bgmv_layers(plan, 0, xd, multi, 0.75)
     torch.cuda.synchronize()
     for p in range(2):
-        assert torch.equal(per[p], multi[p]), p  # same kernels, same order of sums
+        # routed rows: same SGMV kernels, same order of sums; decode rows: the single-layer calls split
+        # the widest adapters' expand items over two warps (another fp32 order, <= 1 bf16 ulp apart)
+        d = (per[p].float() - multi[p].float()).abs()
+        assert (d <= multi[p].float().abs() * 2.0 ** -7 + multi[p].float().abs().max() * 2.0 ** -12).all(), p
+        assert (d > 0).float().mean().item() < 0.05, p
         ref = s.oracle(2, p, x[2], y0[p][2], ta, scale=0.75, nthreads=32)
         assert delta_rel_err(multi[p][2], ref, y0[p][2]) <= TOL_BF16, p
 
