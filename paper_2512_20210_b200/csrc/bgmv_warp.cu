@@ -63,6 +63,16 @@ struct WArgs {
   float* v;
   uint64_t vplane;                    // floats per launched layer
   float scale;
+  // tensor-parallel halves (launch_bgmv_warp_tp; zero for the data-parallel op)
+  uint32_t tp_size, tp_rank, tp_rsmax, tp_T, tp_njobs, tp_ndst;
+  float* tp_part;
+  uint32_t* tp_cnt;
+  float* tp_vout;
+  float* tp_dst[kMaxTp];
+  uint32_t* tp_flags[kMaxTp];
+  uint32_t* tp_done;
+  const float* tp_vg;
+  uint32_t* tp_wait;
 };
 
 struct WI {
@@ -217,7 +227,52 @@ __device__ __forceinline__ void cpa16(uint32_t dst, const void* src, bool valid)
 // issued kRing units (LA = kRing / R chunks) before it is consumed, so the
 // unit issued after consuming (c, i) is (c + LA, i): the same row, a static
 // register index for its page entries.
-template <int T, bool FAST, uint32_t RG>
+// The two warps of a split pair meet here (named barrier 1, 64 threads).
+// The non-.aligned barrier: the warps reach it from different instructions
+// and a warp may arrive not yet reconverged.
+__device__ __forceinline__ void pair_sync() {
+  __syncwarp();
+  asm volatile("barrier.sync 1, 64;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t tok_of(const WI& w, uint32_t t) {
+  return t == 0 ? w.tok[0] : t == 1 ? w.tok[1] : t == 2 ? w.tok[2] : w.tok[3];
+}
+
+// Tensor-parallel shrink: the job's last item (of rs/R row blocks × ks K
+// slices) sums the K-slice partials in slice order into v_part / the peers'
+// gathered buffers; with peers, the launch's last job releases their flags.
+__device__ __forceinline__ void tp_job_done(const WArgs& p, const WI& w, uint32_t lane, uint32_t rs,
+                                         uint32_t nitems) {
+  __syncwarp();
+  uint32_t last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(p.tp_cnt + w.voff, 1u) + 1 == nitems;
+  }
+  if (!__shfl_sync(0xffffffffu, last, 0)) return;
+  __threadfence();
+  const uint32_t ne = w.ntok * rs;
+  for (uint32_t e = lane; e < ne; e += 32) {
+    const uint32_t t = e / rs, row = e - t * rs;
+    float sum = 0.f;
+    for (uint32_t k = 0; k < p.ks; ++k) sum += __ldcg(p.tp_part + w.voff + (k * w.ntok + t) * rs + row);
+    const uint64_t o = static_cast<uint64_t>(tok_of(w, t)) * p.tp_rsmax + row;
+    if (p.tp_vout) p.tp_vout[o] = sum;
+    for (uint32_t d = 0; d < p.tp_ndst; ++d) p.tp_dst[d][o] = sum;  // peer stores over NVLink
+  }
+  if (lane == 0) p.tp_cnt[w.voff] = 0u;  // for the next call (stream-ordered after this grid)
+  if (p.tp_ndst) {
+    ptx::fence_acq_rel_sys();  // this lane's peer stores, before the job counts as done
+    __syncwarp();
+    if (lane == 0 && atomicAdd(p.tp_done, 1u) + 1 == p.tp_njobs) {
+      *p.tp_done = 0u;
+      for (uint32_t d = 0; d < p.tp_ndst; ++d) ptx::red_release_sys_add(p.tp_flags[d], 1u);
+    }
+  }
+}
+
+template <int T, bool FAST, uint32_t RG, bool TPS = false>
 __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
                                             uint32_t ring) {
   constexpr int R = kWarpRows(T);
@@ -301,6 +356,15 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
   for (int k = 0; k < N; ++k) V[k] = k < R * T ? acc[k / T][k % T] : 0.f;
   const float sum = warp_sum_many<N>(V, lane);
   const uint32_t k = warp_sum_index<N>(lane);
+  if (TPS) {  // the item's partial sums of its K slice -> the job's partial block [ks][ntok][rs]
+    const uint32_t rs = w.rank / p.tp_size;
+    if (warp_sum_owner<N>(lane) && k < static_cast<uint32_t>(R * T)) {
+      const uint32_t i = k / T, t = k % T;
+      if (i < w.n) p.tp_part[w.voff + (slice * w.ntok + t) * rs + (row0 + i - p.tp_rank * rs)] = sum;
+    }
+    tp_job_done(p, w, lane, rs, (rs + R - 1) / R * p.ks);
+    return;
+  }
   if (warp_sum_owner<N>(lane) && k < static_cast<uint32_t>(R * T)) {
     const uint32_t i = k / T, t = k % T;
     if (i < w.n)
@@ -332,7 +396,17 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_shrink_ke
 // Rows in blocks of 64 (lane k holds the page entries and v of rows jb + k and
 // jb + 32 + k); row j's NS units go to ring row slot j % DR, issued DR rows
 // ahead of their use.
-template <int T, bool FAST, uint32_t RG, uint32_t KS>
+// Fused all-gather, expand side: the launch's last item (of either half of a
+// split pair) consumes this call's arrival from every source.
+__device__ __forceinline__ void tp_consume(const WArgs& p, uint32_t lane) {
+  __syncwarp();
+  if (lane == 0 && atomicAdd(p.tp_done, 1u) + 1 == p.n_items) {
+    *p.tp_done = 0u;
+    for (uint32_t q = 0; q < p.tp_size; ++q) ptx::red_relaxed_sys_add(p.tp_wait + q, 0xffffffffu);
+  }
+}
+
+template <int T, bool FAST, uint32_t RG, uint32_t KS, bool TPE = false>
 __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
                                             uint32_t ring, uint32_t partner) {
   constexpr int NS = kWarpCols(T) / 256;  // 16-byte column chunks per lane and row
@@ -427,11 +501,26 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
     }
   }
   ptx::cp_async_commit();
+  if (TPE && p.tp_wait) {  // fused all-gather: every rank's v rows of this call have landed
+    if (lane == 0)
+      for (uint32_t q = 0; q < p.tp_size; ++q)
+        while (ptx::ld_acquire_sys(p.tp_wait + q) == 0u) __nanosleep(64);
+    __syncwarp();
+  }
+  const uint32_t trs = TPE ? r / p.tp_size : 1u;  // TP: shard rows per rank of this adapter
   for (uint32_t jb = j0; jb < j1; jb += 64) {
     float vv[T][2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const uint32_t j = jb + h * 32 + lane;
+      if (TPE) {  // v(t, j) = v_gathered[j / rs][tok][j % rs]
+        const uint32_t src = j / trs;
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+          vv[t][h] = j < r ? __ldcg(p.tp_vg + (static_cast<uint64_t>(src) * p.tp_T + w.tok[t]) * p.tp_rsmax + (j - src * trs))
+                           : 0.f;
+        continue;
+      }
 #pragma unroll
       for (int t = 0; t < T; ++t) vv[t][h] = j < r ? vb[t * r + j] : 0.f;
       // the K-slice partials of v, summed in slice order (KS: compile-time
@@ -485,10 +574,11 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
           for (int t = 0; t < T; ++t)
             asm volatile("st.shared.u64 [%0], %1;" ::"r"(ring - lane * 16 + (((s * 4 + q) * T + t) * 32 + lane) * 8),
                          "l"(acc[s][q][t]) : "memory");
-      asm volatile("bar.sync 1, 64;" ::: "memory");
+      pair_sync();
+      if (TPE && p.tp_wait) tp_consume(p, lane);
       return;
     }
-    asm volatile("bar.sync 1, 64;" ::: "memory");
+    pair_sync();
     static_assert(K * 256 <= 16 * 512, "pair partial sums fit the partner's ring");
 #pragma unroll
     for (int s = 0; s < NS; ++s)
@@ -524,6 +614,7 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
       *reinterpret_cast<uint4*>(yr + s * 512 + lane * 16) = make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
+  if (TPE && p.tp_wait) tp_consume(p, lane);
 }
 
 template <bool FAST, uint32_t RG, uint32_t KS>
@@ -547,7 +638,105 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_expand_ke
   }
 }
 
+// Tensor-parallel halves (tp.cu): one layer, single-layer ring geometry.
+template <bool FAST>
+__global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_tp_shrink_kernel(const WArgs p) {
+  extern __shared__ __align__(16) char smem[];
+  ptx::pdl_launch_dependents();
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t wi = blockIdx.x * kWarps + warp;
+  if (wi >= p.n_items) return;
+  const uint32_t ring = ptx::smem_u32(smem) + warp * warp_smem(kDeepRing) + lane * 16;
+  const WI w = load_item(p.items + wi);
+  switch (w.ntok) {
+    case 1: shrink_item<1, FAST, kDeepRing, true>(p, w, 0, lane, ring); break;
+    case 2: shrink_item<2, FAST, kDeepRing, true>(p, w, 0, lane, ring); break;
+    case 3: shrink_item<3, FAST, kDeepRing, true>(p, w, 0, lane, ring); break;
+    default: shrink_item<4, FAST, kDeepRing, true>(p, w, 0, lane, ring); break;
+  }
+}
+
+template <bool FAST>
+__global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_tp_expand_kernel(const WArgs p) {
+  extern __shared__ __align__(16) char smem[];
+  ptx::pdl_launch_dependents();
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t wi = blockIdx.x * kWarps + warp;
+  if (wi >= p.n_items) return;
+  const uint32_t ring = ptx::smem_u32(smem) + warp * warp_smem(kDeepRing) + lane * 16;
+  const uint32_t partner = ptx::smem_u32(smem) + (warp ^ 1u) * warp_smem(kDeepRing);  // a split pair's other warp
+  const WI w = load_item(p.items + wi);
+  switch (w.ntok) {
+    case 1: expand_item<1, FAST, kDeepRing, 1, true>(p, w, 0, lane, ring, partner); break;
+    case 2: expand_item<2, FAST, kDeepRing, 1, true>(p, w, 0, lane, ring, partner); break;
+    case 3: expand_item<3, FAST, kDeepRing, 1, true>(p, w, 0, lane, ring, partner); break;
+    default: expand_item<4, FAST, kDeepRing, 1, true>(p, w, 0, lane, ring, partner); break;
+  }
+}
+
 }  // namespace
+
+void launch_bgmv_warp_tp(const plora_plan& plan, const WarpTp& t, uint32_t layer, uint32_t proj, const void* x,
+                         uint64_t x_stride, void* y, uint64_t y_stride, float scale, cudaStream_t stream) {
+  if (t.n_items == 0) return;
+  const plora_store& st = *plan.store;
+  const ModelGeom& gm = st.geom;
+  WArgs a{};
+  a.n_layers = 1;
+  a.arena = st.arena;
+  a.table = st.d_table;
+  a.items = t.items;
+  a.n_items = t.n_items;
+  a.ks = t.ks;
+  a.d_in = gm.m.d_in[proj];
+  a.log2_page = st.log2_page;
+  a.x = static_cast<const char*>(x);
+  a.x_stride_b = x_stride * 2;
+  a.y[0] = static_cast<char*>(y);
+  a.y_stride_b[0] = y_stride * 2;
+  a.blk_mult[0] = gm.blk_mult(layer, proj);
+  a.d_out[0] = gm.m.d_out[proj];
+  a.plu = gm.per_layer_unit;
+  a.scale = scale;
+  a.tp_size = t.tp_size;
+  a.tp_rank = t.tp_rank;
+  a.tp_rsmax = t.rs_max;
+  a.tp_T = t.n_tokens;
+  a.tp_njobs = t.njobs;
+  a.tp_ndst = t.n_dst;
+  a.tp_part = t.part;
+  a.tp_cnt = t.cnt;
+  a.tp_vout = t.v_out;
+  for (uint32_t d = 0; d < t.n_dst; ++d) {
+    a.tp_dst[d] = t.dst[d];
+    a.tp_flags[d] = t.flags[d];
+  }
+  a.tp_done = t.done;
+  a.tp_vg = t.v_in;
+  a.tp_wait = t.wait;
+  const uint64_t P = 1ull << st.log2_page;
+  const bool fast = P >= 2ull * kWarpCols(1) && (a.d_in * 2ull + P - 1) / P + 1 <= 32;
+  a.fast = fast ? 1u : 0u;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kThreads);
+  cfg.gridDim = dim3((t.n_items + kWarps - 1) / kWarps);
+  cfg.stream = stream;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cfg.dynamicSmemBytes = cta_smem(kDeepRing);
+  auto go = [&](auto k) {
+    set_smem_once(reinterpret_cast<const void*>(k), static_cast<int>(cfg.dynamicSmemBytes));
+    PLORA_CUDA(cudaLaunchKernelEx(&cfg, k, a));
+    count_launch();
+  };
+  if (t.half == 1)
+    fast ? go(bgmv_warp_tp_shrink_kernel<true>) : go(bgmv_warp_tp_shrink_kernel<false>);
+  else
+    fast ? go(bgmv_warp_tp_expand_kernel<true>) : go(bgmv_warp_tp_expand_kernel<false>);
+}
 
 void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0, uint32_t n_layers,
                       const void* x, uint64_t x_stride, uint64_t x_lstride, void* const* ys,

@@ -230,6 +230,32 @@ struct WarpItem {  // 32 bytes, self-contained
 };
 static_assert(sizeof(WarpItem) == 32, "WarpItem layout");
 
+// A tensor-parallel half on the warp-item kernels (tp.cu; the default).
+//   shrink (half 1): S items = (job, <= kWarpRows rows of the rank's shard,
+//     K slice of `ks`); each writes its partial sums to `part` at the job's
+//     block [ks][ntok][rs]; the job's last item (counter at cnt[v_off]) sums
+//     the slices in order into v_out[tok][shard row] and / or every dst[d]
+//     (fused all-gather), and with dst the launch's last job adds 1 to every
+//     flags[d] (this rank's slot of rank d's flag array).
+//   expand (half 2): E items = (job, <= kWarpCols columns of the shard), every
+//     rank row, v read from v_in = [N][T][rs_max]; with `wait` the items first
+//     wait for every local flag slot >= 1 and the launch's last item takes 1
+//     from each.
+struct WarpTp {
+  uint32_t half = 0;
+  const WarpItem* items = nullptr;
+  uint32_t n_items = 0, ks = 1, njobs = 0;
+  uint32_t tp_size = 1, tp_rank = 0, rs_max = 0, n_tokens = 0;
+  float* part = nullptr;
+  uint32_t* cnt = nullptr;
+  float* v_out = nullptr;
+  uint32_t n_dst = 0;
+  float* dst[kMaxTp] = {};
+  uint32_t* flags[kMaxTp] = {};
+  uint32_t* done = nullptr;  // zero between calls
+  const float* v_in = nullptr;
+  uint32_t* wait = nullptr;
+};
 struct WarpWork {  // one launch variant (a projection, or every projection of a layer)
   uint32_t s_off = 0, ns = 0;  // S items [s_off, s_off + ns) of the item array
   uint32_t e_off = 0, ne = 0;  // E items (multi-layer launches)
@@ -359,7 +385,8 @@ struct plora_plan {
   // (tp_rank, tp_size, proj, half), built on first use, dropped on rebuild
   struct TpWork {
     plora::StreamWork w;
-    plora::StreamItem* d_items = nullptr;  // items, then the CTA offsets
+    plora::WarpTp wt;                      // the warp-item path (default): items / partials / counters in d_items
+    plora::StreamItem* d_items = nullptr;  // items, then the CTA offsets (one allocation, freed by drop_tp)
     uint32_t* d_cta = nullptr;
     uint32_t* d_done = nullptr;            // fused all-gather: CTAs of the shrink done (zero between calls)
     char* h_stage = nullptr;               // pinned source of the upload
@@ -412,6 +439,8 @@ void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0
                       const void* x, uint64_t x_stride, uint64_t x_lstride, void* const* ys,
                       const uint64_t* y_strides, const uint64_t* y_lstrides, float scale,
                       cudaStream_t stream);
+void launch_bgmv_warp_tp(const plora_plan& plan, const WarpTp& t, uint32_t layer, uint32_t proj, const void* x,
+                         uint64_t x_stride, void* y, uint64_t y_stride, float scale, cudaStream_t stream);
 // plora_debug_set_bgmv_impl: 0 (default) warp items, 1 streaming kernel,
 // 2 clusters, 3 the hybrid pair (clusters + streaming share)
 uint32_t bgmv_impl();

@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <queue>
@@ -161,6 +162,116 @@ plora_plan::TpWork& tp_work(plora_plan& plan, uint32_t proj, uint32_t tp_rank, u
   return plan.tpw.emplace(key, w).first->second;
 }
 
+// The warp-item lists of one half (the default TP path): shrink items are
+// (job, <= kWarpRows(ntok) shard rows, K slice of 4 chunks = 1024 inputs) —
+// ~16 KiB each, so even a TP = 8 shard gives every SM several — and expand
+// items (job, <= kWarpCols(ntok) columns of the shard), heaviest first.  One
+// allocation: items, then (shrink) the per-job partial blocks and their
+// counters, then the launch counter; counters start at zero and every call
+// leaves them at zero.
+plora_plan::TpWork& tp_work_warp(plora_plan& plan, uint32_t proj, uint32_t tp_rank, uint32_t tp_size,
+                                 uint32_t half, const TpGeom& tg, cudaStream_t stream) {
+  const uint64_t key = (1ull << 56) | (static_cast<uint64_t>(half) << 48) | (static_cast<uint64_t>(proj) << 40) |
+                       (static_cast<uint64_t>(tp_size) << 20) | tp_rank;
+  auto found = plan.tpw.find(key);
+  if (found != plan.tpw.end()) return found->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  PLORA_CUDA(cudaStreamIsCapturing(stream, &cs));
+  if (cs != cudaStreamCaptureStatusNone)
+    throw ValidationError("the first tensor-parallel call of a plan for (proj, tp_rank, tp_size) uploads its "
+                          "item list and must run outside stream capture");
+  const uint32_t ncall = (tg.d_in + 255) / 256;
+  // K slices of the shrink: the fewest (a power of two, slices of >= 4
+  // chunks) that give >= 6 items per SM — cfg5 measured best at ~900-1400
+  // items for every TP size (profiles/r02o_tp_warp.txt: fewer leave SMs idle,
+  // more add per-item and partial-sum overhead)
+  uint32_t ks = 1;
+  if (half == 1) {
+    uint64_t blocks = 0;
+    for (const ClusterJob& j : plan.cjobs) blocks += (j.rank / tp_size + kWarpRows(j.ntok) - 1) / kWarpRows(j.ntok);
+    const uint64_t target = 6ull * std::max(1, plan.store->num_sms);
+    while (blocks * ks < target && (ncall + 2 * ks - 1) / (2 * ks) >= 4) ks *= 2;
+  }
+  std::vector<WarpItem> items, pairs;  // pairs: split expand items (adjacent)
+  uint64_t pfl = 0;  // shrink: partial floats
+  for (const ClusterJob& j : plan.cjobs) {
+    WarpItem base{};
+    base.table_off = j.table_off;
+    for (uint32_t t = 0; t < kWarpJobTok; ++t) base.tok[t] = t < j.ntok ? j.tok[t] : 0u;
+    auto meta = [&](uint32_t n) { return j.rank | (j.ntok << 9) | (n << 16); };
+    if (half == 1) {
+      const uint32_t rs = j.rank / tp_size, R = kWarpRows(j.ntok);
+      base.v_off = static_cast<uint32_t>(pfl);
+      for (uint32_t k = 0; k < ks; ++k)
+        for (uint32_t r0 = 0; r0 < rs; r0 += R) {
+          WarpItem it = base;
+          it.meta = meta(std::min(R, rs - r0));
+          it.off = (tp_rank * rs + r0) | (k << 16);  // absolute A row | K slice
+          items.push_back(it);
+        }
+      pfl += static_cast<uint64_t>(ks) * j.ntok * rs;
+    } else {
+      const uint32_t C = kWarpCols(j.ntok);
+      for (uint32_t c0 = tg.col0; c0 < tg.col0 + tg.ncols; c0 += C) {
+        WarpItem it = base;
+        it.meta = meta(std::min(C, tg.col0 + tg.ncols - c0));
+        it.off = c0;  // absolute output column
+        if (j.rank >= kWarpSplitRows) {  // split pair: rows [0, h) / [h, r) on a CTA's two warps
+          it.meta |= kWarpSplit;
+          pairs.push_back(it);
+          it.meta |= kWarpSecond;
+          pairs.push_back(it);
+        } else {
+          items.push_back(it);
+        }
+      }
+    }
+  }
+  if (pfl > 0xffffffffull) throw ValidationError("batch too large for one plan");
+  auto cost = [&](const WarpItem& it) {
+    return half == 1 ? (it.meta >> 16) & 0x3ffu : (it.meta & 0x1ffu) * ((it.meta >> 16) & 0x3ffu);
+  };
+  std::stable_sort(items.begin(), items.end(), [&](const WarpItem& a, const WarpItem& b) { return cost(a) > cost(b); });
+  if (!pairs.empty()) {  // pairs first, heaviest first, each on an even position
+    std::vector<uint32_t> pi(pairs.size() / 2);
+    std::iota(pi.begin(), pi.end(), 0u);
+    std::stable_sort(pi.begin(), pi.end(),
+                     [&](uint32_t a, uint32_t b) { return cost(pairs[2 * a]) > cost(pairs[2 * b]); });
+    std::vector<WarpItem> all;
+    for (uint32_t k : pi) {
+      all.push_back(pairs[2 * k]);
+      all.push_back(pairs[2 * k + 1]);
+    }
+    all.insert(all.end(), items.begin(), items.end());
+    items.swap(all);
+  }
+  const uint64_t ib = items.size() * sizeof(WarpItem);
+  const uint64_t pb = pfl * 4;                    // partials
+  const uint64_t total = ib + 2 * pb + 16;        // items | partials | counters | launch counter
+  plora_plan::TpWork w;
+  DeviceCtx ctx(plan.store->device);
+  char* d = nullptr;
+  PLORA_CUDA(cudaMalloc(&d, total));
+  w.d_items = reinterpret_cast<StreamItem*>(d);
+  PLORA_CUDA(cudaMallocHost(&w.h_stage, total));
+  std::memset(w.h_stage, 0, total);
+  std::memcpy(w.h_stage, items.data(), ib);
+  PLORA_CUDA(cudaMemcpyAsync(d, w.h_stage, total, cudaMemcpyHostToDevice, stream));
+  w.wt.half = half;
+  w.wt.items = reinterpret_cast<const WarpItem*>(d);
+  w.wt.n_items = static_cast<uint32_t>(items.size());
+  w.wt.ks = ks;
+  w.wt.njobs = static_cast<uint32_t>(plan.cjobs.size());
+  w.wt.tp_size = tp_size;
+  w.wt.tp_rank = tp_rank;
+  w.wt.rs_max = tg.rs_max;
+  w.wt.n_tokens = plan.n_tokens;
+  w.wt.part = reinterpret_cast<float*>(d + ib);
+  w.wt.cnt = reinterpret_cast<uint32_t*>(d + ib + pb);
+  w.wt.done = reinterpret_cast<uint32_t*>(d + ib + 2 * pb);
+  return plan.tpw.emplace(key, w).first->second;
+}
+
 struct TpFlags {
   uint32_t* flags[kMaxTp];
   uint32_t n;
@@ -203,6 +314,16 @@ int tp_expand(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
     throw ValidationError("y_shard must be 16-byte aligned with a row stride >= d_out/tp_size, multiple of 8");
   DeviceCtx ctx(plan->store->device);
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the kernel addresses output column c (absolute in d_out) at y + c
+  char* y = static_cast<char*>(y_shard) - static_cast<ptrdiff_t>(tg.col0) * 2;
+  if (flags && tp_size > kMaxTp) throw ValidationError("fused all-gather: tp_size > " + std::to_string(kMaxTp));
+  if (bgmv_impl() != 1) {  // warp items (default)
+    WarpTp t = tp_work_warp(*plan, proj, tp_rank, tp_size, 2, tg, s).wt;
+    t.v_in = v_gathered;
+    t.wait = flags;
+    launch_bgmv_warp_tp(*plan, t, layer, proj, nullptr, 0, y, y_stride, scale, s);
+    return 0;
+  }
   const plora_plan::TpWork& w = tp_work(*plan, proj, tp_rank, tp_size, 2, tg, s);
   StreamTp tp{};
   tp.mode = 2;
@@ -212,10 +333,7 @@ int tp_expand(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
   tp.v_in = v_gathered;
   tp.items = w.d_items;
   tp.cta_off = w.d_cta;
-  // the kernel addresses output column c (absolute in d_out) at y + c
-  char* y = static_cast<char*>(y_shard) - static_cast<ptrdiff_t>(tg.col0) * 2;
   if (flags) {
-    if (tp_size > kMaxTp) throw ValidationError("fused all-gather: tp_size > " + std::to_string(kMaxTp));
     tp.wait = flags;
     tp.done = w.d_done;
   }
@@ -243,6 +361,12 @@ int plora_bgmv_tp_shrink(plora_plan* plan, uint32_t layer, uint32_t proj, uint32
       throw ValidationError("x must be 16-byte aligned with a row stride >= d_in, multiple of 8");
     DeviceCtx ctx(plan->store->device);
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (bgmv_impl() != 1) {  // warp items (default)
+      WarpTp t = tp_work_warp(*plan, proj, tp_rank, tp_size, 1, tg, s).wt;
+      t.v_out = v_part;
+      launch_bgmv_warp_tp(*plan, t, layer, proj, x, x_stride, nullptr, 0, 1.f, s);
+      return 0;
+    }
     const plora_plan::TpWork& w = tp_work(*plan, proj, tp_rank, tp_size, 1, tg, s);
     StreamTp tp{};
     tp.mode = 1;
@@ -291,6 +415,16 @@ int plora_bgmv_tp_shrink_push(plora_plan* plan, uint32_t layer, uint32_t proj, u
       tp_flag_bump_kernel<<<1, 32, 0, s>>>(f);
       PLORA_CUDA(cudaGetLastError());
       count_launch();
+      return 0;
+    }
+    if (bgmv_impl() != 1) {  // warp items (default)
+      WarpTp t = tp_work_warp(*plan, proj, tp_rank, tp_size, 1, tg, s).wt;
+      t.n_dst = tp_size;
+      for (uint32_t d = 0; d < tp_size; ++d) {
+        t.dst[d] = tp.dst[d];
+        t.flags[d] = tp.flags[d];
+      }
+      launch_bgmv_warp_tp(*plan, t, layer, proj, x, x_stride, nullptr, 0, 1.f, s);
       return 0;
     }
     const plora_plan::TpWork& w = tp_work(*plan, proj, tp_rank, tp_size, 1, tg, s);
