@@ -63,6 +63,8 @@ struct WArgs {
   float* v;
   uint64_t vplane;                    // floats per launched layer
   float scale;
+  uint64_t* trace;  // diagnostics (plora_debug_set_trace): [item][2] globaltimer ns (start, end), or nullptr
+  uint32_t trace_off;  // expand launch: its items follow the shrink's in the trace
   // tensor-parallel halves (launch_bgmv_warp_tp; zero for the data-parallel op)
   uint32_t tp_size, tp_rank, tp_rsmax, tp_T, tp_njobs, tp_ndst;
   float* tp_part;
@@ -79,6 +81,12 @@ struct WI {
   uint32_t toff, rank, ntok, pj, n, off, voff, flags;
   uint32_t tok[kWarpJobTok];
 };
+
+__device__ __forceinline__ uint64_t gtime() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ WI load_item(const WarpItem* it) {
   const uint4 a = __ldg(reinterpret_cast<const uint4*>(it));
@@ -311,43 +319,99 @@ __device__ __forceinline__ void shrink_item(const WArgs& p, const WI& w, uint32_
           valid);
     ptx::cp_async_commit();
   };
-  for (uint32_t c = 0; c < LA; ++c)
-#pragma unroll
-    for (int i = 0; i < R; ++i) issue(c, i);
-  ptx::pdl_wait();  // x (and the v this launch overwrites) belong to earlier kernels
   const char* xr[T];
 #pragma unroll
   for (int t = 0; t < T; ++t)
     xr[t] = p.x + static_cast<uint64_t>(li) * p.x_lstride_b + static_cast<uint64_t>(w.tok[t]) * p.x_stride_b +
             c0 * 512 + lane * 16;
-  auto ldx = [&](uint32_t c, uint4 (&xv)[T]) {
-    const bool valid = c < nc && c * 256 + lane * 8 < kin;
-#pragma unroll
-    for (int t = 0; t < T; ++t)
-      xv[t] = valid ? __ldg(reinterpret_cast<const uint4*>(xr[t] + c * 512)) : make_uint4(0u, 0u, 0u, 0u);
-  };
   float acc[R][T];
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
     for (int t = 0; t < T; ++t) acc[i][t] = 0.f;
-  uint4 xv[T];
-  ldx(0, xv);
-#pragma unroll 1
-  for (uint32_t c = 0; c < nc; ++c) {
-    uint4 xn[T];
-    ldx(c + 1, xn);
-    const uint32_t sb = ring + (c % LA) * R * 512;
+  if constexpr (RG == kDeepRing) {
+    // Single-layer calls (few items per SM, each warp's own latency counts):
+    // the x pieces travel through the ring too, LX chunks ahead like the
+    // weights — one commit group per chunk (its R weight units + T x units);
+    // x registers loaded one chunk ahead left every chunk waiting on an L2
+    // round trip.  The prologue's weight groups precede the dependency wait,
+    // its x groups follow it: waiting for <= LX - 1 pending groups before
+    // chunk c always covers both of chunk c's groups.
+    constexpr uint32_t U = R + T, LX = RG / U;
+    auto issue_w = [&](uint32_t c) {
+      const uint32_t sb = ring + (c % LX) * U * 512;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      ptx::cp_async_wait<RG - 1>();  // unit (c, i) has landed
-      const uint4 wv = lds16(sb + i * 512);
+      for (int i = 0; i < R; ++i) {
+        const uint64_t off = a0 + static_cast<uint64_t>(i) * rowb + c * 512 + lane * 16;
+        const uint32_t pg = static_cast<uint32_t>(off >> L);
+        uint32_t e = 0u;
+        if (FAST) e = __shfl_sync(0xffffffffu, ent[i], (pg - pg0[i]) & 31u);
+        const bool valid = static_cast<uint32_t>(i) < w.n && c < nc && c * 256 + lane * 8 < kin;
+        if (!FAST && valid) e = __ldg(tab + pg);
+        cpa16(sb + i * 512, valid ? p.arena + (static_cast<uint64_t>(e) << L) + (off & pmask) : p.arena, valid);
+      }
+    };
+    auto issue_x = [&](uint32_t c) {
+      const uint32_t sb = ring + ((c % LX) * U + R) * 512;
+      const bool valid = c < nc && c * 256 + lane * 8 < kin;
 #pragma unroll
-      for (int t = 0; t < T; ++t) fh8(acc[i][t], wv, xv[t]);
-      issue(c + LA, i);
+      for (int t = 0; t < T; ++t) cpa16(sb + t * 512, valid ? xr[t] + c * 512 : p.x, valid);
+    };
+    for (uint32_t c = 0; c < LX; ++c) {
+      issue_w(c);
+      ptx::cp_async_commit();
     }
+    ptx::pdl_wait();  // x (and the v this launch overwrites) belong to earlier kernels
+    for (uint32_t c = 0; c < LX; ++c) {
+      issue_x(c);
+      ptx::cp_async_commit();
+    }
+#pragma unroll 1
+    for (uint32_t c = 0; c < nc; ++c) {
+      ptx::cp_async_wait<LX - 1>();  // chunk c's weight and x groups have landed
+      const uint32_t sb = ring + (c % LX) * U * 512;
+      uint4 xv[T];
 #pragma unroll
-    for (int t = 0; t < T; ++t) xv[t] = xn[t];
+      for (int t = 0; t < T; ++t) xv[t] = lds16(sb + (R + t) * 512);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const uint4 wv = lds16(sb + i * 512);
+#pragma unroll
+        for (int t = 0; t < T; ++t) fh8(acc[i][t], wv, xv[t]);
+      }
+      issue_w(c + LX);
+      issue_x(c + LX);
+      ptx::cp_async_commit();
+    }
+  } else {
+    for (uint32_t c = 0; c < LA; ++c)
+#pragma unroll
+      for (int i = 0; i < R; ++i) issue(c, i);
+    ptx::pdl_wait();  // x (and the v this launch overwrites) belong to earlier kernels
+    auto ldx = [&](uint32_t c, uint4 (&xv)[T]) {
+      const bool valid = c < nc && c * 256 + lane * 8 < kin;
+#pragma unroll
+      for (int t = 0; t < T; ++t)
+        xv[t] = valid ? __ldg(reinterpret_cast<const uint4*>(xr[t] + c * 512)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    uint4 xv[T];
+    ldx(0, xv);
+#pragma unroll 1
+    for (uint32_t c = 0; c < nc; ++c) {
+      uint4 xn[T];
+      ldx(c + 1, xn);
+      const uint32_t sb = ring + (c % LA) * R * 512;
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        ptx::cp_async_wait<RG - 1>();  // unit (c, i) has landed
+        const uint4 wv = lds16(sb + i * 512);
+#pragma unroll
+        for (int t = 0; t < T; ++t) fh8(acc[i][t], wv, xv[t]);
+        issue(c + LA, i);
+      }
+#pragma unroll
+      for (int t = 0; t < T; ++t) xv[t] = xn[t];
+    }
   }
   ptx::cp_async_wait<0>();  // (only zero-size copies remain; the ring is reused by the next item)
   constexpr int N = pow2_at_least(R * T);
@@ -383,12 +447,17 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_shrink_ke
   const uint32_t wi = (blockIdx.x / p.n_layers) * kWarps + warp;
   if (wi >= p.n_items) return;
   const uint32_t ring = ptx::smem_u32(smem) + warp * warp_smem(RG) + lane * 16;
+  const uint64_t t0 = p.trace ? gtime() : 0;
   const WI w = load_item(p.items + wi);
   switch (w.ntok) {
     case 1: shrink_item<1, FAST, RG>(p, w, li, lane, ring); break;
     case 2: shrink_item<2, FAST, RG>(p, w, li, lane, ring); break;
     case 3: shrink_item<3, FAST, RG>(p, w, li, lane, ring); break;
     default: shrink_item<4, FAST, RG>(p, w, li, lane, ring); break;
+  }
+  if (p.trace && lane == 0) {
+    p.trace[2 * (blockIdx.x * kWarps + warp)] = t0;
+    p.trace[2 * (blockIdx.x * kWarps + warp) + 1] = gtime();
   }
 }
 
@@ -629,12 +698,18 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_expand_ke
   if (wi >= p.n_items) return;
   const uint32_t ring = ptx::smem_u32(smem) + warp * warp_smem(RG) + lane * 16;
   const uint32_t partner = ptx::smem_u32(smem) + (warp ^ 1u) * warp_smem(RG);  // a split pair's other warp
+  const uint64_t t0 = p.trace ? gtime() : 0;
   const WI w = load_item(p.items + wi);
   switch (w.ntok) {
     case 1: expand_item<1, FAST, RG, KS>(p, w, li, lane, ring, partner); break;
     case 2: expand_item<2, FAST, RG, KS>(p, w, li, lane, ring, partner); break;
     case 3: expand_item<3, FAST, RG, KS>(p, w, li, lane, ring, partner); break;
     default: expand_item<4, FAST, RG, KS>(p, w, li, lane, ring, partner); break;
+  }
+  if (p.trace && lane == 0) {  // expand items after the shrink's (offset by the launch's S item count)
+    const uint64_t o = 2 * (p.trace_off + blockIdx.x * kWarps + warp);
+    p.trace[o] = t0;
+    p.trace[o + 1] = gtime();
   }
 }
 
@@ -784,6 +859,10 @@ void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0
   cfg.numAttrs = 1;
   const bool deep = n_layers == 1;
   cfg.dynamicSmemBytes = cta_smem(deep ? kDeepRing : kRing);
+  if (deep) {
+    a.trace = trace_buffer(16ull * ((w.ns + w.ne1 + 2) / 2 * 2 + 2));
+    a.trace_off = (w.ns + kWarps - 1) / kWarps * kWarps;
+  }
   auto launch = [&](auto k16, auto k32, uint32_t n_items, const WarpItem* items) {
     a.items = items;
     a.n_items = n_items;
