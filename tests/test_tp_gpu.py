@@ -142,3 +142,51 @@ def test_fused_allgather_module_tp1_and_graph(setup70):
     torch.cuda.synchronize()
     assert torch.equal(yg, yc)
     assert int(fused._ff.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("tp_size", [2, 4])
+@pytest.mark.parametrize("page_bytes", [2048, 256])
+def test_tp_warp_items_edge_cases(cuda, tp_size, page_bytes):
+    """The warp-item TP halves away from cfg5: input widths that are not a
+    multiple of the 1024-input K slice (1000: a partial last slice), 1-7
+    tokens per adapter (jobs of 1-4 tokens, a 6-token adapter over two jobs),
+    ranks whose shard is smaller than an item (rs = 2) or spans several row
+    blocks (rs = 32), rank 128 (split expand pairs), 256-byte pages (page
+    entries by table loads); unfused and fused halves against the oracle and
+    each other."""
+    from paper_2512_20210_b200.lora import ModelShape
+    from paper_2512_20210_b200.tp import bgmv_tp_expand_wait, bgmv_tp_shrink_push
+    shape = ModelShape(2, (1000, 1000), (512, 1024), torch.bfloat16)
+    ranks = [8, 16, 64, 128, 4 * tp_size, 8]
+    s = Setup(synth.DecodeConfig("tp_edge", shape, ranks, 1, page_bytes))
+    rng = np.random.default_rng(11)
+    ta = np.concatenate([np.full(1 + (3 * a) % 7, a, np.int32) for a in range(len(ranks))])
+    rng.shuffle(ta)
+    T = len(ta)
+    plan = BatchPlan(s.store, ta)
+    rs = tp_shard_rows(plan, tp_size)
+    for proj in (0, 1):
+        din, dout = shape.d_in[proj], shape.d_out[proj]
+        ncols = dout // tp_size
+        x = synth.activations(T, din, torch.bfloat16, "x", salt=proj + 7)
+        y0 = synth.activations(T, dout, torch.bfloat16, "y", salt=proj + 7)
+        xd = x.cuda()
+        parts = [bgmv_tp_shrink(plan, 1, proj, r, tp_size, xd, torch.zeros(T, rs, dtype=torch.float32, device="cuda"))
+                 for r in range(tp_size)]
+        vu = torch.stack(parts).contiguous()
+        y_u = y0.cuda().clone()
+        for r in range(tp_size):
+            bgmv_tp_expand(plan, 1, proj, r, tp_size, vu, y_u[:, r * ncols:(r + 1) * ncols], 0.5)
+        vg = [torch.zeros(tp_size, T, rs, dtype=torch.float32, device="cuda") for _ in range(tp_size)]
+        flags = [torch.zeros(tp_size, dtype=torch.int32, device="cuda") for _ in range(tp_size)]
+        y_f = y0.cuda().clone()
+        for r in range(tp_size):
+            bgmv_tp_shrink_push(plan, 1, proj, r, tp_size, xd, [v.data_ptr() for v in vg],
+                                [f.data_ptr() for f in flags])
+        for r in range(tp_size):
+            bgmv_tp_expand_wait(plan, 1, proj, r, tp_size, vg[r], flags[r], y_f[:, r * ncols:(r + 1) * ncols], 0.5)
+        torch.cuda.synchronize()
+        ref = s.oracle(1, proj, x, y0, ta, scale=0.5)
+        assert rel_err(y_u, ref) <= TOL_BF16, proj
+        assert torch.equal(y_f, y_u), proj
+        assert all(int(f.abs().sum()) == 0 for f in flags)
