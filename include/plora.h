@@ -365,7 +365,9 @@ int plora_sgmv_fused_layer(plora_plan* plan, uint32_t layer, const void* x, uint
  * (rank-major, e.g. ncclAllGather), and the expand adds
  * scale · v · Bᵀ[:, i·d_out/N : (i+1)·d_out/N] into the rank's output shard
  * y_shard [n_tokens × d_out/N].  Every adapter rank must be divisible by N;
- * bf16 stores only. */
+ * bf16 stores only.  Kernels: warp items (bgmv_warp.cu) — K-sliced shrink
+ * items whose per-job partial sums are added in slice order by the job's
+ * last item (deterministic), column-shard expand items. */
 uint32_t plora_tp_shard_rows(const plora_plan* plan, uint32_t tp_size);
 int plora_bgmv_tp_shrink(plora_plan* plan, uint32_t layer, uint32_t proj, uint32_t tp_rank,
                          uint32_t tp_size, const void* x, uint64_t x_stride, float* v_part,
@@ -570,16 +572,18 @@ int plora_predictor_buffer_at(const plora_predictor* p, uint64_t i, uint32_t* ad
                               double* window, double* label);
 
 /* ------------------------------------------------------------ diagnostics
- * Per-chunk device timestamps (SM clock cycles) of the next bf16 BGMV
- * launches: trace[(cta * 64 + k) * 16 + field] for the first 63 chunks of
- * each CTA, fields as documented in scripts/trace_bgmv.py (chunk 63 holds the
- * CTA start / end).  dev_buf = NULL disables tracing. */
+ * Device timestamps of the next decode / prefill launches, for the
+ * diagnostics scripts: cluster kernel (scripts/trace_bgmv.py), streaming
+ * kernel (scripts/trace_stream.py), single-layer warp-item calls (per item
+ * start / end %globaltimer, scripts/trace_warp_layer.py), persistent SGMV
+ * expand (scripts/trace_sgmv_expand.py).  dev_buf = NULL disables tracing. */
 int plora_debug_set_trace(void* dev_buf, uint64_t bytes);
 /* Diagnostics: the bf16 decode kernel behind plora_bgmv* — 0 warp items
  * (bgmv_warp.cu, the default); 1 the streaming kernel alone (bgmv_stream.cu);
  * 2 thread-block clusters only (bgmv_cluster.cu); 3 clusters with the hybrid
  * streaming share for plora_bgmv_layers (the round-2 pair).  Applies to plans
- * built afterwards for the hybrid split. */
+ * built afterwards for the hybrid split.  The tensor-parallel halves run on
+ * warp items, or on the streaming kernel with impl 1. */
 int plora_debug_set_bgmv_impl(int impl);
 /* Diagnostics for the streaming kernel: 1 consumers skip the math, 2 no
  * weight copies (results are then wrong; timing ablation only). */
