@@ -635,6 +635,7 @@ __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_
   if (split) {  // combine the pair: acc(rows [0, h)) + acc(rows [h, r)), in that order
     constexpr int K = NS * 4 * T;
     if (second) {  // its own ring is idle now: stage the partial sums there
+      __syncwarp();  // every lane's copies into the ring have landed (the staging crosses lanes' slots)
 #pragma unroll
       for (int s = 0; s < NS; ++s)
 #pragma unroll
