@@ -168,6 +168,27 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------- GPU arm
+def dist_setup():
+    """(world, rank, local device index) from the torchrun environment; one
+    process per GPU over NCCL.  PLORA_BENCH_BACKEND=gloo with more ranks than
+    GPUs (ranks sharing a device, LOCAL_RANK modulo the device count) only
+    exercises the multi-rank code path on a one-GPU box (tests/; its numbers
+    mean nothing)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    if world > 1:
+        backend = os.environ.get("PLORA_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return world, rank, local
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -176,12 +197,7 @@ def run_ours(args):
     from paper_2512_20210_b200.lora import (AdapterStore, BatchPlan, bgmv, bgmv_layer,
                                             kernel_launch_count, sgmv, sgmv_layer)
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank, local = dist_setup()
 
     prefill = args.workload == "cfg3"
     cfg = synth.cfg3(page_bytes=args.page_bytes) if prefill else synth.cfg2(page_bytes=args.page_bytes)
@@ -537,13 +553,8 @@ def run_cfg4(args):
     from paper_2512_20210_b200.serving import DecodeServer, ServerConfig, shard_keys
     from paper_2512_20210_b200.workload import SyntheticProfile, generate_synthetic
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
     shape = ModelShape.llama7b_qv()
     n_total = args.cfg4_adapters
     keys = shard_keys(n_total, rank, world)
@@ -723,13 +734,8 @@ def run_cfg5(args):
     from paper_2512_20210_b200.lora import AdapterStore, BatchPlan, kernel_launch_count
     from paper_2512_20210_b200.tp import TensorParallelLoRA
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    world, rank, local = dist_setup()
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
     cfg = synth.cfg5(n_layers=args.cfg5_layers, page_bytes=args.page_bytes)
     shape = cfg.shape
     pool = synth.build_pool(cfg)

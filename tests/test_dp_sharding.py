@@ -9,6 +9,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -104,3 +105,27 @@ def test_request_sharding_world2_matches_single_process():
     images, ta, x, y0 = _data()
     y_single, _, _ = _apply(list(range(len(RANKS))), images, ta, x, y0, 1, 0)
     assert np.array_equal(rows, y_single)  # bit-identical: same per-token arithmetic
+
+
+@pytest.mark.gpu
+def test_bench_multirank_path_on_one_gpu(tmp_path):
+    """bench.py's N > 1 path (torchrun, one process per rank, barrier +
+    max-over-ranks timing, whole-job value) end to end, with two ranks sharing
+    the one GPU of this box over gloo (PLORA_BENCH_BACKEND; the numbers mean
+    nothing here, the multi-GPU driver run uses NCCL on N GPUs)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PLORA_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29531", "bench.py", "--gpus", "2",
+                          "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["config"]["parallelism"] == "request-sharded x2 (no collective)"
