@@ -9,24 +9,29 @@
 //
 // Decode is a pure weight stream (arithmetic intensity ~2 flop/byte at two
 // tokens per adapter), so the design is the one that streams best: every
-// warp runs one self-contained work item with 16-byte ld.global.nc loads,
-// the next chunk's loads in flight while the current chunk's math runs, and
-// nothing else — no shared-memory ring, no clusters, no barriers, no
-// cross-CTA waits.  Two launches per call, chained by programmatic dependent
-// launch:
-//   shrink  S items (<= 8 rank rows of one job, full K):
+// warp runs one self-contained work item; each lane copies its own 16-byte
+// pieces of the paged rows with cp.async into its own slots of a per-warp
+// ring in shared memory and reads back exactly those bytes — no clusters, no
+// cross-warp barriers (except the two warps of a split pair), no cross-CTA
+// waits.  Two launches per call, chained by programmatic dependent launch:
+//   shrink  S items (<= 8 rank rows of one job, one K slice of <= 4096):
 //           v[tok][row] = Σ_k x[tok][k] · A[row][k], exact fp32
 //           (FHFMA: bf16 × bf16 + fp32, one rounding per term, no converts);
 //           lane partials summed by a fixed butterfly -> deterministic.
+//           Single-layer calls also stream x through the ring.
 //   expand  E items (one block of <= 512 output columns, every rank row):
 //           acc[tok][col] = Σ_row v[tok][row] · Bᵀ[row][col] in row order
 //           (FFMA2 on converted weight pairs), then y = bf16(y + scale·acc).
-// The launch boundary orders v (the expand's griddepcontrol.wait); the
-// expand's first rows are loaded before it.  A multi-layer launch
-// (plora_bgmv_layers) is the same item list repeated per layer.
-// Measured at cfg2 (scripts/microbench_ldg.cu, profiles/r02n_*): the same
-// loads without the math reach 6.5 TB/s; with it the step runs at ~0.94 of
-// the copy roofline.
+//           Single-layer calls issue the first Bᵀ rows before the dependency
+//           wait and split rank >= 64 items over a CTA's two warps (partials
+//           added in fixed order).
+// The launch boundary orders v (the expand's griddepcontrol.wait).  A
+// multi-layer launch (plora_bgmv_layers) is the same item list repeated per
+// layer.  The tensor-parallel halves (tp.cu) run on the same items in a TP
+// mode: K-sliced shrink items with per-job in-order partial sums, column-
+// shard expand items reading the gathered v.
+// Measured at cfg2 (profiles/r02n_*, r02o_*): the 32-layer step at 1.00-1.01
+// of the HBM copy peak, one layer per call 0.647 (latency-bound phases).
 #include <cuda_bf16.h>
 
 #include "plan.hpp"
