@@ -17,19 +17,22 @@
 // the HBM traffic per GPU is 1/N of the adapter.  Math: PAPER.md:64-69; the
 // reference has no multi-GPU path.
 //
-// Both halves run on the streaming decode kernel (bgmv_stream.cu): one
-// persistent CTA per SM, weight rows moved page by page with 1-D TMA bulk
-// copies into a multi-slot shared-memory ring, mma.sync consumers.
-//   shrink  = its S items restricted to the shard rows (<= 16 rows, full K
-//             each); the publisher warp stores v_part in fp32.
-//   expand  = its E items restricted to the column shard (<= 1024 columns,
-//             cut at 1024-column boundaries so every row piece stays in one
-//             page); the producer builds the bf16 hi / lo fragments of v from
-//             v_gathered while the slot's weight rows are in flight.
-// No counters: v is complete before either launch.  The item lists depend
-// on (batch, proj, tp_rank, tp_size) only; they are built and uploaded on a
-// plan's first call for that key (outside stream capture) and reused by
-// every layer.
+// Both halves run on the warp-item decode kernels (bgmv_warp.cu,
+// launch_bgmv_warp_tp; the default):
+//   shrink  = items (job, <= kWarpRows shard rows, K slice of >= 4 chunks;
+//             the fewest power-of-two slices giving >= 6 items per SM); each
+//             writes its partial sums, and the job's last item sums the
+//             slices in order into v_part (or every rank's gathered buffer,
+//             with the fused all-gather).
+//   expand  = items (job, <= kWarpCols columns of the rank's shard) over
+//             every rank row, v read from v_gathered; rank >= 64 as split
+//             pairs on a CTA's two warps.
+// With plora_debug_set_bgmv_impl(1) they run on the round-2 streaming kernel
+// (bgmv_stream.cu) instead: one persistent CTA per SM, weight rows moved
+// page by page with 1-D TMA bulk copies, mma.sync consumers.  The item lists
+// depend on (batch, proj, tp_rank, tp_size) only; they are built and
+// uploaded on a plan's first call for that key (outside stream capture) and
+// reused by every layer.
 #include <cuda_bf16.h>
 
 #include <algorithm>
