@@ -240,12 +240,12 @@ __device__ __forceinline__ void cpa16(uint32_t dst, const void* src, bool valid)
 // issued kRing units (LA = kRing / R chunks) before it is consumed, so the
 // unit issued after consuming (c, i) is (c + LA, i): the same row, a static
 // register index for its page entries.
-// The two warps of a split pair meet here (named barrier 1, 64 threads).
-// The non-.aligned barrier: the warps reach it from different instructions
-// and a warp may arrive not yet reconverged.
+// The two warps of a split pair (warps 2c and 2c + 1 of the CTA) meet here:
+// named barrier 1 + c, 64 threads.  The non-.aligned barrier: the warps reach
+// it from different instructions and a warp may arrive not yet reconverged.
 __device__ __forceinline__ void pair_sync() {
   __syncwarp();
-  asm volatile("barrier.sync 1, 64;" ::: "memory");
+  asm volatile("barrier.sync %0, 64;" ::"r"(1u + (threadIdx.x >> 6)) : "memory");
 }
 
 __device__ __forceinline__ uint32_t tok_of(const WI& w, uint32_t t) {
