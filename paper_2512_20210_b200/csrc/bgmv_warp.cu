@@ -243,9 +243,21 @@ __device__ __forceinline__ void cpa16(uint32_t dst, const void* src, bool valid)
 // The two warps of a split pair (warps 2c and 2c + 1 of the CTA) meet here:
 // named barrier 1 + c, 64 threads.  The non-.aligned barrier: the warps reach
 // it from different instructions and a warp may arrive not yet reconverged.
+// (Immediate barrier ids: a register id cost a single layer's call 5 µs,
+// 32.4 -> 37.7, profiles/r02o_warp_split.txt.)
 __device__ __forceinline__ void pair_sync() {
   __syncwarp();
-  asm volatile("barrier.sync %0, 64;" ::"r"(1u + (threadIdx.x >> 6)) : "memory");
+  if constexpr (kWarps == 2) {
+    asm volatile("barrier.sync 1, 64;" ::: "memory");
+  } else {
+    static_assert(kWarps <= 8, "pair barriers 1..4");
+    switch (threadIdx.x >> 6) {
+      case 0: asm volatile("barrier.sync 1, 64;" ::: "memory"); break;
+      case 1: asm volatile("barrier.sync 2, 64;" ::: "memory"); break;
+      case 2: asm volatile("barrier.sync 3, 64;" ::: "memory"); break;
+      default: asm volatile("barrier.sync 4, 64;" ::: "memory"); break;
+    }
+  }
 }
 
 __device__ __forceinline__ uint32_t tok_of(const WI& w, uint32_t t) {
