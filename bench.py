@@ -363,23 +363,29 @@ def run_ours(args):
                 for p in range(NP):
                     op(plan, l, p, x[l], y[l * NP + p])
 
+        G = max(1, args.e2e_group)  # layers per copy (bigger PCIe transfers, longer pipeline fill)
+
         def e2e_step():
             cur = torch.cuda.current_stream()
             hs.wait_stream(cur)
             ds.wait_stream(cur)
             with torch.cuda.stream(hs):
-                for l in range(L):
-                    x[l].copy_(xh[l], non_blocking=True)
-                    y[l * NP:(l + 1) * NP].copy_(yh[l * NP:(l + 1) * NP], non_blocking=True)
-                    ein[l].record(hs)
+                for l0 in range(0, L, G):
+                    l1 = min(L, l0 + G)
+                    x[l0:l1].copy_(xh[l0:l1], non_blocking=True)
+                    y[l0 * NP:l1 * NP].copy_(yh[l0 * NP:l1 * NP], non_blocking=True)
+                    ein[l0].record(hs)
             for l in range(L):
-                cur.wait_event(ein[l])
+                if l % G == 0:
+                    cur.wait_event(ein[l])
                 layer(l)
-                eout[l].record(cur)
+                if (l + 1) % G == 0 or l + 1 == L:
+                    eout[l - l % G].record(cur)
             with torch.cuda.stream(ds):
-                for l in range(L):
-                    ds.wait_event(eout[l])
-                    yout[l * NP:(l + 1) * NP].copy_(y[l * NP:(l + 1) * NP], non_blocking=True)
+                for l0 in range(0, L, G):
+                    l1 = min(L, l0 + G)
+                    ds.wait_event(eout[l0])
+                    yout[l0 * NP:l1 * NP].copy_(y[l0 * NP:l1 * NP], non_blocking=True)
             cur.wait_stream(hs)
             cur.wait_stream(ds)
 
@@ -413,7 +419,7 @@ def run_ours(args):
         e2e = {"value": world * T / (e2e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": xh.numel() * 2 + yh.numel() * 2 + plan_bytes,
                "d2h_bytes_per_step": yout.numel() * 2, "ms_per_step": e2e_ms,
-               "pipeline": "per layer: H2D | calls | D2H on three streams, one CUDA graph"}
+               "pipeline": f"per {G} layer(s): H2D | calls | D2H on three streams, one CUDA graph"}
 
     # ---- roofline of the op (per (layer, proj) call, mean over the timed region)
     per_call = statistics.mean(call_bytes(shape, cfg.ranks, p, T) for p in range(NP))
@@ -1019,6 +1025,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the 64 calls eagerly")
+    ap.add_argument("--e2e-group", type=int, default=2,
+                    help="layers per host<->device copy in the e2e pipeline (profiles/r02o_e2e_group.txt)")
     ap.add_argument("--layers-per-launch", type=int, default=32,
                     help="decode: layers served by one plora_bgmv_layers launch (1 = one "
                          "plora_bgmv_layer launch per layer)")
