@@ -492,10 +492,12 @@ __device__ __forceinline__ void tp_consume(const WArgs& p, uint32_t lane) {
   }
 }
 
-template <int T, bool FAST, uint32_t RG, uint32_t KS, bool TPE = false>
+// NARROW: items of <= 256 columns for every token count (the TP halves, whose
+// column shards leave few items at kWarpCols)
+template <int T, bool FAST, uint32_t RG, uint32_t KS, bool TPE = false, bool NARROW = false>
 __device__ __forceinline__ void expand_item(const WArgs& p, const WI& w, uint32_t li, uint32_t lane,
                                             uint32_t ring, uint32_t partner) {
-  constexpr int NS = kWarpCols(T) / 256;  // 16-byte column chunks per lane and row
+  constexpr int NS = NARROW ? 1 : kWarpCols(T) / 256;  // 16-byte column chunks per lane and row
   constexpr uint32_t DR = RG / NS;        // ring depth in rows
   const uint32_t L = p.log2_page;
   const uint64_t pmask = (1ull << L) - 1;
@@ -749,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_tp_shrink
   }
 }
 
-template <bool FAST>
+template <bool FAST, bool NARROW>
 __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_tp_expand_kernel(const WArgs p) {
   extern __shared__ __align__(16) char smem[];
   ptx::pdl_launch_dependents();
@@ -760,10 +762,10 @@ __global__ void __launch_bounds__(kThreads, PLORA_WARP_MINB) bgmv_warp_tp_expand
   const uint32_t partner = ptx::smem_u32(smem) + (warp ^ 1u) * warp_smem(kDeepRing);  // a split pair's other warp
   const WI w = load_item(p.items + wi);
   switch (w.ntok) {
-    case 1: expand_item<1, FAST, kDeepRing, 1, true>(p, w, 0, lane, ring, partner); break;
-    case 2: expand_item<2, FAST, kDeepRing, 1, true>(p, w, 0, lane, ring, partner); break;
-    case 3: expand_item<3, FAST, kDeepRing, 1, true>(p, w, 0, lane, ring, partner); break;
-    default: expand_item<4, FAST, kDeepRing, 1, true>(p, w, 0, lane, ring, partner); break;
+    case 1: expand_item<1, FAST, kDeepRing, 1, true, NARROW>(p, w, 0, lane, ring, partner); break;
+    case 2: expand_item<2, FAST, kDeepRing, 1, true, NARROW>(p, w, 0, lane, ring, partner); break;
+    case 3: expand_item<3, FAST, kDeepRing, 1, true, NARROW>(p, w, 0, lane, ring, partner); break;
+    default: expand_item<4, FAST, kDeepRing, 1, true, NARROW>(p, w, 0, lane, ring, partner); break;
   }
 }
 
@@ -827,8 +829,10 @@ void launch_bgmv_warp_tp(const plora_plan& plan, const WarpTp& t, uint32_t layer
   };
   if (t.half == 1)
     fast ? go(bgmv_warp_tp_shrink_kernel<true>) : go(bgmv_warp_tp_shrink_kernel<false>);
+  else if (t.narrow)
+    fast ? go(bgmv_warp_tp_expand_kernel<true, true>) : go(bgmv_warp_tp_expand_kernel<false, true>);
   else
-    fast ? go(bgmv_warp_tp_expand_kernel<true>) : go(bgmv_warp_tp_expand_kernel<false>);
+    fast ? go(bgmv_warp_tp_expand_kernel<true, false>) : go(bgmv_warp_tp_expand_kernel<false, false>);
 }
 
 void launch_bgmv_warp(const plora_plan& plan, const WarpWork& w, uint32_t layer0, uint32_t n_layers,

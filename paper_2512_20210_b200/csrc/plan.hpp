@@ -255,6 +255,7 @@ struct WarpTp {
   uint32_t* done = nullptr;  // zero between calls
   const float* v_in = nullptr;
   uint32_t* wait = nullptr;
+  uint32_t narrow = 0;  // expand: items of <= 256 columns (else kWarpCols)
 };
 struct WarpWork {  // one launch variant (a projection, or every projection of a layer)
   uint32_t s_off = 0, ns = 0;  // S items [s_off, s_off + ns) of the item array

@@ -184,6 +184,12 @@ plora_plan::TpWork& tp_work_warp(plora_plan& plan, uint32_t proj, uint32_t tp_ra
     throw ValidationError("the first tensor-parallel call of a plan for (proj, tp_rank, tp_size) uploads its "
                           "item list and must run outside stream capture");
   const uint32_t ncall = (tg.d_in + 255) / 256;
+  // expand items: kWarpCols columns, or 256 when that leaves fewer than 4
+  // items per SM (narrow shards at TP >= 4: rank 0 of cfg5 at TP 4 / 8
+  // 18.7 -> 15.2 / 16.6 -> 14.8 us; wide shards measured slower narrow)
+  uint64_t wide_items = 0;
+  for (const ClusterJob& j : plan.cjobs) wide_items += (tg.ncols + kWarpCols(j.ntok) - 1) / kWarpCols(j.ntok);
+  const bool narrow = half == 2 && wide_items < 4ull * std::max(1, plan.store->num_sms);
   // K slices of the shrink: the fewest (a power of two, slices of >= 4
   // chunks) that give >= 6 items per SM — cfg5 measured best at ~900-1400
   // items for every TP size (profiles/r02o_tp_warp.txt: fewer leave SMs idle,
@@ -214,7 +220,7 @@ plora_plan::TpWork& tp_work_warp(plora_plan& plan, uint32_t proj, uint32_t tp_ra
         }
       pfl += static_cast<uint64_t>(ks) * j.ntok * rs;
     } else {
-      const uint32_t C = kWarpCols(j.ntok);
+      const uint32_t C = narrow ? 256u : kWarpCols(j.ntok);
       for (uint32_t c0 = tg.col0; c0 < tg.col0 + tg.ncols; c0 += C) {
         WarpItem it = base;
         it.meta = meta(std::min(C, tg.col0 + tg.ncols - c0));
@@ -261,6 +267,7 @@ plora_plan::TpWork& tp_work_warp(plora_plan& plan, uint32_t proj, uint32_t tp_ra
   std::memcpy(w.h_stage, items.data(), ib);
   PLORA_CUDA(cudaMemcpyAsync(d, w.h_stage, total, cudaMemcpyHostToDevice, stream));
   w.wt.half = half;
+  w.wt.narrow = narrow ? 1u : 0u;
   w.wt.items = reinterpret_cast<const WarpItem*>(d);
   w.wt.n_items = static_cast<uint32_t>(items.size());
   w.wt.ks = ks;
