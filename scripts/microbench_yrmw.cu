@@ -18,6 +18,7 @@
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
 
 constexpr int M = 16384, N = 4096, TM = 128, TN = 64;
+constexpr int TNW = 128;  // wide reduce-add boxes (mode 5)
 constexpr int TILES = (M / TM) * (N / TN);
 
 __device__ __forceinline__ uint32_t su(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -69,6 +70,40 @@ __global__ void __launch_bounds__(128) yrmw(const __grid_constant__ CUtensorMap 
       else
         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
                      ::"l"(&tm), "r"(c0), "r"(r0), "r"(su(b)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// 5: TMA reduce-add of 128 x 128 boxes (32 KiB, SWIZZLE_NONE): half the ops
+__global__ void __launch_bounds__(128) yrmw_wide(const __grid_constant__ CUtensorMap tm) {
+  extern __shared__ __align__(1024) char smem[];
+  char* buf = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  const uint32_t tid = threadIdx.x;
+  constexpr int TILESW = (M / TM) * (N / TNW);
+  uint32_t k = 0;
+  for (uint32_t t = blockIdx.x; t < TILESW; t += gridDim.x, ++k) {
+    char* b = buf + (k & 1) * 32768;
+    const int c0 = (t % (N / TNW)) * TNW, r0 = (t / (N / TNW)) * TM;
+    if (k >= 2) {
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncthreads();
+    }
+    uint4* row = reinterpret_cast<uint4*>(b + tid * 256);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      uint4 v = make_uint4(0, 0, 0, 0);
+      __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(1.f, 1.f);
+      row[c] = v;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];"
+                   ::"l"(&tm), "r"(c0), "r"(r0), "r"(su(b)) : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
   }
@@ -151,6 +186,33 @@ int main() {
       const double us = tot / 20 * 1e3, bytes = (m == 2 ? 1.0 : 2.0) * M * N * 2;
       printf("grid %4d  %-28s %8.1f us  %6.2f TB/s DRAM\n", grid, names[m], us, bytes / (us * 1e-6) / 1e12);
     }
+  {
+    CUtensorMap tw;
+    const cuuint32_t boxw[2] = {TNW, TM};
+    if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, boxw, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      printf("encode (wide) failed\n");
+      return 1;
+    }
+    const int smw = 2 * 32768 + 1024;
+    CK(cudaFuncSetAttribute(yrmw_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, smw));
+    for (int grid : {296, 444, 888}) {
+      float tot = 0.f;
+      for (int i = 0; i < 20; ++i) {
+        cudaMemset(flush, i, 256 << 20);
+        cudaEventRecord(e0);
+        yrmw_wide<<<grid, 128, smw>>>(tw);
+        cudaEventRecord(e1);
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        tot += ms;
+      }
+      const double us = tot / 20 * 1e3;
+      printf("grid %4d  %-28s %8.1f us  %6.2f TB/s DRAM\n", grid, "TMA reduce-add 128x128 boxes", us,
+             2.0 * M * N * 2 / (us * 1e-6) / 1e12);
+    }
+  }
   for (int grid : {1184, 2368, 4736}) {
     for (int m = 0; m < 2; ++m) {
       float tot = 0.f;
